@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the LDG per-step hot path (BASELINE.json metric).
+
+metric  DOF-updates/s (assembly + solve per implicit-Euler step)
+        = sum over the step of 3*K*N / device time of the step
+workload (default, BASELINE configs[1] = "C2"): Friedrichs-Keller 256x256
+        (K = 131072), p swept 0..4, the analytic c, d(t), f(t) of
+        BASELINE.json, dt = 1/20 (20 steps to T = 1).  One bench "step" is one
+        implicit-Euler step of every p in the sweep (each p its own system).
+value   device time (CUDA events on the library's stream) with the state
+        resident in HBM; e2e = the same steps through the host-buffer C ABI
+        call (ldg_euler_steps_host: H2D + steps + D2H inside the timed region).
+
+`python bench.py --impl reference` times the reference's own CPU path
+(oracle/_ref/libldgref.so = the unmodified reference headers + Eigen shim,
+SciPy SuperLU as its SparseLU) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DOF-updates/s (assembly+solve per step)"
+UNIT = "DOF-updates/s"
+
+WORKLOADS = {
+    # name: (dim, p list, dt, jitter, boundary, description)
+    "c2": (256, [0, 1, 2, 3, 4], 1.0 / 20, 0.0, {1: "D", 2: "D", 3: "D", 4: "D"},
+           "C2: FK 256x256 (K=131072), p=0..4 sweep, implicit Euler dt=1/20, all-Dirichlet BASELINE problem"),
+    "c1": (16, [1], 1.0 / 100, 0.0, {1: "D", 2: "D", 3: "D", 4: "D"},
+           "C1: FK 16x16 (K=512), p=1, dt=1/100, all-Dirichlet BASELINE problem"),
+    "c4": (2048, [3], 1.0 / 10, 0.2, {1: "D", 2: "N", 3: "N", 4: "D"},
+           "C4: FK 2048x2048 jittered +-0.2h (seed 0), p=3, dt=1/10, D on x1=0,x2=0, N elsewhere"),
+    "c5": (4096, [2], 1.0 / 5, 0.0, {1: "D", 2: "D", 3: "D", 4: "D"},
+           "C5: FK 4096x4096 (K=33.5M), p=2, dt=1/5"),
+}
+
+
+def n_of(p):
+    return (p + 1) * (p + 2) // 2
+
+
+def e_int(dim):
+    return 3 * dim * dim - 2 * dim
+
+
+def bytes_schur(dim, p):
+    """Algorithmic bytes of one Schur apply (stage 1 + stage 2):
+    B^1, B^2, S, E^1, E^2 blocks (K + 2 E_int each), vectors x, t^1, t^2, y, indices."""
+    K, N = 2 * dim * dim, n_of(p)
+    blocks = 5 * N * N * (K + 2 * e_int(dim))
+    return 8 * blocks + 8 * 7 * K * N + 4 * 2 * 3 * K + 8 * 2 * K
+
+
+def bytes_asm(dim, p):
+    """8*2*N^2*(K + 2 E_int) + 8*K*N."""
+    K, N = 2 * dim * dim, n_of(p)
+    return 8 * 2 * N * N * (K + 2 * e_int(dim)) + 8 * K * N
+
+
+def bytes_spmv(dim, p):
+    """8 N^2 nb + 4 nb + 4 (3K+1) + 2*8*3KN, nb = 7K + 10 E_int."""
+    K, N = 2 * dim * dim, n_of(p)
+    nb = 7 * K + 10 * e_int(dim)
+    return 8 * N * N * nb + 4 * nb + 4 * (3 * K + 1) + 2 * 8 * 3 * K * N
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+        self._thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._proc = None
+            return self
+        self._thread = threading.Thread(target=self._read, daemon=True)
+        self._thread.start()
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+        if self._thread is not None:
+            self._thread.join(timeout=5)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_sample(workload, steps, warmup):
+    """Reference CPU path on a bounded sample: one implicit-Euler step of every
+    p of the sweep on FK 16x16 (K = 512); DOF-updates/s over the sample."""
+    from oracle import reflib as R
+
+    dim0, ps, dt, jitter, boundary, _ = WORKLOADS[workload]
+    dim = 16
+    funcs = dict(d=(9, []), f=(10, []), c_d=(8, []), g_n=(11, []), c0=(8, []))
+    if not R.available():
+        raise RuntimeError("oracle/_ref/libldgref.so missing")
+    cases = []
+    for p in ps:
+        mesh = R.RefMesh.square(1.0 / dim)
+        case = R.RefCase(mesh, n_of(p), 1.0, funcs, boundary)
+        cases.append([case, case.initial_state(), 0.0, mesh])
+    dof, sec = 0, 0.0
+    for it in range(warmup + steps):
+        for c in cases:
+            y, t, s = c[0].euler(c[1], c[2], dt, 1)
+            c[1], c[2] = y, t
+            if it >= warmup:
+                sec += s
+                dof += 3 * c[3].num_t * n_of(c[0].n)
+    sample = (f"reference (unmodified headers + Eigen shim, SciPy SuperLU for SparseLU): "
+              f"FK {dim}x{dim} (K={2 * dim * dim}), p={ps}, {steps} timed implicit-Euler steps each, dt={dt:g}; "
+              f"the reference's LU cost grows superlinearly in K, so this sample overstates its 256x256 rate")
+    return dof / sec, sec, sample
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    value, sec, sample = reference_sample(args.workload, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic BASELINE.json problem)",
+            "config": {"workload": WORKLOADS[args.workload][5] + " [reference: bounded sample, see cpu_baseline]"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+
+    world, rank, local = dist_env()
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import paper_1408_3877_b200 as ld
+
+    ld.set_device(local)
+    dim, ps, dt, jitter, boundary, desc = WORKLOADS[args.workload]
+    if args.p is not None:
+        ps = [int(x) for x in args.p.split(",")]
+    spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
+                          boundary=boundary)
+    opts = ld.SolverOptions()
+    systems = []
+    for p in ps:
+        s = ld.LdgSystem.square(dim, p, spec, jitter=jitter, seed=0)
+        s.initial_state()
+        systems.append(s)
+    dof_step = sum(3 * s.num_t * s.n for s in systems)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up (W full steps)
+    for _ in range(args.warmup):
+        for s in systems:
+            s.euler_steps(dt, 1, opts)
+    barrier()
+    launches0 = sum(s.info()["launches"] for s in systems)
+    per_p = {p: dict(ms=0.0, ms_asm=0.0, ms_solve=0.0, iters=0, applies=0, residual=0.0) for p in ps}
+    clocks = ClockSampler(local).start()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        for p, s in zip(ps, systems):
+            st = s.euler_steps(dt, 1, opts)
+            r = per_p[p]
+            r["ms_asm"] += st["ms_assemble"]
+            r["ms_solve"] += st["ms_solve"]
+            r["ms"] += st["ms_assemble"] + st["ms_solve"]
+            r["iters"] += st["iterations"]
+            r["applies"] += st["applies"]
+            r["residual"] = max(r["residual"], st["residual"])
+    barrier()
+    clk = clocks.stop()
+    launches = sum(s.info()["launches"] for s in systems) - launches0
+    total_ms = sum(r["ms"] for r in per_p.values())
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * dof_step * args.steps / (total_ms * 1e-3)
+
+    # e2e through the host-buffer C ABI call
+    e2e_ms = 0.0
+    h2d = 0
+    for p, s in zip(ps, systems):
+        y, t = s.get_state()
+        pin_in = torch.from_numpy(y).pin_memory()
+        pin_out = torch.empty_like(pin_in).pin_memory()
+        for _ in range(args.steps):
+            st = s.euler_steps_host(pin_in.data_ptr(), t, dt, 1, pin_out.data_ptr(), opts)
+            e2e_ms += st["ms_total"]
+            t += dt
+            pin_in.copy_(pin_out)
+        h2d += y.nbytes
+    e2e_value = world * dof_step * args.steps / (e2e_ms * 1e-3)
+
+    # per-kernel timing for the roofline (CUDA events on the library's stream, L2 flushed)
+    peak, peak_src = hbm_peak()
+    kern = {}
+    for p, s in zip(ps, systems):
+        kern[p] = s.time_kernels(s.t, dt, reps=5, flush=True)
+    # dominant kernel = the Schur operator apply (stage1 + stage2) at the p with the largest share
+    shares = {p: kern[p]["ms_schur"] * per_p[p]["applies"] / max(total_ms, 1e-9) for p in ps}
+    pd = max(shares, key=shares.get)
+    bs = bytes_schur(dim, pd)
+    achieved = bs / (kern[pd]["ms_schur"] * 1e-3) / 1e9
+    roof = {"kernel": f"schur_apply (k_stage1+k_stage2), p={pd}", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "peak_source": peak_src, "share_of_step": shares[pd],
+            "bytes_per_launch": bs,
+            "others": {str(p): {"assemble_GBps": bytes_asm(dim, p) / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
+                                "spmv_GBps": bytes_spmv(dim, p) / (kern[p]["ms_spmv"] * 1e-3) / 1e9,
+                                "schur_GBps": bytes_schur(dim, p) / (kern[p]["ms_schur"] * 1e-3) / 1e9,
+                                "ms": kern[p]} for p in ps}}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            v, sec, sample = reference_sample(args.workload, 1, 0)
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: analytic c, d(t), f(t) of BASELINE.json; FK mesh generated on device",
+            "config": {"workload": desc, "dim": dim, "K": 2 * dim * dim, "p": ps, "dt": dt,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (256 MB write) before every timed step; p>=2 working sets exceed L2",
+                       "solver": "BiCGStab on the exact Schur complement, block-Jacobi, reference contract 1e-10",
+                       "per_p": {str(p): {"ms_per_step": per_p[p]["ms"] / args.steps,
+                                          "ms_assemble": per_p[p]["ms_asm"] / args.steps,
+                                          "ms_solve": per_p[p]["ms_solve"] / args.steps,
+                                          "iterations_per_step": per_p[p]["iters"] / args.steps,
+                                          "max_residual": per_p[p]["residual"],
+                                          "dof_updates_per_s": 3 * 2 * dim * dim * n_of(p) * args.steps /
+                                          (per_p[p]["ms"] * 1e-3)} for p in ps}},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    for s in systems:
+        s.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--p", default=None, help="comma-separated degrees (overrides the workload's sweep)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

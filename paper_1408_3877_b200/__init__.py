@@ -1,0 +1,408 @@
+"""B200-native LDG diffusion path (arXiv 1408.3877, FESTUNG Part I).
+
+Python host mirror of the reference's entry points (proj/include/ldg), bound
+through ctypes to the C ABI of include/ldg_b200.h (libldg_b200.so, built
+in-tree by __graft_entry__.build()).  There is no CPU fallback: every call
+runs the sm_100a kernels, and loading fails loudly when the library or a GPU
+is missing.
+
+Reference interface -> this module
+  generate_grid_data / domain_square   LdgSystem.from_mesh / LdgSystem.square
+  LdgSystem(mesh, spec, rt) ctor       ditto (static operators, selectors)
+  project(mesh, f, t, q_ord, rt)       LdgSystem.project
+  build_blocks(t)                      LdgSystem.build_blocks / assemble
+  assemble_* operators                 LdgSystem.operator(name)
+  initial_state / euler_step           LdgSystem.initial_state / euler_step
+  solve_stationary                     LdgSystem.solve_stationary
+Exceptions follow the reference: ValueError for std::invalid_argument,
+MeshError for ldg::MeshError, RuntimeError for solver failures.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["FN", "ProblemSpec", "LdgSystem", "MeshError", "SolverOptions", "library_path", "load_library",
+           "OPERATORS", "VECTORS", "BASELINE_SPEC"]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def library_path() -> str:
+    return os.path.join(HERE, "libldg_b200.so")
+
+
+class MeshError(RuntimeError):
+    """ldg::MeshError (mesh.hpp:25-27)."""
+
+
+# coefficient ids of include/ldg_b200_coeffs.h
+FN = dict(zero=0, const=1, poly=2, exp_sum=3, cos7x1_x2=4, mms_exact=5, mms_f=6, mms_gn=7, base_c=8, base_d=9,
+          base_f=10, base_gn=11, sin_x1x2=12, cos3x1_plus_x2=13, mms_z1=14, mms_z2=15, sin3x1_x2sq=16,
+          exp_x1_minus_x2=17)
+
+OPERATORS = ["mass", "h1", "h2", "g1", "g2", "r1", "rd1", "r2", "rd2", "q1", "qn1", "q2", "qn2", "s", "sd", "A"]
+VECTORS = ["D", "F", "jd1", "jd2", "kd", "kn", "l", "V", "Y"]
+
+
+class _Coeff(C.Structure):
+    _fields_ = [("id", C.c_int), ("p", C.c_double * 4)]
+
+
+class _Problem(C.Structure):
+    _fields_ = [("d", _Coeff), ("f", _Coeff), ("c_d", _Coeff), ("g_n", _Coeff), ("c0", _Coeff),
+                ("eta", C.c_double), ("n_bc", C.c_int), ("bc_id", C.c_int * 16), ("bc_kind", C.c_int * 16)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("maxit", C.c_int), ("precond", C.c_int),
+                ("check_residual", C.c_int), ("contract_tol", C.c_double)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("applies", C.c_int), ("schur_relres", C.c_double),
+                ("residual", C.c_double), ("ms_assemble", C.c_double), ("ms_solve", C.c_double)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("p", C.c_int), ("n_local", C.c_int), ("num_t", C.c_int), ("num_owned", C.c_int),
+                ("num_ghost", C.c_int), ("num_v", C.c_int), ("rank", C.c_int), ("size", C.c_int),
+                ("bytes_device", C.c_int64), ("launches", C.c_int64)]
+
+
+class _Times(C.Structure):
+    _fields_ = [("ms_project", C.c_double), ("ms_assemble", C.c_double), ("ms_spmv", C.c_double),
+                ("ms_schur", C.c_double), ("reps", C.c_int)]
+
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_lp = C.POINTER(C.c_int64)
+_H = C.c_void_p
+_lib = None
+
+# The C ABI: name -> (restype, argtypes).  tests/test_capi.py checks that the
+# library exports exactly what include/ldg_b200.h declares.
+_SIGNATURES = {
+    "ldg_set_device": (C.c_int, [C.c_int]),
+    "ldg_create": (C.c_int, [_dp, C.c_int, _ip, C.c_int, _ip, C.c_int, C.POINTER(_Problem), C.POINTER(_H)]),
+    "ldg_create_square": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(_Problem),
+                                    C.POINTER(_H)]),
+    "ldg_destroy": (None, [_H]),
+    "ldg_last_error": (C.c_char_p, [_H]),
+    "ldg_get_info": (C.c_int, [_H, C.POINTER(_Info)]),
+    "ldg_mesh_lists": (C.c_int, [_H, _dp, _ip, _dp, _dp, _dp, _dp, _ip, _ip, _ip]),
+    "ldg_project": (C.c_int, [_H, C.POINTER(_Coeff), C.c_double, C.c_int, _dp]),
+    "ldg_assemble": (C.c_int, [_H, C.c_double]),
+    "ldg_export_operator": (C.c_int, [_H, C.c_int, _lp, _lp, _lp, _dp, C.c_int64]),
+    "ldg_export_vector": (C.c_int, [_H, C.c_int, _dp, C.c_int64]),
+    "ldg_initial_state": (C.c_int, [_H]),
+    "ldg_set_state": (C.c_int, [_H, _dp, C.c_double]),
+    "ldg_get_state": (C.c_int, [_H, _dp, _dp]),
+    "ldg_default_solver_opts": (_Opts, []),
+    "ldg_euler_steps": (C.c_int, [_H, C.c_double, C.c_int, C.POINTER(_Opts), C.POINTER(_Stats)]),
+    "ldg_euler_steps_host": (C.c_int, [_H, C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_void_p,
+                                       C.POINTER(_Opts), C.POINTER(_Stats), _dp]),
+    "ldg_solve_stationary": (C.c_int, [_H, C.c_double, C.POINTER(_Opts), C.POINTER(_Stats)]),
+    "ldg_apply_lhs": (C.c_int, [_H, C.c_double, _dp, _dp]),
+    "ldg_time_kernels": (C.c_int, [_H, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(_Times)]),
+    "ldg_sync": (C.c_int, [_H]),
+}
+
+
+def load_library():
+    """Loads libldg_b200.so (no fallback: raises if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not os.path.exists(path):
+        raise ImportError(f"libldg_b200.so not built ({path}); run __graft_entry__.build() — "
+                          "the LDG path has no CPU fallback")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def set_device(device: int) -> None:
+    """cudaSetDevice in the library's runtime (one process per GPU)."""
+    lib = load_library()
+    _raise(lib.ldg_set_device(int(device)), lib.ldg_last_error(None).decode())
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _i(a):
+    return a.ctypes.data_as(_ip)
+
+
+def _coeff(fn) -> _Coeff:
+    if isinstance(fn, str):
+        fn = (FN[fn], [])
+    fid, params = fn
+    if isinstance(fid, str):
+        fid = FN[fid]
+    c = _Coeff()
+    c.id = int(fid)
+    for i, v in enumerate(list(params)[:4]):
+        c.p[i] = float(v)
+    return c
+
+
+@dataclass
+class ProblemSpec:
+    """ProblemSpec (system.hpp:26-37); coefficients are (id, params) or names of FN."""
+    d: object = ("const", [1.0])
+    f: object = "zero"
+    c_d: object = "zero"
+    g_n: object = "zero"
+    c0: object = "zero"
+    eta: float = 1.0
+    boundary: dict = field(default_factory=dict)  # id -> "D" | "N"
+    t_end: float = 1.0
+    num_steps: int = 1
+
+    def to_c(self) -> _Problem:
+        pr = _Problem()
+        pr.d, pr.f, pr.c_d, pr.g_n, pr.c0 = (_coeff(x) for x in (self.d, self.f, self.c_d, self.g_n, self.c0))
+        pr.eta = float(self.eta)
+        if len(self.boundary) > 16:
+            raise ValueError("too many boundary conditions")
+        pr.n_bc = len(self.boundary)
+        for i, (bid, kind) in enumerate(sorted(self.boundary.items())):
+            pr.bc_id[i] = int(bid)
+            pr.bc_kind[i] = 0 if kind in ("D", "dirichlet", 0) else 1
+        return pr
+
+
+# The BASELINE.json problem: c = cos7x1 cos7x2 + e^-t,
+# d = e^(x1+x2)(1 + 0.5 sin t), f derived, Dirichlet everywhere.
+BASELINE_SPEC = ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
+                            boundary={1: "D", 2: "D", 3: "D", 4: "D"})
+
+
+@dataclass
+class SolverOptions:
+    rtol: float = 0.0
+    atol: float = 0.0
+    maxit: int = 20000
+    precond: int = 1
+    check_residual: bool = True
+    contract_tol: float = 1e-10
+
+    def to_c(self) -> _Opts:
+        o = _Opts()
+        o.rtol, o.atol, o.maxit, o.precond = self.rtol, self.atol, self.maxit, self.precond
+        o.check_residual, o.contract_tol = int(self.check_residual), self.contract_tol
+        return o
+
+
+def _raise(rc: int, msg: str):
+    if rc == 0:
+        return
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise MeshError(msg)
+    raise RuntimeError(msg)
+
+
+class LdgSystem:
+    """Device-resident LdgSystem (system.hpp:65-213) of one GPU."""
+
+    def __init__(self, handle, spec: ProblemSpec, p: int):
+        self._h = handle
+        self.spec = spec
+        self.p = p
+        info = self.info()
+        self.num_t = info["num_t"]
+        self.n = info["n_local"]
+        self.t = 0.0
+
+    # ---- construction --------------------------------------------------
+    @classmethod
+    def square(cls, dim: int, p: int, spec: ProblemSpec, jitter: float = 0.0, seed: int = 0) -> "LdgSystem":
+        lib = load_library()
+        h = _H()
+        pr = spec.to_c()
+        rc = lib.ldg_create_square(int(dim), float(jitter), int(seed), int(p), C.byref(pr), C.byref(h))
+        _raise(rc, lib.ldg_last_error(None).decode())
+        return cls(h, spec, p)
+
+    @classmethod
+    def from_mesh(cls, coords, v0t, p: int, spec: ProblemSpec, id_e0t=None) -> "LdgSystem":
+        lib = load_library()
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        v0t = np.ascontiguousarray(v0t, dtype=np.int32)
+        ids = None if id_e0t is None else np.ascontiguousarray(id_e0t, dtype=np.int32)
+        h = _H()
+        pr = spec.to_c()
+        rc = lib.ldg_create(_d(coords), coords.shape[0], _i(v0t), v0t.shape[0], None if ids is None else _i(ids),
+                            int(p), C.byref(pr), C.byref(h))
+        _raise(rc, lib.ldg_last_error(None).decode())
+        return cls(h, spec, p)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().ldg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc != 0:
+            _raise(rc, load_library().ldg_last_error(self._h).decode())
+
+    # ---- info -----------------------------------------------------------
+    def info(self) -> dict:
+        inf = _Info()
+        self._check(load_library().ldg_get_info(self._h, C.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in _Info._fields_}
+
+    @property
+    def block_dim(self) -> int:
+        return self.num_t * self.n
+
+    def mesh_lists(self) -> dict:
+        K, V = self.num_t, self.info()["num_v"]
+        out = dict(coords=np.zeros((V, 2)), v0t=np.zeros((K, 3), np.int32), b=np.zeros((K, 4)), area=np.zeros(K),
+                   len=np.zeros((K, 3)), nu=np.zeros((K, 3, 2)), nbr=np.zeros((K, 3), np.int32),
+                   nbr_n=np.zeros((K, 3), np.int32), id_e0t=np.zeros((K, 3), np.int32))
+        self._check(load_library().ldg_mesh_lists(self._h, _d(out["coords"]), _i(out["v0t"]), _d(out["b"]),
+                                                  _d(out["area"]), _d(out["len"]), _d(out["nu"]),
+                                                  _i(out["nbr"]), _i(out["nbr_n"]), _i(out["id_e0t"])))
+        return out
+
+    # ---- per-step path --------------------------------------------------
+    def project(self, fn, t: float, q_ord: int | None = None) -> np.ndarray:
+        """project(mesh, func, t, q_ord, rt) (fields.hpp:53-82) -> K x N."""
+        if q_ord is None:
+            q_ord = max(2 * self.p, 1)
+        out = np.zeros(self.num_t * self.n)
+        c = _coeff(fn)
+        self._check(load_library().ldg_project(self._h, C.byref(c), float(t), int(q_ord), _d(out)))
+        return out.reshape(self.num_t, self.n)
+
+    def assemble(self, t: float):
+        """The device half of build_blocks(t) (system.hpp:110-152)."""
+        self._check(load_library().ldg_assemble(self._h, float(t)))
+
+    def operator(self, name: str):
+        """COO (rows, cols, vals) of one operator at the last assemble time."""
+        which = OPERATORS.index(name)
+        lib = load_library()
+        nnz = C.c_int64()
+        self._check(lib.ldg_export_operator(self._h, which, C.byref(nnz), None, None, None, 0))
+        r, c, v = np.zeros(nnz.value, np.int64), np.zeros(nnz.value, np.int64), np.zeros(nnz.value)
+        self._check(lib.ldg_export_operator(self._h, which, C.byref(nnz), r.ctypes.data_as(_lp),
+                                            c.ctypes.data_as(_lp), _d(v), nnz.value))
+        return r, c, v
+
+    def vector(self, name: str) -> np.ndarray:
+        which = VECTORS.index(name)
+        n = (3 if name in ("V", "Y") else 1) * self.block_dim
+        out = np.zeros(n)
+        self._check(load_library().ldg_export_vector(self._h, which, _d(out), n))
+        return out
+
+    def build_blocks(self, t: float):
+        """(A, V) of system.hpp:110-152; A as a scipy CSR matrix (3KN x 3KN)."""
+        import scipy.sparse as sp
+
+        self.assemble(t)
+        r, c, v = self.operator("A")
+        n3 = 3 * self.block_dim
+        return sp.coo_matrix((v, (r, c)), shape=(n3, n3)).tocsr(), self.vector("V")
+
+    def initial_state(self):
+        """system.hpp:99-107 -> (y, t)."""
+        self._check(load_library().ldg_initial_state(self._h))
+        self.t = 0.0
+        return self.get_state()
+
+    def set_state(self, y, t: float):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if y.size != 3 * self.block_dim:
+            raise ValueError("state length does not match 3*K*N")
+        self._check(load_library().ldg_set_state(self._h, _d(y), float(t)))
+        self.t = float(t)
+
+    def get_state(self):
+        y = np.zeros(3 * self.block_dim)
+        t = C.c_double()
+        self._check(load_library().ldg_get_state(self._h, _d(y), C.byref(t)))
+        return y, t.value
+
+    def euler_steps(self, dt: float, nsteps: int, opts: SolverOptions | None = None) -> dict:
+        """nsteps implicit Euler steps on the device-resident state (system.hpp:155-174)."""
+        o = (opts or SolverOptions()).to_c()
+        st = _Stats()
+        self._check(load_library().ldg_euler_steps(self._h, float(dt), int(nsteps), C.byref(o), C.byref(st)))
+        self.t = self.get_time()
+        return {k: getattr(st, k) for k, _ in _Stats._fields_}
+
+    def get_time(self) -> float:
+        t = C.c_double()
+        self._check(load_library().ldg_get_state(self._h, None, C.byref(t)))
+        return t.value
+
+    def euler_step(self, y, t: float, dt: float, opts: SolverOptions | None = None):
+        """SystemState euler_step(state, dt) with host vectors -> (y_next, t_next)."""
+        self.set_state(y, t)
+        self.euler_steps(dt, 1, opts)
+        return self.get_state()
+
+    def euler_steps_host(self, y_in_ptr: int, t: float, dt: float, nsteps: int, y_out_ptr: int,
+                         opts: SolverOptions | None = None) -> dict:
+        """Host-buffer euler_step through the C ABI (copies inside; device-timed).
+        y_in_ptr / y_out_ptr are host addresses of 3KN doubles (k-major), ideally pinned."""
+        o = (opts or SolverOptions()).to_c()
+        st = _Stats()
+        ms = C.c_double()
+        self._check(load_library().ldg_euler_steps_host(self._h, C.c_void_p(y_in_ptr), float(t), float(dt),
+                                                        int(nsteps), C.c_void_p(y_out_ptr), C.byref(o),
+                                                        C.byref(st), C.byref(ms)))
+        self.t = float(t) + nsteps * float(dt)
+        out = {k: getattr(st, k) for k, _ in _Stats._fields_}
+        out["ms_total"] = ms.value
+        return out
+
+    def solve_stationary(self, t: float = 0.0, opts: SolverOptions | None = None):
+        """system.hpp:177-185 -> (c, z1, z2) as K x N."""
+        o = (opts or SolverOptions()).to_c()
+        st = _Stats()
+        self._check(load_library().ldg_solve_stationary(self._h, float(t), C.byref(o), C.byref(st)))
+        y, _ = self.get_state()
+        kn = self.block_dim
+        K, n = self.num_t, self.n
+        self.last_stats = {k: getattr(st, k) for k, _ in _Stats._fields_}
+        return y[2 * kn:].reshape(K, n), y[:kn].reshape(K, n), y[kn:2 * kn].reshape(K, n)
+
+    def apply_lhs(self, dt: float, x) -> np.ndarray:
+        """(W + dt A) x with the operators of the last assemble."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros_like(x)
+        self._check(load_library().ldg_apply_lhs(self._h, float(dt), _d(x), _d(y)))
+        return y
+
+    def time_kernels(self, t: float, dt: float, reps: int = 10, flush: bool = True) -> dict:
+        tm = _Times()
+        self._check(load_library().ldg_time_kernels(self._h, float(t), float(dt), int(reps), int(flush),
+                                                    C.byref(tm)))
+        return {k: getattr(tm, k) for k, _ in _Times._fields_}
+
+    def sync(self):
+        self._check(load_library().ldg_sync(self._h))

@@ -1,0 +1,148 @@
+// Internal host-side state of an ldg_handle and the kernel launchers shared
+// by the translation units of libldg_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ldg_b200.h"
+#include "ldg_device.cuh"
+#include "ldg_tables.hpp"
+
+namespace ldgb {
+
+// Exceptions carry the ABI status they map to.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define LDG_CUDA(call)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ::ldgb::Error(LDG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+// Device buffer owned by a handle.
+template <typename T>
+struct DBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+  void alloc(size_t count, int64_t* counter) {
+    release(counter);
+    if (count == 0) return;
+    LDG_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    LDG_CUDA(cudaMemset(ptr, 0, count * sizeof(T)));
+    n = count;
+    if (counter) *counter += static_cast<int64_t>(count * sizeof(T));
+  }
+  void release(int64_t* counter) {
+    if (ptr) {
+      cudaFree(ptr);
+      if (counter) *counter -= static_cast<int64_t>(n * sizeof(T));
+    }
+    ptr = nullptr;
+    n = 0;
+  }
+};
+
+struct Handle {
+  // sizes
+  int p = 0, N = 0;
+  int K = 0;       // owned elements
+  int Kg = 0;      // owned + ghost
+  long Kp = 0;     // plane stride
+  int Kglobal = 0;
+  int V = 0;
+  int rank = 0, size = 1;
+  ldg_problem prob{};
+  int64_t bytes = 0;
+  int64_t launches = 0;  // kernels issued (bench evidence: gpu_launches)
+
+  HostTables tables;
+  DBuf<double> tab;
+  DevTables dtab{};
+
+  // mesh
+  DBuf<double> coords;   // V*2 (interleaved)
+  DBuf<int> v0t;         // Kg*3 (local vertex ids)
+  DBuf<double> geom;     // kGeomCount * Kp
+  DBuf<int> nbr, nbrn, kind, bid;  // 3 * Kp
+  std::vector<int> gid;  // local -> global element id
+
+  // per-step operators / vectors
+  DBuf<double> D, F;     // N * Kp
+  DBuf<double> E;        // 2 * 4 * N*N * Kp
+  DBuf<double> Bst;      // 2 * 4 * N*N * Kp
+  DBuf<double> Sst;      // 4 * N*N * Kp
+  DBuf<double> Vv;       // 3 * N * Kp
+  DBuf<double> Y, Yold;  // 3 * N * Kp
+  double t = 0.0;
+  double t_assembled = -1.0;
+  bool assembled = false;
+
+  // Krylov workspace (N * Kp each)
+  DBuf<double> kr_r, kr_rh, kr_p, kr_v, kr_s, kr_t, kr_ph, kr_sh, kr_b;
+  DBuf<double> tz;       // 2 * N * Kp : M^-1 B^m x
+  DBuf<double> Pinv;     // N*N * Kp : block-Jacobi inverse
+  DBuf<double> full_r, full_y;  // 3 * N * Kp : reference residual contract
+  DBuf<double> red;      // reduction scratch
+  double* red_host = nullptr;  // pinned
+  DBuf<double> flush;    // L2 flush buffer (measurement only)
+  DBuf<double> host_stage;  // k-major staging of host states (3KN)
+  DBuf<double> rule_elem;  // projection rule of order max(2p,1)
+  int rule_elem_R = 0;
+
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  std::string err;
+
+  DevMesh mesh() const { return DevMesh{K, Kg, Kp, geom.ptr, nbr.ptr, nbrn.ptr, kind.ptr}; }
+  long vec_len() const { return static_cast<long>(N) * Kp; }
+};
+
+// ---- launchers (defined in the .cu files) ----------------------------------
+// mesh (ldg_mesh.cu)
+void build_square_mesh(Handle& h, int dim, double jitter, uint64_t seed);
+void build_general_mesh(Handle& h, const double* coords, int nv, const int* v0t, int nt, const int* id_e0t);
+
+// assembly (ldg_assemble.cu)
+enum AsmMode { kModeE = 0, kModeG = 1, kModeR = 2, kModeRD = 3 };
+enum StaticMode { kStB = 0, kStS = 1, kStM = 2, kStH = 3, kStQ = 4, kStQN = 5, kStSint = 6, kStSD = 7 };
+void launch_project(Handle& h, const ldg_coeff& fn, double t, const double* rule_dev, int R, double* out,
+                    int count);
+void launch_rhs(Handle& h, double t);
+void launch_rhs_which(Handle& h, double t, int which, double* out);
+void launch_project_df(Handle& h, double t, const double* rule_dev, int R);
+void launch_assemble(Handle& h, int mode, double* out);
+void launch_static(Handle& h, int mode, double* out);
+void upload_rule(Handle& h, int q_ord, DBuf<double>& buf, int* R);
+
+// solver (ldg_solve.cu)
+void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);
+void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
+                   const double* w, double delta, double* y);
+void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double* out);
+void launch_bjac_setup(Handle& h, double wm, double dt);
+void launch_bjac_apply(Handle& h, const double* x, double* y);
+void launch_axpby(Handle& h, long n, double a, const double* x, double b, double* y);
+void launch_dots(Handle& h, long n, int ndots, const double* const* xs, const double* const* ys, double* out_host);
+void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev);
+void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa);
+
+// driver pieces (ldg_solve.cu)
+void assemble_step(Handle& h, double t);
+int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st);
+
+}  // namespace ldgb

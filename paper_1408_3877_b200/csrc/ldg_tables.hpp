@@ -1,0 +1,66 @@
+// Host-side reference-element math for the LDG path: the modal basis, the
+// quadrature rules, the reference integral tensors and the flat tables the
+// sm_100a kernels read.  Computed once per (p) at ldg_create, uploaded once.
+//
+// Mirrors (behaviour, not code) of the reference:
+//   basis              proj/include/ldg/basis.hpp:42-158
+//   quadrature rules   proj/include/ldg/quadrature.hpp:39-174
+//   reference tensors  proj/include/ldg/reftensors.hpp:55-154
+#pragma once
+
+#include <array>
+#include <vector>
+
+namespace ldgb {
+
+constexpr int kMaxP = 4;
+constexpr int kMaxN = 15;
+
+inline int dofs_of(int p) { return (p + 1) * (p + 2) / 2; }
+
+// phi_i and grad phi_i (i = 0..14) at a reference point, table-driven.
+double basis_value(int i, double x1, double x2);
+void basis_gradient(int i, double x1, double x2, double* g1, double* g2);
+
+struct Rule1D {
+  std::vector<double> s, w;  // nodes on (0,1), weights sum to 1
+};
+struct Rule2D {
+  std::vector<double> x1, x2, w;  // weights sum to 1/2
+};
+
+Rule1D gauss_unit(int npts);       // Newton on Legendre P_n
+Rule1D rule_1d(int order);         // reference quad_rule_1d(order)
+Rule2D rule_2d(int order);         // reference quad_rule_2d(order)
+void edge_point(int n, double s, double* x1, double* x2);                 // gamma_n, n = 0..2
+void edge_to_edge(int nm, int np, double x1, double x2, double* y1, double* y2);  // theta
+
+struct RefTensors {
+  int n = 0;
+  std::vector<double> m, h, g, sd, so, rd, ro;  // same index layout as reftensors.hpp:36-50
+};
+RefTensors reference_tensors(int n);
+
+// Flat device tables; every array is an offset (in doubles) into one buffer.
+struct TableLayout {
+  int p = 0, N = 0;
+  int R = 0;    // projection rule points (order max(2p,1))
+  int Qe = 0;   // exact edge rule for the rank-Q R assembly (degree 3p)
+  int Qb = 0;   // boundary-vector edge rule (order 2p+1, reference BasisQuadCache)
+  long proj_phi, proj_w, proj_x;     // [R][N], [R], [R][2]
+  long mhat, minv;                   // [N][N]
+  long ghat;                         // [i][j][l][m]  (reftensors.hpp:38-40)
+  long hhat, sdiag, soff;            // [i][j][m], [i][j][n], [i][j][nm][np]
+  long pe, pth, we;                  // [n][q][i], [nm][np][q][j], [q]   (rank-Q edge form)
+  long pb, sb, wb;                   // [n][q][i], [q], [q]              (RHS edge rule)
+  long total = 0;
+};
+
+struct HostTables {
+  TableLayout lay;
+  std::vector<double> data;
+};
+
+HostTables build_tables(int p);
+
+}  // namespace ldgb
