@@ -91,6 +91,12 @@ typedef struct ldg_info_t {
 
 typedef struct ldg_handle ldg_handle;
 
+/* Host-only (no GPU needed): the reference tensors this library uploads,
+ * build_ref_tensors (reftensors.hpp:55-154), in the reference index layout:
+ * m n*n, h n*n*2, g n^3*2, sd n*n*3, so n*n*9, rd n^3*3, ro n^3*9. */
+int ldg_reference_tensors(int n_local, double* m, double* h, double* g, double* sd, double* so, double* rd,
+                          double* ro);
+
 /* Selects the CUDA device used by handles created afterwards on this thread
  * (one process per GPU: the rank's local device). */
 int ldg_set_device(int device);

@@ -87,6 +87,7 @@ _lib = None
 # The C ABI: name -> (restype, argtypes).  tests/test_capi.py checks that the
 # library exports exactly what include/ldg_b200.h declares.
 _SIGNATURES = {
+    "ldg_reference_tensors": (C.c_int, [C.c_int] + [_dp] * 7),
     "ldg_set_device": (C.c_int, [C.c_int]),
     "ldg_create": (C.c_int, [_dp, C.c_int, _ip, C.c_int, _ip, C.c_int, C.POINTER(_Problem), C.POINTER(_H)]),
     "ldg_create_square": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(_Problem),
@@ -129,6 +130,18 @@ def load_library():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def reference_tensors(n_local: int) -> dict:
+    """The library's host-built reference tensors (build_ref_tensors, reftensors.hpp:55); no GPU needed."""
+    n = int(n_local)
+    arrs = dict(m=np.zeros(n * n), h=np.zeros(n * n * 2), g=np.zeros(n ** 3 * 2), sd=np.zeros(n * n * 3),
+                so=np.zeros(n * n * 9), rd=np.zeros(n ** 3 * 3), ro=np.zeros(n ** 3 * 9))
+    lib = load_library()
+    rc = lib.ldg_reference_tensors(n, *[arrs[k].ctypes.data_as(_dp) for k in ("m", "h", "g", "sd", "so", "rd",
+                                                                             "ro")])
+    _raise(rc, lib.ldg_last_error(None).decode())
+    return arrs
 
 
 def set_device(device: int) -> None:

@@ -158,6 +158,23 @@ const char* ldg_last_error(const ldg_handle* H) {
   return g_last_error.c_str();
 }
 
+int ldg_reference_tensors(int n_local, double* m, double* h, double* g, double* sd, double* so, double* rd,
+                          double* ro) {
+  return guarded(nullptr, [&] {
+    const ldgb::RefTensors t = ldgb::reference_tensors(n_local);
+    auto put = [](const std::vector<double>& v, double* out) {
+      if (out) std::copy(v.begin(), v.end(), out);
+    };
+    put(t.m, m);
+    put(t.h, h);
+    put(t.g, g);
+    put(t.sd, sd);
+    put(t.so, so);
+    put(t.rd, rd);
+    put(t.ro, ro);
+  });
+}
+
 int ldg_set_device(int device) {
   return guarded(nullptr, [&] { LDG_CUDA(cudaSetDevice(device)); });
 }
