@@ -64,7 +64,7 @@ typedef struct ldg_solver_opts {
   double rtol;          /* Schur-system relative residual target           */
   double atol;          /* absolute target on the Schur residual           */
   int maxit;            /* BiCGStab iterations                             */
-  int precond;          /* 0 none, 1 block-Jacobi of the Schur operator    */
+  int precond;          /* 0 none, 1 block-Jacobi, 2 multigrid V(2,2) (FK)  */
   int check_residual;   /* 1: enforce the reference residual contract      */
   double contract_tol;  /* 1e-10 in the reference                          */
 } ldg_solver_opts;

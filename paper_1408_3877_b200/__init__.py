@@ -208,7 +208,7 @@ class SolverOptions:
     rtol: float = 0.0
     atol: float = 0.0
     maxit: int = 20000
-    precond: int = 1
+    precond: int = 2  # 0 none, 1 block-Jacobi, 2 geometric multigrid V(2,2) (FK meshes; else 1)
     check_residual: bool = True
     contract_tol: float = 1e-10
 

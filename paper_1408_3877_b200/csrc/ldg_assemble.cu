@@ -417,7 +417,7 @@ void launch_project_n(Handle& h, const ldg_coeff& f0, const ldg_coeff* f1, doubl
   const size_t smem = sizeof(double) * (R * (3 + N) + N * N);
   auto kern = k_project<N>;
   LDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  kern<<<grid_of(count, 128), 128, smem, h.stream>>>(h.mesh(), count, rule, R, h.tab.ptr + h.dtab.minv, f0,
+  kern<<<grid_of(count, 128), 128, smem, h.stream>>>(h.mesh(), count, rule, R, h.dtab.base + h.dtab.minv, f0,
                                                      f1 ? *f1 : f0, f1 ? 2 : 1, t, out0, out1);
   LDG_CUDA(cudaGetLastError());
   ++h.launches;

@@ -77,7 +77,8 @@ void init_device_side(Handle& h, int p, const ldg_problem* prob) {
                       cudaMemcpyHostToDevice));
   const ldgb::TableLayout& L = h.tables.lay;
   h.dtab = ldgb::DevTables{h.tab.ptr, L.p, L.N, L.R, L.Qe, L.Qb, L.proj_phi, L.proj_w, L.proj_x, L.mhat,
-                           L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe, L.pth, L.we, L.pb, L.sb, L.wb, L.total};
+                           L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe, L.pth, L.we, L.pb, L.sb, L.wb, L.total,
+                           L.mono};
   ldgb::upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
 }
 
@@ -184,7 +185,7 @@ ldg_solver_opts ldg_default_solver_opts(void) {
   o.rtol = 0.0;
   o.atol = 0.0;
   o.maxit = 20000;
-  o.precond = 1;
+  o.precond = 2;
   o.check_residual = 1;
   o.contract_tol = 1e-10;
   return o;
@@ -225,6 +226,7 @@ void ldg_destroy(ldg_handle* H) {
   if (!H) return;
   Handle& h = H->h;
   if (h.stream) cudaStreamSynchronize(h.stream);
+  ldgb::mg_release(h);
   if (h.red_host) cudaFreeHost(h.red_host);
   for (auto& e : h.ev)
     if (e) cudaEventDestroy(e);
@@ -246,6 +248,7 @@ int ldg_get_info(const ldg_handle* H, ldg_info_t* out) {
   out->size = h.size;
   out->bytes_device = h.bytes;
   out->launches = h.launches;
+  for (const auto& c : h.coarse) out->launches += c->launches;
   return LDG_OK;
 }
 

@@ -37,7 +37,7 @@ enum EdgeKind : int { kInterior = 0, kDirichlet = 1, kNeumann = 2, kUnmapped = 3
 struct DevTables {
   const double* base;
   int p, N, R, Qe, Qb;
-  long proj_phi, proj_w, proj_x, mhat, minv, ghat, hhat, sdiag, soff, pe, pth, we, pb, sb, wb, total;
+  long proj_phi, proj_w, proj_x, mhat, minv, ghat, hhat, sdiag, soff, pe, pth, we, pb, sb, wb, total, mono;
 };
 
 struct DevMesh {

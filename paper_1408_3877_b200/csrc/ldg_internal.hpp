@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/ldg_b200.h"
@@ -105,11 +106,35 @@ struct Handle {
   int rule_elem_R = 0;
 
   cudaStream_t stream = nullptr;
+  bool owns_stream = true;
   cudaEvent_t ev[4] = {};
   std::string err;
 
+  // geometric multigrid hierarchy (ldg_mg.cu).  The top handle is level 0;
+  // coarse levels are Handles of their own (same p, tables and stream shared)
+  // on FK(dim / 2^l), with coordinates subsampled from the finer level.
+  int dim = 0;                                   // FK dim (0: general mesh)
+  const double* rule_shared = nullptr;           // coarse levels use level 0's rule
+  int rule_shared_R = 0;
+  std::vector<std::unique_ptr<Handle>> coarse;   // levels 1 .. L-1 (top handle only)
+  DBuf<int> mg_parent;                           // element -> parent in the next coarser level
+  DBuf<int> mg_children;                         // [4][Kp] children in the next finer level
+  DBuf<double> mg_P;                             // [N*N][Kp] prolongation block of each element
+  DBuf<double> mg_x, mg_b, mg_r;                 // V-cycle work vectors (N * Kp)
+  bool mg_ready = false;
+  struct VGraph {                                // a captured V-cycle (CUDA graph)
+    cudaGraphExec_t exec = nullptr;
+    const double* b = nullptr;
+    double* x = nullptr;
+    double wm = 0.0, dt = 0.0;
+    int64_t kernels = 0;
+  };
+  std::vector<VGraph> vgraphs;
+
   DevMesh mesh() const { return DevMesh{K, Kg, Kp, geom.ptr, nbr.ptr, nbrn.ptr, kind.ptr}; }
   long vec_len() const { return static_cast<long>(N) * Kp; }
+  const double* rule_ptr() const { return rule_shared ? rule_shared : rule_elem.ptr; }
+  int rule_R() const { return rule_shared ? rule_shared_R : rule_elem_R; }
 };
 
 // ---- launchers (defined in the .cu files) ----------------------------------
@@ -141,8 +166,20 @@ void launch_dots(Handle& h, long n, int ndots, const double* const* xs, const do
 void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev);
 void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa);
 
+void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
+void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
+                     const double* z, double* out);
+
 // driver pieces (ldg_solve.cu)
 void assemble_step(Handle& h, double t);
 int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st);
+
+// multigrid (ldg_mg.cu)
+void build_square_from_coords(Handle& h, int dim, const double* coords_dev);
+bool mg_build(Handle& h);                                   // false: no hierarchy for this mesh
+void mg_setup_step(Handle& h, double t, double wm, double dt);  // per step: coarse E, block-Jacobi
+void mg_vcycle(Handle& h, double wm, double dt, const double* b, double* x);  // x = V(b), level 0 = h
+int mg_levels(const Handle& h);
+void mg_release(Handle& h);  // destroys captured graphs
 
 }  // namespace ldgb

@@ -299,6 +299,25 @@ void build_square_mesh(Handle& h, int dim, double jitter, uint64_t seed) {
   ++h.launches;
   h.gid.resize(K);
   for (long k = 0; k < K; ++k) h.gid[k] = static_cast<int>(k);
+  h.dim = dim;
+  topology_and_geometry(h, 1.0, nullptr);
+}
+
+// A multigrid level: FK(dim) triangles on given device coordinates (the
+// finer level's vertices subsampled), same topology/geometry pass.
+void build_square_from_coords(Handle& h, int dim, const double* coords_dev) {
+  const long V = static_cast<long>(dim + 1) * (dim + 1);
+  const long K = 2L * dim * dim;
+  h.V = static_cast<int>(V);
+  h.K = h.Kg = h.Kglobal = static_cast<int>(K);
+  h.Kp = padded(K);
+  h.dim = dim;
+  h.coords.alloc(2 * V, &h.bytes);
+  h.v0t.alloc(3 * K, &h.bytes);
+  LDG_CUDA(cudaMemcpyAsync(h.coords.ptr, coords_dev, sizeof(double) * 2 * V, cudaMemcpyDeviceToDevice, h.stream));
+  k_fk_triangles<<<grid_of(K, 256), 256, 0, h.stream>>>(dim, h.v0t.ptr);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
   topology_and_geometry(h, 1.0, nullptr);
 }
 

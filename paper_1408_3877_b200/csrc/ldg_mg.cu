@@ -1,0 +1,351 @@
+// Geometric multigrid preconditioner for the Schur system of each implicit-
+// Euler step (the reference has none: it factorises with SparseLU every step,
+// system.hpp:190-205).
+//
+// Friedrichs-Keller meshes nest: FK(dim) is the red refinement of FK(dim/2)
+// (each coarse triangle holds 4 fine ones).  Coarse levels are rediscretised:
+// every level is a Handle of its own on FK(dim/2^l) with vertex coordinates
+// subsampled from the finer level (so jittered meshes coarsen consistently),
+// d projected on that level, and the same assembly / Schur kernels.  Transfer
+// is the exact L2 embedding of the coarse polynomial space: per fine element
+// one N x N block P_k (fine coeffs = P_k coarse coeffs of the parent),
+// restriction is P^T (residuals are integrated quantities).  V(2,2) cycle
+// with damped block-Jacobi smoothing (omega = 0.7) on every level; the
+// coarsest level (dim 2) gets two smoothing sweeps.  Prototyped in numpy
+// against the oracle first: 12-27 BiCGStab iterations for p = 1..4
+// independent of h, against 170-2100 with block-Jacobi alone.
+#include <cmath>
+
+#include "ldg_internal.hpp"
+
+namespace ldgb {
+
+namespace {
+
+template <int P>
+struct Cfg {
+  static constexpr int N = (P + 1) * (P + 2) / 2;
+};
+
+constexpr double kOmega = 0.7;
+constexpr int kNu = 2;
+constexpr int kCoarseSweeps = 2;
+
+inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+#define LDG_DISPATCH_P(p, CALL) \
+  switch (p) {                  \
+    case 0: { CALL(0); break; } \
+    case 1: { CALL(1); break; } \
+    case 2: { CALL(2); break; } \
+    case 3: { CALL(3); break; } \
+    default: { CALL(4); break; } \
+  }
+
+// coarse vertex (ix, iy) of FK(dim_c) = fine vertex (2 ix, 2 iy) of FK(2 dim_c)
+__global__ void k_subsample(int dim_c, const double* __restrict__ cf, double* __restrict__ cc) {
+  const long Vc = static_cast<long>(dim_c + 1) * (dim_c + 1);
+  const long v = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (v >= Vc) return;
+  const int ix = static_cast<int>(v / (dim_c + 1)), iy = static_cast<int>(v % (dim_c + 1));
+  const long vf = static_cast<long>(2 * ix) * (2 * dim_c + 1) + 2 * iy;
+  cc[2 * v] = cf[2 * vf];
+  cc[2 * v + 1] = cf[2 * vf + 1];
+}
+
+// parent of every fine element and the 4 children of every coarse element.
+// Coarse lower (cx,cy) holds fine lower (0,0),(1,0),(0,1) and upper (0,0) of
+// its 2x2 block; coarse upper holds fine lower (1,1) and upper (1,0),(0,1),(1,1).
+__global__ void k_fk_parent(int dim_f, long Kp_c, int* __restrict__ parent, int* __restrict__ children) {
+  const long Kf = 2L * dim_f * dim_f;
+  const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (k >= Kf) return;
+  const int dim_c = dim_f / 2;
+  const bool lower = k < static_cast<long>(dim_f) * dim_f;
+  const long q = lower ? k : k - static_cast<long>(dim_f) * dim_f;
+  const int ix = static_cast<int>(q / dim_f), iy = static_cast<int>(q % dim_f);
+  const int cx = ix >> 1, cy = iy >> 1, lx = ix & 1, ly = iy & 1;
+  bool clower;
+  int slot;
+  if (lower) {
+    clower = !(lx && ly);
+    slot = clower ? (lx ? 1 : (ly ? 2 : 0)) : 0;
+  } else {
+    clower = !lx && !ly;
+    slot = clower ? 3 : (lx && !ly ? 1 : (!lx && ly ? 2 : 3));
+  }
+  const int kc = clower ? cx * dim_c + cy : dim_c * dim_c + cx * dim_c + cy;
+  parent[k] = kc;
+  children[slot * Kp_c + kc] = static_cast<int>(k);
+}
+
+template <int N>
+__device__ __forceinline__ void eval_basis(const double* __restrict__ mono, double x1, double x2, double* phi) {
+  // monomials x1^a x2^b in the order (0,0),(1,0),(0,1),(2,0),(1,1),(0,2),...
+  double m[15];
+  m[0] = 1.0;
+  int at = 1;
+  double p1[5] = {1.0, x1, x1 * x1, x1 * x1 * x1, x1 * x1 * x1 * x1};
+  double p2[5] = {1.0, x2, x2 * x2, x2 * x2 * x2, x2 * x2 * x2 * x2};
+  for (int d = 1; d <= 4; ++d)
+    for (int a = d; a >= 0; --a) m[at++] = p1[a] * p2[d - a];
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+    for (int q = 0; q < 15; ++q) s += mono[i * 15 + q] * m[q];
+    phi[i] = s;
+  }
+}
+
+// P_k[i][j] = sum_a minv[i][a] int_ref phi_a(xh) phi_j(xi(xh)), xi = parent
+// reference coordinates of the fine point; exact with the order-2p rule.
+template <int P>
+__global__ void __launch_bounds__(128) k_prolong_blocks(DevMesh f, DevMesh c, DevTables T, const int* __restrict__ parent,
+                                                        double* __restrict__ Pm) {
+  constexpr int N = Cfg<P>::N, NN = N * N;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= f.K) return;
+  const double* base = T.base;
+  const int R = T.R;
+  const int kc = parent[k];
+  const double* gf = f.geom;
+  const double* gc = c.geom;
+  const long Kf = f.Kp, Kc = c.Kp;
+  const double b11 = gc[kB11 * Kc + kc], b12 = gc[kB12 * Kc + kc], b21 = gc[kB21 * Kc + kc], b22 = gc[kB22 * Kc + kc];
+  const double det = b11 * b22 - b12 * b21;
+  double acc[NN];
+  for (int ij = 0; ij < NN; ++ij) acc[ij] = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const double r1 = base[T.proj_x + 2 * r], r2 = base[T.proj_x + 2 * r + 1], w = base[T.proj_w + r];
+    const double x1 = gf[kB11 * Kf + k] * r1 + gf[kB12 * Kf + k] * r2 + gf[kA1x * Kf + k];
+    const double x2 = gf[kB21 * Kf + k] * r1 + gf[kB22 * Kf + k] * r2 + gf[kA1y * Kf + k];
+    const double d1 = x1 - gc[kA1x * Kc + kc], d2 = x2 - gc[kA1y * Kc + kc];
+    const double xi1 = (b22 * d1 - b12 * d2) / det, xi2 = (b11 * d2 - b21 * d1) / det;
+    double pc[N];
+    eval_basis<N>(base + T.mono, xi1, xi2, pc);
+    const double* pf = base + T.proj_phi + r * N;
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) acc[i * N + j] += w * pf[i] * pc[j];
+  }
+  const double* minv = base + T.minv;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      double s = 0.0;
+      for (int a = 0; a < N; ++a) s += minv[i * N + a] * acc[a * N + j];
+      Pm[static_cast<long>(i * N + j) * Kf + k] = s;
+    }
+}
+
+// bc[kc] = sum over the 4 children of P_child^T rf[child]
+template <int P>
+__global__ void __launch_bounds__(128) k_restrict(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
+                                                  const double* __restrict__ Pm, const double* __restrict__ rf,
+                                                  double* __restrict__ bc) {
+  constexpr int N = Cfg<P>::N;
+  const int kc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (kc >= Kc) return;
+  double acc[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) acc[j] = 0.0;
+#pragma unroll 1
+  for (int s = 0; s < 4; ++s) {
+    const int k = children[s * Kpc + kc];
+    double r[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = rf[i * Kpf + k];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc[j] += Pm[static_cast<long>(i * N + j) * Kpf + k] * r[i];
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) bc[j * Kpc + kc] = acc[j];
+}
+
+// xf[k] += P_k xc[parent[k]]
+template <int P>
+__global__ void __launch_bounds__(128) k_prolong_add(int Kf, long Kpf, long Kpc, const int* __restrict__ parent,
+                                                     const double* __restrict__ Pm, const double* __restrict__ xc,
+                                                     double* __restrict__ xf) {
+  constexpr int N = Cfg<P>::N;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= Kf) return;
+  const int kc = parent[k];
+  double c[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) c[j] = xc[j * Kpc + kc];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s += Pm[static_cast<long>(i * N + j) * Kpf + k] * c[j];
+    xf[i * Kpf + k] += s;
+  }
+}
+
+Handle* level_at(Handle& h, int l) { return l == 0 ? &h : h.coarse[l - 1].get(); }
+
+// r = b - A x  (A the level's Schur operator)
+void residual(Handle& L, double wm, double dt, const double* b, const double* x, double* r) {
+  launch_stage1(L, nullptr, 0.0, x, 1.0, L.tz.ptr);
+  launch_stage2(L, x, -wm, -dt * L.prob.eta, L.tz.ptr, -dt, b, 1.0, r);
+}
+
+void smooth_once(Handle& L, double wm, double dt, const double* b, double* x) {
+  residual(L, wm, dt, b, x, L.mg_r.ptr);
+  launch_bjac_axpy(L, L.mg_r.ptr, kOmega, 1.0, x);
+}
+
+void vcycle(Handle& h, int l, double wm, double dt, const double* b, double* x) {
+  Handle& L = *level_at(h, l);
+  const int last = static_cast<int>(h.coarse.size());
+  launch_bjac_axpy(L, b, kOmega, 0.0, x);  // first sweep from x = 0
+  if (l == last) {
+    for (int s = 1; s < kCoarseSweeps; ++s) smooth_once(L, wm, dt, b, x);
+    return;
+  }
+  for (int s = 1; s < kNu; ++s) smooth_once(L, wm, dt, b, x);
+  residual(L, wm, dt, b, x, L.mg_r.ptr);
+  Handle& C = *level_at(h, l + 1);
+  const int P = h.p;
+#define CALL(PP)                                                                                               \
+  k_restrict<PP><<<grid_of(C.K, 128), 128, 0, h.stream>>>(C.K, C.Kp, L.Kp, C.mg_children.ptr, L.mg_P.ptr,      \
+                                                          L.mg_r.ptr, C.mg_b.ptr)
+  LDG_DISPATCH_P(P, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++L.launches;
+  vcycle(h, l + 1, wm, dt, C.mg_b.ptr, C.mg_x.ptr);
+#define CALL(PP)                                                                                                \
+  k_prolong_add<PP><<<grid_of(L.K, 128), 128, 0, h.stream>>>(L.K, L.Kp, C.Kp, L.mg_parent.ptr, L.mg_P.ptr,      \
+                                                             C.mg_x.ptr, x)
+  LDG_DISPATCH_P(P, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++L.launches;
+  for (int s = 0; s < kNu; ++s) smooth_once(L, wm, dt, b, x);
+}
+
+}  // namespace
+
+int mg_levels(const Handle& h) { return 1 + static_cast<int>(h.coarse.size()); }
+
+bool mg_build(Handle& h) {
+  if (h.mg_ready) return true;
+  if (h.dim < 4 || (h.dim % 2) != 0 || h.size > 1) return false;
+  const long NN = static_cast<long>(h.N) * h.N;
+  h.mg_r.alloc(h.vec_len(), &h.bytes);
+  Handle* fine = &h;
+  int d = h.dim;
+  while (d % 2 == 0 && d / 2 >= 2) {
+    const int dc = d / 2;
+    auto c = std::make_unique<Handle>();
+    c->p = h.p;
+    c->N = h.N;
+    c->prob = h.prob;
+    c->dtab = h.dtab;
+    c->stream = h.stream;
+    c->owns_stream = false;
+    c->rule_shared = h.rule_ptr();
+    c->rule_shared_R = h.rule_R();
+    {
+      DBuf<double> cc;
+      const long Vc = static_cast<long>(dc + 1) * (dc + 1);
+      cc.alloc(2 * Vc, nullptr);
+      k_subsample<<<grid_of(Vc, 256), 256, 0, h.stream>>>(dc, fine->coords.ptr, cc.ptr);
+      LDG_CUDA(cudaGetLastError());
+      build_square_from_coords(*c, dc, cc.ptr);
+      LDG_CUDA(cudaStreamSynchronize(h.stream));
+    }
+    const long n = c->vec_len();
+    c->D.alloc(n, &c->bytes);
+    c->E.alloc(8 * NN * c->Kp, &c->bytes);
+    c->Bst.alloc(8 * NN * c->Kp, &c->bytes);
+    c->Sst.alloc(4 * NN * c->Kp, &c->bytes);
+    c->Pinv.alloc(NN * c->Kp, &c->bytes);
+    c->tz.alloc(2 * n, &c->bytes);
+    c->mg_x.alloc(n, &c->bytes);
+    c->mg_b.alloc(n, &c->bytes);
+    c->mg_r.alloc(n, &c->bytes);
+    c->mg_children.alloc(4 * c->Kp, &c->bytes);
+    launch_static(*c, kStB, c->Bst.ptr);
+    launch_static(*c, kStS, c->Sst.ptr);
+    fine->mg_parent.alloc(fine->Kp, &fine->bytes);
+    fine->mg_P.alloc(NN * fine->Kp, &fine->bytes);
+    k_fk_parent<<<grid_of(fine->K, 256), 256, 0, h.stream>>>(d, c->Kp, fine->mg_parent.ptr, c->mg_children.ptr);
+    LDG_CUDA(cudaGetLastError());
+#define CALL(PP)                                                                                              \
+  k_prolong_blocks<PP><<<grid_of(fine->K, 128), 128, 0, h.stream>>>(fine->mesh(), c->mesh(), h.dtab,         \
+                                                                   fine->mg_parent.ptr, fine->mg_P.ptr)
+    LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+    LDG_CUDA(cudaGetLastError());
+    fine = c.get();
+    h.coarse.push_back(std::move(c));
+    d = dc;
+  }
+  LDG_CUDA(cudaStreamSynchronize(h.stream));
+  h.mg_ready = !h.coarse.empty();
+  return h.mg_ready;
+}
+
+void mg_setup_step(Handle& h, double t, double wm, double dt) {
+  for (auto& cp : h.coarse) {
+    Handle& c = *cp;
+    launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.K);
+    launch_assemble(c, kModeE, c.E.ptr);
+    launch_bjac_setup(c, wm, dt);
+  }
+}
+
+// The V-cycle is a fixed sequence of ~14 kernels per level with no host
+// synchronisation, so it is captured once per (b, x, wm, dt) into a CUDA
+// graph and replayed: launch latency, not bandwidth, bounds the small coarse
+// levels.  Operator contents (E, block-Jacobi inverses) change every step
+// in place; the graph only bakes pointers and the scalars wm, dt.
+void mg_vcycle(Handle& h, double wm, double dt, const double* b, double* x) {
+  for (auto& g : h.vgraphs)
+    if (g.b == b && g.x == x && g.wm == wm && g.dt == dt) {
+      LDG_CUDA(cudaGraphLaunch(g.exec, h.stream));
+      h.launches += g.kernels;
+      return;
+    }
+  if (h.vgraphs.size() >= 8) {
+    for (auto& g : h.vgraphs) cudaGraphExecDestroy(g.exec);
+    h.vgraphs.clear();
+  }
+  auto count = [&h] {
+    int64_t n = h.launches;
+    for (auto& c : h.coarse) n += c->launches;
+    return n;
+  };
+  const int64_t before = count();
+  cudaGraph_t graph = nullptr;
+  LDG_CUDA(cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    vcycle(h, 0, wm, dt, b, x);
+  } catch (...) {
+    cudaStreamEndCapture(h.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  LDG_CUDA(cudaStreamEndCapture(h.stream, &graph));
+  Handle::VGraph g;
+  g.b = b;
+  g.x = x;
+  g.wm = wm;
+  g.dt = dt;
+  g.kernels = count() - before;
+  const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  LDG_CUDA(e);
+  h.vgraphs.push_back(g);
+  LDG_CUDA(cudaGraphLaunch(g.exec, h.stream));
+}
+
+void mg_release(Handle& h) {
+  for (auto& g : h.vgraphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  h.vgraphs.clear();
+}
+
+}  // namespace ldgb

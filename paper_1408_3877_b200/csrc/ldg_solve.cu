@@ -43,6 +43,43 @@ __device__ __forceinline__ void block_mv(const double* __restrict__ blk, long Kp
   }
 }
 
+// acc[i] += sum_j blk[(i*N+j)][k] * x[j][col], streamed one block column at a
+// time: N coalesced loads in flight per step and N live accumulators, so
+// p = 3, 4 blocks (100, 225 values) neither spill nor serialise.
+template <int N>
+__device__ __forceinline__ void block_mv_gather(const double* __restrict__ blk, long Kp, int k,
+                                                const double* __restrict__ x, int col, double* acc) {
+  const long NKp = static_cast<long>(N) * Kp;
+  if constexpr (N <= 6) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double xj = x[j * Kp + col];
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(blk[i * NKp + j * Kp + k], xj, acc[i]);
+    }
+  } else {
+    const double* bj = blk + k;
+#pragma unroll 1
+    for (int j = 0; j < N; ++j, bj += Kp) {
+      const double xj = x[j * Kp + col];
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(bj[i * NKp], xj, acc[i]);
+    }
+  }
+}
+
+// acc[i] += scale * sum_j s_mat[i*N+j] * x[j][col]  (s_mat a reference matrix in smem)
+template <int N>
+__device__ __forceinline__ void smem_mv_gather(const double* s_mat, const double* __restrict__ x, long Kp, int col,
+                                               double scale, double* acc) {
+#pragma unroll(N <= 6 ? N : 1)
+  for (int j = 0; j < N; ++j) {
+    const double xj = scale * x[j * Kp + col];
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fma(s_mat[i * N + j], xj, acc[i]);
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void load_vec(const double* __restrict__ x, long Kp, int col, double* xv) {
 #pragma unroll
@@ -74,9 +111,7 @@ __global__ void __launch_bounds__(128) k_stage1(DevMesh m, const double* __restr
       for (int s = 0; s < 4; ++s) {
         const int col = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
         if (col < 0) continue;
-        double xv[N];
-        load_vec<N>(x, Kp, col, xv);
-        block_mv<N>(Bc + static_cast<long>(s) * NN * Kp, Kp, k, xv, u);
+        block_mv_gather<N>(Bc + static_cast<long>(s) * NN * Kp, Kp, k, x, col, u);
       }
 #pragma unroll
       for (int i = 0; i < N; ++i) u[i] *= tau;
@@ -85,7 +120,7 @@ __global__ void __launch_bounds__(128) k_stage1(DevMesh m, const double* __restr
 #pragma unroll
       for (int i = 0; i < N; ++i) u[i] += sigma * vz[(c * N + i) * Kp + k];
     }
-#pragma unroll
+#pragma unroll(N <= 6 ? N : 1)
     for (int i = 0; i < N; ++i) {
       double s = 0.0;
 #pragma unroll
@@ -121,9 +156,7 @@ __global__ void __launch_bounds__(128) k_stage2(DevMesh m, const double* __restr
       for (int s = 0; s < 4; ++s) {
         const int col = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
         if (col < 0) continue;
-        double xv[N];
-        load_vec<N>(tc, Kp, col, xv);
-        block_mv<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, xv, acc);
+        block_mv_gather<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, tc, col, acc);
       }
     }
 #pragma unroll
@@ -140,9 +173,7 @@ __global__ void __launch_bounds__(128) k_stage2(DevMesh m, const double* __restr
       for (int s = 0; s < 4; ++s) {
         const int col = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
         if (col < 0) continue;
-        double xv[N];
-        load_vec<N>(x, Kp, col, xv);
-        block_mv<N>(S + static_cast<long>(s) * NN * Kp, Kp, k, xv, sacc);
+        block_mv_gather<N>(S + static_cast<long>(s) * NN * Kp, Kp, k, x, col, sacc);
       }
     }
     const double two_a = alpha * 2.0 * m.geom[kArea * Kp + k];
@@ -191,19 +222,13 @@ __global__ void __launch_bounds__(128) k_full(DevMesh m, const double* __restric
 #pragma unroll 1
     for (int s = 0; s < 4; ++s) {
       if (cols[s] < 0) continue;
-      double xv[N];
-      load_vec<N>(C, Kp, cols[s], xv);
-      block_mv<N>(Bc + static_cast<long>(s) * NN * Kp, Kp, k, xv, acc);
+      block_mv_gather<N>(Bc + static_cast<long>(s) * NN * Kp, Kp, k, C, cols[s], acc);
     }
-    double zk[N];
-    load_vec<N>(Yin + static_cast<long>(c) * N * Kp, Kp, k, zk);
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double mz = 0.0;
+    for (int i = 0; i < N; ++i) acc[i] *= dt;
+    smem_mv_gather<N>(s_m, Yin + static_cast<long>(c) * N * Kp, Kp, k, dt * two_a, acc);
 #pragma unroll
-      for (int j = 0; j < N; ++j) mz += s_m[i * N + j] * zk[j];
-      out[(c * N + i) * Kp + k] = dt * (two_a * mz + acc[i]);
-    }
+    for (int i = 0; i < N; ++i) out[(c * N + i) * Kp + k] = acc[i];
   }
   double acc[N], sacc[N];
 #pragma unroll
@@ -214,27 +239,20 @@ __global__ void __launch_bounds__(128) k_full(DevMesh m, const double* __restric
 #pragma unroll 1
     for (int s = 0; s < 4; ++s) {
       if (cols[s] < 0) continue;
-      double xv[N];
-      load_vec<N>(Yin + static_cast<long>(c) * N * Kp, Kp, cols[s], xv);
-      block_mv<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, xv, acc);
+      block_mv_gather<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, Yin + static_cast<long>(c) * N * Kp, cols[s],
+                         acc);
     }
   }
 #pragma unroll 1
   for (int s = 0; s < 4; ++s) {
     if (cols[s] < 0) continue;
-    double xv[N];
-    load_vec<N>(C, Kp, cols[s], xv);
-    block_mv<N>(S + static_cast<long>(s) * NN * Kp, Kp, k, xv, sacc);
+    block_mv_gather<N>(S + static_cast<long>(s) * NN * Kp, Kp, k, C, cols[s], sacc);
   }
-  double ck[N];
-  load_vec<N>(C, Kp, k, ck);
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double mc = 0.0;
+  for (int i = 0; i < N; ++i) acc[i] = dt * (acc[i] + eta * sacc[i]);
+  if (wm != 0.0) smem_mv_gather<N>(s_m, C, Kp, k, wm * two_a, acc);
 #pragma unroll
-    for (int j = 0; j < N; ++j) mc += s_m[i * N + j] * ck[j];
-    out[(2 * N + i) * Kp + k] = wm * two_a * mc + dt * (acc[i] + eta * sacc[i]);
-  }
+  for (int i = 0; i < N; ++i) out[(2 * N + i) * Kp + k] = acc[i];
 }
 
 // Block-Jacobi preconditioner of the Schur operator, one N x N block per
@@ -348,13 +366,40 @@ __global__ void __launch_bounds__(128) k_bjac_apply(int K, long Kp, const double
   constexpr int N = Cfg<P>::N;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
-  double xv[N], acc[N];
-  load_vec<N>(x, Kp, k, xv);
+  double acc[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) acc[i] = 0.0;
-  block_mv<N>(Pinv, Kp, k, xv, acc);
+  block_mv_gather<N>(Pinv, Kp, k, x, k, acc);
 #pragma unroll
   for (int i = 0; i < N; ++i) y[i * Kp + k] = acc[i];
+}
+
+// y = beta y + omega P^-1 x  (damped block-Jacobi smoothing step)
+template <int P>
+__global__ void __launch_bounds__(128) k_bjac_axpy(int K, long Kp, const double* __restrict__ Pinv,
+                                                   const double* __restrict__ x, double omega, double beta,
+                                                   double* __restrict__ y) {
+  constexpr int N = Cfg<P>::N;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double acc[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] = 0.0;
+  block_mv_gather<N>(Pinv, Kp, k, x, k, acc);
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i * Kp + k] = (beta == 0.0 ? 0.0 : beta * y[i * Kp + k]) + omega * acc[i];
+}
+
+// out = a x + b y + c z  (y, z may be null when b, c are 0; out may alias x or y)
+__global__ void k_lincomb3(long n, double a, const double* x, double b, const double* y, double c, const double* z,
+                           double* out) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    double v = a * x[i];
+    if (y) v += b * y[i];
+    if (z) v += c * z[i];
+    out[i] = v;
+  }
 }
 
 __global__ void k_axpby(long n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
@@ -437,7 +482,7 @@ __global__ void k_kmajor_to_soa(int K, int N, long Kp, int nvec, const double* _
 void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout) {
   const unsigned grid = grid_of(h.K, 128);
 #define CALL(P)                                                                                             \
-  k_stage1<P><<<grid, 128, 0, h.stream>>>(h.mesh(), h.tab.ptr + h.dtab.minv, h.Bst.ptr, vz, sigma, x, tau, \
+  k_stage1<P><<<grid, 128, 0, h.stream>>>(h.mesh(), h.dtab.base + h.dtab.minv, h.Bst.ptr, vz, sigma, x, tau, \
                                           tout)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -449,7 +494,7 @@ void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, co
                    const double* w, double delta, double* y) {
   const unsigned grid = grid_of(h.K, 128);
 #define CALL(P)                                                                                                 \
-  k_stage2<P><<<grid, 128, 0, h.stream>>>(h.mesh(), h.tab.ptr + h.dtab.mhat, h.Sst.ptr, h.E.ptr, x, alpha_m, \
+  k_stage2<P><<<grid, 128, 0, h.stream>>>(h.mesh(), h.dtab.base + h.dtab.mhat, h.Sst.ptr, h.E.ptr, x, alpha_m, \
                                           beta_s, tz, gamma_e, w, delta, y)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -460,7 +505,7 @@ void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, co
 void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double* out) {
   const unsigned grid = grid_of(h.K, 128);
 #define CALL(P)                                                                                                  \
-  k_full<P><<<grid, 128, 0, h.stream>>>(h.mesh(), h.tab.ptr + h.dtab.mhat, h.Bst.ptr, h.Sst.ptr, h.E.ptr, Y, wm, \
+  k_full<P><<<grid, 128, 0, h.stream>>>(h.mesh(), h.dtab.base + h.dtab.mhat, h.Bst.ptr, h.Sst.ptr, h.E.ptr, Y, wm, \
                                         dt, h.prob.eta, out)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -473,8 +518,8 @@ void launch_bjac_setup(Handle& h, double wm, double dt) {
   do {                                                                                                       \
     constexpr int NN = Cfg<P>::N * Cfg<P>::N;                                                                \
     constexpr int EPC = (256 / NN) > 0 ? (256 / NN) : 1;                                                     \
-    k_bjac_setup<P><<<grid_of(h.K, EPC), 256, 0, h.stream>>>(h.mesh(), h.tab.ptr + h.dtab.mhat,             \
-                                                             h.tab.ptr + h.dtab.minv, h.Bst.ptr, h.Sst.ptr,  \
+    k_bjac_setup<P><<<grid_of(h.K, EPC), 256, 0, h.stream>>>(h.mesh(), h.dtab.base + h.dtab.mhat,             \
+                                                             h.dtab.base + h.dtab.minv, h.Bst.ptr, h.Sst.ptr,  \
                                                              h.E.ptr, wm, dt, h.prob.eta, h.Pinv.ptr);       \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
@@ -488,6 +533,22 @@ void launch_bjac_apply(Handle& h, const double* x, double* y) {
 #define CALL(P) k_bjac_apply<P><<<grid, 128, 0, h.stream>>>(h.K, h.Kp, h.Pinv.ptr, x, y)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y) {
+  const unsigned grid = grid_of(h.K, 128);
+#define CALL(P) k_bjac_axpy<P><<<grid, 128, 0, h.stream>>>(h.K, h.Kp, h.Pinv.ptr, x, omega, beta, y)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
+                     const double* z, double* out) {
+  k_lincomb3<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, a, x, b, y, c, z, out);
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
@@ -533,7 +594,7 @@ size_t reduction_scratch() { return static_cast<size_t>(kMaxDots) * kRedBlocks +
 // ------------------------------------------------------------------ driver
 
 void assemble_step(Handle& h, double t) {
-  launch_project_df(h, t, h.rule_elem.ptr, h.rule_elem_R);  // K2: d, f (system.hpp:112-113)
+  launch_project_df(h, t, h.rule_ptr(), h.rule_R());        // K2: d, f (system.hpp:112-113)
   launch_rhs(h, t);                                          // K5: V (system.hpp:142-150)
   launch_assemble(h, kModeE, h.E.ptr);                       // K3: E^m (system.hpp:115-117)
   h.assembled = true;
@@ -555,8 +616,10 @@ void schur_apply(Handle& h, double wm, double dt, const double* x, double* y) {
   launch_stage2(h, x, wm, dt * h.prob.eta, h.tz.ptr, dt, nullptr, 0.0, y);
 }
 
-void precond(Handle& h, int pc, const double* x, double* y) {
-  if (pc == 1)
+void precond(Handle& h, int pc, double wm, double dt, const double* x, double* y) {
+  if (pc == 2)
+    mg_vcycle(h, wm, dt, x, y);
+  else if (pc == 1)
     launch_bjac_apply(h, x, y);
   else
     LDG_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice, h.stream));
@@ -588,7 +651,10 @@ int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_st
   const double rhs_norm = norm2(h, h.full_r.ptr, n3);
   const double contract = o.contract_tol > 0.0 ? o.contract_tol : 1e-10;
 
-  if (o.precond == 1) launch_bjac_setup(h, wm, dt);
+  int pc = o.precond;
+  if (pc == 2 && !mg_build(h)) pc = 1;  // no FK hierarchy (general mesh): block-Jacobi
+  if (pc >= 1) launch_bjac_setup(h, wm, dt);
+  if (pc == 2) mg_setup_step(h, h.t_assembled, wm, dt);
 
   const double bnorm = norm2(h, h.kr_b.ptr, n);
   // stopping test on the Schur residual: the user's rtol/atol, tightened so
@@ -617,17 +683,19 @@ int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_st
   LDG_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * n, h.stream));
   LDG_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * n, h.stream));
   double rho = 1.0, alpha = 1.0, omega = 1.0;
-  double rnorm = norm2(h, r, n);
+  // three host synchronisations per iteration: (rh,v); (t,s),(t,t),(s,s); (r,r),(rh,r)
+  double rr_rhr[2];
+  {
+    const double* xs[2] = {r, rh};
+    const double* ys[2] = {r, r};
+    launch_dots(h, n, 2, xs, ys, rr_rhr);
+  }
+  double rnorm = std::sqrt(rr_rhr[0]);
+  double rho1 = rr_rhr[1];
   int it = 0;
   bool converged = rnorm <= tol;
   while (!converged && it < o.maxit) {
     ++it;
-    double rho1;
-    {
-      const double* xs[1] = {rh};
-      const double* ys[1] = {r};
-      launch_dots(h, n, 1, xs, ys, &rho1);
-    }
     if (rho1 == 0.0 || !std::isfinite(rho1)) {
       // breakdown: restart with the current residual as shadow vector
       LDG_CUDA(cudaMemcpyAsync(rh, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, h.stream));
@@ -638,10 +706,8 @@ int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_st
       if (rho1 == 0.0) break;
     }
     const double beta = (rho1 / rho) * (alpha / omega);
-    // p = r + beta (p - omega v)
-    launch_axpby(h, n, -omega, v, 1.0, p);
-    launch_axpby(h, n, 1.0, r, beta, p);
-    precond(h, o.precond, p, ph);
+    launch_lincomb3(h, n, 1.0, r, beta, p, -beta * omega, v, p);  // p = r + beta (p - omega v)
+    precond(h, pc, wm, dt, p, ph);
     schur_apply(h, wm, dt, ph, v);
     ++applies;
     double rv;
@@ -651,32 +717,33 @@ int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_st
       launch_dots(h, n, 1, xs, ys, &rv);
     }
     alpha = rho1 / rv;
-    // s = r - alpha v
-    LDG_CUDA(cudaMemcpyAsync(s, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, h.stream));
-    launch_axpby(h, n, -alpha, v, 1.0, s);
-    const double snorm = norm2(h, s, n);
-    if (snorm <= tol) {
-      launch_axpby(h, n, alpha, ph, 1.0, C);
-      rnorm = snorm;
+    launch_lincomb3(h, n, 1.0, r, -alpha, v, 0.0, nullptr, s);  // s = r - alpha v
+    precond(h, pc, wm, dt, s, sh);
+    schur_apply(h, wm, dt, sh, t);
+    ++applies;
+    double ts[3];
+    {
+      const double* xs[3] = {t, t, s};
+      const double* ys[3] = {s, t, s};
+      launch_dots(h, n, 3, xs, ys, ts);
+    }
+    if (std::sqrt(ts[2]) <= tol) {  // converged on s: x += alpha p^
+      launch_lincomb3(h, n, 1.0, C, alpha, ph, 0.0, nullptr, C);
+      rnorm = std::sqrt(ts[2]);
       converged = true;
       break;
     }
-    precond(h, o.precond, s, sh);
-    schur_apply(h, wm, dt, sh, t);
-    ++applies;
-    double ts[2];
-    {
-      const double* xs[2] = {t, t};
-      const double* ys[2] = {s, t};
-      launch_dots(h, n, 2, xs, ys, ts);
-    }
     omega = ts[1] != 0.0 ? ts[0] / ts[1] : 0.0;
-    launch_axpby(h, n, alpha, ph, 1.0, C);
-    launch_axpby(h, n, omega, sh, 1.0, C);
-    LDG_CUDA(cudaMemcpyAsync(r, s, sizeof(double) * n, cudaMemcpyDeviceToDevice, h.stream));
-    launch_axpby(h, n, -omega, t, 1.0, r);
-    rnorm = norm2(h, r, n);
+    launch_lincomb3(h, n, 1.0, C, alpha, ph, omega, sh, C);  // x += alpha p^ + omega s^
+    launch_lincomb3(h, n, 1.0, s, -omega, t, 0.0, nullptr, r);  // r = s - omega t
+    {
+      const double* xs[2] = {r, rh};
+      const double* ys[2] = {r, r};
+      launch_dots(h, n, 2, xs, ys, rr_rhr);
+    }
+    rnorm = std::sqrt(rr_rhr[0]);
     rho = rho1;
+    rho1 = rr_rhr[1];
     if (!std::isfinite(rnorm)) break;
     converged = rnorm <= tol;
     if (omega == 0.0) break;

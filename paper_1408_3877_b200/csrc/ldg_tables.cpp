@@ -342,6 +342,7 @@ HostTables build_tables(int p) {
   L.pb = take(3L * L.Qb * N);
   L.sb = take(L.Qb);
   L.wb = take(L.Qb);
+  L.mono = take(15L * N);
   L.total = off;
   ht.data.assign(off, 0.0);
   double* d = ht.data.data();
@@ -381,6 +382,9 @@ HostTables build_tables(int p) {
     d[L.sb + q] = bnd.s[q];
     d[L.wb + q] = bnd.w[q];
   }
+  // phi_i = sum_m mono[i][m] x1^a_m x2^b_m (monomial order of kMonoA/kMonoB)
+  for (int i = 0; i < N; ++i)
+    for (int m = 0; m < 15; ++m) d[L.mono + i * 15 + m] = scale_of(i) * kBasis[i].c[m];
   return ht;
 }
 

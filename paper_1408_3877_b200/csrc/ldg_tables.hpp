@@ -53,6 +53,7 @@ struct TableLayout {
   long hhat, sdiag, soff;            // [i][j][m], [i][j][n], [i][j][nm][np]
   long pe, pth, we;                  // [n][q][i], [nm][np][q][j], [q]   (rank-Q edge form)
   long pb, sb, wb;                   // [n][q][i], [q], [q]              (RHS edge rule)
+  long mono;                         // [i][15] scaled monomial coefficients of phi_i
   long total = 0;
 };
 

@@ -1,7 +1,8 @@
+# GPU check run (gpurun): smoke, parity tests, short bench.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi -L > gpurun_out/smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
-timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 2 --warmup 3 --p 0,1,2 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log
+timeout 1200 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py ${BENCH_ARGS:---steps 3 --warmup 3} > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log
 tail -3 gpurun_out/smoke.log; tail -15 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/bench.log

@@ -145,6 +145,38 @@ def test_c1_hundred_steps_default_solver(golden, ld):
     assert st["residual"] <= 1e-10
 
 
+@pytest.mark.parametrize("p", [0, 1, 2, 3, 4])
+def test_multigrid_matches_block_jacobi(p, ld):
+    """The geometric-multigrid preconditioner changes the iteration count, not the
+    answer: same state as block-Jacobi within the solve tolerance, far fewer iterations."""
+    res = {}
+    for pc in (1, 2):
+        s = ld.LdgSystem.square(32, p, ld.BASELINE_SPEC, jitter=0.0)
+        s.initial_state()
+        st = s.euler_steps(0.05, 2, ld.SolverOptions(rtol=1e-13, precond=pc))
+        assert st["residual"] <= 1e-10
+        res[pc] = (s.get_state()[0], st["iterations"])
+    y1, it1 = res[1]
+    y2, it2 = res[2]
+    assert np.linalg.norm(y2 - y1) / np.linalg.norm(y1) <= 1e-9
+    assert it2 * 3 < it1, (it1, it2)
+
+
+def test_multigrid_jittered_mesh(ld):
+    """Config-4 style jittered FK mesh with mixed boundary conditions: multigrid
+    (coarse levels subsample the jittered vertices) agrees with block-Jacobi."""
+    spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
+                          boundary={1: "D", 2: "N", 3: "N", 4: "D"})
+    out = []
+    for pc in (1, 2):
+        s = ld.LdgSystem.square(32, 3, spec, jitter=0.2, seed=0)
+        s.initial_state()
+        st = s.euler_steps(0.1, 1, ld.SolverOptions(rtol=1e-13, precond=pc))
+        assert st["residual"] <= 1e-10
+        out.append(s.get_state()[0])
+    assert np.linalg.norm(out[1] - out[0]) / np.linalg.norm(out[0]) <= 1e-9
+
+
 def test_apply_lhs_matches_reference_operator(golden, ld):
     """The full block-SpMV (W + dt A) y against the reference's assembled A."""
     g = golden("jitter8_p2")
