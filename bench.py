@@ -55,11 +55,16 @@ def e_int(dim):
 
 
 def bytes_schur(dim, p):
-    """Algorithmic bytes of one Schur apply (stage 1 + stage 2):
-    B^1, B^2, S, E^1, E^2 blocks (K + 2 E_int each), vectors x, t^1, t^2, y, indices."""
+    """Compulsory bytes of one Schur-operator apply (k_stage1 + k_stage2):
+    the time-dependent E^1, E^2 blocks (K + 2 E_int blocks each, the only stored
+    blocks: M, B^m and S are rebuilt from shared-memory tables), the vectors
+    x (read twice), t^1, t^2 (written, read), y (written) and the per-element
+    geometry/topology (area, 3 lengths, 6 normal components; 3 nbr, 3 nbrn, 3 kind)."""
     K, N = 2 * dim * dim, n_of(p)
-    blocks = 5 * N * N * (K + 2 * e_int(dim))
-    return 8 * blocks + 8 * 7 * K * N + 4 * 2 * 3 * K + 8 * 2 * K
+    blocks = 2 * N * N * (K + 2 * e_int(dim))
+    vectors = 7 * K * N
+    geometry = 2 * 10 * K
+    return 8 * (blocks + vectors + geometry) + 4 * 2 * 9 * K
 
 
 def bytes_asm(dim, p):

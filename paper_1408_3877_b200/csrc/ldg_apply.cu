@@ -1,0 +1,665 @@
+// K6 — block-SpMV of the LDG operator, with the static blocks applied
+// matrix-free.
+//
+// Of the blocks of W + dt A (system.hpp:120-135, 162-167) only E^m =
+// -G^m + R^m + R_D^m (the C rows' Z columns) depend on d(t); they are
+// assembled every step (ldg_assemble.cu) and streamed from HBM here.  The
+// static ones — M = 2|T| mhat, B^m = -H^m + Q^m + Q_N^m (Z rows' C column) and
+// eta (S + S_D) (C row's C column) — are linear combinations of at most 14
+// reference matrices (hhat, s_diag, s_offdiag, mhat; assembly.hpp:76-208)
+// with per-element scalars (B_k, |T_k|, nu_kn, |E_kn|, edge kinds), so they
+// are rebuilt on the fly from shared memory instead of being read: 8 of the
+// 20 N x N blocks per element remain in HBM traffic.
+// The reference tables are stored transposed and padded (row j of T^t is 16
+// bytes aligned), so one 128-bit shared load feeds two FP64 FMAs and every
+// lane of a warp reads the same address (broadcast).
+#include <cmath>
+#include <cstdlib>
+
+#include "ldg_internal.hpp"
+
+namespace ldgb {
+
+namespace {
+
+template <int P>
+struct Cfg {
+  static constexpr int N = (P + 1) * (P + 2) / 2;
+  static constexpr int NP = (N % 2) ? N + 1 : N;
+  static constexpr int TAB = 16 * N * NP;  // tH(2) + tSd(3) + tSo(9) + tM + tMinv
+};
+
+inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+#define LDG_DISPATCH_P(p, CALL) \
+  switch (p) {                  \
+    case 0: { CALL(0); break; } \
+    case 1: { CALL(1); break; } \
+    case 2: { CALL(2); break; } \
+    case 3: { CALL(3); break; } \
+    default: { CALL(4); break; } \
+  }
+
+// shared-memory image of the static tables: [tH 2 | tSd 3 | tSo 9 | tM | tMinv]
+template <int P>
+struct STab {
+  static constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP, NNP = N * NP;
+  const double* s;
+  __device__ const double* H(int m) const { return s + m * NNP; }
+  __device__ const double* Sd(int n) const { return s + (2 + n) * NNP; }
+  __device__ const double* So(int nm, int np) const { return s + (5 + nm * 3 + np) * NNP; }
+  __device__ const double* M() const { return s + 14 * NNP; }
+  __device__ const double* Minv() const { return s + 15 * NNP; }
+};
+
+// The five table blocks are contiguous in the device table buffer in this
+// order (ldg_tables.cpp), so staging is one vectorised copy.
+template <int P>
+__device__ __forceinline__ STab<P> stage_tables(double* sm, const DevTables& T) {
+  constexpr int n = Cfg<P>::TAB;
+  const double2* src = reinterpret_cast<const double2*>(T.base + T.tH);
+  double2* dst = reinterpret_cast<double2*>(sm);
+  for (int i = threadIdx.x; i < n / 2; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+  return STab<P>{sm};
+}
+
+// w = T x with x in registers (T^t in shared memory, rows of NP doubles)
+template <int N, int NP>
+__device__ __forceinline__ void tab_mv(const double* sT, const double* x, double* w) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double xj = x[j];
+    const double2* row = reinterpret_cast<const double2*>(sT + j * NP);
+#pragma unroll
+    for (int q = 0; q < N / 2; ++q) {
+      const double2 t = row[q];
+      w[2 * q] = fma(t.x, xj, w[2 * q]);
+      w[2 * q + 1] = fma(t.y, xj, w[2 * q + 1]);
+    }
+    if (N & 1) w[N - 1] = fma(sT[j * NP + N - 1], xj, w[N - 1]);
+  }
+}
+
+// w = T x[.][col] with x streamed from memory (L1-resident after first use):
+// for N > 6 the column loop stays rolled so at most N accumulators and one
+// table row are live (p = 3, 4 would spill with x and T fully unrolled).
+template <int N, int NP>
+__device__ __forceinline__ void tab_mv_g(const double* sT, const double* __restrict__ x, long Kp, int col,
+                                         double* w) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = 0.0;
+#pragma unroll(N <= 6 ? N : 1)
+  for (int j = 0; j < N; ++j) {
+    const double xj = x[j * Kp + col];
+    const double2* row = reinterpret_cast<const double2*>(sT + j * NP);
+#pragma unroll
+    for (int q = 0; q < N / 2; ++q) {
+      const double2 t = row[q];
+      w[2 * q] = fma(t.x, xj, w[2 * q]);
+      w[2 * q + 1] = fma(t.y, xj, w[2 * q + 1]);
+    }
+    if (N & 1) w[N - 1] = fma(sT[j * NP + N - 1], xj, w[N - 1]);
+  }
+}
+
+// out[i][k] = scale * (T u)_i for u in registers: rows of T (columns of the
+// stored transpose) one at a time, results stored directly.
+template <int N, int NP>
+__device__ __forceinline__ void tab_mv_store(const double* sT, const double* u, double scale,
+                                             double* __restrict__ out, long Kp, int k) {
+#pragma unroll(N <= 6 ? N : 1)
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(sT[j * NP + i], u[j], s);
+    out[i * Kp + k] = scale * s;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void load_vec(const double* __restrict__ x, long Kp, int col, double* xv) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) xv[j] = x[j * Kp + col];
+}
+
+// acc[i] += sum_j blk[(i*N+j)][k] * x[j][col]: a stored block streamed one
+// column at a time (N coalesced loads in flight, N live accumulators)
+template <int N, typename TB>
+__device__ __forceinline__ void block_mv_gather(const TB* __restrict__ blk, long Kp, int k,
+                                                const double* __restrict__ x, int col, double* acc) {
+  const long NKp = static_cast<long>(N) * Kp;
+  if constexpr (N <= 6) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double xj = x[j * Kp + col];
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(static_cast<double>(blk[i * NKp + j * Kp + k]), xj, acc[i]);
+    }
+  } else {
+    // U block columns per round: U*N streaming loads in flight per thread
+    // (one round per column left the warps latency-bound at ~60% of HBM;
+    // U = 5 for FP32 blocks measured slower: 126 registers, lower occupancy)
+    constexpr int U = (N % 3 == 0) ? 3 : 2;
+    const TB* bj = blk + k;
+#pragma unroll 1
+    for (int j = 0; j < N; j += U, bj += U * Kp) {
+      double xj[U];
+      TB v[U][N];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xj[u] = x[(j + u) * Kp + col];
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[u][i] = __ldcs(bj + u * Kp + i * NKp);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] = fma(static_cast<double>(v[u][i]), xj[u], acc[i]);
+    }
+  }
+}
+
+struct EdgeData {
+  int kind[3], nbr[3], nbrn[3];
+  double len[3], nux[3], nuy[3];
+};
+
+__device__ __forceinline__ EdgeData load_edges(const DevMesh& m, int k) {
+  EdgeData e;
+  const long Kp = m.Kp;
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    e.kind[n] = m.kind[n * Kp + k];
+    e.nbr[n] = m.nbr[n * Kp + k];
+    e.nbrn[n] = m.nbrn[n * Kp + k];
+    e.len[n] = m.geom[(kLen0 + n) * Kp + k];
+    e.nux[n] = m.geom[(kNux0 + n) * Kp + k];
+    e.nuy[n] = m.geom[(kNuy0 + n) * Kp + k];
+  }
+  return e;
+}
+
+// u^m += sum_s B^m[s] x_col(s), B^m = -H^m + Q^m + Q_N^m rebuilt from tables
+// (assembly.hpp:92-109, 174-208): diagonal -H^m_k + sum_n c^m_n s_diag_n with
+// c = nu^m |E|/2 (interior), nu^m |E| (Neumann); off-diagonal nu^m|E|/2 s_off.
+template <int P>
+__device__ __forceinline__ void apply_B(const STab<P>& tb, const DevMesh& m, const EdgeData& e, int k, double b11,
+                                        double b12, double b21, double b22, const double* __restrict__ x,
+                                        double* u1, double* u2) {
+  constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP;
+  const long Kp = m.Kp;
+  double w[N];
+  tab_mv_g<N, NP>(tb.H(0), x, Kp, k, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    u1[i] = fma(-b22, w[i], u1[i]);
+    u2[i] = fma(b12, w[i], u2[i]);
+  }
+  tab_mv_g<N, NP>(tb.H(1), x, Kp, k, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    u1[i] = fma(b21, w[i], u1[i]);
+    u2[i] = fma(-b11, w[i], u2[i]);
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const double c = e.kind[n] == kInterior ? 0.5 * e.len[n] : (e.kind[n] == kNeumann ? e.len[n] : 0.0);
+    if (c == 0.0) continue;
+    tab_mv_g<N, NP>(tb.Sd(n), x, Kp, k, w);
+    const double c1 = c * e.nux[n], c2 = c * e.nuy[n];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fma(c1, w[i], u1[i]);
+      u2[i] = fma(c2, w[i], u2[i]);
+    }
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    if (e.nbr[n] < 0) continue;
+    tab_mv_g<N, NP>(tb.So(n, e.nbrn[n]), x, Kp, e.nbr[n], w);
+    const double c1 = 0.5 * e.len[n] * e.nux[n], c2 = 0.5 * e.len[n] * e.nuy[n];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fma(c1, w[i], u1[i]);
+      u2[i] = fma(c2, w[i], u2[i]);
+    }
+  }
+}
+
+// acc += beta (S + S_D) x  (assembly.hpp:142-168: + s_diag on interior and
+// Dirichlet edges, - s_offdiag to the neighbour; the edge length cancels)
+template <int P>
+__device__ __forceinline__ void apply_S(const STab<P>& tb, const DevMesh& m, const EdgeData& e, int k,
+                                        const double* __restrict__ x, double beta, double* acc) {
+  constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP;
+  const long Kp = m.Kp;
+  double w[N];
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    if (e.kind[n] != kInterior && e.kind[n] != kDirichlet) continue;
+    tab_mv_g<N, NP>(tb.Sd(n), x, Kp, k, w);
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fma(beta, w[i], acc[i]);
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    if (e.nbr[n] < 0) continue;
+    tab_mv_g<N, NP>(tb.So(n, e.nbrn[n]), x, Kp, e.nbr[n], w);
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fma(-beta, w[i], acc[i]);
+  }
+}
+
+// stage 1: tout^m = M_k^-1 (sigma vz^m + tau sum_s B^m[s] x_col(s))
+template <int P>
+__global__ void __launch_bounds__(128) k_stage1(DevMesh m, DevTables T, const double* __restrict__ vz, double sigma,
+                                                const double* __restrict__ x, double tau, double* __restrict__ tout) {
+  constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP;
+  extern __shared__ __align__(16) double sm[];
+  const STab<P> tb = stage_tables<P>(sm, T);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m.K) return;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  double u1[N], u2[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) u1[i] = u2[i] = 0.0;
+  if (x) {
+    const EdgeData e = load_edges(m, k);
+    apply_B<P>(tb, m, e, k, g[kB11 * Kp + k], g[kB12 * Kp + k], g[kB21 * Kp + k], g[kB22 * Kp + k], x, u1, u2);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] *= tau;
+      u2[i] *= tau;
+    }
+  }
+  if (vz) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fma(sigma, vz[i * Kp + k], u1[i]);
+      u2[i] = fma(sigma, vz[(N + i) * Kp + k], u2[i]);
+    }
+  }
+  const double inv2a = 1.0 / (2.0 * g[kArea * Kp + k]);
+  tab_mv_store<N, NP>(tb.Minv(), u1, inv2a, tout, Kp, k);
+  tab_mv_store<N, NP>(tb.Minv(), u2, inv2a, tout + N * Kp, Kp, k);
+}
+
+// stage 2: y = alpha M_k x_k + beta (S + S_D) x - gamma sum_m sum_s E^m[s] tz^m_col + delta w
+// TE = double for the Krylov operator, float for the multigrid smoother's
+// copy of E (FP32 storage, FP64 arithmetic: the preconditioner only).
+template <int P, typename TE>
+__global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const TE* __restrict__ E,
+                                                const double* __restrict__ x, double alpha, double beta,
+                                                const double* __restrict__ tz, double gamma,
+                                                const double* __restrict__ w, double delta, double* __restrict__ y) {
+  constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
+  extern __shared__ __align__(16) double sm[];
+  const STab<P> tb = stage_tables<P>(sm, T);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m.K) return;
+  const long Kp = m.Kp;
+  double acc[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] = 0.0;
+  const EdgeData e = load_edges(m, k);
+  if (tz) {
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const TE* Ec = E + static_cast<long>(c) * 4 * NN * Kp;
+      const double* tc = tz + static_cast<long>(c) * N * Kp;
+      block_mv_gather<N>(Ec, Kp, k, tc, k, acc);
+#pragma unroll 1
+      for (int s = 1; s < 4; ++s) {
+        const int col = e.nbr[s - 1];
+        if (col < 0) continue;
+        block_mv_gather<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, tc, col, acc);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] *= -gamma;
+  }
+  if (x) {
+    if (alpha != 0.0) {
+      double v[N];
+      tab_mv_g<N, NP>(tb.M(), x, Kp, k, v);
+      const double sa = alpha * 2.0 * m.geom[kArea * Kp + k];
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(sa, v[i], acc[i]);
+    }
+    if (beta != 0.0) apply_S<P>(tb, m, e, k, x, beta, acc);
+  }
+  if (w) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fma(delta, w[i * Kp + k], acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i * Kp + k] = acc[i];
+}
+
+// full (W + dt A) Y, Y = [Z1; Z2; C] (system.hpp:161-167):
+//   out_Zm = dt (M z^m_k + B^m c)
+//   out_C  = wm M c_k + dt (sum_m E^m z^m + eta (S + S_D) c)
+template <int P>
+__global__ void __launch_bounds__(128) k_full(DevMesh m, DevTables T, const double* __restrict__ E,
+                                              const double* __restrict__ Yin, double wm, double dt, double eta,
+                                              double* __restrict__ out) {
+  constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
+  extern __shared__ __align__(16) double sm[];
+  const STab<P> tb = stage_tables<P>(sm, T);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m.K) return;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  const double two_a = 2.0 * g[kArea * Kp + k];
+  const double* C = Yin + 2L * N * Kp;
+  const EdgeData e = load_edges(m, k);
+  double w[N];
+  {
+    double u1[N], u2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) u1[i] = u2[i] = 0.0;
+    apply_B<P>(tb, m, e, k, g[kB11 * Kp + k], g[kB12 * Kp + k], g[kB21 * Kp + k], g[kB22 * Kp + k], C, u1, u2);
+    tab_mv_g<N, NP>(tb.M(), Yin, Kp, k, w);
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i * Kp + k] = dt * fma(two_a, w[i], u1[i]);
+    tab_mv_g<N, NP>(tb.M(), Yin + static_cast<long>(N) * Kp, Kp, k, w);
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[(N + i) * Kp + k] = dt * fma(two_a, w[i], u2[i]);
+  }
+  double acc[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] = 0.0;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    const double* Ec = E + static_cast<long>(c) * 4 * NN * Kp;
+    const double* Zc = Yin + static_cast<long>(c) * N * Kp;
+    block_mv_gather<N>(Ec, Kp, k, Zc, k, acc);
+#pragma unroll 1
+    for (int s = 1; s < 4; ++s) {
+      const int col = e.nbr[s - 1];
+      if (col < 0) continue;
+      block_mv_gather<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, Zc, col, acc);
+    }
+  }
+  apply_S<P>(tb, m, e, k, C, eta, acc);
+  tab_mv_g<N, NP>(tb.M(), C, Kp, k, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[(2 * N + i) * Kp + k] = fma(wm * two_a, w[i], dt * acc[i]);
+}
+
+// Block-Jacobi preconditioner of the Schur operator, one N x N block per
+// element: P_k = w M_k + dt (eta S_kk - sum_m sum_{j in {k} U nbr(k)}
+// E^m_kj M_j^-1 B^m_jk), inverted in shared memory (Gauss-Jordan, partial
+// pivoting).  A group of N^2 threads owns one element; the static blocks
+// B^m_jk are rebuilt from the reference tables (row j, the slot facing k).
+template <int P, typename TE, typename TO>
+__global__ void __launch_bounds__(256) k_bjac_setup(DevMesh m, DevTables T, const TE* __restrict__ E, double wm,
+                                                    double dt, double eta, TO* __restrict__ Pinv) {
+  constexpr int N = Cfg<P>::N, NN = N * N;
+  constexpr int EPC = (256 / NN) > 0 ? (256 / NN) : 1;
+  __shared__ double s_minv[NN];
+  __shared__ double s_P[EPC][NN], s_A[EPC][NN], s_T[EPC][NN], s_I[EPC][NN];
+  __shared__ int s_piv[EPC];
+  const double* tb = T.base;
+  for (int i = threadIdx.x; i < NN; i += blockDim.x) s_minv[i] = tb[T.minv + i];
+  const int grp = threadIdx.x / NN, lane = threadIdx.x % NN;
+  const int k = blockIdx.x * EPC + grp;
+  const bool active = grp < EPC && k < m.K;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  const int i = lane / N, j = lane % N;
+  __syncthreads();
+  if (active) {
+    double s = 0.0;
+    for (int n = 0; n < 3; ++n) {
+      const int kd = m.kind[n * Kp + k];
+      if (kd == kInterior || kd == kDirichlet) s += tb[T.sdiag + lane * 3 + n];
+    }
+    s_P[grp][lane] = wm * 2.0 * g[kArea * Kp + k] * tb[T.mhat + lane] + dt * eta * s;
+  }
+  for (int c = 0; c < 2; ++c)
+    for (int s = 0; s < 4; ++s) {
+      int je = -1;
+      if (active) je = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
+      if (active && je >= 0) {
+        double b;
+        if (s == 0) {  // diagonal block of k: -H^m_k + sum_n c^m_n s_diag_n
+          const double h1 = tb[T.hhat + 2 * lane], h2 = tb[T.hhat + 2 * lane + 1];
+          b = c == 0 ? -(g[kB22 * Kp + k] * h1 - g[kB21 * Kp + k] * h2)
+                     : -(g[kB11 * Kp + k] * h2 - g[kB12 * Kp + k] * h1);
+          for (int n = 0; n < 3; ++n) {
+            const int kd = m.kind[n * Kp + k];
+            const double f = kd == kInterior ? 0.5 : (kd == kNeumann ? 1.0 : 0.0);
+            const double nu = g[((c == 0 ? kNux0 : kNuy0) + n) * Kp + k];
+            b += f * nu * g[(kLen0 + n) * Kp + k] * tb[T.sdiag + lane * 3 + n];
+          }
+        } else {  // off-diagonal block of je toward k: nu^m|E|/2 s_off(n', n)
+          const int np = m.nbrn[(s - 1) * Kp + k];
+          const double nu = g[((c == 0 ? kNux0 : kNuy0) + np) * Kp + je];
+          b = 0.5 * nu * g[(kLen0 + np) * Kp + je] * tb[T.soff + (lane * 3 + np) * 3 + (s - 1)];
+        }
+        s_A[grp][lane] = b;
+      }
+      __syncthreads();
+      if (active && je >= 0) {
+        const double inv2a = 1.0 / (2.0 * g[kArea * Kp + je]);
+        double acc = 0.0;
+        for (int q = 0; q < N; ++q) acc += s_minv[i * N + q] * s_A[grp][q * N + j];
+        s_T[grp][lane] = inv2a * acc;
+        s_A[grp][lane] = static_cast<double>(E[(static_cast<long>(c * 4 + s) * NN + lane) * Kp + k]);  // E^m_{k,je}
+      }
+      __syncthreads();
+      if (active && je >= 0) {
+        double acc = 0.0;
+        for (int q = 0; q < N; ++q) acc += s_A[grp][i * N + q] * s_T[grp][q * N + j];
+        s_P[grp][lane] -= dt * acc;
+      }
+      __syncthreads();
+    }
+  if (active) s_I[grp][lane] = (i == j) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int col = 0; col < N; ++col) {
+    if (active && lane == 0) {
+      int piv = col;
+      double best = fabs(s_P[grp][col * N + col]);
+      for (int r = col + 1; r < N; ++r)
+        if (fabs(s_P[grp][r * N + col]) > best) {
+          best = fabs(s_P[grp][r * N + col]);
+          piv = r;
+        }
+      s_piv[grp] = piv;
+    }
+    __syncthreads();
+    if (active) {
+      const int piv = s_piv[grp];
+      if (piv != col && i == col) {
+        const double a = s_P[grp][col * N + j], b = s_P[grp][piv * N + j];
+        s_P[grp][col * N + j] = b;
+        s_P[grp][piv * N + j] = a;
+        const double c2 = s_I[grp][col * N + j], d2 = s_I[grp][piv * N + j];
+        s_I[grp][col * N + j] = d2;
+        s_I[grp][piv * N + j] = c2;
+      }
+    }
+    __syncthreads();
+    double f = 0.0, prow = 0.0, irow = 0.0, pivv = 1.0;
+    if (active) {
+      pivv = s_P[grp][col * N + col];
+      f = s_P[grp][i * N + col];
+      prow = s_P[grp][col * N + j];
+      irow = s_I[grp][col * N + j];
+    }
+    __syncthreads();
+    if (active) {
+      const double pr = prow / pivv, ir = irow / pivv;
+      if (i == col) {
+        s_P[grp][lane] = pr;
+        s_I[grp][lane] = ir;
+      } else {
+        s_P[grp][lane] -= f * pr;
+        s_I[grp][lane] -= f * ir;
+      }
+    }
+    __syncthreads();
+  }
+  if (active) Pinv[static_cast<long>(lane) * Kp + k] = static_cast<TO>(s_I[grp][lane]);
+}
+
+// y = beta y + omega P^-1 x  (beta = 0: plain block-Jacobi application)
+template <int P, typename TP>
+__global__ void __launch_bounds__(128) k_bjac_axpy(int K, long Kp, const TP* __restrict__ Pinv,
+                                                   const double* __restrict__ x, double omega, double beta,
+                                                   double* __restrict__ y) {
+  constexpr int N = Cfg<P>::N;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double acc[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] = 0.0;
+  block_mv_gather<N>(Pinv, Kp, k, x, k, acc);
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i * Kp + k] = (beta == 0.0 ? 0.0 : beta * y[i * Kp + k]) + omega * acc[i];
+}
+
+template <int P>
+size_t tab_smem() {
+  return sizeof(double) * Cfg<P>::TAB;
+}
+
+template <typename Kern>
+void set_smem(Kern kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    LDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+__global__ void k_to_f32(long n, const double* __restrict__ src, float* __restrict__ dst) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<float>(src[i]);
+}
+
+// Kernel shape per launch: thread-per-element (this file) keeps each vector
+// value in a register for all N rows and issues the fewest load
+// instructions, which wins once a level fills the GPU; the row-parallel
+// kernels (ldg_rows.cu) win on small levels, where a thread's serial load
+// chain is the latency (measured at p = 4: fine level 246 vs 354 us, coarse
+// levels 35 vs 90 us).  LDG_ROWS_BELOW overrides the element-count switch.
+bool use_rows(const Handle& h) {
+  static const long below = [] {
+    const char* s = std::getenv("LDG_ROWS_BELOW");
+    return s ? std::atol(s) : 65536L;
+  }();
+  return h.K < below;
+}
+
+}  // namespace
+
+void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout) {
+  if (use_rows(h)) return rows_stage1(h, vz, sigma, x, tau, tout);
+  const unsigned grid = grid_of(h.K, 128);
+#define CALL(P)                                                                                       \
+  do {                                                                                                \
+    set_smem(k_stage1<P>, tab_smem<P>());                                                             \
+    k_stage1<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, vz, sigma, x, tau, tout);   \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+// precision of the stored E / block-Jacobi blocks a launch reads:
+// FP64 for the Krylov operator, FP32 for the multigrid smoother's copies.
+template <typename TE>
+void stage2_impl(Handle& h, const TE* E, const double* x, double alpha_m, double beta_s, const double* tz,
+                 double gamma_e, const double* w, double delta, double* y) {
+  if (use_rows(h)) return rows_stage2<TE>(h, E, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
+  const unsigned grid = grid_of(h.K, 128);
+#define CALL(P)                                                                                                \
+  do {                                                                                                         \
+    set_smem(k_stage2<P, TE>, tab_smem<P>());                                                                  \
+    k_stage2<P, TE><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, E, x, alpha_m, beta_s, tz,       \
+                                                            gamma_e, w, delta, y);                             \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
+                   const double* w, double delta, double* y) {
+  stage2_impl<double>(h, h.E.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
+}
+
+void launch_stage2_f32(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz,
+                       double gamma_e, const double* w, double delta, double* y) {
+  stage2_impl<float>(h, h.E32.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
+}
+
+void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double* out) {
+  const unsigned grid = grid_of(h.K, 128);
+#define CALL(P)                                                                                                 \
+  do {                                                                                                          \
+    set_smem(k_full<P>, tab_smem<P>());                                                                         \
+    k_full<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, Y, wm, dt, h.prob.eta, out);   \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+template <typename TE, typename TO>
+void bjac_setup_impl(Handle& h, const TE* E, double wm, double dt, TO* out) {
+#define CALL(P)                                                                                         \
+  do {                                                                                                  \
+    constexpr int NN = Cfg<P>::N * Cfg<P>::N;                                                           \
+    constexpr int EPC = (256 / NN) > 0 ? (256 / NN) : 1;                                                \
+    k_bjac_setup<P, TE, TO><<<grid_of(h.K, EPC), 256, 0, h.stream>>>(h.mesh(), h.dtab, E, wm, dt,      \
+                                                                     h.prob.eta, out);                  \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_bjac_setup(Handle& h, double wm, double dt) { bjac_setup_impl<double, double>(h, h.E.ptr, wm, dt, h.Pinv.ptr); }
+
+void launch_bjac_setup_f32(Handle& h, double wm, double dt) {
+  bjac_setup_impl<float, float>(h, h.E32.ptr, wm, dt, h.Pinv32.ptr);
+}
+
+void launch_bjac_apply(Handle& h, const double* x, double* y) { launch_bjac_axpy(h, x, 1.0, 0.0, y); }
+
+template <typename TP>
+void bjac_axpy_impl(Handle& h, const TP* Pinv, const double* x, double omega, double beta, double* y) {
+  if (use_rows(h)) return rows_bjac<TP>(h, Pinv, x, omega, beta, y);
+  const unsigned grid = grid_of(h.K, 128);
+#define CALL(P) k_bjac_axpy<P, TP><<<grid, 128, 0, h.stream>>>(h.K, h.Kp, Pinv, x, omega, beta, y)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y) {
+  bjac_axpy_impl<double>(h, h.Pinv.ptr, x, omega, beta, y);
+}
+
+void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y) {
+  bjac_axpy_impl<float>(h, h.Pinv32.ptr, x, omega, beta, y);
+}
+
+void launch_to_f32(Handle& h, long n, const double* src, float* dst) {
+  k_to_f32<<<1184, 256, 0, h.stream>>>(n, src, dst);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+}  // namespace ldgb

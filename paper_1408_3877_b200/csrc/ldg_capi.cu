@@ -78,7 +78,7 @@ void init_device_side(Handle& h, int p, const ldg_problem* prob) {
   const ldgb::TableLayout& L = h.tables.lay;
   h.dtab = ldgb::DevTables{h.tab.ptr, L.p, L.N, L.R, L.Qe, L.Qb, L.proj_phi, L.proj_w, L.proj_x, L.mhat,
                            L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe, L.pth, L.we, L.pb, L.sb, L.wb, L.total,
-                           L.mono};
+                           L.mono, L.NP, L.tH, L.tSd, L.tSo, L.tM, L.tMinv, L.tmH, L.tmSd, L.tmSo};
   ldgb::upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
 }
 
@@ -95,11 +95,9 @@ void alloc_step_buffers(Handle& h) {
 // Solver-side buffers and the static blocks, allocated on first use so an
 // assembly-only run (BASELINE config 3) does not pay for them.
 void ensure_solver(Handle& h) {
-  if (h.Bst.ptr) return;
+  if (h.Yold.ptr) return;
   const long n = h.vec_len();
   const long NN = static_cast<long>(h.N) * h.N;
-  h.Bst.alloc(8 * NN * h.Kp, &h.bytes);
-  h.Sst.alloc(4 * NN * h.Kp, &h.bytes);
   h.Yold.alloc(3 * n, &h.bytes);
   for (DBuf<double>* b : {&h.kr_r, &h.kr_rh, &h.kr_p, &h.kr_v, &h.kr_s, &h.kr_t, &h.kr_ph, &h.kr_sh, &h.kr_b})
     b->alloc(n, &h.bytes);
@@ -108,8 +106,6 @@ void ensure_solver(Handle& h) {
   h.full_r.alloc(3 * n, &h.bytes);
   h.full_y.alloc(3 * n, &h.bytes);
   h.red.alloc(ldgb::reduction_scratch(), &h.bytes);
-  ldgb::launch_static(h, ldgb::kStB, h.Bst.ptr);  // K4 (system.hpp:83-87)
-  ldgb::launch_static(h, ldgb::kStS, h.Sst.ptr);
   LDG_CUDA(cudaStreamSynchronize(h.stream));
 }
 
@@ -338,11 +334,14 @@ int ldg_export_operator(ldg_handle* H, int which, int64_t* nnz, int64_t* rows, i
         for (int s = 0; s < (off ? 4 : 1); ++s) push_block(h, nb, base, k, s, ru, cu, scale, coo);
     };
     if (which == LDG_OP_A) {
-      tmp.alloc(4 * NN * h.Kp, nullptr);
+      // the static blocks exactly as the matrix-free kernels rebuild them (K4)
+      tmp.alloc(8 * NN * h.Kp, nullptr);
       ldgb::launch_static(h, ldgb::kStM, tmp.ptr);
       const auto M = blocks_to_host(h, tmp.ptr, 1);
-      const auto B = blocks_to_host(h, h.Bst.ptr, 2);
-      const auto S = blocks_to_host(h, h.Sst.ptr, 1);
+      ldgb::launch_static(h, ldgb::kStB, tmp.ptr);
+      const auto B = blocks_to_host(h, tmp.ptr, 2);
+      ldgb::launch_static(h, ldgb::kStS, tmp.ptr);
+      const auto S = blocks_to_host(h, tmp.ptr, 1);
       const auto E = blocks_to_host(h, h.E.ptr, 2);
       emit(M, 0, false, 0, 0, 1.0);
       emit(B, 0, true, 0, 2, 1.0);

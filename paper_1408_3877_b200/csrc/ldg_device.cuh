@@ -38,6 +38,9 @@ struct DevTables {
   const double* base;
   int p, N, R, Qe, Qb;
   long proj_phi, proj_w, proj_x, mhat, minv, ghat, hhat, sdiag, soff, pe, pth, we, pb, sb, wb, total, mono;
+  int NP;
+  long tH, tSd, tSo, tM, tMinv;
+  long tmH, tmSd, tmSo;
 };
 
 struct DevMesh {

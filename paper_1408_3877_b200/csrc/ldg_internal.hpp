@@ -121,6 +121,8 @@ struct Handle {
   DBuf<int> mg_children;                         // [4][Kp] children in the next finer level
   DBuf<double> mg_P;                             // [N*N][Kp] prolongation block of each element
   DBuf<double> mg_x, mg_b, mg_r;                 // V-cycle work vectors (N * Kp)
+  DBuf<float> E32, Pinv32;                       // FP32 copies read by the smoother
+  bool mg_f32 = true;                            // smoother on FP32 copies (precond 2) or FP64 (3)
   bool mg_ready = false;
   struct VGraph {                                // a captured V-cycle (CUDA graph)
     cudaGraphExec_t exec = nullptr;
@@ -167,6 +169,19 @@ void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor
 void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa);
 
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
+void launch_stage2_f32(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz,
+                       double gamma_e, const double* w, double delta, double* y);
+void launch_bjac_setup_f32(Handle& h, double wm, double dt);
+void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);
+void launch_to_f32(Handle& h, long n, const double* src, float* dst);
+
+// row-parallel operator kernels (ldg_rows.cu), used by the launchers above
+void rows_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);
+template <typename TE>
+void rows_stage2(Handle& h, const TE* E, const double* x, double alpha, double beta, const double* tz, double gamma,
+                 const double* w, double delta, double* y);
+template <typename TP>
+void rows_bjac(Handle& h, const TP* Pinv, const double* x, double omega, double beta, double* y);
 void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
                      const double* z, double* out);
 

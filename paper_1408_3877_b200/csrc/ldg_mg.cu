@@ -28,7 +28,8 @@ struct Cfg {
 };
 
 constexpr double kOmega = 0.7;
-constexpr int kNu = 2;
+constexpr int kPre = 2;   // pre-smoothing sweeps (the first one from x = 0 is residual-free)
+constexpr int kPost = 2;  // post-smoothing sweeps (V(2,1) measured slower overall: +20-40% iterations)
 constexpr int kCoarseSweeps = 2;
 
 inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
@@ -56,7 +57,8 @@ __global__ void k_subsample(int dim_c, const double* __restrict__ cf, double* __
 // parent of every fine element and the 4 children of every coarse element.
 // Coarse lower (cx,cy) holds fine lower (0,0),(1,0),(0,1) and upper (0,0) of
 // its 2x2 block; coarse upper holds fine lower (1,1) and upper (1,0),(0,1),(1,1).
-__global__ void k_fk_parent(int dim_f, long Kp_c, int* __restrict__ parent, int* __restrict__ children) {
+__global__ void k_fk_parent(int dim_f, long Kp_c, int* __restrict__ parent, int* __restrict__ slots,
+                            int* __restrict__ children) {
   const long Kf = 2L * dim_f * dim_f;
   const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   if (k >= Kf) return;
@@ -76,6 +78,7 @@ __global__ void k_fk_parent(int dim_f, long Kp_c, int* __restrict__ parent, int*
   }
   const int kc = clower ? cx * dim_c + cy : dim_c * dim_c + cx * dim_c + cy;
   parent[k] = kc;
+  slots[k] = slot;
   children[slot * Kp_c + kc] = static_cast<int>(k);
 }
 
@@ -98,9 +101,11 @@ __device__ __forceinline__ void eval_basis(const double* __restrict__ mono, doub
 
 // P_k[i][j] = sum_a minv[i][a] int_ref phi_a(xh) phi_j(xi(xh)), xi = parent
 // reference coordinates of the fine point; exact with the order-2p rule.
+// Pm is stored on the coarse level, [slot][N*N][Kp_c], so restriction and
+// prolongation (both driven from the coarse side) read it coalesced.
 template <int P>
 __global__ void __launch_bounds__(128) k_prolong_blocks(DevMesh f, DevMesh c, DevTables T, const int* __restrict__ parent,
-                                                        double* __restrict__ Pm) {
+                                                        const int* __restrict__ slots, double* __restrict__ Pm) {
   constexpr int N = Cfg<P>::N, NN = N * N;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= f.K) return;
@@ -127,102 +132,109 @@ __global__ void __launch_bounds__(128) k_prolong_blocks(DevMesh f, DevMesh c, De
       for (int j = 0; j < N; ++j) acc[i * N + j] += w * pf[i] * pc[j];
   }
   const double* minv = base + T.minv;
+  double* out = Pm + static_cast<long>(slots[k]) * NN * Kc;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) {
       double s = 0.0;
       for (int a = 0; a < N; ++a) s += minv[i * N + a] * acc[a * N + j];
-      Pm[static_cast<long>(i * N + j) * Kf + k] = s;
+      out[static_cast<long>(i * N + j) * Kc + kc] = s;
     }
 }
 
-// bc[kc] = sum over the 4 children of P_child^T rf[child]
+// bc[j][kc] = sum over the 4 children s, rows i of P_s[i][j] rf[i][child_s]:
+// one thread per (j, kc) output value (coarse levels hold too few elements
+// for a thread per element to hide the load latency)
 template <int P>
-__global__ void __launch_bounds__(128) k_restrict(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
+__global__ void __launch_bounds__(256) k_restrict(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
                                                   const double* __restrict__ Pm, const double* __restrict__ rf,
                                                   double* __restrict__ bc) {
-  constexpr int N = Cfg<P>::N;
-  const int kc = blockIdx.x * blockDim.x + threadIdx.x;
-  if (kc >= Kc) return;
-  double acc[N];
+  constexpr int N = Cfg<P>::N, NN = N * N;
+  const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (t >= static_cast<long>(N) * Kc) return;
+  const int kc = static_cast<int>(t % Kc), j = static_cast<int>(t / Kc);
+  double acc = 0.0;
 #pragma unroll
-  for (int j = 0; j < N; ++j) acc[j] = 0.0;
-#pragma unroll 1
   for (int s = 0; s < 4; ++s) {
     const int k = children[s * Kpc + kc];
-    double r[N];
+    const double* Ps = Pm + (static_cast<long>(s) * NN + j) * Kpc + kc;
 #pragma unroll
-    for (int i = 0; i < N; ++i) r[i] = rf[i * Kpf + k];
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-      for (int j = 0; j < N; ++j) acc[j] += Pm[static_cast<long>(i * N + j) * Kpf + k] * r[i];
+    for (int i = 0; i < N; ++i) acc = fma(__ldcs(Ps + static_cast<long>(i) * N * Kpc), rf[i * Kpf + k], acc);
   }
-#pragma unroll
-  for (int j = 0; j < N; ++j) bc[j * Kpc + kc] = acc[j];
+  bc[j * Kpc + kc] = acc;
 }
 
-// xf[k] += P_k xc[parent[k]]
+// xf[i][child_s] += sum_j P_s[i][j] xc[j][kc]: one thread per (i, s, kc)
 template <int P>
-__global__ void __launch_bounds__(128) k_prolong_add(int Kf, long Kpf, long Kpc, const int* __restrict__ parent,
+__global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
                                                      const double* __restrict__ Pm, const double* __restrict__ xc,
                                                      double* __restrict__ xf) {
-  constexpr int N = Cfg<P>::N;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= Kf) return;
-  const int kc = parent[k];
-  double c[N];
+  constexpr int N = Cfg<P>::N, NN = N * N;
+  const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (t >= 4L * N * Kc) return;
+  const int kc = static_cast<int>(t % Kc);
+  const int rest = static_cast<int>(t / Kc);
+  const int s = rest % 4, i = rest / 4;
+  const int k = children[s * Kpc + kc];
+  const double* Ps = Pm + (static_cast<long>(s) * NN + static_cast<long>(i) * N) * Kpc + kc;
+  double acc = 0.0;
 #pragma unroll
-  for (int j = 0; j < N; ++j) c[j] = xc[j * Kpc + kc];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j) s += Pm[static_cast<long>(i * N + j) * Kpf + k] * c[j];
-    xf[i * Kpf + k] += s;
-  }
+  for (int j = 0; j < N; ++j) acc = fma(__ldcs(Ps + static_cast<long>(j) * Kpc), xc[j * Kpc + kc], acc);
+  xf[i * Kpf + k] += acc;
 }
 
 Handle* level_at(Handle& h, int l) { return l == 0 ? &h : h.coarse[l - 1].get(); }
 
-// r = b - A x  (A the level's Schur operator)
-void residual(Handle& L, double wm, double dt, const double* b, const double* x, double* r) {
+// r = b - A x  (A the level's Schur operator; E read from the FP32 copy when
+// the smoother runs in mixed precision — vectors and arithmetic stay FP64)
+void residual(Handle& L, bool f32, double wm, double dt, const double* b, const double* x, double* r) {
   launch_stage1(L, nullptr, 0.0, x, 1.0, L.tz.ptr);
-  launch_stage2(L, x, -wm, -dt * L.prob.eta, L.tz.ptr, -dt, b, 1.0, r);
+  if (f32)
+    launch_stage2_f32(L, x, -wm, -dt * L.prob.eta, L.tz.ptr, -dt, b, 1.0, r);
+  else
+    launch_stage2(L, x, -wm, -dt * L.prob.eta, L.tz.ptr, -dt, b, 1.0, r);
 }
 
-void smooth_once(Handle& L, double wm, double dt, const double* b, double* x) {
-  residual(L, wm, dt, b, x, L.mg_r.ptr);
-  launch_bjac_axpy(L, L.mg_r.ptr, kOmega, 1.0, x);
+void bjac_axpy(Handle& L, bool f32, const double* x, double omega, double beta, double* y) {
+  if (f32)
+    launch_bjac_axpy_f32(L, x, omega, beta, y);
+  else
+    launch_bjac_axpy(L, x, omega, beta, y);
+}
+
+void smooth_once(Handle& L, bool f32, double wm, double dt, const double* b, double* x) {
+  residual(L, f32, wm, dt, b, x, L.mg_r.ptr);
+  bjac_axpy(L, f32, L.mg_r.ptr, kOmega, 1.0, x);
 }
 
 void vcycle(Handle& h, int l, double wm, double dt, const double* b, double* x) {
   Handle& L = *level_at(h, l);
+  const bool f32 = h.mg_f32;
   const int last = static_cast<int>(h.coarse.size());
-  launch_bjac_axpy(L, b, kOmega, 0.0, x);  // first sweep from x = 0
+  bjac_axpy(L, f32, b, kOmega, 0.0, x);  // first sweep from x = 0
   if (l == last) {
-    for (int s = 1; s < kCoarseSweeps; ++s) smooth_once(L, wm, dt, b, x);
+    for (int s = 1; s < kCoarseSweeps; ++s) smooth_once(L, f32, wm, dt, b, x);
     return;
   }
-  for (int s = 1; s < kNu; ++s) smooth_once(L, wm, dt, b, x);
-  residual(L, wm, dt, b, x, L.mg_r.ptr);
+  for (int s = 1; s < kPre; ++s) smooth_once(L, f32, wm, dt, b, x);
+  residual(L, f32, wm, dt, b, x, L.mg_r.ptr);
   Handle& C = *level_at(h, l + 1);
   const int P = h.p;
 #define CALL(PP)                                                                                               \
-  k_restrict<PP><<<grid_of(C.K, 128), 128, 0, h.stream>>>(C.K, C.Kp, L.Kp, C.mg_children.ptr, L.mg_P.ptr,      \
-                                                          L.mg_r.ptr, C.mg_b.ptr)
+  k_restrict<PP><<<grid_of(static_cast<long>(h.N) * C.K, 256), 256, 0, h.stream>>>(                          \
+      C.K, C.Kp, L.Kp, C.mg_children.ptr, C.mg_P.ptr, L.mg_r.ptr, C.mg_b.ptr)
   LDG_DISPATCH_P(P, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
   ++L.launches;
   vcycle(h, l + 1, wm, dt, C.mg_b.ptr, C.mg_x.ptr);
 #define CALL(PP)                                                                                                \
-  k_prolong_add<PP><<<grid_of(L.K, 128), 128, 0, h.stream>>>(L.K, L.Kp, C.Kp, L.mg_parent.ptr, L.mg_P.ptr,      \
-                                                             C.mg_x.ptr, x)
+  k_prolong_add<PP><<<grid_of(4L * h.N * C.K, 256), 256, 0, h.stream>>>(C.K, C.Kp, L.Kp, C.mg_children.ptr,    \
+                                                                        C.mg_P.ptr, C.mg_x.ptr, x)
   LDG_DISPATCH_P(P, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
   ++L.launches;
-  for (int s = 0; s < kNu; ++s) smooth_once(L, wm, dt, b, x);
+  for (int s = 0; s < kPost; ++s) smooth_once(L, f32, wm, dt, b, x);
 }
 
 }  // namespace
@@ -259,23 +271,22 @@ bool mg_build(Handle& h) {
     const long n = c->vec_len();
     c->D.alloc(n, &c->bytes);
     c->E.alloc(8 * NN * c->Kp, &c->bytes);
-    c->Bst.alloc(8 * NN * c->Kp, &c->bytes);
-    c->Sst.alloc(4 * NN * c->Kp, &c->bytes);
     c->Pinv.alloc(NN * c->Kp, &c->bytes);
     c->tz.alloc(2 * n, &c->bytes);
     c->mg_x.alloc(n, &c->bytes);
     c->mg_b.alloc(n, &c->bytes);
     c->mg_r.alloc(n, &c->bytes);
     c->mg_children.alloc(4 * c->Kp, &c->bytes);
-    launch_static(*c, kStB, c->Bst.ptr);
-    launch_static(*c, kStS, c->Sst.ptr);
     fine->mg_parent.alloc(fine->Kp, &fine->bytes);
-    fine->mg_P.alloc(NN * fine->Kp, &fine->bytes);
-    k_fk_parent<<<grid_of(fine->K, 256), 256, 0, h.stream>>>(d, c->Kp, fine->mg_parent.ptr, c->mg_children.ptr);
+    DBuf<int> slots;
+    slots.alloc(fine->Kp, nullptr);
+    c->mg_P.alloc(4 * NN * c->Kp, &c->bytes);
+    k_fk_parent<<<grid_of(fine->K, 256), 256, 0, h.stream>>>(d, c->Kp, fine->mg_parent.ptr, slots.ptr,
+                                                             c->mg_children.ptr);
     LDG_CUDA(cudaGetLastError());
 #define CALL(PP)                                                                                              \
   k_prolong_blocks<PP><<<grid_of(fine->K, 128), 128, 0, h.stream>>>(fine->mesh(), c->mesh(), h.dtab,         \
-                                                                   fine->mg_parent.ptr, fine->mg_P.ptr)
+                                                                   fine->mg_parent.ptr, slots.ptr, c->mg_P.ptr)
     LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
     LDG_CUDA(cudaGetLastError());
@@ -288,12 +299,34 @@ bool mg_build(Handle& h) {
   return h.mg_ready;
 }
 
+// Per step: rediscretise every coarse level at time t (projection of d,
+// E^m assembly) and build the block-Jacobi inverses; in mixed precision the
+// smoother reads FP32 copies of E and of the inverses.  Level 0's FP64
+// block-Jacobi inverse is built by the caller.
 void mg_setup_step(Handle& h, double t, double wm, double dt) {
+  const long NN = static_cast<long>(h.N) * h.N;
+  if (h.mg_f32) {
+    if (!h.E32.ptr) {
+      h.E32.alloc(8 * NN * h.Kp, &h.bytes);
+      h.Pinv32.alloc(NN * h.Kp, &h.bytes);
+    }
+    launch_to_f32(h, 8 * NN * h.Kp, h.E.ptr, h.E32.ptr);
+    launch_to_f32(h, NN * h.Kp, h.Pinv.ptr, h.Pinv32.ptr);
+  }
   for (auto& cp : h.coarse) {
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.K);
     launch_assemble(c, kModeE, c.E.ptr);
-    launch_bjac_setup(c, wm, dt);
+    if (h.mg_f32) {
+      if (!c.E32.ptr) {
+        c.E32.alloc(8 * NN * c.Kp, &c.bytes);
+        c.Pinv32.alloc(NN * c.Kp, &c.bytes);
+      }
+      launch_to_f32(c, 8 * NN * c.Kp, c.E.ptr, c.E32.ptr);
+      launch_bjac_setup_f32(c, wm, dt);
+    } else {
+      launch_bjac_setup(c, wm, dt);
+    }
   }
 }
 

@@ -343,6 +343,15 @@ HostTables build_tables(int p) {
   L.sb = take(L.Qb);
   L.wb = take(L.Qb);
   L.mono = take(15L * N);
+  L.NP = (N % 2) ? N + 1 : N;
+  L.tH = take(2L * N * L.NP);
+  L.tSd = take(3L * N * L.NP);
+  L.tSo = take(9L * N * L.NP);
+  L.tM = take(1L * N * L.NP);
+  L.tMinv = take(1L * N * L.NP);
+  L.tmH = take(2L * N * L.NP);
+  L.tmSd = take(3L * N * L.NP);
+  L.tmSo = take(9L * N * L.NP);
   L.total = off;
   ht.data.assign(off, 0.0);
   double* d = ht.data.data();
@@ -385,6 +394,33 @@ HostTables build_tables(int p) {
   // phi_i = sum_m mono[i][m] x1^a_m x2^b_m (monomial order of kMonoA/kMonoB)
   for (int i = 0; i < N; ++i)
     for (int m = 0; m < 15; ++m) d[L.mono + i * 15 + m] = scale_of(i) * kBasis[i].c[m];
+  const int NP = L.NP;
+  auto put_t = [&](long at, auto value) {  // at[j*NP + i] = value(i, j)
+    for (int j = 0; j < N; ++j)
+      for (int i = 0; i < N; ++i) d[at + j * NP + i] = value(i, j);
+  };
+  for (int m = 0; m < 2; ++m) put_t(L.tH + m * N * NP, [&](int i, int j) { return rt.h[(i * N + j) * 2 + m]; });
+  for (int n = 0; n < 3; ++n) put_t(L.tSd + n * N * NP, [&](int i, int j) { return rt.sd[(i * N + j) * 3 + n]; });
+  for (int nm = 0; nm < 3; ++nm)
+    for (int np = 0; np < 3; ++np)
+      put_t(L.tSo + (nm * 3 + np) * N * NP, [&](int i, int j) { return rt.so[((i * N + j) * 3 + nm) * 3 + np]; });
+  put_t(L.tM, [&](int i, int j) { return rt.m[i * N + j]; });
+  put_t(L.tMinv, [&](int i, int j) { return minv[i * N + j]; });
+  // (m_hat^-1 T)[i][j] = sum_a minv[i][a] T[a][j]
+  auto minv_times = [&](long at, auto value) {
+    put_t(at, [&](int i, int j) {
+      double s = 0.0;
+      for (int a = 0; a < N; ++a) s += minv[i * N + a] * value(a, j);
+      return s;
+    });
+  };
+  for (int m = 0; m < 2; ++m) minv_times(L.tmH + m * N * NP, [&](int a, int j) { return rt.h[(a * N + j) * 2 + m]; });
+  for (int n = 0; n < 3; ++n)
+    minv_times(L.tmSd + n * N * NP, [&](int a, int j) { return rt.sd[(a * N + j) * 3 + n]; });
+  for (int nm = 0; nm < 3; ++nm)
+    for (int np = 0; np < 3; ++np)
+      minv_times(L.tmSo + (nm * 3 + np) * N * NP,
+                 [&](int a, int j) { return rt.so[((a * N + j) * 3 + nm) * 3 + np]; });
   return ht;
 }
 

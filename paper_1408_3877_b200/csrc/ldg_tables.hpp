@@ -54,6 +54,16 @@ struct TableLayout {
   long pe, pth, we;                  // [n][q][i], [nm][np][q][j], [q]   (rank-Q edge form)
   long pb, sb, wb;                   // [n][q][i], [q], [q]              (RHS edge rule)
   long mono;                         // [i][15] scaled monomial coefficients of phi_i
+  // matrix-free static operators: reference matrices transposed and padded
+  // to NP = N rounded up to even, T^t[j][i] at j*NP + i (16-byte rows)
+  int NP = 0;
+  long tH;                           // [2][N][NP]  h_hat(.,.,m)^t
+  long tSd;                          // [3][N][NP]  s_diag(.,.,n)^t
+  long tSo;                          // [9][N][NP]  s_offdiag(.,.,nm,np)^t
+  long tM;                           // [N][NP]     m_hat^t
+  long tMinv;                        // [N][NP]     m_hat^-1 ^t
+  long tmH, tmSd, tmSo;              // the same with m_hat^-1 applied: (m_hat^-1 T)^t,
+                                     // for stage 1 (t = M^-1 B x in one pass)
   long total = 0;
 };
 

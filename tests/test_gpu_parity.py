@@ -150,16 +150,17 @@ def test_multigrid_matches_block_jacobi(p, ld):
     """The geometric-multigrid preconditioner changes the iteration count, not the
     answer: same state as block-Jacobi within the solve tolerance, far fewer iterations."""
     res = {}
-    for pc in (1, 2):
+    for pc in (1, 2, 3):  # block-Jacobi, multigrid (FP32 smoother copies), multigrid (FP64)
         s = ld.LdgSystem.square(32, p, ld.BASELINE_SPEC, jitter=0.0)
         s.initial_state()
         st = s.euler_steps(0.05, 2, ld.SolverOptions(rtol=1e-13, precond=pc))
         assert st["residual"] <= 1e-10
         res[pc] = (s.get_state()[0], st["iterations"])
     y1, it1 = res[1]
-    y2, it2 = res[2]
-    assert np.linalg.norm(y2 - y1) / np.linalg.norm(y1) <= 1e-9
-    assert it2 * 3 < it1, (it1, it2)
+    for pc in (2, 3):
+        y2, it2 = res[pc]
+        assert np.linalg.norm(y2 - y1) / np.linalg.norm(y1) <= 1e-9
+        assert it2 * 3 < it1, (pc, it1, it2)
 
 
 def test_multigrid_jittered_mesh(ld):
