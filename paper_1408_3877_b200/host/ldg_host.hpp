@@ -1,0 +1,194 @@
+// C++ host mirror of the reference's entry points over the C ABI of
+// include/ldg_b200.h — the same class/function shapes as
+// proj/include/ldg/system.hpp and fields.hpp, the same exception types
+// (std::invalid_argument, ldg::b200::MeshError, std::runtime_error), so a
+// caller written against ldg::LdgSystem (e.g. cmd_simulate, ldg_main.cpp:
+// 174-222) switches by changing the namespace and the coefficient type.
+//
+// Header-only; link with -lldg_b200.  Not thread-safe per object (one
+// LdgSystem per GPU/thread), like the handle it wraps.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "ldg_b200.h"
+
+namespace ldg::b200 {
+
+/// mesh.hpp:25-27
+struct MeshError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+/// A compiled-in coefficient function (the device cannot call std::function,
+/// fields.hpp:19); see include/ldg_b200_coeffs.h for the ids.
+inline ldg_coeff coeff(int id, double p0 = 0.0, double p1 = 0.0, double p2 = 0.0, double p3 = 0.0) {
+  ldg_coeff c;
+  c.id = id;
+  c.p[0] = p0;
+  c.p[1] = p1;
+  c.p[2] = p2;
+  c.p[3] = p3;
+  return c;
+}
+
+enum class Bc { kDirichlet, kNeumann };  // system.hpp:23
+
+/// system.hpp:26-37
+struct ProblemSpec {
+  ldg_coeff d = coeff(LDG_FN_CONST, 1.0);
+  ldg_coeff f = coeff(LDG_FN_ZERO);
+  ldg_coeff c_d = coeff(LDG_FN_ZERO);
+  ldg_coeff g_n = coeff(LDG_FN_ZERO);
+  ldg_coeff c0 = coeff(LDG_FN_ZERO);
+  double eta = 1.0;
+  std::map<int, Bc> boundary;
+  double t_end = 1.0;
+  int num_steps = 1;
+};
+
+/// system.hpp:40-43
+struct SystemState {
+  std::vector<double> y;  // 3*K*N, ordered (Z1, Z2, C), k-major per block
+  double t = 0.0;
+};
+
+namespace detail {
+
+inline void check(int rc, const ldg_handle* h) {
+  if (rc == LDG_OK) return;
+  const std::string msg = ldg_last_error(h);
+  switch (rc) {
+    case LDG_EINVAL: throw std::invalid_argument(msg);
+    case LDG_EMESH: throw MeshError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+inline ldg_problem to_c(const ProblemSpec& s) {
+  ldg_problem p{};
+  p.d = s.d;
+  p.f = s.f;
+  p.c_d = s.c_d;
+  p.g_n = s.g_n;
+  p.c0 = s.c0;
+  p.eta = s.eta;
+  if (s.boundary.size() > LDG_MAX_BC) throw std::invalid_argument("too many boundary conditions");
+  p.n_bc = 0;
+  for (const auto& [id, kind] : s.boundary) {
+    p.bc_id[p.n_bc] = id;
+    p.bc_kind[p.n_bc] = kind == Bc::kDirichlet ? LDG_BC_DIRICHLET : LDG_BC_NEUMANN;
+    ++p.n_bc;
+  }
+  return p;
+}
+
+struct HandleDeleter {
+  void operator()(ldg_handle* h) const { ldg_destroy(h); }
+};
+
+}  // namespace detail
+
+/// Device-resident LdgSystem (system.hpp:65-213).
+class LdgSystem {
+ public:
+  /// domain_square(1/dim) (mesh.hpp:225-254) generated on the device.
+  static LdgSystem square(int dim, int p, const ProblemSpec& spec, double jitter = 0.0, uint64_t seed = 0) {
+    const ldg_problem pr = detail::to_c(spec);
+    ldg_handle* h = nullptr;
+    detail::check(ldg_create_square(dim, jitter, seed, p, &pr, &h), nullptr);
+    return LdgSystem(h, spec);
+  }
+
+  /// generate_grid_data(coords, v0t) + the LdgSystem ctor; id_e0t (K x 3,
+  /// optional) carries boundary IDs per (triangle, local edge).
+  LdgSystem(const std::vector<std::array<double, 2>>& coords, const std::vector<std::array<int, 3>>& v0t, int p,
+            const ProblemSpec& spec, const std::vector<std::array<int, 3>>* id_e0t = nullptr)
+      : spec_(spec) {
+    const ldg_problem pr = detail::to_c(spec);
+    ldg_handle* h = nullptr;
+    detail::check(ldg_create(coords.empty() ? nullptr : coords[0].data(), static_cast<int>(coords.size()),
+                             v0t.empty() ? nullptr : v0t[0].data(), static_cast<int>(v0t.size()),
+                             id_e0t ? (*id_e0t)[0].data() : nullptr, p, &pr, &h),
+                  nullptr);
+    h_.reset(h);
+    load_info();
+  }
+
+  int n_local() const { return info_.n_local; }
+  int num_t() const { return info_.num_t; }
+  int block_dim() const { return info_.num_t * info_.n_local; }  // system.hpp:95
+  const ProblemSpec& spec() const { return spec_; }
+  ldg_handle* handle() const { return h_.get(); }
+
+  /// project(mesh, func, t, q_ord, rt) (fields.hpp:53-82): K x N, k-major.
+  std::vector<double> project(const ldg_coeff& fn, double t, int q_ord) const {
+    std::vector<double> out(static_cast<size_t>(block_dim()));
+    detail::check(ldg_project(h_.get(), &fn, t, q_ord, out.data()), h_.get());
+    return out;
+  }
+
+  /// The device half of build_blocks(t) (system.hpp:110-152); operators
+  /// stay in HBM (exports: ldg_export_operator).
+  void build_blocks(double t) const { detail::check(ldg_assemble(h_.get(), t), h_.get()); }
+
+  /// system.hpp:99-107
+  SystemState initial_state() const {
+    detail::check(ldg_initial_state(h_.get()), h_.get());
+    return state();
+  }
+
+  /// system.hpp:155-174: one implicit Euler step of length dt.
+  SystemState euler_step(const SystemState& s, double dt, const ldg_solver_opts* opts = nullptr) const {
+    if (s.y.size() != 3u * static_cast<size_t>(block_dim()))
+      throw std::invalid_argument("state length does not match 3*K*N");
+    SystemState next;
+    next.y.resize(s.y.size());
+    detail::check(ldg_euler_steps_host(h_.get(), s.y.data(), s.t, dt, 1, next.y.data(), opts, nullptr, nullptr),
+                  h_.get());
+    next.t = s.t + dt;
+    return next;
+  }
+
+  /// nsteps steps on the device-resident state (no host copies in between).
+  ldg_step_stats advance(double dt, int nsteps, const ldg_solver_opts* opts = nullptr) const {
+    ldg_step_stats st{};
+    detail::check(ldg_euler_steps(h_.get(), dt, nsteps, opts, &st), h_.get());
+    return st;
+  }
+
+  SystemState state() const {
+    SystemState s;
+    s.y.resize(3u * static_cast<size_t>(block_dim()));
+    detail::check(ldg_get_state(h_.get(), s.y.data(), &s.t), h_.get());
+    return s;
+  }
+
+  /// system.hpp:177-185 -> (c, z1, z2), each K x N k-major.
+  std::tuple<std::vector<double>, std::vector<double>, std::vector<double>> solve_stationary(
+      double t = 0.0, const ldg_solver_opts* opts = nullptr) const {
+    detail::check(ldg_solve_stationary(h_.get(), t, opts, nullptr), h_.get());
+    const SystemState s = state();
+    const size_t kn = static_cast<size_t>(block_dim());
+    return {std::vector<double>(s.y.begin() + 2 * kn, s.y.end()), std::vector<double>(s.y.begin(), s.y.begin() + kn),
+            std::vector<double>(s.y.begin() + kn, s.y.begin() + 2 * kn)};
+  }
+
+ private:
+  LdgSystem(ldg_handle* h, ProblemSpec spec) : h_(h), spec_(std::move(spec)) { load_info(); }
+  void load_info() { detail::check(ldg_get_info(h_.get(), &info_), h_.get()); }
+
+  std::unique_ptr<ldg_handle, detail::HandleDeleter> h_;
+  ProblemSpec spec_;
+  ldg_info_t info_{};
+};
+
+}  // namespace ldg::b200

@@ -83,3 +83,16 @@ def test_no_cpu_fallback():
 
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         ld.LdgSystem.square(4, 1, ld.BASELINE_SPEC)
+
+
+SIM = os.path.join(ROOT, "tools", "ldg_simulate")
+
+
+@pytest.mark.skipif(_have_gpu(), reason="checks the no-GPU failure mode")
+def test_cpp_host_mirror_fails_loudly_without_gpu():
+    """tools/ldg_simulate (C++ mirror of cmd_simulate over ldg_host.hpp) maps the
+    C ABI status to the reference's exit behaviour (ldg_main.cpp:302-305)."""
+    assert os.path.exists(SIM), "build() must produce tools/ldg_simulate"
+    r = subprocess.run([SIM, "4", "1", "2"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 1
+    assert "no CPU fallback" in r.stderr

@@ -226,3 +226,16 @@ def test_reference_exceptions(ld):
         s.euler_steps(0.0, 1)
     with pytest.raises(ValueError):
         ld.LdgSystem.square(2, 5, ld.BASELINE_SPEC)
+
+
+def test_cpp_host_mirror_simulate(ld):
+    """The C++ host mirror (paper_1408_3877_b200/host/ldg_host.hpp) driving the
+    reference's simulate loop, host-buffer and device-resident variants."""
+    import os
+    import subprocess
+
+    sim = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "ldg_simulate")
+    for extra in ([], ["--device-resident"]):
+        r = subprocess.run([sim, "16", "1", "10", "1.0"] + extra, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        assert "simulate: 10 steps" in r.stdout
