@@ -73,6 +73,13 @@ def bytes_asm(dim, p):
     return 8 * 2 * N * N * (K + 2 * e_int(dim)) + 8 * K * N
 
 
+def bytes_full_compulsory(dim, p):
+    """Compulsory bytes of the full (W + dt A) Y apply as implemented: E blocks
+    streamed, static blocks rebuilt from tables, Y (3 vectors, read twice), out."""
+    K, N = 2 * dim * dim, n_of(p)
+    return 8 * (2 * N * N * (K + 2 * e_int(dim)) + 9 * K * N + 20 * K) + 72 * K
+
+
 def bytes_spmv(dim, p):
     """8 N^2 nb + 4 nb + 4 (3K+1) + 2*8*3KN, nb = 7K + 10 E_int."""
     K, N = 2 * dim * dim, n_of(p)
@@ -192,8 +199,6 @@ def run_reference_arm(args):
 
 
 def run_ours(args):
-    import numpy as np
-
     world, rank, local = dist_env()
     import torch
 
@@ -203,26 +208,41 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     import paper_1408_3877_b200 as ld
+    from paper_1408_3877_b200 import strips
 
     ld.set_device(local)
-    dim, ps, dt, jitter, boundary, desc = WORKLOADS[args.workload]
+    dim1, ps, dt, jitter, boundary, desc = WORKLOADS[args.workload]
     if args.p is not None:
         ps = [int(x) for x in args.p.split(",")]
+    # N > 1: strips of one FK(dim) mesh, dim chosen for ~dim1^2 elements per GPU (weak scaling)
+    dim = strips.weak_dim(dim1, world)
     spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
                           boundary=boundary)
     opts = ld.SolverOptions()
     systems = []
     for p in ps:
-        s = ld.LdgSystem.square(dim, p, spec, jitter=jitter, seed=0)
+        if world > 1:
+            ids = [ld.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(ids, src=0)
+            s = ld.LdgSystem.square_dist(dim, p, spec, rank, world, ids[0], jitter=jitter, seed=0)
+        else:
+            s = ld.LdgSystem.square(dim, p, spec, jitter=jitter, seed=0)
         s.initial_state()
         systems.append(s)
-    dof_step = sum(3 * s.num_t * s.n for s in systems)
+    dof_step = sum(3 * s.num_t * s.n for s in systems)  # whole-job DOF per step (global K)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > 126 MB L2
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
     # warm-up (W full steps)
     for _ in range(args.warmup):
@@ -247,14 +267,10 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     launches = sum(s.info()["launches"] for s in systems) - launches0
-    total_ms = sum(r["ms"] for r in per_p.values())
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * dof_step * args.steps / (total_ms * 1e-3)
+    total_ms = max_over_ranks(sum(r["ms"] for r in per_p.values()))
+    value = dof_step * args.steps / (total_ms * 1e-3)
 
-    # e2e through the host-buffer C ABI call
+    # e2e through the host-buffer C ABI call (each rank copies its owned rows)
     e2e_ms = 0.0
     h2d = 0
     for p, s in zip(ps, systems):
@@ -267,29 +283,36 @@ def run_ours(args):
             t += dt
             pin_in.copy_(pin_out)
         h2d += y.nbytes
-    e2e_value = world * dof_step * args.steps / (e2e_ms * 1e-3)
+    e2e_ms = max_over_ranks(e2e_ms)
+    e2e_value = dof_step * args.steps / (e2e_ms * 1e-3)
 
     # per-kernel timing for the roofline (CUDA events on the library's stream, L2 flushed)
     peak, peak_src = hbm_peak()
     kern = {}
     for p, s in zip(ps, systems):
         kern[p] = s.time_kernels(s.t, dt, reps=5, flush=True)
+    kloc = dim if world == 1 else None  # per-rank byte counts below assume one GPU
     # dominant kernel = the Schur operator apply (stage1 + stage2) at the p with the largest share
     shares = {p: kern[p]["ms_schur"] * per_p[p]["applies"] / max(total_ms, 1e-9) for p in ps}
     pd = max(shares, key=shares.get)
-    bs = bytes_schur(dim, pd)
-    achieved = bs / (kern[pd]["ms_schur"] * 1e-3) / 1e9
-    roof = {"kernel": f"schur_apply (k_stage1+k_stage2), p={pd}", "bound": "hbm", "achieved": achieved,
-            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-            "peak_source": peak_src, "share_of_step": shares[pd],
-            "bytes_per_launch": bs,
-            "others": {str(p): {"assemble_GBps": bytes_asm(dim, p) / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
-                                "spmv_GBps": bytes_spmv(dim, p) / (kern[p]["ms_spmv"] * 1e-3) / 1e9,
-                                "schur_GBps": bytes_schur(dim, p) / (kern[p]["ms_schur"] * 1e-3) / 1e9,
-                                "ms": kern[p]} for p in ps}}
+    roof = None
+    if kloc is not None:
+        bs = bytes_schur(dim, pd)
+        achieved = bs / (kern[pd]["ms_schur"] * 1e-3) / 1e9
+        roof = {"kernel": f"schur_apply (stage1+stage2), p={pd}", "bound": "hbm", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": peak_src, "share_of_step_bicgstab_applies": shares[pd],
+                "bytes_per_launch": bs,
+                "others": {str(p): {"assemble_GBps": bytes_asm(dim, p) / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
+                                    "spmv_compulsory_GBps": bytes_full_compulsory(dim, p)
+                                    / (kern[p]["ms_spmv"] * 1e-3) / 1e9,
+                                    "spmv_effective_GBps_survey_formula": bytes_spmv(dim, p)
+                                    / (kern[p]["ms_spmv"] * 1e-3) / 1e9,
+                                    "schur_GBps": bytes_schur(dim, p) / (kern[p]["ms_schur"] * 1e-3) / 1e9,
+                                    "ms": kern[p]} for p in ps}}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             v, sec, sample = reference_sample(args.workload, 1, 0)
             cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample}
@@ -303,9 +326,10 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: analytic c, d(t), f(t) of BASELINE.json; FK mesh generated on device",
             "config": {"workload": desc, "dim": dim, "K": 2 * dim * dim, "p": ps, "dt": dt,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": f"strips{world} (NCCL halos + allreduce)" if world > 1 else "single",
                        "l2": "flushed (256 MB write) before every timed step; p>=2 working sets exceed L2",
-                       "solver": "BiCGStab on the exact Schur complement, block-Jacobi, reference contract 1e-10",
+                       "solver": "BiCGStab on the exact Schur complement, geometric multigrid V(2,2) "
+                                 "(FP32 smoother copies), reference residual contract 1e-10",
                        "per_p": {str(p): {"ms_per_step": per_p[p]["ms"] / args.steps,
                                           "ms_assemble": per_p[p]["ms_asm"] / args.steps,
                                           "ms_solve": per_p[p]["ms_solve"] / args.steps,

@@ -117,6 +117,25 @@ int ldg_create(const double* coords, int num_v, const int* v0t, int num_t, const
 int ldg_create_square(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob,
                       ldg_handle** out);
 
+/* ---- multi-GPU strips --------------------------------------
+ * FK(dim) is split into `size` strips of dim/size element columns; each rank
+ * owns its strip plus one ghost column per side.  One process per GPU:
+ * rank 0 calls ldg_nccl_unique_id, broadcasts the 128 bytes (e.g. with
+ * torch.distributed), every rank calls ldg_create_square_dist.  Halos of the
+ * operator applies go through ncclSend/Recv, Krylov dot products through
+ * ncclAllReduce.  All other calls are collective over the ranks and keep
+ * their single-GPU meaning; host arrays use global numbering and each rank
+ * fills / reads its owned rows. */
+int ldg_nccl_unique_id(char* out /* 128 bytes */);
+int ldg_create_square_dist(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob, int rank, int size,
+                           const char* nccl_id, ldg_handle** out);
+
+/* The same decomposition with all `nranks` ranks in this process on the
+ * current GPU ("virtual ranks", halos by device copies): validates the
+ * distributed algorithm on one device; results match ldg_create_square. */
+int ldg_create_square_group(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob, int nranks,
+                            ldg_handle** out);
+
 void ldg_destroy(ldg_handle* h);
 
 /* Message of the last failure on this thread (or of handle h if given). */

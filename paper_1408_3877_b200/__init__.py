@@ -92,6 +92,11 @@ _SIGNATURES = {
     "ldg_create": (C.c_int, [_dp, C.c_int, _ip, C.c_int, _ip, C.c_int, C.POINTER(_Problem), C.POINTER(_H)]),
     "ldg_create_square": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(_Problem),
                                     C.POINTER(_H)]),
+    "ldg_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "ldg_create_square_dist": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(_Problem), C.c_int,
+                                         C.c_int, C.c_char_p, C.POINTER(_H)]),
+    "ldg_create_square_group": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(_Problem), C.c_int,
+                                          C.POINTER(_H)]),
     "ldg_destroy": (None, [_H]),
     "ldg_last_error": (C.c_char_p, [_H]),
     "ldg_get_info": (C.c_int, [_H, C.POINTER(_Info)]),
@@ -142,6 +147,14 @@ def reference_tensors(n_local: int) -> dict:
                                                                              "ro")])
     _raise(rc, lib.ldg_last_error(None).decode())
     return arrs
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, every rank passes it to square_dist)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    _raise(lib.ldg_nccl_unique_id(buf), lib.ldg_last_error(None).decode())
+    return buf.raw
 
 
 def set_device(device: int) -> None:
@@ -248,6 +261,30 @@ class LdgSystem:
         h = _H()
         pr = spec.to_c()
         rc = lib.ldg_create_square(int(dim), float(jitter), int(seed), int(p), C.byref(pr), C.byref(h))
+        _raise(rc, lib.ldg_last_error(None).decode())
+        return cls(h, spec, p)
+
+    @classmethod
+    def square_group(cls, dim: int, p: int, spec: ProblemSpec, nranks: int, jitter: float = 0.0,
+                     seed: int = 0) -> "LdgSystem":
+        """The strip decomposition with all `nranks` ranks on this GPU (virtual ranks)."""
+        lib = load_library()
+        h = _H()
+        pr = spec.to_c()
+        rc = lib.ldg_create_square_group(int(dim), float(jitter), int(seed), int(p), C.byref(pr), int(nranks),
+                                         C.byref(h))
+        _raise(rc, lib.ldg_last_error(None).decode())
+        return cls(h, spec, p)
+
+    @classmethod
+    def square_dist(cls, dim: int, p: int, spec: ProblemSpec, rank: int, size: int, nccl_id: bytes | None,
+                    jitter: float = 0.0, seed: int = 0) -> "LdgSystem":
+        """Rank `rank` of `size` (one process per GPU, NCCL halos and allreduce)."""
+        lib = load_library()
+        h = _H()
+        pr = spec.to_c()
+        rc = lib.ldg_create_square_dist(int(dim), float(jitter), int(seed), int(p), C.byref(pr), int(rank),
+                                        int(size), nccl_id, C.byref(h))
         _raise(rc, lib.ldg_last_error(None).decode())
         return cls(h, spec, p)
 

@@ -1,22 +1,24 @@
 // The C ABI of include/ldg_b200.h: handle lifecycle, status/exception
-// mapping, exports for parity, and kernel timing.
+// mapping, exports for parity, and kernel timing.  A handle is a Team: one
+// rank (single GPU), one rank of a multi-GPU strip decomposition (NCCL), or
+// several virtual ranks sharing this process's GPU (validation of the
+// decomposition on one device).  Host-facing arrays always use the global
+// reference numbering; each rank contributes its owned rows.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "ldg_internal.hpp"
 
-namespace ldgb {
-size_t reduction_scratch();
-}
-
 struct ldg_handle {
-  ldgb::Handle h;
+  ldgb::Team team;
 };
 
 namespace {
@@ -25,24 +27,24 @@ thread_local std::string g_last_error;
 
 template <typename F>
 int guarded(ldg_handle* H, F&& fn) {
+  auto fail = [H](const std::string& m) {
+    g_last_error = m;
+    if (H) H->team.err = m;
+  };
   try {
     fn();
     return LDG_OK;
   } catch (const ldgb::Error& e) {
-    g_last_error = e.what();
-    if (H) H->h.err = e.what();
+    fail(e.what());
     return e.status;
   } catch (const std::invalid_argument& e) {
-    g_last_error = e.what();
-    if (H) H->h.err = e.what();
+    fail(e.what());
     return LDG_EINVAL;
   } catch (const std::bad_alloc&) {
-    g_last_error = "host allocation failed";
-    if (H) H->h.err = g_last_error;
+    fail("host allocation failed");
     return LDG_ECUDA;
   } catch (const std::exception& e) {
-    g_last_error = e.what();
-    if (H) H->h.err = e.what();
+    fail(e.what());
     return LDG_ENOCONV;
   }
 }
@@ -50,6 +52,7 @@ int guarded(ldg_handle* H, F&& fn) {
 using ldgb::DBuf;
 using ldgb::Error;
 using ldgb::Handle;
+using ldgb::Team;
 
 void validate_problem(const ldg_problem* prob, int p) {
   if (!prob) throw Error(LDG_EINVAL, "problem description is NULL");
@@ -61,16 +64,27 @@ void validate_problem(const ldg_problem* prob, int p) {
     if (f->id < 0 || f->id >= LDG_FN_COUNT) throw Error(LDG_EINVAL, "unknown coefficient function id");
 }
 
-void init_device_side(Handle& h, int p, const ldg_problem* prob) {
+void init_team(Team& T) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(LDG_ECUDA, "no CUDA device available: the LDG path has no CPU fallback");
+  LDG_CUDA(cudaStreamCreateWithFlags(&T.stream, cudaStreamNonBlocking));
+  LDG_CUDA(cudaMallocHost(&T.red_host, 256 * sizeof(double)));
+  T.red_all.alloc(256, nullptr);
+}
+
+// One rank's device-side state: tables, rule, stream (the team's).
+std::unique_ptr<Handle> make_rank(Team& T, int p, const ldg_problem* prob, int rank, int size) {
+  auto hp = std::make_unique<Handle>();
+  Handle& h = *hp;
   h.p = p;
   h.N = ldgb::dofs_of(p);
   h.prob = *prob;
-  LDG_CUDA(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+  h.rank = rank;
+  h.size = size;
+  h.stream = T.stream;
+  h.owns_stream = false;
   for (auto& e : h.ev) LDG_CUDA(cudaEventCreate(&e));
-  LDG_CUDA(cudaMallocHost(&h.red_host, 64 * sizeof(double)));
   h.tables = ldgb::build_tables(p);
   h.tab.alloc(h.tables.data.size(), &h.bytes);
   LDG_CUDA(cudaMemcpy(h.tab.ptr, h.tables.data.data(), sizeof(double) * h.tables.data.size(),
@@ -80,6 +94,7 @@ void init_device_side(Handle& h, int p, const ldg_problem* prob) {
                            L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe, L.pth, L.we, L.pb, L.sb, L.wb, L.total,
                            L.mono, L.NP, L.tH, L.tSd, L.tSo, L.tM, L.tMinv, L.tmH, L.tmSd, L.tmSo};
   ldgb::upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
+  return hp;
 }
 
 void alloc_step_buffers(Handle& h) {
@@ -92,25 +107,28 @@ void alloc_step_buffers(Handle& h) {
   h.Y.alloc(3 * n, &h.bytes);
 }
 
-// Solver-side buffers and the static blocks, allocated on first use so an
-// assembly-only run (BASELINE config 3) does not pay for them.
-void ensure_solver(Handle& h) {
-  if (h.Yold.ptr) return;
-  const long n = h.vec_len();
-  const long NN = static_cast<long>(h.N) * h.N;
-  h.Yold.alloc(3 * n, &h.bytes);
-  for (DBuf<double>* b : {&h.kr_r, &h.kr_rh, &h.kr_p, &h.kr_v, &h.kr_s, &h.kr_t, &h.kr_ph, &h.kr_sh, &h.kr_b})
-    b->alloc(n, &h.bytes);
-  h.tz.alloc(2 * n, &h.bytes);
-  h.Pinv.alloc(NN * h.Kp, &h.bytes);
-  h.full_r.alloc(3 * n, &h.bytes);
-  h.full_y.alloc(3 * n, &h.bytes);
-  h.red.alloc(ldgb::reduction_scratch(), &h.bytes);
-  LDG_CUDA(cudaStreamSynchronize(h.stream));
+// Solver-side buffers, allocated on first use so an assembly-only run
+// (BASELINE config 3) does not pay for them.
+void ensure_solver(Team& T) {
+  for (auto& rp : T.ranks) {
+    Handle& h = *rp;
+    if (h.Yold.ptr) continue;
+    const long n = h.vec_len();
+    const long NN = static_cast<long>(h.N) * h.N;
+    h.Yold.alloc(3 * n, &h.bytes);
+    for (DBuf<double>* b : {&h.kr_r, &h.kr_rh, &h.kr_p, &h.kr_v, &h.kr_s, &h.kr_t, &h.kr_ph, &h.kr_sh, &h.kr_b})
+      b->alloc(n, &h.bytes);
+    h.tz.alloc(2 * n, &h.bytes);
+    h.Pinv.alloc(NN * h.Kp, &h.bytes);
+    h.full_r.alloc(3 * n, &h.bytes);
+    h.full_y.alloc(3 * n, &h.bytes);
+    h.red.alloc(ldgb::reduction_scratch(), &h.bytes);
+  }
+  LDG_CUDA(cudaStreamSynchronize(T.stream));
 }
 
-void require_assembled(const Handle& h) {
-  if (!h.assembled) throw Error(LDG_EINVAL, "no assembled operators: call ldg_assemble first");
+void require_assembled(const Team& T) {
+  if (!T.h0().assembled) throw Error(LDG_EINVAL, "no assembled operators: call ldg_assemble first");
 }
 
 // Device SoA blocks [ncomp][4][N*N][Kp] -> host copy
@@ -128,8 +146,8 @@ struct Coo {
 };
 
 // Appends block slot s of element k: rows (ru*K + gid(k))*N + i, cols (cu*K + gid(col))*N + j.
-void push_block(const Handle& h, const std::vector<int>& nbr_host, const double* blk, int k, int s, int ru,
-                int cu, double scale, Coo& out) {
+void push_block(const Handle& h, const std::vector<int>& nbr_host, const double* blk, int k, int s, int ru, int cu,
+                double scale, Coo& out) {
   const int N = h.N;
   int col = k;
   if (s > 0) {
@@ -146,12 +164,100 @@ void push_block(const Handle& h, const std::vector<int>& nbr_host, const double*
     }
 }
 
+// owned rows of nvec N-plane device vectors -> global k-major host array
+void gather_to_host(Team& T, const std::function<const double*(Handle&)>& src, int nvec, double* out) {
+  for (auto& rp : T.ranks) {
+    Handle& h = *rp;
+    const size_t cnt = static_cast<size_t>(nvec) * h.K * h.N;
+    DBuf<double> km;
+    km.alloc(cnt, nullptr);
+    ldgb::launch_soa_to_kmajor(h, src(h), nvec, km.ptr);
+    std::vector<double> loc(cnt);
+    LDG_CUDA(cudaMemcpyAsync(loc.data(), km.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+    const long KN = static_cast<long>(h.Kglobal) * h.N;
+    for (int v = 0; v < nvec; ++v)
+      for (int k = 0; k < h.K; ++k)
+        std::memcpy(out + v * KN + static_cast<long>(h.gid[k]) * h.N,
+                    loc.data() + (static_cast<size_t>(v) * h.K + k) * h.N, sizeof(double) * h.N);
+  }
+}
+
+// global k-major host array -> owned rows of nvec N-plane device vectors
+void scatter_from_host(Team& T, const double* in, int nvec, const std::function<double*(Handle&)>& dst) {
+  for (auto& rp : T.ranks) {
+    Handle& h = *rp;
+    const size_t cnt = static_cast<size_t>(nvec) * h.K * h.N;
+    const long KN = static_cast<long>(h.Kglobal) * h.N;
+    std::vector<double> loc(cnt);
+    for (int v = 0; v < nvec; ++v)
+      for (int k = 0; k < h.K; ++k)
+        std::memcpy(loc.data() + (static_cast<size_t>(v) * h.K + k) * h.N,
+                    in + v * KN + static_cast<long>(h.gid[k]) * h.N, sizeof(double) * h.N);
+    DBuf<double> km;
+    km.alloc(cnt, nullptr);
+    LDG_CUDA(cudaMemcpyAsync(km.ptr, loc.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice, T.stream));
+    ldgb::launch_kmajor_to_soa(h, km.ptr, nvec, dst(h));
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+  }
+}
+
+int64_t team_launches(const Team& T) {
+  int64_t n = 0;
+  for (const auto& rp : T.ranks) {
+    n += rp->launches;
+    for (const auto& c : rp->coarse) n += c->launches;
+  }
+  return n;
+}
+
+// Creates a team of strips of FK(dim): ranks [first, first + nlocal) of size.
+int create_square_team(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob, int first, int nlocal,
+                       int size, const char* nccl_id, ldg_handle** out) {
+  if (!out) return LDG_EINVAL;
+  *out = nullptr;
+  auto H = std::make_unique<ldg_handle>();
+  const int rc = guarded(nullptr, [&] {
+    validate_problem(prob, p);
+    if (size < 1 || nlocal < 1 || first < 0 || first + nlocal > size) throw Error(LDG_EINVAL, "invalid rank layout");
+    if (dim < 1) throw Error(LDG_EINVAL, "maximum edge length must be positive");
+    if (size > 1 && dim % size != 0) throw Error(LDG_EINVAL, "dim must be a multiple of the rank count");
+    Team& T = H->team;
+    init_team(T);
+    T.size = size;
+    T.first = first;
+    if (nccl_id && size > nlocal) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      ncclComm_t comm;
+      const ncclResult_t r = ncclCommInitRank(&comm, size, id, first);
+      if (r != ncclSuccess) throw Error(LDG_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      T.nccl = comm;
+      T.owns_nccl = true;
+    } else if (size > nlocal) {
+      throw Error(LDG_EINVAL, "remote ranks need an NCCL unique id");
+    }
+    for (int r = 0; r < nlocal; ++r) {
+      const int g = first + r;
+      auto hp = make_rank(T, p, prob, g, size);
+      const int a = static_cast<int>(static_cast<long>(g) * dim / size);
+      const int b = static_cast<int>(static_cast<long>(g + 1) * dim / size);
+      ldgb::build_square_strip(*hp, dim, a, b, 1, dim, jitter, seed);
+      alloc_step_buffers(*hp);
+      T.ranks.push_back(std::move(hp));
+    }
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+  });
+  if (rc == LDG_OK) *out = H.release();
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* ldg_last_error(const ldg_handle* H) {
-  if (H && !H->h.err.empty()) return H->h.err.c_str();
+  if (H && !H->team.err.empty()) return H->team.err.c_str();
   return g_last_error.c_str();
 }
 
@@ -176,6 +282,16 @@ int ldg_set_device(int device) {
   return guarded(nullptr, [&] { LDG_CUDA(cudaSetDevice(device)); });
 }
 
+int ldg_nccl_unique_id(char* out) {
+  if (!out) return LDG_EINVAL;
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw Error(LDG_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
 ldg_solver_opts ldg_default_solver_opts(void) {
   ldg_solver_opts o;
   o.rtol = 0.0;
@@ -194,57 +310,68 @@ int ldg_create(const double* coords, int num_v, const int* v0t, int num_t, const
   auto H = std::make_unique<ldg_handle>();
   const int rc = guarded(nullptr, [&] {
     validate_problem(prob, p);
-    init_device_side(H->h, p, prob);
-    ldgb::build_general_mesh(H->h, coords, num_v, v0t, num_t, id_e0t);
-    alloc_step_buffers(H->h);
-    LDG_CUDA(cudaStreamSynchronize(H->h.stream));
+    Team& T = H->team;
+    init_team(T);
+    auto hp = make_rank(T, p, prob, 0, 1);
+    ldgb::build_general_mesh(*hp, coords, num_v, v0t, num_t, id_e0t);
+    alloc_step_buffers(*hp);
+    T.ranks.push_back(std::move(hp));
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
   if (rc == LDG_OK) *out = H.release();
   return rc;
 }
 
 int ldg_create_square(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob, ldg_handle** out) {
-  if (!out) return LDG_EINVAL;
-  *out = nullptr;
-  auto H = std::make_unique<ldg_handle>();
-  const int rc = guarded(nullptr, [&] {
-    validate_problem(prob, p);
-    init_device_side(H->h, p, prob);
-    ldgb::build_square_mesh(H->h, dim, jitter, seed);
-    alloc_step_buffers(H->h);
-    LDG_CUDA(cudaStreamSynchronize(H->h.stream));
-  });
-  if (rc == LDG_OK) *out = H.release();
-  return rc;
+  return create_square_team(dim, jitter, seed, p, prob, 0, 1, 1, nullptr, out);
+}
+
+int ldg_create_square_group(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob, int nranks,
+                            ldg_handle** out) {
+  return create_square_team(dim, jitter, seed, p, prob, 0, nranks, nranks, nullptr, out);
+}
+
+int ldg_create_square_dist(int dim, double jitter, uint64_t seed, int p, const ldg_problem* prob, int rank,
+                           int size, const char* nccl_id, ldg_handle** out) {
+  return create_square_team(dim, jitter, seed, p, prob, rank, 1, size, size > 1 ? nccl_id : nullptr, out);
 }
 
 void ldg_destroy(ldg_handle* H) {
   if (!H) return;
-  Handle& h = H->h;
-  if (h.stream) cudaStreamSynchronize(h.stream);
-  ldgb::mg_release(h);
-  if (h.red_host) cudaFreeHost(h.red_host);
-  for (auto& e : h.ev)
-    if (e) cudaEventDestroy(e);
-  cudaStream_t s = h.stream;
+  Team& T = H->team;
+  if (T.stream) cudaStreamSynchronize(T.stream);
+  for (auto& rp : T.ranks) {
+    ldgb::mg_release(*rp);
+    for (auto& e : rp->ev)
+      if (e) cudaEventDestroy(e);
+  }
+  if (T.nccl && T.owns_nccl) ncclCommDestroy(static_cast<ncclComm_t>(T.nccl));
+  if (T.red_host) cudaFreeHost(T.red_host);
+  cudaStream_t s = T.stream;
   delete H;  // DBuf destructors free device memory
   if (s) cudaStreamDestroy(s);
 }
 
 int ldg_get_info(const ldg_handle* H, ldg_info_t* out) {
-  if (!H || !out) return LDG_EINVAL;
-  const Handle& h = H->h;
+  if (!H || !out || H->team.ranks.empty()) return LDG_EINVAL;
+  const Team& T = H->team;
+  const Handle& h = T.h0();
   out->p = h.p;
   out->n_local = h.N;
   out->num_t = h.Kglobal;
-  out->num_owned = h.K;
-  out->num_ghost = h.Kg - h.K;
-  out->num_v = h.V;
-  out->rank = h.rank;
-  out->size = h.size;
-  out->bytes_device = h.bytes;
-  out->launches = h.launches;
-  for (const auto& c : h.coarse) out->launches += c->launches;
+  out->num_owned = 0;
+  out->num_ghost = 0;
+  out->bytes_device = 0;
+  for (const auto& rp : T.ranks) {
+    out->num_owned += rp->K;
+    out->num_ghost += rp->Kg - rp->K;
+    out->bytes_device += rp->bytes;
+    for (const auto& c : rp->coarse) out->bytes_device += c->bytes;
+  }
+  out->num_v = h.dim > 0 ? (h.dim + 1) * (h.dim + 1) : h.V;  // global vertex count
+  out->rank = T.first;
+  out->size = T.size;
+  out->launches = team_launches(T);
   return LDG_OK;
 }
 
@@ -252,37 +379,50 @@ int ldg_mesh_lists(ldg_handle* H, double* coords, int* v0t, double* b, double* a
                    int* nbr, int* nbr_n, int* id_e0t) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    const long Kp = h.Kp;
-    std::vector<double> g(static_cast<size_t>(ldgb::kGeomCount) * Kp);
-    std::vector<int> nb(3 * Kp), nn(3 * Kp), bid(3 * Kp), vt(3L * h.Kg);
-    LDG_CUDA(cudaMemcpy(g.data(), h.geom.ptr, sizeof(double) * g.size(), cudaMemcpyDeviceToHost));
-    LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
-    LDG_CUDA(cudaMemcpy(nn.data(), h.nbrn.ptr, sizeof(int) * nn.size(), cudaMemcpyDeviceToHost));
-    LDG_CUDA(cudaMemcpy(bid.data(), h.bid.ptr, sizeof(int) * bid.size(), cudaMemcpyDeviceToHost));
-    LDG_CUDA(cudaMemcpy(vt.data(), h.v0t.ptr, sizeof(int) * vt.size(), cudaMemcpyDeviceToHost));
-    if (coords) LDG_CUDA(cudaMemcpy(coords, h.coords.ptr, sizeof(double) * 2 * h.V, cudaMemcpyDeviceToHost));
-    for (int k = 0; k < h.K; ++k) {
-      const int gk = h.gid[k];
-      if (v0t)
-        for (int i = 0; i < 3; ++i) v0t[3 * gk + i] = vt[3 * k + i];
-      if (b) {
-        b[4 * gk] = g[ldgb::kB11 * Kp + k];
-        b[4 * gk + 1] = g[ldgb::kB12 * Kp + k];
-        b[4 * gk + 2] = g[ldgb::kB21 * Kp + k];
-        b[4 * gk + 3] = g[ldgb::kB22 * Kp + k];
-      }
-      if (area) area[gk] = g[ldgb::kArea * Kp + k];
-      for (int n = 0; n < 3; ++n) {
-        if (len) len[3 * gk + n] = g[(ldgb::kLen0 + n) * Kp + k];
-        if (nu) {
-          nu[6 * gk + 2 * n] = g[(ldgb::kNux0 + n) * Kp + k];
-          nu[6 * gk + 2 * n + 1] = g[(ldgb::kNuy0 + n) * Kp + k];
+    Team& T = H->team;
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      const long Kp = h.Kp;
+      std::vector<double> g(static_cast<size_t>(ldgb::kGeomCount) * Kp);
+      std::vector<int> nb(3 * Kp), nn(3 * Kp), bid(3 * Kp), vt(3L * h.Kg);
+      std::vector<double> cl(2L * h.V);
+      LDG_CUDA(cudaMemcpy(g.data(), h.geom.ptr, sizeof(double) * g.size(), cudaMemcpyDeviceToHost));
+      LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
+      LDG_CUDA(cudaMemcpy(nn.data(), h.nbrn.ptr, sizeof(int) * nn.size(), cudaMemcpyDeviceToHost));
+      LDG_CUDA(cudaMemcpy(bid.data(), h.bid.ptr, sizeof(int) * bid.size(), cudaMemcpyDeviceToHost));
+      LDG_CUDA(cudaMemcpy(vt.data(), h.v0t.ptr, sizeof(int) * vt.size(), cudaMemcpyDeviceToHost));
+      LDG_CUDA(cudaMemcpy(cl.data(), h.coords.ptr, sizeof(double) * cl.size(), cudaMemcpyDeviceToHost));
+      // local vertex id -> global: square strips number vertex columns from vx0
+      const bool square = h.dim > 0;
+      const int vx0 = square ? (h.strip_a > 0 ? h.strip_a - 1 : 0) : 0;
+      auto gv = [&](int lv) { return square ? lv + vx0 * (h.dim + 1) : lv; };
+      if (coords)
+        for (int lv = 0; lv < h.V; ++lv) {
+          coords[2 * gv(lv)] = cl[2 * lv];
+          coords[2 * gv(lv) + 1] = cl[2 * lv + 1];
         }
-        const int kp = nb[n * Kp + k];
-        if (nbr) nbr[3 * gk + n] = kp < 0 ? -1 : h.gid[kp];
-        if (nbr_n) nbr_n[3 * gk + n] = nn[n * Kp + k];
-        if (id_e0t) id_e0t[3 * gk + n] = bid[n * Kp + k];
+      for (int k = 0; k < h.K; ++k) {
+        const int gk = h.gid[k];
+        if (v0t)
+          for (int i = 0; i < 3; ++i) v0t[3 * gk + i] = gv(vt[3 * k + i]);
+        if (b) {
+          b[4 * gk] = g[ldgb::kB11 * Kp + k];
+          b[4 * gk + 1] = g[ldgb::kB12 * Kp + k];
+          b[4 * gk + 2] = g[ldgb::kB21 * Kp + k];
+          b[4 * gk + 3] = g[ldgb::kB22 * Kp + k];
+        }
+        if (area) area[gk] = g[ldgb::kArea * Kp + k];
+        for (int n = 0; n < 3; ++n) {
+          if (len) len[3 * gk + n] = g[(ldgb::kLen0 + n) * Kp + k];
+          if (nu) {
+            nu[6 * gk + 2 * n] = g[(ldgb::kNux0 + n) * Kp + k];
+            nu[6 * gk + 2 * n + 1] = g[(ldgb::kNuy0 + n) * Kp + k];
+          }
+          const int kp = nb[n * Kp + k];
+          if (nbr) nbr[3 * gk + n] = kp < 0 ? -1 : h.gid[kp];
+          if (nbr_n) nbr_n[3 * gk + n] = nn[n * Kp + k];
+          if (id_e0t) id_e0t[3 * gk + n] = bid[n * Kp + k];
+        }
       }
     }
   });
@@ -291,25 +431,29 @@ int ldg_mesh_lists(ldg_handle* H, double* coords, int* v0t, double* b, double* a
 int ldg_project(ldg_handle* H, const ldg_coeff* fn, double t, int q_ord, double* out) {
   if (!H || !fn) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
+    Team& T = H->team;
     if (fn->id < 0 || fn->id >= LDG_FN_COUNT) throw Error(LDG_EINVAL, "unknown coefficient function id");
-    DBuf<double> rule, tmp, km;
-    int R = 0;
-    ldgb::upload_rule(h, q_ord, rule, &R);
-    tmp.alloc(h.vec_len(), nullptr);
-    km.alloc(static_cast<size_t>(h.K) * h.N, nullptr);
-    ldgb::launch_project(h, *fn, t, rule.ptr, R, tmp.ptr, h.K);
-    ldgb::launch_soa_to_kmajor(h, tmp.ptr, 1, km.ptr);
-    LDG_CUDA(cudaMemcpyAsync(out, km.ptr, sizeof(double) * h.K * h.N, cudaMemcpyDeviceToHost, h.stream));
-    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    std::vector<std::unique_ptr<DBuf<double>>> tmp;
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      DBuf<double> rule;
+      int R = 0;
+      ldgb::upload_rule(h, q_ord, rule, &R);
+      tmp.push_back(std::make_unique<DBuf<double>>());
+      tmp.back()->alloc(h.vec_len(), nullptr);
+      ldgb::launch_project(h, *fn, t, rule.ptr, R, tmp.back()->ptr, h.K);
+      LDG_CUDA(cudaStreamSynchronize(T.stream));
+    }
+    size_t i = 0;
+    gather_to_host(T, [&](Handle&) { return static_cast<const double*>(tmp[i++]->ptr); }, 1, out);
   });
 }
 
 int ldg_assemble(ldg_handle* H, double t) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {
-    ldgb::assemble_step(H->h, t);
-    LDG_CUDA(cudaStreamSynchronize(H->h.stream));
+    ldgb::team_assemble(H->team, t);
+    LDG_CUDA(cudaStreamSynchronize(H->team.stream));
   });
 }
 
@@ -317,41 +461,42 @@ int ldg_export_operator(ldg_handle* H, int which, int64_t* nnz, int64_t* rows, i
                         int64_t cap) {
   if (!H || !nnz) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
+    Team& T = H->team;
     if (which < 0 || which >= LDG_OP_COUNT) throw Error(LDG_EINVAL, "unknown operator");
     const bool needs_d = which == LDG_OP_G1 || which == LDG_OP_G2 || which == LDG_OP_R1 || which == LDG_OP_R2 ||
                          which == LDG_OP_RD1 || which == LDG_OP_RD2 || which == LDG_OP_A;
-    if (needs_d) require_assembled(h);
-    ensure_solver(h);
-    std::vector<int> nb(3 * h.Kp);
-    LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
-    const long NN = static_cast<long>(h.N) * h.N;
-    DBuf<double> tmp;
+    if (needs_d) require_assembled(T);
     Coo coo;
-    auto emit = [&](const std::vector<double>& blk, int comp, bool off, int ru, int cu, double scale) {
-      const double* base = blk.data() + static_cast<size_t>(comp) * 4 * NN * h.Kp;
-      for (int k = 0; k < h.K; ++k)
-        for (int s = 0; s < (off ? 4 : 1); ++s) push_block(h, nb, base, k, s, ru, cu, scale, coo);
-    };
-    if (which == LDG_OP_A) {
-      // the static blocks exactly as the matrix-free kernels rebuild them (K4)
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      std::vector<int> nb(3 * h.Kp);
+      LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
+      const long NN = static_cast<long>(h.N) * h.N;
+      DBuf<double> tmp;
       tmp.alloc(8 * NN * h.Kp, nullptr);
-      ldgb::launch_static(h, ldgb::kStM, tmp.ptr);
-      const auto M = blocks_to_host(h, tmp.ptr, 1);
-      ldgb::launch_static(h, ldgb::kStB, tmp.ptr);
-      const auto B = blocks_to_host(h, tmp.ptr, 2);
-      ldgb::launch_static(h, ldgb::kStS, tmp.ptr);
-      const auto S = blocks_to_host(h, tmp.ptr, 1);
-      const auto E = blocks_to_host(h, h.E.ptr, 2);
-      emit(M, 0, false, 0, 0, 1.0);
-      emit(B, 0, true, 0, 2, 1.0);
-      emit(M, 0, false, 1, 1, 1.0);
-      emit(B, 1, true, 1, 2, 1.0);
-      emit(E, 0, true, 2, 0, 1.0);
-      emit(E, 1, true, 2, 1, 1.0);
-      emit(S, 0, true, 2, 2, h.prob.eta);
-    } else {
-      tmp.alloc(8 * NN * h.Kp, nullptr);
+      auto emit = [&](const std::vector<double>& blk, int comp, bool off, int ru, int cu, double scale) {
+        const double* base = blk.data() + static_cast<size_t>(comp) * 4 * NN * h.Kp;
+        for (int k = 0; k < h.K; ++k)
+          for (int s = 0; s < (off ? 4 : 1); ++s) push_block(h, nb, base, k, s, ru, cu, scale, coo);
+      };
+      if (which == LDG_OP_A) {
+        // the static blocks exactly as the matrix-free kernels rebuild them (K4)
+        ldgb::launch_static(h, ldgb::kStM, tmp.ptr);
+        const auto M = blocks_to_host(h, tmp.ptr, 1);
+        ldgb::launch_static(h, ldgb::kStB, tmp.ptr);
+        const auto B = blocks_to_host(h, tmp.ptr, 2);
+        ldgb::launch_static(h, ldgb::kStS, tmp.ptr);
+        const auto S = blocks_to_host(h, tmp.ptr, 1);
+        const auto E = blocks_to_host(h, h.E.ptr, 2);
+        emit(M, 0, false, 0, 0, 1.0);
+        emit(B, 0, true, 0, 2, 1.0);
+        emit(M, 0, false, 1, 1, 1.0);
+        emit(B, 1, true, 1, 2, 1.0);
+        emit(E, 0, true, 2, 0, 1.0);
+        emit(E, 1, true, 2, 1, 1.0);
+        emit(S, 0, true, 2, 2, h.prob.eta);
+        continue;
+      }
       int comp = 0;
       bool off = false;
       switch (which) {
@@ -404,91 +549,103 @@ int ldg_export_operator(ldg_handle* H, int which, int64_t* nnz, int64_t* rows, i
 int ldg_export_vector(ldg_handle* H, int which, double* out, int64_t cap) {
   if (!H || !out) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    const long n = h.vec_len();
-    const double* src = nullptr;
+    Team& T = H->team;
     int nvec = 1;
-    DBuf<double> tmp;
+    std::vector<std::unique_ptr<DBuf<double>>> tmp;
+    std::function<const double*(Handle&)> src;
     switch (which) {
-      case LDG_VEC_D: require_assembled(h); src = h.D.ptr; break;
-      case LDG_VEC_F: require_assembled(h); src = h.F.ptr; break;
-      case LDG_VEC_JD1: case LDG_VEC_JD2: case LDG_VEC_KD: case LDG_VEC_KN: case LDG_VEC_L:
-        require_assembled(h);
-        tmp.alloc(n, nullptr);
-        ldgb::launch_rhs_which(h, h.t_assembled, 1 + (which - LDG_VEC_JD1), tmp.ptr);
-        src = tmp.ptr;
+      case LDG_VEC_D: require_assembled(T); src = [](Handle& h) { return static_cast<const double*>(h.D.ptr); }; break;
+      case LDG_VEC_F: require_assembled(T); src = [](Handle& h) { return static_cast<const double*>(h.F.ptr); }; break;
+      case LDG_VEC_JD1: case LDG_VEC_JD2: case LDG_VEC_KD: case LDG_VEC_KN: case LDG_VEC_L: {
+        require_assembled(T);
+        for (auto& rp : T.ranks) {
+          tmp.push_back(std::make_unique<DBuf<double>>());
+          tmp.back()->alloc(rp->vec_len(), nullptr);
+          ldgb::launch_rhs_which(*rp, rp->t_assembled, 1 + (which - LDG_VEC_JD1), tmp.back()->ptr);
+        }
+        size_t i = 0;
+        src = [&tmp, i](Handle&) mutable { return static_cast<const double*>(tmp[i++]->ptr); };
         break;
-      case LDG_VEC_V: require_assembled(h); src = h.Vv.ptr; nvec = 3; break;
-      case LDG_VEC_Y: src = h.Y.ptr; nvec = 3; break;
+      }
+      case LDG_VEC_V:
+        require_assembled(T);
+        src = [](Handle& h) { return static_cast<const double*>(h.Vv.ptr); };
+        nvec = 3;
+        break;
+      case LDG_VEC_Y: src = [](Handle& h) { return static_cast<const double*>(h.Y.ptr); }; nvec = 3; break;
       default: throw Error(LDG_EINVAL, "unknown vector");
     }
-    const int64_t cnt = static_cast<int64_t>(nvec) * h.K * h.N;
+    const int64_t cnt = static_cast<int64_t>(nvec) * T.h0().Kglobal * T.h0().N;
     if (cap < cnt) throw Error(LDG_EINVAL, "export capacity too small");
-    DBuf<double> km;
-    km.alloc(cnt, nullptr);
-    ldgb::launch_soa_to_kmajor(h, src, nvec, km.ptr);
-    LDG_CUDA(cudaMemcpyAsync(out, km.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h.stream));
-    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    gather_to_host(T, src, nvec, out);
   });
 }
 
 int ldg_initial_state(ldg_handle* H) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    LDG_CUDA(cudaMemsetAsync(h.Y.ptr, 0, sizeof(double) * 3 * h.vec_len(), h.stream));
-    ldgb::launch_project(h, h.prob.c0, 0.0, h.rule_elem.ptr, h.rule_elem_R, h.Y.ptr + 2 * h.vec_len(), h.K);
-    h.t = 0.0;
-    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    Team& T = H->team;
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      LDG_CUDA(cudaMemsetAsync(h.Y.ptr, 0, sizeof(double) * 3 * h.vec_len(), T.stream));
+      ldgb::launch_project(h, h.prob.c0, 0.0, h.rule_ptr(), h.rule_R(), h.Y.ptr + 2 * h.vec_len(), h.K);
+      h.t = 0.0;
+    }
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
 }
 
 int ldg_set_state(ldg_handle* H, const double* y, double t) {
   if (!H || !y) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    const size_t cnt = 3L * h.K * h.N;
-    DBuf<double> km;
-    km.alloc(cnt, nullptr);
-    LDG_CUDA(cudaMemcpyAsync(km.ptr, y, sizeof(double) * cnt, cudaMemcpyHostToDevice, h.stream));
-    ldgb::launch_kmajor_to_soa(h, km.ptr, 3, h.Y.ptr);
-    h.t = t;
-    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    Team& T = H->team;
+    scatter_from_host(T, y, 3, [](Handle& h) { return h.Y.ptr; });
+    for (auto& rp : T.ranks) rp->t = t;
   });
 }
 
 int ldg_get_state(ldg_handle* H, double* y, double* t) {
   if (!H) return LDG_EINVAL;
-  if (t) *t = H->h.t;
+  if (t) *t = H->team.h0().t;
   if (!y) return LDG_OK;
-  return ldg_export_vector(H, LDG_VEC_Y, y, 3L * H->h.K * H->h.N);
+  const Handle& h = H->team.h0();
+  return ldg_export_vector(H, LDG_VEC_Y, y, 3L * h.Kglobal * h.N);
 }
+
+namespace {
+
+void run_steps(Team& T, double dt, int nsteps, const ldg_solver_opts& o, ldg_step_stats* st) {
+  Handle& h0 = T.h0();
+  for (int s = 0; s < nsteps; ++s) {
+    const double t_next = h0.t + dt;  // system.hpp:158
+    LDG_CUDA(cudaEventRecord(h0.ev[0], T.stream));
+    ldgb::team_assemble(T, t_next);
+    LDG_CUDA(cudaEventRecord(h0.ev[1], T.stream));
+    ldgb::team_solve(T, 1.0, dt, o, st);
+    LDG_CUDA(cudaEventRecord(h0.ev[2], T.stream));
+    LDG_CUDA(cudaEventSynchronize(h0.ev[2]));
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, h0.ev[0], h0.ev[1]);
+    cudaEventElapsedTime(&b, h0.ev[1], h0.ev[2]);
+    if (st) {
+      st->ms_assemble += a;
+      st->ms_solve += b;
+    }
+    for (auto& rp : T.ranks) rp->t = t_next;
+  }
+}
+
+}  // namespace
 
 int ldg_euler_steps(ldg_handle* H, double dt, int nsteps, const ldg_solver_opts* opts, ldg_step_stats* st) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
+    Team& T = H->team;
     if (!(dt > 0.0)) throw Error(LDG_EINVAL, "time step must be positive");
-    ensure_solver(h);
+    ensure_solver(T);
     const ldg_solver_opts o = opts ? *opts : ldg_default_solver_opts();
     if (st) *st = ldg_step_stats{};
-    for (int s = 0; s < nsteps; ++s) {
-      const double t_next = h.t + dt;  // system.hpp:158
-      LDG_CUDA(cudaEventRecord(h.ev[0], h.stream));
-      ldgb::assemble_step(h, t_next);
-      LDG_CUDA(cudaEventRecord(h.ev[1], h.stream));
-      ldgb::solve_step(h, 1.0, dt, o, st);
-      LDG_CUDA(cudaEventRecord(h.ev[2], h.stream));
-      LDG_CUDA(cudaEventSynchronize(h.ev[2]));
-      float a = 0.f, b = 0.f;
-      cudaEventElapsedTime(&a, h.ev[0], h.ev[1]);
-      cudaEventElapsedTime(&b, h.ev[1], h.ev[2]);
-      if (st) {
-        st->ms_assemble += a;
-        st->ms_solve += b;
-      }
-      h.t = t_next;
-    }
+    run_steps(T, dt, nsteps, o, st);
   });
 }
 
@@ -496,40 +653,35 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
                          const ldg_solver_opts* opts, ldg_step_stats* st, double* ms_total) {
   if (!H || !y_in || !y_out) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
+    Team& T = H->team;
     if (!(dt > 0.0)) throw Error(LDG_EINVAL, "time step must be positive");
-    ensure_solver(h);
+    ensure_solver(T);
     const ldg_solver_opts o = opts ? *opts : ldg_default_solver_opts();
     if (st) *st = ldg_step_stats{};
-    const size_t cnt = 3L * h.K * h.N;
-    if (!h.host_stage.ptr) h.host_stage.alloc(cnt, &h.bytes);
-    LDG_CUDA(cudaEventRecord(h.ev[3], h.stream));
-    LDG_CUDA(cudaMemcpyAsync(h.host_stage.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice, h.stream));
-    ldgb::launch_kmajor_to_soa(h, h.host_stage.ptr, 3, h.Y.ptr);
-    h.t = t;
-    for (int s = 0; s < nsteps; ++s) {
-      const double t_next = h.t + dt;
-      LDG_CUDA(cudaEventRecord(h.ev[0], h.stream));
-      ldgb::assemble_step(h, t_next);
-      LDG_CUDA(cudaEventRecord(h.ev[1], h.stream));
-      ldgb::solve_step(h, 1.0, dt, o, st);
-      LDG_CUDA(cudaEventRecord(h.ev[2], h.stream));
-      LDG_CUDA(cudaEventSynchronize(h.ev[2]));
-      float a = 0.f, b = 0.f;
-      cudaEventElapsedTime(&a, h.ev[0], h.ev[1]);
-      cudaEventElapsedTime(&b, h.ev[1], h.ev[2]);
-      if (st) {
-        st->ms_assemble += a;
-        st->ms_solve += b;
-      }
-      h.t = t_next;
+    Handle& h0 = T.h0();
+    LDG_CUDA(cudaEventRecord(h0.ev[3], T.stream));
+    if (T.nlocal() == 1 && T.size == 1) {
+      // one rank: the stacked host state is exactly the rank's owned rows
+      const size_t cnt = 3L * h0.K * h0.N;
+      if (!h0.host_stage.ptr) h0.host_stage.alloc(cnt, &h0.bytes);
+      LDG_CUDA(cudaMemcpyAsync(h0.host_stage.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice, T.stream));
+      ldgb::launch_kmajor_to_soa(h0, h0.host_stage.ptr, 3, h0.Y.ptr);
+    } else {
+      scatter_from_host(T, y_in, 3, [](Handle& h) { return h.Y.ptr; });
     }
-    ldgb::launch_soa_to_kmajor(h, h.Y.ptr, 3, h.host_stage.ptr);
-    LDG_CUDA(cudaMemcpyAsync(y_out, h.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h.stream));
-    LDG_CUDA(cudaEventRecord(h.ev[2], h.stream));
-    LDG_CUDA(cudaEventSynchronize(h.ev[2]));
+    for (auto& rp : T.ranks) rp->t = t;
+    run_steps(T, dt, nsteps, o, st);
+    if (T.nlocal() == 1 && T.size == 1) {
+      const size_t cnt = 3L * h0.K * h0.N;
+      ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
+      LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
+    } else {
+      gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.Y.ptr); }, 3, y_out);
+    }
+    LDG_CUDA(cudaEventRecord(h0.ev[2], T.stream));
+    LDG_CUDA(cudaEventSynchronize(h0.ev[2]));
     float tot = 0.f;
-    cudaEventElapsedTime(&tot, h.ev[3], h.ev[2]);
+    cudaEventElapsedTime(&tot, h0.ev[3], h0.ev[2]);
     if (ms_total) *ms_total = tot;
   });
 }
@@ -537,57 +689,57 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
 int ldg_solve_stationary(ldg_handle* H, double t, const ldg_solver_opts* opts, ldg_step_stats* st) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    ensure_solver(h);
+    Team& T = H->team;
+    ensure_solver(T);
     const ldg_solver_opts o = opts ? *opts : ldg_default_solver_opts();
     if (st) *st = ldg_step_stats{};
-    ldgb::assemble_step(h, t);
-    ldgb::solve_step(h, 0.0, 1.0, o, st);
-    h.t = t;
-    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    ldgb::team_assemble(T, t);
+    ldgb::team_solve(T, 0.0, 1.0, o, st);
+    for (auto& rp : T.ranks) rp->t = t;
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
 }
 
 int ldg_apply_lhs(ldg_handle* H, double dt, const double* x, double* y) {
   if (!H || !x || !y) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    require_assembled(h);
-    ensure_solver(h);
-    const size_t cnt = 3L * h.K * h.N;
-    DBuf<double> km, xs, ys;
-    km.alloc(cnt, nullptr);
-    xs.alloc(3 * h.vec_len(), nullptr);
-    ys.alloc(3 * h.vec_len(), nullptr);
-    LDG_CUDA(cudaMemcpyAsync(km.ptr, x, sizeof(double) * cnt, cudaMemcpyHostToDevice, h.stream));
-    ldgb::launch_kmajor_to_soa(h, km.ptr, 3, xs.ptr);
-    ldgb::launch_full_apply(h, xs.ptr, 1.0, dt, ys.ptr);
-    ldgb::launch_soa_to_kmajor(h, ys.ptr, 3, km.ptr);
-    LDG_CUDA(cudaMemcpyAsync(y, km.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h.stream));
-    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    Team& T = H->team;
+    require_assembled(T);
+    ensure_solver(T);
+    for (auto& rp : T.ranks)  // keep the state: Yold is the solver's scratch
+      LDG_CUDA(cudaMemcpyAsync(rp->Yold.ptr, rp->Y.ptr, sizeof(double) * 3 * rp->vec_len(), cudaMemcpyDeviceToDevice,
+                               T.stream));
+    scatter_from_host(T, x, 3, [](Handle& h) { return h.Y.ptr; });
+    ldgb::team_full_apply(T, 1.0, dt);
+    gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.full_y.ptr); }, 3, y);
+    for (auto& rp : T.ranks)
+      LDG_CUDA(cudaMemcpyAsync(rp->Y.ptr, rp->Yold.ptr, sizeof(double) * 3 * rp->vec_len(), cudaMemcpyDeviceToDevice,
+                               T.stream));
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
 }
 
 int ldg_sync(ldg_handle* H) {
   if (!H) return LDG_EINVAL;
-  return guarded(H, [&] { LDG_CUDA(cudaStreamSynchronize(H->h.stream)); });
+  return guarded(H, [&] { LDG_CUDA(cudaStreamSynchronize(H->team.stream)); });
 }
 
 int ldg_time_kernels(ldg_handle* H, double t, double dt, int reps, int flush, ldg_kernel_times* out) {
   if (!H || !out || reps < 1) return LDG_EINVAL;
   return guarded(H, [&] {
-    Handle& h = H->h;
-    ensure_solver(h);
+    Team& T = H->team;
+    Handle& h = T.h0();
+    ensure_solver(T);
     const size_t flush_n = (256ull << 20) / sizeof(double);  // 256 MB > 126 MB L2
     if (flush && !h.flush.ptr) h.flush.alloc(flush_n, nullptr);
     auto timed = [&](auto&& fn) {
       for (int w = 0; w < 2; ++w) fn();  // warm-up
       float total = 0.f;
       for (int r = 0; r < reps; ++r) {
-        if (flush) LDG_CUDA(cudaMemsetAsync(h.flush.ptr, r & 0xff, flush_n * sizeof(double), h.stream));
-        LDG_CUDA(cudaEventRecord(h.ev[0], h.stream));
+        if (flush) LDG_CUDA(cudaMemsetAsync(h.flush.ptr, r & 0xff, flush_n * sizeof(double), T.stream));
+        LDG_CUDA(cudaEventRecord(h.ev[0], T.stream));
         fn();
-        LDG_CUDA(cudaEventRecord(h.ev[1], h.stream));
+        LDG_CUDA(cudaEventRecord(h.ev[1], T.stream));
         LDG_CUDA(cudaEventSynchronize(h.ev[1]));
         float ms = 0.f;
         cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]);
@@ -597,18 +749,20 @@ int ldg_time_kernels(ldg_handle* H, double t, double dt, int reps, int flush, ld
     };
     out->reps = reps;
     out->ms_project = timed([&] {
-      ldgb::launch_project_df(h, t, h.rule_elem.ptr, h.rule_elem_R);
-      ldgb::launch_rhs(h, t);
+      for (auto& rp : T.ranks) {
+        ldgb::launch_project_df(*rp, t, rp->rule_ptr(), rp->rule_R());
+        ldgb::launch_rhs(*rp, t);
+      }
     });
-    out->ms_assemble = timed([&] { ldgb::launch_assemble(h, ldgb::kModeE, h.E.ptr); });
-    h.assembled = true;
-    h.t_assembled = t;
-    out->ms_spmv = timed([&] { ldgb::launch_full_apply(h, h.Y.ptr, 1.0, dt, h.full_y.ptr); });
-    out->ms_schur = timed([&] {
-      ldgb::launch_stage1(h, nullptr, 0.0, h.Y.ptr + 2 * h.vec_len(), 1.0, h.tz.ptr);
-      ldgb::launch_stage2(h, h.Y.ptr + 2 * h.vec_len(), 1.0, dt * h.prob.eta, h.tz.ptr, dt, nullptr, 0.0,
-                          h.kr_v.ptr);
+    out->ms_assemble = timed([&] {
+      for (auto& rp : T.ranks) ldgb::launch_assemble(*rp, ldgb::kModeE, rp->E.ptr);
     });
+    for (auto& rp : T.ranks) {
+      rp->assembled = true;
+      rp->t_assembled = t;
+    }
+    out->ms_spmv = timed([&] { ldgb::team_full_apply(T, 1.0, dt); });
+    out->ms_schur = timed([&] { ldgb::team_schur_apply_c(T, 1.0, dt); });
   });
 }
 

@@ -133,15 +133,61 @@ struct Handle {
   };
   std::vector<VGraph> vgraphs;
 
+  // strip decomposition of FK meshes: this handle owns element
+  // columns [strip_a, strip_b) of FK(dim); local numbering is owned lowers
+  // ((ix-a)*dim+iy), owned uppers (W*dim + ...), then the ghost uppers of
+  // column a-1 and the ghost lowers of column b (one halo column per side).
+  // Vertex (ix, iy) of this level is vertex (ix*stride, iy*stride) of the
+  // finest mesh FK(dim_fine), so every level and rank regenerates identical
+  // (jittered) coordinates from the same splitmix64 stream.
+  int strip_a = 0, strip_b = 0;
+  int ghost_left = 0, ghost_right = 0;  // ghost element counts (dim or 0)
+  int stride = 1, dim_fine = 0;
+  double jitter = 0.0;
+  uint64_t seed = 0;
+  int strip_w() const { return strip_b - strip_a; }
+  long own_left_off() const { return 0; }                                                // lowers of column a
+  long own_right_off() const { return static_cast<long>(2 * strip_w() - 1) * dim; }     // uppers of column b-1
+  long ghost_left_off() const { return 2L * strip_w() * dim; }
+  long ghost_right_off() const { return 2L * strip_w() * dim + ghost_left; }
+
   DevMesh mesh() const { return DevMesh{K, Kg, Kp, geom.ptr, nbr.ptr, nbrn.ptr, kind.ptr}; }
   long vec_len() const { return static_cast<long>(N) * Kp; }
   const double* rule_ptr() const { return rule_shared ? rule_shared : rule_elem.ptr; }
   int rule_R() const { return rule_shared ? rule_shared_R : rule_elem_R; }
 };
 
+// A group of ranks driven in lockstep: the local ranks of this process
+// (one per GPU in a real multi-GPU run, or several "virtual" ranks sharing
+// one GPU and one stream, used to validate the decomposition on one device)
+// plus the NCCL communicator to remote ranks.  Halo values of local
+// neighbours move with device copies, of remote ones with ncclSend/Recv;
+// dot products are summed over local ranks, then ncclAllReduce'd.
+struct Team {
+  std::vector<std::unique_ptr<Handle>> ranks;
+  int size = 1;        // global rank count
+  int first = 0;       // global rank of ranks[0]
+  void* nccl = nullptr;  // ncclComm_t when size > local ranks
+  bool owns_nccl = false;
+  cudaStream_t stream = nullptr;
+  DBuf<double> send_l, send_r, recv_l, recv_r;  // NCCL halo staging
+  DBuf<double> red_all;                         // allreduce scratch
+  double* red_host = nullptr;                   // pinned
+  std::string err;
+  Handle& h0() { return *ranks[0]; }
+  const Handle& h0() const { return *ranks[0]; }
+  int nlocal() const { return static_cast<int>(ranks.size()); }
+  Handle* local(int global_rank) {
+    const int i = global_rank - first;
+    return (i >= 0 && i < nlocal()) ? ranks[i].get() : nullptr;
+  }
+};
+
 // ---- launchers (defined in the .cu files) ----------------------------------
 // mesh (ldg_mesh.cu)
 void build_square_mesh(Handle& h, int dim, double jitter, uint64_t seed);
+// strip [a, b) of FK(dim) (level with vertex stride `stride` of FK(dim_fine))
+void build_square_strip(Handle& h, int dim, int a, int b, int stride, int dim_fine, double jitter, uint64_t seed);
 void build_general_mesh(Handle& h, const double* coords, int nv, const int* v0t, int nt, const int* id_e0t);
 
 // assembly (ldg_assemble.cu)
@@ -185,15 +231,22 @@ void rows_bjac(Handle& h, const TP* Pinv, const double* x, double omega, double 
 void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
                      const double* z, double* out);
 
-// driver pieces (ldg_solve.cu)
+// per-rank assembly step (ldg_vec.cu)
 void assemble_step(Handle& h, double t);
-int solve_step(Handle& h, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st);
+size_t reduction_scratch();
+
+// team driver (ldg_team.cu)
+void team_assemble(Team& T, double t);
+int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st);
+void team_full_apply(Team& T, double wm, double dt);        // full_y = (W + dt A) Y, halos refreshed
+void team_schur_apply_c(Team& T, double wm, double dt);     // kr_v = S_c C (kernel timing)
 
 // multigrid (ldg_mg.cu)
-void build_square_from_coords(Handle& h, int dim, const double* coords_dev);
-bool mg_build(Handle& h);                                   // false: no hierarchy for this mesh
-void mg_setup_step(Handle& h, double t, double wm, double dt);  // per step: coarse E, block-Jacobi
-void mg_vcycle(Handle& h, double wm, double dt, const double* b, double* x);  // x = V(b), level 0 = h
+int mg_depth(int dim, int team_size);
+bool mg_build(Handle& h, int team_size);                    // false: no hierarchy for this mesh
+void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32);  // per step: coarse E, block-Jacobi
+void mg_restrict(Handle& fine, Handle& coarse);             // coarse.mg_b = P^T fine.mg_r
+void mg_prolong_add(Handle& fine, Handle& coarse, double* x);  // x += P coarse.mg_x
 int mg_levels(const Handle& h);
 void mg_release(Handle& h);  // destroys captured graphs
 

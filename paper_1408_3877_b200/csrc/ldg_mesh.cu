@@ -280,45 +280,123 @@ void topology_and_geometry(Handle& h, double bbox_area, const int* id_in_dev) {
 
 long padded(long k) { return ((k + 31) / 32) * 32; }
 
+// Vertices of columns [vx0, vx1] of FK(dim) on one level: vertex (ix, iy) is
+// vertex (ix*stride, iy*stride) of the finest FK(dim_fine), coordinates and
+// jitter computed exactly as k_fk_vertices does for that finest vertex.
+__global__ void k_fk_vertices_strip(int dim, int vx0, int vx1, int stride, int dim_fine, double jitter,
+                                    uint64_t seed, double* coords) {
+  const long V = static_cast<long>(vx1 - vx0 + 1) * (dim + 1);
+  const long v = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (v >= V) return;
+  const int fx = (vx0 + static_cast<int>(v / (dim + 1))) * stride;
+  const int fy = static_cast<int>(v % (dim + 1)) * stride;
+  const double h = 1.0 / dim_fine;
+  double x = fx * h, y = fy * h;
+  if (jitter > 0.0 && fx > 0 && fx < dim_fine && fy > 0 && fy < dim_fine) {
+    const uint64_t vf = static_cast<uint64_t>(fx) * static_cast<uint64_t>(dim_fine + 1) + static_cast<uint64_t>(fy);
+    const uint64_t base = seed << 32;
+    const double amp = __dmul_rn(jitter, h);
+    const double ux = static_cast<double>(splitmix64(base + 2ull * vf) >> 11) * (1.0 / 9007199254740992.0);
+    const double uy = static_cast<double>(splitmix64(base + 2ull * vf + 1ull) >> 11) * (1.0 / 9007199254740992.0);
+    x = __dadd_rn(x, __dmul_rn(__dsub_rn(__dmul_rn(2.0, ux), 1.0), amp));
+    y = __dadd_rn(y, __dmul_rn(__dsub_rn(__dmul_rn(2.0, uy), 1.0), amp));
+  }
+  coords[2 * v] = x;
+  coords[2 * v + 1] = y;
+}
+
+// FK triangles of the strip in local numbering: owned lowers, owned uppers,
+// ghost uppers of column a-1 (gl of them), ghost lowers of column b.
+__global__ void k_fk_triangles_strip(int dim, int a, int b, int gl, int gr, int vx0, int* v0t) {
+  const long W = b - a;
+  const long Kg = 2 * W * dim + gl + gr;
+  const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (k >= Kg) return;
+  bool upper;
+  int ix, iy;
+  if (k < W * dim) {
+    upper = false;
+    ix = a + static_cast<int>(k / dim);
+    iy = static_cast<int>(k % dim);
+  } else if (k < 2 * W * dim) {
+    upper = true;
+    ix = a + static_cast<int>((k - W * dim) / dim);
+    iy = static_cast<int>((k - W * dim) % dim);
+  } else if (k < 2 * W * dim + gl) {
+    upper = true;
+    ix = a - 1;
+    iy = static_cast<int>(k - 2 * W * dim);
+  } else {
+    upper = false;
+    ix = b;
+    iy = static_cast<int>(k - 2 * W * dim - gl);
+  }
+  auto vid = [dim, vx0](int x, int y) { return (x - vx0) * (dim + 1) + y; };
+  if (!upper) {
+    v0t[3 * k] = vid(ix, iy);
+    v0t[3 * k + 1] = vid(ix + 1, iy);
+    v0t[3 * k + 2] = vid(ix, iy + 1);
+  } else {
+    v0t[3 * k] = vid(ix + 1, iy);
+    v0t[3 * k + 1] = vid(ix + 1, iy + 1);
+    v0t[3 * k + 2] = vid(ix, iy + 1);
+  }
+}
+
 }  // namespace
 
-void build_square_mesh(Handle& h, int dim, double jitter, uint64_t seed) {
+// Columns [a, b) of FK(dim) plus one ghost column per side (the full mesh
+// when a = 0, b = dim).  Element order within the owned part matches the
+// reference's (lowers then uppers, column-major), so a single strip is
+// exactly domain_square's numbering (mesh.hpp:237-242).
+void build_square_strip(Handle& h, int dim, int a, int b, int stride, int dim_fine, double jitter, uint64_t seed) {
   if (dim < 1) throw Error(LDG_EINVAL, "maximum edge length must be positive");
   if (!(jitter >= 0.0 && jitter < 0.5)) throw Error(LDG_EINVAL, "jitter must be in [0, 0.5)");
-  const long V = static_cast<long>(dim + 1) * (dim + 1);
-  const long K = 2L * dim * dim;
-  if (K > 0x7fffffffL / 3) throw Error(LDG_EINVAL, "mesh too large for 32-bit element indices");
-  h.V = static_cast<int>(V);
-  h.K = h.Kg = h.Kglobal = static_cast<int>(K);
-  h.Kp = padded(K);
-  h.coords.alloc(2 * V, &h.bytes);
-  h.v0t.alloc(3 * K, &h.bytes);
-  k_fk_vertices<<<grid_of(V, 256), 256, 0, h.stream>>>(dim, jitter, seed, h.coords.ptr);
-  k_fk_triangles<<<grid_of(K, 256), 256, 0, h.stream>>>(dim, h.v0t.ptr);
-  LDG_CUDA(cudaGetLastError());
-  ++h.launches;
-  h.gid.resize(K);
-  for (long k = 0; k < K; ++k) h.gid[k] = static_cast<int>(k);
+  if (a < 0 || b > dim || b <= a) throw Error(LDG_EINVAL, "empty or invalid strip");
+  if (2L * dim * dim > 0x7fffffffL / 3) throw Error(LDG_EINVAL, "mesh too large for 32-bit element indices");
+  const int W = b - a;
+  const int gl = a > 0 ? dim : 0, gr = b < dim ? dim : 0;
+  const int vx0 = a > 0 ? a - 1 : a, vx1 = b < dim ? b + 1 : b;
+  const long V = static_cast<long>(vx1 - vx0 + 1) * (dim + 1);
+  const long K = 2L * W * dim;
+  const long Kg = K + gl + gr;
   h.dim = dim;
+  h.strip_a = a;
+  h.strip_b = b;
+  h.ghost_left = gl;
+  h.ghost_right = gr;
+  h.stride = stride;
+  h.dim_fine = dim_fine;
+  h.jitter = jitter;
+  h.seed = seed;
+  h.V = static_cast<int>(V);
+  h.K = static_cast<int>(K);
+  h.Kg = static_cast<int>(Kg);
+  h.Kglobal = 2 * dim * dim;
+  h.Kp = padded(Kg);
+  h.coords.alloc(2 * V, &h.bytes);
+  h.v0t.alloc(3 * Kg, &h.bytes);
+  k_fk_vertices_strip<<<grid_of(V, 256), 256, 0, h.stream>>>(dim, vx0, vx1, stride, dim_fine, jitter, seed,
+                                                             h.coords.ptr);
+  k_fk_triangles_strip<<<grid_of(Kg, 256), 256, 0, h.stream>>>(dim, a, b, gl, gr, vx0, h.v0t.ptr);
+  LDG_CUDA(cudaGetLastError());
+  h.launches += 2;
+  // global element index (reference numbering) of every local element,
+  // ghosts included (exports resolve neighbour columns through it)
+  h.gid.resize(Kg);
+  const long dd = static_cast<long>(dim) * dim;
+  for (long k = 0; k < K; ++k) {
+    const long q = k < static_cast<long>(W) * dim ? k : k - static_cast<long>(W) * dim;
+    const long ix = a + q / dim, iy = q % dim;
+    h.gid[k] = static_cast<int>((k < static_cast<long>(W) * dim ? 0 : dd) + ix * dim + iy);
+  }
+  for (long iy = 0; iy < gl; ++iy) h.gid[K + iy] = static_cast<int>(dd + static_cast<long>(a - 1) * dim + iy);
+  for (long iy = 0; iy < gr; ++iy) h.gid[K + gl + iy] = static_cast<int>(static_cast<long>(b) * dim + iy);
   topology_and_geometry(h, 1.0, nullptr);
 }
 
-// A multigrid level: FK(dim) triangles on given device coordinates (the
-// finer level's vertices subsampled), same topology/geometry pass.
-void build_square_from_coords(Handle& h, int dim, const double* coords_dev) {
-  const long V = static_cast<long>(dim + 1) * (dim + 1);
-  const long K = 2L * dim * dim;
-  h.V = static_cast<int>(V);
-  h.K = h.Kg = h.Kglobal = static_cast<int>(K);
-  h.Kp = padded(K);
-  h.dim = dim;
-  h.coords.alloc(2 * V, &h.bytes);
-  h.v0t.alloc(3 * K, &h.bytes);
-  LDG_CUDA(cudaMemcpyAsync(h.coords.ptr, coords_dev, sizeof(double) * 2 * V, cudaMemcpyDeviceToDevice, h.stream));
-  k_fk_triangles<<<grid_of(K, 256), 256, 0, h.stream>>>(dim, h.v0t.ptr);
-  LDG_CUDA(cudaGetLastError());
-  ++h.launches;
-  topology_and_geometry(h, 1.0, nullptr);
+void build_square_mesh(Handle& h, int dim, double jitter, uint64_t seed) {
+  build_square_strip(h, dim, 0, dim, 1, dim, jitter, seed);
 }
 
 void build_general_mesh(Handle& h, const double* coords, int nv, const int* v0t, int nt, const int* id_e0t) {

@@ -43,29 +43,20 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
     default: { CALL(4); break; } \
   }
 
-// coarse vertex (ix, iy) of FK(dim_c) = fine vertex (2 ix, 2 iy) of FK(2 dim_c)
-__global__ void k_subsample(int dim_c, const double* __restrict__ cf, double* __restrict__ cc) {
-  const long Vc = static_cast<long>(dim_c + 1) * (dim_c + 1);
-  const long v = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-  if (v >= Vc) return;
-  const int ix = static_cast<int>(v / (dim_c + 1)), iy = static_cast<int>(v % (dim_c + 1));
-  const long vf = static_cast<long>(2 * ix) * (2 * dim_c + 1) + 2 * iy;
-  cc[2 * v] = cf[2 * vf];
-  cc[2 * v + 1] = cf[2 * vf + 1];
-}
-
-// parent of every fine element and the 4 children of every coarse element.
-// Coarse lower (cx,cy) holds fine lower (0,0),(1,0),(0,1) and upper (0,0) of
-// its 2x2 block; coarse upper holds fine lower (1,1) and upper (1,0),(0,1),(1,1).
-__global__ void k_fk_parent(int dim_f, long Kp_c, int* __restrict__ parent, int* __restrict__ slots,
-                            int* __restrict__ children) {
-  const long Kf = 2L * dim_f * dim_f;
+// Parent of every owned fine element and the 4 children of every owned
+// coarse element, in strip-local numbering (fine strip [2a, 2b) of FK(dim_f)
+// over coarse strip [a, b)).  Coarse lower (cx,cy) holds fine lower
+// (0,0),(1,0),(0,1) and upper (0,0) of its 2x2 block; coarse upper holds fine
+// lower (1,1) and upper (1,0),(0,1),(1,1).
+__global__ void k_fk_parent(int dim_f, int a_c, int w_c, long Kp_c, int* __restrict__ parent,
+                            int* __restrict__ slots, int* __restrict__ children) {
+  const int w_f = 2 * w_c, a_f = 2 * a_c, dim_c = dim_f / 2;
+  const long Kf = 2L * w_f * dim_f;
   const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   if (k >= Kf) return;
-  const int dim_c = dim_f / 2;
-  const bool lower = k < static_cast<long>(dim_f) * dim_f;
-  const long q = lower ? k : k - static_cast<long>(dim_f) * dim_f;
-  const int ix = static_cast<int>(q / dim_f), iy = static_cast<int>(q % dim_f);
+  const bool lower = k < static_cast<long>(w_f) * dim_f;
+  const long q = lower ? k : k - static_cast<long>(w_f) * dim_f;
+  const int ix = a_f + static_cast<int>(q / dim_f), iy = static_cast<int>(q % dim_f);
   const int cx = ix >> 1, cy = iy >> 1, lx = ix & 1, ly = iy & 1;
   bool clower;
   int slot;
@@ -76,7 +67,7 @@ __global__ void k_fk_parent(int dim_f, long Kp_c, int* __restrict__ parent, int*
     clower = !lx && !ly;
     slot = clower ? 3 : (lx && !ly ? 1 : (!lx && ly ? 2 : 3));
   }
-  const int kc = clower ? cx * dim_c + cy : dim_c * dim_c + cx * dim_c + cy;
+  const int kc = (clower ? 0 : w_c * dim_c) + (cx - a_c) * dim_c + cy;
   parent[k] = kc;
   slots[k] = slot;
   children[slot * Kp_c + kc] = static_cast<int>(k);
@@ -182,74 +173,35 @@ __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf,
   xf[i * Kpf + k] += acc;
 }
 
-Handle* level_at(Handle& h, int l) { return l == 0 ? &h : h.coarse[l - 1].get(); }
-
-// r = b - A x  (A the level's Schur operator; E read from the FP32 copy when
-// the smoother runs in mixed precision — vectors and arithmetic stay FP64)
-void residual(Handle& L, bool f32, double wm, double dt, const double* b, const double* x, double* r) {
-  launch_stage1(L, nullptr, 0.0, x, 1.0, L.tz.ptr);
-  if (f32)
-    launch_stage2_f32(L, x, -wm, -dt * L.prob.eta, L.tz.ptr, -dt, b, 1.0, r);
-  else
-    launch_stage2(L, x, -wm, -dt * L.prob.eta, L.tz.ptr, -dt, b, 1.0, r);
-}
-
-void bjac_axpy(Handle& L, bool f32, const double* x, double omega, double beta, double* y) {
-  if (f32)
-    launch_bjac_axpy_f32(L, x, omega, beta, y);
-  else
-    launch_bjac_axpy(L, x, omega, beta, y);
-}
-
-void smooth_once(Handle& L, bool f32, double wm, double dt, const double* b, double* x) {
-  residual(L, f32, wm, dt, b, x, L.mg_r.ptr);
-  bjac_axpy(L, f32, L.mg_r.ptr, kOmega, 1.0, x);
-}
-
-void vcycle(Handle& h, int l, double wm, double dt, const double* b, double* x) {
-  Handle& L = *level_at(h, l);
-  const bool f32 = h.mg_f32;
-  const int last = static_cast<int>(h.coarse.size());
-  bjac_axpy(L, f32, b, kOmega, 0.0, x);  // first sweep from x = 0
-  if (l == last) {
-    for (int s = 1; s < kCoarseSweeps; ++s) smooth_once(L, f32, wm, dt, b, x);
-    return;
-  }
-  for (int s = 1; s < kPre; ++s) smooth_once(L, f32, wm, dt, b, x);
-  residual(L, f32, wm, dt, b, x, L.mg_r.ptr);
-  Handle& C = *level_at(h, l + 1);
-  const int P = h.p;
-#define CALL(PP)                                                                                               \
-  k_restrict<PP><<<grid_of(static_cast<long>(h.N) * C.K, 256), 256, 0, h.stream>>>(                          \
-      C.K, C.Kp, L.Kp, C.mg_children.ptr, C.mg_P.ptr, L.mg_r.ptr, C.mg_b.ptr)
-  LDG_DISPATCH_P(P, CALL)
-#undef CALL
-  LDG_CUDA(cudaGetLastError());
-  ++L.launches;
-  vcycle(h, l + 1, wm, dt, C.mg_b.ptr, C.mg_x.ptr);
-#define CALL(PP)                                                                                                \
-  k_prolong_add<PP><<<grid_of(4L * h.N * C.K, 256), 256, 0, h.stream>>>(C.K, C.Kp, L.Kp, C.mg_children.ptr,    \
-                                                                        C.mg_P.ptr, C.mg_x.ptr, x)
-  LDG_DISPATCH_P(P, CALL)
-#undef CALL
-  LDG_CUDA(cudaGetLastError());
-  ++L.launches;
-  for (int s = 0; s < kPost; ++s) smooth_once(L, f32, wm, dt, b, x);
-}
-
 }  // namespace
 
 int mg_levels(const Handle& h) { return 1 + static_cast<int>(h.coarse.size()); }
 
-bool mg_build(Handle& h) {
+// Number of coarse levels for FK(dim) split into `size` equal strips: halve
+// while dim stays even, the coarse mesh keeps dim >= 2, and every rank keeps
+// at least one whole column with even strip boundaries.  Every rank computes
+// the same count, so the distributed V-cycle stays in lockstep.
+int mg_depth(int dim, int size) {
+  if (dim % size != 0) return 0;
+  int w = dim / size, d = dim, n = 0;
+  while (d % 2 == 0 && d / 2 >= 2 && w % 2 == 0) {
+    d /= 2;
+    w /= 2;
+    ++n;
+  }
+  return n;
+}
+
+bool mg_build(Handle& h, int team_size) {
   if (h.mg_ready) return true;
-  if (h.dim < 4 || (h.dim % 2) != 0 || h.size > 1) return false;
+  if (h.dim < 4 || h.dim_fine == 0) return false;
+  const int depth = mg_depth(h.dim, team_size);
+  if (depth < 1) return false;
   const long NN = static_cast<long>(h.N) * h.N;
   h.mg_r.alloc(h.vec_len(), &h.bytes);
   Handle* fine = &h;
-  int d = h.dim;
-  while (d % 2 == 0 && d / 2 >= 2) {
-    const int dc = d / 2;
+  for (int l = 0; l < depth; ++l) {
+    const int dc = fine->dim / 2;
     auto c = std::make_unique<Handle>();
     c->p = h.p;
     c->N = h.N;
@@ -259,15 +211,12 @@ bool mg_build(Handle& h) {
     c->owns_stream = false;
     c->rule_shared = h.rule_ptr();
     c->rule_shared_R = h.rule_R();
-    {
-      DBuf<double> cc;
-      const long Vc = static_cast<long>(dc + 1) * (dc + 1);
-      cc.alloc(2 * Vc, nullptr);
-      k_subsample<<<grid_of(Vc, 256), 256, 0, h.stream>>>(dc, fine->coords.ptr, cc.ptr);
-      LDG_CUDA(cudaGetLastError());
-      build_square_from_coords(*c, dc, cc.ptr);
-      LDG_CUDA(cudaStreamSynchronize(h.stream));
-    }
+    c->rank = h.rank;
+    c->size = h.size;
+    // coarse vertices are the finest mesh's vertices (stride 2^l): jittered
+    // meshes coarsen consistently on every rank
+    build_square_strip(*c, dc, fine->strip_a / 2, fine->strip_b / 2, fine->stride * 2, h.dim_fine, h.jitter,
+                       h.seed);
     const long n = c->vec_len();
     c->D.alloc(n, &c->bytes);
     c->E.alloc(8 * NN * c->Kp, &c->bytes);
@@ -281,8 +230,8 @@ bool mg_build(Handle& h) {
     DBuf<int> slots;
     slots.alloc(fine->Kp, nullptr);
     c->mg_P.alloc(4 * NN * c->Kp, &c->bytes);
-    k_fk_parent<<<grid_of(fine->K, 256), 256, 0, h.stream>>>(d, c->Kp, fine->mg_parent.ptr, slots.ptr,
-                                                             c->mg_children.ptr);
+    k_fk_parent<<<grid_of(fine->K, 256), 256, 0, h.stream>>>(fine->dim, c->strip_a, c->strip_w(), c->Kp,
+                                                             fine->mg_parent.ptr, slots.ptr, c->mg_children.ptr);
     LDG_CUDA(cudaGetLastError());
 #define CALL(PP)                                                                                              \
   k_prolong_blocks<PP><<<grid_of(fine->K, 128), 128, 0, h.stream>>>(fine->mesh(), c->mesh(), h.dtab,         \
@@ -290,22 +239,21 @@ bool mg_build(Handle& h) {
     LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
     LDG_CUDA(cudaGetLastError());
+    LDG_CUDA(cudaStreamSynchronize(h.stream));
     fine = c.get();
     h.coarse.push_back(std::move(c));
-    d = dc;
   }
-  LDG_CUDA(cudaStreamSynchronize(h.stream));
-  h.mg_ready = !h.coarse.empty();
-  return h.mg_ready;
+  h.mg_ready = true;
+  return true;
 }
 
-// Per step: rediscretise every coarse level at time t (projection of d,
-// E^m assembly) and build the block-Jacobi inverses; in mixed precision the
-// smoother reads FP32 copies of E and of the inverses.  Level 0's FP64
-// block-Jacobi inverse is built by the caller.
-void mg_setup_step(Handle& h, double t, double wm, double dt) {
+// Per step: rediscretise every coarse level at time t (projection of d on
+// owned + ghost elements, E^m assembly) and build the block-Jacobi inverses;
+// in mixed precision the smoother reads FP32 copies of E and the inverses.
+// Level 0's FP64 block-Jacobi inverse is built by the caller.
+void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
   const long NN = static_cast<long>(h.N) * h.N;
-  if (h.mg_f32) {
+  if (f32) {
     if (!h.E32.ptr) {
       h.E32.alloc(8 * NN * h.Kp, &h.bytes);
       h.Pinv32.alloc(NN * h.Kp, &h.bytes);
@@ -315,9 +263,9 @@ void mg_setup_step(Handle& h, double t, double wm, double dt) {
   }
   for (auto& cp : h.coarse) {
     Handle& c = *cp;
-    launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.K);
+    launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);
     launch_assemble(c, kModeE, c.E.ptr);
-    if (h.mg_f32) {
+    if (f32) {
       if (!c.E32.ptr) {
         c.E32.alloc(8 * NN * c.Kp, &c.bytes);
         c.Pinv32.alloc(NN * c.Kp, &c.bytes);
@@ -330,49 +278,26 @@ void mg_setup_step(Handle& h, double t, double wm, double dt) {
   }
 }
 
-// The V-cycle is a fixed sequence of ~14 kernels per level with no host
-// synchronisation, so it is captured once per (b, x, wm, dt) into a CUDA
-// graph and replayed: launch latency, not bandwidth, bounds the small coarse
-// levels.  Operator contents (E, block-Jacobi inverses) change every step
-// in place; the graph only bakes pointers and the scalars wm, dt.
-void mg_vcycle(Handle& h, double wm, double dt, const double* b, double* x) {
-  for (auto& g : h.vgraphs)
-    if (g.b == b && g.x == x && g.wm == wm && g.dt == dt) {
-      LDG_CUDA(cudaGraphLaunch(g.exec, h.stream));
-      h.launches += g.kernels;
-      return;
-    }
-  if (h.vgraphs.size() >= 8) {
-    for (auto& g : h.vgraphs) cudaGraphExecDestroy(g.exec);
-    h.vgraphs.clear();
-  }
-  auto count = [&h] {
-    int64_t n = h.launches;
-    for (auto& c : h.coarse) n += c->launches;
-    return n;
-  };
-  const int64_t before = count();
-  cudaGraph_t graph = nullptr;
-  LDG_CUDA(cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal));
-  try {
-    vcycle(h, 0, wm, dt, b, x);
-  } catch (...) {
-    cudaStreamEndCapture(h.stream, &graph);
-    if (graph) cudaGraphDestroy(graph);
-    throw;
-  }
-  LDG_CUDA(cudaStreamEndCapture(h.stream, &graph));
-  Handle::VGraph g;
-  g.b = b;
-  g.x = x;
-  g.wm = wm;
-  g.dt = dt;
-  g.kernels = count() - before;
-  const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
-  cudaGraphDestroy(graph);
-  LDG_CUDA(e);
-  h.vgraphs.push_back(g);
-  LDG_CUDA(cudaGraphLaunch(g.exec, h.stream));
+// C.mg_b = P^T L.mg_r (restriction of the fine residual to the coarse level)
+void mg_restrict(Handle& L, Handle& C) {
+#define CALL(PP)                                                                                             \
+  k_restrict<PP><<<grid_of(static_cast<long>(L.N) * C.K, 256), 256, 0, L.stream>>>(                        \
+      C.K, C.Kp, L.Kp, C.mg_children.ptr, C.mg_P.ptr, L.mg_r.ptr, C.mg_b.ptr)
+  LDG_DISPATCH_P(L.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++L.launches;
+}
+
+// x += P C.mg_x (prolongation of the coarse correction)
+void mg_prolong_add(Handle& L, Handle& C, double* x) {
+#define CALL(PP)                                                                                              \
+  k_prolong_add<PP><<<grid_of(4L * L.N * C.K, 256), 256, 0, L.stream>>>(C.K, C.Kp, L.Kp, C.mg_children.ptr,  \
+                                                                        C.mg_P.ptr, C.mg_x.ptr, x)
+  LDG_DISPATCH_P(L.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++L.launches;
 }
 
 void mg_release(Handle& h) {

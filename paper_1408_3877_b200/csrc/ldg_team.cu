@@ -1,0 +1,506 @@
+// K7 driver: the implicit-Euler solve of one step over a Team of ranks
+// (one rank on one GPU, strips over several GPUs with NCCL, or several
+// virtual ranks on one GPU for validating the decomposition).
+//
+// The reference factorises W + dt A with SparseLU every step and checks
+// ||lhs y - rhs|| / max(||rhs||, 1) <= 1e-10 (system.hpp:155-205).  Here the
+// flux rows are eliminated exactly — their diagonal blocks are the block-
+// diagonal mass matrix, Z^m = M^-1 (V_Z^m - B^m C) — and BiCGStab runs on the
+// Schur system of the primary variable,
+//     S_c C = [wM + dt(eta S - sum_m E^m M^-1 B^m)] C
+//           = wM C^n + dt (V_C - sum_m E^m M^-1 V_Z^m),
+// applied in two block-SpMV passes (stage 1: t^m = M^-1 B^m x, stage 2:
+// y = wMx + dt(eta S x - sum_m E^m t^m)), preconditioned by a geometric
+// multigrid V-cycle (ldg_mg.cu builds the levels).  The reference residual
+// contract is checked on the full 3KN system afterwards.
+//
+// Exchange points: before stage 1 the ghost column of x, before
+// stage 2 the ghost column of t^1, t^2 (and of Y before the full apply);
+// every reduction is a sum over local ranks then one ncclAllReduce.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "ldg_internal.hpp"
+
+namespace ldgb {
+
+size_t reduction_scratch();
+void launch_dots_async(Handle& h, int nd, const double* const* xs, const double* const* ys);
+double* dots_result(Handle& h);
+
+namespace {
+
+constexpr double kOmega = 0.7;   // damped block-Jacobi smoother
+constexpr int kPre = 2;          // pre-smoothing sweeps (the first from x = 0 is residual-free)
+constexpr int kPost = 2;         // post-smoothing sweeps (V(2,1) measured slower: +20-40% iterations)
+constexpr int kCoarseSweeps = 2;
+
+#define LDG_NCCL(call)                                                                          \
+  do {                                                                                          \
+    ncclResult_t r_ = (call);                                                                   \
+    if (r_ != ncclSuccess) throw Error(LDG_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+Handle& level_of(Handle& h, int l) { return l == 0 ? h : *h.coarse[l - 1]; }
+
+// named per-rank vectors: a Team operation names a vector, each rank
+// resolves it to its own buffer
+enum Vec : int {
+  kR, kRh, kP, kV, kS, kT, kPh, kSh, kB, kC, kY, kTz, kMgX, kMgB, kMgR, kVz, kVc, kFullR, kFullY, kCold, kYold, kNone
+};
+
+double* vp(Handle& h, Vec v) {
+  const long n = h.vec_len();
+  switch (v) {
+    case kR: return h.kr_r.ptr;
+    case kRh: return h.kr_rh.ptr;
+    case kP: return h.kr_p.ptr;
+    case kV: return h.kr_v.ptr;
+    case kS: return h.kr_s.ptr;
+    case kT: return h.kr_t.ptr;
+    case kPh: return h.kr_ph.ptr;
+    case kSh: return h.kr_sh.ptr;
+    case kB: return h.kr_b.ptr;
+    case kC: return h.Y.ptr + 2 * n;
+    case kY: return h.Y.ptr;
+    case kTz: return h.tz.ptr;
+    case kMgX: return h.mg_x.ptr;
+    case kMgB: return h.mg_b.ptr;
+    case kMgR: return h.mg_r.ptr;
+    case kVz: return h.Vv.ptr;
+    case kVc: return h.Vv.ptr + 2 * n;
+    case kFullR: return h.full_r.ptr;
+    case kFullY: return h.full_y.ptr;
+    case kCold: return h.Yold.ptr + 2 * n;
+    case kYold: return h.Yold.ptr;
+    default: return nullptr;
+  }
+}
+
+// ---------------------------------------------------------------- exchange
+
+void copy_cols(double* dst, long dpitch, const double* src, long spitch, long width, long rows, cudaStream_t s) {
+  LDG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * dpitch, src, sizeof(double) * spitch, sizeof(double) * width,
+                             rows, cudaMemcpyDeviceToDevice, s));
+}
+
+// Refreshes the ghost columns of vector v (ncomp blocks of N planes) on
+// level `level` of every local rank.
+void halo(Team& T, int level, Vec v, int ncomp) {
+  if (T.size == 1) return;
+  bool remote = false;
+  for (int r = 0; r < T.nlocal(); ++r) {
+    Handle& L = level_of(*T.ranks[r], level);
+    const int g = T.first + r;
+    const long rows = static_cast<long>(ncomp) * L.N;
+    if (L.ghost_left) {
+      if (Handle* nb = T.local(g - 1)) {
+        Handle& R = level_of(*nb, level);
+        copy_cols(vp(L, v) + L.ghost_left_off(), L.Kp, vp(R, v) + R.own_right_off(), R.Kp, L.dim, rows, T.stream);
+      } else {
+        remote = true;
+      }
+    }
+    if (L.ghost_right) {
+      if (Handle* nb = T.local(g + 1)) {
+        Handle& R = level_of(*nb, level);
+        copy_cols(vp(L, v) + L.ghost_right_off(), L.Kp, vp(R, v) + R.own_left_off(), R.Kp, L.dim, rows, T.stream);
+      } else {
+        remote = true;
+      }
+    }
+  }
+  if (!remote) return;
+  // remote neighbours: pack the owned boundary columns, exchange, unpack
+  auto* comm = static_cast<ncclComm_t>(T.nccl);
+  if (!comm) throw Error(LDG_ENCCL, "ranks without a communicator");
+  for (int r = 0; r < T.nlocal(); ++r) {
+    Handle& L = level_of(*T.ranks[r], level);
+    const int g = T.first + r;
+    const long rows = static_cast<long>(ncomp) * L.N;
+    const long cnt = rows * L.dim;
+    const bool left = L.ghost_left && !T.local(g - 1), right = L.ghost_right && !T.local(g + 1);
+    if (static_cast<long>(T.send_l.n) < cnt) {
+      for (DBuf<double>* b : {&T.send_l, &T.send_r, &T.recv_l, &T.recv_r}) b->alloc(cnt, nullptr);
+    }
+    if (left) copy_cols(T.send_l.ptr, L.dim, vp(L, v) + L.own_left_off(), L.Kp, L.dim, rows, T.stream);
+    if (right) copy_cols(T.send_r.ptr, L.dim, vp(L, v) + L.own_right_off(), L.Kp, L.dim, rows, T.stream);
+    LDG_NCCL(ncclGroupStart());
+    if (left) {
+      LDG_NCCL(ncclSend(T.send_l.ptr, cnt, ncclDouble, g - 1, comm, T.stream));
+      LDG_NCCL(ncclRecv(T.recv_l.ptr, cnt, ncclDouble, g - 1, comm, T.stream));
+    }
+    if (right) {
+      LDG_NCCL(ncclSend(T.send_r.ptr, cnt, ncclDouble, g + 1, comm, T.stream));
+      LDG_NCCL(ncclRecv(T.recv_r.ptr, cnt, ncclDouble, g + 1, comm, T.stream));
+    }
+    LDG_NCCL(ncclGroupEnd());
+    if (left) copy_cols(vp(L, v) + L.ghost_left_off(), L.Kp, T.recv_l.ptr, L.dim, L.dim, rows, T.stream);
+    if (right) copy_cols(vp(L, v) + L.ghost_right_off(), L.Kp, T.recv_r.ptr, L.dim, L.dim, rows, T.stream);
+  }
+}
+
+// Launches per-rank partial dots (launch(h) issues launch_dots_async), then
+// sums over local ranks in a fixed order (deterministic) and across
+// processes with one ncclAllReduce.
+template <typename F>
+void reduce_dots(Team& T, int nd, F launch, double* out) {
+  for (auto& rp : T.ranks) launch(*rp);
+  if (T.nlocal() == 1 && T.size == 1) {
+    LDG_CUDA(cudaMemcpyAsync(T.red_host, dots_result(T.h0()), sizeof(double) * nd, cudaMemcpyDeviceToHost, T.stream));
+  } else {
+    for (int r = 0; r < T.nlocal(); ++r)
+      LDG_CUDA(cudaMemcpyAsync(T.red_all.ptr + 4 * r, dots_result(*T.ranks[r]), sizeof(double) * nd,
+                               cudaMemcpyDeviceToDevice, T.stream));
+    LDG_CUDA(cudaMemcpyAsync(T.red_host + 8, T.red_all.ptr, sizeof(double) * 4 * T.nlocal(), cudaMemcpyDeviceToHost,
+                             T.stream));
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+    for (int d = 0; d < nd; ++d) {
+      double s = 0.0;
+      for (int r = 0; r < T.nlocal(); ++r) s += T.red_host[8 + 4 * r + d];
+      T.red_host[d] = s;
+    }
+    if (T.nccl && T.size > T.nlocal()) {
+      LDG_CUDA(cudaMemcpyAsync(T.red_all.ptr, T.red_host, sizeof(double) * nd, cudaMemcpyHostToDevice, T.stream));
+      LDG_NCCL(ncclAllReduce(T.red_all.ptr, T.red_all.ptr, nd, ncclDouble, ncclSum,
+                             static_cast<ncclComm_t>(T.nccl), T.stream));
+      LDG_CUDA(cudaMemcpyAsync(T.red_host, T.red_all.ptr, sizeof(double) * nd, cudaMemcpyDeviceToHost, T.stream));
+    }
+  }
+  LDG_CUDA(cudaStreamSynchronize(T.stream));
+  for (int d = 0; d < nd; ++d) out[d] = T.red_host[d];
+}
+
+// Sum over all ranks of nd dot products of level-0 vectors (owned entries).
+void dots(Team& T, int nd, const Vec* xs, const Vec* ys, double* out) {
+  reduce_dots(
+      T, nd,
+      [&](Handle& h) {
+        const double* px[4];
+        const double* py[4];
+        for (int d = 0; d < nd; ++d) {
+          px[d] = vp(h, xs[d]);
+          py[d] = vp(h, ys[d]);
+        }
+        launch_dots_async(h, nd, px, py);
+      },
+      out);
+}
+
+// squared 2-norm of a 3-block (Z1, Z2, C) vector
+double sq_norm3(Team& T, Vec v) {
+  double s[3];
+  reduce_dots(
+      T, 3,
+      [&](Handle& h) {
+        const long n = h.vec_len();
+        const double* p[3] = {vp(h, v), vp(h, v) + n, vp(h, v) + 2 * n};
+        launch_dots_async(h, 3, p, p);
+      },
+      s);
+  return s[0] + s[1] + s[2];
+}
+
+double norm(Team& T, Vec x) {
+  double r;
+  dots(T, 1, &x, &x, &r);
+  return std::sqrt(r);
+}
+
+template <typename F>
+void each(Team& T, int level, F f) {
+  for (auto& rp : T.ranks) f(level_of(*rp, level));
+}
+
+// ---------------------------------------------------------------- operators
+
+// y = a1 (wM x) + b1 dt eta S x - g1 dt sum E^m t^m(x) + d1 w   (tz = M^-1 B x computed here)
+void schur_like(Team& T, int level, bool f32, Vec x, double alpha, double beta, double gamma, Vec w, double delta,
+                Vec y) {
+  halo(T, level, x, 1);
+  each(T, level, [&](Handle& L) { launch_stage1(L, nullptr, 0.0, vp(L, x), 1.0, L.tz.ptr); });
+  halo(T, level, kTz, 2);
+  each(T, level, [&](Handle& L) {
+    if (f32)
+      launch_stage2_f32(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y));
+    else
+      launch_stage2(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y));
+  });
+}
+
+void schur_apply(Team& T, double wm, double dt, Vec x, Vec y) {
+  schur_like(T, 0, false, x, wm, dt * T.h0().prob.eta, dt, kNone, 0.0, y);
+}
+
+// r = b - A x on a multigrid level
+void residual(Team& T, int level, bool f32, double wm, double dt, Vec b, Vec x, Vec r) {
+  schur_like(T, level, f32, x, -wm, -dt * T.h0().prob.eta, -dt, b, 1.0, r);
+}
+
+void bjac_axpy(Handle& L, bool f32, const double* x, double omega, double beta, double* y) {
+  if (f32)
+    launch_bjac_axpy_f32(L, x, omega, beta, y);
+  else
+    launch_bjac_axpy(L, x, omega, beta, y);
+}
+
+void smooth(Team& T, int level, bool f32, double wm, double dt, Vec b, Vec x) {
+  residual(T, level, f32, wm, dt, b, x, kMgR);
+  each(T, level, [&](Handle& L) { bjac_axpy(L, f32, L.mg_r.ptr, kOmega, 1.0, vp(L, x)); });
+}
+
+int levels(Team& T) { return 1 + static_cast<int>(T.h0().coarse.size()); }
+
+void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
+  each(T, l, [&](Handle& L) { bjac_axpy(L, f32, vp(L, b), kOmega, 0.0, vp(L, x)); });  // first sweep, x = 0
+  if (l == levels(T) - 1) {
+    // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
+    // (every rank keeps a column), so a larger coarsest grid gets more sweeps
+    const int sweeps = std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim);
+    for (int s = 1; s < sweeps; ++s) smooth(T, l, f32, wm, dt, b, x);
+    return;
+  }
+  for (int s = 1; s < kPre; ++s) smooth(T, l, f32, wm, dt, b, x);
+  residual(T, l, f32, wm, dt, b, x, kMgR);
+  for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
+  vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
+  for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
+  for (int s = 0; s < kPost; ++s) smooth(T, l, f32, wm, dt, b, x);
+}
+
+int64_t team_launches(Team& T) {
+  int64_t n = 0;
+  for (auto& rp : T.ranks) {
+    n += rp->launches;
+    for (auto& c : rp->coarse) n += c->launches;
+  }
+  return n;
+}
+
+// The V-cycle is a fixed sequence of kernels, copies and (multi-GPU) NCCL
+// halo calls with no host synchronisation: captured once per (b, x, wm, dt)
+// into a CUDA graph and replayed.  Operator contents change every step in
+// place; the graph only bakes pointers and the scalars.
+void precond_mg(Team& T, bool f32, double wm, double dt, Vec b, Vec x) {
+  Handle& h = T.h0();
+  for (auto& g : h.vgraphs)
+    if (g.b == vp(h, b) && g.x == vp(h, x) && g.wm == wm && g.dt == dt && (g.kernels < 0) == f32) {
+      LDG_CUDA(cudaGraphLaunch(g.exec, T.stream));
+      h.launches += g.kernels < 0 ? -g.kernels : g.kernels;
+      return;
+    }
+  if (h.vgraphs.size() >= 8) mg_release(h);
+  const int64_t before = team_launches(T);
+  cudaGraph_t graph = nullptr;
+  LDG_CUDA(cudaStreamBeginCapture(T.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    vcycle(T, 0, f32, wm, dt, b, x);
+  } catch (...) {
+    cudaStreamEndCapture(T.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  LDG_CUDA(cudaStreamEndCapture(T.stream, &graph));
+  Handle::VGraph g;
+  g.b = vp(h, b);
+  g.x = vp(h, x);
+  g.wm = wm;
+  g.dt = dt;
+  const int64_t k = team_launches(T) - before;
+  g.kernels = f32 ? -k : k;  // sign tags the precision variant
+  const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  LDG_CUDA(e);
+  h.vgraphs.push_back(g);
+  LDG_CUDA(cudaGraphLaunch(g.exec, T.stream));
+}
+
+void precond(Team& T, int pc, bool f32, double wm, double dt, Vec b, Vec x) {
+  if (pc == 2) return precond_mg(T, f32, wm, dt, b, x);
+  each(T, 0, [&](Handle& h) {
+    if (pc == 1)
+      launch_bjac_apply(h, vp(h, b), vp(h, x));
+    else
+      LDG_CUDA(cudaMemcpyAsync(vp(h, x), vp(h, b), sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice, T.stream));
+  });
+}
+
+void lincomb(Team& T, double a, Vec x, double b, Vec y, double c, Vec z, Vec out) {
+  each(T, 0, [&](Handle& h) {
+    launch_lincomb3(h, h.vec_len(), a, vp(h, x), b, y == kNone ? nullptr : vp(h, y), c,
+                    z == kNone ? nullptr : vp(h, z), vp(h, out));
+  });
+}
+
+}  // namespace
+
+void team_assemble(Team& T, double t) {
+  for (auto& rp : T.ranks) assemble_step(*rp, t);
+}
+
+// One linear solve with the operators of the last team_assemble: wm = 1, dt
+// for W + dt A (euler_step), wm = 0, dt = 1 for A (solve_stationary).
+// Y holds the previous state on entry and the solution on exit.
+int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st) {
+  Handle& h0 = T.h0();
+  each(T, 0, [&](Handle& h) {
+    const long n = h.vec_len();
+    LDG_CUDA(cudaMemcpyAsync(h.Yold.ptr, h.Y.ptr, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, T.stream));
+    // Schur right-hand side b = wm M C^n + dt (V_C - sum E^m M^-1 V_Z^m): t = M^-1 V_Z (local)
+    launch_stage1(h, h.Vv.ptr, 1.0, nullptr, 0.0, h.tz.ptr);
+  });
+  halo(T, 0, kTz, 2);
+  each(T, 0, [&](Handle& h) {
+    const long n = h.vec_len();
+    launch_stage2(h, wm != 0.0 ? vp(h, kCold) : nullptr, wm, 0.0, h.tz.ptr, dt, vp(h, kVc), dt, h.kr_b.ptr);
+    // full right-hand side of the reference system: r = W Y^n + dt V
+    launch_lincomb3(h, 3 * n, dt, h.Vv.ptr, 0.0, nullptr, 0.0, nullptr, h.full_r.ptr);
+    if (wm != 0.0) launch_stage2(h, vp(h, kCold), wm, 0.0, nullptr, 0.0, vp(h, kVc), dt, h.full_r.ptr + 2 * n);
+  });
+  const double rhs_norm = std::sqrt(sq_norm3(T, kFullR));
+  const double contract = o.contract_tol > 0.0 ? o.contract_tol : 1e-10;
+
+  // precond: 0 none, 1 block-Jacobi, 2 multigrid with the smoother on FP32
+  // copies of E / block inverses (mixed precision), 3 multigrid all-FP64
+  int pc = o.precond;
+  if (pc >= 2) {
+    bool ok = true;
+    for (auto& rp : T.ranks) ok = mg_build(*rp, T.size) && ok;
+    if (!ok) pc = 1;  // no FK hierarchy (general mesh): block-Jacobi
+  }
+  const bool f32 = pc == 2;
+  if (pc >= 1) each(T, 0, [&](Handle& h) { launch_bjac_setup(h, wm, dt); });
+  if (pc >= 2) {
+    for (auto& rp : T.ranks) mg_setup_step(*rp, rp->t_assembled, wm, dt, f32);
+    pc = 2;
+  }
+
+  const double bnorm = norm(T, kB);
+  // stopping test on the Schur residual: the user's rtol/atol, tightened so
+  // that the full-system contract (Schur residual = C-row residual) holds
+  double tol = std::max(o.rtol * bnorm, o.atol);
+  if (o.check_residual) {
+    const double tc = 0.25 * contract * std::max(rhs_norm, 1.0);
+    tol = tol > 0.0 ? std::min(tol, tc) : tc;
+  }
+  if (!(tol > 0.0)) tol = 1e-300;
+
+  // BiCGStab (right preconditioned), x = C warm-started from C^n
+  int applies = 0;
+  schur_apply(T, wm, dt, kC, kR);
+  ++applies;
+  lincomb(T, 1.0, kB, -1.0, kR, 0.0, kNone, kR);  // r = b - A x
+  each(T, 0, [&](Handle& h) {
+    const long n = h.vec_len();
+    LDG_CUDA(cudaMemcpyAsync(h.kr_rh.ptr, h.kr_r.ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, T.stream));
+    LDG_CUDA(cudaMemsetAsync(h.kr_p.ptr, 0, sizeof(double) * n, T.stream));
+    LDG_CUDA(cudaMemsetAsync(h.kr_v.ptr, 0, sizeof(double) * n, T.stream));
+  });
+  double rho = 1.0, alpha = 1.0, omega = 1.0;
+  // three host synchronisations per iteration: (rh,v); (t,s),(t,t),(s,s); (r,r),(rh,r)
+  double rr_rhr[2];
+  {
+    const Vec xs[2] = {kR, kRh}, ys[2] = {kR, kR};
+    dots(T, 2, xs, ys, rr_rhr);
+  }
+  double rnorm = std::sqrt(rr_rhr[0]);
+  double rho1 = rr_rhr[1];
+  int it = 0;
+  bool converged = rnorm <= tol;
+  while (!converged && it < o.maxit) {
+    ++it;
+    if (rho1 == 0.0 || !std::isfinite(rho1)) {
+      // breakdown: restart with the current residual as shadow vector
+      each(T, 0, [&](Handle& h) {
+        const long n = h.vec_len();
+        LDG_CUDA(cudaMemcpyAsync(h.kr_rh.ptr, h.kr_r.ptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, T.stream));
+        LDG_CUDA(cudaMemsetAsync(h.kr_p.ptr, 0, sizeof(double) * n, T.stream));
+        LDG_CUDA(cudaMemsetAsync(h.kr_v.ptr, 0, sizeof(double) * n, T.stream));
+      });
+      rho = alpha = omega = 1.0;
+      rho1 = rnorm * rnorm;
+      if (rho1 == 0.0) break;
+    }
+    const double beta = (rho1 / rho) * (alpha / omega);
+    lincomb(T, 1.0, kR, beta, kP, -beta * omega, kV, kP);  // p = r + beta (p - omega v)
+    precond(T, pc, f32, wm, dt, kP, kPh);
+    schur_apply(T, wm, dt, kPh, kV);
+    ++applies;
+    double rv;
+    {
+      const Vec xs[1] = {kRh}, ys[1] = {kV};
+      dots(T, 1, xs, ys, &rv);
+    }
+    alpha = rho1 / rv;
+    lincomb(T, 1.0, kR, -alpha, kV, 0.0, kNone, kS);  // s = r - alpha v
+    precond(T, pc, f32, wm, dt, kS, kSh);
+    schur_apply(T, wm, dt, kSh, kT);
+    ++applies;
+    double ts[3];
+    {
+      const Vec xs[3] = {kT, kT, kS}, ys[3] = {kS, kT, kS};
+      dots(T, 3, xs, ys, ts);
+    }
+    if (std::sqrt(ts[2]) <= tol) {  // converged on s: x += alpha p^
+      lincomb(T, 1.0, kC, alpha, kPh, 0.0, kNone, kC);
+      rnorm = std::sqrt(ts[2]);
+      converged = true;
+      break;
+    }
+    omega = ts[1] != 0.0 ? ts[0] / ts[1] : 0.0;
+    lincomb(T, 1.0, kC, alpha, kPh, omega, kSh, kC);  // x += alpha p^ + omega s^
+    lincomb(T, 1.0, kS, -omega, kT, 0.0, kNone, kR);  // r = s - omega t
+    {
+      const Vec xs[2] = {kR, kRh}, ys[2] = {kR, kR};
+      dots(T, 2, xs, ys, rr_rhr);
+    }
+    rnorm = std::sqrt(rr_rhr[0]);
+    rho = rho1;
+    rho1 = rr_rhr[1];
+    if (!std::isfinite(rnorm)) break;
+    converged = rnorm <= tol;
+    if (omega == 0.0) break;
+  }
+
+  // flux recovery Z^m = M^-1 (V_Z^m - B^m C), written into Y[0 .. 2n)
+  halo(T, 0, kC, 1);
+  each(T, 0, [&](Handle& h) { launch_stage1(h, h.Vv.ptr, 1.0, vp(h, kC), -1.0, h.Y.ptr); });
+
+  // reference residual contract on the full system (system.hpp:198-203)
+  halo(T, 0, kY, 3);
+  each(T, 0, [&](Handle& h) {
+    const long n3 = 3 * h.vec_len();
+    launch_full_apply(h, h.Y.ptr, wm, dt, h.full_y.ptr);
+    launch_lincomb3(h, n3, 1.0, h.full_y.ptr, -1.0, h.full_r.ptr, 0.0, nullptr, h.full_y.ptr);
+  });
+  const double res = std::sqrt(sq_norm3(T, kFullY)) / std::max(rhs_norm, 1.0);
+  if (st) {
+    st->iterations += it;
+    st->applies += applies;
+    st->schur_relres = bnorm > 0.0 ? rnorm / bnorm : rnorm;
+    st->residual = res;
+  }
+  if (o.check_residual && !(res <= contract)) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "linear solve residual %.6e exceeds tolerance (eta = %f, p = %d; BiCGStab %d iterations, "
+             "Schur residual %.3e)",
+             res, h0.prob.eta, h0.p, it, rnorm);
+    throw Error(LDG_ENOCONV, buf);
+  }
+  return it;
+}
+
+// (W + dt A) Y on the team's current state buffers (used by exports/tests)
+void team_full_apply(Team& T, double wm, double dt) {
+  halo(T, 0, kY, 3);
+  each(T, 0, [&](Handle& h) { launch_full_apply(h, h.Y.ptr, wm, dt, h.full_y.ptr); });
+}
+
+// Schur operator apply on level-0 buffers C -> kr_v (kernel timing)
+void team_schur_apply_c(Team& T, double wm, double dt) { schur_apply(T, wm, dt, kC, kV); }
+
+}  // namespace ldgb

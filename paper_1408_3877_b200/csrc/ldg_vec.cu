@@ -1,0 +1,198 @@
+// K7 vector kernels of the Krylov solve: fused linear combinations,
+// deterministic dot-product reductions (fixed grid, fixed order; owned
+// entries only, so strip ghosts never count twice), layout conversion
+// between the element-interleaved device vectors and the reference's
+// k-major host vectors, and the per-rank assembly step.
+#include <cmath>
+#include <vector>
+
+#include "ldg_internal.hpp"
+
+namespace ldgb {
+
+namespace {
+
+inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+__global__ void k_lincomb3(long n, double a, const double* x, double b, const double* y, double c, const double* z,
+                           double* out) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    double v = a * x[i];
+    if (y) v += b * y[i];
+    if (z) v += c * z[i];
+    out[i] = v;
+  }
+}
+
+__global__ void k_axpby(long n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    y[i] = a * x[i] + b * y[i];
+}
+
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs
+constexpr int kMaxDots = 4;
+
+struct DotArgs {
+  const double* x[kMaxDots];
+  const double* y[kMaxDots];
+};
+
+// Deterministic two-pass reduction: fixed grid, fixed per-block order.
+__global__ void __launch_bounds__(256) k_dots_partial(long n, int nd, DotArgs a, double* __restrict__ part) {
+  double s[kMaxDots] = {0.0, 0.0, 0.0, 0.0};
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    for (int d = 0; d < nd; ++d) s[d] += a.x[d][i] * a.y[d][i];
+  __shared__ double sh[kMaxDots][8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int d = 0; d < nd; ++d) {
+    double v = s[d];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[d][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nd) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += sh[threadIdx.x][w];
+    part[threadIdx.x * kRedBlocks + blockIdx.x] = v;
+  }
+}
+
+// dots over planes j < N, elements k < K of vectors laid out [j][Kp]
+__global__ void __launch_bounds__(256) k_dots_owned(int N, long Kp, int K, int nd, DotArgs a,
+                                                    double* __restrict__ part) {
+  double s[kMaxDots] = {0.0, 0.0, 0.0, 0.0};
+  const long n = static_cast<long>(N) * K;
+  for (long q = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long i = (q / K) * Kp + q % K;
+    for (int d = 0; d < nd; ++d) s[d] += a.x[d][i] * a.y[d][i];
+  }
+  __shared__ double sh[kMaxDots][8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int d = 0; d < nd; ++d) {
+    double v = s[d];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[d][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nd) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += sh[threadIdx.x][w];
+    part[threadIdx.x * kRedBlocks + blockIdx.x] = v;
+  }
+}
+
+__global__ void k_dots_final(int nd, const double* __restrict__ part, double* __restrict__ out) {
+  const int d = threadIdx.x;
+  if (d >= nd) return;
+  double v = 0.0;
+  for (int b = 0; b < kRedBlocks; ++b) v += part[d * kRedBlocks + b];
+  out[d] = v;
+}
+
+// SoA [nvec][N][Kp] <-> k-major [nvec][K][N]
+__global__ void k_soa_to_kmajor(int K, int N, long Kp, int nvec, const double* __restrict__ soa,
+                                double* __restrict__ km) {
+  const long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  const long total = static_cast<long>(nvec) * K * N;
+  if (idx >= total) return;
+  const long v = idx / (static_cast<long>(K) * N);
+  const long r = idx % (static_cast<long>(K) * N);
+  const long k = r / N, j = r % N;
+  km[idx] = soa[(v * N + j) * Kp + k];
+}
+
+__global__ void k_kmajor_to_soa(int K, int N, long Kp, int nvec, const double* __restrict__ km,
+                                double* __restrict__ soa) {
+  const long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  const long total = static_cast<long>(nvec) * K * N;
+  if (idx >= total) return;
+  const long v = idx / (static_cast<long>(K) * N);
+  const long r = idx % (static_cast<long>(K) * N);
+  const long k = r / N, j = r % N;
+  soa[(v * N + j) * Kp + k] = km[idx];
+}
+
+#define LDG_DISPATCH_P(p, CALL) \
+  switch (p) {                  \
+    case 0: { CALL(0); break; } \
+    case 1: { CALL(1); break; } \
+    case 2: { CALL(2); break; } \
+    case 3: { CALL(3); break; } \
+    default: { CALL(4); break; } \
+  }
+
+}  // namespace
+void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
+                     const double* z, double* out) {
+  k_lincomb3<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, a, x, b, y, c, z, out);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_axpby(Handle& h, long n, double a, const double* x, double b, double* y) {
+  k_axpby<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, a, x, b, y);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_dots(Handle& h, long n, int nd, const double* const* xs, const double* const* ys, double* out_host) {
+  DotArgs a{};
+  for (int d = 0; d < nd; ++d) {
+    a.x[d] = xs[d];
+    a.y[d] = ys[d];
+  }
+  k_dots_partial<<<kRedBlocks, 256, 0, h.stream>>>(n, nd, a, h.red.ptr);
+  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxDots * kRedBlocks);
+  LDG_CUDA(cudaGetLastError());
+  h.launches += 2;
+  LDG_CUDA(cudaMemcpyAsync(h.red_host, h.red.ptr + kMaxDots * kRedBlocks, sizeof(double) * nd,
+                           cudaMemcpyDeviceToHost, h.stream));
+  LDG_CUDA(cudaStreamSynchronize(h.stream));
+  for (int d = 0; d < nd; ++d) out_host[d] = h.red_host[d];
+}
+
+void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* km) {
+  const long total = static_cast<long>(nvec) * h.K * h.N;
+  k_soa_to_kmajor<<<grid_of(total, 256), 256, 0, h.stream>>>(h.K, h.N, h.Kp, nvec, soa, km);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_kmajor_to_soa(Handle& h, const double* km, int nvec, double* soa) {
+  const long total = static_cast<long>(nvec) * h.K * h.N;
+  k_kmajor_to_soa<<<grid_of(total, 256), 256, 0, h.stream>>>(h.K, h.N, h.Kp, nvec, km, soa);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+size_t reduction_scratch() { return static_cast<size_t>(kMaxDots) * kRedBlocks + kMaxDots; }
+
+void assemble_step(Handle& h, double t) {
+  launch_project_df(h, t, h.rule_ptr(), h.rule_R());        // K2: d, f (system.hpp:112-113)
+  launch_rhs(h, t);                                          // K5: V (system.hpp:142-150)
+  launch_assemble(h, kModeE, h.E.ptr);                       // K3: E^m (system.hpp:115-117)
+  h.assembled = true;
+  h.t_assembled = t;
+}
+
+// Partial dots over the OWNED entries of N-plane vectors (ghost columns of
+// a strip are skipped); result left on the device at dots_result(h).
+void launch_dots_async(Handle& h, int nd, const double* const* xs, const double* const* ys) {
+  DotArgs a{};
+  for (int d = 0; d < nd; ++d) {
+    a.x[d] = xs[d];
+    a.y[d] = ys[d];
+  }
+  k_dots_owned<<<kRedBlocks, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nd, a, h.red.ptr);
+  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxDots * kRedBlocks);
+  LDG_CUDA(cudaGetLastError());
+  h.launches += 2;
+}
+
+double* dots_result(Handle& h) { return h.red.ptr + kMaxDots * kRedBlocks; }
+
+}  // namespace ldgb
