@@ -215,6 +215,9 @@ typedef struct ldg_kernel_times {
   double ms_spmv;       /* K6 full (W + dt A) block-SpMV                  */
   double ms_schur;      /* one Schur operator application (2 launches)     */
   int reps;
+  int levels;           /* multigrid levels timed below (0: no FK hierarchy) */
+  double ms_vcycle;     /* one preconditioner V-cycle (FP32 smoother), graph replay, L2 warm */
+  double ms_level[8];   /* one smoothing sweep (residual + block-Jacobi) on level l, graph replay */
 } ldg_kernel_times;
 
 /* Times each hot kernel over reps launches with CUDA events on the handle's

@@ -75,7 +75,8 @@ class _Info(C.Structure):
 
 class _Times(C.Structure):
     _fields_ = [("ms_project", C.c_double), ("ms_assemble", C.c_double), ("ms_spmv", C.c_double),
-                ("ms_schur", C.c_double), ("reps", C.c_int)]
+                ("ms_schur", C.c_double), ("reps", C.c_int), ("levels", C.c_int), ("ms_vcycle", C.c_double),
+                ("ms_level", C.c_double * 8)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -452,7 +453,9 @@ class LdgSystem:
         tm = _Times()
         self._check(load_library().ldg_time_kernels(self._h, float(t), float(dt), int(reps), int(flush),
                                                     C.byref(tm)))
-        return {k: getattr(tm, k) for k, _ in _Times._fields_}
+        out = {k: getattr(tm, k) for k, _ in _Times._fields_}
+        out["ms_level"] = list(tm.ms_level)[: tm.levels]
+        return out
 
     def sync(self):
         self._check(load_library().ldg_sync(self._h))

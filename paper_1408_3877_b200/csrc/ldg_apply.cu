@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "ldg_internal.hpp"
+#include "ldg_pack.cuh"
 
 namespace ldgb {
 
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(128) k_full(DevMesh m, DevTables T, const doub
 // E^m_kj M_j^-1 B^m_jk), inverted in shared memory (Gauss-Jordan, partial
 // pivoting).  A group of N^2 threads owns one element; the static blocks
 // B^m_jk are rebuilt from the reference tables (row j, the slot facing k).
-template <int P, typename TE, typename TO>
+template <int P, typename TE, typename TO, bool QUAD = false>
 __global__ void __launch_bounds__(256) k_bjac_setup(DevMesh m, DevTables T, const TE* __restrict__ E, double wm,
                                                     double dt, double eta, TO* __restrict__ Pinv) {
   constexpr int N = Cfg<P>::N, NN = N * N;
@@ -506,7 +507,13 @@ __global__ void __launch_bounds__(256) k_bjac_setup(DevMesh m, DevTables T, cons
     }
     __syncthreads();
   }
-  if (active) Pinv[static_cast<long>(lane) * Kp + k] = static_cast<TO>(s_I[grp][lane]);
+  if (active) {
+    if constexpr (QUAD) {  // packed float4 layout of the fused smoother (ldg_pack.cuh)
+      Pinv[sm_packed_p_index<P>(i, j, Kp, k)] = static_cast<TO>(s_I[grp][lane]);
+    } else {
+      Pinv[static_cast<long>(lane) * Kp + k] = static_cast<TO>(s_I[grp][lane]);
+    }
+  }
 }
 
 // y = beta y + omega P^-1 x  (beta = 0: plain block-Jacobi application)
@@ -614,14 +621,14 @@ void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double*
   ++h.launches;
 }
 
-template <typename TE, typename TO>
+template <typename TE, typename TO, bool QUAD = false>
 void bjac_setup_impl(Handle& h, const TE* E, double wm, double dt, TO* out) {
 #define CALL(P)                                                                                         \
   do {                                                                                                  \
     constexpr int NN = Cfg<P>::N * Cfg<P>::N;                                                           \
     constexpr int EPC = (256 / NN) > 0 ? (256 / NN) : 1;                                                \
-    k_bjac_setup<P, TE, TO><<<grid_of(h.K, EPC), 256, 0, h.stream>>>(h.mesh(), h.dtab, E, wm, dt,      \
-                                                                     h.prob.eta, out);                  \
+    k_bjac_setup<P, TE, TO, QUAD><<<grid_of(h.K, EPC), 256, 0, h.stream>>>(h.mesh(), h.dtab, E, wm, dt, \
+                                                                           h.prob.eta, out);            \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -634,6 +641,18 @@ void launch_bjac_setup(Handle& h, double wm, double dt) { bjac_setup_impl<double
 void launch_bjac_setup_f32(Handle& h, double wm, double dt) {
   bjac_setup_impl<float, float>(h, h.E32.ptr, wm, dt, h.Pinv32.ptr);
 }
+
+// FP32 inverses from the FP64 E of the level (multigrid smoother copies):
+// packed for the fused smoother kernels, plain SoA for the row kernels
+void launch_bjac_setup_quad(Handle& h, double wm, double dt) {
+  bjac_setup_impl<double, float, true>(h, h.E.ptr, wm, dt, reinterpret_cast<float*>(h.Pq.ptr));
+}
+
+void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt) {
+  bjac_setup_impl<double, float>(h, h.E.ptr, wm, dt, h.Pinv32.ptr);
+}
+
+bool level_uses_rows(const Handle& h) { return use_rows(h); }
 
 void launch_bjac_apply(Handle& h, const double* x, double* y) { launch_bjac_axpy(h, x, 1.0, 0.0, y); }
 

@@ -93,6 +93,19 @@ std::unique_ptr<Handle> make_rank(Team& T, int p, const ldg_problem* prob, int r
   h.dtab = ldgb::DevTables{h.tab.ptr, L.p, L.N, L.R, L.Qe, L.Qb, L.proj_phi, L.proj_w, L.proj_x, L.mhat,
                            L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe, L.pth, L.we, L.pb, L.sb, L.wb, L.total,
                            L.mono, L.NP, L.tH, L.tSd, L.tSo, L.tM, L.tMinv, L.tmH, L.tmSd, L.tmSo};
+  {
+    const ldgb::FTables F = ldgb::build_f32_tables(h.tables);
+    h.ftab.alloc(F.data.size(), &h.bytes);
+    LDG_CUDA(cudaMemcpy(h.ftab.ptr, F.data.data(), sizeof(float) * F.data.size(), cudaMemcpyHostToDevice));
+    h.dtab.fbase = h.ftab.ptr;
+    h.dtab.NF = F.NF;
+    h.dtab.fmH = F.fmH;
+    h.dtab.fmSd = F.fmSd;
+    h.dtab.fmSo = F.fmSo;
+    h.dtab.fM = F.fM;
+    h.dtab.fSd = F.fSd;
+    h.dtab.fSo = F.fSo;
+  }
   ldgb::upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
   return hp;
 }
@@ -763,6 +776,9 @@ int ldg_time_kernels(ldg_handle* H, double t, double dt, int reps, int flush, ld
     }
     out->ms_spmv = timed([&] { ldgb::team_full_apply(T, 1.0, dt); });
     out->ms_schur = timed([&] { ldgb::team_schur_apply_c(T, 1.0, dt); });
+    for (double& v : out->ms_level) v = 0.0;
+    out->ms_vcycle = 0.0;
+    out->levels = ldgb::team_time_mg(T, 1.0, dt, reps, &out->ms_vcycle, out->ms_level, 8);
   });
 }
 

@@ -41,6 +41,10 @@ struct DevTables {
   int NP;
   long tH, tSd, tSo, tM, tMinv;
   long tmH, tmSd, tmSo;
+  // FP32 smoother tables (FTables in ldg_tables.hpp), offsets in floats
+  const float* fbase;
+  int NF;
+  long fmH, fmSd, fmSo, fM, fSd, fSo;
 };
 
 struct DevMesh {

@@ -73,6 +73,7 @@ struct Handle {
 
   HostTables tables;
   DBuf<double> tab;
+  DBuf<float> ftab;      // FP32 smoother tables (build_f32_tables)
   DevTables dtab{};
 
   // mesh
@@ -121,7 +122,9 @@ struct Handle {
   DBuf<int> mg_children;                         // [4][Kp] children in the next finer level
   DBuf<double> mg_P;                             // [N*N][Kp] prolongation block of each element
   DBuf<double> mg_x, mg_b, mg_r;                 // V-cycle work vectors (N * Kp)
-  DBuf<float> E32, Pinv32;                       // FP32 copies read by the smoother
+  DBuf<float> E32, Pinv32;                       // FP32 copies read by the row-kernel smoother (small levels)
+  DBuf<float4> Eq, Pq;                           // packed FP32 copies read by the fused smoother (ldg_smooth.cu)
+  DBuf<double> mg_s;                             // V-cycle ping-pong partner of x (fused smoother)
   bool mg_f32 = true;                            // smoother on FP32 copies (precond 2) or FP64 (3)
   bool mg_ready = false;
   struct VGraph {                                // a captured V-cycle (CUDA graph)
@@ -220,6 +223,18 @@ void launch_stage2_f32(Handle& h, const double* x, double alpha_m, double beta_s
 void launch_bjac_setup_f32(Handle& h, double wm, double dt);
 void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_to_f32(Handle& h, long n, const double* src, float* dst);
+void launch_bjac_setup_quad(Handle& h, double wm, double dt);        // Pq from E (FP64)
+void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt);  // Pinv32 from E (FP64)
+bool level_uses_rows(const Handle& h);
+
+// fused mixed-precision smoother (ldg_smooth.cu)
+long packed_p_quads(int p);                                           // float4 quads of one packed P^-1 block
+void smooth_pack_e(Handle& h);                                        // Eq from E
+void smooth_stage1(Handle& h, const double* x);                       // tz = M^-1 B x (FP32 arithmetic)
+// mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)
+void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
+                   double* out);
+void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 
 // row-parallel operator kernels (ldg_rows.cu), used by the launchers above
 void rows_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);
@@ -240,6 +255,7 @@ void team_assemble(Team& T, double t);
 int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st);
 void team_full_apply(Team& T, double wm, double dt);        // full_y = (W + dt A) Y, halos refreshed
 void team_schur_apply_c(Team& T, double wm, double dt);     // kr_v = S_c C (kernel timing)
+int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, double* ms_level, int max_levels);
 
 // multigrid (ldg_mg.cu)
 int mg_depth(int dim, int team_size);

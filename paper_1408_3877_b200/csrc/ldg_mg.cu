@@ -27,11 +27,6 @@ struct Cfg {
   static constexpr int N = (P + 1) * (P + 2) / 2;
 };
 
-constexpr double kOmega = 0.7;
-constexpr int kPre = 2;   // pre-smoothing sweeps (the first one from x = 0 is residual-free)
-constexpr int kPost = 2;  // post-smoothing sweeps (V(2,1) measured slower overall: +20-40% iterations)
-constexpr int kCoarseSweeps = 2;
-
 inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
 
 #define LDG_DISPATCH_P(p, CALL) \
@@ -199,6 +194,7 @@ bool mg_build(Handle& h, int team_size) {
   if (depth < 1) return false;
   const long NN = static_cast<long>(h.N) * h.N;
   h.mg_r.alloc(h.vec_len(), &h.bytes);
+  h.mg_s.alloc(h.vec_len(), &h.bytes);
   Handle* fine = &h;
   for (int l = 0; l < depth; ++l) {
     const int dc = fine->dim / 2;
@@ -225,6 +221,7 @@ bool mg_build(Handle& h, int team_size) {
     c->mg_x.alloc(n, &c->bytes);
     c->mg_b.alloc(n, &c->bytes);
     c->mg_r.alloc(n, &c->bytes);
+    c->mg_s.alloc(n, &c->bytes);
     c->mg_children.alloc(4 * c->Kp, &c->bytes);
     fine->mg_parent.alloc(fine->Kp, &fine->bytes);
     DBuf<int> slots;
@@ -248,33 +245,37 @@ bool mg_build(Handle& h, int team_size) {
 }
 
 // Per step: rediscretise every coarse level at time t (projection of d on
-// owned + ghost elements, E^m assembly) and build the block-Jacobi inverses;
-// in mixed precision the smoother reads FP32 copies of E and the inverses.
-// Level 0's FP64 block-Jacobi inverse is built by the caller.
-void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
-  const long NN = static_cast<long>(h.N) * h.N;
-  if (f32) {
-    if (!h.E32.ptr) {
-      h.E32.alloc(8 * NN * h.Kp, &h.bytes);
-      h.Pinv32.alloc(NN * h.Kp, &h.bytes);
+// owned + ghost elements, E^m assembly) and build the block-Jacobi inverses.
+// Mixed precision (f32): every level gets FP32 copies of E and of the
+// inverses (built from the FP64 E) — packed float4 for the levels the fused
+// smoother runs on, plain SoA for the small levels on the row kernels.
+// All-FP64 (precond 3): level 0's inverse is built by the caller.
+void mg_setup_f32_level(Handle& L, double wm, double dt) {
+  const long NN = static_cast<long>(L.N) * L.N;
+  if (!level_uses_rows(L)) {
+    if (!L.Pq.ptr) L.Pq.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
+    smooth_pack_e(L);
+    launch_bjac_setup_quad(L, wm, dt);
+  } else {
+    if (!L.E32.ptr) {
+      L.E32.alloc(8 * NN * L.Kp, &L.bytes);
+      L.Pinv32.alloc(NN * L.Kp, &L.bytes);
     }
-    launch_to_f32(h, 8 * NN * h.Kp, h.E.ptr, h.E32.ptr);
-    launch_to_f32(h, NN * h.Kp, h.Pinv.ptr, h.Pinv32.ptr);
+    launch_to_f32(L, 8 * NN * L.Kp, L.E.ptr, L.E32.ptr);
+    launch_bjac_setup_f32_from64(L, wm, dt);
   }
+}
+
+void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
+  if (f32) mg_setup_f32_level(h, wm, dt);
   for (auto& cp : h.coarse) {
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);
     launch_assemble(c, kModeE, c.E.ptr);
-    if (f32) {
-      if (!c.E32.ptr) {
-        c.E32.alloc(8 * NN * c.Kp, &c.bytes);
-        c.Pinv32.alloc(NN * c.Kp, &c.bytes);
-      }
-      launch_to_f32(c, 8 * NN * c.Kp, c.E.ptr, c.E32.ptr);
-      launch_bjac_setup_f32(c, wm, dt);
-    } else {
+    if (f32)
+      mg_setup_f32_level(c, wm, dt);
+    else
       launch_bjac_setup(c, wm, dt);
-    }
   }
 }
 

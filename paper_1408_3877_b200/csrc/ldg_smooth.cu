@@ -1,0 +1,432 @@
+// Mixed-precision multigrid smoother kernels (the preconditioner's hot path).
+//
+// The V-cycle spends most of each implicit-Euler step in three operations per
+// smoothing sweep on the large levels: t^m = M^-1 B^m x (stage 1), the
+// residual r = b - S_c x (stage 2) and the damped block-Jacobi update
+// x += omega P^-1 r.  Here they run in FP32 arithmetic on FP32 operator
+// copies; vectors stay FP64 and the outer Krylov operator is untouched, so
+// only the preconditioner's contraction depends on the rounding.
+//
+//  * Stored blocks are packed per element and streamed as float4: Eq[c][q][k]
+//    holds values 4q..4q+3 of component c's four blocks in (slot, column, row)
+//    order, so a warp moves 512 contiguous bytes per load instruction and the
+//    quarter as many load instructions as the FP32 scalar layout issues.
+//    P^-1 is packed the same way (column-major, NN rounded up to 4).
+//  * Stage 2 and the block-Jacobi update are one kernel: the residual of the
+//    element never leaves registers (ping-pong x_in -> x_out, since stage 2
+//    reads the neighbours' x).
+//  * The reference tables live in shared memory as FP32 rows of NF = N
+//    rounded to 4 (one 128-bit broadcast load per 4 entries).
+//
+// Reference operators restated (as in ldg_apply.cu): B^m = -H^m + Q^m + Q_N^m
+// (assembly.hpp:92-109, 174-208), S + S_D (assembly.hpp:142-168), M = 2|T| mhat.
+#include <cmath>
+
+#include "ldg_internal.hpp"
+#include "ldg_pack.cuh"
+
+namespace ldgb {
+
+namespace {
+
+template <int P>
+using Cfg = SmCfg<P>;
+
+inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+#define LDG_DISPATCH_P(p, CALL) \
+  switch (p) {                  \
+    case 0: { CALL(0); break; } \
+    case 1: { CALL(1); break; } \
+    case 2: { CALL(2); break; } \
+    case 3: { CALL(3); break; } \
+    default: { CALL(4); break; } \
+  }
+
+__device__ __forceinline__ float comp(const float4& v, int r) {
+  return r == 0 ? v.x : (r == 1 ? v.y : (r == 2 ? v.z : v.w));
+}
+
+// copies `count` floats of the FP32 tables into shared memory
+__device__ __forceinline__ const float* stage_f(float* sm, const float* src, int count) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(sm);
+  for (int i = threadIdx.x; i < count / 4; i += blockDim.x) d4[i] = s4[i];
+  __syncthreads();
+  return sm;
+}
+
+// w = T x, T^t rows of NF floats in shared memory
+template <int N, int NF>
+__device__ __forceinline__ void ftab_mv(const float* sT, const float* x, float* w) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float4* row = reinterpret_cast<const float4*>(sT + j * NF);
+#pragma unroll
+    for (int q = 0; q < NF / 4; ++q) {
+      const float4 t = row[q];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (4 * q + r < N) w[4 * q + r] = fmaf(comp(t, r), x[j], w[4 * q + r]);
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, int col, float* v) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = static_cast<float>(x[j * Kp + col]);
+}
+
+// tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
+template <int P>
+__global__ void __launch_bounds__(128) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
+                                             double* __restrict__ tout) {
+  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
+  extern __shared__ __align__(16) float smf[];
+  const float* tb = stage_f(smf, T.fbase + T.fmH, 14 * TAB);  // tmH 2 | tmSd 3 | tmSo 9
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m.K) return;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  float xv[N], w[N], u1[N], u2[N];
+  load_f<N>(x, Kp, k, xv);
+  const float b11 = static_cast<float>(g[kB11 * Kp + k]), b12 = static_cast<float>(g[kB12 * Kp + k]);
+  const float b21 = static_cast<float>(g[kB21 * Kp + k]), b22 = static_cast<float>(g[kB22 * Kp + k]);
+  ftab_mv<N, NF>(tb, xv, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    u1[i] = -b22 * w[i];
+    u2[i] = b12 * w[i];
+  }
+  ftab_mv<N, NF>(tb + TAB, xv, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    u1[i] = fmaf(b21, w[i], u1[i]);
+    u2[i] = fmaf(-b11, w[i], u2[i]);
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kind = m.kind[n * Kp + k];
+    const double len = g[(kLen0 + n) * Kp + k];
+    const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
+    if (f == 0.0) continue;
+    ftab_mv<N, NF>(tb + (2 + n) * TAB, xv, w);
+    const float c1 = static_cast<float>(f * g[(kNux0 + n) * Kp + k]);
+    const float c2 = static_cast<float>(f * g[(kNuy0 + n) * Kp + k]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fmaf(c1, w[i], u1[i]);
+      u2[i] = fmaf(c2, w[i], u2[i]);
+    }
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kp = m.nbr[n * Kp + k];
+    if (kp < 0) continue;
+    float xn[N];
+    load_f<N>(x, Kp, kp, xn);
+    ftab_mv<N, NF>(tb + (5 + n * 3 + m.nbrn[n * Kp + k]) * TAB, xn, w);
+    const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+    const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
+    const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fmaf(c1, w[i], u1[i]);
+      u2[i] = fmaf(c2, w[i], u2[i]);
+    }
+  }
+  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    tout[i * Kp + k] = static_cast<double>(inv2a * u1[i]);
+    tout[(N + i) * Kp + k] = static_cast<double>(inv2a * u2[i]);
+  }
+}
+
+// acc[i] += sum_j blk[i][j] v[j] over one column group: quad q of the group
+// holds values u = 4q..4q+3, u = jj*N + i, column j0 + jj
+template <int N, int QC>
+__device__ __forceinline__ void group_mv(const float4* __restrict__ g, long Kp, const float* v, float* acc) {
+  float4 e[QC];
+#pragma unroll
+  for (int q = 0; q < QC; ++q) e[q] = __ldcs(g + q * Kp);
+#pragma unroll
+  for (int q = 0; q < QC; ++q)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int u = 4 * q + r;
+      acc[u % N] = fmaf(comp(e[q], r), v[u / N], acc[u % N]);
+    }
+}
+
+// acc += sum_s E^m[s] t^m_col(s) for component c (E packed, t FP64 planes)
+template <int P>
+__device__ __forceinline__ void e_component(const float4* __restrict__ Ec, const double* __restrict__ tc, long Kp,
+                                            int k, const int* __restrict__ nbr, float* acc) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN;
+  if constexpr (C::kFlat) {
+    float t[4][N];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int col = s == 0 ? k : nbr[(s - 1) * Kp + k];
+#pragma unroll
+      for (int j = 0; j < N; ++j) t[s][j] = col >= 0 ? static_cast<float>(tc[j * Kp + col]) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < NN; ++q) {
+      const float4 e = __ldcs(Ec + q * Kp);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int v = 4 * q + r, s = v / NN, rem = v % NN;
+        acc[rem % N] = fmaf(comp(e, r), t[s][rem / N], acc[rem % N]);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int s = 0; s < 4; ++s) {
+      const int col = s == 0 ? k : nbr[(s - 1) * Kp + k];
+      if (col < 0) continue;
+      const float4* Es = Ec + static_cast<long>(s) * C::QS * Kp;
+      const double* tcol = tc + col;
+#pragma unroll(C::UNR)
+      for (int ch = 0; ch < C::NCH; ++ch) {
+        float v[C::CC];
+#pragma unroll
+        for (int jj = 0; jj < C::CC; ++jj) {
+          const int j = ch * C::CC + jj;
+          v[jj] = (C::NCOL == N || j < N) ? static_cast<float>(tcol[j * Kp]) : 0.f;
+        }
+        group_mv<N, C::QC>(Es + static_cast<long>(ch) * C::QC * Kp, Kp, v, acc);
+      }
+    }
+  }
+}
+
+// d = P^-1 r, r from `load(j)` (FP32 value of column j)
+template <int P, typename F>
+__device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long Kp, F load, float* d) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN;
+#pragma unroll
+  for (int i = 0; i < N; ++i) d[i] = 0.f;
+  if constexpr (C::kFlat) {
+    float r[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) r[j] = load(j);
+#pragma unroll
+    for (int q = 0; q < C::QP; ++q) {
+      const float4 e = __ldcs(Pk + q * Kp);
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int v = 4 * q + rr;
+        if (v < NN) d[v % N] = fmaf(comp(e, rr), r[v / N], d[v % N]);
+      }
+    }
+  } else {
+#pragma unroll(C::UNR)
+    for (int ch = 0; ch < C::NCH; ++ch) {
+      float v[C::CC];
+#pragma unroll
+      for (int jj = 0; jj < C::CC; ++jj) {
+        const int j = ch * C::CC + jj;
+        v[jj] = (C::NCOL == N || j < N) ? load(j) : 0.f;
+      }
+      group_mv<N, C::QC>(Pk + static_cast<long>(ch) * C::QC * Kp, Kp, v, d);
+    }
+  }
+}
+
+// r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
+//   MODE 0: out = r
+//   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
+template <int P, int MODE>
+__global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const float4* __restrict__ Eq,
+                                             const double* __restrict__ x, const double* __restrict__ tz,
+                                             const double* __restrict__ b, double wm, double dteta, double dt,
+                                             const float4* __restrict__ Pq, float omega, double* __restrict__ out) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NF = C::NF, TAB = N * NF;
+  extern __shared__ __align__(16) float smf[];
+  const float* tb = stage_f(smf, T.fbase + T.fM, 13 * TAB);  // tM | tSd 3 | tSo 9
+  __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m.K) return;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  float acc[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c)
+    e_component<P>(Eq + static_cast<long>(c) * C::QE * Kp + k, tz + static_cast<long>(c) * N * Kp, Kp, k, m.nbr,
+                   acc);
+  const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] *= fdt;
+  {
+    float xv[N], w[N];
+    load_f<N>(x, Kp, k, xv);
+    ftab_mv<N, NF>(tb, xv, w);
+    const float sm = static_cast<float>(-wm * 2.0 * g[kArea * Kp + k]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fmaf(sm, w[i], acc[i]);
+#pragma unroll 1
+    for (int n = 0; n < 3; ++n) {
+      const int kind = m.kind[n * Kp + k];
+      if (kind != kInterior && kind != kDirichlet) continue;
+      ftab_mv<N, NF>(tb + (1 + n) * TAB, xv, w);
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fmaf(-fdteta, w[i], acc[i]);
+    }
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kp = m.nbr[n * Kp + k];
+    if (kp < 0) continue;
+    float xn[N], w[N];
+    load_f<N>(x, Kp, kp, xn);
+    ftab_mv<N, NF>(tb + (4 + n * 3 + m.nbrn[n * Kp + k]) * TAB, xn, w);
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fmaf(fdteta, w[i], acc[i]);
+  }
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i * Kp + k] = b[i * Kp + k] + static_cast<double>(acc[i]);
+  } else {
+    float d[N];
+    if constexpr (C::kFlat) {
+      pinv_apply<P>(Pq + k, Kp,
+                    [&](int j) { return static_cast<float>(b[j * Kp + k] + static_cast<double>(acc[j])); }, d);
+    } else {
+      const int tid = threadIdx.x;
+#pragma unroll
+      for (int i = 0; i < N; ++i) s_r[i][tid] = static_cast<float>(b[i * Kp + k] + static_cast<double>(acc[i]));
+      pinv_apply<P>(Pq + k, Kp, [&](int j) { return s_r[j][tid]; }, d);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      out[i * Kp + k] = fma(static_cast<double>(omega), static_cast<double>(d[i]), x[i * Kp + k]);
+  }
+}
+
+// out = omega P^-1 b  (the first sweep from x = 0)
+template <int P>
+__global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const float4* __restrict__ Pq,
+                                             const double* __restrict__ b, float omega, double* __restrict__ out) {
+  constexpr int N = Cfg<P>::N;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  float d[N];
+  pinv_apply<P>(Pq + k, Kp, [&](int j) { return static_cast<float>(b[j * Kp + k]); }, d);
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[i * Kp + k] = static_cast<double>(omega * d[i]);
+}
+
+// Eq[c][q][k] from E[(c*4 + s)*NN + i*N + j][k] (FP64, row-major blocks);
+// one thread per output quad, zero in the padding columns
+template <int P>
+__global__ void k_pack_e(long Kp, const double* __restrict__ E, float4* __restrict__ Eq) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN;
+  const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (t >= 2L * C::QE * Kp) return;
+  const long k = t % Kp;
+  const int cq = static_cast<int>(t / Kp);
+  const int c = cq / C::QE, q = cq % C::QE;
+  float v[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int s, i, j;
+    if (C::kFlat) {
+      const int val = 4 * q + r, rem = val % NN;
+      s = val / NN;
+      j = rem / N;
+      i = rem % N;
+    } else {
+      s = q / C::QS;
+      const int rq = q % C::QS, ch = rq / C::QC, u = (rq % C::QC) * 4 + r;
+      j = ch * C::CC + u / N;
+      i = u % N;
+    }
+    v[r] = j < N ? static_cast<float>(E[(static_cast<long>(c * 4 + s) * NN + i * N + j) * Kp + k]) : 0.f;
+  }
+  Eq[t] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+template <int P>
+size_t s1_smem() {
+  return sizeof(float) * 14 * Cfg<P>::N * Cfg<P>::NF;
+}
+template <int P>
+size_t s2_smem() {
+  return sizeof(float) * 13 * Cfg<P>::N * Cfg<P>::NF;
+}
+
+}  // namespace
+
+long packed_p_quads(int p) {
+  switch (p) {
+    case 0: return Cfg<0>::QP;
+    case 1: return Cfg<1>::QP;
+    case 2: return Cfg<2>::QP;
+    case 3: return Cfg<3>::QP;
+    default: return Cfg<4>::QP;
+  }
+}
+
+void smooth_pack_e(Handle& h) {
+#define CALL(P)                                                                                            \
+  do {                                                                                                     \
+    const long nq = 2L * Cfg<P>::QE * h.Kp;                                                                \
+    if (!h.Eq.ptr) h.Eq.alloc(nq, &h.bytes);                                                               \
+    k_pack_e<P><<<grid_of(nq, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr, h.Eq.ptr);                          \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void smooth_stage1(Handle& h, const double* x) {
+#define CALL(P)                                                                            \
+  k_s1f<P><<<grid_of(h.K, 128), 128, s1_smem<P>(), h.stream>>>(h.mesh(), h.dtab, x, h.tz.ptr)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
+                   double* out) {
+  const double dteta = dt * h.prob.eta;
+#define CALL(P)                                                                                                   \
+  do {                                                                                                            \
+    if (mode == 0)                                                                                                \
+      k_s2f<P, 0><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.Eq.ptr, x, h.tz.ptr,  \
+                                                                       b, wm, dteta, dt, h.Pq.ptr,               \
+                                                                       static_cast<float>(omega), out);          \
+    else                                                                                                          \
+      k_s2f<P, 1><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.Eq.ptr, x, h.tz.ptr,  \
+                                                                       b, wm, dteta, dt, h.Pq.ptr,               \
+                                                                       static_cast<float>(omega), out);          \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void smooth_zero(Handle& h, const double* b, double omega, double* out) {
+#define CALL(P)                                                                                        \
+  k_bjf<P><<<grid_of(h.K, 128), 128, 0, h.stream>>>(h.K, h.Kp, h.Pq.ptr, b, static_cast<float>(omega), out)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+}  // namespace ldgb

@@ -424,4 +424,33 @@ HostTables build_tables(int p) {
   return ht;
 }
 
+FTables build_f32_tables(const HostTables& ht) {
+  const TableLayout& L = ht.lay;
+  const int N = L.N, NP = L.NP;
+  FTables f;
+  f.NF = (N + 3) / 4 * 4;
+  const long tab = static_cast<long>(N) * f.NF;
+  f.fmH = 0;
+  f.fmSd = f.fmH + 2 * tab;
+  f.fmSo = f.fmSd + 3 * tab;
+  f.fM = f.fmSo + 9 * tab;
+  f.fSd = f.fM + tab;
+  f.fSo = f.fSd + 3 * tab;
+  f.total = f.fSo + 9 * tab;
+  f.data.assign(f.total, 0.0f);
+  auto copy = [&](long dst, long src, int count) {  // count tables, NP -> NF row padding
+    for (int t = 0; t < count; ++t)
+      for (int j = 0; j < N; ++j)
+        for (int i = 0; i < N; ++i)
+          f.data[dst + t * tab + j * f.NF + i] = static_cast<float>(ht.data[src + (static_cast<long>(t) * N + j) * NP + i]);
+  };
+  copy(f.fmH, L.tmH, 2);
+  copy(f.fmSd, L.tmSd, 3);
+  copy(f.fmSo, L.tmSo, 9);
+  copy(f.fM, L.tM, 1);
+  copy(f.fSd, L.tSd, 3);
+  copy(f.fSo, L.tSo, 9);
+  return f;
+}
+
 }  // namespace ldgb

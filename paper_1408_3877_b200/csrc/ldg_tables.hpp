@@ -74,4 +74,16 @@ struct HostTables {
 
 HostTables build_tables(int p);
 
+// FP32 copies of the transposed static tables for the mixed-precision
+// multigrid smoother (ldg_smooth.cu), rows padded to NF = N rounded up to 4
+// (one 128-bit shared load per 4 entries), T^t[j][i] at j*NF + i:
+//   [tmH 2 | tmSd 3 | tmSo 9]  stage 1 (m_hat^-1 applied)
+//   [tM 1 | tSd 3 | tSo 9]     stage 2
+struct FTables {
+  int NF = 0;
+  long fmH = 0, fmSd = 0, fmSo = 0, fM = 0, fSd = 0, fSo = 0, total = 0;
+  std::vector<float> data;
+};
+FTables build_f32_tables(const HostTables& ht);
+
 }  // namespace ldgb

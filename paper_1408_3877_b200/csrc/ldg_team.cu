@@ -49,7 +49,8 @@ Handle& level_of(Handle& h, int l) { return l == 0 ? h : *h.coarse[l - 1]; }
 // named per-rank vectors: a Team operation names a vector, each rank
 // resolves it to its own buffer
 enum Vec : int {
-  kR, kRh, kP, kV, kS, kT, kPh, kSh, kB, kC, kY, kTz, kMgX, kMgB, kMgR, kVz, kVc, kFullR, kFullY, kCold, kYold, kNone
+  kR, kRh, kP, kV, kS, kT, kPh, kSh, kB, kC, kY, kTz, kMgX, kMgB, kMgR, kMgS, kVz, kVc, kFullR, kFullY, kCold, kYold,
+  kNone
 };
 
 double* vp(Handle& h, Vec v) {
@@ -70,6 +71,7 @@ double* vp(Handle& h, Vec v) {
     case kMgX: return h.mg_x.ptr;
     case kMgB: return h.mg_b.ptr;
     case kMgR: return h.mg_r.ptr;
+    case kMgS: return h.mg_s.ptr;
     case kVz: return h.Vv.ptr;
     case kVc: return h.Vv.ptr + 2 * n;
     case kFullR: return h.full_r.ptr;
@@ -254,13 +256,58 @@ void smooth(Team& T, int level, bool f32, double wm, double dt, Vec b, Vec x) {
 
 int levels(Team& T) { return 1 + static_cast<int>(T.h0().coarse.size()); }
 
+// Levels large enough for the thread-per-element kernels run the fused
+// mixed-precision smoother (ldg_smooth.cu): one stage-1 and one stage-2 +
+// block-Jacobi launch per sweep, x ping-ponging between two buffers.
+bool fused(Team& T, int l, bool f32) { return f32 && !level_uses_rows(level_of(T.h0(), l)); }
+
+// r = b - S_c x (fused levels)
+void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
+  halo(T, l, x, 1);
+  each(T, l, [&](Handle& L) { smooth_stage1(L, vp(L, x)); });
+  halo(T, l, kTz, 2);
+  each(T, l, [&](Handle& L) { smooth_stage2(L, 0, vp(L, x), vp(L, b), wm, dt, kOmega, vp(L, r)); });
+}
+
+// xo = xi + omega P^-1 (b - S_c xi) (fused levels)
+void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo) {
+  halo(T, l, xi, 1);
+  each(T, l, [&](Handle& L) { smooth_stage1(L, vp(L, xi)); });
+  halo(T, l, kTz, 2);
+  each(T, l, [&](Handle& L) { smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, kOmega, vp(L, xo)); });
+}
+
+// One V-cycle on level l: x = V(b).  Fused levels alternate x with the
+// level's scratch vector; the first (residual-free) sweep writes whichever
+// buffer makes the last sweep land in x.
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
+  const bool coarsest = l == levels(T) - 1;
+  // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
+  // (every rank keeps a column), so a larger coarsest grid gets more sweeps
+  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (kPre - 1) + kPost;
+  if (fused(T, l, f32)) {
+    Vec cur = (sweeps % 2) ? kMgS : x;
+    auto other = [&](Vec v) { return v == x ? kMgS : x; };
+    each(T, l, [&](Handle& L) { smooth_zero(L, vp(L, b), kOmega, vp(L, cur)); });
+    const int pre = coarsest ? sweeps : kPre - 1;
+    for (int s = 0; s < pre; ++s) {
+      sweep_f(T, l, wm, dt, b, cur, other(cur));
+      cur = other(cur);
+    }
+    if (coarsest) return;
+    residual_f(T, l, wm, dt, b, cur, kMgR);
+    for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
+    vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
+    for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
+    for (int s = 0; s < kPost; ++s) {
+      sweep_f(T, l, wm, dt, b, cur, other(cur));
+      cur = other(cur);
+    }
+    return;
+  }
   each(T, l, [&](Handle& L) { bjac_axpy(L, f32, vp(L, b), kOmega, 0.0, vp(L, x)); });  // first sweep, x = 0
-  if (l == levels(T) - 1) {
-    // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
-    // (every rank keeps a column), so a larger coarsest grid gets more sweeps
-    const int sweeps = std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim);
-    for (int s = 1; s < sweeps; ++s) smooth(T, l, f32, wm, dt, b, x);
+  if (coarsest) {
+    for (int s = 0; s < sweeps; ++s) smooth(T, l, f32, wm, dt, b, x);
     return;
   }
   for (int s = 1; s < kPre; ++s) smooth(T, l, f32, wm, dt, b, x);
@@ -328,6 +375,24 @@ void precond(Team& T, int pc, bool f32, double wm, double dt, Vec b, Vec x) {
   });
 }
 
+// precond: 0 none, 1 block-Jacobi, 2 multigrid with the smoother on FP32
+// copies of E / block inverses (mixed precision), 3 multigrid all-FP64.
+// Returns the preconditioner that runs (2 = multigrid, f32 tells which).
+int prepare_precond(Team& T, int pc, double wm, double dt, bool* f32) {
+  if (pc >= 2) {
+    bool ok = true;
+    for (auto& rp : T.ranks) ok = mg_build(*rp, T.size) && ok;
+    if (!ok) pc = 1;  // no FK hierarchy (general mesh): block-Jacobi
+  }
+  *f32 = pc == 2;
+  if (pc == 1 || pc == 3) each(T, 0, [&](Handle& h) { launch_bjac_setup(h, wm, dt); });
+  if (pc >= 2) {
+    for (auto& rp : T.ranks) mg_setup_step(*rp, rp->t_assembled, wm, dt, *f32);
+    pc = 2;
+  }
+  return pc;
+}
+
 void lincomb(Team& T, double a, Vec x, double b, Vec y, double c, Vec z, Vec out) {
   each(T, 0, [&](Handle& h) {
     launch_lincomb3(h, h.vec_len(), a, vp(h, x), b, y == kNone ? nullptr : vp(h, y), c,
@@ -363,20 +428,8 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   const double rhs_norm = std::sqrt(sq_norm3(T, kFullR));
   const double contract = o.contract_tol > 0.0 ? o.contract_tol : 1e-10;
 
-  // precond: 0 none, 1 block-Jacobi, 2 multigrid with the smoother on FP32
-  // copies of E / block inverses (mixed precision), 3 multigrid all-FP64
-  int pc = o.precond;
-  if (pc >= 2) {
-    bool ok = true;
-    for (auto& rp : T.ranks) ok = mg_build(*rp, T.size) && ok;
-    if (!ok) pc = 1;  // no FK hierarchy (general mesh): block-Jacobi
-  }
-  const bool f32 = pc == 2;
-  if (pc >= 1) each(T, 0, [&](Handle& h) { launch_bjac_setup(h, wm, dt); });
-  if (pc >= 2) {
-    for (auto& rp : T.ranks) mg_setup_step(*rp, rp->t_assembled, wm, dt, f32);
-    pc = 2;
-  }
+  bool f32 = false;
+  const int pc = prepare_precond(T, o.precond, wm, dt, &f32);
 
   const double bnorm = norm(T, kB);
   // stopping test on the Schur residual: the user's rtol/atol, tightened so
@@ -502,5 +555,44 @@ void team_full_apply(Team& T, double wm, double dt) {
 
 // Schur operator apply on level-0 buffers C -> kr_v (kernel timing)
 void team_schur_apply_c(Team& T, double wm, double dt) { schur_apply(T, wm, dt, kC, kV); }
+
+// Multigrid cost breakdown (kernel timing): one V-cycle of the FP32-smoother
+// preconditioner and one smoothing sweep (residual + block-Jacobi) per level,
+// each captured in a graph of `reps` repetitions and replayed once after a
+// warm-up replay, so the figures carry the same launch gaps as the solve.
+int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, double* ms_level, int max_levels) {
+  bool f32 = false;
+  if (prepare_precond(T, 2, wm, dt, &f32) != 2) return 0;
+  Handle& h = T.h0();
+  const int nl = levels(T);
+  auto graph_time = [&](auto&& body) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    LDG_CUDA(cudaStreamBeginCapture(T.stream, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < reps; ++r) body();
+    LDG_CUDA(cudaStreamEndCapture(T.stream, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    LDG_CUDA(e);
+    LDG_CUDA(cudaGraphLaunch(exec, T.stream));  // warm-up
+    LDG_CUDA(cudaEventRecord(h.ev[0], T.stream));
+    LDG_CUDA(cudaGraphLaunch(exec, T.stream));
+    LDG_CUDA(cudaEventRecord(h.ev[1], T.stream));
+    LDG_CUDA(cudaEventSynchronize(h.ev[1]));
+    cudaGraphExecDestroy(exec);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]);
+    return static_cast<double>(ms) / reps;
+  };
+  *ms_vcycle = graph_time([&] { vcycle(T, 0, f32, wm, dt, kP, kPh); });
+  for (int l = 0; l < nl && l < max_levels; ++l) {
+    const Vec b = l == 0 ? kP : kMgB, x = l == 0 ? kPh : kMgX;
+    if (fused(T, l, f32))
+      ms_level[l] = graph_time([&] { sweep_f(T, l, wm, dt, b, x, kMgS); });
+    else
+      ms_level[l] = graph_time([&] { smooth(T, l, f32, wm, dt, b, x); });
+  }
+  return nl;
+}
 
 }  // namespace ldgb
