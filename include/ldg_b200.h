@@ -63,10 +63,12 @@ typedef struct ldg_problem {
 typedef struct ldg_solver_opts {
   double rtol;          /* Schur-system relative residual target           */
   double atol;          /* absolute target on the Schur residual           */
-  int maxit;            /* BiCGStab iterations                             */
+  int maxit;            /* Krylov iterations per solve                     */
   int precond;          /* 0 none, 1 block-Jacobi, 2 multigrid V(2,2) (FK)  */
   int check_residual;   /* 1: enforce the reference residual contract      */
   double contract_tol;  /* 1e-10 in the reference                          */
+  int krylov;           /* 0 FGMRES(restart) (default), 1 BiCGStab          */
+  int restart;          /* FGMRES basis size (<= 78; 0: 60)                 */
 } ldg_solver_opts;
 
 typedef struct ldg_step_stats {

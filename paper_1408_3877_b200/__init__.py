@@ -59,7 +59,8 @@ class _Problem(C.Structure):
 
 class _Opts(C.Structure):
     _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("maxit", C.c_int), ("precond", C.c_int),
-                ("check_residual", C.c_int), ("contract_tol", C.c_double)]
+                ("check_residual", C.c_int), ("contract_tol", C.c_double), ("krylov", C.c_int),
+                ("restart", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -225,11 +226,14 @@ class SolverOptions:
     precond: int = 2  # 0 none, 1 block-Jacobi, 2 geometric multigrid V(2,2) (FK meshes; else 1)
     check_residual: bool = True
     contract_tol: float = 1e-10
+    krylov: int = 0  # 0 FGMRES(restart), 1 BiCGStab
+    restart: int = 60
 
     def to_c(self) -> _Opts:
         o = _Opts()
         o.rtol, o.atol, o.maxit, o.precond = self.rtol, self.atol, self.maxit, self.precond
         o.check_residual, o.contract_tol = int(self.check_residual), self.contract_tol
+        o.krylov, o.restart = self.krylov, self.restart
         return o
 
 

@@ -554,11 +554,13 @@ __global__ void k_to_f32(long n, const double* __restrict__ src, float* __restri
 // instructions, which wins once a level fills the GPU; the row-parallel
 // kernels (ldg_rows.cu) win on small levels, where a thread's serial load
 // chain is the latency (measured at p = 4: fine level 246 vs 354 us, coarse
-// levels 35 vs 90 us).  LDG_ROWS_BELOW overrides the element-count switch.
+// levels 35 vs 90 us; with the packed FP32 smoother the 32768-element level
+// sweeps in 80 us vs 135 us on the row kernels, the 8192-element one in 70 vs
+// 44 us, hence the default of 16384).  LDG_ROWS_BELOW overrides the switch.
 bool use_rows(const Handle& h) {
   static const long below = [] {
     const char* s = std::getenv("LDG_ROWS_BELOW");
-    return s ? std::atol(s) : 65536L;
+    return s ? std::atol(s) : 16384L;
   }();
   return h.K < below;
 }
@@ -653,6 +655,18 @@ void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt) {
 }
 
 bool level_uses_rows(const Handle& h) { return use_rows(h); }
+
+// Levels below LDG_SMALL_BELOW elements (default 4096) run the multigrid
+// smoother on the lane-split kernels of ldg_small.cu (latency-bound sizes);
+// measured at p = 4 on an 8192-element level they were 3x slower than the
+// row kernels, whose streams stay coalesced.
+bool level_is_small(const Handle& h) {
+  static const long below = [] {
+    const char* s = std::getenv("LDG_SMALL_BELOW");
+    return s ? std::atol(s) : 4096L;
+  }();
+  return h.K < below;
+}
 
 void launch_bjac_apply(Handle& h, const double* x, double* y) { launch_bjac_axpy(h, x, 1.0, 0.0, y); }
 

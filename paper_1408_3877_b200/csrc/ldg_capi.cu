@@ -69,8 +69,9 @@ void init_team(Team& T) {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(LDG_ECUDA, "no CUDA device available: the LDG path has no CPU fallback");
   LDG_CUDA(cudaStreamCreateWithFlags(&T.stream, cudaStreamNonBlocking));
-  LDG_CUDA(cudaMallocHost(&T.red_host, 256 * sizeof(double)));
-  T.red_all.alloc(256, nullptr);
+  const size_t nred = static_cast<size_t>(ldgb::kMaxRed) * (ldgb::kMaxLocalRanks + 1);
+  LDG_CUDA(cudaMallocHost(&T.red_host, nred * sizeof(double)));
+  T.red_all.alloc(nred, nullptr);
 }
 
 // One rank's device-side state: tables, rule, stream (the team's).
@@ -313,6 +314,8 @@ ldg_solver_opts ldg_default_solver_opts(void) {
   o.precond = 2;
   o.check_residual = 1;
   o.contract_tol = 1e-10;
+  o.krylov = 0;
+  o.restart = 60;
   return o;
 }
 

@@ -16,6 +16,9 @@
 
 namespace ldgb {
 
+constexpr int kMaxRed = 80;        // dot products per reduction (FGMRES basis + 1)
+constexpr int kMaxLocalRanks = 16; // ranks of one process (virtual ranks share a GPU)
+
 // Exceptions carry the ABI status they map to.
 struct Error : std::runtime_error {
   int status;
@@ -125,6 +128,8 @@ struct Handle {
   DBuf<float> E32, Pinv32;                       // FP32 copies read by the row-kernel smoother (small levels)
   DBuf<float4> Eq, Pq;                           // packed FP32 copies read by the fused smoother (ldg_smooth.cu)
   DBuf<double> mg_s;                             // V-cycle ping-pong partner of x (fused smoother)
+  DBuf<double> gm_V, gm_Z;                       // FGMRES basis and preconditioned basis ((m+1) and m vectors)
+  int gm_m = 0;
   bool mg_f32 = true;                            // smoother on FP32 copies (precond 2) or FP64 (3)
   bool mg_ready = false;
   struct VGraph {                                // a captured V-cycle (CUDA graph)
@@ -226,6 +231,7 @@ void launch_to_f32(Handle& h, long n, const double* src, float* dst);
 void launch_bjac_setup_quad(Handle& h, double wm, double dt);        // Pq from E (FP64)
 void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt);  // Pinv32 from E (FP64)
 bool level_uses_rows(const Handle& h);
+bool level_is_small(const Handle& h);
 
 // fused mixed-precision smoother (ldg_smooth.cu)
 long packed_p_quads(int p);                                           // float4 quads of one packed P^-1 block
@@ -235,6 +241,11 @@ void smooth_stage1(Handle& h, const double* x);                       // tz = M^
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
                    double* out);
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
+// the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
+void small_stage1(Handle& h, const double* x);
+void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
+                  double* out);
+void small_zero(Handle& h, const double* b, double omega, double* out);
 
 // row-parallel operator kernels (ldg_rows.cu), used by the launchers above
 void rows_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);
@@ -245,6 +256,8 @@ template <typename TP>
 void rows_bjac(Handle& h, const TP* Pinv, const double* x, double omega, double beta, double* y);
 void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
                      const double* z, double* out);
+void launch_mdots_async(Handle& h, int nv, const double* const* v, const double* w);
+void launch_maxpy(Handle& h, int nv, const double* const* v, const double* c, double alpha, double* w);
 
 // per-rank assembly step (ldg_vec.cu)
 void assemble_step(Handle& h, double t);

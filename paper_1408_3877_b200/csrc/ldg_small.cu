@@ -1,0 +1,244 @@
+// Multigrid smoother kernels for the small (coarse) levels.
+//
+// A coarse level holds a few thousand elements or fewer, so a launch is pure
+// latency: with one thread per (element, row) the time is a thread's serial
+// chain of ~8 dependent block-row products (8-15 us per kernel measured on
+// levels of 8..2048 elements at p = 4).  Here every (element, row) item gets
+// 8 lanes: for the stage-2 residual lane l = (m, slot) streams one of the 8
+// E blocks of the row, lanes 0..6 also take one of the 7 static-table products
+// (M, S_diag x3, S_off x3); for stage 1 lane l takes one of the 8 static
+// products (H x2, S_diag x3, S_off x3).  The chain is one block row (N FMAs,
+// loads issued together) plus a 3-step shuffle reduction.  A CTA holds every
+// row of EPC elements, so the damped block-Jacobi update of a sweep runs in
+// the same kernel on the residual in shared memory.
+//
+// Operands: E and P^-1 as FP32 SoA copies (E32, Pinv32), vectors FP64,
+// arithmetic FP64 (these levels are latency-bound; precision is free).
+// Reference operators as in ldg_apply.cu / ldg_rows.cu (assembly.hpp:76-208).
+#include <cmath>
+
+#include "ldg_internal.hpp"
+
+namespace ldgb {
+
+namespace {
+
+template <int P>
+struct Cfg {
+  static constexpr int N = (P + 1) * (P + 2) / 2;
+  static constexpr int NN = N * N;
+  static constexpr int NP = (N % 2) ? N + 1 : N;
+  static constexpr int NNP = N * NP;
+  // elements per CTA: <= 1024 threads of 8 lanes x N rows, a multiple of 4
+  // (a warp = 4 consecutive elements of one row: table reads broadcast)
+  static constexpr int EPC = (1024 / (8 * N)) / 4 * 4 > 0 ? (1024 / (8 * N)) / 4 * 4 : 4;
+  static constexpr int THREADS = EPC * N * 8;
+};
+
+inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+#define LDG_DISPATCH_P(p, CALL) \
+  switch (p) {                  \
+    case 0: { CALL(0); break; } \
+    case 1: { CALL(1); break; } \
+    case 2: { CALL(2); break; } \
+    case 3: { CALL(3); break; } \
+    default: { CALL(4); break; } \
+  }
+
+struct Item {
+  int lane, i, ke, k;
+  bool live;
+};
+
+template <int P>
+__device__ __forceinline__ Item item_of(int K) {
+  using C = Cfg<P>;
+  Item it;
+  it.lane = threadIdx.x & 7;
+  const int q = threadIdx.x >> 3;
+  it.i = q / C::EPC;
+  it.ke = q % C::EPC;
+  it.k = blockIdx.x * C::EPC + it.ke;
+  it.live = it.k < K;
+  return it;
+}
+
+__device__ __forceinline__ double lane_sum8(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
+// (T x[.][col])_i, T^t[j][i] at tab + j*NP + i
+template <int N, int NP>
+__device__ __forceinline__ double trow(const double* __restrict__ tab, int i, const double* __restrict__ x, long Kp,
+                                       int col) {
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) s = fma(__ldg(tab + j * NP + i), x[j * Kp + col], s);
+  return s;
+}
+
+// tout^m_i = (1/2|T|) (mhat^-1 B^m x)_i with the premultiplied tables
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS) k_s1_small(DevMesh m, DevTables T, const double* __restrict__ x,
+                                                              double* __restrict__ tout) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NP = C::NP, NNP = C::NNP;
+  const Item it = item_of<P>(m.K);
+  const int k = it.live ? it.k : 0, i = it.i, l = it.lane;  // dead items compute on element 0, never store
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  const double* tb = T.base;
+  double u1 = 0.0, u2 = 0.0;
+  if (l < 2) {
+    const double d = trow<N, NP>(tb + T.tmH + l * NNP, i, x, Kp, k);
+    const double b11 = g[kB11 * Kp + k], b12 = g[kB12 * Kp + k], b21 = g[kB21 * Kp + k], b22 = g[kB22 * Kp + k];
+    u1 = l == 0 ? -b22 * d : b21 * d;
+    u2 = l == 0 ? b12 * d : -b11 * d;
+  } else if (l < 5) {
+    const int n = l - 2;
+    const int kind = m.kind[n * Kp + k];
+    const double len = g[(kLen0 + n) * Kp + k];
+    const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
+    if (f != 0.0) {
+      const double d = trow<N, NP>(tb + T.tmSd + n * NNP, i, x, Kp, k);
+      u1 = f * g[(kNux0 + n) * Kp + k] * d;
+      u2 = f * g[(kNuy0 + n) * Kp + k] * d;
+    }
+  } else {
+    const int n = l - 5;
+    const int kp = m.nbr[n * Kp + k];
+    if (kp >= 0) {
+      const double d = trow<N, NP>(tb + T.tmSo + (n * 3 + m.nbrn[n * Kp + k]) * NNP, i, x, Kp, kp);
+      const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+      u1 = hl * g[(kNux0 + n) * Kp + k] * d;
+      u2 = hl * g[(kNuy0 + n) * Kp + k] * d;
+    }
+  }
+  u1 = lane_sum8(u1);
+  u2 = lane_sum8(u2);
+  if (it.live && l == 0) {
+    const double inv2a = 1.0 / (2.0 * g[kArea * Kp + k]);
+    tout[i * Kp + k] = inv2a * u1;
+    tout[(N + i) * Kp + k] = inv2a * u2;
+  }
+}
+
+// r_i = b_i - [wm M x + dt (eta (S + S_D) x - sum_m E^m t^m)]_i, then
+//   MODE 0: out = r;  MODE 1: out = x + omega P^-1 r
+template <int P, int MODE>
+__global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
+                                                              const double* __restrict__ x,
+                                                              const double* __restrict__ tz,
+                                                              const double* __restrict__ b, double wm, double dteta,
+                                                              double dt, const float* __restrict__ Pinv,
+                                                              double omega, double* __restrict__ out) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP;
+  __shared__ double s_r[N][C::EPC];
+  const Item it = item_of<P>(m.K);
+  const int k = it.k, i = it.i, l = it.lane;
+  const long Kp = m.Kp;
+  double part = 0.0;
+  if (it.live) {
+    const double* g = m.geom;
+    const double* tb = T.base;
+    {  // lane (c, s): E^c[s] row i against t^c of the slot's column
+      const int c = l >> 2, s = l & 3;
+      const int col = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
+      if (col >= 0) {
+        const float* blk = E + (static_cast<long>(c * 4 + s) * NN + i * N) * Kp + k;
+        const double* tc = tz + static_cast<long>(c) * N * Kp + col;
+        double e = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) e = fma(static_cast<double>(blk[j * Kp]), tc[j * Kp], e);
+        part = dt * e;
+      }
+    }
+    if (l == 0) {
+      part -= wm * 2.0 * g[kArea * Kp + k] * trow<N, NP>(tb + T.tM, i, x, Kp, k);
+    } else if (l < 4) {
+      const int n = l - 1;
+      const int kind = m.kind[n * Kp + k];
+      if (kind == kInterior || kind == kDirichlet) part -= dteta * trow<N, NP>(tb + T.tSd + n * NNP, i, x, Kp, k);
+    } else if (l < 7) {
+      const int n = l - 4;
+      const int kp = m.nbr[n * Kp + k];
+      if (kp >= 0) part += dteta * trow<N, NP>(tb + T.tSo + (n * 3 + m.nbrn[n * Kp + k]) * NNP, i, x, Kp, kp);
+    }
+  }
+  part = lane_sum8(part);
+  if constexpr (MODE == 0) {
+    if (it.live && l == 0) out[i * Kp + k] = b[i * Kp + k] + part;
+  } else {
+    if (it.live && l == 0) s_r[i][it.ke] = b[i * Kp + k] + part;
+    __syncthreads();
+    double d = 0.0;
+    if (it.live) {
+      const float* row = Pinv + static_cast<long>(i) * N * Kp + k;
+      for (int j = l; j < N; j += 8) d = fma(static_cast<double>(row[j * Kp]), s_r[j][it.ke], d);
+    }
+    d = lane_sum8(d);
+    if (it.live && l == 0) out[i * Kp + k] = fma(omega, d, x[i * Kp + k]);
+  }
+}
+
+// out = omega P^-1 b
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS) k_bj_small(int K, long Kp, const float* __restrict__ Pinv,
+                                                              const double* __restrict__ b, double omega,
+                                                              double* __restrict__ out) {
+  constexpr int N = Cfg<P>::N;
+  const Item it = item_of<P>(K);
+  const int k = it.live ? it.k : 0, i = it.i, l = it.lane;
+  const float* row = Pinv + static_cast<long>(i) * N * Kp + k;
+  double d = 0.0;
+  for (int j = l; j < N; j += 8) d = fma(static_cast<double>(row[j * Kp]), b[j * Kp + k], d);
+  d = lane_sum8(d);
+  if (it.live && l == 0) out[i * Kp + k] = omega * d;
+}
+
+}  // namespace
+
+void small_stage1(Handle& h, const double* x) {
+#define CALL(P)                                                                                          \
+  k_s1_small<P><<<grid_of(h.K, Cfg<P>::EPC), Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, x, h.tz.ptr)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
+                  double* out) {
+  const double dteta = dt * h.prob.eta;
+#define CALL(P)                                                                                                \
+  do {                                                                                                         \
+    const unsigned grid = grid_of(h.K, Cfg<P>::EPC);                                                           \
+    if (mode == 0)                                                                                             \
+      k_s2_small<P, 0><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, x, h.tz.ptr, b,   \
+                                                               wm, dteta, dt, h.Pinv32.ptr, omega, out);     \
+    else                                                                                                       \
+      k_s2_small<P, 1><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, x, h.tz.ptr, b,   \
+                                                               wm, dteta, dt, h.Pinv32.ptr, omega, out);     \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void small_zero(Handle& h, const double* b, double omega, double* out) {
+#define CALL(P)                                                                                              \
+  k_bj_small<P><<<grid_of(h.K, Cfg<P>::EPC), Cfg<P>::THREADS, 0, h.stream>>>(h.K, h.Kp, h.Pinv32.ptr, b, omega, \
+                                                                             out)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+}  // namespace ldgb

@@ -33,6 +33,7 @@ __global__ void k_axpby(long n, double a, const double* __restrict__ x, double b
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs
 constexpr int kMaxDots = 4;
+constexpr int kMdotChunk = 8;    // dots per block row of the multi-dot kernel
 
 struct DotArgs {
   const double* x[kMaxDots];
@@ -82,6 +83,58 @@ __global__ void __launch_bounds__(256) k_dots_owned(int N, long Kp, int K, int n
     double v = 0.0;
     for (int w = 0; w < 8; ++w) v += sh[threadIdx.x][w];
     part[threadIdx.x * kRedBlocks + blockIdx.x] = v;
+  }
+}
+
+// (v_d, w) for d < nv over the owned entries; block row y handles dots
+// [8y, 8y + 8) (w re-read per row, from L2 for the small row counts used)
+struct MDotArgs {
+  const double* v[kMaxRed];
+};
+__global__ void __launch_bounds__(256) k_mdot_owned(int N, long Kp, int K, int nv, MDotArgs a,
+                                                    const double* __restrict__ w, double* __restrict__ part) {
+  const int d0 = blockIdx.y * kMdotChunk;
+  const int nd = min(kMdotChunk, nv - d0);
+  double s[kMdotChunk];
+#pragma unroll
+  for (int d = 0; d < kMdotChunk; ++d) s[d] = 0.0;
+  const long n = static_cast<long>(N) * K;
+  for (long q = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long i = (q / K) * Kp + q % K;
+    const double wi = w[i];
+#pragma unroll
+    for (int d = 0; d < kMdotChunk; ++d)
+      if (d < nd) s[d] = fma(a.v[d0 + d][i], wi, s[d]);
+  }
+  __shared__ double sh[kMdotChunk][8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < kMdotChunk; ++d) {
+    double v = s[d];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[d][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nd) {
+    double v = 0.0;
+    for (int ww = 0; ww < 8; ++ww) v += sh[threadIdx.x][ww];
+    part[(d0 + threadIdx.x) * kRedBlocks + blockIdx.x] = v;
+  }
+}
+
+// w = alpha w + sum_d c_d v_d over the whole vector (n values)
+struct MAxpyArgs {
+  const double* v[kMaxRed];
+  double c[kMaxRed];
+};
+__global__ void __launch_bounds__(256) k_maxpy(long n, int nv, MAxpyArgs a, double alpha, double* __restrict__ w) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    double acc = alpha == 0.0 ? 0.0 : alpha * w[i];
+#pragma unroll 4
+    for (int d = 0; d < nv; ++d) acc = fma(a.c[d], a.v[d][i], acc);
+    w[i] = acc;
   }
 }
 
@@ -146,10 +199,10 @@ void launch_dots(Handle& h, long n, int nd, const double* const* xs, const doubl
     a.y[d] = ys[d];
   }
   k_dots_partial<<<kRedBlocks, 256, 0, h.stream>>>(n, nd, a, h.red.ptr);
-  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxDots * kRedBlocks);
+  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
   LDG_CUDA(cudaGetLastError());
   h.launches += 2;
-  LDG_CUDA(cudaMemcpyAsync(h.red_host, h.red.ptr + kMaxDots * kRedBlocks, sizeof(double) * nd,
+  LDG_CUDA(cudaMemcpyAsync(h.red_host, h.red.ptr + kMaxRed * kRedBlocks, sizeof(double) * nd,
                            cudaMemcpyDeviceToHost, h.stream));
   LDG_CUDA(cudaStreamSynchronize(h.stream));
   for (int d = 0; d < nd; ++d) out_host[d] = h.red_host[d];
@@ -169,7 +222,7 @@ void launch_kmajor_to_soa(Handle& h, const double* km, int nvec, double* soa) {
   ++h.launches;
 }
 
-size_t reduction_scratch() { return static_cast<size_t>(kMaxDots) * kRedBlocks + kMaxDots; }
+size_t reduction_scratch() { return static_cast<size_t>(kMaxRed) * kRedBlocks + kMaxRed; }
 
 void assemble_step(Handle& h, double t) {
   launch_project_df(h, t, h.rule_ptr(), h.rule_R());        // K2: d, f (system.hpp:112-113)
@@ -188,11 +241,36 @@ void launch_dots_async(Handle& h, int nd, const double* const* xs, const double*
     a.y[d] = ys[d];
   }
   k_dots_owned<<<kRedBlocks, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nd, a, h.red.ptr);
-  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxDots * kRedBlocks);
+  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
   LDG_CUDA(cudaGetLastError());
   h.launches += 2;
 }
 
-double* dots_result(Handle& h) { return h.red.ptr + kMaxDots * kRedBlocks; }
+double* dots_result(Handle& h) { return h.red.ptr + kMaxRed * kRedBlocks; }
+
+// (v_d, w), d < nv (<= kMaxRed), owned entries; result at dots_result(h)
+void launch_mdots_async(Handle& h, int nv, const double* const* v, const double* w) {
+  if (nv < 1 || nv > kMaxRed) throw Error(LDG_EINVAL, "multi-dot count out of range");
+  MDotArgs a{};
+  for (int d = 0; d < nv; ++d) a.v[d] = v[d];
+  const dim3 grid(kRedBlocks, (nv + kMdotChunk - 1) / kMdotChunk);
+  k_mdot_owned<<<grid, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nv, a, w, h.red.ptr);
+  k_dots_final<<<1, 96, 0, h.stream>>>(nv, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
+  LDG_CUDA(cudaGetLastError());
+  h.launches += 2;
+}
+
+// w = alpha w + sum_d c[d] v[d] over all n = N * Kp entries
+void launch_maxpy(Handle& h, int nv, const double* const* v, const double* c, double alpha, double* w) {
+  if (nv < 0 || nv > kMaxRed) throw Error(LDG_EINVAL, "multi-axpy count out of range");
+  MAxpyArgs a{};
+  for (int d = 0; d < nv; ++d) {
+    a.v[d] = v[d];
+    a.c[d] = c[d];
+  }
+  k_maxpy<<<kRedBlocks * 4, 256, 0, h.stream>>>(h.vec_len(), nv, a, alpha, w);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
 
 }  // namespace ldgb
