@@ -17,7 +17,6 @@
 #include <cstdlib>
 
 #include "ldg_internal.hpp"
-#include "ldg_pack.cuh"
 
 namespace ldgb {
 
@@ -392,130 +391,6 @@ __global__ void __launch_bounds__(128) k_full(DevMesh m, DevTables T, const doub
   for (int i = 0; i < N; ++i) out[(2 * N + i) * Kp + k] = fma(wm * two_a, w[i], dt * acc[i]);
 }
 
-// Block-Jacobi preconditioner of the Schur operator, one N x N block per
-// element: P_k = w M_k + dt (eta S_kk - sum_m sum_{j in {k} U nbr(k)}
-// E^m_kj M_j^-1 B^m_jk), inverted in shared memory (Gauss-Jordan, partial
-// pivoting).  A group of N^2 threads owns one element; the static blocks
-// B^m_jk are rebuilt from the reference tables (row j, the slot facing k).
-template <int P, typename TE, typename TO, bool QUAD = false>
-__global__ void __launch_bounds__(256) k_bjac_setup(DevMesh m, DevTables T, const TE* __restrict__ E, double wm,
-                                                    double dt, double eta, TO* __restrict__ Pinv) {
-  constexpr int N = Cfg<P>::N, NN = N * N;
-  constexpr int EPC = (256 / NN) > 0 ? (256 / NN) : 1;
-  __shared__ double s_minv[NN];
-  __shared__ double s_P[EPC][NN], s_A[EPC][NN], s_T[EPC][NN], s_I[EPC][NN];
-  __shared__ int s_piv[EPC];
-  const double* tb = T.base;
-  for (int i = threadIdx.x; i < NN; i += blockDim.x) s_minv[i] = tb[T.minv + i];
-  const int grp = threadIdx.x / NN, lane = threadIdx.x % NN;
-  const int k = blockIdx.x * EPC + grp;
-  const bool active = grp < EPC && k < m.K;
-  const long Kp = m.Kp;
-  const double* g = m.geom;
-  const int i = lane / N, j = lane % N;
-  __syncthreads();
-  if (active) {
-    double s = 0.0;
-    for (int n = 0; n < 3; ++n) {
-      const int kd = m.kind[n * Kp + k];
-      if (kd == kInterior || kd == kDirichlet) s += tb[T.sdiag + lane * 3 + n];
-    }
-    s_P[grp][lane] = wm * 2.0 * g[kArea * Kp + k] * tb[T.mhat + lane] + dt * eta * s;
-  }
-  for (int c = 0; c < 2; ++c)
-    for (int s = 0; s < 4; ++s) {
-      int je = -1;
-      if (active) je = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
-      if (active && je >= 0) {
-        double b;
-        if (s == 0) {  // diagonal block of k: -H^m_k + sum_n c^m_n s_diag_n
-          const double h1 = tb[T.hhat + 2 * lane], h2 = tb[T.hhat + 2 * lane + 1];
-          b = c == 0 ? -(g[kB22 * Kp + k] * h1 - g[kB21 * Kp + k] * h2)
-                     : -(g[kB11 * Kp + k] * h2 - g[kB12 * Kp + k] * h1);
-          for (int n = 0; n < 3; ++n) {
-            const int kd = m.kind[n * Kp + k];
-            const double f = kd == kInterior ? 0.5 : (kd == kNeumann ? 1.0 : 0.0);
-            const double nu = g[((c == 0 ? kNux0 : kNuy0) + n) * Kp + k];
-            b += f * nu * g[(kLen0 + n) * Kp + k] * tb[T.sdiag + lane * 3 + n];
-          }
-        } else {  // off-diagonal block of je toward k: nu^m|E|/2 s_off(n', n)
-          const int np = m.nbrn[(s - 1) * Kp + k];
-          const double nu = g[((c == 0 ? kNux0 : kNuy0) + np) * Kp + je];
-          b = 0.5 * nu * g[(kLen0 + np) * Kp + je] * tb[T.soff + (lane * 3 + np) * 3 + (s - 1)];
-        }
-        s_A[grp][lane] = b;
-      }
-      __syncthreads();
-      if (active && je >= 0) {
-        const double inv2a = 1.0 / (2.0 * g[kArea * Kp + je]);
-        double acc = 0.0;
-        for (int q = 0; q < N; ++q) acc += s_minv[i * N + q] * s_A[grp][q * N + j];
-        s_T[grp][lane] = inv2a * acc;
-        s_A[grp][lane] = static_cast<double>(E[(static_cast<long>(c * 4 + s) * NN + lane) * Kp + k]);  // E^m_{k,je}
-      }
-      __syncthreads();
-      if (active && je >= 0) {
-        double acc = 0.0;
-        for (int q = 0; q < N; ++q) acc += s_A[grp][i * N + q] * s_T[grp][q * N + j];
-        s_P[grp][lane] -= dt * acc;
-      }
-      __syncthreads();
-    }
-  if (active) s_I[grp][lane] = (i == j) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int col = 0; col < N; ++col) {
-    if (active && lane == 0) {
-      int piv = col;
-      double best = fabs(s_P[grp][col * N + col]);
-      for (int r = col + 1; r < N; ++r)
-        if (fabs(s_P[grp][r * N + col]) > best) {
-          best = fabs(s_P[grp][r * N + col]);
-          piv = r;
-        }
-      s_piv[grp] = piv;
-    }
-    __syncthreads();
-    if (active) {
-      const int piv = s_piv[grp];
-      if (piv != col && i == col) {
-        const double a = s_P[grp][col * N + j], b = s_P[grp][piv * N + j];
-        s_P[grp][col * N + j] = b;
-        s_P[grp][piv * N + j] = a;
-        const double c2 = s_I[grp][col * N + j], d2 = s_I[grp][piv * N + j];
-        s_I[grp][col * N + j] = d2;
-        s_I[grp][piv * N + j] = c2;
-      }
-    }
-    __syncthreads();
-    double f = 0.0, prow = 0.0, irow = 0.0, pivv = 1.0;
-    if (active) {
-      pivv = s_P[grp][col * N + col];
-      f = s_P[grp][i * N + col];
-      prow = s_P[grp][col * N + j];
-      irow = s_I[grp][col * N + j];
-    }
-    __syncthreads();
-    if (active) {
-      const double pr = prow / pivv, ir = irow / pivv;
-      if (i == col) {
-        s_P[grp][lane] = pr;
-        s_I[grp][lane] = ir;
-      } else {
-        s_P[grp][lane] -= f * pr;
-        s_I[grp][lane] -= f * ir;
-      }
-    }
-    __syncthreads();
-  }
-  if (active) {
-    if constexpr (QUAD) {  // packed float4 layout of the fused smoother (ldg_pack.cuh)
-      Pinv[sm_packed_p_index<P>(i, j, Kp, k)] = static_cast<TO>(s_I[grp][lane]);
-    } else {
-      Pinv[static_cast<long>(lane) * Kp + k] = static_cast<TO>(s_I[grp][lane]);
-    }
-  }
-}
-
 // y = beta y + omega P^-1 x  (beta = 0: plain block-Jacobi application)
 template <int P, typename TP>
 __global__ void __launch_bounds__(128) k_bjac_axpy(int K, long Kp, const TP* __restrict__ Pinv,
@@ -623,36 +498,13 @@ void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double*
   ++h.launches;
 }
 
-template <typename TE, typename TO, bool QUAD = false>
-void bjac_setup_impl(Handle& h, const TE* E, double wm, double dt, TO* out) {
-#define CALL(P)                                                                                         \
-  do {                                                                                                  \
-    constexpr int NN = Cfg<P>::N * Cfg<P>::N;                                                           \
-    constexpr int EPC = (256 / NN) > 0 ? (256 / NN) : 1;                                                \
-    k_bjac_setup<P, TE, TO, QUAD><<<grid_of(h.K, EPC), 256, 0, h.stream>>>(h.mesh(), h.dtab, E, wm, dt, \
-                                                                           h.prob.eta, out);            \
-  } while (0)
-  LDG_DISPATCH_P(h.p, CALL)
-#undef CALL
-  LDG_CUDA(cudaGetLastError());
-  ++h.launches;
-}
-
-void launch_bjac_setup(Handle& h, double wm, double dt) { bjac_setup_impl<double, double>(h, h.E.ptr, wm, dt, h.Pinv.ptr); }
-
-void launch_bjac_setup_f32(Handle& h, double wm, double dt) {
-  bjac_setup_impl<float, float>(h, h.E32.ptr, wm, dt, h.Pinv32.ptr);
-}
+void launch_bjac_setup(Handle& h, double wm, double dt) { launch_bjac(h, wm, dt, 0); }
 
 // FP32 inverses from the FP64 E of the level (multigrid smoother copies):
 // packed for the fused smoother kernels, plain SoA for the row kernels
-void launch_bjac_setup_quad(Handle& h, double wm, double dt) {
-  bjac_setup_impl<double, float, true>(h, h.E.ptr, wm, dt, reinterpret_cast<float*>(h.Pq.ptr));
-}
+void launch_bjac_setup_quad(Handle& h, double wm, double dt) { launch_bjac(h, wm, dt, 2); }
 
-void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt) {
-  bjac_setup_impl<double, float>(h, h.E.ptr, wm, dt, h.Pinv32.ptr);
-}
+void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt) { launch_bjac(h, wm, dt, 1); }
 
 bool level_uses_rows(const Handle& h) { return use_rows(h); }
 

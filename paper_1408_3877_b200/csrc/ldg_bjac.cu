@@ -1,0 +1,225 @@
+// Block-Jacobi setup of the Schur operator, once per step and level.
+//
+//   P_k = wm M_k + dt (eta S_kk - sum_m sum_{j in {k} u nbr(k)} E^m_kj M_j^-1 B^m_jk)
+//
+// and its inverse, one N x N block per element.  M_j^-1 B^m_jk is a linear
+// combination of the m_hat^-1-premultiplied reference tables (ldg_tables.cpp
+// tmH, tmSd, tmSo) with per-element scalars, so the 8 block products fold
+// into 8 "combined E x table" products: the diagonal slot mixes E^1, E^2 into
+// one matrix per table (H^1, H^2, S_diag x3), each off-diagonal slot into one
+// matrix against its S_off table.  Static blocks as in assembly.hpp:76-208;
+// the reference itself has no preconditioner (system.hpp:190-205 factorises).
+//
+// Shape: a group of NG = N rounded up to a power of two lanes per element
+// (2 elements per warp at p = 3, 4), lane i holding row i of P and of the
+// augmented identity in registers; the tables sit in shared memory and are
+// read as broadcasts.  Gauss-Jordan with partial pivoting without row swaps:
+// the pivot row of each column is chosen among the rows not yet used and
+// broadcast through shared memory; the lane that pivoted column c holds row c
+// of P^-1 at the end.
+#include <cmath>
+
+#include "ldg_internal.hpp"
+#include "ldg_pack.cuh"
+
+namespace ldgb {
+
+namespace {
+
+template <int P>
+struct Cfg {
+  static constexpr int N = (P + 1) * (P + 2) / 2;
+  static constexpr int NN = N * N;
+  static constexpr int NP = (N % 2) ? N + 1 : N;
+  static constexpr int NNP = N * NP;
+  static constexpr int NG = N <= 1 ? 1 : (N <= 2 ? 2 : (N <= 4 ? 4 : (N <= 8 ? 8 : 16)));
+  static constexpr int EPW = 32 / NG;  // elements per warp
+  static constexpr int WARPS = 8;
+  static constexpr int EPB = EPW * WARPS;
+};
+
+inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+#define LDG_DISPATCH_P(p, CALL) \
+  switch (p) {                  \
+    case 0: { CALL(0); break; } \
+    case 1: { CALL(1); break; } \
+    case 2: { CALL(2); break; } \
+    case 3: { CALL(3); break; } \
+    default: { CALL(4); break; } \
+  }
+
+// OUT: 0 FP64 SoA, 1 FP32 SoA, 2 FP32 packed (ldg_pack.cuh)
+template <int P, int OUT>
+__global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E, double wm,
+                                                   double dt, double eta, void* __restrict__ out) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG;
+  __shared__ __align__(16) double s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
+  __shared__ double s_piv[C::WARPS][C::EPW][2 * N + 2];
+  {
+    const double2* src = reinterpret_cast<const double2*>(T.base + T.tmH);
+    double2* dst = reinterpret_cast<double2*>(s_tab);
+    for (int t = threadIdx.x; t < 14 * NNP / 2; t += blockDim.x) dst[t] = src[t];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / NG, i = lane % NG;
+  const int k = (blockIdx.x * C::WARPS + warp) * C::EPW + sub;
+  const bool live = k < m.K;
+  const bool row = live && i < N;
+  const int kk = live ? k : 0;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  const double* tb = T.base;
+
+  // a[jj] = row i of P_k
+  double a[N];
+  const int ir = row ? i : 0;
+  {
+    const double two_a = 2.0 * g[kArea * Kp + kk];
+    int kind[3];
+#pragma unroll
+    for (int n = 0; n < 3; ++n) kind[n] = m.kind[n * Kp + kk];
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) {
+      double s = 0.0;
+#pragma unroll
+      for (int n = 0; n < 3; ++n)
+        if (kind[n] == kInterior || kind[n] == kDirichlet) s += tb[T.sdiag + (ir * N + jj) * 3 + n];
+      a[jj] = wm * two_a * tb[T.mhat + ir * N + jj] + dt * eta * s;
+    }
+  }
+  // a -= dt sum E (M^-1 B), as combined-E rows against the tables:
+  // a[jj] += sum_q e_t[q] Tab_t[q][jj] with Tab_t^t[jj][q] at jj*NP + q
+  {
+    // diagonal slot: E^1_k0, E^2_k0 against H^1, H^2, S_diag x3 (k's own geometry)
+    const double inv2a = 1.0 / (2.0 * g[kArea * Kp + kk]);
+    const double b11 = g[kB11 * Kp + kk], b12 = g[kB12 * Kp + kk], b21 = g[kB21 * Kp + kk], b22 = g[kB22 * Kp + kk];
+    // B^1_kk = -(b22 H1 - b21 H2) + sum_n f_n nu^x_n |E_n| S_d,n;  B^2_kk = -(b11 H2 - b12 H1) + ... nu^y
+    double c1[5], c2[5];  // coefficients of (tmH1, tmH2, tmSd0..2) for E^1 and E^2, with -dt and 1/(2|T|)
+    const double sc = -dt * inv2a;
+    c1[0] = -b22 * sc;
+    c1[1] = b21 * sc;
+    c2[0] = b12 * sc;
+    c2[1] = -b11 * sc;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      const int kd = m.kind[n * Kp + kk];
+      const double f = kd == kInterior ? 0.5 : (kd == kNeumann ? 1.0 : 0.0);
+      const double fl = f * g[(kLen0 + n) * Kp + kk] * sc;
+      c1[2 + n] = fl * g[(kNux0 + n) * Kp + kk];
+      c2[2 + n] = fl * g[(kNuy0 + n) * Kp + kk];
+    }
+#pragma unroll 1
+    for (int q = 0; q < N; ++q) {
+      const double e1 = E[(static_cast<long>(0) * NN + ir * N + q) * Kp + kk];
+      const double e2 = E[(static_cast<long>(4) * NN + ir * N + q) * Kp + kk];
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const double e = c1[t] * e1 + c2[t] * e2;
+        const double* tab = s_tab + t * NNP + q;
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab[jj * NP], a[jj]);
+      }
+    }
+    // off-diagonal slots: E^m_{k,j} against M_j^-1 B^m_{j,k} = (nu^m_j |E_j| / (4 |T_j|)) s_off(np, n)
+#pragma unroll 1
+    for (int s = 1; s < 4; ++s) {
+      const int j = m.nbr[(s - 1) * Kp + kk];
+      if (j < 0) continue;
+      const int np = m.nbrn[(s - 1) * Kp + kk];
+      const double h = -dt * 0.5 * g[(kLen0 + np) * Kp + j] / (2.0 * g[kArea * Kp + j]);
+      const double cx = h * g[(kNux0 + np) * Kp + j], cy = h * g[(kNuy0 + np) * Kp + j];
+      const double* tab0 = s_tab + (5 + np * 3 + (s - 1)) * NNP;
+#pragma unroll 1
+      for (int q = 0; q < N; ++q) {
+        const double e = cx * E[(static_cast<long>(s) * NN + ir * N + q) * Kp + kk] +
+                         cy * E[(static_cast<long>(4 + s) * NN + ir * N + q) * Kp + kk];
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab0[jj * NP + q], a[jj]);
+      }
+    }
+  }
+  double v[N];  // row i of the augmented identity
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) v[jj] = (jj == i) ? 1.0 : 0.0;
+
+  // Gauss-Jordan, partial pivoting over the rows not yet used
+  bool used = !row;
+  int my_col = -1;
+  double* piv = s_piv[warp][sub];
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double best = used ? -1.0 : fabs(a[c]);
+    int who = i;
+#pragma unroll
+    for (int o = NG / 2; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+      if (ob > best || (ob == best && ow < who)) {
+        best = ob;
+        who = ow;
+      }
+    }
+    if (i == who && row) {
+      const double inv = 1.0 / a[c];
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) {
+        a[jj] *= inv;
+        v[jj] *= inv;
+        piv[jj] = a[jj];
+        piv[N + jj] = v[jj];
+      }
+      used = true;
+      my_col = c;
+    }
+    __syncwarp();
+    if (row && i != who) {
+      const double f = a[c];
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) {
+        a[jj] = fma(-f, piv[jj], a[jj]);
+        v[jj] = fma(-f, piv[N + jj], v[jj]);
+      }
+    }
+    __syncwarp();
+  }
+  if (row) {  // this lane holds row my_col of P^-1
+    const int r = my_col;
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) {
+      if constexpr (OUT == 0) {
+        static_cast<double*>(out)[static_cast<long>(r * N + jj) * Kp + k] = v[jj];
+      } else if constexpr (OUT == 1) {
+        static_cast<float*>(out)[static_cast<long>(r * N + jj) * Kp + k] = static_cast<float>(v[jj]);
+      } else {
+        static_cast<float*>(out)[sm_packed_p_index<P>(r, jj, Kp, k)] = static_cast<float>(v[jj]);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// Pinv (FP64 SoA), Pinv32 (FP32 SoA) or Pq (FP32 packed) from the level's FP64 E
+void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
+  void* out = out_kind == 0 ? static_cast<void*>(h.Pinv.ptr)
+                            : (out_kind == 1 ? static_cast<void*>(h.Pinv32.ptr) : static_cast<void*>(h.Pq.ptr));
+#define CALL(P)                                                                                               \
+  do {                                                                                                        \
+    const unsigned grid = grid_of(h.K, Cfg<P>::EPB);                                                          \
+    if (out_kind == 0)                                                                                        \
+      k_bjac_warp<P, 0><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, wm, dt, h.prob.eta, out);      \
+    else if (out_kind == 1)                                                                                   \
+      k_bjac_warp<P, 1><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, wm, dt, h.prob.eta, out);      \
+    else                                                                                                      \
+      k_bjac_warp<P, 2><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, wm, dt, h.prob.eta, out);      \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+}  // namespace ldgb

@@ -225,9 +225,9 @@ void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double*
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_stage2_f32(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz,
                        double gamma_e, const double* w, double delta, double* y);
-void launch_bjac_setup_f32(Handle& h, double wm, double dt);
 void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_to_f32(Handle& h, long n, const double* src, float* dst);
+void launch_bjac(Handle& h, double wm, double dt, int out_kind);     // ldg_bjac.cu: 0 Pinv, 1 Pinv32, 2 Pq
 void launch_bjac_setup_quad(Handle& h, double wm, double dt);        // Pq from E (FP64)
 void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt);  // Pinv32 from E (FP64)
 bool level_uses_rows(const Handle& h);

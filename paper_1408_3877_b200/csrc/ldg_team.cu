@@ -602,7 +602,7 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
     });
   };
 
-  int applies = 0, it = 0;
+  int applies = 0, it = 0, reorth = 0;
   double rnorm = 0.0;
   std::vector<double> H(static_cast<size_t>(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   auto Hij = [&](int i, int j) -> double& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
@@ -630,19 +630,29 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
       }
       schur_apply(T, wm, dt, gmZ(j), gmV(j + 1));
       ++applies;
-      // CGS2: h = V^T w; w -= V h; h2 = V^T w (+ |w|^2); w -= V h2
+      // classical Gram-Schmidt: h = V^T w (+ |w|^2), w -= V h; a second pass
+      // only when the projection removed more than half of |w|^2 ("twice is
+      // enough"), so the basis stays orthogonal to working precision
       double h1[kMaxRed], h2[kMaxRed];
-      project(j + 1, gmV(j + 1), false, h1);
+      project(j + 1, gmV(j + 1), true, h1);
       subtract(j + 1, h1, gmV(j + 1));
-      project(j + 1, gmV(j + 1), true, h2);
-      subtract(j + 1, h2, gmV(j + 1));
-      double ss = h2[j + 1];
+      double ss = h1[j + 1];
       for (int i = 0; i <= j; ++i) {
-        Hij(i, j) = h1[i] + h2[i];
-        ss -= h2[i] * h2[i];
+        Hij(i, j) = h1[i];
+        ss -= h1[i] * h1[i];
+      }
+      if (!(ss > 0.5 * h1[j + 1])) {
+        project(j + 1, gmV(j + 1), true, h2);
+        subtract(j + 1, h2, gmV(j + 1));
+        ss = h2[j + 1];
+        for (int i = 0; i <= j; ++i) {
+          Hij(i, j) += h2[i];
+          ss -= h2[i] * h2[i];
+        }
+        ++reorth;
       }
       double hn = ss > 0.0 ? std::sqrt(ss) : 0.0;
-      if (!(hn > 1e-8 * std::sqrt(std::max(h2[j + 1], 0.0)))) hn = norm(T, gmV(j + 1));  // cancellation guard
+      if (!(hn > 1e-6 * std::sqrt(std::max(h1[j + 1], 0.0)))) hn = norm(T, gmV(j + 1));  // cancellation guard
       Hij(j + 1, j) = hn;
       if (hn > 0.0) scale_into(1.0 / hn, gmV(j + 1), gmV(j + 1));
       // Givens rotations
@@ -683,6 +693,7 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
   *it_out = it;
   *applies_out = applies;
   *rnorm_out = rnorm;
+  (void)reorth;
 }
 
 }  // namespace
