@@ -127,6 +127,8 @@ struct Handle {
   DBuf<double> mg_x, mg_b, mg_r;                 // V-cycle work vectors (N * Kp)
   DBuf<float> E32, Pinv32;                       // FP32 copies read by the row-kernel smoother (small levels)
   DBuf<float4> Eq, Pq;                           // packed FP32 copies read by the fused smoother (ldg_smooth.cu)
+  DBuf<uint2> Eh;                                // packed FP16 copy of E (4 values per uint2), scaled per element
+  DBuf<float> Escale;                            // per-element scale of Eh
   DBuf<double> mg_s;                             // V-cycle ping-pong partner of x (fused smoother)
   DBuf<double> gm_V, gm_Z;                       // FGMRES basis and preconditioned basis ((m+1) and m vectors)
   int gm_m = 0;

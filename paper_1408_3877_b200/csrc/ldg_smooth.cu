@@ -20,7 +20,11 @@
 //
 // Reference operators restated (as in ldg_apply.cu): B^m = -H^m + Q^m + Q_N^m
 // (assembly.hpp:92-109, 174-208), S + S_D (assembly.hpp:142-168), M = 2|T| mhat.
+#include <cuda_fp16.h>
+
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "ldg_internal.hpp"
 #include "ldg_pack.cuh"
@@ -146,13 +150,23 @@ __global__ void __launch_bounds__(128) k_s1f(DevMesh m, DevTables T, const doubl
   }
 }
 
+// A quad of the packed stream: float4 (FP32 copy) or four FP16 values in a
+// uint2 (E scaled per element into [-1, 1], ldg_smooth.cu k_pack_e)
+__device__ __forceinline__ float4 ld_quad(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld_quad(const uint2* p) {
+  const uint2 u = __ldcs(p);
+  const float2 fa = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 fb = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(fa.x, fa.y, fb.x, fb.y);
+}
+
 // acc[i] += sum_j blk[i][j] v[j] over one column group: quad q of the group
 // holds values u = 4q..4q+3, u = jj*N + i, column j0 + jj
-template <int N, int QC>
-__device__ __forceinline__ void group_mv(const float4* __restrict__ g, long Kp, const float* v, float* acc) {
+template <int N, int QC, typename TQ>
+__device__ __forceinline__ void group_mv(const TQ* __restrict__ g, long Kp, const float* v, float* acc) {
   float4 e[QC];
 #pragma unroll
-  for (int q = 0; q < QC; ++q) e[q] = __ldcs(g + q * Kp);
+  for (int q = 0; q < QC; ++q) e[q] = ld_quad(g + q * Kp);
 #pragma unroll
   for (int q = 0; q < QC; ++q)
 #pragma unroll
@@ -163,8 +177,8 @@ __device__ __forceinline__ void group_mv(const float4* __restrict__ g, long Kp, 
 }
 
 // acc += sum_s E^m[s] t^m_col(s) for component c (E packed, t FP64 planes)
-template <int P>
-__device__ __forceinline__ void e_component(const float4* __restrict__ Ec, const double* __restrict__ tc, long Kp,
+template <int P, typename TQ>
+__device__ __forceinline__ void e_component(const TQ* __restrict__ Ec, const double* __restrict__ tc, long Kp,
                                             int k, const int* __restrict__ nbr, float* acc) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN;
@@ -178,7 +192,7 @@ __device__ __forceinline__ void e_component(const float4* __restrict__ Ec, const
     }
 #pragma unroll
     for (int q = 0; q < NN; ++q) {
-      const float4 e = __ldcs(Ec + q * Kp);
+      const float4 e = ld_quad(Ec + q * Kp);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int v = 4 * q + r, s = v / NN, rem = v % NN;
@@ -190,7 +204,7 @@ __device__ __forceinline__ void e_component(const float4* __restrict__ Ec, const
     for (int s = 0; s < 4; ++s) {
       const int col = s == 0 ? k : nbr[(s - 1) * Kp + k];
       if (col < 0) continue;
-      const float4* Es = Ec + static_cast<long>(s) * C::QS * Kp;
+      const TQ* Es = Ec + static_cast<long>(s) * C::QS * Kp;
       const double* tcol = tc + col;
 #pragma unroll(C::UNR)
       for (int ch = 0; ch < C::NCH; ++ch) {
@@ -200,7 +214,7 @@ __device__ __forceinline__ void e_component(const float4* __restrict__ Ec, const
           const int j = ch * C::CC + jj;
           v[jj] = (C::NCOL == N || j < N) ? static_cast<float>(tcol[j * Kp]) : 0.f;
         }
-        group_mv<N, C::QC>(Es + static_cast<long>(ch) * C::QC * Kp, Kp, v, acc);
+        group_mv<N, C::QC, TQ>(Es + static_cast<long>(ch) * C::QC * Kp, Kp, v, acc);
       }
     }
   }
@@ -235,7 +249,7 @@ __device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long K
         const int j = ch * C::CC + jj;
         v[jj] = (C::NCOL == N || j < N) ? load(j) : 0.f;
       }
-      group_mv<N, C::QC>(Pk + static_cast<long>(ch) * C::QC * Kp, Kp, v, d);
+      group_mv<N, C::QC, float4>(Pk + static_cast<long>(ch) * C::QC * Kp, Kp, v, d);
     }
   }
 }
@@ -243,11 +257,12 @@ __device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long K
 // r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
-template <int P, int MODE>
-__global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const float4* __restrict__ Eq,
-                                             const double* __restrict__ x, const double* __restrict__ tz,
-                                             const double* __restrict__ b, double wm, double dteta, double dt,
-                                             const float4* __restrict__ Pq, float omega, double* __restrict__ out) {
+template <int P, int MODE, typename TQ>
+__global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
+                                             const float* __restrict__ Escale, const double* __restrict__ x,
+                                             const double* __restrict__ tz, const double* __restrict__ b, double wm,
+                                             double dteta, double dt, const float4* __restrict__ Pq, float omega,
+                                             double* __restrict__ out) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
   extern __shared__ __align__(16) float smf[];
@@ -262,11 +277,12 @@ __global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const float
   for (int i = 0; i < N; ++i) acc[i] = 0.f;
 #pragma unroll 1
   for (int c = 0; c < 2; ++c)
-    e_component<P>(Eq + static_cast<long>(c) * C::QE * Kp + k, tz + static_cast<long>(c) * N * Kp, Kp, k, m.nbr,
-                   acc);
+    e_component<P, TQ>(Eq + static_cast<long>(c) * C::QE * Kp + k, tz + static_cast<long>(c) * N * Kp, Kp, k,
+                       m.nbr, acc);
   const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
+  const float es = Escale ? fdt * Escale[k] : fdt;
 #pragma unroll
-  for (int i = 0; i < N; ++i) acc[i] *= fdt;
+  for (int i = 0; i < N; ++i) acc[i] *= es;
   {
     float xv[N], w[N];
     load_f<N>(x, Kp, k, xv);
@@ -328,8 +344,28 @@ __global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const float4* __res
 
 // Eq[c][q][k] from E[(c*4 + s)*NN + i*N + j][k] (FP64, row-major blocks);
 // one thread per output quad, zero in the padding columns
+// per-element scale of the FP16 copy: max |E| over the element's 8 blocks
 template <int P>
-__global__ void k_pack_e(long Kp, const double* __restrict__ E, float4* __restrict__ Eq) {
+__global__ void k_escale(long Kp, const double* __restrict__ E, float* __restrict__ scale) {
+  constexpr int NN = Cfg<P>::NN;
+  const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (k >= Kp) return;
+  double mx = 0.0;
+  for (int v = 0; v < 8 * NN; ++v) mx = fmax(mx, fabs(E[v * Kp + k]));
+  scale[k] = mx > 0.0 ? static_cast<float>(mx) : 1.0f;
+}
+
+__device__ __forceinline__ void put_quad(float4* q, const float* v, float) { *q = make_float4(v[0], v[1], v[2], v[3]); }
+__device__ __forceinline__ void put_quad(uint2* q, const float* v, float inv) {
+  const __half2 a = __floats2half2_rn(v[0] * inv, v[1] * inv), b = __floats2half2_rn(v[2] * inv, v[3] * inv);
+  uint2 u;
+  u.x = *reinterpret_cast<const unsigned*>(&a);
+  u.y = *reinterpret_cast<const unsigned*>(&b);
+  *q = u;
+}
+
+template <int P, typename TQ>
+__global__ void k_pack_e(long Kp, const double* __restrict__ E, const float* __restrict__ scale, TQ* __restrict__ Eq) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN;
   const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
@@ -354,7 +390,7 @@ __global__ void k_pack_e(long Kp, const double* __restrict__ E, float4* __restri
     }
     v[r] = j < N ? static_cast<float>(E[(static_cast<long>(c * 4 + s) * NN + i * N + j) * Kp + k]) : 0.f;
   }
-  Eq[t] = make_float4(v[0], v[1], v[2], v[3]);
+  put_quad(Eq + t, v, scale ? 1.0f / scale[k] : 1.0f);
 }
 
 template <int P>
@@ -378,12 +414,34 @@ long packed_p_quads(int p) {
   }
 }
 
+// Storage of the stored blocks read by the big-level smoother: FP16 with a
+// per-element scale (default; half the bytes of FP32 in the HBM-bound stage
+// 2) or FP32 (LDG_SMOOTHER_E=32).
+bool smoother_e16() {
+  static const bool on = [] {
+    const char* s = std::getenv("LDG_SMOOTHER_E");
+    return !(s && std::atoi(s) == 32);
+  }();
+  return on;
+}
+
 void smooth_pack_e(Handle& h) {
+  const bool e16 = smoother_e16();
 #define CALL(P)                                                                                            \
   do {                                                                                                     \
     const long nq = 2L * Cfg<P>::QE * h.Kp;                                                                \
-    if (!h.Eq.ptr) h.Eq.alloc(nq, &h.bytes);                                                               \
-    k_pack_e<P><<<grid_of(nq, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr, h.Eq.ptr);                          \
+    if (e16) {                                                                                             \
+      if (!h.Eh.ptr) {                                                                                     \
+        h.Eh.alloc(nq, &h.bytes);                                                                          \
+        h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
+      }                                                                                                    \
+      k_escale<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr);                  \
+      k_pack_e<P, uint2><<<grid_of(nq, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr, h.Eh.ptr);   \
+      h.launches += 1;                                                                                     \
+    } else {                                                                                               \
+      if (!h.Eq.ptr) h.Eq.alloc(nq, &h.bytes);                                                             \
+      k_pack_e<P, float4><<<grid_of(nq, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr, nullptr, h.Eq.ptr);       \
+    }                                                                                                      \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -403,19 +461,28 @@ void smooth_stage1(Handle& h, const double* x) {
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
                    double* out) {
   const double dteta = dt * h.prob.eta;
-#define CALL(P)                                                                                                   \
-  do {                                                                                                            \
-    if (mode == 0)                                                                                                \
-      k_s2f<P, 0><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.Eq.ptr, x, h.tz.ptr,  \
-                                                                       b, wm, dteta, dt, h.Pq.ptr,               \
-                                                                       static_cast<float>(omega), out);          \
-    else                                                                                                          \
-      k_s2f<P, 1><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.Eq.ptr, x, h.tz.ptr,  \
-                                                                       b, wm, dteta, dt, h.Pq.ptr,               \
-                                                                       static_cast<float>(omega), out);          \
+  const float om = static_cast<float>(omega);
+  const bool e16 = h.Eh.ptr != nullptr;
+#define LAUNCH(P, M, TQ, EP, SC)                                                                                   \
+  k_s2f<P, M, TQ><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, EP, SC, x, h.tz.ptr, b,  \
+                                                                      wm, dteta, dt, h.Pq.ptr, om, out)
+#define CALL(P)                                                                         \
+  do {                                                                                  \
+    if (e16) {                                                                          \
+      if (mode == 0)                                                                    \
+        LAUNCH(P, 0, uint2, h.Eh.ptr, h.Escale.ptr);                                    \
+      else                                                                              \
+        LAUNCH(P, 1, uint2, h.Eh.ptr, h.Escale.ptr);                                    \
+    } else {                                                                            \
+      if (mode == 0)                                                                    \
+        LAUNCH(P, 0, float4, h.Eq.ptr, static_cast<const float*>(nullptr));             \
+      else                                                                              \
+        LAUNCH(P, 1, float4, h.Eq.ptr, static_cast<const float*>(nullptr));             \
+    }                                                                                   \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
+#undef LAUNCH
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
