@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "ldg_internal.hpp"
+#include "ldg_offdiag.cuh"
 
 namespace ldgb {
 
@@ -27,6 +28,8 @@ struct Cfg {
   static constexpr int N = (P + 1) * (P + 2) / 2;
   static constexpr int NP = (N % 2) ? N + 1 : N;
   static constexpr int TAB = 16 * N * NP;  // tH(2) + tSd(3) + tSo(9) + tM + tMinv
+  static constexpr int Q = (3 * P + 2) / 2;  // edge rule of the off-diagonal E blocks
+  static constexpr int EDGE = (12 * Q * N + Q + 1) / 2 * 2;  // pe(3) + pth(9) + we, padded to even
 };
 
 inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
@@ -53,16 +56,25 @@ struct STab {
 };
 
 // The five table blocks are contiguous in the device table buffer in this
-// order (ldg_tables.cpp), so staging is one vectorised copy.
-template <int P>
+// order (ldg_tables.cpp), so staging is one vectorised copy.  With EDGE the
+// edge tables of the matrix-free off-diagonal E blocks follow them
+// (pe [3][Q][N] | pth [9][Q][N] | we [Q]).
+template <int P, bool EDGE = false>
 __device__ __forceinline__ STab<P> stage_tables(double* sm, const DevTables& T) {
-  constexpr int n = Cfg<P>::TAB;
+  constexpr int n = Cfg<P>::TAB, N = Cfg<P>::N, Q = Cfg<P>::Q;
   const double2* src = reinterpret_cast<const double2*>(T.base + T.tH);
   double2* dst = reinterpret_cast<double2*>(sm);
   for (int i = threadIdx.x; i < n / 2; i += blockDim.x) dst[i] = src[i];
+  if constexpr (EDGE) {
+    double* e = sm + n;
+    for (int i = threadIdx.x; i < 3 * Q * N; i += blockDim.x) e[i] = T.base[T.pe + i];
+    for (int i = threadIdx.x; i < 9 * Q * N; i += blockDim.x) e[3 * Q * N + i] = T.base[T.pth + i];
+    for (int i = threadIdx.x; i < Q; i += blockDim.x) e[12 * Q * N + i] = T.base[T.we + i];
+  }
   __syncthreads();
   return STab<P>{sm};
 }
+
 
 // w = T x with x in registers (T^t in shared memory, rows of NP doubles)
 template <int N, int NP>
@@ -182,6 +194,29 @@ __device__ __forceinline__ EdgeData load_edges(const DevMesh& m, int k) {
   return e;
 }
 
+// sum_m E^m_{k,kp} t^m_kp over the interior edges of k, added to acc
+// (ldg_offdiag.cuh); edge tables staged after the STab block
+template <int P>
+__device__ __forceinline__ void offdiag_all(const double* sm_edge, const double* __restrict__ D,
+                                            const double* __restrict__ t, long Kp, const EdgeData& e,
+                                            double* acc) {
+  constexpr int N = Cfg<P>::N, Q = Cfg<P>::Q;
+  const double* pe = sm_edge;
+  const double* pth = sm_edge + 3 * Q * N;
+  const double* we = sm_edge + 12 * Q * N;
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kp = e.nbr[n];
+    if (kp < 0) continue;
+    const double co1 = 0.5 * e.len[n] * e.nux[n], co2 = 0.5 * e.len[n] * e.nuy[n];
+    double z[Q];
+    offdiag_z<N, Q, double>(
+        pth + (n * 3 + e.nbrn[n]) * Q * N, we, [&](int j) { return D[j * Kp + kp]; },
+        [&](int j) { return fma(co1, t[j * Kp + kp], co2 * t[(N + j) * Kp + kp]); }, z);
+    offdiag_rows<N, Q, double>(pe + n * Q * N, z, 1.0, acc);
+  }
+}
+
 // u^m += sum_s B^m[s] x_col(s), B^m = -H^m + Q^m + Q_N^m rebuilt from tables
 // (assembly.hpp:92-109, 174-208): diagonal -H^m_k + sum_n c^m_n s_diag_n with
 // c = nu^m |E|/2 (interior), nu^m |E| (Neumann); off-diagonal nu^m|E|/2 s_off.
@@ -289,16 +324,17 @@ __global__ void __launch_bounds__(128) k_stage1(DevMesh m, DevTables T, const do
 }
 
 // stage 2: y = alpha M_k x_k + beta (S + S_D) x - gamma sum_m sum_s E^m[s] tz^m_col + delta w
-// TE = double for the Krylov operator, float for the multigrid smoother's
-// copy of E (FP32 storage, FP64 arithmetic: the preconditioner only).
-template <int P, typename TE>
-__global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const TE* __restrict__ E,
-                                                const double* __restrict__ x, double alpha, double beta,
-                                                const double* __restrict__ tz, double gamma,
-                                                const double* __restrict__ w, double delta, double* __restrict__ y) {
+// (the Krylov operator, FP64): stored diagonal blocks streamed, off-diagonal
+// blocks matrix-free from D.
+template <int P>
+__global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const double* __restrict__ E,
+                                                const double* __restrict__ D, const double* __restrict__ x,
+                                                double alpha, double beta, const double* __restrict__ tz,
+                                                double gamma, const double* __restrict__ w, double delta,
+                                                double* __restrict__ y) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
-  const STab<P> tb = stage_tables<P>(sm, T);
+  const STab<P> tb = stage_tables<P, true>(sm, T);
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
   const long Kp = m.Kp;
@@ -308,17 +344,9 @@ __global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const TE
   const EdgeData e = load_edges(m, k);
   if (tz) {
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      const TE* Ec = E + static_cast<long>(c) * 4 * NN * Kp;
-      const double* tc = tz + static_cast<long>(c) * N * Kp;
-      block_mv_gather<N>(Ec, Kp, k, tc, k, acc);
-#pragma unroll 1
-      for (int s = 1; s < 4; ++s) {
-        const int col = e.nbr[s - 1];
-        if (col < 0) continue;
-        block_mv_gather<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, tc, col, acc);
-      }
-    }
+    for (int c = 0; c < 2; ++c)
+      block_mv_gather<N>(E + static_cast<long>(c) * NN * Kp, Kp, k, tz + static_cast<long>(c) * N * Kp, k, acc);
+    offdiag_all<P>(sm + Cfg<P>::TAB, D, tz, Kp, e, acc);
 #pragma unroll
     for (int i = 0; i < N; ++i) acc[i] *= -gamma;
   }
@@ -345,11 +373,11 @@ __global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const TE
 //   out_C  = wm M c_k + dt (sum_m E^m z^m + eta (S + S_D) c)
 template <int P>
 __global__ void __launch_bounds__(128) k_full(DevMesh m, DevTables T, const double* __restrict__ E,
-                                              const double* __restrict__ Yin, double wm, double dt, double eta,
-                                              double* __restrict__ out) {
+                                              const double* __restrict__ D, const double* __restrict__ Yin,
+                                              double wm, double dt, double eta, double* __restrict__ out) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
-  const STab<P> tb = stage_tables<P>(sm, T);
+  const STab<P> tb = stage_tables<P, true>(sm, T);
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
   const long Kp = m.Kp;
@@ -374,17 +402,9 @@ __global__ void __launch_bounds__(128) k_full(DevMesh m, DevTables T, const doub
 #pragma unroll
   for (int i = 0; i < N; ++i) acc[i] = 0.0;
 #pragma unroll 1
-  for (int c = 0; c < 2; ++c) {
-    const double* Ec = E + static_cast<long>(c) * 4 * NN * Kp;
-    const double* Zc = Yin + static_cast<long>(c) * N * Kp;
-    block_mv_gather<N>(Ec, Kp, k, Zc, k, acc);
-#pragma unroll 1
-    for (int s = 1; s < 4; ++s) {
-      const int col = e.nbr[s - 1];
-      if (col < 0) continue;
-      block_mv_gather<N>(Ec + static_cast<long>(s) * NN * Kp, Kp, k, Zc, col, acc);
-    }
-  }
+  for (int c = 0; c < 2; ++c)
+    block_mv_gather<N>(E + static_cast<long>(c) * NN * Kp, Kp, k, Yin + static_cast<long>(c) * N * Kp, k, acc);
+  offdiag_all<P>(sm + Cfg<P>::TAB, D, Yin, Kp, e, acc);
   apply_S<P>(tb, m, e, k, C, eta, acc);
   tab_mv_g<N, NP>(tb.M(), C, Kp, k, w);
 #pragma unroll
@@ -410,6 +430,10 @@ __global__ void __launch_bounds__(128) k_bjac_axpy(int K, long Kp, const TP* __r
 template <int P>
 size_t tab_smem() {
   return sizeof(double) * Cfg<P>::TAB;
+}
+template <int P>
+size_t tab_edge_smem() {
+  return sizeof(double) * (Cfg<P>::TAB + Cfg<P>::EDGE);
 }
 
 template <typename Kern>
@@ -456,18 +480,15 @@ void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, d
   ++h.launches;
 }
 
-// precision of the stored E / block-Jacobi blocks a launch reads:
-// FP64 for the Krylov operator, FP32 for the multigrid smoother's copies.
-template <typename TE>
-void stage2_impl(Handle& h, const TE* E, const double* x, double alpha_m, double beta_s, const double* tz,
-                 double gamma_e, const double* w, double delta, double* y) {
-  if (use_rows(h)) return rows_stage2<TE>(h, E, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
+void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
+                   const double* w, double delta, double* y) {
+  if (use_rows(h)) return rows_stage2<double>(h, h.E.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
   const unsigned grid = grid_of(h.K, 128);
-#define CALL(P)                                                                                                \
-  do {                                                                                                         \
-    set_smem(k_stage2<P, TE>, tab_smem<P>());                                                                  \
-    k_stage2<P, TE><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, E, x, alpha_m, beta_s, tz,       \
-                                                            gamma_e, w, delta, y);                             \
+#define CALL(P)                                                                                               \
+  do {                                                                                                        \
+    set_smem(k_stage2<P>, tab_edge_smem<P>());                                                                \
+    k_stage2<P><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, x, alpha_m,  \
+                                                             beta_s, tz, gamma_e, w, delta, y);               \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -475,22 +496,13 @@ void stage2_impl(Handle& h, const TE* E, const double* x, double alpha_m, double
   ++h.launches;
 }
 
-void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
-                   const double* w, double delta, double* y) {
-  stage2_impl<double>(h, h.E.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
-}
-
-void launch_stage2_f32(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz,
-                       double gamma_e, const double* w, double delta, double* y) {
-  stage2_impl<float>(h, h.E32.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
-}
-
 void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double* out) {
   const unsigned grid = grid_of(h.K, 128);
 #define CALL(P)                                                                                                 \
   do {                                                                                                          \
-    set_smem(k_full<P>, tab_smem<P>());                                                                         \
-    k_full<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, Y, wm, dt, h.prob.eta, out);   \
+    set_smem(k_full<P>, tab_edge_smem<P>());                                                                    \
+    k_full<P><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, Y, wm, dt,       \
+                                                           h.prob.eta, out);                                    \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

@@ -181,10 +181,14 @@ __global__ void __launch_bounds__(128) k_rhs(DevMesh m, DevTables T, ldg_coeff c
 
 // ---------------------------------------------------------------- K3
 // out[(m*4 + s)*N*N + i*N + j][k]: s = 0 diagonal block, s = 1+n the block in
-// column nbr[n].  MODE selects E = -G + R + R_D (hot path) or one operator.
-template <int P, int MODE>
+// column nbr[n].  MODE selects E = -G + R + R_D or one operator; kModeEdiag
+// (the solver's per-step assembly) writes only the diagonal blocks,
+// out[m*N*N + i*N + j][k].
+template <int P, int MODE_>
 __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const double* __restrict__ D,
                                                   double* __restrict__ out) {
+  constexpr bool kDiagOnly = MODE_ == kModeEdiag;
+  constexpr int MODE = kDiagOnly ? kModeE : MODE_;
   constexpr int N = Cfg<P>::N, Q = Cfg<P>::QE, NN = N * N;
   extern __shared__ double sm[];
   double* s_g = sm;                    // [i][j][l][2]
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const 
     }
   }
   double* o1 = out;
-  double* o2 = out + 4L * NN * Kp;
+  double* o2 = out + (kDiagOnly ? 1L : 4L) * NN * Kp;
   // diagonal blocks
 #pragma unroll 1
   for (int i = 0; i < N; ++i) {
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const 
       o2[static_cast<long>(i * N + j) * Kp + k] = e2;
     }
   }
+  if constexpr (kDiagOnly) return;
   // off-diagonal blocks: neighbour coefficient, normal and length of the k- side
 #pragma unroll 1
   for (int n = 0; n < 3; ++n) {
@@ -405,6 +410,7 @@ template <int P>
 void launch_assemble_mode(Handle& h, int mode, double* out) {
   switch (mode) {
     case kModeE: launch_assemble_p<P, kModeE>(h, out); break;
+    case kModeEdiag: launch_assemble_p<P, kModeEdiag>(h, out); break;
     case kModeG: launch_assemble_p<P, kModeG>(h, out); break;
     case kModeR: launch_assemble_p<P, kModeR>(h, out); break;
     default: launch_assemble_p<P, kModeRD>(h, out); break;

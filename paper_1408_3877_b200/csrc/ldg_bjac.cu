@@ -1,4 +1,5 @@
-// Block-Jacobi setup of the Schur operator, once per step and level.
+// Block-Jacobi setup of the Schur operator, once per step and level
+// (diagonal E blocks stored, off-diagonal ones matrix-free from D, E_D here).
 //
 //   P_k = wm M_k + dt (eta S_kk - sum_m sum_{j in {k} u nbr(k)} E^m_kj M_j^-1 B^m_jk)
 //
@@ -36,6 +37,7 @@ struct Cfg {
   static constexpr int EPW = 32 / NG;  // elements per warp
   static constexpr int WARPS = 8;
   static constexpr int EPB = EPW * WARPS;
+  static constexpr int Q = (3 * P + 2) / 2;  // edge rule of the off-diagonal E blocks
 };
 
 inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
@@ -51,10 +53,11 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
 
 // OUT: 0 FP64 SoA, 1 FP32 SoA, 2 FP32 packed (ldg_pack.cuh)
 template <int P, int OUT>
-__global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E, double wm,
-                                                   double dt, double eta, void* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E,
+                                                   const double* __restrict__ E_D, double wm, double dt, double eta,
+                                                   void* __restrict__ out) {
   using C = Cfg<P>;
-  constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG;
+  constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG, Q = C::Q;
   __shared__ __align__(16) double s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
   __shared__ double s_piv[C::WARPS][C::EPW][2 * N + 2];
   {
@@ -113,8 +116,8 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
     }
 #pragma unroll 1
     for (int q = 0; q < N; ++q) {
-      const double e1 = E[(static_cast<long>(0) * NN + ir * N + q) * Kp + kk];
-      const double e2 = E[(static_cast<long>(4) * NN + ir * N + q) * Kp + kk];
+      const double e1 = E[(static_cast<long>(ir) * N + q) * Kp + kk];
+      const double e2 = E[(static_cast<long>(NN) + ir * N + q) * Kp + kk];
 #pragma unroll
       for (int t = 0; t < 5; ++t) {
         const double e = c1[t] * e1 + c2[t] * e2;
@@ -123,21 +126,36 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
         for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab[jj * NP], a[jj]);
       }
     }
-    // off-diagonal slots: E^m_{k,j} against M_j^-1 B^m_{j,k} = (nu^m_j |E_j| / (4 |T_j|)) s_off(np, n)
+    // off-diagonal slots: E^m_{k,j} against M_j^-1 B^m_{j,k} = (nu^m_j |E_j| / (4 |T_j|)) s_off(np, n).
+    // E^m_{k,j} = co_m U diag(wd) V^T is matrix-free (ldg_offdiag.cuh): row i of
+    // cx E^1 + cy E^2 is kappa sum_q U[i][q] wd[q] V[:, q], kappa = cx co_1 + cy co_2
 #pragma unroll 1
     for (int s = 1; s < 4; ++s) {
       const int j = m.nbr[(s - 1) * Kp + kk];
       if (j < 0) continue;
-      const int np = m.nbrn[(s - 1) * Kp + kk];
+      const int n = s - 1, np = m.nbrn[n * Kp + kk];
       const double h = -dt * 0.5 * g[(kLen0 + np) * Kp + j] / (2.0 * g[kArea * Kp + j]);
       const double cx = h * g[(kNux0 + np) * Kp + j], cy = h * g[(kNuy0 + np) * Kp + j];
-      const double* tab0 = s_tab + (5 + np * 3 + (s - 1)) * NNP;
-#pragma unroll 1
-      for (int q = 0; q < N; ++q) {
-        const double e = cx * E[(static_cast<long>(s) * NN + ir * N + q) * Kp + kk] +
-                         cy * E[(static_cast<long>(4 + s) * NN + ir * N + q) * Kp + kk];
+      const double hl = 0.5 * g[(kLen0 + n) * Kp + kk];
+      const double kappa = hl * (cx * g[(kNux0 + n) * Kp + kk] + cy * g[(kNuy0 + n) * Kp + kk]);
+      const double* pth = tb + T.pth + (n * 3 + np) * Q * N;  // V^t [q][.]
+      const double* pe = tb + T.pe + n * Q * N;               // U^t [q][.]
+      double aq[Q];
 #pragma unroll
-        for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab0[jj * NP + q], a[jj]);
+      for (int q = 0; q < Q; ++q) {
+        double dv = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) dv = fma(E_D[l * Kp + j], pth[q * N + l], dv);
+        aq[q] = kappa * pe[q * N + ir] * tb[T.we + q] * dv;
+      }
+      const double* tab0 = s_tab + (5 + np * 3 + n) * NNP;
+#pragma unroll 1
+      for (int q2 = 0; q2 < N; ++q2) {
+        double e = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) e = fma(aq[q], pth[q * N + q2], e);
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab0[jj * NP + q2], a[jj]);
       }
     }
   }
@@ -210,11 +228,11 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
   do {                                                                                                        \
     const unsigned grid = grid_of(h.K, Cfg<P>::EPB);                                                          \
     if (out_kind == 0)                                                                                        \
-      k_bjac_warp<P, 0><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, wm, dt, h.prob.eta, out);      \
+      k_bjac_warp<P, 0><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out);      \
     else if (out_kind == 1)                                                                                   \
-      k_bjac_warp<P, 1><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, wm, dt, h.prob.eta, out);      \
+      k_bjac_warp<P, 1><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out);      \
     else                                                                                                      \
-      k_bjac_warp<P, 2><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, wm, dt, h.prob.eta, out);      \
+      k_bjac_warp<P, 2><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out);      \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

@@ -106,6 +106,9 @@ std::unique_ptr<Handle> make_rank(Team& T, int p, const ldg_problem* prob, int r
     h.dtab.fM = F.fM;
     h.dtab.fSd = F.fSd;
     h.dtab.fSo = F.fSo;
+    h.dtab.fpe = F.fpe;
+    h.dtab.fpth = F.fpth;
+    h.dtab.fwe = F.fwe;
   }
   ldgb::upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
   return hp;
@@ -116,7 +119,7 @@ void alloc_step_buffers(Handle& h) {
   const long NN = static_cast<long>(h.N) * h.N;
   h.D.alloc(n, &h.bytes);
   h.F.alloc(n, &h.bytes);
-  h.E.alloc(8 * NN * h.Kp, &h.bytes);
+  h.E.alloc(2 * NN * h.Kp, &h.bytes);  // diagonal blocks; the off-diagonal ones are matrix-free
   h.Vv.alloc(3 * n, &h.bytes);
   h.Y.alloc(3 * n, &h.bytes);
 }
@@ -503,7 +506,8 @@ int ldg_export_operator(ldg_handle* H, int which, int64_t* nnz, int64_t* rows, i
         const auto B = blocks_to_host(h, tmp.ptr, 2);
         ldgb::launch_static(h, ldgb::kStS, tmp.ptr);
         const auto S = blocks_to_host(h, tmp.ptr, 1);
-        const auto E = blocks_to_host(h, h.E.ptr, 2);
+        ldgb::launch_assemble(h, ldgb::kModeE, tmp.ptr);  // all 8 blocks (the solver keeps the diagonal ones)
+        const auto E = blocks_to_host(h, tmp.ptr, 2);
         emit(M, 0, false, 0, 0, 1.0);
         emit(B, 0, true, 0, 2, 1.0);
         emit(M, 0, false, 1, 1, 1.0);
@@ -771,7 +775,7 @@ int ldg_time_kernels(ldg_handle* H, double t, double dt, int reps, int flush, ld
       }
     });
     out->ms_assemble = timed([&] {
-      for (auto& rp : T.ranks) ldgb::launch_assemble(*rp, ldgb::kModeE, rp->E.ptr);
+      for (auto& rp : T.ranks) ldgb::launch_assemble(*rp, ldgb::kModeEdiag, rp->E.ptr);
     });
     for (auto& rp : T.ranks) {
       rp->assembled = true;

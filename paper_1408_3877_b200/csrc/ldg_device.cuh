@@ -10,9 +10,10 @@
 //  topology   nbr[n][k], nbrn[n][k], kind[n][k]   (neighbour k+, its edge n+,
 //             edge kind: interior / Dirichlet / Neumann)
 //  D, F       [N][Kp]          projected d(t) and f(t)
-//  E          [m][s][i*N+j][Kp]  time-dependent C-row blocks
-//                              E^m = -G^m + R^m + R_D^m, slot s = 0 diagonal,
-//                              s = 1+n the block coupling to nbr[n]
+//  E          [m][i*N+j][Kp]     diagonal blocks E^m_kk of the time-dependent
+//                              C-row operator E^m = -G^m + R^m + R_D^m; the
+//                              off-diagonal blocks (pure R^m, rank Qe) are
+//                              evaluated from D in the kernels (ldg_offdiag.cuh)
 //  Bst        [m][s][i*N+j][Kp]  static Z-row blocks B^m = -H^m + Q^m + Q_N^m
 //  Sst        [s][i*N+j][Kp]     static penalty S + S_D (eta applied in SpMV)
 //  vectors    [u][j][Kp]       u = Z1, Z2, C
@@ -44,7 +45,7 @@ struct DevTables {
   // FP32 smoother tables (FTables in ldg_tables.hpp), offsets in floats
   const float* fbase;
   int NF;
-  long fmH, fmSd, fmSo, fM, fSd, fSo;
+  long fmH, fmSd, fmSo, fM, fSd, fSo, fpe, fpth, fwe;
 };
 
 struct DevMesh {

@@ -201,7 +201,9 @@ void build_square_strip(Handle& h, int dim, int a, int b, int stride, int dim_fi
 void build_general_mesh(Handle& h, const double* coords, int nv, const int* v0t, int nt, const int* id_e0t);
 
 // assembly (ldg_assemble.cu)
-enum AsmMode { kModeE = 0, kModeG = 1, kModeR = 2, kModeRD = 3 };
+// kModeE: all 8 blocks [m][s] (exports); kModeEdiag: the diagonal blocks
+// [m] the solver stores (off-diagonal ones are matrix-free, ldg_offdiag.cuh)
+enum AsmMode { kModeE = 0, kModeG = 1, kModeR = 2, kModeRD = 3, kModeEdiag = 4 };
 enum StaticMode { kStB = 0, kStS = 1, kStM = 2, kStH = 3, kStQ = 4, kStQN = 5, kStSint = 6, kStSD = 7 };
 void launch_project(Handle& h, const ldg_coeff& fn, double t, const double* rule_dev, int R, double* out,
                     int count);
@@ -225,8 +227,6 @@ void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor
 void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa);
 
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
-void launch_stage2_f32(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz,
-                       double gamma_e, const double* w, double delta, double* y);
 void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_to_f32(Handle& h, long n, const double* src, float* dst);
 void launch_bjac(Handle& h, double wm, double dt, int out_kind);     // ldg_bjac.cu: 0 Pinv, 1 Pinv32, 2 Pq

@@ -215,7 +215,7 @@ bool mg_build(Handle& h, int team_size) {
                        h.seed);
     const long n = c->vec_len();
     c->D.alloc(n, &c->bytes);
-    c->E.alloc(8 * NN * c->Kp, &c->bytes);
+    c->E.alloc(2 * NN * c->Kp, &c->bytes);  // diagonal blocks (off-diagonal ones matrix-free)
     c->Pinv.alloc(NN * c->Kp, &c->bytes);
     c->tz.alloc(2 * n, &c->bytes);
     c->mg_x.alloc(n, &c->bytes);
@@ -258,10 +258,10 @@ void mg_setup_f32_level(Handle& L, double wm, double dt) {
     launch_bjac_setup_quad(L, wm, dt);
   } else {
     if (!L.E32.ptr) {
-      L.E32.alloc(8 * NN * L.Kp, &L.bytes);
+      L.E32.alloc(2 * NN * L.Kp, &L.bytes);
       L.Pinv32.alloc(NN * L.Kp, &L.bytes);
     }
-    launch_to_f32(L, 8 * NN * L.Kp, L.E.ptr, L.E32.ptr);
+    launch_to_f32(L, 2 * NN * L.Kp, L.E.ptr, L.E32.ptr);
     launch_bjac_setup_f32_from64(L, wm, dt);
   }
 }
@@ -271,7 +271,7 @@ void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
   for (auto& cp : h.coarse) {
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);
-    launch_assemble(c, kModeE, c.E.ptr);
+    launch_assemble(c, kModeEdiag, c.E.ptr);
     if (f32)
       mg_setup_f32_level(c, wm, dt);
     else

@@ -5,8 +5,8 @@
 namespace ldgb {
 
 // Packing of the stored N x N blocks into float4 quads.
-//  flat (p <= 1): the four blocks of component c back to back, column-major,
-//    NN quads per component; streamed fully unrolled.
+//  flat (p <= 1): the block column-major, padded to a multiple of 4 values;
+//    streamed fully unrolled.
 //  chunked (p >= 2): each block on its own, columns grouped CC at a time
 //    (CC*N a multiple of 4, N padded with zero columns to NCOL), QC quads per
 //    group.  The stream is a rolled loop over column groups whose body has a
@@ -24,8 +24,9 @@ struct SmCfg {
   static constexpr int QC = kFlat ? 1 : CC * N / 4;       // quads per column group
   static constexpr int NCH = NCOL / CC;                   // column groups per block
   static constexpr int QS = NCH * QC;                     // quads per block (chunked)
-  static constexpr int QE = kFlat ? NN : 4 * QS;          // quads per component of E
-  static constexpr int QP = kFlat ? (NN + 3) / 4 : QS;    // quads of P^-1
+  static constexpr int QP = kFlat ? (NN + 3) / 4 : QS;    // quads of one packed block (E^m_kk or P^-1)
+  static constexpr int Q = (3 * P + 2) / 2;               // edge rule of the matrix-free off-diagonal E
+  static constexpr int EDGE = (12 * Q * N + Q + 3) / 4 * 4;  // FP32 edge tables (pe, pth, we), padded
   static constexpr int UNR = kFlat ? 1 : (16 / QC > 0 ? 16 / QC : 1);  // groups unrolled per step
 };
 

@@ -16,6 +16,7 @@
 #include <cmath>
 
 #include "ldg_internal.hpp"
+#include "ldg_offdiag.cuh"
 
 namespace ldgb {
 
@@ -27,6 +28,7 @@ template <int P>
 struct Cfg {
   static constexpr int N = (P + 1) * (P + 2) / 2;
   static constexpr int NP = (N % 2) ? N + 1 : N;
+  static constexpr int Q = (3 * P + 2) / 2;  // edge rule of the off-diagonal E blocks
 };
 
 inline unsigned tiles_of(int K) { return static_cast<unsigned>((K + kTile - 1) / kTile); }
@@ -125,18 +127,21 @@ __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_stage1_rows(DevMesh m, De
 }
 
 // y_i = alpha (M x_k)_i + beta ((S + S_D) x)_i - gamma sum_m sum_s (E^m[s] tz^m_col)_i + delta w_i
+// (diagonal E blocks stored, off-diagonal ones matrix-free: ldg_offdiag.cuh)
 template <int P, typename TE>
 __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_stage2_rows(DevMesh m, DevTables T, const TE* __restrict__ E,
+                                                                   const double* __restrict__ D,
                                                                    const double* __restrict__ x, double alpha,
                                                                    double beta, const double* __restrict__ tz,
                                                                    double gamma, const double* __restrict__ w,
                                                                    double delta, double* __restrict__ y) {
-  constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP, NNP = N * NP;
+  constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP, NNP = N * NP, Q = Cfg<P>::Q;
   const RowCtx c = row_ctx(m.K);
   if (!c.live) return;
   const int k = c.k, i = c.i;
   const long Kp = m.Kp;
   const double* tb = T.base;
+  const double* g = m.geom;
   int nbr[3];
 #pragma unroll
   for (int n = 0; n < 3; ++n) nbr[n] = m.nbr[n * Kp + k];
@@ -144,17 +149,24 @@ __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_stage2_rows(DevMesh m, De
   if (tz) {
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
-      const double* tc = tz + static_cast<long>(cc) * N * Kp;
+      const TE* blk = E + (static_cast<long>(cc) * NN + i * N) * Kp + k;
+      const double* tc = tz + static_cast<long>(cc) * N * Kp + k;
+      double part = 0.0;
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const int col = s == 0 ? k : nbr[s - 1];
-        if (col < 0) continue;
-        const TE* blk = E + (static_cast<long>(cc * 4 + s) * NN + i * N) * Kp + k;
-        double part = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) part = fma(static_cast<double>(__ldcs(blk + j * Kp)), tc[j * Kp + col], part);
-        acc += part;
-      }
+      for (int j = 0; j < N; ++j) part = fma(static_cast<double>(__ldcs(blk + j * Kp)), tc[j * Kp], part);
+      acc += part;
+    }
+#pragma unroll 1
+    for (int n = 0; n < 3; ++n) {
+      const int kp = m.nbr[n * Kp + k];
+      if (kp < 0) continue;
+      const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+      const double co1 = hl * g[(kNux0 + n) * Kp + k], co2 = hl * g[(kNuy0 + n) * Kp + k];
+      double z[Q];
+      offdiag_z<N, Q, double>(
+          tb + T.pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, tb + T.we, [&](int j) { return D[j * Kp + kp]; },
+          [&](int j) { return fma(co1, tz[j * Kp + kp], co2 * tz[(N + j) * Kp + kp]); }, z);
+      acc += offdiag_row<N, Q, double>(tb + T.pe + n * Q * N, z, i);
     }
     acc *= -gamma;
   }
@@ -207,8 +219,8 @@ template <typename TE>
 void rows_stage2(Handle& h, const TE* E, const double* x, double alpha, double beta, const double* tz, double gamma,
                  const double* w, double delta, double* y) {
 #define CALL(P)                                                                                           \
-  k_stage2_rows<P, TE><<<tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream>>>(h.mesh(), h.dtab, E, x, alpha, \
-                                                                           beta, tz, gamma, w, delta, y)
+  k_stage2_rows<P, TE><<<tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream>>>(h.mesh(), h.dtab, E, h.D.ptr, x,  \
+                                                                           alpha, beta, tz, gamma, w, delta, y)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

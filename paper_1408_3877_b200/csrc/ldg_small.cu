@@ -18,6 +18,7 @@
 #include <cmath>
 
 #include "ldg_internal.hpp"
+#include "ldg_offdiag.cuh"
 
 namespace ldgb {
 
@@ -33,6 +34,7 @@ struct Cfg {
   // (a warp = 4 consecutive elements of one row: table reads broadcast)
   static constexpr int EPC = (1024 / (8 * N)) / 4 * 4 > 0 ? (1024 / (8 * N)) / 4 * 4 : 4;
   static constexpr int THREADS = EPC * N * 8;
+  static constexpr int Q = (3 * P + 2) / 2;  // edge rule of the off-diagonal E blocks
 };
 
 inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
@@ -131,13 +133,14 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s1_small(DevMesh m, DevTabl
 //   MODE 0: out = r;  MODE 1: out = x + omega P^-1 r
 template <int P, int MODE>
 __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
+                                                              const double* __restrict__ D,
                                                               const double* __restrict__ x,
                                                               const double* __restrict__ tz,
                                                               const double* __restrict__ b, double wm, double dteta,
                                                               double dt, const float* __restrict__ Pinv,
                                                               double omega, double* __restrict__ out) {
   using C = Cfg<P>;
-  constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP;
+  constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, Q = C::Q;
   __shared__ double s_r[N][C::EPC];
   const Item it = item_of<P>(m.K);
   const int k = it.k, i = it.i, l = it.lane;
@@ -146,16 +149,25 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTabl
   if (it.live) {
     const double* g = m.geom;
     const double* tb = T.base;
-    {  // lane (c, s): E^c[s] row i against t^c of the slot's column
+    {  // lane (c, s): E^c[s] row i against t^c of the slot's column; the diagonal
+       // block stored, the off-diagonal ones matrix-free (ldg_offdiag.cuh)
       const int c = l >> 2, s = l & 3;
       const int col = s == 0 ? k : m.nbr[(s - 1) * Kp + k];
-      if (col >= 0) {
-        const float* blk = E + (static_cast<long>(c * 4 + s) * NN + i * N) * Kp + k;
-        const double* tc = tz + static_cast<long>(c) * N * Kp + col;
+      const double* tc = tz + static_cast<long>(c) * N * Kp + col;
+      if (s == 0) {
+        const float* blk = E + (static_cast<long>(c) * NN + i * N) * Kp + k;
         double e = 0.0;
 #pragma unroll
         for (int j = 0; j < N; ++j) e = fma(static_cast<double>(blk[j * Kp]), tc[j * Kp], e);
         part = dt * e;
+      } else if (col >= 0) {
+        const int n = s - 1;
+        const double co = 0.5 * g[(kLen0 + n) * Kp + k] * g[((c == 0 ? kNux0 : kNuy0) + n) * Kp + k];
+        double z[Q];
+        offdiag_z<N, Q, double>(
+            tb + T.pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, tb + T.we, [&](int j) { return D[j * Kp + col]; },
+            [&](int j) { return tc[j * Kp]; }, z);
+        part = dt * co * offdiag_row<N, Q, double>(tb + T.pe + n * Q * N, z, i);
       }
     }
     if (l == 0) {
@@ -219,10 +231,12 @@ void small_stage2(Handle& h, int mode, const double* x, const double* b, double 
   do {                                                                                                         \
     const unsigned grid = grid_of(h.K, Cfg<P>::EPC);                                                           \
     if (mode == 0)                                                                                             \
-      k_s2_small<P, 0><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, x, h.tz.ptr, b,   \
+      k_s2_small<P, 0><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x,       \
+                                                               h.tz.ptr, b,                                   \
                                                                wm, dteta, dt, h.Pinv32.ptr, omega, out);     \
     else                                                                                                       \
-      k_s2_small<P, 1><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, x, h.tz.ptr, b,   \
+      k_s2_small<P, 1><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x,       \
+                                                               h.tz.ptr, b,                                   \
                                                                wm, dteta, dt, h.Pinv32.ptr, omega, out);     \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)

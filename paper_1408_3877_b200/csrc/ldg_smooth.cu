@@ -28,6 +28,7 @@
 
 #include "ldg_internal.hpp"
 #include "ldg_pack.cuh"
+#include "ldg_offdiag.cuh"
 
 namespace ldgb {
 
@@ -176,68 +177,23 @@ __device__ __forceinline__ void group_mv(const TQ* __restrict__ g, long Kp, cons
     }
 }
 
-// acc += sum_s E^m[s] t^m_col(s) for component c (E packed, t FP64 planes)
-template <int P, typename TQ>
-__device__ __forceinline__ void e_component(const TQ* __restrict__ Ec, const double* __restrict__ tc, long Kp,
-                                            int k, const int* __restrict__ nbr, float* acc) {
+// acc += blk v for one packed N x N block (E^m_kk or P_k^-1, ldg_pack.cuh
+// layout), v from `load(j)` (FP32 value of column j)
+template <int P, typename TQ, typename F>
+__device__ __forceinline__ void packed_apply(const TQ* __restrict__ blk, long Kp, F load, float* acc) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN;
-  if constexpr (C::kFlat) {
-    float t[4][N];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int col = s == 0 ? k : nbr[(s - 1) * Kp + k];
-#pragma unroll
-      for (int j = 0; j < N; ++j) t[s][j] = col >= 0 ? static_cast<float>(tc[j * Kp + col]) : 0.f;
-    }
-#pragma unroll
-    for (int q = 0; q < NN; ++q) {
-      const float4 e = ld_quad(Ec + q * Kp);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int v = 4 * q + r, s = v / NN, rem = v % NN;
-        acc[rem % N] = fmaf(comp(e, r), t[s][rem / N], acc[rem % N]);
-      }
-    }
-  } else {
-#pragma unroll 1
-    for (int s = 0; s < 4; ++s) {
-      const int col = s == 0 ? k : nbr[(s - 1) * Kp + k];
-      if (col < 0) continue;
-      const TQ* Es = Ec + static_cast<long>(s) * C::QS * Kp;
-      const double* tcol = tc + col;
-#pragma unroll(C::UNR)
-      for (int ch = 0; ch < C::NCH; ++ch) {
-        float v[C::CC];
-#pragma unroll
-        for (int jj = 0; jj < C::CC; ++jj) {
-          const int j = ch * C::CC + jj;
-          v[jj] = (C::NCOL == N || j < N) ? static_cast<float>(tcol[j * Kp]) : 0.f;
-        }
-        group_mv<N, C::QC, TQ>(Es + static_cast<long>(ch) * C::QC * Kp, Kp, v, acc);
-      }
-    }
-  }
-}
-
-// d = P^-1 r, r from `load(j)` (FP32 value of column j)
-template <int P, typename F>
-__device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long Kp, F load, float* d) {
-  using C = Cfg<P>;
-  constexpr int N = C::N, NN = C::NN;
-#pragma unroll
-  for (int i = 0; i < N; ++i) d[i] = 0.f;
   if constexpr (C::kFlat) {
     float r[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) r[j] = load(j);
 #pragma unroll
     for (int q = 0; q < C::QP; ++q) {
-      const float4 e = __ldcs(Pk + q * Kp);
+      const float4 e = ld_quad(blk + q * Kp);
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
         const int v = 4 * q + rr;
-        if (v < NN) d[v % N] = fmaf(comp(e, rr), r[v / N], d[v % N]);
+        if (v < NN) acc[v % N] = fmaf(comp(e, rr), r[v / N], acc[v % N]);
       }
     }
   } else {
@@ -249,9 +205,17 @@ __device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long K
         const int j = ch * C::CC + jj;
         v[jj] = (C::NCOL == N || j < N) ? load(j) : 0.f;
       }
-      group_mv<N, C::QC, float4>(Pk + static_cast<long>(ch) * C::QC * Kp, Kp, v, d);
+      group_mv<N, C::QC, TQ>(blk + static_cast<long>(ch) * C::QC * Kp, Kp, v, acc);
     }
   }
+}
+
+// d = P^-1 r
+template <int P, typename F>
+__device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long Kp, F load, float* d) {
+#pragma unroll
+  for (int i = 0; i < Cfg<P>::N; ++i) d[i] = 0.f;
+  packed_apply<P, float4>(Pk, Kp, load, d);
 }
 
 // r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
@@ -259,14 +223,20 @@ __device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long K
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
 template <int P, int MODE, typename TQ>
 __global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
-                                             const float* __restrict__ Escale, const double* __restrict__ x,
+                                             const float* __restrict__ Escale, const double* __restrict__ D,
+                                             const double* __restrict__ x,
                                              const double* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const float4* __restrict__ Pq, float omega,
                                              double* __restrict__ out) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
+  constexpr int Q = C::Q;
   extern __shared__ __align__(16) float smf[];
-  const float* tb = stage_f(smf, T.fbase + T.fM, 13 * TAB);  // tM | tSd 3 | tSo 9
+  // tM | tSd 3 | tSo 9 | pe 3 | pth 9 | we (contiguous in the FP32 table buffer)
+  const float* tb = stage_f(smf, T.fbase + T.fM, 13 * TAB + C::EDGE);
+  const float* s_pe = tb + 13 * TAB;
+  const float* s_pth = s_pe + 3 * Q * N;
+  const float* s_we = s_pth + 9 * Q * N;
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
@@ -275,14 +245,39 @@ __global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const TQ* _
   float acc[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) acc[i] = 0.f;
+  // diagonal blocks E^m_kk t^m_k (packed stream), scaled copy
 #pragma unroll 1
-  for (int c = 0; c < 2; ++c)
-    e_component<P, TQ>(Eq + static_cast<long>(c) * C::QE * Kp + k, tz + static_cast<long>(c) * N * Kp, Kp, k,
-                       m.nbr, acc);
-  const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
-  const float es = Escale ? fdt * Escale[k] : fdt;
+  for (int c = 0; c < 2; ++c) {
+    const double* tc = tz + static_cast<long>(c) * N * Kp + k;
+    packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
+                        [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
+  }
+  if (Escale) {
+    const float es = Escale[k];
 #pragma unroll
-  for (int i = 0; i < N; ++i) acc[i] *= es;
+    for (int i = 0; i < N; ++i) acc[i] *= es;
+  }
+  // off-diagonal blocks, matrix-free from D (ldg_offdiag.cuh)
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kp = m.nbr[n * Kp + k];
+    if (kp < 0) continue;
+    const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+    const float co1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
+    const float co2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
+    float z[Q];
+    offdiag_z<N, Q, float>(
+        s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we,
+        [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
+        [&](int j) {
+          return fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
+        },
+        z);
+    offdiag_rows<N, Q, float>(s_pe + n * Q * N, z, 1.0f, acc);
+  }
+  const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
+#pragma unroll
+  for (int i = 0; i < N; ++i) acc[i] *= fdt;
   {
     float xv[N], w[N];
     load_f<N>(x, Kp, k, xv);
@@ -344,53 +339,35 @@ __global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const float4* __res
 
 // Eq[c][q][k] from E[(c*4 + s)*NN + i*N + j][k] (FP64, row-major blocks);
 // one thread per output quad, zero in the padding columns
-// per-element scale of the FP16 copy: max |E| over the element's 8 blocks
+// per-element scale of the FP16 copy: max |E| over the element's 2 diagonal blocks
 template <int P>
 __global__ void k_escale(long Kp, const double* __restrict__ E, float* __restrict__ scale) {
   constexpr int NN = Cfg<P>::NN;
   const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   if (k >= Kp) return;
   double mx = 0.0;
-  for (int v = 0; v < 8 * NN; ++v) mx = fmax(mx, fabs(E[v * Kp + k]));
+  for (int v = 0; v < 2 * NN; ++v) mx = fmax(mx, fabs(E[v * Kp + k]));
   scale[k] = mx > 0.0 ? static_cast<float>(mx) : 1.0f;
 }
 
-__device__ __forceinline__ void put_quad(float4* q, const float* v, float) { *q = make_float4(v[0], v[1], v[2], v[3]); }
-__device__ __forceinline__ void put_quad(uint2* q, const float* v, float inv) {
-  const __half2 a = __floats2half2_rn(v[0] * inv, v[1] * inv), b = __floats2half2_rn(v[2] * inv, v[3] * inv);
-  uint2 u;
-  u.x = *reinterpret_cast<const unsigned*>(&a);
-  u.y = *reinterpret_cast<const unsigned*>(&b);
-  *q = u;
+__device__ __forceinline__ void put_val(float4* q, int r, float v, float) { reinterpret_cast<float*>(q)[r] = v; }
+__device__ __forceinline__ void put_val(uint2* q, int r, float v, float inv) {
+  reinterpret_cast<__half*>(q)[r] = __float2half_rn(v * inv);
 }
 
+// packed copy of the diagonal blocks E[(c*NN + i*N + j)][k] (FP64), one thread
+// per value; the padding slots keep the zeros of the allocation
 template <int P, typename TQ>
 __global__ void k_pack_e(long Kp, const double* __restrict__ E, const float* __restrict__ scale, TQ* __restrict__ Eq) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN;
   const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-  if (t >= 2L * C::QE * Kp) return;
+  if (t >= 2L * NN * Kp) return;
   const long k = t % Kp;
-  const int cq = static_cast<int>(t / Kp);
-  const int c = cq / C::QE, q = cq % C::QE;
-  float v[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    int s, i, j;
-    if (C::kFlat) {
-      const int val = 4 * q + r, rem = val % NN;
-      s = val / NN;
-      j = rem / N;
-      i = rem % N;
-    } else {
-      s = q / C::QS;
-      const int rq = q % C::QS, ch = rq / C::QC, u = (rq % C::QC) * 4 + r;
-      j = ch * C::CC + u / N;
-      i = u % N;
-    }
-    v[r] = j < N ? static_cast<float>(E[(static_cast<long>(c * 4 + s) * NN + i * N + j) * Kp + k]) : 0.f;
-  }
-  put_quad(Eq + t, v, scale ? 1.0f / scale[k] : 1.0f);
+  const int rest = static_cast<int>(t / Kp), c = rest / NN, ij = rest % NN, i = ij / N, j = ij % N;
+  const int v = sm_packed_slot<P>(i, j);
+  put_val(Eq + (static_cast<long>(c) * C::QP + (v >> 2)) * Kp + k, v & 3, static_cast<float>(E[t]),
+          scale ? 1.0f / scale[k] : 1.0f);
 }
 
 template <int P>
@@ -399,7 +376,7 @@ size_t s1_smem() {
 }
 template <int P>
 size_t s2_smem() {
-  return sizeof(float) * 13 * Cfg<P>::N * Cfg<P>::NF;
+  return sizeof(float) * (13 * Cfg<P>::N * Cfg<P>::NF + Cfg<P>::EDGE);
 }
 
 }  // namespace
@@ -429,18 +406,20 @@ void smooth_pack_e(Handle& h) {
   const bool e16 = smoother_e16();
 #define CALL(P)                                                                                            \
   do {                                                                                                     \
-    const long nq = 2L * Cfg<P>::QE * h.Kp;                                                                \
+    const long nq = 2L * Cfg<P>::QP * h.Kp;                                                                \
     if (e16) {                                                                                             \
       if (!h.Eh.ptr) {                                                                                     \
         h.Eh.alloc(nq, &h.bytes);                                                                          \
         h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
       }                                                                                                    \
       k_escale<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr);                  \
-      k_pack_e<P, uint2><<<grid_of(nq, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr, h.Eh.ptr);   \
+      k_pack_e<P, uint2><<<grid_of(2L * Cfg<P>::NN * h.Kp, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr,         \
+                                                                                   h.Escale.ptr, h.Eh.ptr); \
       h.launches += 1;                                                                                     \
     } else {                                                                                               \
       if (!h.Eq.ptr) h.Eq.alloc(nq, &h.bytes);                                                             \
-      k_pack_e<P, float4><<<grid_of(nq, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr, nullptr, h.Eq.ptr);       \
+      k_pack_e<P, float4><<<grid_of(2L * Cfg<P>::NN * h.Kp, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr,        \
+                                                                                    nullptr, h.Eq.ptr);     \
     }                                                                                                      \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
@@ -464,7 +443,8 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
   const float om = static_cast<float>(omega);
   const bool e16 = h.Eh.ptr != nullptr;
 #define LAUNCH(P, M, TQ, EP, SC)                                                                                   \
-  k_s2f<P, M, TQ><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, EP, SC, x, h.tz.ptr, b,  \
+  k_s2f<P, M, TQ><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, EP, SC, h.D.ptr, x,    \
+                                                                      h.tz.ptr, b,                              \
                                                                       wm, dteta, dt, h.Pq.ptr, om, out)
 #define CALL(P)                                                                         \
   do {                                                                                  \

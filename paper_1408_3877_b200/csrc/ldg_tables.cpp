@@ -436,8 +436,15 @@ FTables build_f32_tables(const HostTables& ht) {
   f.fM = f.fmSo + 9 * tab;
   f.fSd = f.fM + tab;
   f.fSo = f.fSd + 3 * tab;
-  f.total = f.fSo + 9 * tab;
+  const long qn = static_cast<long>(L.Qe) * N;
+  f.fpe = f.fSo + 9 * tab;
+  f.fpth = f.fpe + 3 * qn;
+  f.fwe = f.fpth + 9 * qn;
+  f.total = (f.fwe + L.Qe + 3) / 4 * 4;
   f.data.assign(f.total, 0.0f);
+  for (long t = 0; t < 3 * qn; ++t) f.data[f.fpe + t] = static_cast<float>(ht.data[L.pe + t]);
+  for (long t = 0; t < 9 * qn; ++t) f.data[f.fpth + t] = static_cast<float>(ht.data[L.pth + t]);
+  for (int q = 0; q < L.Qe; ++q) f.data[f.fwe + q] = static_cast<float>(ht.data[L.we + q]);
   auto copy = [&](long dst, long src, int count) {  // count tables, NP -> NF row padding
     for (int t = 0; t < count; ++t)
       for (int j = 0; j < N; ++j)

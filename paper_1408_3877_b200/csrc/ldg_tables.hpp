@@ -79,9 +79,10 @@ HostTables build_tables(int p);
 // (one 128-bit shared load per 4 entries), T^t[j][i] at j*NF + i:
 //   [tmH 2 | tmSd 3 | tmSo 9]  stage 1 (m_hat^-1 applied)
 //   [tM 1 | tSd 3 | tSo 9]     stage 2
+//   [pe 3*Qe*N | pth 9*Qe*N | we Qe (padded to 4)]  matrix-free off-diagonal E
 struct FTables {
   int NF = 0;
-  long fmH = 0, fmSd = 0, fmSo = 0, fM = 0, fSd = 0, fSo = 0, total = 0;
+  long fmH = 0, fmSd = 0, fmSo = 0, fM = 0, fSd = 0, fSo = 0, fpe = 0, fpth = 0, fwe = 0, total = 0;
   std::vector<float> data;
 };
 FTables build_f32_tables(const HostTables& ht);

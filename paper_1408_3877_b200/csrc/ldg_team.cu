@@ -235,12 +235,8 @@ void schur_like(Team& T, int level, bool f32, Vec x, double alpha, double beta, 
   halo(T, level, x, 1);
   each(T, level, [&](Handle& L) { launch_stage1(L, nullptr, 0.0, vp(L, x), 1.0, L.tz.ptr); });
   halo(T, level, kTz, 2);
-  each(T, level, [&](Handle& L) {
-    if (f32)
-      launch_stage2_f32(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y));
-    else
-      launch_stage2(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y));
-  });
+  (void)f32;  // the FP32 smoother has its own kernels (f_stage1 / f_stage2)
+  each(T, level, [&](Handle& L) { launch_stage2(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y)); });
 }
 
 void schur_apply(Team& T, double wm, double dt, Vec x, Vec y) {

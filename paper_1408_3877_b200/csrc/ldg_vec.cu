@@ -227,7 +227,7 @@ size_t reduction_scratch() { return static_cast<size_t>(kMaxRed) * kRedBlocks + 
 void assemble_step(Handle& h, double t) {
   launch_project_df(h, t, h.rule_ptr(), h.rule_R());        // K2: d, f (system.hpp:112-113)
   launch_rhs(h, t);                                          // K5: V (system.hpp:142-150)
-  launch_assemble(h, kModeE, h.E.ptr);                       // K3: E^m (system.hpp:115-117)
+  launch_assemble(h, kModeEdiag, h.E.ptr);                   // K3: E^m diagonal blocks (system.hpp:115-117)
   h.assembled = true;
   h.t_assembled = t;
 }
