@@ -219,6 +219,10 @@ def run_ours(args):
     spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
                           boundary=boundary)
     opts = ld.SolverOptions()
+    if args.krylov is not None:
+        opts.krylov = args.krylov
+    if args.restart is not None:
+        opts.restart = args.restart
     systems = []
     for p in ps:
         if world > 1:
@@ -251,7 +255,9 @@ def run_ours(args):
     barrier()
     launches0 = sum(s.info()["launches"] for s in systems)
     per_p = {p: dict(ms=0.0, ms_asm=0.0, ms_solve=0.0, iters=0, applies=0, residual=0.0) for p in ps}
-    clocks = ClockSampler(local).start()
+    clocks = ClockSampler(local)
+    if not args.no_clocks:
+        clocks.start()
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -360,6 +366,9 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--p", default=None, help="comma-separated degrees (overrides the workload's sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi sampler (diagnostics only)")
+    ap.add_argument("--krylov", type=int, default=None, help="0 FGMRES (default), 1 BiCGStab")
+    ap.add_argument("--restart", type=int, default=None, help="FGMRES restart length")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -32,7 +32,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def library_path() -> str:
-    return os.path.join(HERE, "libldg_b200.so")
+    # LDG_B200_LIB: an alternative build of the same library (kernel-tuning
+    # experiments in scripts/); the in-tree build otherwise
+    return os.environ.get("LDG_B200_LIB") or os.path.join(HERE, "libldg_b200.so")
 
 
 class MeshError(RuntimeError):

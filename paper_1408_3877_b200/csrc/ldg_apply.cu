@@ -19,6 +19,15 @@
 #include "ldg_internal.hpp"
 #include "ldg_offdiag.cuh"
 
+// min resident CTAs per SM of the thread-per-element kernels: at p = 4 the
+// register-heavy kernels are latency-bound at 1 CTA; 4 CTAs (<= 128 registers)
+// measured 7-15% faster there and slower at p <= 3 (-DLDG_MINB_STAGE=n overrides)
+#ifdef LDG_MINB_STAGE
+#define LDG_MINB_STAGE_P(P) LDG_MINB_STAGE
+#else
+#define LDG_MINB_STAGE_P(P) ((P) == 4 ? 4 : 1)
+#endif
+
 namespace ldgb {
 
 namespace {
@@ -290,7 +299,7 @@ __device__ __forceinline__ void apply_S(const STab<P>& tb, const DevMesh& m, con
 
 // stage 1: tout^m = M_k^-1 (sigma vz^m + tau sum_s B^m[s] x_col(s))
 template <int P>
-__global__ void __launch_bounds__(128) k_stage1(DevMesh m, DevTables T, const double* __restrict__ vz, double sigma,
+__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1(DevMesh m, DevTables T, const double* __restrict__ vz, double sigma,
                                                 const double* __restrict__ x, double tau, double* __restrict__ tout) {
   constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(128) k_stage1(DevMesh m, DevTables T, const do
 // (the Krylov operator, FP64): stored diagonal blocks streamed, off-diagonal
 // blocks matrix-free from D.
 template <int P>
-__global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const double* __restrict__ E,
+__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage2(DevMesh m, DevTables T, const double* __restrict__ E,
                                                 const double* __restrict__ D, const double* __restrict__ x,
                                                 double alpha, double beta, const double* __restrict__ tz,
                                                 double gamma, const double* __restrict__ w, double delta,
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(128) k_stage2(DevMesh m, DevTables T, const do
 //   out_Zm = dt (M z^m_k + B^m c)
 //   out_C  = wm M c_k + dt (sum_m E^m z^m + eta (S + S_D) c)
 template <int P>
-__global__ void __launch_bounds__(128) k_full(DevMesh m, DevTables T, const double* __restrict__ E,
+__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_full(DevMesh m, DevTables T, const double* __restrict__ E,
                                               const double* __restrict__ D, const double* __restrict__ Yin,
                                               double wm, double dt, double eta, double* __restrict__ out) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
@@ -453,13 +462,15 @@ __global__ void k_to_f32(long n, const double* __restrict__ src, float* __restri
 // instructions, which wins once a level fills the GPU; the row-parallel
 // kernels (ldg_rows.cu) win on small levels, where a thread's serial load
 // chain is the latency (measured at p = 4: fine level 246 vs 354 us, coarse
-// levels 35 vs 90 us; with the packed FP32 smoother the 32768-element level
-// sweeps in 80 us vs 135 us on the row kernels, the 8192-element one in 70 vs
-// 44 us, hence the default of 16384).  LDG_ROWS_BELOW overrides the switch.
+// levels 35 vs 90 us; with the packed FP16/FP32 smoother, matrix-free
+// off-diagonal blocks and loads issued ahead of the FMA chains, the 8192- and
+// 2048-element levels sweep in 27 / 26 us on thread-per-element kernels vs
+// 57 / 54 us otherwise at p = 4, hence the default of 2048).
+// LDG_ROWS_BELOW overrides the switch.
 bool use_rows(const Handle& h) {
   static const long below = [] {
     const char* s = std::getenv("LDG_ROWS_BELOW");
-    return s ? std::atol(s) : 16384L;
+    return s ? std::atol(s) : 2048L;
   }();
   return h.K < below;
 }

@@ -60,4 +60,12 @@ struct DevMesh {
 
 __host__ __device__ inline long plane(long v, long Kp) { return v * Kp; }
 
+// Programmatic dependent launch (launch_pdl, ldg_internal.hpp): a kernel
+// launched with it may start while its stream predecessor drains; it calls
+// pdl_wait() before touching the predecessor's output (everything before the
+// wait may only read launch-invariant data such as the reference tables) and
+// pdl_trigger() to let its own successor start.  Both are no-ops otherwise.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace ldgb

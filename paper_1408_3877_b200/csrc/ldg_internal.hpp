@@ -193,6 +193,25 @@ struct Team {
   }
 };
 
+// Launch with programmatic stream serialisation (PDL): the kernel must call
+// pdl_wait() before reading what its predecessor wrote (ldg_device.cuh).
+// Used for the latency-bound multigrid kernels; LDG_PDL=0 disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LDG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // ---- launchers (defined in the .cu files) ----------------------------------
 // mesh (ldg_mesh.cu)
 void build_square_mesh(Handle& h, int dim, double jitter, uint64_t seed);

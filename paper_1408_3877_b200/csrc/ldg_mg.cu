@@ -15,6 +15,7 @@
 // against the oracle first: 12-27 BiCGStab iterations for p = 1..4
 // independent of h, against 170-2100 with block-Jacobi alone.
 #include <cmath>
+#include <cstdlib>
 
 #include "ldg_internal.hpp"
 
@@ -135,16 +136,26 @@ __global__ void __launch_bounds__(256) k_restrict(int Kc, long Kpc, long Kpf, co
                                                   const double* __restrict__ Pm, const double* __restrict__ rf,
                                                   double* __restrict__ bc) {
   constexpr int N = Cfg<P>::N, NN = N * N;
+  pdl_wait();
+  pdl_trigger();
   const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   if (t >= static_cast<long>(N) * Kc) return;
   const int kc = static_cast<int>(t % Kc), j = static_cast<int>(t / Kc);
+  int ch[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) ch[s] = children[s * Kpc + kc];
   double acc = 0.0;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int k = children[s * Kpc + kc];
+  for (int s = 0; s < 4; ++s) {  // loads of a child first, then its FMA chain (latency-bound on coarse levels)
     const double* Ps = Pm + (static_cast<long>(s) * NN + j) * Kpc + kc;
+    double pv[N], rv[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc = fma(__ldcs(Ps + static_cast<long>(i) * N * Kpc), rf[i * Kpf + k], acc);
+    for (int i = 0; i < N; ++i) {
+      pv[i] = __ldcs(Ps + static_cast<long>(i) * N * Kpc);
+      rv[i] = rf[i * Kpf + ch[s]];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc = fma(pv[i], rv[i], acc);
   }
   bc[j * Kpc + kc] = acc;
 }
@@ -155,6 +166,8 @@ __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf,
                                                      const double* __restrict__ Pm, const double* __restrict__ xc,
                                                      double* __restrict__ xf) {
   constexpr int N = Cfg<P>::N, NN = N * N;
+  pdl_wait();
+  pdl_trigger();
   const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   if (t >= 4L * N * Kc) return;
   const int kc = static_cast<int>(t % Kc);
@@ -162,10 +175,16 @@ __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf,
   const int s = rest % 4, i = rest / 4;
   const int k = children[s * Kpc + kc];
   const double* Ps = Pm + (static_cast<long>(s) * NN + static_cast<long>(i) * N) * Kpc + kc;
-  double acc = 0.0;
+  double pv[N], xv[N];
 #pragma unroll
-  for (int j = 0; j < N; ++j) acc = fma(__ldcs(Ps + static_cast<long>(j) * Kpc), xc[j * Kpc + kc], acc);
-  xf[i * Kpf + k] += acc;
+  for (int j = 0; j < N; ++j) {
+    pv[j] = __ldcs(Ps + static_cast<long>(j) * Kpc);
+    xv[j] = xc[j * Kpc + kc];
+  }
+  double acc = xf[i * Kpf + k];
+#pragma unroll
+  for (int j = 0; j < N; ++j) acc = fma(pv[j], xv[j], acc);
+  xf[i * Kpf + k] = acc;
 }
 
 }  // namespace
@@ -202,6 +221,10 @@ bool mg_build(Handle& h, int team_size) {
     c->p = h.p;
     c->N = h.N;
     c->prob = h.prob;
+    {  // tuning experiment: penalty of the rediscretised coarse operators
+      const char* es = std::getenv("LDG_MG_ETA_SCALE");
+      if (es) c->prob.eta = fine->prob.eta * std::atof(es);
+    }
     c->dtab = h.dtab;
     c->stream = h.stream;
     c->owns_stream = false;
@@ -282,8 +305,8 @@ void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
 // C.mg_b = P^T L.mg_r (restriction of the fine residual to the coarse level)
 void mg_restrict(Handle& L, Handle& C) {
 #define CALL(PP)                                                                                             \
-  k_restrict<PP><<<grid_of(static_cast<long>(L.N) * C.K, 256), 256, 0, L.stream>>>(                        \
-      C.K, C.Kp, L.Kp, C.mg_children.ptr, C.mg_P.ptr, L.mg_r.ptr, C.mg_b.ptr)
+  launch_pdl(k_restrict<PP>, grid_of(static_cast<long>(L.N) * C.K, 256), 256, 0, L.stream, C.K, C.Kp, L.Kp,      \
+             C.mg_children.ptr, C.mg_P.ptr, L.mg_r.ptr, C.mg_b.ptr)
   LDG_DISPATCH_P(L.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
@@ -293,8 +316,8 @@ void mg_restrict(Handle& L, Handle& C) {
 // x += P C.mg_x (prolongation of the coarse correction)
 void mg_prolong_add(Handle& L, Handle& C, double* x) {
 #define CALL(PP)                                                                                              \
-  k_prolong_add<PP><<<grid_of(4L * L.N * C.K, 256), 256, 0, L.stream>>>(C.K, C.Kp, L.Kp, C.mg_children.ptr,  \
-                                                                        C.mg_P.ptr, C.mg_x.ptr, x)
+  launch_pdl(k_prolong_add<PP>, grid_of(4L * L.N * C.K, 256), 256, 0, L.stream, C.K, C.Kp, L.Kp,                \
+             C.mg_children.ptr, C.mg_P.ptr, C.mg_x.ptr, x)
   LDG_DISPATCH_P(L.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

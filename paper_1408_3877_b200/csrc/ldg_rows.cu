@@ -60,9 +60,15 @@ __device__ __forceinline__ RowCtx row_ctx(int K) {
 template <int N, int NP>
 __device__ __forceinline__ double row_dot(const double* __restrict__ tab, int i, const double* __restrict__ x,
                                           long Kp, int col) {
+  double tv[N], xv[N];  // loads first, then the chain (see ldg_small.cu trow)
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    tv[j] = __ldg(tab + j * NP + i);
+    xv[j] = x[j * Kp + col];
+  }
   double s = 0.0;
 #pragma unroll
-  for (int j = 0; j < N; ++j) s = fma(__ldg(tab + j * NP + i), x[j * Kp + col], s);
+  for (int j = 0; j < N; ++j) s = fma(tv[j], xv[j], s);
   return s;
 }
 
@@ -74,6 +80,8 @@ __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_stage1_rows(DevMesh m, De
                                                                    const double* __restrict__ x, double tau,
                                                                    double* __restrict__ tout) {
   constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP, NNP = N * NP;
+  pdl_wait();
+  pdl_trigger();
   const RowCtx c = row_ctx(m.K);
   if (!c.live) return;
   const int k = c.k, i = c.i;
@@ -136,6 +144,8 @@ __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_stage2_rows(DevMesh m, De
                                                                    double gamma, const double* __restrict__ w,
                                                                    double delta, double* __restrict__ y) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP, NNP = N * NP, Q = Cfg<P>::Q;
+  pdl_wait();
+  pdl_trigger();
   const RowCtx c = row_ctx(m.K);
   if (!c.live) return;
   const int k = c.k, i = c.i;
@@ -193,6 +203,8 @@ __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_bjac_rows(int K, long Kp,
                                                                  const double* __restrict__ x, double omega,
                                                                  double beta, double* __restrict__ y) {
   constexpr int N = Cfg<P>::N;
+  pdl_wait();
+  pdl_trigger();
   const RowCtx c = row_ctx(K);
   if (!c.live) return;
   const int k = c.k, i = c.i;
@@ -207,8 +219,8 @@ __global__ void __launch_bounds__(kTile * Cfg<P>::N) k_bjac_rows(int K, long Kp,
 
 void rows_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout) {
 #define CALL(P)                                                                                         \
-  k_stage1_rows<P><<<tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream>>>(h.mesh(), h.dtab, vz, sigma, x, \
-                                                                       tau, tout)
+  launch_pdl(k_stage1_rows<P>, tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream, h.mesh(), h.dtab, vz, sigma, x, \
+             tau, tout)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
@@ -219,8 +231,8 @@ template <typename TE>
 void rows_stage2(Handle& h, const TE* E, const double* x, double alpha, double beta, const double* tz, double gamma,
                  const double* w, double delta, double* y) {
 #define CALL(P)                                                                                           \
-  k_stage2_rows<P, TE><<<tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream>>>(h.mesh(), h.dtab, E, h.D.ptr, x,  \
-                                                                           alpha, beta, tz, gamma, w, delta, y)
+  launch_pdl(k_stage2_rows<P, TE>, tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream, h.mesh(), h.dtab, E, h.D.ptr, \
+             x, alpha, beta, tz, gamma, w, delta, y)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
@@ -234,7 +246,7 @@ template void rows_stage2<float>(Handle&, const float*, const double*, double, d
 template <typename TP>
 void rows_bjac(Handle& h, const TP* Pinv, const double* x, double omega, double beta, double* y) {
 #define CALL(P) \
-  k_bjac_rows<P, TP><<<tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream>>>(h.K, h.Kp, Pinv, x, omega, beta, y)
+  launch_pdl(k_bjac_rows<P, TP>, tiles_of(h.K), kTile * Cfg<P>::N, 0, h.stream, h.K, h.Kp, Pinv, x, omega, beta, y)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

@@ -30,9 +30,10 @@ struct Cfg {
   static constexpr int NN = N * N;
   static constexpr int NP = (N % 2) ? N + 1 : N;
   static constexpr int NNP = N * NP;
-  // elements per CTA: <= 1024 threads of 8 lanes x N rows, a multiple of 4
-  // (a warp = 4 consecutive elements of one row: table reads broadcast)
-  static constexpr int EPC = (1024 / (8 * N)) / 4 * 4 > 0 ? (1024 / (8 * N)) / 4 * 4 : 4;
+  // elements per CTA: ~512 threads of 8 lanes x N rows, a multiple of 4 (a
+  // warp = 4 consecutive elements of one row: table reads broadcast); small
+  // CTAs leave each thread the registers to issue all its loads up front
+  static constexpr int EPC = (512 / (8 * N)) / 4 * 4 > 0 ? (512 / (8 * N)) / 4 * 4 : 4;
   static constexpr int THREADS = EPC * N * 8;
   static constexpr int Q = (3 * P + 2) / 2;  // edge rule of the off-diagonal E blocks
 };
@@ -73,22 +74,33 @@ __device__ __forceinline__ double lane_sum8(double v) {
   return v;
 }
 
-// (T x[.][col])_i, T^t[j][i] at tab + j*NP + i
+// (T x[.][col])_i, T^t[j][i] at tab + j*NP + i.  All 2N loads are issued
+// before the FMA chain: these kernels are a handful of dependent load rounds
+// (with the loads interleaved into the chain ptxas left ~2 in flight and a
+// 8-element level took ~11 us per launch).
 template <int N, int NP>
 __device__ __forceinline__ double trow(const double* __restrict__ tab, int i, const double* __restrict__ x, long Kp,
                                        int col) {
+  double tv[N], xv[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    tv[j] = __ldg(tab + j * NP + i);
+    xv[j] = x[j * Kp + col];
+  }
   double s = 0.0;
 #pragma unroll
-  for (int j = 0; j < N; ++j) s = fma(__ldg(tab + j * NP + i), x[j * Kp + col], s);
+  for (int j = 0; j < N; ++j) s = fma(tv[j], xv[j], s);
   return s;
 }
 
 // tout^m_i = (1/2|T|) (mhat^-1 B^m x)_i with the premultiplied tables
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS) k_s1_small(DevMesh m, DevTables T, const double* __restrict__ x,
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s1_small(DevMesh m, DevTables T, const double* __restrict__ x,
                                                               double* __restrict__ tout) {
   using C = Cfg<P>;
   constexpr int N = C::N, NP = C::NP, NNP = C::NNP;
+  pdl_wait();
+  pdl_trigger();
   const Item it = item_of<P>(m.K);
   const int k = it.live ? it.k : 0, i = it.i, l = it.lane;  // dead items compute on element 0, never store
   const long Kp = m.Kp;
@@ -132,7 +144,7 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s1_small(DevMesh m, DevTabl
 // r_i = b_i - [wm M x + dt (eta (S + S_D) x - sum_m E^m t^m)]_i, then
 //   MODE 0: out = r;  MODE 1: out = x + omega P^-1 r
 template <int P, int MODE>
-__global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
                                                               const double* __restrict__ D,
                                                               const double* __restrict__ x,
                                                               const double* __restrict__ tz,
@@ -142,6 +154,8 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTabl
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, Q = C::Q;
   __shared__ double s_r[N][C::EPC];
+  pdl_wait();
+  pdl_trigger();
   const Item it = item_of<P>(m.K);
   const int k = it.k, i = it.i, l = it.lane;
   const long Kp = m.Kp;
@@ -156,17 +170,29 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTabl
       const double* tc = tz + static_cast<long>(c) * N * Kp + col;
       if (s == 0) {
         const float* blk = E + (static_cast<long>(c) * NN + i * N) * Kp + k;
+        float ev[N];
+        double tv[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          ev[j] = blk[j * Kp];
+          tv[j] = tc[j * Kp];
+        }
         double e = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) e = fma(static_cast<double>(blk[j * Kp]), tc[j * Kp], e);
+        for (int j = 0; j < N; ++j) e = fma(static_cast<double>(ev[j]), tv[j], e);
         part = dt * e;
       } else if (col >= 0) {
         const int n = s - 1;
         const double co = 0.5 * g[(kLen0 + n) * Kp + k] * g[((c == 0 ? kNux0 : kNuy0) + n) * Kp + k];
-        double z[Q];
+        double dv[N], uv[N], z[Q];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          dv[j] = D[j * Kp + col];
+          uv[j] = tc[j * Kp];
+        }
         offdiag_z<N, Q, double>(
-            tb + T.pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, tb + T.we, [&](int j) { return D[j * Kp + col]; },
-            [&](int j) { return tc[j * Kp]; }, z);
+            tb + T.pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, tb + T.we, [&](int j) { return dv[j]; },
+            [&](int j) { return uv[j]; }, z);
         part = dt * co * offdiag_row<N, Q, double>(tb + T.pe + n * Q * N, z, i);
       }
     }
@@ -200,10 +226,12 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_s2_small(DevMesh m, DevTabl
 
 // out = omega P^-1 b
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS) k_bj_small(int K, long Kp, const float* __restrict__ Pinv,
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_bj_small(int K, long Kp, const float* __restrict__ Pinv,
                                                               const double* __restrict__ b, double omega,
                                                               double* __restrict__ out) {
   constexpr int N = Cfg<P>::N;
+  pdl_wait();
+  pdl_trigger();
   const Item it = item_of<P>(K);
   const int k = it.live ? it.k : 0, i = it.i, l = it.lane;
   const float* row = Pinv + static_cast<long>(i) * N * Kp + k;
@@ -217,7 +245,7 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS) k_bj_small(int K, long Kp, co
 
 void small_stage1(Handle& h, const double* x) {
 #define CALL(P)                                                                                          \
-  k_s1_small<P><<<grid_of(h.K, Cfg<P>::EPC), Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, x, h.tz.ptr)
+  launch_pdl(k_s1_small<P>, grid_of(h.K, Cfg<P>::EPC), Cfg<P>::THREADS, 0, h.stream, h.mesh(), h.dtab, x, h.tz.ptr)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
@@ -231,13 +259,11 @@ void small_stage2(Handle& h, int mode, const double* x, const double* b, double 
   do {                                                                                                         \
     const unsigned grid = grid_of(h.K, Cfg<P>::EPC);                                                           \
     if (mode == 0)                                                                                             \
-      k_s2_small<P, 0><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x,       \
-                                                               h.tz.ptr, b,                                   \
-                                                               wm, dteta, dt, h.Pinv32.ptr, omega, out);     \
+      launch_pdl(k_s2_small<P, 0>, grid, Cfg<P>::THREADS, 0, h.stream, h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x, \
+                 h.tz.ptr, b, wm, dteta, dt, h.Pinv32.ptr, omega, out);                                       \
     else                                                                                                       \
-      k_s2_small<P, 1><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x,       \
-                                                               h.tz.ptr, b,                                   \
-                                                               wm, dteta, dt, h.Pinv32.ptr, omega, out);     \
+      launch_pdl(k_s2_small<P, 1>, grid, Cfg<P>::THREADS, 0, h.stream, h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x, \
+                 h.tz.ptr, b, wm, dteta, dt, h.Pinv32.ptr, omega, out);                                       \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -247,8 +273,8 @@ void small_stage2(Handle& h, int mode, const double* x, const double* b, double 
 
 void small_zero(Handle& h, const double* b, double omega, double* out) {
 #define CALL(P)                                                                                              \
-  k_bj_small<P><<<grid_of(h.K, Cfg<P>::EPC), Cfg<P>::THREADS, 0, h.stream>>>(h.K, h.Kp, h.Pinv32.ptr, b, omega, \
-                                                                             out)
+  launch_pdl(k_bj_small<P>, grid_of(h.K, Cfg<P>::EPC), Cfg<P>::THREADS, 0, h.stream, h.K, h.Kp, h.Pinv32.ptr, b, \
+             omega, out)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

@@ -30,6 +30,15 @@
 #include "ldg_pack.cuh"
 #include "ldg_offdiag.cuh"
 
+// min resident CTAs per SM of the thread-per-element kernels: at p = 4 the
+// register-heavy kernels are latency-bound at 1 CTA; 4 CTAs (<= 128 registers)
+// measured 7-15% faster there and slower at p <= 3 (-DLDG_MINB_SMOOTH=n overrides)
+#ifdef LDG_MINB_SMOOTH
+#define LDG_MINB_SMOOTH_P(P) LDG_MINB_SMOOTH
+#else
+#define LDG_MINB_SMOOTH_P(P) ((P) == 4 ? 4 : 1)
+#endif
+
 namespace ldgb {
 
 namespace {
@@ -87,11 +96,13 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
 
 // tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
 template <int P>
-__global__ void __launch_bounds__(128) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
+__global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
                                              double* __restrict__ tout) {
   constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
   extern __shared__ __align__(16) float smf[];
   const float* tb = stage_f(smf, T.fbase + T.fmH, 14 * TAB);  // tmH 2 | tmSd 3 | tmSo 9
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
   const long Kp = m.Kp;
@@ -222,7 +233,7 @@ __device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long K
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
 template <int P, int MODE, typename TQ>
-__global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
+__global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
                                              const double* __restrict__ x,
                                              const double* __restrict__ tz, const double* __restrict__ b, double wm,
@@ -238,6 +249,8 @@ __global__ void __launch_bounds__(128) k_s2f(DevMesh m, DevTables T, const TQ* _
   const float* s_pth = s_pe + 3 * Q * N;
   const float* s_we = s_pth + 9 * Q * N;
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
   const long Kp = m.Kp;
@@ -329,6 +342,8 @@ template <int P>
 __global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const float4* __restrict__ Pq,
                                              const double* __restrict__ b, float omega, double* __restrict__ out) {
   constexpr int N = Cfg<P>::N;
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   float d[N];
@@ -430,7 +445,7 @@ void smooth_pack_e(Handle& h) {
 
 void smooth_stage1(Handle& h, const double* x) {
 #define CALL(P)                                                                            \
-  k_s1f<P><<<grid_of(h.K, 128), 128, s1_smem<P>(), h.stream>>>(h.mesh(), h.dtab, x, h.tz.ptr)
+  launch_pdl(k_s1f<P>, grid_of(h.K, 128), 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
@@ -443,9 +458,8 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
   const float om = static_cast<float>(omega);
   const bool e16 = h.Eh.ptr != nullptr;
 #define LAUNCH(P, M, TQ, EP, SC)                                                                                   \
-  k_s2f<P, M, TQ><<<grid_of(h.K, 128), 128, s2_smem<P>(), h.stream>>>(h.mesh(), h.dtab, EP, SC, h.D.ptr, x,    \
-                                                                      h.tz.ptr, b,                              \
-                                                                      wm, dteta, dt, h.Pq.ptr, om, out)
+  launch_pdl(k_s2f<P, M, TQ>, grid_of(h.K, 128), 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr, \
+             x, h.tz.ptr, b, wm, dteta, dt, h.Pq.ptr, om, out)
 #define CALL(P)                                                                         \
   do {                                                                                  \
     if (e16) {                                                                          \
@@ -469,7 +483,7 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
 
 void smooth_zero(Handle& h, const double* b, double omega, double* out) {
 #define CALL(P)                                                                                        \
-  k_bjf<P><<<grid_of(h.K, 128), 128, 0, h.stream>>>(h.K, h.Kp, h.Pq.ptr, b, static_cast<float>(omega), out)
+  launch_pdl(k_bjf<P>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Pq.ptr, b, static_cast<float>(omega), out)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

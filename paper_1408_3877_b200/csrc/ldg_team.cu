@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ldg_internal.hpp"
@@ -34,10 +35,19 @@ double* dots_result(Handle& h);
 
 namespace {
 
-constexpr double kOmega = 0.7;   // damped block-Jacobi smoother
-constexpr int kPre = 2;          // pre-smoothing sweeps (the first from x = 0 is residual-free)
-constexpr int kPost = 2;         // post-smoothing sweeps (V(2,1) measured slower: +20-40% iterations)
-constexpr int kCoarseSweeps = 2;
+// V-cycle parameters (LDG_MG_* environment overrides for tuning runs)
+double env_or(const char* name, double dflt) {
+  const char* s = std::getenv(name);
+  return s ? std::atof(s) : dflt;
+}
+const double kOmega = env_or("LDG_MG_OMEGA", 0.7);  // damped block-Jacobi smoother
+const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));    // pre-smoothing sweeps (the first from x = 0 is residual-free)
+const int kPost = static_cast<int>(env_or("LDG_MG_POST", 2));  // post-smoothing sweeps (V(2,1) measured slower: +20-40% iterations)
+const int kPre0 = static_cast<int>(env_or("LDG_MG_PRE0", kPre));    // level 0
+const int kPost0 = static_cast<int>(env_or("LDG_MG_POST0", kPost));  // level 0
+const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
+int pre_of(int l) { return l == 0 ? kPre0 : kPre; }
+int post_of(int l) { return l == 0 ? kPost0 : kPost; }
 
 #define LDG_NCCL(call)                                                                          \
   do {                                                                                          \
@@ -339,12 +349,12 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   const bool coarsest = l == levels(T) - 1;
   // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
   // (every rank keeps a column), so a larger coarsest grid gets more sweeps
-  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (kPre - 1) + kPost;
+  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(l) - 1) + post_of(l);
   if (fused(T, l, f32)) {
     Vec cur = (sweeps % 2) ? kMgS : x;
     auto other = [&](Vec v) { return v == x ? kMgS : x; };
     each(T, l, [&](Handle& L) { f_zero(L, b, cur); });
-    const int pre = coarsest ? sweeps : kPre - 1;
+    const int pre = coarsest ? sweeps : pre_of(l) - 1;
     for (int s = 0; s < pre; ++s) {
       sweep_f(T, l, wm, dt, b, cur, other(cur));
       cur = other(cur);
@@ -354,7 +364,7 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
-    for (int s = 0; s < kPost; ++s) {
+    for (int s = 0; s < post_of(l); ++s) {
       sweep_f(T, l, wm, dt, b, cur, other(cur));
       cur = other(cur);
     }

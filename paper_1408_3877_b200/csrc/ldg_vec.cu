@@ -4,6 +4,7 @@
 // between the element-interleaved device vectors and the reference's
 // k-major host vectors, and the per-rank assembly step.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ldg_internal.hpp"
@@ -179,6 +180,15 @@ __global__ void k_kmajor_to_soa(int K, int N, long Kp, int nvec, const double* _
   }
 
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* s = std::getenv("LDG_PDL");
+    return !(s && std::atoi(s) == 0);
+  }();
+  return on;
+}
+
 void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, const double* y, double c,
                      const double* z, double* out) {
   k_lincomb3<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, a, x, b, y, c, z, out);
