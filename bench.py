@@ -54,30 +54,60 @@ def e_int(dim):
     return 3 * dim * dim - 2 * dim
 
 
+def packed_quads(p):
+    """float4-sized quads of one packed N x N block (paper_1408_3877_b200/csrc/ldg_pack.cuh)."""
+    n = n_of(p)
+    if p <= 1:
+        return (n * n + 3) // 4
+    cc = 2 if n % 2 == 0 else 4
+    ncol = (n + cc - 1) // cc * cc
+    return ncol * n // 4
+
+
 def bytes_schur(dim, p):
     """Compulsory bytes of one Schur-operator apply (k_stage1 + k_stage2):
-    the time-dependent E^1, E^2 blocks (K + 2 E_int blocks each, the only stored
-    blocks: M, B^m and S are rebuilt from shared-memory tables), the vectors
-    x (read twice), t^1, t^2 (written, read), y (written) and the per-element
-    geometry/topology (area, 3 lengths, 6 normal components; 3 nbr, 3 nbrn, 3 kind)."""
+    the stored diagonal blocks E^1_kk, E^2_kk (FP64; the off-diagonal E blocks are
+    evaluated from D, the static M, B^m, S from shared-memory tables), the vectors
+    x (read by both stages), t^1, t^2 (written, read), D (read), y (written) and the
+    per-element geometry/topology (area, 3 lengths, 6 normal components, B (4);
+    3 nbr, 3 nbrn, 3 kind)."""
     K, N = 2 * dim * dim, n_of(p)
-    blocks = 2 * N * N * (K + 2 * e_int(dim))
-    vectors = 7 * K * N
-    geometry = 2 * 10 * K
+    blocks = 2 * N * N * K
+    vectors = (2 + 4 + 1 + 1) * K * N
+    geometry = 2 * 14 * K
     return 8 * (blocks + vectors + geometry) + 4 * 2 * 9 * K
 
 
+def bytes_sweep_s2(dim, p):
+    """Compulsory bytes of the level-0 smoother stage 2 with the fused block-Jacobi
+    update (k_s2f, FP16 packed E diagonal blocks + per-element scale, FP32 packed
+    P^-1): E 2 blocks x quads x 8 B, P quads x 16 B, vectors x, t (2), D, b, out
+    (FP64), geometry (10 doubles) and topology (9 ints)."""
+    K, N = 2 * dim * dim, n_of(p)
+    q = packed_quads(p)
+    return K * (2 * q * 8 + 4 + q * 16 + 8 * 6 * N + 8 * 10 + 4 * 9)
+
+
 def bytes_asm(dim, p):
+    """Assembly as run by the solver (kModeEdiag): writes the 2 diagonal blocks,
+    reads D: 8*2*N^2*K + 8*K*N (+ geometry).  SURVEY.md §8d's B_asm assumes all
+    8 blocks are written (8*2*N^2*(K + 2 E_int) + 8*K*N); see bytes_asm_survey."""
+    K, N = 2 * dim * dim, n_of(p)
+    return 8 * 2 * N * N * K + 8 * K * N + 8 * 16 * K
+
+
+def bytes_asm_survey(dim, p):
     """8*2*N^2*(K + 2 E_int) + 8*K*N."""
     K, N = 2 * dim * dim, n_of(p)
     return 8 * 2 * N * N * (K + 2 * e_int(dim)) + 8 * K * N
 
 
 def bytes_full_compulsory(dim, p):
-    """Compulsory bytes of the full (W + dt A) Y apply as implemented: E blocks
-    streamed, static blocks rebuilt from tables, Y (3 vectors, read twice), out."""
+    """Compulsory bytes of the full (W + dt A) Y apply as implemented: diagonal E
+    blocks streamed, off-diagonal ones from D, static blocks from tables, Y (3
+    vectors), D, out (3 vectors), geometry/topology."""
     K, N = 2 * dim * dim, n_of(p)
-    return 8 * (2 * N * N * (K + 2 * e_int(dim)) + 9 * K * N + 20 * K) + 72 * K
+    return 8 * (2 * N * N * K + 7 * K * N + 14 * K) + 36 * K
 
 
 def bytes_spmv(dim, p):
@@ -298,23 +328,27 @@ def run_ours(args):
     for p, s in zip(ps, systems):
         kern[p] = s.time_kernels(s.t, dt, reps=5, flush=True)
     kloc = dim if world == 1 else None  # per-rank byte counts below assume one GPU
-    # dominant kernel = the Schur operator apply (stage1 + stage2) at the p with the largest share
-    shares = {p: kern[p]["ms_schur"] * per_p[p]["applies"] / max(total_ms, 1e-9) for p in ps}
+    # dominant kernel: stage 2 of the level-0 multigrid smoother (k_s2f; 3 sweep
+    # launches + 1 residual launch per V-cycle, one V-cycle per FGMRES iteration),
+    # taken at the p where it holds the largest share of the step
+    shares = {p: kern[p]["ms_sweep_s2"] * 4 * per_p[p]["iters"] / max(total_ms, 1e-9) for p in ps}
     pd = max(shares, key=shares.get)
     roof = None
     if kloc is not None:
-        bs = bytes_schur(dim, pd)
-        achieved = bs / (kern[pd]["ms_schur"] * 1e-3) / 1e9
-        roof = {"kernel": f"schur_apply (stage1+stage2), p={pd}", "bound": "hbm", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                "peak_source": peak_src, "share_of_step_bicgstab_applies": shares[pd],
-                "bytes_per_launch": bs,
-                "others": {str(p): {"assemble_GBps": bytes_asm(dim, p) / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
-                                    "spmv_compulsory_GBps": bytes_full_compulsory(dim, p)
+        bs = bytes_sweep_s2(dim, pd)
+        achieved = bs / (kern[pd]["ms_sweep_s2"] * 1e-3) / 1e9
+        roof = {"kernel": f"k_s2f (level-0 smoother stage 2 + block-Jacobi update, FP16 E), p={pd}",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": peak_src, "share_of_step_est": shares[pd], "bytes_per_launch": bs,
+                "others": {str(p): {"sweep_s2_GBps": bytes_sweep_s2(dim, p) / (kern[p]["ms_sweep_s2"] * 1e-3) / 1e9,
+                                    "schur_apply_GBps": bytes_schur(dim, p) / (kern[p]["ms_schur"] * 1e-3) / 1e9,
+                                    "assemble_GBps": bytes_asm(dim, p) / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
+                                    "full_apply_compulsory_GBps": bytes_full_compulsory(dim, p)
                                     / (kern[p]["ms_spmv"] * 1e-3) / 1e9,
-                                    "spmv_effective_GBps_survey_formula": bytes_spmv(dim, p)
+                                    "full_apply_effective_GBps_survey_formula": bytes_spmv(dim, p)
                                     / (kern[p]["ms_spmv"] * 1e-3) / 1e9,
-                                    "schur_GBps": bytes_schur(dim, p) / (kern[p]["ms_schur"] * 1e-3) / 1e9,
+                                    "assemble_effective_GBps_survey_formula": bytes_asm_survey(dim, p)
+                                    / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
                                     "ms": kern[p]} for p in ps}}
 
     cpu = None

@@ -220,6 +220,7 @@ typedef struct ldg_kernel_times {
   int levels;           /* multigrid levels timed below (0: no FK hierarchy) */
   double ms_vcycle;     /* one preconditioner V-cycle (FP32 smoother), graph replay, L2 warm */
   double ms_level[8];   /* one smoothing sweep (residual + block-Jacobi) on level l, graph replay */
+  double ms_sweep_s2;   /* level-0 smoother stage 2 + block-Jacobi update, one launch (L2 flushed if asked) */
 } ldg_kernel_times;
 
 /* Times each hot kernel over reps launches with CUDA events on the handle's

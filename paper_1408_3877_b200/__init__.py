@@ -79,7 +79,7 @@ class _Info(C.Structure):
 class _Times(C.Structure):
     _fields_ = [("ms_project", C.c_double), ("ms_assemble", C.c_double), ("ms_spmv", C.c_double),
                 ("ms_schur", C.c_double), ("reps", C.c_int), ("levels", C.c_int), ("ms_vcycle", C.c_double),
-                ("ms_level", C.c_double * 8)]
+                ("ms_level", C.c_double * 8), ("ms_sweep_s2", C.c_double)]
 
 
 _dp = C.POINTER(C.c_double)

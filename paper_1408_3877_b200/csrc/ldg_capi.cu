@@ -786,6 +786,11 @@ int ldg_time_kernels(ldg_handle* H, double t, double dt, int reps, int flush, ld
     for (double& v : out->ms_level) v = 0.0;
     out->ms_vcycle = 0.0;
     out->levels = ldgb::team_time_mg(T, 1.0, dt, reps, &out->ms_vcycle, out->ms_level, 8);
+    out->ms_sweep_s2 = 0.0;
+    if (out->levels > 0) {
+      ldgb::team_sweep_s2_prepare(T, 1.0, dt);
+      out->ms_sweep_s2 = timed([&] { ldgb::team_sweep_s2(T, 1.0, dt); });
+    }
   });
 }
 

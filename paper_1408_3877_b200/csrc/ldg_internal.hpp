@@ -290,6 +290,8 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
 void team_full_apply(Team& T, double wm, double dt);        // full_y = (W + dt A) Y, halos refreshed
 void team_schur_apply_c(Team& T, double wm, double dt);     // kr_v = S_c C (kernel timing)
 int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, double* ms_level, int max_levels);
+void team_sweep_s2_prepare(Team& T, double wm, double dt);  // multigrid set up, level-0 stage 1 done
+void team_sweep_s2(Team& T, double wm, double dt);          // one level-0 smoother stage-2 launch
 
 // multigrid (ldg_mg.cu)
 int mg_depth(int dim, int team_size);

@@ -791,6 +791,18 @@ void team_full_apply(Team& T, double wm, double dt) {
 // Schur operator apply on level-0 buffers C -> kr_v (kernel timing)
 void team_schur_apply_c(Team& T, double wm, double dt) { schur_apply(T, wm, dt, kC, kV); }
 
+// The dominant kernel of the step for the roofline (kernel timing): stage 2
+// of one level-0 smoothing sweep (fused block-Jacobi update), on the
+// level's current operators, from kPh into the scratch vector.
+void team_sweep_s2_prepare(Team& T, double wm, double dt) {
+  bool f32 = false;
+  prepare_precond(T, 2, wm, dt, &f32);
+  each(T, 0, [&](Handle& L) { f_stage1(L, kPh); });
+}
+void team_sweep_s2(Team& T, double wm, double dt) {
+  each(T, 0, [&](Handle& L) { f_stage2(L, 1, kPh, kP, wm, dt, kMgS); });
+}
+
 // Multigrid cost breakdown (kernel timing): one V-cycle of the FP32-smoother
 // preconditioner and one smoothing sweep (residual + block-Jacobi) per level,
 // each captured in a graph of `reps` repetitions and replayed once after a

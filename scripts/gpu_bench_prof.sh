@@ -11,7 +11,7 @@ for line in open('gpurun_out/bench.log'):
             print(p, 'ms %.1f it %.1f dofs %.3e' % (r['ms_per_step'], r['iterations_per_step'], r['dof_updates_per_s']))
         print('roof', d['roofline']['kernel'], '%.0f GB/s frac %.2f' % (d['roofline']['achieved'], d['roofline']['frac']))
         for p, o in d['roofline']['others'].items():
-            print(p, 'asm %.0f spmv %.0f schur %.0f' % (o['assemble_GBps'], o['spmv_compulsory_GBps'], o['schur_GBps']))
+            print(p, 'asm %.0f spmv %.0f schur %.0f' % (o['assemble_GBps'], o['full_apply_compulsory_GBps'], o['schur_apply_GBps']))
 PY
 tail -1 gpurun_out/bench.log
 for P in ${PS:-4}; do
