@@ -78,6 +78,8 @@ typedef struct ldg_step_stats {
   double residual;      /* reference contract residual (last step)         */
   double ms_assemble;   /* device time: projection + assembly + rhs        */
   double ms_solve;      /* device time: Krylov solve + Z recovery + check  */
+  double ms_setup;      /* part of ms_solve: rhs, preconditioner setup      */
+  double ms_krylov;     /* part of ms_solve: the Krylov iterations          */
 } ldg_step_stats;
 
 typedef struct ldg_info_t {

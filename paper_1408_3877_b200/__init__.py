@@ -67,7 +67,8 @@ class _Opts(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("applies", C.c_int), ("schur_relres", C.c_double),
-                ("residual", C.c_double), ("ms_assemble", C.c_double), ("ms_solve", C.c_double)]
+                ("residual", C.c_double), ("ms_assemble", C.c_double), ("ms_solve", C.c_double),
+                ("ms_setup", C.c_double), ("ms_krylov", C.c_double)]
 
 
 class _Info(C.Structure):

@@ -644,12 +644,16 @@ void run_steps(Team& T, double dt, int nsteps, const ldg_solver_opts& o, ldg_ste
     ldgb::team_solve(T, 1.0, dt, o, st);
     LDG_CUDA(cudaEventRecord(h0.ev[2], T.stream));
     LDG_CUDA(cudaEventSynchronize(h0.ev[2]));
-    float a = 0.f, b = 0.f;
+    float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
     cudaEventElapsedTime(&a, h0.ev[0], h0.ev[1]);
     cudaEventElapsedTime(&b, h0.ev[1], h0.ev[2]);
+    cudaEventElapsedTime(&c, h0.ev[1], h0.ev[3]);
+    cudaEventElapsedTime(&d, h0.ev[3], h0.ev[4]);
     if (st) {
       st->ms_assemble += a;
       st->ms_solve += b;
+      st->ms_setup += c;
+      st->ms_krylov += d;
     }
     for (auto& rp : T.ranks) rp->t = t_next;
   }

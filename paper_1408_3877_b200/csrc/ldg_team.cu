@@ -746,12 +746,14 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   int applies = 0;
   int it = 0;
   double rnorm = 0.0;
+  LDG_CUDA(cudaEventRecord(h0.ev[3], T.stream));  // end of the per-solve setup
   if (o.krylov == 0) {
     fgmres(T, pc, f32, wm, dt, o, tol, &it, &applies, &rnorm);
   } else {
     bicgstab(T, pc, f32, wm, dt, o, tol, &it, &applies, &rnorm);
   }
 
+  LDG_CUDA(cudaEventRecord(h0.ev[4], T.stream));  // end of the Krylov loop
   // flux recovery Z^m = M^-1 (V_Z^m - B^m C), written into Y[0 .. 2n)
 
   halo(T, 0, kC, 1);
