@@ -259,13 +259,15 @@ long packed_p_quads(int p);                                           // float4 
 void smooth_pack_e(Handle& h);                                        // Eq from E
 void smooth_stage1(Handle& h, const double* x);                       // tz = M^-1 B x (FP32 arithmetic)
 // mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)
+// [k0, kend): element range (default all owned); out may equal x for one
+// colour of the FK element graph (red-black Gauss-Seidel half-sweep)
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out);
+                   double* out, int k0 = 0, int kend = -1);
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 // the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
 void small_stage1(Handle& h, const double* x);
 void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                  double* out);
+                  double* out, int k0 = 0, int kend = -1);
 void small_zero(Handle& h, const double* b, double omega, double* out);
 
 // row-parallel operator kernels (ldg_rows.cu), used by the launchers above

@@ -5,7 +5,8 @@
 // Friedrichs-Keller meshes nest: FK(dim) is the red refinement of FK(dim/2)
 // (each coarse triangle holds 4 fine ones).  Coarse levels are rediscretised:
 // every level is a Handle of its own on FK(dim/2^l) with vertex coordinates
-// subsampled from the finer level (so jittered meshes coarsen consistently),
+// generated from the finest mesh's stream (jittered meshes: a reduced jitter,
+// see coarse_jitter_scale),
 // d projected on that level, and the same assembly / Schur kernels.  Transfer
 // is the exact L2 embedding of the coarse polynomial space: per fine element
 // one N x N block P_k (fine coeffs = P_k coarse coeffs of the parent),
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) k_restrict(int Kc, long Kpc, long Kpf, co
 template <int P>
 __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
                                                      const double* __restrict__ Pm, const double* __restrict__ xc,
-                                                     double* __restrict__ xf) {
+                                                     double* __restrict__ xf, double theta) {
   constexpr int N = Cfg<P>::N, NN = N * N;
   pdl_wait();
   pdl_trigger();
@@ -181,15 +182,17 @@ __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf,
     pv[j] = __ldcs(Ps + static_cast<long>(j) * Kpc);
     xv[j] = xc[j * Kpc + kc];
   }
-  double acc = xf[i * Kpf + k];
+  double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < N; ++j) acc = fma(pv[j], xv[j], acc);
-  xf[i * Kpf + k] = acc;
+  xf[i * Kpf + k] = fma(theta, acc, xf[i * Kpf + k]);
 }
 
 }  // namespace
 
 int mg_levels(const Handle& h) { return 1 + static_cast<int>(h.coarse.size()); }
+
+double coarse_jitter_scale();
 
 // Number of coarse levels for FK(dim) split into `size` equal strips: halve
 // while dim stays even, the coarse mesh keeps dim >= 2, and every rank keeps
@@ -234,8 +237,8 @@ bool mg_build(Handle& h, int team_size) {
     c->size = h.size;
     // coarse vertices are the finest mesh's vertices (stride 2^l): jittered
     // meshes coarsen consistently on every rank
-    build_square_strip(*c, dc, fine->strip_a / 2, fine->strip_b / 2, fine->stride * 2, h.dim_fine, h.jitter,
-                       h.seed);
+    const double cj = coarse_jitter_scale() * h.jitter;
+    build_square_strip(*c, dc, fine->strip_a / 2, fine->strip_b / 2, fine->stride * 2, h.dim_fine, cj, h.seed);
     const long n = c->vec_len();
     c->D.alloc(n, &c->bytes);
     c->E.alloc(2 * NN * c->Kp, &c->bytes);  // diagonal blocks (off-diagonal ones matrix-free)
@@ -313,11 +316,35 @@ void mg_restrict(Handle& L, Handle& C) {
   ++L.launches;
 }
 
+// scale of the coarse-grid correction (LDG_MG_THETA, tuning runs; 1 = plain)
+double coarse_theta() {
+  static const double th = [] {
+    const char* e = std::getenv("LDG_MG_THETA");
+    return e ? std::atof(e) : 1.0;
+  }();
+  return th;
+}
+
+// Jitter of the coarse levels' vertices as a fraction of the finest mesh's
+// displacement (same splitmix64 stream): on a jittered FK mesh the fine
+// triangles do not tile the coarse ones whatever the coarse vertices are, and
+// subsampling the fine vertices (1.0) made the rediscretised coarse operators
+// a poor match -- measured at 512^2, p = 3, jitter 0.2, mixed BCs: 93
+// iterations with 1.0, 60 with a regular coarse lattice (0.0), 52.5 with 0.4
+// (0.25..0.75 swept).  LDG_MG_COARSE_JITTER overrides.
+double coarse_jitter_scale() {
+  static const double js = [] {
+    const char* e = std::getenv("LDG_MG_COARSE_JITTER");
+    return e ? std::atof(e) : 0.4;
+  }();
+  return js;
+}
+
 // x += P C.mg_x (prolongation of the coarse correction)
 void mg_prolong_add(Handle& L, Handle& C, double* x) {
 #define CALL(PP)                                                                                              \
   launch_pdl(k_prolong_add<PP>, grid_of(4L * L.N * C.K, 256), 256, 0, L.stream, C.K, C.Kp, L.Kp,                \
-             C.mg_children.ptr, C.mg_P.ptr, C.mg_x.ptr, x)
+             C.mg_children.ptr, C.mg_P.ptr, C.mg_x.ptr, x, coarse_theta())
   LDG_DISPATCH_P(L.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

@@ -55,14 +55,14 @@ struct Item {
 };
 
 template <int P>
-__device__ __forceinline__ Item item_of(int K) {
+__device__ __forceinline__ Item item_of(int K, int k0 = 0) {  // elements [k0, K)
   using C = Cfg<P>;
   Item it;
   it.lane = threadIdx.x & 7;
   const int q = threadIdx.x >> 3;
   it.i = q / C::EPC;
   it.ke = q % C::EPC;
-  it.k = blockIdx.x * C::EPC + it.ke;
+  it.k = k0 + blockIdx.x * C::EPC + it.ke;
   it.live = it.k < K;
   return it;
 }
@@ -145,18 +145,17 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s1_small(DevMesh m, DevT
 //   MODE 0: out = r;  MODE 1: out = x + omega P^-1 r
 template <int P, int MODE>
 __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
-                                                              const double* __restrict__ D,
-                                                              const double* __restrict__ x,
+                                                              const double* __restrict__ D, const double* x,
                                                               const double* __restrict__ tz,
                                                               const double* __restrict__ b, double wm, double dteta,
                                                               double dt, const float* __restrict__ Pinv,
-                                                              double omega, double* __restrict__ out) {
+                                                              double omega, double* out, int k0, int kend) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, Q = C::Q;
   __shared__ double s_r[N][C::EPC];
   pdl_wait();
   pdl_trigger();
-  const Item it = item_of<P>(m.K);
+  const Item it = item_of<P>(kend, k0);  // (in place for one colour: see k_s2f)
   const int k = it.k, i = it.i, l = it.lane;
   const long Kp = m.Kp;
   double part = 0.0;
@@ -253,17 +252,18 @@ void small_stage1(Handle& h, const double* x) {
 }
 
 void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                  double* out) {
+                  double* out, int k0, int kend) {
   const double dteta = dt * h.prob.eta;
+  if (kend < 0) kend = h.K;
 #define CALL(P)                                                                                                \
   do {                                                                                                         \
-    const unsigned grid = grid_of(h.K, Cfg<P>::EPC);                                                           \
+    const unsigned grid = grid_of(kend - k0, Cfg<P>::EPC);                                                     \
     if (mode == 0)                                                                                             \
       launch_pdl(k_s2_small<P, 0>, grid, Cfg<P>::THREADS, 0, h.stream, h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x, \
-                 h.tz.ptr, b, wm, dteta, dt, h.Pinv32.ptr, omega, out);                                       \
+                 h.tz.ptr, b, wm, dteta, dt, h.Pinv32.ptr, omega, out, k0, kend);                             \
     else                                                                                                       \
       launch_pdl(k_s2_small<P, 1>, grid, Cfg<P>::THREADS, 0, h.stream, h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, x, \
-                 h.tz.ptr, b, wm, dteta, dt, h.Pinv32.ptr, omega, out);                                       \
+                 h.tz.ptr, b, wm, dteta, dt, h.Pinv32.ptr, omega, out, k0, kend);                             \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

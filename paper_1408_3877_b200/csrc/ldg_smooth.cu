@@ -70,22 +70,27 @@ __device__ __forceinline__ const float* stage_f(float* sm, const float* src, int
   return sm;
 }
 
-// w = T x, T^t rows of NF floats in shared memory
+// w = T x, T^t rows of NF floats in shared memory.  Paired FP32 FMAs
+// (FFMA2, sm_100): one 128-bit broadcast load feeds two of them, half the
+// FMA instructions of the scalar form (these kernels are issue-bound).
 template <int N, int NF>
 __device__ __forceinline__ void ftab_mv(const float* sT, const float* x, float* w) {
+  float2 acc[NF / 2];
 #pragma unroll
-  for (int i = 0; i < N; ++i) w[i] = 0.f;
+  for (int q = 0; q < NF / 2; ++q) acc[q] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const float4* row = reinterpret_cast<const float4*>(sT + j * NF);
+    const float2 xj = make_float2(x[j], x[j]);
 #pragma unroll
     for (int q = 0; q < NF / 4; ++q) {
       const float4 t = row[q];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (4 * q + r < N) w[4 * q + r] = fmaf(comp(t, r), x[j], w[4 * q + r]);
+      acc[2 * q] = __ffma2_rn(make_float2(t.x, t.y), xj, acc[2 * q]);
+      if (4 * q + 2 < N) acc[2 * q + 1] = __ffma2_rn(make_float2(t.z, t.w), xj, acc[2 * q + 1]);
     }
   }
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = (i & 1) ? acc[i / 2].y : acc[i / 2].x;
 }
 
 template <int N>
@@ -138,13 +143,23 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s1f(DevMesh m, De
       u2[i] = fmaf(c2, w[i], u2[i]);
     }
   }
-#pragma unroll 1
+  // the neighbours' x: every load issued before the products (one latency
+  // round instead of one per neighbour)
+  int nb[3], nbn[3];
+#pragma unroll
   for (int n = 0; n < 3; ++n) {
-    const int kp = m.nbr[n * Kp + k];
-    if (kp < 0) continue;
-    float xn[N];
-    load_f<N>(x, Kp, kp, xn);
-    ftab_mv<N, NF>(tb + (5 + n * 3 + m.nbrn[n * Kp + k]) * TAB, xn, w);
+    nb[n] = m.nbr[n * Kp + k];
+    nbn[n] = m.nbrn[n * Kp + k];
+  }
+  float xn[3][N];
+#pragma unroll
+  for (int n = 0; n < 3; ++n)
+#pragma unroll
+    for (int j = 0; j < N; ++j) xn[n][j] = nb[n] >= 0 ? static_cast<float>(x[j * Kp + nb[n]]) : 0.f;
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    if (nb[n] < 0) continue;
+    ftab_mv<N, NF>(tb + (5 + n * 3 + nbn[n]) * TAB, xn[n], w);
     const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
     const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
     const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
@@ -235,10 +250,10 @@ __device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long K
 template <int P, int MODE, typename TQ>
 __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
-                                             const double* __restrict__ x,
+                                             const double* x,
                                              const double* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const float4* __restrict__ Pq, float omega,
-                                             double* __restrict__ out) {
+                                             double* out, int k0, int kend) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
   constexpr int Q = C::Q;
@@ -251,8 +266,11 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, De
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
   pdl_wait();
   pdl_trigger();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m.K) return;
+  // elements [k0, kend): all of them (Jacobi, out != x) or one colour of the
+  // bipartite FK element graph (red-black Gauss-Seidel, in place: an element
+  // reads only the other colour's x)
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= kend) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
   float acc[N];
@@ -453,13 +471,15 @@ void smooth_stage1(Handle& h, const double* x) {
 }
 
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out) {
+                   double* out, int k0, int kend) {
   const double dteta = dt * h.prob.eta;
   const float om = static_cast<float>(omega);
   const bool e16 = h.Eh.ptr != nullptr;
+  if (kend < 0) kend = h.K;
+  const unsigned grid = grid_of(kend - k0, 128);
 #define LAUNCH(P, M, TQ, EP, SC)                                                                                   \
-  launch_pdl(k_s2f<P, M, TQ>, grid_of(h.K, 128), 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr, \
-             x, h.tz.ptr, b, wm, dteta, dt, h.Pq.ptr, om, out)
+  launch_pdl(k_s2f<P, M, TQ>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr,               \
+             x, h.tz.ptr, b, wm, dteta, dt, h.Pq.ptr, om, out, k0, kend)
 #define CALL(P)                                                                         \
   do {                                                                                  \
     if (e16) {                                                                          \

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "ldg_internal.hpp"
@@ -342,6 +343,38 @@ void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo) {
   each(T, l, [&](Handle& L) { f_stage2(L, 1, xi, b, wm, dt, xo); });
 }
 
+// Red-black block Gauss-Seidel (LDG_MG_SMOOTHER=rb): the element graph of an
+// FK mesh is bipartite (a lower triangle's neighbours are uppers), so each
+// colour is updated in place from the other colour's current values; stage 1
+// is recomputed in between (t depends on x).  Owned lowers are the elements
+// [0, K/2), owned uppers [K/2, K) on every level and strip.
+bool rb_smoother() {
+  static const bool on = [] {
+    const char* s = std::getenv("LDG_MG_SMOOTHER");
+    return s && std::string(s) == "rb";
+  }();
+  return on;
+}
+const double kOmegaGS = env_or("LDG_MG_OMEGA_GS", 1.0);
+
+void sweep_rb(Team& T, int l, double wm, double dt, Vec b, Vec x, bool reverse) {
+  for (int h = 0; h < 2; ++h) {
+    const int c = reverse ? 1 - h : h;
+    halo(T, l, x, 1);
+    each(T, l, [&](Handle& L) { f_stage1(L, x); });
+    halo(T, l, kTz, 2);
+    each(T, l, [&](Handle& L) {
+      const int half = L.K / 2, k0 = c ? half : 0, k1 = c ? L.K : half;
+      if (tier(L) == kBig)
+        smooth_stage2(L, 1, vp(L, x), vp(L, b), wm, dt, kOmegaGS, vp(L, x), k0, k1);
+      else
+        small_stage2(L, 1, vp(L, x), vp(L, b), wm, dt, kOmegaGS, vp(L, x), k0, k1);
+    });
+  }
+}
+
+bool rb_level(Team& T, int l) { return rb_smoother() && tier(level_of(T.h0(), l)) != kMid; }
+
 // One V-cycle on level l: x = V(b).  Fused levels alternate x with the
 // level's scratch vector; the first (residual-free) sweep writes whichever
 // buffer makes the last sweep land in x.
@@ -350,6 +383,18 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
   // (every rank keeps a column), so a larger coarsest grid gets more sweeps
   const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(l) - 1) + post_of(l);
+  if (fused(T, l, f32) && rb_level(T, l)) {
+    each(T, l, [&](Handle& L) { f_zero(L, b, x); });
+    const int pre = coarsest ? sweeps : pre_of(l) - 1;
+    for (int s = 0; s < pre; ++s) sweep_rb(T, l, wm, dt, b, x, false);
+    if (coarsest) return;
+    residual_f(T, l, wm, dt, b, x, kMgR);
+    for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
+    vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
+    for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
+    for (int s = 0; s < post_of(l); ++s) sweep_rb(T, l, wm, dt, b, x, true);
+    return;
+  }
   if (fused(T, l, f32)) {
     Vec cur = (sweeps % 2) ? kMgS : x;
     auto other = [&](Vec v) { return v == x ? kMgS : x; };

@@ -11,11 +11,10 @@ for line in open('gpurun_out/bench_tune.log'):
         print('%-60s' % sys.argv[1], ' '.join('p%s %6.1fms/%5.1fit' % (p, r['ms_per_step'], r['iterations_per_step']) for p, r in d['config']['per_p'].items()), flush=True)
 PY
 done <<'LIST'
-LDG_MG_ETA_SCALE=1
-LDG_MG_ETA_SCALE=1.5
-LDG_MG_ETA_SCALE=2
-LDG_MG_ETA_SCALE=3
-LDG_MG_ETA_SCALE=4
-LDG_MG_ETA_SCALE=0.7
-LDG_MG_ETA_SCALE=2 LDG_MG_PRE=3 LDG_MG_POST=3
+LDG_MG_THETA=1
+LDG_MG_THETA=0.8
+LDG_MG_THETA=1.2
+LDG_MG_THETA=1.4
+LDG_MG_THETA=1.7
+LDG_MG_THETA=1.4 LDG_MG_SMOOTHER=rb LDG_MG_OMEGA_GS=0.9
 LIST

@@ -56,17 +56,18 @@ print("JSON" + json.dumps(out))
 """
 
 
-def _run(rows_below: int) -> dict:
-    env = dict(os.environ, LDG_ROWS_BELOW=str(rows_below))
+def _run(rows_below: int, extra: dict | None = None) -> dict:
+    env = dict(os.environ, LDG_ROWS_BELOW=str(rows_below), **(extra or {}))
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("JSON")][-1]
     return json.loads(line[4:])
 
 
-@pytest.mark.parametrize("rows_below", [0, 1 << 30], ids=["thread_kernels_fused_smoother", "row_kernels"])
-def test_kernel_shape(rows_below):
-    out = _run(rows_below)
+@pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (2048, {"LDG_MG_SMOOTHER": "rb"})],
+                         ids=["thread_kernels_fused_smoother", "row_kernels", "red_black_gauss_seidel"])
+def test_kernel_shape(rows_below, extra):
+    out = _run(rows_below, extra)
     for key, r in out.items():
         print("RESULT", rows_below, key, json.dumps(r))
     for key, r in out.items():
