@@ -39,6 +39,9 @@ WORKLOADS = {
            "C2: FK 256x256 (K=131072), p=0..4 sweep, implicit Euler dt=1/20, all-Dirichlet BASELINE problem"),
     "c1": (16, [1], 1.0 / 100, 0.0, {1: "D", 2: "D", 3: "D", 4: "D"},
            "C1: FK 16x16 (K=512), p=1, dt=1/100, all-Dirichlet BASELINE problem"),
+    "c3": (1024, [4], 0.0, 0.0, {1: "D", 2: "D", 3: "D", 4: "D"},
+           "C3: assembly-only stress, FK 1024x1024 (K=2097152), p=4: projection of d, f, right-hand side and "
+           "all 8 time-dependent C-row blocks per element each step"),
     "c4": (2048, [3], 1.0 / 10, 0.2, {1: "D", 2: "N", 3: "N", 4: "D"},
            "C4: FK 2048x2048 jittered +-0.2h (seed 0), p=3, dt=1/10, D on x1=0,x2=0, N elsewhere"),
     "c5": (4096, [2], 1.0 / 5, 0.0, {1: "D", 2: "D", 3: "D", 4: "D"},
@@ -212,9 +215,41 @@ def reference_sample(workload, steps, warmup):
     return dof / sec, sec, sample
 
 
+C3_METRIC, C3_UNIT = "assembled BSR bytes/s (time-dependent C-row blocks, SURVEY.md §8d)", "B/s"
+
+
+def reference_sample_c3(steps, warmup):
+    """Reference build_blocks (system.hpp:110-152) on FK 64x64 at p=4: assembled
+    time-dependent BSR bytes (SURVEY §8d formula) per second."""
+    from oracle import reflib as R
+
+    dim, p = 64, 4
+    funcs = dict(d=(9, []), f=(10, []), c_d=(8, []), g_n=(11, []), c0=(8, []))
+    if not R.available():
+        raise RuntimeError("oracle/_ref/libldgref.so missing")
+    mesh = R.RefMesh.square(1.0 / dim)
+    case = R.RefCase(mesh, n_of(p), 1.0, funcs, {1: "D", 2: "D", 3: "D", 4: "D"})
+    case.time_build(0.0, max(warmup, 0) or 1)
+    sec = case.time_build(0.1, steps)
+    sample = (f"reference build_blocks (unmodified headers + Eigen shim): FK {dim}x{dim} (K={2 * dim * dim}), p={p}, "
+              f"{steps} calls (projection, all operators as triplets, CSC merge)")
+    return bytes_asm_survey(dim, p) * steps / sec, sec, sample
+
+
 def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
+        return 0
+    if args.workload == "c3":
+        value, sec, sample = reference_sample_c3(args.steps, args.warmup)
+        line = {"impl": "reference", "metric": C3_METRIC, "value": value, "unit": C3_UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (analytic BASELINE.json problem)",
+                "config": {"workload": WORKLOADS["c3"][5] + " [reference: bounded sample, see cpu_baseline]"},
+                "cpu_baseline": {"value": value, "unit": C3_UNIT, "cores": 1, "kind": "reference", "sample": sample},
+                "e2e": {"value": value, "unit": C3_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
         return 0
     value, sec, sample = reference_sample(args.workload, args.steps, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -228,7 +263,71 @@ def run_reference_arm(args):
     return 0
 
 
+def run_assembly_c3(args):
+    """BASELINE config 3: projection + right-hand side + the full time-dependent
+    C-row BSR (8 blocks per element) every step, device-resident output."""
+    world, rank, local = dist_env()
+    import torch
+
+    import paper_1408_3877_b200 as ld
+
+    ld.set_device(local)
+    dim, ps, _, _, boundary, desc = WORKLOADS["c3"]
+    p = ps[0]
+    spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
+                          boundary=boundary)
+    s = ld.LdgSystem.square(dim, p, spec)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")
+    for i in range(args.warmup):
+        s.assemble_blocks(0.01 * (i + 1))
+    clocks = ClockSampler(local)
+    if not args.no_clocks:
+        clocks.start()
+    total_ms = 0.0
+    launches0 = s.info()["launches"]
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        total_ms += s.assemble_blocks(0.1 * (i + 1))
+    clk = clocks.stop()
+    launches = s.info()["launches"] - launches0
+    bsr = bytes_asm_survey(dim, p)
+    value = bsr * args.steps / (total_ms * 1e-3)
+    peak, peak_src = hbm_peak()
+    kern = s.time_kernels(0.5, 0.05, reps=3, flush=True)  # the solver's diagonal-block assembly, for reference
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            v, sec, sample = reference_sample_c3(1, 1)
+            cpu = {"value": v, "unit": C3_UNIT, "cores": 1, "kind": "reference", "sample": sample}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": C3_UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+    line = {
+        "metric": C3_METRIC, "value": value, "unit": C3_UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: analytic d(t), f(t) of BASELINE.json; FK mesh generated on device",
+        "config": {"workload": desc, "dim": dim, "K": 2 * dim * dim, "p": p,
+                   "bytes_per_step": bsr, "l2": "flushed (256 MB write) before every timed step"},
+        "e2e": {"value": None, "unit": C3_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "note": "the assembled blocks stay on the device (30 GB per step); the reference's build_blocks "
+                        "result is its host CSC"},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "projection + rhs + k_assemble<4, kModeE> (all 8 blocks), one call", "bound": "hbm",
+                     "achieved": value / 1e9, "peak": peak, "unit": "GB/s", "frac": value / 1e9 / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "solver_assembly_diagonal_blocks_ms": kern["ms_assemble"]},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    s.close()
+    return 0
+
+
 def run_ours(args):
+    if args.workload == "c3":
+        return run_assembly_c3(args)
     world, rank, local = dist_env()
     import torch
 

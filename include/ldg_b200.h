@@ -165,6 +165,15 @@ int ldg_project(ldg_handle* h, const ldg_coeff* fn, double t, int q_ord, double*
  * (assembly.hpp:256-338).  Device-resident; nothing is copied back. */
 int ldg_assemble(ldg_handle* h, double t);
 
+/* The time-dependent C-row blocks as the reference assembles them: all 8 N x N
+ * blocks per element (E^m_kk and E^m_{k,nbr(k)}, device layout
+ * [m][s][i*N+j][Kp]) together with the projection of d, f and the right-hand
+ * side -- the assembly-only workload (BASELINE config 3).  The solver path
+ * (ldg_assemble) stores only the diagonal blocks and evaluates the others
+ * from D.  Device-resident (library buffer, allocated on first use); *ms
+ * (optional) receives the device time of the call. */
+int ldg_assemble_blocks(ldg_handle* h, double t, double* ms);
+
 enum ldg_operator {
   LDG_OP_MASS = 0, LDG_OP_H1, LDG_OP_H2, LDG_OP_G1, LDG_OP_G2, LDG_OP_R1, LDG_OP_RD1, LDG_OP_R2,
   LDG_OP_RD2, LDG_OP_Q1, LDG_OP_QN1, LDG_OP_Q2, LDG_OP_QN2, LDG_OP_S, LDG_OP_SD,

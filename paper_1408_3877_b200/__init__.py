@@ -108,6 +108,7 @@ _SIGNATURES = {
     "ldg_mesh_lists": (C.c_int, [_H, _dp, _ip, _dp, _dp, _dp, _dp, _ip, _ip, _ip]),
     "ldg_project": (C.c_int, [_H, C.POINTER(_Coeff), C.c_double, C.c_int, _dp]),
     "ldg_assemble": (C.c_int, [_H, C.c_double]),
+    "ldg_assemble_blocks": (C.c_int, [_H, C.c_double, _dp]),
     "ldg_export_operator": (C.c_int, [_H, C.c_int, _lp, _lp, _lp, _dp, C.c_int64]),
     "ldg_export_vector": (C.c_int, [_H, C.c_int, _dp, C.c_int64]),
     "ldg_initial_state": (C.c_int, [_H]),
@@ -357,6 +358,14 @@ class LdgSystem:
     def assemble(self, t: float):
         """The device half of build_blocks(t) (system.hpp:110-152)."""
         self._check(load_library().ldg_assemble(self._h, float(t)))
+
+    def assemble_blocks(self, t: float) -> float:
+        """All 8 time-dependent C-row blocks per element as the reference assembles
+        them, with the projection of d, f and the right-hand side (BASELINE config 3);
+        returns the device time in ms."""
+        ms = C.c_double()
+        self._check(load_library().ldg_assemble_blocks(self._h, float(t), C.byref(ms)))
+        return ms.value
 
     def operator(self, name: str):
         """COO (rows, cols, vals) of one operator at the last assemble time."""

@@ -476,6 +476,27 @@ int ldg_assemble(ldg_handle* H, double t) {
   });
 }
 
+int ldg_assemble_blocks(ldg_handle* H, double t, double* ms) {
+  if (!H) return LDG_EINVAL;
+  return guarded(H, [&] {
+    Team& T = H->team;
+    Handle& h0 = T.h0();
+    for (auto& rp : T.ranks)
+      if (!rp->Efull.ptr) rp->Efull.alloc(8L * rp->N * rp->N * rp->Kp, &rp->bytes);
+    LDG_CUDA(cudaEventRecord(h0.ev[0], T.stream));
+    for (auto& rp : T.ranks) {
+      ldgb::launch_project_df(*rp, t, rp->rule_ptr(), rp->rule_R());
+      ldgb::launch_rhs(*rp, t);
+      ldgb::launch_assemble(*rp, ldgb::kModeE, rp->Efull.ptr);
+    }
+    LDG_CUDA(cudaEventRecord(h0.ev[1], T.stream));
+    LDG_CUDA(cudaEventSynchronize(h0.ev[1]));
+    float e = 0.f;
+    cudaEventElapsedTime(&e, h0.ev[0], h0.ev[1]);
+    if (ms) *ms = e;
+  });
+}
+
 int ldg_export_operator(ldg_handle* H, int which, int64_t* nnz, int64_t* rows, int64_t* cols, double* vals,
                         int64_t cap) {
   if (!H || !nnz) return LDG_EINVAL;

@@ -88,7 +88,8 @@ struct Handle {
 
   // per-step operators / vectors
   DBuf<double> D, F;     // N * Kp
-  DBuf<double> E;        // 2 * 4 * N*N * Kp
+  DBuf<double> E;        // 2 * N*N * Kp (diagonal blocks; see ldg_device.cuh)
+  DBuf<double> Efull;    // 2 * 4 * N*N * Kp, ldg_assemble_blocks only
   DBuf<double> Bst;      // 2 * 4 * N*N * Kp
   DBuf<double> Sst;      // 4 * N*N * Kp
   DBuf<double> Vv;       // 3 * N * Kp
