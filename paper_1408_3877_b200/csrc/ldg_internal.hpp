@@ -124,7 +124,7 @@ struct Handle {
   std::vector<std::unique_ptr<Handle>> coarse;   // levels 1 .. L-1 (top handle only)
   DBuf<int> mg_parent;                           // element -> parent in the next coarser level
   DBuf<int> mg_children;                         // [4][Kp] children in the next finer level
-  DBuf<double> mg_P;                             // [N*N][Kp] prolongation block of each element
+  DBuf<float> mg_P;                              // [4][N*N][Kp] prolongation blocks (on the coarse level, FP32)
   DBuf<double> mg_x, mg_b, mg_r;                 // V-cycle work vectors (N * Kp)
   DBuf<float> E32, Pinv32;                       // FP32 copies read by the row-kernel smoother (small levels)
   DBuf<float4> Eq, Pq;                           // packed FP32 copies read by the fused smoother (ldg_smooth.cu)
@@ -270,6 +270,8 @@ void small_stage1(Handle& h, const double* x);
 void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
                   double* out, int k0 = 0, int kend = -1);
 void small_zero(Handle& h, const double* b, double omega, double* out);
+// the V-cycle from coarse level `top` (>= 1) down, in one thread block (single rank)
+void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, int pre, int post, int coarse_min);
 
 // row-parallel operator kernels (ldg_rows.cu), used by the launchers above
 void rows_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);

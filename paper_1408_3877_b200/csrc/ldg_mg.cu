@@ -89,11 +89,12 @@ __device__ __forceinline__ void eval_basis(const double* __restrict__ mono, doub
 
 // P_k[i][j] = sum_a minv[i][a] int_ref phi_a(xh) phi_j(xi(xh)), xi = parent
 // reference coordinates of the fine point; exact with the order-2p rule.
-// Pm is stored on the coarse level, [slot][N*N][Kp_c], so restriction and
+// Pm (FP32: a preconditioner transfer; half the bytes of the level-0/1
+// transfers, the largest of them) is stored on the coarse level, [slot][N*N][Kp_c], so restriction and
 // prolongation (both driven from the coarse side) read it coalesced.
 template <int P>
 __global__ void __launch_bounds__(128) k_prolong_blocks(DevMesh f, DevMesh c, DevTables T, const int* __restrict__ parent,
-                                                        const int* __restrict__ slots, double* __restrict__ Pm) {
+                                                        const int* __restrict__ slots, float* __restrict__ Pm) {
   constexpr int N = Cfg<P>::N, NN = N * N;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= f.K) return;
@@ -120,12 +121,12 @@ __global__ void __launch_bounds__(128) k_prolong_blocks(DevMesh f, DevMesh c, De
       for (int j = 0; j < N; ++j) acc[i * N + j] += w * pf[i] * pc[j];
   }
   const double* minv = base + T.minv;
-  double* out = Pm + static_cast<long>(slots[k]) * NN * Kc;
+  float* out = Pm + static_cast<long>(slots[k]) * NN * Kc;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) {
       double s = 0.0;
       for (int a = 0; a < N; ++a) s += minv[i * N + a] * acc[a * N + j];
-      out[static_cast<long>(i * N + j) * Kc + kc] = s;
+      out[static_cast<long>(i * N + j) * Kc + kc] = static_cast<float>(s);
     }
 }
 
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(128) k_prolong_blocks(DevMesh f, DevMesh c, De
 // for a thread per element to hide the load latency)
 template <int P>
 __global__ void __launch_bounds__(256) k_restrict(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
-                                                  const double* __restrict__ Pm, const double* __restrict__ rf,
+                                                  const float* __restrict__ Pm, const double* __restrict__ rf,
                                                   double* __restrict__ bc) {
   constexpr int N = Cfg<P>::N, NN = N * N;
   pdl_wait();
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(256) k_restrict(int Kc, long Kpc, long Kpf, co
   double acc = 0.0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {  // loads of a child first, then its FMA chain (latency-bound on coarse levels)
-    const double* Ps = Pm + (static_cast<long>(s) * NN + j) * Kpc + kc;
+    const float* Ps = Pm + (static_cast<long>(s) * NN + j) * Kpc + kc;
     double pv[N], rv[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) k_restrict(int Kc, long Kpc, long Kpf, co
 // xf[i][child_s] += sum_j P_s[i][j] xc[j][kc]: one thread per (i, s, kc)
 template <int P>
 __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf, const int* __restrict__ children,
-                                                     const double* __restrict__ Pm, const double* __restrict__ xc,
+                                                     const float* __restrict__ Pm, const double* __restrict__ xc,
                                                      double* __restrict__ xf, double theta) {
   constexpr int N = Cfg<P>::N, NN = N * N;
   pdl_wait();
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(256) k_prolong_add(int Kc, long Kpc, long Kpf,
   const int rest = static_cast<int>(t / Kc);
   const int s = rest % 4, i = rest / 4;
   const int k = children[s * Kpc + kc];
-  const double* Ps = Pm + (static_cast<long>(s) * NN + static_cast<long>(i) * N) * Kpc + kc;
+  const float* Ps = Pm + (static_cast<long>(s) * NN + static_cast<long>(i) * N) * Kpc + kc;
   double pv[N], xv[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {

@@ -54,15 +54,16 @@ struct Item {
   bool live;
 };
 
+// item of thread t (< THREADS) in virtual block vb, elements [k0, K)
 template <int P>
-__device__ __forceinline__ Item item_of(int K, int k0 = 0) {  // elements [k0, K)
+__device__ __forceinline__ Item item_of(int K, int k0, int vb, int t) {
   using C = Cfg<P>;
   Item it;
-  it.lane = threadIdx.x & 7;
-  const int q = threadIdx.x >> 3;
+  it.lane = t & 7;
+  const int q = t >> 3;
   it.i = q / C::EPC;
   it.ke = q % C::EPC;
-  it.k = k0 + blockIdx.x * C::EPC + it.ke;
+  it.k = k0 + vb * C::EPC + it.ke;
   it.live = it.k < K;
   return it;
 }
@@ -95,13 +96,11 @@ __device__ __forceinline__ double trow(const double* __restrict__ tab, int i, co
 
 // tout^m_i = (1/2|T|) (mhat^-1 B^m x)_i with the premultiplied tables
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s1_small(DevMesh m, DevTables T, const double* __restrict__ x,
-                                                              double* __restrict__ tout) {
+__device__ __forceinline__ void s1_body(const DevMesh& m, const DevTables& T, const double* __restrict__ x,
+                                        double* __restrict__ tout, int vb, int t) {
   using C = Cfg<P>;
   constexpr int N = C::N, NP = C::NP, NNP = C::NNP;
-  pdl_wait();
-  pdl_trigger();
-  const Item it = item_of<P>(m.K);
+  const Item it = item_of<P>(m.K, 0, vb, t);
   const int k = it.live ? it.k : 0, i = it.i, l = it.lane;  // dead items compute on element 0, never store
   const long Kp = m.Kp;
   const double* g = m.geom;
@@ -141,21 +140,25 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s1_small(DevMesh m, DevT
   }
 }
 
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s1_small(DevMesh m, DevTables T, const double* __restrict__ x,
+                                                              double* __restrict__ tout) {
+  pdl_wait();
+  pdl_trigger();
+  s1_body<P>(m, T, x, tout, blockIdx.x, threadIdx.x);
+}
+
 // r_i = b_i - [wm M x + dt (eta (S + S_D) x - sum_m E^m t^m)]_i, then
 //   MODE 0: out = r;  MODE 1: out = x + omega P^-1 r
 template <int P, int MODE>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
-                                                              const double* __restrict__ D, const double* x,
-                                                              const double* __restrict__ tz,
-                                                              const double* __restrict__ b, double wm, double dteta,
-                                                              double dt, const float* __restrict__ Pinv,
-                                                              double omega, double* out, int k0, int kend) {
+__device__ __forceinline__ void s2_body(const DevMesh& m, const DevTables& T, const float* __restrict__ E,
+                                        const double* __restrict__ D, const double* x, const double* __restrict__ tz,
+                                        const double* __restrict__ b, double wm, double dteta, double dt,
+                                        const float* __restrict__ Pinv, double omega, double* out, int k0, int kend,
+                                        double (*s_r)[Cfg<P>::EPC], int vb, int t) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, Q = C::Q;
-  __shared__ double s_r[N][C::EPC];
-  pdl_wait();
-  pdl_trigger();
-  const Item it = item_of<P>(kend, k0);  // (in place for one colour: see k_s2f)
+  const Item it = item_of<P>(kend, k0, vb, t);  // (in place for one colour: see k_s2f)
   const int k = it.k, i = it.i, l = it.lane;
   const long Kp = m.Kp;
   double part = 0.0;
@@ -220,24 +223,171 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_small(DevMesh m, DevT
     }
     d = lane_sum8(d);
     if (it.live && l == 0) out[i * Kp + k] = fma(omega, d, x[i * Kp + k]);
+    __syncthreads();  // s_r is reused by the next virtual block (tail kernel)
   }
+}
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_small(DevMesh m, DevTables T, const float* __restrict__ E,
+                                                              const double* __restrict__ D, const double* x,
+                                                              const double* __restrict__ tz,
+                                                              const double* __restrict__ b, double wm, double dteta,
+                                                              double dt, const float* __restrict__ Pinv,
+                                                              double omega, double* out, int k0, int kend) {
+  __shared__ double s_r[Cfg<P>::N][Cfg<P>::EPC];
+  pdl_wait();
+  pdl_trigger();
+  s2_body<P, MODE>(m, T, E, D, x, tz, b, wm, dteta, dt, Pinv, omega, out, k0, kend, s_r, blockIdx.x, threadIdx.x);
 }
 
 // out = omega P^-1 b
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_bj_small(int K, long Kp, const float* __restrict__ Pinv,
-                                                              const double* __restrict__ b, double omega,
-                                                              double* __restrict__ out) {
+__device__ __forceinline__ void bj_body(int K, long Kp, const float* __restrict__ Pinv, const double* __restrict__ b,
+                                        double omega, double* __restrict__ out, int vb, int t) {
   constexpr int N = Cfg<P>::N;
-  pdl_wait();
-  pdl_trigger();
-  const Item it = item_of<P>(K);
+  const Item it = item_of<P>(K, 0, vb, t);
   const int k = it.live ? it.k : 0, i = it.i, l = it.lane;
   const float* row = Pinv + static_cast<long>(i) * N * Kp + k;
   double d = 0.0;
   for (int j = l; j < N; j += 8) d = fma(static_cast<double>(row[j * Kp]), b[j * Kp + k], d);
   d = lane_sum8(d);
   if (it.live && l == 0) out[i * Kp + k] = omega * d;
+}
+
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_bj_small(int K, long Kp, const float* __restrict__ Pinv,
+                                                              const double* __restrict__ b, double omega,
+                                                              double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  bj_body<P>(K, Kp, Pinv, b, omega, out, blockIdx.x, threadIdx.x);
+}
+
+// ---------------------------------------------------------------- tail
+// The coarsest levels (a few dozen elements) of a V-cycle in ONE thread block:
+// every phase (sweep stages, residual, restriction, prolongation) is a loop
+// of the bodies above over the level's virtual blocks, separated by
+// __syncthreads, so the level data stays in this SM's L1 and no launch or
+// grid drain sits between the ~30 dependent phases (separate launches cost
+// 6-7 us each on these levels, mostly dependent L2 round trips).
+constexpr int kTailMax = 6;
+
+struct TailLevel {
+  DevMesh m;
+  const float* E32;
+  const float* Pinv32;
+  const double* D;
+  double *x, *s, *b, *r, *tz;
+  const int* children;  // this level as the coarse side of the transfer from the level above
+  const float* Pm;
+  int dim;
+};
+
+struct TailArgs {
+  TailLevel lv[kTailMax];
+  int nlev;
+  double wm, dt, dteta, omega;
+  int pre, post, coarse_min;
+};
+
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTables T) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN;
+  __shared__ double s_r[N][C::EPC];
+  pdl_wait();
+  pdl_trigger();
+  const int t = threadIdx.x;
+  auto nvb = [](int K) { return (K + C::EPC - 1) / C::EPC; };
+  auto zero = [&](const TailLevel& L, const double* b, double* out) {
+    for (int vb = 0; vb < nvb(L.m.K); ++vb) bj_body<P>(L.m.K, L.m.Kp, L.Pinv32, b, a.omega, out, vb, t);
+    __syncthreads();
+  };
+  auto stage1 = [&](const TailLevel& L, const double* x) {
+    for (int vb = 0; vb < nvb(L.m.K); ++vb) s1_body<P>(L.m, T, x, L.tz, vb, t);
+    __syncthreads();
+  };
+  auto stage2 = [&](const TailLevel& L, int mode, const double* x, const double* b, double* out) {
+    for (int vb = 0; vb < nvb(L.m.K); ++vb) {
+      if (mode == 0)
+        s2_body<P, 0>(L.m, T, L.E32, L.D, x, L.tz, b, a.wm, a.dteta, a.dt, L.Pinv32, a.omega, out, 0, L.m.K, s_r, vb,
+                      t);
+      else
+        s2_body<P, 1>(L.m, T, L.E32, L.D, x, L.tz, b, a.wm, a.dteta, a.dt, L.Pinv32, a.omega, out, 0, L.m.K, s_r, vb,
+                      t);
+    }
+    __syncthreads();
+  };
+  auto sweep = [&](const TailLevel& L, const double* xi, double* xo) {
+    stage1(L, xi);
+    stage2(L, 1, xi, L.b, xo);
+  };
+  // C.b = P^T F.r  (ldg_mg.cu k_restrict)
+  auto restrict_ = [&](const TailLevel& F, const TailLevel& Cl) {
+    const long Kpc = Cl.m.Kp, Kpf = F.m.Kp;
+    for (int it = t; it < N * Cl.m.K; it += blockDim.x) {
+      const int kc = it % Cl.m.K, j = it / Cl.m.K;
+      double acc = 0.0;
+      for (int sl = 0; sl < 4; ++sl) {
+        const int k = Cl.children[sl * Kpc + kc];
+        const float* Ps = Cl.Pm + (static_cast<long>(sl) * NN + j) * Kpc + kc;
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc = fma(static_cast<double>(Ps[static_cast<long>(i) * N * Kpc]), F.r[i * Kpf + k], acc);
+      }
+      Cl.b[j * Kpc + kc] = acc;
+    }
+    __syncthreads();
+  };
+  // xf += P C.x  (ldg_mg.cu k_prolong_add)
+  auto prolong = [&](const TailLevel& F, const TailLevel& Cl, double* xf) {
+    const long Kpc = Cl.m.Kp, Kpf = F.m.Kp;
+    for (int it = t; it < 4 * N * Cl.m.K; it += blockDim.x) {
+      const int kc = it % Cl.m.K, rest = it / Cl.m.K, sl = rest % 4, i = rest / 4;
+      const int k = Cl.children[sl * Kpc + kc];
+      const float* Ps = Cl.Pm + (static_cast<long>(sl) * NN + static_cast<long>(i) * N) * Kpc + kc;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fma(static_cast<double>(Ps[static_cast<long>(j) * Kpc]), Cl.x[j * Kpc + kc], acc);
+      xf[i * Kpf + k] += acc;
+    }
+    __syncthreads();
+  };
+
+  double* cur[kTailMax];
+  for (int l = 0; l + 1 < a.nlev; ++l) {  // down
+    const TailLevel& L = a.lv[l];
+    const int sweeps = (a.pre - 1) + a.post;
+    cur[l] = (sweeps % 2) ? L.s : L.x;
+    zero(L, L.b, cur[l]);
+    for (int sw = 0; sw < a.pre - 1; ++sw) {
+      double* o = cur[l] == L.x ? L.s : L.x;
+      sweep(L, cur[l], o);
+      cur[l] = o;
+    }
+    stage1(L, cur[l]);
+    stage2(L, 0, cur[l], L.b, L.r);
+    restrict_(L, a.lv[l + 1]);
+  }
+  {  // coarsest
+    const TailLevel& L = a.lv[a.nlev - 1];
+    const int sweeps = max(a.coarse_min, 2 * L.dim) - 1;
+    double* c = (sweeps % 2) ? L.s : L.x;
+    zero(L, L.b, c);
+    for (int sw = 0; sw < sweeps; ++sw) {
+      double* o = c == L.x ? L.s : L.x;
+      sweep(L, c, o);
+      c = o;
+    }
+  }
+  for (int l = a.nlev - 2; l >= 0; --l) {  // up
+    const TailLevel& L = a.lv[l];
+    prolong(L, a.lv[l + 1], cur[l]);
+    for (int sw = 0; sw < a.post; ++sw) {
+      double* o = cur[l] == L.x ? L.s : L.x;
+      sweep(L, cur[l], o);
+      cur[l] = o;
+    }
+  }
 }
 
 }  // namespace
@@ -279,6 +429,47 @@ void small_zero(Handle& h, const double* b, double omega, double* out) {
 #undef CALL
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
+}
+
+}  // namespace ldgb
+
+namespace ldgb {
+
+// The V-cycle below level `top` (inclusive) of h's hierarchy in one block
+// (see k_tail); x of the top level receives the result, b its right-hand side.
+void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, int pre, int post, int coarse_min) {
+  TailArgs a{};
+  const int nl = 1 + static_cast<int>(h0.coarse.size());
+  a.nlev = nl - top;
+  if (a.nlev < 1 || a.nlev > kTailMax) throw Error(LDG_EINVAL, "tail V-cycle: level count out of range");
+  for (int l = 0; l < a.nlev; ++l) {
+    Handle& L = *h0.coarse[top + l - 1];
+    TailLevel& t = a.lv[l];
+    t.m = L.mesh();
+    t.E32 = L.E32.ptr;
+    t.Pinv32 = L.Pinv32.ptr;
+    t.D = L.D.ptr;
+    t.x = L.mg_x.ptr;
+    t.s = L.mg_s.ptr;
+    t.b = L.mg_b.ptr;
+    t.r = L.mg_r.ptr;
+    t.tz = L.tz.ptr;
+    t.children = L.mg_children.ptr;
+    t.Pm = L.mg_P.ptr;
+    t.dim = L.dim;
+  }
+  a.wm = wm;
+  a.dt = dt;
+  a.dteta = dt * h0.prob.eta;
+  a.omega = omega;
+  a.pre = pre;
+  a.post = post;
+  a.coarse_min = coarse_min;
+#define CALL(P) launch_pdl(k_tail<P>, 1, Cfg<P>::THREADS, 0, h0.stream, a, h0.dtab)
+  LDG_DISPATCH_P(h0.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  ++h0.launches;
 }
 
 }  // namespace ldgb

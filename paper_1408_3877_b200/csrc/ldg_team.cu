@@ -378,8 +378,25 @@ bool rb_level(Team& T, int l) { return rb_smoother() && tier(level_of(T.h0(), l)
 // One V-cycle on level l: x = V(b).  Fused levels alternate x with the
 // level's scratch vector; the first (residual-free) sweep writes whichever
 // buffer makes the last sweep land in x.
+// Levels below LDG_TAIL_BELOW elements (default 64, i.e. the 8- and
+// 32-element levels, and only for p <= 1) run as one block
+// (small_tail_vcycle) on a single rank with the Jacobi smoother.  Measured
+// V-cycle at 256^2: p = 0 222 vs 239 us; p = 2 527 vs 504 us and p = 4 1593
+// vs 1312 us (one SM lacks the issue rate for the larger blocks).
+bool tail_level(Team& T, int l, bool f32) {
+  static const long below = static_cast<long>(env_or("LDG_TAIL_BELOW", 64));
+  static const int pmax = static_cast<int>(env_or("LDG_TAIL_PMAX", 1));
+  if (!f32 || l < 1 || rb_smoother() || T.size != 1 || T.nlocal() != 1 || T.h0().p > pmax) return false;
+  const Handle& L = level_of(T.h0(), l);
+  return L.K < below && levels(T) - l <= 6 && level_uses_rows(L) && level_is_small(L);
+}
+
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   const bool coarsest = l == levels(T) - 1;
+  if (tail_level(T, l, f32) && b == kMgB && x == kMgX) {
+    small_tail_vcycle(T.h0(), l, wm, dt, kOmega, pre_of(l), post_of(l), kCoarseSweeps);
+    return;
+  }
   // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
   // (every rank keeps a column), so a larger coarsest grid gets more sweeps
   const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(l) - 1) + post_of(l);

@@ -64,8 +64,10 @@ def _run(rows_below: int, extra: dict | None = None) -> dict:
     return json.loads(line[4:])
 
 
-@pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (2048, {"LDG_MG_SMOOTHER": "rb"})],
-                         ids=["thread_kernels_fused_smoother", "row_kernels", "red_black_gauss_seidel"])
+@pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (2048, {"LDG_MG_SMOOTHER": "rb"}),
+                                               (2048, {"LDG_TAIL_PMAX": "4", "LDG_TAIL_BELOW": "200"})],
+                         ids=["thread_kernels_fused_smoother", "row_kernels", "red_black_gauss_seidel",
+                              "single_block_coarse_tail"])
 def test_kernel_shape(rows_below, extra):
     out = _run(rows_below, extra)
     for key, r in out.items():
