@@ -66,12 +66,12 @@ __global__ void __launch_bounds__(256) k_dots_partial(long n, int nd, DotArgs a,
 __global__ void __launch_bounds__(256) k_dots_owned(int N, long Kp, int K, int nd, DotArgs a,
                                                     double* __restrict__ part) {
   double s[kMaxDots] = {0.0, 0.0, 0.0, 0.0};
-  const long n = static_cast<long>(N) * K;
-  for (long q = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; q < n;
-       q += static_cast<long>(gridDim.x) * blockDim.x) {
-    const long i = (q / K) * Kp + q % K;
-    for (int d = 0; d < nd; ++d) s[d] += a.x[d][i] * a.y[d][i];
-  }
+  for (int j = 0; j < N; ++j)
+    for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<long>(gridDim.x) * blockDim.x) {
+      const long i = j * Kp + k;
+      for (int d = 0; d < nd; ++d) s[d] += a.x[d][i] * a.y[d][i];
+    }
   __shared__ double sh[kMaxDots][8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int d = 0; d < nd; ++d) {
@@ -99,15 +99,16 @@ __global__ void __launch_bounds__(256) k_mdot_owned(int N, long Kp, int K, int n
   double s[kMdotChunk];
 #pragma unroll
   for (int d = 0; d < kMdotChunk; ++d) s[d] = 0.0;
-  const long n = static_cast<long>(N) * K;
-  for (long q = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; q < n;
-       q += static_cast<long>(gridDim.x) * blockDim.x) {
-    const long i = (q / K) * Kp + q % K;
-    const double wi = w[i];
+  // owned entries: planes j < N, elements k < K (no division in the loop)
+  for (int j = 0; j < N; ++j)
+    for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < K;
+         k += static_cast<long>(gridDim.x) * blockDim.x) {
+      const long i = j * Kp + k;
+      const double wi = w[i];
 #pragma unroll
-    for (int d = 0; d < kMdotChunk; ++d)
-      if (d < nd) s[d] = fma(a.v[d0 + d][i], wi, s[d]);
-  }
+      for (int d = 0; d < kMdotChunk; ++d)
+        if (d < nd) s[d] = fma(a.v[d0 + d][i], wi, s[d]);
+    }
   __shared__ double sh[kMdotChunk][8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -139,13 +140,20 @@ __global__ void __launch_bounds__(256) k_maxpy(long n, int nv, MAxpyArgs a, doub
   }
 }
 
+// one warp per dot product: lane l sums partials l, l+32, ... then a fixed
+// shuffle tree (deterministic; the former one-thread-per-dot loop over the
+// 296 partials took ~17 us, twice per Krylov iteration)
 __global__ void k_dots_final(int nd, const double* __restrict__ part, double* __restrict__ out) {
-  const int d = threadIdx.x;
+  const int d = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
   if (d >= nd) return;
   double v = 0.0;
-  for (int b = 0; b < kRedBlocks; ++b) v += part[d * kRedBlocks + b];
-  out[d] = v;
+  for (int b = lane; b < kRedBlocks; b += 32) v += part[d * kRedBlocks + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) out[d] = v;
 }
+
+inline unsigned final_blocks(int nd) { return static_cast<unsigned>((nd + 7) / 8); }  // 8 warps per block
 
 // SoA [nvec][N][Kp] <-> k-major [nvec][K][N]
 __global__ void k_soa_to_kmajor(int K, int N, long Kp, int nvec, const double* __restrict__ soa,
@@ -209,7 +217,7 @@ void launch_dots(Handle& h, long n, int nd, const double* const* xs, const doubl
     a.y[d] = ys[d];
   }
   k_dots_partial<<<kRedBlocks, 256, 0, h.stream>>>(n, nd, a, h.red.ptr);
-  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
+  k_dots_final<<<final_blocks(nd), 256, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
   LDG_CUDA(cudaGetLastError());
   h.launches += 2;
   LDG_CUDA(cudaMemcpyAsync(h.red_host, h.red.ptr + kMaxRed * kRedBlocks, sizeof(double) * nd,
@@ -251,7 +259,7 @@ void launch_dots_async(Handle& h, int nd, const double* const* xs, const double*
     a.y[d] = ys[d];
   }
   k_dots_owned<<<kRedBlocks, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nd, a, h.red.ptr);
-  k_dots_final<<<1, 32, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
+  k_dots_final<<<final_blocks(nd), 256, 0, h.stream>>>(nd, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
   LDG_CUDA(cudaGetLastError());
   h.launches += 2;
 }
@@ -265,7 +273,7 @@ void launch_mdots_async(Handle& h, int nv, const double* const* v, const double*
   for (int d = 0; d < nv; ++d) a.v[d] = v[d];
   const dim3 grid(kRedBlocks, (nv + kMdotChunk - 1) / kMdotChunk);
   k_mdot_owned<<<grid, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nv, a, w, h.red.ptr);
-  k_dots_final<<<1, 96, 0, h.stream>>>(nv, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
+  k_dots_final<<<final_blocks(nv), 256, 0, h.stream>>>(nv, h.red.ptr, h.red.ptr + kMaxRed * kRedBlocks);
   LDG_CUDA(cudaGetLastError());
   h.launches += 2;
 }
