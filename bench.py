@@ -129,6 +129,26 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(kernel_prefix, p, dim):
+    """dram__bytes_read + dram__bytes_write of the first matching launch (the
+    level-0 one: largest grid) in the committed ncu --set full summary
+    (profiles/*_ncu_traffic.json, scripts/ncu_traffic.py), or None."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        if d.get("p") != p or d.get("dim") != dim:
+            continue
+        ks = [k for k in d["kernels"] if k["kernel"].startswith(kernel_prefix) and k.get("dram_bytes")]
+        if ks:
+            k = max(ks, key=lambda k: k.get("launch__grid_size") or 0)
+            return k["dram_bytes"], f"{os.path.basename(path)}: {k['kernel']} grid {k['grid']}"
+    return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -436,9 +456,11 @@ def run_ours(args):
     if kloc is not None:
         bs = bytes_sweep_s2(dim, pd)
         achieved = bs / (kern[pd]["ms_sweep_s2"] * 1e-3) / 1e9
+        traffic, traffic_src = ncu_traffic("k_s2f<(int)%d, (int)1" % pd, pd, dim)
         roof = {"kernel": f"k_s2f (level-0 smoother stage 2 + block-Jacobi update, FP16 E), p={pd}",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": peak_src, "share_of_step_est": shares[pd], "bytes_per_launch": bs,
+                "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                "share_of_step_est": shares[pd], "bytes_per_launch": bs,
                 "others": {str(p): {"sweep_s2_GBps": bytes_sweep_s2(dim, p) / (kern[p]["ms_sweep_s2"] * 1e-3) / 1e9,
                                     "schur_apply_GBps": bytes_schur(dim, p) / (kern[p]["ms_schur"] * 1e-3) / 1e9,
                                     "assemble_GBps": bytes_asm(dim, p) / (kern[p]["ms_assemble"] * 1e-3) / 1e9,
