@@ -489,7 +489,7 @@ def run_ours(args):
             "config": {"workload": desc, "dim": dim, "K": 2 * dim * dim, "p": ps, "dt": dt,
                        "parallelism": f"strips{world} (NCCL halos + allreduce)" if world > 1 else "single",
                        "l2": "flushed (256 MB write) before every timed step; p>=2 working sets exceed L2",
-                       "solver": "FGMRES(60) on the exact Schur complement, geometric multigrid V(2,2) "
+                       "solver": "FGMRES(30) on the exact Schur complement, geometric multigrid V(2,2) "
                                  "(mixed-precision smoother), reference residual contract 1e-10",
                        "per_p": {str(p): {"ms_per_step": per_p[p]["ms"] / args.steps,
                                           "ms_assemble": per_p[p]["ms_asm"] / args.steps,

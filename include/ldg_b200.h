@@ -68,7 +68,7 @@ typedef struct ldg_solver_opts {
   int check_residual;   /* 1: enforce the reference residual contract      */
   double contract_tol;  /* 1e-10 in the reference                          */
   int krylov;           /* 0 FGMRES(restart) (default), 1 BiCGStab          */
-  int restart;          /* FGMRES basis size (<= 78; 0: 60)                 */
+  int restart;          /* FGMRES basis size (<= 78; 0: 30)                 */
 } ldg_solver_opts;
 
 typedef struct ldg_step_stats {

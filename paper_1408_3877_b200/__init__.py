@@ -231,7 +231,7 @@ class SolverOptions:
     check_residual: bool = True
     contract_tol: float = 1e-10
     krylov: int = 0  # 0 FGMRES(restart), 1 BiCGStab
-    restart: int = 60
+    restart: int = 30
 
     def to_c(self) -> _Opts:
         o = _Opts()

@@ -18,6 +18,8 @@
 // the pivot row of each column is chosen among the rows not yet used and
 // broadcast through shared memory; the lane that pivoted column c holds row c
 // of P^-1 at the end.
+#include <cuda_fp16.h>
+
 #include <cmath>
 
 #include "ldg_internal.hpp"
@@ -55,7 +57,7 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
 template <int P, int OUT>
 __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E,
                                                    const double* __restrict__ E_D, double wm, double dt, double eta,
-                                                   void* __restrict__ out) {
+                                                   void* __restrict__ out, float* __restrict__ out_scale) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG, Q = C::Q;
   __shared__ __align__(16) double s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
@@ -203,6 +205,23 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
     }
     __syncwarp();
   }
+  if constexpr (OUT == 3) {  // FP16 packed, scaled per element by max |P^-1|
+    double mx = 0.0;
+    if (row)
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) mx = fmax(mx, fabs(v[jj]));
+#pragma unroll
+    for (int o = NG / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double sc = mx > 0.0 ? mx : 1.0;
+    if (row) {
+      if (i == 0) out_scale[k] = static_cast<float>(sc);
+      const double inv = 1.0 / sc;
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj)
+        static_cast<__half*>(out)[sm_packed_p_index<P>(my_col, jj, Kp, k)] = __double2half(v[jj] * inv);
+    }
+    return;
+  }
   if (row) {  // this lane holds row my_col of P^-1
     const int r = my_col;
 #pragma unroll
@@ -220,22 +239,29 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
 
 }  // namespace
 
-// Pinv (FP64 SoA), Pinv32 (FP32 SoA) or Pq (FP32 packed) from the level's FP64 E
+// Pinv (FP64 SoA), Pinv32 (FP32 SoA), Pq (FP32 packed) or Ph + Pscale (FP16
+// packed, scaled per element) from the level's FP64 E
 void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
-  void* out = out_kind == 0 ? static_cast<void*>(h.Pinv.ptr)
-                            : (out_kind == 1 ? static_cast<void*>(h.Pinv32.ptr) : static_cast<void*>(h.Pq.ptr));
-#define CALL(P)                                                                                               \
-  do {                                                                                                        \
-    const unsigned grid = grid_of(h.K, Cfg<P>::EPB);                                                          \
-    if (out_kind == 0)                                                                                        \
-      k_bjac_warp<P, 0><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out);      \
-    else if (out_kind == 1)                                                                                   \
-      k_bjac_warp<P, 1><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out);      \
-    else                                                                                                      \
-      k_bjac_warp<P, 2><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out);      \
+  void* out = out_kind == 0   ? static_cast<void*>(h.Pinv.ptr)
+              : out_kind == 1 ? static_cast<void*>(h.Pinv32.ptr)
+              : out_kind == 2 ? static_cast<void*>(h.Pq.ptr)
+                              : static_cast<void*>(h.Ph.ptr);
+  float* sc = out_kind == 3 ? h.Pscale.ptr : nullptr;
+#define LAUNCH(P, O) \
+  k_bjac_warp<P, O><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, sc)
+#define CALL(P)                                                      \
+  do {                                                               \
+    const unsigned grid = grid_of(h.K, Cfg<P>::EPB);                 \
+    switch (out_kind) {                                              \
+      case 0: LAUNCH(P, 0); break;                                   \
+      case 1: LAUNCH(P, 1); break;                                   \
+      case 2: LAUNCH(P, 2); break;                                   \
+      default: LAUNCH(P, 3); break;                                  \
+    }                                                                \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
+#undef LAUNCH
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }

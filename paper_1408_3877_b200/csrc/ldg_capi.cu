@@ -318,7 +318,7 @@ ldg_solver_opts ldg_default_solver_opts(void) {
   o.check_residual = 1;
   o.contract_tol = 1e-10;
   o.krylov = 0;
-  o.restart = 60;
+  o.restart = 30;
   return o;
 }
 

@@ -130,6 +130,8 @@ struct Handle {
   DBuf<float4> Eq, Pq;                           // packed FP32 copies read by the fused smoother (ldg_smooth.cu)
   DBuf<uint2> Eh;                                // packed FP16 copy of E (4 values per uint2), scaled per element
   DBuf<float> Escale;                            // per-element scale of Eh
+  DBuf<uint2> Ph;                                // packed FP16 P^-1, scaled per element (Pscale)
+  DBuf<float> Pscale;
   DBuf<double> mg_s;                             // V-cycle ping-pong partner of x (fused smoother)
   DBuf<double> gm_V, gm_Z;                       // FGMRES basis and preconditioned basis ((m+1) and m vectors)
   int gm_m = 0;
@@ -249,7 +251,9 @@ void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double*
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_to_f32(Handle& h, long n, const double* src, float* dst);
-void launch_bjac(Handle& h, double wm, double dt, int out_kind);     // ldg_bjac.cu: 0 Pinv, 1 Pinv32, 2 Pq
+void launch_bjac(Handle& h, double wm, double dt, int out_kind);     // ldg_bjac.cu: 0 Pinv, 1 Pinv32, 2 Pq, 3 Ph
+bool smoother_e16();                                                  // FP16 E copies for the big-level smoother
+bool smoother_p16();                                                  // FP16 P^-1 copies likewise
 void launch_bjac_setup_quad(Handle& h, double wm, double dt);        // Pq from E (FP64)
 void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt);  // Pinv32 from E (FP64)
 bool level_uses_rows(const Handle& h);

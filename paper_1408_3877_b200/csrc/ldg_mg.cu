@@ -280,9 +280,17 @@ bool mg_build(Handle& h, int team_size) {
 void mg_setup_f32_level(Handle& L, double wm, double dt) {
   const long NN = static_cast<long>(L.N) * L.N;
   if (!level_uses_rows(L)) {
-    if (!L.Pq.ptr) L.Pq.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
+    if (smoother_p16()) {
+      if (!L.Ph.ptr) {
+        L.Ph.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
+        L.Pscale.alloc(L.Kp, &L.bytes);
+      }
+      launch_bjac(L, wm, dt, 3);
+    } else {
+      if (!L.Pq.ptr) L.Pq.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
+      launch_bjac_setup_quad(L, wm, dt);
+    }
     smooth_pack_e(L);
-    launch_bjac_setup_quad(L, wm, dt);
   } else {
     if (!L.E32.ptr) {
       L.E32.alloc(2 * NN * L.Kp, &L.bytes);

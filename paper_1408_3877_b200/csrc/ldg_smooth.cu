@@ -236,24 +236,25 @@ __device__ __forceinline__ void packed_apply(const TQ* __restrict__ blk, long Kp
   }
 }
 
-// d = P^-1 r
-template <int P, typename F>
-__device__ __forceinline__ void pinv_apply(const float4* __restrict__ Pk, long Kp, F load, float* d) {
+// d = P^-1 r (FP32 packed, or FP16 packed times the element's scale)
+template <int P, typename TQ, typename F>
+__device__ __forceinline__ void pinv_apply(const TQ* __restrict__ Pk, long Kp, F load, float* d) {
 #pragma unroll
   for (int i = 0; i < Cfg<P>::N; ++i) d[i] = 0.f;
-  packed_apply<P, float4>(Pk, Kp, load, d);
+  packed_apply<P, TQ>(Pk, Kp, load, d);
 }
 
 // r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
-template <int P, int MODE, typename TQ>
+template <int P, int MODE, typename TQ, typename TP>
 __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
                                              const double* x,
                                              const double* __restrict__ tz, const double* __restrict__ b, double wm,
-                                             double dteta, double dt, const float4* __restrict__ Pq, float omega,
-                                             double* out, int k0, int kend) {
+                                             double dteta, double dt, const TP* __restrict__ Pq,
+                                             const float* __restrict__ Pscale, float omega, double* out, int k0,
+                                             int kend) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
   constexpr int Q = C::Q;
@@ -341,33 +342,36 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, De
   } else {
     float d[N];
     if constexpr (C::kFlat) {
-      pinv_apply<P>(Pq + k, Kp,
-                    [&](int j) { return static_cast<float>(b[j * Kp + k] + static_cast<double>(acc[j])); }, d);
+      pinv_apply<P, TP>(Pq + k, Kp,
+                        [&](int j) { return static_cast<float>(b[j * Kp + k] + static_cast<double>(acc[j])); }, d);
     } else {
       const int tid = threadIdx.x;
 #pragma unroll
       for (int i = 0; i < N; ++i) s_r[i][tid] = static_cast<float>(b[i * Kp + k] + static_cast<double>(acc[i]));
-      pinv_apply<P>(Pq + k, Kp, [&](int j) { return s_r[j][tid]; }, d);
+      pinv_apply<P, TP>(Pq + k, Kp, [&](int j) { return s_r[j][tid]; }, d);
     }
+    const float om = Pscale ? omega * Pscale[k] : omega;
 #pragma unroll
     for (int i = 0; i < N; ++i)
-      out[i * Kp + k] = fma(static_cast<double>(omega), static_cast<double>(d[i]), x[i * Kp + k]);
+      out[i * Kp + k] = fma(static_cast<double>(om), static_cast<double>(d[i]), x[i * Kp + k]);
   }
 }
 
 // out = omega P^-1 b  (the first sweep from x = 0)
-template <int P>
-__global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const float4* __restrict__ Pq,
-                                             const double* __restrict__ b, float omega, double* __restrict__ out) {
+template <int P, typename TP>
+__global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const TP* __restrict__ Pq,
+                                             const float* __restrict__ Pscale, const double* __restrict__ b,
+                                             float omega, double* __restrict__ out) {
   constexpr int N = Cfg<P>::N;
   pdl_wait();
   pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   float d[N];
-  pinv_apply<P>(Pq + k, Kp, [&](int j) { return static_cast<float>(b[j * Kp + k]); }, d);
+  pinv_apply<P, TP>(Pq + k, Kp, [&](int j) { return static_cast<float>(b[j * Kp + k]); }, d);
+  const float om = Pscale ? omega * Pscale[k] : omega;
 #pragma unroll
-  for (int i = 0; i < N; ++i) out[i * Kp + k] = static_cast<double>(omega * d[i]);
+  for (int i = 0; i < N; ++i) out[i * Kp + k] = static_cast<double>(om * d[i]);
 }
 
 // Eq[c][q][k] from E[(c*4 + s)*NN + i*N + j][k] (FP64, row-major blocks);
@@ -424,13 +428,20 @@ long packed_p_quads(int p) {
   }
 }
 
-// Storage of the stored blocks read by the big-level smoother: FP16 with a
-// per-element scale (default; half the bytes of FP32 in the HBM-bound stage
-// 2) or FP32 (LDG_SMOOTHER_E=32).
+// Storage of the stored blocks read by the big-level smoother (diagonal E
+// blocks and P^-1): FP16 with a per-element scale (default; half the bytes of
+// FP32 in the HBM-bound stage 2) or FP32 (LDG_SMOOTHER_E=32).
 bool smoother_e16() {
   static const bool on = [] {
     const char* s = std::getenv("LDG_SMOOTHER_E");
     return !(s && std::atoi(s) == 32);
+  }();
+  return on;
+}
+bool smoother_p16() {  // P^-1 copy: FP16 unless LDG_SMOOTHER_P=32 (or E is FP32)
+  static const bool on = [] {
+    const char* s = std::getenv("LDG_SMOOTHER_P");
+    return smoother_e16() && !(s && std::atoi(s) == 32);
   }();
   return on;
 }
@@ -474,28 +485,32 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
                    double* out, int k0, int kend) {
   const double dteta = dt * h.prob.eta;
   const float om = static_cast<float>(omega);
-  const bool e16 = h.Eh.ptr != nullptr;
+  const bool e16 = h.Eh.ptr != nullptr, p16 = h.Ph.ptr != nullptr;
   if (kend < 0) kend = h.K;
   const unsigned grid = grid_of(kend - k0, 128);
-#define LAUNCH(P, M, TQ, EP, SC)                                                                                   \
-  launch_pdl(k_s2f<P, M, TQ>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr,               \
-             x, h.tz.ptr, b, wm, dteta, dt, h.Pq.ptr, om, out, k0, kend)
-#define CALL(P)                                                                         \
-  do {                                                                                  \
-    if (e16) {                                                                          \
-      if (mode == 0)                                                                    \
-        LAUNCH(P, 0, uint2, h.Eh.ptr, h.Escale.ptr);                                    \
-      else                                                                              \
-        LAUNCH(P, 1, uint2, h.Eh.ptr, h.Escale.ptr);                                    \
-    } else {                                                                            \
-      if (mode == 0)                                                                    \
-        LAUNCH(P, 0, float4, h.Eq.ptr, static_cast<const float*>(nullptr));             \
-      else                                                                              \
-        LAUNCH(P, 1, float4, h.Eq.ptr, static_cast<const float*>(nullptr));             \
-    }                                                                                   \
+#define LAUNCH(P, M, TQ, EP, SC, TP, PP, PS)                                                                       \
+  launch_pdl(k_s2f<P, M, TQ, TP>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr,           \
+             x, h.tz.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend)
+#define MODES(P, TQ, EP, SC, TP, PP, PS)        \
+  do {                                          \
+    if (mode == 0)                              \
+      LAUNCH(P, 0, TQ, EP, SC, TP, PP, PS);     \
+    else                                        \
+      LAUNCH(P, 1, TQ, EP, SC, TP, PP, PS);     \
+  } while (0)
+#define CALL(P)                                                                                             \
+  do {                                                                                                      \
+    const float* nos = nullptr;                                                                             \
+    if (e16 && p16)                                                                                         \
+      MODES(P, uint2, h.Eh.ptr, h.Escale.ptr, uint2, h.Ph.ptr, h.Pscale.ptr);                               \
+    else if (e16)                                                                                           \
+      MODES(P, uint2, h.Eh.ptr, h.Escale.ptr, float4, h.Pq.ptr, nos);                                       \
+    else                                                                                                    \
+      MODES(P, float4, h.Eq.ptr, nos, float4, h.Pq.ptr, nos);                                               \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
+#undef MODES
 #undef LAUNCH
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
@@ -503,7 +518,14 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
 
 void smooth_zero(Handle& h, const double* b, double omega, double* out) {
 #define CALL(P)                                                                                        \
-  launch_pdl(k_bjf<P>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Pq.ptr, b, static_cast<float>(omega), out)
+  do {                                                                                                          \
+    if (h.Ph.ptr)                                                                                               \
+      launch_pdl(k_bjf<P, uint2>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Ph.ptr, h.Pscale.ptr, b,    \
+                 static_cast<float>(omega), out);                                                               \
+    else                                                                                                        \
+      launch_pdl(k_bjf<P, float4>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Pq.ptr,                    \
+                 static_cast<const float*>(nullptr), b, static_cast<float>(omega), out);                        \
+  } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -620,10 +621,48 @@ void bicgstab(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_
 // reorthogonalisation pass, each pass one fused multi-dot (one host
 // synchronisation) and one fused multi-axpy over the basis; the Hessenberg
 // least-squares problem (Givens rotations) is solved on the host.
+// LDG_TRACE_ITER=1: device time of the parts of each FGMRES iteration
+// (copy in, V-cycle, copy out, operator, projections), summed and printed to
+// stderr per solve (diagnostics)
+struct IterTrace {
+  bool on = env_or("LDG_TRACE_ITER", 0) != 0;
+  cudaEvent_t ev[7] = {};  // 0..4 marks of the iteration, 5 after the projection, 6 the previous 5
+  double sum[6] = {0, 0, 0, 0, 0, 0};
+  int n = 0;
+  IterTrace() {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  ~IterTrace() {
+    if (!on || n == 0) return;
+    fprintf(stderr,
+            "[ldg trace] %d its, ms/it: copy-in %.3f vcycle %.3f copy-out %.3f operator %.3f project+sync %.3f "
+            "update+host %.3f\n",
+            n, sum[0] / n, sum[1] / n, sum[2] / n, sum[3] / n, sum[4] / n, n > 1 ? sum[5] / (n - 1) : 0.0);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void add(cudaStream_t st) {  // after the projection's host synchronisation
+    cudaEventRecord(ev[5], st);
+    cudaEventSynchronize(ev[5]);
+    float a;
+    for (int q = 0; q < 5; ++q) {
+      cudaEventElapsedTime(&a, ev[q], ev[q + 1]);
+      sum[q] += a;
+    }
+    if (n > 0) {  // previous projection end -> this iteration's start
+      cudaEventElapsedTime(&a, ev[6], ev[0]);
+      sum[5] += a;
+    }
+    std::swap(ev[5], ev[6]);
+    n++;
+  }
+};
+
 void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_opts& o, double tol, int* it_out,
             int* applies_out, double* rnorm_out) {
   Handle& h0 = T.h0();
-  int m = o.restart > 0 ? o.restart : 60;
+  IterTrace tr;
+  int m = o.restart > 0 ? o.restart : 30;
   m = std::min(m, kMaxRed - 2);
   {  // basis memory: (2m + 1) vectors per rank, within free device memory
     size_t free_b = 0, total_b = 0;
@@ -688,15 +727,20 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
     bool done = false;
     for (; j < m && it < o.maxit; ++j) {
       ++it;
+      if (tr.on) LDG_CUDA(cudaEventRecord(tr.ev[0], T.stream));
       // Z_j = M^-1 V_j (the V-cycle graph is keyed on kP -> kPh)
       if (pc == 2) {
         copy(kP, gmV(j));
+        if (tr.on) LDG_CUDA(cudaEventRecord(tr.ev[1], T.stream));
         precond(T, pc, f32, wm, dt, kP, kPh);
+        if (tr.on) LDG_CUDA(cudaEventRecord(tr.ev[2], T.stream));
         copy(gmZ(j), kPh);
       } else {
         precond(T, pc, f32, wm, dt, gmV(j), gmZ(j));
       }
+      if (tr.on) LDG_CUDA(cudaEventRecord(tr.ev[3], T.stream));
       schur_apply(T, wm, dt, gmZ(j), gmV(j + 1));
+      if (tr.on) LDG_CUDA(cudaEventRecord(tr.ev[4], T.stream));
       ++applies;
       // classical Gram-Schmidt: h = V^T w (+ |w|^2), w -= V h; a second pass
       // only when the projection removed more than half of |w|^2 ("twice is
@@ -709,6 +753,7 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
         Hij(i, j) = h1[i];
         ss -= h1[i] * h1[i];
       }
+      if (tr.on) tr.add(T.stream);  // (project() synchronised the stream: "project" includes that gap)
       if (!(ss > 0.5 * h1[j + 1])) {
         project(j + 1, gmV(j + 1), true, h2);
         subtract(j + 1, h2, gmV(j + 1));

@@ -7,13 +7,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1408_3877_b200 as ld
 
 dim = int(os.environ.get("DIM", "256"))
+OPTS = dict(restart=int(os.environ["RESTART"])) if "RESTART" in os.environ else {}
 for p in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2,3,4").split(",")]:
     s = ld.LdgSystem.square(dim, p, ld.BASELINE_SPEC)
     s.initial_state()
-    s.euler_steps(0.05, 2, ld.SolverOptions())
+    s.euler_steps(0.05, 2, ld.SolverOptions(**OPTS))
     rows = []
     for i in range(8):
-        st = s.euler_steps(0.05, 1, ld.SolverOptions())
+        st = s.euler_steps(0.05, 1, ld.SolverOptions(**OPTS))
         fin = st["ms_solve"] - st["ms_setup"] - st["ms_krylov"]
         rows.append((st["ms_assemble"] + st["ms_solve"], st["ms_assemble"], st["ms_setup"], st["ms_krylov"], fin,
                      st["iterations"]))

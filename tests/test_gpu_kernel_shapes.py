@@ -65,9 +65,10 @@ def _run(rows_below: int, extra: dict | None = None) -> dict:
 
 
 @pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (2048, {"LDG_MG_SMOOTHER": "rb"}),
-                                               (2048, {"LDG_TAIL_PMAX": "4", "LDG_TAIL_BELOW": "200"})],
+                                               (2048, {"LDG_TAIL_PMAX": "4", "LDG_TAIL_BELOW": "200"}),
+                                               (0, {"LDG_SMOOTHER_P": "32"}), (0, {"LDG_SMOOTHER_E": "32"})],
                          ids=["thread_kernels_fused_smoother", "row_kernels", "red_black_gauss_seidel",
-                              "single_block_coarse_tail"])
+                              "single_block_coarse_tail", "fp32_block_inverse_copy", "fp32_smoother_copies"])
 def test_kernel_shape(rows_below, extra):
     out = _run(rows_below, extra)
     for key, r in out.items():
