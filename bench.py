@@ -83,12 +83,12 @@ def bytes_schur(dim, p):
 
 def bytes_sweep_s2(dim, p):
     """Compulsory bytes of the level-0 smoother stage 2 with the fused block-Jacobi
-    update (k_s2f, FP16 packed E diagonal blocks + per-element scale, FP32 packed
-    P^-1): E 2 blocks x quads x 8 B, P quads x 16 B, vectors x, t (2), D, b, out
-    (FP64), geometry (10 doubles) and topology (9 ints)."""
+    update (k_s2f, FP16 packed E diagonal blocks and P^-1, each with a per-element
+    scale): E 2 blocks x quads x 8 B, P quads x 8 B, 2 scales, vectors x, t (2),
+    D, b, out (FP64), geometry (10 doubles) and topology (9 ints)."""
     K, N = 2 * dim * dim, n_of(p)
     q = packed_quads(p)
-    return K * (2 * q * 8 + 4 + q * 16 + 8 * 6 * N + 8 * 10 + 4 * 9)
+    return K * (2 * q * 8 + q * 8 + 2 * 4 + 8 * 6 * N + 8 * 10 + 4 * 9)
 
 
 def bytes_asm(dim, p):
@@ -456,7 +456,7 @@ def run_ours(args):
     if kloc is not None:
         bs = bytes_sweep_s2(dim, pd)
         achieved = bs / (kern[pd]["ms_sweep_s2"] * 1e-3) / 1e9
-        traffic, traffic_src = ncu_traffic("k_s2f<(int)%d, (int)1" % pd, pd, dim)
+        traffic, traffic_src = ncu_traffic("k_s2f<%d, 1" % pd, pd, dim)
         roof = {"kernel": f"k_s2f (level-0 smoother stage 2 + block-Jacobi update, FP16 E), p={pd}",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,

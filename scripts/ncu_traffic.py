@@ -16,10 +16,12 @@ txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", "
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 h, units = rows[0], rows[1]
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6,
+         "us": 1e-3, "ms": 1.0, "ns": 1e-6}
 res = []
 for r in rows[2:]:
-    e = {"kernel": r[h.index("Kernel Name")].split("(DevMesh")[0].replace("void ldgb::<unnamed>::", ""),
+    name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "")
+    e = {"kernel": name.split("::")[-1].replace("(int)", ""),
          "grid": r[h.index("Grid Size")]}
     for m in M:
         if m not in h:
