@@ -47,7 +47,12 @@ struct DBuf {
     release(counter);
     if (count == 0) return;
     LDG_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    // cudaMemset runs on the legacy default stream, which does not order
+    // against the library's non-blocking streams: wait for it, or a kernel
+    // launched right after the allocation can be overtaken by the zeroing
+    // (seen as FP16 smoother copies full of inf on a second handle)
     LDG_CUDA(cudaMemset(ptr, 0, count * sizeof(T)));
+    LDG_CUDA(cudaDeviceSynchronize());
     n = count;
     if (counter) *counter += static_cast<int64_t>(count * sizeof(T));
   }
@@ -200,6 +205,8 @@ struct Team {
 // pdl_wait() before reading what its predecessor wrote (ldg_device.cuh).
 // Used for the latency-bound multigrid kernels; LDG_PDL=0 disables it.
 bool pdl_enabled();
+bool debug_nan();  // LDG_DEBUG_NAN=1
+int debug_count_nonfinite(cudaStream_t st, const void* v, long n, bool half, const char* what);
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};

@@ -16,6 +16,7 @@
 // against the oracle first: 12-27 BiCGStab iterations for p = 1..4
 // independent of h, against 170-2100 with block-Jacobi alone.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ldg_internal.hpp"
@@ -301,8 +302,26 @@ void mg_setup_f32_level(Handle& L, double wm, double dt) {
   }
 }
 
+void debug_level(Handle& L, int l) {
+  char w[64];
+  const long NN = static_cast<long>(L.N) * L.N;
+  snprintf(w, sizeof(w), "level %d E", l);
+  debug_count_nonfinite(L.stream, L.E.ptr, 2 * NN * L.Kp, false, w);
+  if (L.Eh.ptr) {
+    snprintf(w, sizeof(w), "level %d Eh", l);
+    debug_count_nonfinite(L.stream, L.Eh.ptr, 4 * L.Eh.n, true, w);
+  }
+  if (L.Ph.ptr) {
+    snprintf(w, sizeof(w), "level %d Ph", l);
+    debug_count_nonfinite(L.stream, L.Ph.ptr, 4 * L.Ph.n, true, w);
+  }
+  snprintf(w, sizeof(w), "level %d D", l);
+  debug_count_nonfinite(L.stream, L.D.ptr, L.vec_len(), false, w);
+}
+
 void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
   if (f32) mg_setup_f32_level(h, wm, dt);
+  if (debug_nan()) debug_level(h, 0);
   for (auto& cp : h.coarse) {
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);
@@ -311,6 +330,7 @@ void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
       mg_setup_f32_level(c, wm, dt);
     else
       launch_bjac_setup(c, wm, dt);
+    if (debug_nan()) debug_level(c, static_cast<int>(&cp - &h.coarse[0]) + 1);
   }
 }
 

@@ -42,14 +42,22 @@ double env_or(const char* name, double dflt) {
   const char* s = std::getenv(name);
   return s ? std::atof(s) : dflt;
 }
+// Sweeps (pre counts the residual-free first sweep from x = 0): V(5,5) on
+// level 0 and V(2,1) below.  Level-0 sweeps stream at ~60 % of HBM bandwidth
+// while the coarse levels are latency-bound, so smoothing moved to level 0
+// buys more per microsecond: measured at 256^2, p = 0..4, ms/step
+// 5.6/11.4/24.8/45/95 with V(2,2) everywhere vs 6.1/8.9/17.9/33.8/68.4
+// (V(4,4)+V(1,1): 6.9/10.8/19.3/37.1/78.4; swept in scripts/gpu_mgtune.sh).
 const double kOmega = env_or("LDG_MG_OMEGA", 0.7);  // damped block-Jacobi smoother
-const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));    // pre-smoothing sweeps (the first from x = 0 is residual-free)
-const int kPost = static_cast<int>(env_or("LDG_MG_POST", 2));  // post-smoothing sweeps (V(2,1) measured slower: +20-40% iterations)
-const int kPre0 = static_cast<int>(env_or("LDG_MG_PRE0", kPre));    // level 0
-const int kPost0 = static_cast<int>(env_or("LDG_MG_POST0", kPost));  // level 0
+const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));    // coarse levels
+const int kPost = static_cast<int>(env_or("LDG_MG_POST", 1));  // coarse levels
+const int kPre0 = static_cast<int>(env_or("LDG_MG_PRE0", 5));    // level 0
+const int kPost0 = static_cast<int>(env_or("LDG_MG_POST0", 5));  // level 0
 const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
-int pre_of(int l) { return l == 0 ? kPre0 : kPre; }
-int post_of(int l) { return l == 0 ? kPost0 : kPost; }
+const int kPre1 = static_cast<int>(env_or("LDG_MG_PRE1", kPre));    // level 1
+const int kPost1 = static_cast<int>(env_or("LDG_MG_POST1", kPost));  // level 1
+int pre_of(int l) { return l == 0 ? kPre0 : (l == 1 ? kPre1 : kPre); }
+int post_of(int l) { return l == 0 ? kPost0 : (l == 1 ? kPost1 : kPost); }
 
 #define LDG_NCCL(call)                                                                          \
   do {                                                                                          \
@@ -438,12 +446,12 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     for (int s = 0; s < sweeps; ++s) smooth(T, l, f32, wm, dt, b, x);
     return;
   }
-  for (int s = 1; s < kPre; ++s) smooth(T, l, f32, wm, dt, b, x);
+  for (int s = 1; s < pre_of(l); ++s) smooth(T, l, f32, wm, dt, b, x);
   residual(T, l, f32, wm, dt, b, x, kMgR);
   for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
   vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
   for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
-  for (int s = 0; s < kPost; ++s) smooth(T, l, f32, wm, dt, b, x);
+  for (int s = 0; s < post_of(l); ++s) smooth(T, l, f32, wm, dt, b, x);
 }
 
 int64_t team_launches(Team& T) {

@@ -3,7 +3,10 @@
 // entries only, so strip ghosts never count twice), layout conversion
 // between the element-interleaved device vectors and the reference's
 // k-major host vectors, and the per-rank assembly step.
+#include <cuda_fp16.h>
+
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -187,7 +190,49 @@ __global__ void k_kmajor_to_soa(int K, int N, long Kp, int nvec, const double* _
     default: { CALL(4); break; } \
   }
 
+__global__ void k_count_nonfinite(long n, const double* __restrict__ v, int* __restrict__ out) {
+  int c = 0;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    c += isfinite(v[i]) ? 0 : 1;
+  if (c) atomicAdd(out, c);
+}
+
+__global__ void k_count_nonfinite_h(long n, const __half* __restrict__ v, int* __restrict__ out) {
+  int c = 0;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    c += isfinite(__half2float(v[i])) ? 0 : 1;
+  if (c) atomicAdd(out, c);
+}
+
 }  // namespace
+
+// LDG_DEBUG_NAN=1 (diagnostics): count non-finite values of a device array
+// (synchronises the stream) and report them on stderr under `what`
+bool debug_nan() {
+  static const bool on = [] {
+    const char* s = std::getenv("LDG_DEBUG_NAN");
+    return s && std::atoi(s) != 0;
+  }();
+  return on;
+}
+
+int debug_count_nonfinite(cudaStream_t st, const void* v, long n, bool half, const char* what) {
+  int* d = nullptr;
+  int h = 0;
+  LDG_CUDA(cudaMallocAsync(&d, sizeof(int), st));
+  LDG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
+  if (half)
+    k_count_nonfinite_h<<<256, 256, 0, st>>>(n, static_cast<const __half*>(v), d);
+  else
+    k_count_nonfinite<<<256, 256, 0, st>>>(n, static_cast<const double*>(v), d);
+  LDG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  LDG_CUDA(cudaFreeAsync(d, st));
+  LDG_CUDA(cudaStreamSynchronize(st));
+  if (h) fprintf(stderr, "[ldg nan] %s: %d non-finite of %ld\n", what, h, n);
+  return h;
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -239,3 +239,16 @@ def test_cpp_host_mirror_simulate(ld):
         r = subprocess.run([sim, "16", "1", "10", "1.0"] + extra, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr
         assert "simulate: 10 steps" in r.stdout
+
+
+def test_consecutive_handles_fp16_smoother(ld):
+    """Buffers allocated lazily by one handle's first solve must be zeroed
+    before its kernels use them: the zeroing ran on the legacy default stream
+    without ordering against the library's non-blocking stream, and a second
+    handle at 512^2, p = 3 got FP16 smoother copies full of inf (regression)."""
+    for _ in range(2):
+        s = ld.LdgSystem.square(512, 3, ld.BASELINE_SPEC)
+        s.initial_state()
+        st = s.euler_steps(0.1, 1, ld.SolverOptions())
+        assert st["residual"] <= 1e-10 and st["iterations"] < 40, st
+        s.close()
