@@ -365,6 +365,8 @@ bool rb_smoother() {
   return on;
 }
 const double kOmegaGS = env_or("LDG_MG_OMEGA_GS", 1.0);
+// second Gram-Schmidt pass when the first removed more than (1 - eta) of |w|^2
+const double kReorthEta = env_or("LDG_REORTH_ETA", 0.5);
 
 void sweep_rb(Team& T, int l, double wm, double dt, Vec b, Vec x, bool reverse) {
   for (int h = 0; h < 2; ++h) {
@@ -762,7 +764,7 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
         ss -= h1[i] * h1[i];
       }
       if (tr.on) tr.add(T.stream);  // (project() synchronised the stream: "project" includes that gap)
-      if (!(ss > 0.5 * h1[j + 1])) {
+      if (!(ss > kReorthEta * h1[j + 1])) {
         project(j + 1, gmV(j + 1), true, h2);
         subtract(j + 1, h2, gmV(j + 1));
         ss = h2[j + 1];
