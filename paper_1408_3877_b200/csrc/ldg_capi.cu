@@ -263,6 +263,10 @@ int create_square_team(int dim, double jitter, uint64_t seed, int p, const ldg_p
       alloc_step_buffers(*hp);
       T.ranks.push_back(std::move(hp));
     }
+    if (T.nccl) {  // NCCL halo staging at its final size (captured graphs bake the pointers)
+      const long cap = 3L * T.h0().N * dim;
+      for (ldgb::DBuf<double>* b : {&T.send_l, &T.send_r, &T.recv_l, &T.recv_r}) b->alloc(cap, nullptr);
+    }
     LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
   if (rc == LDG_OK) *out = H.release();

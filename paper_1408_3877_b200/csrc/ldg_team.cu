@@ -117,6 +117,12 @@ void copy_cols(double* dst, long dpitch, const double* src, long spitch, long wi
                              rows, cudaMemcpyDeviceToDevice, s));
 }
 
+bool cudaStreamIsCapturing_(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  LDG_CUDA(cudaStreamIsCapturing(s, &st));
+  return st != cudaStreamCaptureStatusNone;
+}
+
 // Refreshes the ghost columns of vector v (ncomp blocks of N planes) on
 // level `level` of every local rank.
 void halo(Team& T, int level, Vec v, int ncomp) {
@@ -154,7 +160,11 @@ void halo(Team& T, int level, Vec v, int ncomp) {
     const long cnt = rows * L.dim;
     const bool left = L.ghost_left && !T.local(g - 1), right = L.ghost_right && !T.local(g + 1);
     if (static_cast<long>(T.send_l.n) < cnt) {
-      for (DBuf<double>* b : {&T.send_l, &T.send_r, &T.recv_l, &T.recv_r}) b->alloc(cnt, nullptr);
+      // sized once for the largest exchange (3 components on level 0): the
+      // V-cycle graphs bake these pointers, so they must never move
+      if (cudaStreamIsCapturing_(T.stream)) throw Error(LDG_ENCCL, "halo staging allocated during graph capture");
+      const long cap = std::max(cnt, 3L * T.h0().N * T.h0().dim);
+      for (DBuf<double>* b : {&T.send_l, &T.send_r, &T.recv_l, &T.recv_r}) b->alloc(cap, nullptr);
     }
     if (left) copy_cols(T.send_l.ptr, L.dim, vp(L, v) + L.own_left_off(), L.Kp, L.dim, rows, T.stream);
     if (right) copy_cols(T.send_r.ptr, L.dim, vp(L, v) + L.own_right_off(), L.Kp, L.dim, rows, T.stream);
