@@ -106,6 +106,7 @@ struct Handle {
   // Krylov workspace (N * Kp each)
   DBuf<double> kr_r, kr_rh, kr_p, kr_v, kr_s, kr_t, kr_ph, kr_sh, kr_b;
   DBuf<double> tz;       // 2 * N * Kp : M^-1 B^m x
+  DBuf<float> tz32;      // the same for the FP32 smoother on single-rank thread-per-element levels
   DBuf<double> Pinv;     // N*N * Kp : block-Jacobi inverse
   DBuf<double> full_r, full_y;  // 3 * N * Kp : reference residual contract
   DBuf<double> red;      // reduction scratch

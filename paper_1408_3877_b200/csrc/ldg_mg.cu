@@ -196,6 +196,14 @@ int mg_levels(const Handle& h) { return 1 + static_cast<int>(h.coarse.size()); }
 
 double coarse_jitter_scale();
 
+bool tz32_enabled() {  // LDG_SMOOTHER_TZ=64: keep the FP64 stage-1 output in the smoother
+  static const bool on = [] {
+    const char* e = std::getenv("LDG_SMOOTHER_TZ");
+    return !(e && std::atoi(e) == 64);
+  }();
+  return on;
+}
+
 // Number of coarse levels for FK(dim) split into `size` equal strips: halve
 // while dim stays even, the coarse mesh keeps dim >= 2, and every rank keeps
 // at least one whole column with even strip boundaries.  Every rank computes
@@ -281,6 +289,8 @@ bool mg_build(Handle& h, int team_size) {
 void mg_setup_f32_level(Handle& L, double wm, double dt) {
   const long NN = static_cast<long>(L.N) * L.N;
   if (!level_uses_rows(L)) {
+    // stage-1 output of the smoother in FP32 (no halo of it across ranks: single rank only)
+    if (L.size == 1 && !L.tz32.ptr && tz32_enabled()) L.tz32.alloc(2 * L.vec_len(), &L.bytes);
     if (smoother_p16()) {
       if (!L.Ph.ptr) {
         L.Ph.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);

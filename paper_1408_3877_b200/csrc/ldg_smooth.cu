@@ -100,9 +100,9 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
 }
 
 // tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
-template <int P>
+template <int P, typename TT>
 __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
-                                             double* __restrict__ tout) {
+                                             TT* __restrict__ tout) {
   constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
   extern __shared__ __align__(16) float smf[];
   const float* tb = stage_f(smf, T.fbase + T.fmH, 14 * TAB);  // tmH 2 | tmSd 3 | tmSo 9
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s1f(DevMesh m, De
   const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    tout[i * Kp + k] = static_cast<double>(inv2a * u1[i]);
-    tout[(N + i) * Kp + k] = static_cast<double>(inv2a * u2[i]);
+    tout[i * Kp + k] = static_cast<TT>(inv2a * u1[i]);
+    tout[(N + i) * Kp + k] = static_cast<TT>(inv2a * u2[i]);
   }
 }
 
@@ -247,11 +247,11 @@ __device__ __forceinline__ void pinv_apply(const TQ* __restrict__ Pk, long Kp, F
 // r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
-template <int P, int MODE, typename TQ, typename TP>
+template <int P, int MODE, typename TQ, typename TP, typename TT>
 __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
                                              const double* x,
-                                             const double* __restrict__ tz, const double* __restrict__ b, double wm,
+                                             const TT* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const TP* __restrict__ Pq,
                                              const float* __restrict__ Pscale, float omega, double* out, int k0,
                                              int kend) {
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, De
   // diagonal blocks E^m_kk t^m_k (packed stream), scaled copy
 #pragma unroll 1
   for (int c = 0; c < 2; ++c) {
-    const double* tc = tz + static_cast<long>(c) * N * Kp + k;
+    const TT* tc = tz + static_cast<long>(c) * N * Kp + k;
     packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
                         [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
   }
@@ -474,7 +474,14 @@ void smooth_pack_e(Handle& h) {
 
 void smooth_stage1(Handle& h, const double* x) {
 #define CALL(P)                                                                            \
-  launch_pdl(k_s1f<P>, grid_of(h.K, 128), 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr)
+  do {                                                                                                          \
+    if (h.tz32.ptr)                                                                                             \
+      launch_pdl(k_s1f<P, float>, grid_of(h.K, 128), 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x,          \
+                 h.tz32.ptr);                                                                                   \
+    else                                                                                                        \
+      launch_pdl(k_s1f<P, double>, grid_of(h.K, 128), 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x,         \
+                 h.tz.ptr);                                                                                     \
+  } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
@@ -489,8 +496,14 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
   if (kend < 0) kend = h.K;
   const unsigned grid = grid_of(kend - k0, 128);
 #define LAUNCH(P, M, TQ, EP, SC, TP, PP, PS)                                                                       \
-  launch_pdl(k_s2f<P, M, TQ, TP>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr,           \
-             x, h.tz.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend)
+  do {                                                                                                            \
+    if (h.tz32.ptr)                                                                                               \
+      launch_pdl(k_s2f<P, M, TQ, TP, float>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,        \
+                 h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend);                            \
+    else                                                                                                          \
+      launch_pdl(k_s2f<P, M, TQ, TP, double>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,       \
+                 h.D.ptr, x, h.tz.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend);                              \
+  } while (0)
 #define MODES(P, TQ, EP, SC, TP, PP, PS)        \
   do {                                          \
     if (mode == 0)                              \
