@@ -139,6 +139,8 @@ struct Handle {
   DBuf<uint2> Ph;                                // packed FP16 P^-1, scaled per element (Pscale)
   DBuf<float> Pscale;
   DBuf<double> mg_s;                             // V-cycle ping-pong partner of x (fused smoother)
+  DBuf<double> mg_zero;                          // zeros (Chebyshev eigenvalue estimate)
+  double cheb_lmax = 0.0;                        // estimated largest eigenvalue of P^-1 S_c (0: not yet)
   DBuf<double> gm_V, gm_Z;                       // FGMRES basis and preconditioned basis ((m+1) and m vectors)
   int gm_m = 0;
   bool mg_f32 = true;                            // smoother on FP32 copies (precond 2) or FP64 (3)
@@ -206,6 +208,7 @@ struct Team {
 // pdl_wait() before reading what its predecessor wrote (ldg_device.cuh).
 // Used for the latency-bound multigrid kernels; LDG_PDL=0 disables it.
 bool pdl_enabled();
+void launch_fill_hash(Handle& h, double* v);  // fixed pseudo-random vector
 bool debug_nan();  // LDG_DEBUG_NAN=1
 int debug_count_nonfinite(cudaStream_t st, const void* v, long n, bool half, const char* what);
 template <typename... KArgs, typename... Args>
@@ -274,8 +277,10 @@ void smooth_stage1(Handle& h, const double* x);                       // tz = M^
 // mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)
 // [k0, kend): element range (default all owned); out may equal x for one
 // colour of the FK element graph (red-black Gauss-Seidel half-sweep)
+// cheb_beta != 0: Chebyshev step out <- x + omega P^-1 r + cheb_beta (x - out_old)
+// (out_old = x_{k-1}, taken as 0 when prev_zero)
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, int k0 = 0, int kend = -1);
+                   double* out, int k0 = 0, int kend = -1, double cheb_beta = 0.0, int prev_zero = 0);
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 // the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
 void small_stage1(Handle& h, const double* x);

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, De
                                              const TT* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const TP* __restrict__ Pq,
                                              const float* __restrict__ Pscale, float omega, double* out, int k0,
-                                             int kend) {
+                                             int kend, double cheb_beta, int prev_zero) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
   constexpr int Q = C::Q;
@@ -351,9 +351,17 @@ __global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, De
       pinv_apply<P, TP>(Pq + k, Kp, [&](int j) { return s_r[j][tid]; }, d);
     }
     const float om = Pscale ? omega * Pscale[k] : omega;
+    if (cheb_beta == 0.0) {
 #pragma unroll
-    for (int i = 0; i < N; ++i)
-      out[i * Kp + k] = fma(static_cast<double>(om), static_cast<double>(d[i]), x[i * Kp + k]);
+      for (int i = 0; i < N; ++i)
+        out[i * Kp + k] = fma(static_cast<double>(om), static_cast<double>(d[i]), x[i * Kp + k]);
+    } else {  // Chebyshev step: out (holding x_{k-1}, or 0) <- x + a P^-1 r + beta (x - x_{k-1})
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double xi = x[i * Kp + k], xp = prev_zero ? 0.0 : out[i * Kp + k];
+        out[i * Kp + k] = fma(static_cast<double>(om), static_cast<double>(d[i]), fma(cheb_beta, xi - xp, xi));
+      }
+    }
   }
 }
 
@@ -489,7 +497,7 @@ void smooth_stage1(Handle& h, const double* x) {
 }
 
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, int k0, int kend) {
+                   double* out, int k0, int kend, double cheb_beta, int prev_zero) {
   const double dteta = dt * h.prob.eta;
   const float om = static_cast<float>(omega);
   const bool e16 = h.Eh.ptr != nullptr, p16 = h.Ph.ptr != nullptr;
@@ -499,10 +507,10 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
   do {                                                                                                            \
     if (h.tz32.ptr)                                                                                               \
       launch_pdl(k_s2f<P, M, TQ, TP, float>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,        \
-                 h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend);                            \
+                 h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend, cheb_beta, prev_zero);       \
     else                                                                                                          \
       launch_pdl(k_s2f<P, M, TQ, TP, double>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,       \
-                 h.D.ptr, x, h.tz.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend);                              \
+                 h.D.ptr, x, h.tz.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend, cheb_beta, prev_zero);         \
   } while (0)
 #define MODES(P, TQ, EP, SC, TP, PP, PS)        \
   do {                                          \

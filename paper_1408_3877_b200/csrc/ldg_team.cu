@@ -70,8 +70,8 @@ Handle& level_of(Handle& h, int l) { return l == 0 ? h : *h.coarse[l - 1]; }
 // named per-rank vectors: a Team operation names a vector, each rank
 // resolves it to its own buffer
 enum Vec : int {
-  kR, kRh, kP, kV, kS, kT, kPh, kSh, kB, kC, kY, kTz, kMgX, kMgB, kMgR, kMgS, kVz, kVc, kFullR, kFullY, kCold, kYold,
-  kNone
+  kR, kRh, kP, kV, kS, kT, kPh, kSh, kB, kC, kY, kTz, kMgX, kMgB, kMgR, kMgS, kMgZ, kVz, kVc, kFullR, kFullY, kCold,
+  kYold, kNone
 };
 
 // FGMRES basis vectors: V_j = kGmV0 + j, Z_j = kGmZ0 + j
@@ -100,6 +100,7 @@ double* vp(Handle& h, Vec v) {
     case kMgB: return h.mg_b.ptr;
     case kMgR: return h.mg_r.ptr;
     case kMgS: return h.mg_s.ptr;
+    case kMgZ: return h.mg_zero.ptr;
     case kVz: return h.Vv.ptr;
     case kVc: return h.Vv.ptr + 2 * n;
     case kFullR: return h.full_r.ptr;
@@ -396,6 +397,77 @@ void sweep_rb(Team& T, int l, double wm, double dt, Vec b, Vec x, bool reverse) 
 
 bool rb_level(Team& T, int l) { return rb_smoother() && tier(level_of(T.h0(), l)) != kMid; }
 
+// Chebyshev smoothing on level 0 (LDG_MG_CHEB=1): the damped Jacobi sweeps
+// replaced by Chebyshev steps for P^-1 S_c on [lmax / ratio, lmax], lmax from
+// a power iteration when the V-cycle graph is captured.  Same kernels (the
+// step's extra term reads x_{k-1} from the ping-pong partner).
+bool cheb_on() {
+  static const bool on = env_or("LDG_MG_CHEB", 1) != 0;
+  return on;
+}
+const double kChebRatio = env_or("LDG_MG_CHEB_RATIO", 20.0);
+const double kChebSafety = env_or("LDG_MG_CHEB_SAFETY", 1.15);
+const int kChebPower = static_cast<int>(env_or("LDG_MG_CHEB_POWER", 30));  // power iterations
+bool cheb_level(Team& T, int l) { return cheb_on() && l == 0 && tier(level_of(T.h0(), 0)) == kBig; }
+
+struct Cheb {
+  double theta, delta, sigma, rho;
+  explicit Cheb(double lmax) {
+    const double hi = kChebSafety * lmax, lo = hi / kChebRatio;
+    theta = 0.5 * (hi + lo);
+    delta = 0.5 * (hi - lo);
+    sigma = theta / delta;
+    rho = 1.0 / sigma;
+  }
+  // coefficients of step k (k = 0 starts the recurrence)
+  void step(int k, double* alpha, double* beta) {
+    if (k == 0) {
+      rho = 1.0 / sigma;
+      *alpha = 1.0 / theta;
+      *beta = 0.0;
+      return;
+    }
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    *alpha = 2.0 * rn / delta;
+    *beta = rn * rho;
+    rho = rn;
+  }
+};
+
+void sweep_cheb(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo, double alpha, double beta,
+                bool prev_zero) {
+  halo(T, l, xi, 1);
+  each(T, l, [&](Handle& L) { f_stage1(L, xi); });
+  halo(T, l, kTz, 2);
+  each(T, l, [&](Handle& L) {
+    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), 0, -1, beta, prev_zero ? 1 : 0);
+  });
+}
+
+void lincomb(Team& T, double a, Vec x, double b, Vec y, double c, Vec z, Vec out);
+
+// largest eigenvalue of P^-1 S_c on level 0 by power iteration from a fixed
+// pseudo-random vector (an underestimate lets the Chebyshev polynomial amplify
+// the modes above it; a start from kP lacks the high-frequency modes)
+double estimate_lmax(Team& T, double wm, double dt) {
+  each(T, 0, [&](Handle& L) {
+    if (!L.mg_zero.ptr) L.mg_zero.alloc(L.vec_len(), &L.bytes);
+  });
+  if (env_or("LDG_MG_CHEB_START", 0) != 0)
+    lincomb(T, 1.0, kP, 0.0, kNone, 0.0, kNone, kMgS);
+  else
+    each(T, 0, [&](Handle& L) { launch_fill_hash(L, vp(L, kMgS)); });  // all modes present
+  double nv = norm(T, kMgS), lam = 0.0;
+  for (int it = 0; it < kChebPower && nv > 0.0; ++it) {
+    lincomb(T, 1.0 / nv, kMgS, 0.0, kNone, 0.0, kNone, kMgS);
+    residual_f(T, 0, wm, dt, kMgZ, kMgS, kMgR);                                     // r = -S_c v
+    each(T, 0, [&](Handle& L) { smooth_zero(L, vp(L, kMgR), -1.0, vp(L, kMgS)); });  // v <- P^-1 S_c v
+    nv = norm(T, kMgS);
+    lam = nv;
+  }
+  return lam;
+}
+
 // One V-cycle on level l: x = V(b).  Fused levels alternate x with the
 // level's scratch vector; the first (residual-free) sweep writes whichever
 // buffer makes the last sweep land in x.
@@ -431,6 +503,29 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
     for (int s = 0; s < post_of(l); ++s) sweep_rb(T, l, wm, dt, b, x, true);
+    return;
+  }
+  if (fused(T, l, f32) && cheb_level(T, l) && !coarsest) {
+    Cheb ch(T.h0().cheb_lmax);
+    double a, be;
+    Vec cur = (sweeps % 2) ? kMgS : x;
+    auto other = [&](Vec v) { return v == x ? kMgS : x; };
+    ch.step(0, &a, &be);
+    each(T, l, [&](Handle& L) { smooth_zero(L, vp(L, b), a, vp(L, cur)); });
+    for (int s = 0; s < pre_of(l) - 1; ++s) {
+      ch.step(s + 1, &a, &be);
+      sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, s == 0);
+      cur = other(cur);
+    }
+    residual_f(T, l, wm, dt, b, cur, kMgR);
+    for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
+    vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
+    for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
+    for (int s = 0; s < post_of(l); ++s) {
+      ch.step(s, &a, &be);
+      sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, false);
+      cur = other(cur);
+    }
     return;
   }
   if (fused(T, l, f32)) {
@@ -488,6 +583,10 @@ void precond_mg(Team& T, bool f32, double wm, double dt, Vec b, Vec x) {
       return;
     }
   if (h.vgraphs.size() >= 8) mg_release(h);
+  if (f32 && cheb_level(T, 0)) {
+    h.cheb_lmax = estimate_lmax(T, wm, dt);  // (kernels run eagerly, before capture)
+    if (env_or("LDG_DEBUG_CHEB", 0) != 0) fprintf(stderr, "[ldg cheb] lmax %.6g\n", h.cheb_lmax);
+  }
   const int64_t before = team_launches(T);
   cudaGraph_t graph = nullptr;
   LDG_CUDA(cudaStreamBeginCapture(T.stream, cudaStreamCaptureModeThreadLocal));

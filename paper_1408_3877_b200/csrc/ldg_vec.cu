@@ -234,6 +234,27 @@ int debug_count_nonfinite(cudaStream_t st, const void* v, long n, bool half, con
   return h;
 }
 
+namespace {
+// a fixed pseudo-random vector in [-0.5, 0.5) on the owned entries (halo and
+// padding slots zero: start of power iterations)
+__global__ void k_fill_hash(long n, long Kp, int K, double* __restrict__ v) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    unsigned long long z = static_cast<unsigned long long>(i) + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    v[i] = i % Kp < K ? static_cast<double>(z >> 11) * 0x1.0p-53 - 0.5 : 0.0;
+  }
+}
+}  // namespace
+
+void launch_fill_hash(Handle& h, double* v) {
+  k_fill_hash<<<kRedBlocks * 4, 256, 0, h.stream>>>(h.vec_len(), h.Kp, h.K, v);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* s = std::getenv("LDG_PDL");

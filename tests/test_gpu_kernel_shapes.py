@@ -2,11 +2,13 @@
 
 The library picks per level between thread-per-element kernels (with the
 fused mixed-precision smoother of ldg_smooth.cu) and the row-parallel kernels
-(ldg_rows.cu) by element count (LDG_ROWS_BELOW, default 65536), so the
+(ldg_rows.cu) by element count (LDG_ROWS_BELOW, default 2048), so the
 parity meshes (<= 32^2) would only ever see the row kernels.  Each case runs
 in a subprocess with the switch forced one way, and checks the multigrid
 solve against block-Jacobi (same state to the solve tolerance) and the FP32
-smoother against the FP64 one (same iteration count within a small margin)."""
+smoother against the FP64 one (same iteration count within a small margin).
+With the thread kernels on level 0 the default V-cycle smooths level 0 with
+Chebyshev polynomials (LDG_MG_CHEB); the last case covers the Jacobi sweeps."""
 from __future__ import annotations
 
 import json
@@ -66,9 +68,11 @@ def _run(rows_below: int, extra: dict | None = None) -> dict:
 
 @pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (2048, {"LDG_MG_SMOOTHER": "rb"}),
                                                (2048, {"LDG_TAIL_PMAX": "4", "LDG_TAIL_BELOW": "200"}),
-                                               (0, {"LDG_SMOOTHER_P": "32"}), (0, {"LDG_SMOOTHER_E": "32"})],
+                                               (0, {"LDG_SMOOTHER_P": "32"}), (0, {"LDG_SMOOTHER_E": "32"}),
+                                               (0, {"LDG_MG_CHEB": "0"})],
                          ids=["thread_kernels_fused_smoother", "row_kernels", "red_black_gauss_seidel",
-                              "single_block_coarse_tail", "fp32_block_inverse_copy", "fp32_smoother_copies"])
+                              "single_block_coarse_tail", "fp32_block_inverse_copy", "fp32_smoother_copies",
+                              "jacobi_level0_no_chebyshev"])
 def test_kernel_shape(rows_below, extra):
     out = _run(rows_below, extra)
     for key, r in out.items():
