@@ -150,7 +150,12 @@ def ncu_traffic(kernel_prefix, p, dim):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region.
+
+    The nvidia-smi process is started before the warm-up (its start-up, a
+    driver/NVML initialisation, stalls the GPU's first launches by several ms)
+    and only the samples taken after mark() -- the start of the timed region --
+    are reported."""
 
     def __init__(self, index=0):
         self.index = index
@@ -158,6 +163,10 @@ class ClockSampler:
         self._stop = threading.Event()
         self._proc = None
         self._thread = None
+        self._mark = 0
+
+    def mark(self):
+        self._mark = len(self.samples)
 
     def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -188,6 +197,8 @@ class ClockSampler:
                 self._proc.kill()
         if self._thread is not None:
             self._thread.join(timeout=5)
+        if len(self.samples) > self._mark:
+            self.samples = self.samples[self._mark:]
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
@@ -298,11 +309,13 @@ def run_assembly_c3(args):
                           boundary=boundary)
     s = ld.LdgSystem.square(dim, p, spec)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")
-    for i in range(args.warmup):
-        s.assemble_blocks(0.01 * (i + 1))
     clocks = ClockSampler(local)
     if not args.no_clocks:
         clocks.start()
+    for i in range(args.warmup):
+        s.assemble_blocks(0.01 * (i + 1))
+    torch.cuda.synchronize()
+    clocks.mark()
     total_ms = 0.0
     launches0 = s.info()["launches"]
     for i in range(args.steps):
@@ -397,16 +410,17 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    clocks = ClockSampler(local)
+    if not args.no_clocks:
+        clocks.start()
     # warm-up (W full steps)
     for _ in range(args.warmup):
         for s in systems:
             s.euler_steps(dt, 1, opts)
     barrier()
+    clocks.mark()
     launches0 = sum(s.info()["launches"] for s in systems)
     per_p = {p: dict(ms=0.0, ms_asm=0.0, ms_solve=0.0, iters=0, applies=0, residual=0.0) for p in ps}
-    clocks = ClockSampler(local)
-    if not args.no_clocks:
-        clocks.start()
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()

@@ -188,15 +188,17 @@ void halo(Team& T, int level, Vec v, int ncomp) {
 // sums over local ranks in a fixed order (deterministic) and across
 // processes with one ncclAllReduce.
 template <typename F>
-void reduce_dots(Team& T, int nd, F launch, double* out) {
+void reduce_dots(Team& T, int nd, F launch, double* out, int level = 0) {
   if (nd > kMaxRed || T.nlocal() > kMaxLocalRanks) throw Error(LDG_EINVAL, "reduction too large");
-  for (auto& rp : T.ranks) launch(*rp);
+  for (auto& rp : T.ranks) launch(level_of(*rp, level));
   if (T.nlocal() == 1 && T.size == 1) {
-    LDG_CUDA(cudaMemcpyAsync(T.red_host, dots_result(T.h0()), sizeof(double) * nd, cudaMemcpyDeviceToHost, T.stream));
+    LDG_CUDA(cudaMemcpyAsync(T.red_host, dots_result(level_of(T.h0(), level)), sizeof(double) * nd,
+                             cudaMemcpyDeviceToHost, T.stream));
   } else {
     // rank r's partial sums in slot r + 1 of the scratch (slot 0: the result)
     for (int r = 0; r < T.nlocal(); ++r)
-      LDG_CUDA(cudaMemcpyAsync(T.red_all.ptr + kMaxRed * (r + 1), dots_result(*T.ranks[r]), sizeof(double) * nd,
+      LDG_CUDA(cudaMemcpyAsync(T.red_all.ptr + kMaxRed * (r + 1), dots_result(level_of(*T.ranks[r], level)),
+                               sizeof(double) * nd,
                                cudaMemcpyDeviceToDevice, T.stream));
     LDG_CUDA(cudaMemcpyAsync(T.red_host + kMaxRed, T.red_all.ptr + kMaxRed, sizeof(double) * kMaxRed * T.nlocal(),
                              cudaMemcpyDeviceToHost, T.stream));
@@ -250,6 +252,19 @@ double sq_norm3(Team& T, Vec v) {
 double norm(Team& T, Vec x) {
   double r;
   dots(T, 1, &x, &x, &r);
+  return std::sqrt(r);
+}
+
+// 2-norm of a level-l vector (owned entries, all ranks)
+double norm_level(Team& T, int l, Vec x) {
+  double r;
+  reduce_dots(
+      T, 1,
+      [&](Handle& L) {
+        const double* px = vp(L, x);
+        launch_dots_async(L, 1, &px, &px);
+      },
+      &r, l);
   return std::sqrt(r);
 }
 
@@ -397,10 +412,11 @@ void sweep_rb(Team& T, int l, double wm, double dt, Vec b, Vec x, bool reverse) 
 
 bool rb_level(Team& T, int l) { return rb_smoother() && tier(level_of(T.h0(), l)) != kMid; }
 
-// Chebyshev smoothing on level 0 (LDG_MG_CHEB=1): the damped Jacobi sweeps
-// replaced by Chebyshev steps for P^-1 S_c on [lmax / ratio, lmax], lmax from
-// a power iteration when the V-cycle graph is captured.  Same kernels (the
-// step's extra term reads x_{k-1} from the ping-pong partner).
+// Chebyshev smoothing (LDG_MG_CHEB=1) on the first LDG_MG_CHEB_LEVELS levels
+// that run the fused thread kernels: the damped Jacobi sweeps replaced by
+// Chebyshev steps for P^-1 S_c on [lmax / ratio, lmax], lmax from a power
+// iteration when the V-cycle graph is captured.  Same kernels (the step's
+// extra term reads x_{k-1} from the ping-pong partner).
 bool cheb_on() {
   static const bool on = env_or("LDG_MG_CHEB", 1) != 0;
   return on;
@@ -408,7 +424,10 @@ bool cheb_on() {
 const double kChebRatio = env_or("LDG_MG_CHEB_RATIO", 20.0);
 const double kChebSafety = env_or("LDG_MG_CHEB_SAFETY", 1.15);
 const int kChebPower = static_cast<int>(env_or("LDG_MG_CHEB_POWER", 30));  // power iterations
-bool cheb_level(Team& T, int l) { return cheb_on() && l == 0 && tier(level_of(T.h0(), 0)) == kBig; }
+const int kChebLevels = static_cast<int>(env_or("LDG_MG_CHEB_LEVELS", 1));
+bool cheb_level(Team& T, int l) {
+  return cheb_on() && l < kChebLevels && l + 1 < levels(T) && tier(level_of(T.h0(), l)) == kBig;
+}
 
 struct Cheb {
   double theta, delta, sigma, rho;
@@ -449,20 +468,20 @@ void lincomb(Team& T, double a, Vec x, double b, Vec y, double c, Vec z, Vec out
 // largest eigenvalue of P^-1 S_c on level 0 by power iteration from a fixed
 // pseudo-random vector (an underestimate lets the Chebyshev polynomial amplify
 // the modes above it; a start from kP lacks the high-frequency modes)
-double estimate_lmax(Team& T, double wm, double dt) {
-  each(T, 0, [&](Handle& L) {
+double estimate_lmax(Team& T, int l, double wm, double dt) {
+  each(T, l, [&](Handle& L) {
     if (!L.mg_zero.ptr) L.mg_zero.alloc(L.vec_len(), &L.bytes);
+    if (!L.red.ptr) L.red.alloc(reduction_scratch(), &L.bytes);
+    launch_fill_hash(L, vp(L, kMgS));  // all modes present
   });
-  if (env_or("LDG_MG_CHEB_START", 0) != 0)
-    lincomb(T, 1.0, kP, 0.0, kNone, 0.0, kNone, kMgS);
-  else
-    each(T, 0, [&](Handle& L) { launch_fill_hash(L, vp(L, kMgS)); });  // all modes present
-  double nv = norm(T, kMgS), lam = 0.0;
+  double nv = norm_level(T, l, kMgS), lam = 0.0;
   for (int it = 0; it < kChebPower && nv > 0.0; ++it) {
-    lincomb(T, 1.0 / nv, kMgS, 0.0, kNone, 0.0, kNone, kMgS);
-    residual_f(T, 0, wm, dt, kMgZ, kMgS, kMgR);                                     // r = -S_c v
-    each(T, 0, [&](Handle& L) { smooth_zero(L, vp(L, kMgR), -1.0, vp(L, kMgS)); });  // v <- P^-1 S_c v
-    nv = norm(T, kMgS);
+    each(T, l, [&](Handle& L) {
+      launch_lincomb3(L, L.vec_len(), 1.0 / nv, vp(L, kMgS), 0.0, nullptr, 0.0, nullptr, vp(L, kMgS));
+    });
+    residual_f(T, l, wm, dt, kMgZ, kMgS, kMgR);                                     // r = -S_c v
+    each(T, l, [&](Handle& L) { smooth_zero(L, vp(L, kMgR), -1.0, vp(L, kMgS)); });  // v <- P^-1 S_c v
+    nv = norm_level(T, l, kMgS);
     lam = nv;
   }
   return lam;
@@ -506,7 +525,7 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     return;
   }
   if (fused(T, l, f32) && cheb_level(T, l) && !coarsest) {
-    Cheb ch(T.h0().cheb_lmax);
+    Cheb ch(level_of(T.h0(), l).cheb_lmax);
     double a, be;
     Vec cur = (sweeps % 2) ? kMgS : x;
     auto other = [&](Vec v) { return v == x ? kMgS : x; };
@@ -583,9 +602,11 @@ void precond_mg(Team& T, bool f32, double wm, double dt, Vec b, Vec x) {
       return;
     }
   if (h.vgraphs.size() >= 8) mg_release(h);
-  if (f32 && cheb_level(T, 0)) {
-    h.cheb_lmax = estimate_lmax(T, wm, dt);  // (kernels run eagerly, before capture)
-    if (env_or("LDG_DEBUG_CHEB", 0) != 0) fprintf(stderr, "[ldg cheb] lmax %.6g\n", h.cheb_lmax);
+  for (int l = 0; f32 && l < levels(T); ++l) {
+    if (!cheb_level(T, l)) continue;
+    const double lmax = estimate_lmax(T, l, wm, dt);  // (kernels run eagerly, before capture)
+    for (auto& rp : T.ranks) level_of(*rp, l).cheb_lmax = lmax;
+    if (env_or("LDG_DEBUG_CHEB", 0) != 0) fprintf(stderr, "[ldg cheb] level %d lmax %.6g\n", l, lmax);
   }
   const int64_t before = team_launches(T);
   cudaGraph_t graph = nullptr;
