@@ -708,7 +708,8 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
     const ldg_solver_opts o = opts ? *opts : ldg_default_solver_opts();
     if (st) *st = ldg_step_stats{};
     Handle& h0 = T.h0();
-    LDG_CUDA(cudaEventRecord(h0.ev[3], T.stream));
+    // ev[5]: run_steps/team_solve re-record ev[0..4] inside the region
+    LDG_CUDA(cudaEventRecord(h0.ev[5], T.stream));
     if (T.nlocal() == 1 && T.size == 1) {
       // one rank: the stacked host state is exactly the rank's owned rows
       const size_t cnt = 3L * h0.K * h0.N;
@@ -730,7 +731,7 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
     LDG_CUDA(cudaEventRecord(h0.ev[2], T.stream));
     LDG_CUDA(cudaEventSynchronize(h0.ev[2]));
     float tot = 0.f;
-    cudaEventElapsedTime(&tot, h0.ev[3], h0.ev[2]);
+    cudaEventElapsedTime(&tot, h0.ev[5], h0.ev[2]);
     if (ms_total) *ms_total = tot;
   });
 }

@@ -118,7 +118,7 @@ struct Handle {
 
   cudaStream_t stream = nullptr;
   bool owns_stream = true;
-  cudaEvent_t ev[6] = {};  // 0-2 step timing, 3-4 solve phases (team_solve), 5 spare
+  cudaEvent_t ev[6] = {};  // 0-2 step timing, 3-4 solve phases (team_solve), 5 host-buffer call span
   std::string err;
 
   // geometric multigrid hierarchy (ldg_mg.cu).  The top handle is level 0;
