@@ -200,6 +200,20 @@ int ldg_initial_state(ldg_handle* h);  /* system.hpp:99-107 */
 int ldg_set_state(ldg_handle* h, const double* y, double t);
 int ldg_get_state(ldg_handle* h, double* y, double* t);
 
+/* ---- post-processing of the device-resident state (fields.hpp:84-123) -- */
+
+/* l2_error (fields.hpp:100-123): ||u_h - exact(t, .)||_{L2} of state
+ * component `component` (0 Z1, 1 Z2, 2 C, the SystemState order of
+ * system.hpp:40-43) with a quad_rule_2d of order q_ord; the convergence
+ * study uses order 2p + 2 on C (convergence.hpp:96).  Summed over all ranks. */
+int ldg_l2_error(ldg_handle* h, int component, const ldg_coeff* exact, double t, int q_ord, double* err);
+
+/* to_lagrange (fields.hpp:87-97) of state component `component`: values at
+ * the 3 vertices (p <= 1) or vertices + edge midpoints (p >= 2) of every
+ * element, K x nodes k-major on the host (global element order); *nodes
+ * receives 3 or 6. */
+int ldg_to_lagrange(ldg_handle* h, int component, double* out, int* nodes);
+
 ldg_solver_opts ldg_default_solver_opts(void);
 
 /* nsteps implicit Euler steps of length dt (system.hpp:155-174), entirely on

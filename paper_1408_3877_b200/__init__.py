@@ -14,6 +14,7 @@ Reference interface -> this module
   assemble_* operators                 LdgSystem.operator(name)
   initial_state / euler_step           LdgSystem.initial_state / euler_step
   solve_stationary                     LdgSystem.solve_stationary
+  l2_error / to_lagrange (fields.hpp)  LdgSystem.l2_error / to_lagrange
 Exceptions follow the reference: ValueError for std::invalid_argument,
 MeshError for ldg::MeshError, RuntimeError for solver failures.
 """
@@ -119,6 +120,8 @@ _SIGNATURES = {
     "ldg_euler_steps_host": (C.c_int, [_H, C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_void_p,
                                        C.POINTER(_Opts), C.POINTER(_Stats), _dp]),
     "ldg_solve_stationary": (C.c_int, [_H, C.c_double, C.POINTER(_Opts), C.POINTER(_Stats)]),
+    "ldg_l2_error": (C.c_int, [_H, C.c_int, C.POINTER(_Coeff), C.c_double, C.c_int, _dp]),
+    "ldg_to_lagrange": (C.c_int, [_H, C.c_int, _dp, C.POINTER(C.c_int)]),
     "ldg_apply_lhs": (C.c_int, [_H, C.c_double, _dp, _dp]),
     "ldg_time_kernels": (C.c_int, [_H, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(_Times)]),
     "ldg_sync": (C.c_int, [_H]),
@@ -178,8 +181,8 @@ def _i(a):
 
 
 def _coeff(fn) -> _Coeff:
-    if isinstance(fn, str):
-        fn = (FN[fn], [])
+    if isinstance(fn, (str, int)):
+        fn = (fn, [])
     fid, params = fn
     if isinstance(fid, str):
         fid = FN[fid]
@@ -457,6 +460,26 @@ class LdgSystem:
         K, n = self.num_t, self.n
         self.last_stats = {k: getattr(st, k) for k, _ in _Stats._fields_}
         return y[2 * kn:].reshape(K, n), y[:kn].reshape(K, n), y[kn:2 * kn].reshape(K, n)
+
+    _COMPONENTS = dict(z1=0, z2=1, c=2)
+
+    def l2_error(self, exact, t: float, q_ord: int, component: str = "c") -> float:
+        """l2_error(mesh, dof, exact, t, q_ord) (fields.hpp:100-123) of a component
+        of the device-resident state ('c', 'z1' or 'z2')."""
+        err = C.c_double()
+        c = _coeff(exact)
+        self._check(load_library().ldg_l2_error(self._h, self._COMPONENTS[component], C.byref(c), float(t),
+                                                int(q_ord), C.byref(err)))
+        return err.value
+
+    def to_lagrange(self, component: str = "c") -> np.ndarray:
+        """to_lagrange(dof) (fields.hpp:87-97) of a state component -> K x 3 (p <= 1) or K x 6."""
+        m = 3 if self.p <= 1 else 6
+        out = np.zeros(self.num_t * m)
+        nodes = C.c_int()
+        self._check(load_library().ldg_to_lagrange(self._h, self._COMPONENTS[component], _d(out), C.byref(nodes)))
+        assert nodes.value == m
+        return out.reshape(self.num_t, m)
 
     def apply_lhs(self, dt: float, x) -> np.ndarray:
         """(W + dt A) x with the operators of the last assemble."""

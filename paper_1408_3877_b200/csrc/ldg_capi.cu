@@ -472,6 +472,54 @@ int ldg_project(ldg_handle* H, const ldg_coeff* fn, double t, int q_ord, double*
   });
 }
 
+int ldg_l2_error(ldg_handle* H, int component, const ldg_coeff* exact, double t, int q_ord, double* err) {
+  if (!H || !exact || !err) return LDG_EINVAL;
+  return guarded(H, [&] {
+    Team& T = H->team;
+    if (component < 0 || component > 2) throw Error(LDG_EINVAL, "state component must be 0 (Z1), 1 (Z2) or 2 (C)");
+    if (exact->id < 0 || exact->id >= LDG_FN_COUNT) throw Error(LDG_EINVAL, "unknown coefficient function id");
+    if (q_ord < 0) throw Error(LDG_EINVAL, "quadrature order must be non-negative");
+    std::vector<std::unique_ptr<DBuf<double>>> tmp;
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      DBuf<double> rule;
+      int R = 0;
+      ldgb::upload_rule(h, q_ord, rule, &R);
+      tmp.push_back(std::make_unique<DBuf<double>>());
+      tmp.back()->alloc(h.vec_len(), nullptr);
+      LDG_CUDA(cudaMemsetAsync(tmp.back()->ptr, 0, sizeof(double) * h.vec_len(), T.stream));
+      ldgb::launch_l2err(h, rule.ptr, R, *exact, t, h.Y.ptr + static_cast<long>(component) * h.vec_len(),
+                         tmp.back()->ptr);
+      LDG_CUDA(cudaStreamSynchronize(T.stream));
+    }
+    size_t i = 0;
+    *err = std::sqrt(ldgb::team_sum_sq(T, [&](Handle&) { return static_cast<const double*>(tmp[i++]->ptr); }));
+  });
+}
+
+int ldg_to_lagrange(ldg_handle* H, int component, double* out, int* nodes) {
+  if (!H || !out) return LDG_EINVAL;
+  return guarded(H, [&] {
+    Team& T = H->team;
+    if (component < 0 || component > 2) throw Error(LDG_EINVAL, "state component must be 0 (Z1), 1 (Z2) or 2 (C)");
+    const int M = ldgb::lagrange_nodes(T.h0().p);
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      DBuf<double> phi, dev;
+      ldgb::upload_lagrange_phi(h, phi);
+      dev.alloc(static_cast<size_t>(h.K) * M, nullptr);
+      ldgb::launch_lagrange(h, phi.ptr, h.Y.ptr + static_cast<long>(component) * h.vec_len(), dev.ptr);
+      std::vector<double> loc(static_cast<size_t>(h.K) * M);
+      LDG_CUDA(cudaMemcpyAsync(loc.data(), dev.ptr, sizeof(double) * loc.size(), cudaMemcpyDeviceToHost, T.stream));
+      LDG_CUDA(cudaStreamSynchronize(T.stream));
+      for (int k = 0; k < h.K; ++k)
+        std::memcpy(out + static_cast<long>(h.gid[k]) * M, loc.data() + static_cast<size_t>(k) * M,
+                    sizeof(double) * M);
+    }
+    if (nodes) *nodes = M;
+  });
+}
+
 int ldg_assemble(ldg_handle* H, double t) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {

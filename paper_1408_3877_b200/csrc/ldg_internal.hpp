@@ -8,6 +8,7 @@
 #include <stdexcept>
 #include <string>
 #include <memory>
+#include <functional>
 #include <vector>
 
 #include "../../include/ldg_b200.h"
@@ -247,6 +248,13 @@ void launch_assemble(Handle& h, int mode, double* out);
 void launch_static(Handle& h, int mode, double* out);
 void upload_rule(Handle& h, int q_ord, DBuf<double>& buf, int* R);
 
+// field post-processing (ldg_fields.cu; fields.hpp:84-123)
+void launch_l2err(Handle& h, const double* rule, int R, const ldg_coeff& f, double t, const double* u,
+                  double* out);  // out (Kp plane): per-element error, owned-entry self-dot = squared error
+int lagrange_nodes(int p);     // 3 (p <= 1) or 6 output nodes per element
+void upload_lagrange_phi(Handle& h, DBuf<double>& buf);
+void launch_lagrange(Handle& h, const double* phi, const double* u, double* out);  // out: K x nodes k-major
+
 // solver (ldg_solve.cu)
 void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);
 void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
@@ -314,6 +322,7 @@ void team_schur_apply_c(Team& T, double wm, double dt);     // kr_v = S_c C (ker
 int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, double* ms_level, int max_levels);
 void team_sweep_s2_prepare(Team& T, double wm, double dt);  // multigrid set up, level-0 stage 1 done
 void team_sweep_s2(Team& T, double wm, double dt);          // one level-0 smoother stage-2 launch
+double team_sum_sq(Team& T, const std::function<const double*(Handle&)>& v);  // owned entries, all ranks
 
 // multigrid (ldg_mg.cu)
 int mg_depth(int dim, int team_size);

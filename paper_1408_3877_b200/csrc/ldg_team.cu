@@ -1091,4 +1091,17 @@ int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, dou
   return nl;
 }
 
+// sum of squares of the owned entries of one vector per rank, over all ranks
+double team_sum_sq(Team& T, const std::function<const double*(Handle&)>& v) {
+  double s;
+  reduce_dots(
+      T, 1,
+      [&](Handle& h) {
+        const double* p[1] = {v(h)};
+        launch_dots_async(h, 1, p, p);
+      },
+      &s);
+  return s;
+}
+
 }  // namespace ldgb

@@ -182,6 +182,23 @@ class LdgSystem {
             std::vector<double>(s.y.begin() + kn, s.y.begin() + 2 * kn)};
   }
 
+  /// l2_error(mesh, dof, exact, t, q_ord) (fields.hpp:100-123) of the
+  /// device-resident state component (0 Z1, 1 Z2, 2 C).
+  double l2_error(const ldg_coeff& exact, double t, int q_ord, int component = 2) const {
+    double e = 0.0;
+    detail::check(ldg_l2_error(h_.get(), component, &exact, t, q_ord, &e), h_.get());
+    return e;
+  }
+
+  /// to_lagrange(dof) (fields.hpp:87-97) of a state component: K x 3 (p <= 1)
+  /// or K x 6, k-major; *nodes receives the column count.
+  std::vector<double> to_lagrange(int component = 2, int* nodes = nullptr) const {
+    const int m = info_.p <= 1 ? 3 : 6;
+    std::vector<double> out(static_cast<size_t>(num_t()) * m);
+    detail::check(ldg_to_lagrange(h_.get(), component, out.data(), nodes), h_.get());
+    return out;
+  }
+
  private:
   LdgSystem(ldg_handle* h, ProblemSpec spec) : h_(h), spec_(std::move(spec)) { load_info(); }
   void load_info() { detail::check(ldg_get_info(h_.get(), &info_), h_.get()); }

@@ -1,0 +1,105 @@
+"""Field post-processing on the device (fields.hpp:84-123) and the
+reference's order-(p+1) L2 convergence reproduced with the device solver.
+
+* ldg_l2_error / ldg_to_lagrange against the CPU oracle restatement on the
+  same device state;
+* the convergence study of convergence.hpp:77-103 (manufactured stationary
+  problem, Dirichlet on IDs 2/4, Neumann on 1/3, domain_square(1/3) refined j
+  times) solved on the device for p = 0..4, j = 0..4: errors against the
+  reference's own rows (tests/golden/convergence.npz, p <= 3, j <= 3) and the
+  estimated orders against the acceptance thresholds of SURVEY.md §8d
+  (|alpha - (p+1)| <= 0.25 for p = 1..3, <= 0.35 for p = 4, |alpha| <= 0.15
+  for p = 0; acceptance.cpp:77-93).  FK(3 * 2^j) is exactly the j-times
+  red-refined domain_square(1/3) (same triangles, other numbering), so the L2
+  errors agree up to rounding and the solver tolerance.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ldg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ld():
+    import paper_1408_3877_b200 as ld
+
+    ld.load_library()
+    return ld
+
+
+def mms_spec(ld):
+    return ld.ProblemSpec(d="exp_sum", f="mms_f", c_d="mms_exact", g_n="mms_gn", c0="mms_exact", eta=1.0,
+                          boundary={1: "N", 2: "D", 3: "N", 4: "D"})
+
+
+def _oracle_mesh(s):
+    lists = s.mesh_lists()
+    return O.generate_grid_data(lists["coords"], lists["v0t"])
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3, 4])
+def test_l2_error_and_lagrange_match_oracle(p, ld):
+    s = ld.LdgSystem.square(6, p, ld.BASELINE_SPEC)
+    y, _ = s.initial_state()
+    s.euler_steps(0.05, 2, ld.SolverOptions(rtol=1e-14))
+    y, t = s.get_state()
+    kn = s.block_dim
+    m = _oracle_mesh(s)
+    for comp, sl, fn in (("c", slice(2 * kn, 3 * kn), (8, [])), ("z1", slice(0, kn), (14, [])),
+                         ("z2", slice(kn, 2 * kn), (15, []))):
+        dof = y[sl].reshape(s.num_t, s.n)
+        for q in (2 * p + 2, 1, 7):
+            dev = s.l2_error(fn[0], t, q, comp)
+            ref = O.l2_error(m, dof, O.coeff(fn), t, q)
+            assert abs(dev - ref) <= 1e-12 * ref, (comp, q, dev, ref)
+        lag = s.to_lagrange(comp)
+        np.testing.assert_allclose(lag, O.to_lagrange(dof), rtol=0, atol=1e-13 * np.abs(dof).max())
+
+
+def test_l2_error_of_projection_is_small(ld):
+    """l2_error of the projected initial state shrinks with p (fields.hpp:53-123)."""
+    errs = []
+    for p in range(5):
+        s = ld.LdgSystem.square(16, p, ld.BASELINE_SPEC)
+        s.initial_state()
+        errs.append(s.l2_error("base_c", 0.0, 2 * p + 2))
+    assert all(b < a for a, b in zip(errs, errs[1:])), errs
+
+
+def test_l2_error_rejects_bad_arguments(ld):
+    s = ld.LdgSystem.square(4, 1, ld.BASELINE_SPEC)
+    s.initial_state()
+    with pytest.raises(ValueError):
+        s.l2_error(99, 0.0, 4)
+    with pytest.raises(KeyError):
+        s.l2_error("mms_exact", 0.0, 4, component="y")
+
+
+ORDER_TOL = {0: 0.15, 1: 0.25, 2: 0.25, 3: 0.25, 4: 0.35}
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3, 4])
+def test_convergence_order_on_device(p, ld, golden):
+    ref = golden("convergence")["rows"]  # (p, j, h, K, error, alpha), reference run_convergence
+    spec = mms_spec(ld)
+    errs = []
+    for j in range(5):
+        dim = 3 * 2 ** j
+        s = ld.LdgSystem.square(dim, p, spec)
+        s.solve_stationary(0.0, ld.SolverOptions(rtol=1e-13, maxit=100000))
+        assert s.num_t == 2 * dim * dim
+        errs.append(s.l2_error("mms_exact", 0.0, 2 * p + 2))
+        s.close()
+        row = ref[(ref[:, 0] == p) & (ref[:, 1] == j)]
+        if len(row):
+            assert int(row[0][3]) == 2 * dim * dim
+            assert abs(errs[-1] - row[0][4]) <= 1e-8 * row[0][4], (j, errs[-1], row[0][4])
+    alphas = [math.log(a / b) / math.log(2.0) for a, b in zip(errs, errs[1:])]
+    target = 0.0 if p == 0 else p + 1.0
+    assert abs(alphas[-1] - target) <= ORDER_TOL[p], (p, alphas)
