@@ -479,6 +479,7 @@ int ldg_l2_error(ldg_handle* H, int component, const ldg_coeff* exact, double t,
     if (component < 0 || component > 2) throw Error(LDG_EINVAL, "state component must be 0 (Z1), 1 (Z2) or 2 (C)");
     if (exact->id < 0 || exact->id >= LDG_FN_COUNT) throw Error(LDG_EINVAL, "unknown coefficient function id");
     if (q_ord < 0) throw Error(LDG_EINVAL, "quadrature order must be non-negative");
+    ensure_solver(T);  // reduction scratch
     std::vector<std::unique_ptr<DBuf<double>>> tmp;
     for (auto& rp : T.ranks) {
       Handle& h = *rp;

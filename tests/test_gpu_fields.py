@@ -11,7 +11,9 @@ reference's order-(p+1) L2 convergence reproduced with the device solver.
   (|alpha - (p+1)| <= 0.25 for p = 1..3, <= 0.35 for p = 4, |alpha| <= 0.15
   for p = 0; acceptance.cpp:77-93).  FK(3 * 2^j) is exactly the j-times
   red-refined domain_square(1/3) (same triangles, other numbering), so the L2
-  errors agree up to rounding and the solver tolerance.
+  errors agree to ~1e-3 (the vertex order moves the quadrature points); the
+  reference-numbered ladder (oracle refine_uniform, through ldg_create) pins
+  the reference's rows to 1e-8.
 """
 from __future__ import annotations
 
@@ -84,9 +86,44 @@ def test_l2_error_rejects_bad_arguments(ld):
 ORDER_TOL = {0: 0.15, 1: 0.25, 2: 0.25, 3: 0.25, 4: 0.35}
 
 
+def _ladder_meshes(j_max):
+    """domain_square(1/3) refined j times (convergence.hpp:84-88), reference numbering."""
+    m = O.domain_square(1.0 / 3.0)
+    out = [m]
+    for _ in range(j_max):
+        m = O.refine_uniform(m)
+        out.append(m)
+    return out
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3])
+def test_convergence_rows_match_reference(p, ld, golden):
+    """The reference's own rows (run_convergence, p <= 3, j <= 3) on the reference's
+    refined meshes (same numbering, hence the same quadrature points), solved on
+    the device: errors within 1e-8 relative."""
+    ref = golden("convergence")["rows"]  # (p, j, h, K, error, alpha)
+    spec = mms_spec(ld)
+    errs = []
+    for j, m in enumerate(_ladder_meshes(3)):
+        ids = np.asarray(m.id_e0t, dtype=np.int32)
+        s = ld.LdgSystem.from_mesh(m.coord_v, m.v0t, p, spec, id_e0t=ids)
+        s.solve_stationary(0.0, ld.SolverOptions(rtol=1e-13, maxit=200000))
+        errs.append(s.l2_error("mms_exact", 0.0, 2 * p + 2))
+        s.close()
+        row = ref[(ref[:, 0] == p) & (ref[:, 1] == j)][0]
+        assert int(row[3]) == m.num_t
+        assert abs(errs[-1] - row[4]) <= 1e-8 * row[4], (j, errs[-1], row[4])
+        if j > 0:
+            alpha = math.log(errs[-2] / errs[-1]) / math.log(2.0)
+            assert abs(alpha - row[5]) <= 1e-6, (j, alpha, row[5])
+
+
 @pytest.mark.parametrize("p", [0, 1, 2, 3, 4])
 def test_convergence_order_on_device(p, ld, golden):
-    ref = golden("convergence")["rows"]  # (p, j, h, K, error, alpha), reference run_convergence
+    """Order p+1 on device-generated FK(3 * 2^j), j = 0..4, multigrid-preconditioned:
+    FK(3 * 2^j) holds the same triangles as the refined ladder (other vertex
+    order, so quadrature points differ and errors agree to ~1e-3 only)."""
+    ref = golden("convergence")["rows"]
     spec = mms_spec(ld)
     errs = []
     for j in range(5):
@@ -98,8 +135,7 @@ def test_convergence_order_on_device(p, ld, golden):
         s.close()
         row = ref[(ref[:, 0] == p) & (ref[:, 1] == j)]
         if len(row):
-            assert int(row[0][3]) == 2 * dim * dim
-            assert abs(errs[-1] - row[0][4]) <= 1e-8 * row[0][4], (j, errs[-1], row[0][4])
+            assert abs(errs[-1] - row[0][4]) <= 1e-2 * row[0][4], (j, errs[-1], row[0][4])
     alphas = [math.log(a / b) / math.log(2.0) for a, b in zip(errs, errs[1:])]
     target = 0.0 if p == 0 else p + 1.0
     assert abs(alphas[-1] - target) <= ORDER_TOL[p], (p, alphas)
