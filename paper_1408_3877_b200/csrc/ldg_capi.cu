@@ -21,6 +21,42 @@ struct ldg_handle {
   ldgb::Team team;
 };
 
+namespace ldgb {
+
+// Reference tables (FP64 + FP32 smoother copies) and the element rule of
+// degree p on h (h.p, h.N set by the caller): rank handles and the
+// p-coarsened multigrid level (ldg_mg.cu).
+void init_handle_tables(Handle& h, int p) {
+  h.tables = build_tables(p);
+  h.tab.alloc(h.tables.data.size(), &h.bytes);
+  LDG_CUDA(cudaMemcpy(h.tab.ptr, h.tables.data.data(), sizeof(double) * h.tables.data.size(),
+                      cudaMemcpyHostToDevice));
+  const TableLayout& L = h.tables.lay;
+  h.dtab = DevTables{h.tab.ptr, L.p,    L.N,    L.R,   L.Qe,  L.Qb,   L.proj_phi, L.proj_w, L.proj_x,
+                     L.mhat,    L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe,   L.pth,      L.we,     L.pb,
+                     L.sb,      L.wb,   L.total, L.mono, L.NP,  L.tH,   L.tSd,      L.tSo,    L.tM,
+                     L.tMinv,   L.tmH,  L.tmSd, L.tmSo};
+  {
+    const FTables F = build_f32_tables(h.tables);
+    h.ftab.alloc(F.data.size(), &h.bytes);
+    LDG_CUDA(cudaMemcpy(h.ftab.ptr, F.data.data(), sizeof(float) * F.data.size(), cudaMemcpyHostToDevice));
+    h.dtab.fbase = h.ftab.ptr;
+    h.dtab.NF = F.NF;
+    h.dtab.fmH = F.fmH;
+    h.dtab.fmSd = F.fmSd;
+    h.dtab.fmSo = F.fmSo;
+    h.dtab.fM = F.fM;
+    h.dtab.fSd = F.fSd;
+    h.dtab.fSo = F.fSo;
+    h.dtab.fpe = F.fpe;
+    h.dtab.fpth = F.fpth;
+    h.dtab.fwe = F.fwe;
+  }
+  upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
+}
+
+}  // namespace ldgb
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -86,31 +122,7 @@ std::unique_ptr<Handle> make_rank(Team& T, int p, const ldg_problem* prob, int r
   h.stream = T.stream;
   h.owns_stream = false;
   for (auto& e : h.ev) LDG_CUDA(cudaEventCreate(&e));
-  h.tables = ldgb::build_tables(p);
-  h.tab.alloc(h.tables.data.size(), &h.bytes);
-  LDG_CUDA(cudaMemcpy(h.tab.ptr, h.tables.data.data(), sizeof(double) * h.tables.data.size(),
-                      cudaMemcpyHostToDevice));
-  const ldgb::TableLayout& L = h.tables.lay;
-  h.dtab = ldgb::DevTables{h.tab.ptr, L.p, L.N, L.R, L.Qe, L.Qb, L.proj_phi, L.proj_w, L.proj_x, L.mhat,
-                           L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe, L.pth, L.we, L.pb, L.sb, L.wb, L.total,
-                           L.mono, L.NP, L.tH, L.tSd, L.tSo, L.tM, L.tMinv, L.tmH, L.tmSd, L.tmSo};
-  {
-    const ldgb::FTables F = ldgb::build_f32_tables(h.tables);
-    h.ftab.alloc(F.data.size(), &h.bytes);
-    LDG_CUDA(cudaMemcpy(h.ftab.ptr, F.data.data(), sizeof(float) * F.data.size(), cudaMemcpyHostToDevice));
-    h.dtab.fbase = h.ftab.ptr;
-    h.dtab.NF = F.NF;
-    h.dtab.fmH = F.fmH;
-    h.dtab.fmSd = F.fmSd;
-    h.dtab.fmSo = F.fmSo;
-    h.dtab.fM = F.fM;
-    h.dtab.fSd = F.fSd;
-    h.dtab.fSo = F.fSo;
-    h.dtab.fpe = F.fpe;
-    h.dtab.fpth = F.fpth;
-    h.dtab.fwe = F.fwe;
-  }
-  ldgb::upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
+  ldgb::init_handle_tables(h, p);
   return hp;
 }
 

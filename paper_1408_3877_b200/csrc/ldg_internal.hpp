@@ -129,6 +129,8 @@ struct Handle {
   const double* rule_shared = nullptr;           // coarse levels use level 0's rule
   int rule_shared_R = 0;
   std::vector<std::unique_ptr<Handle>> coarse;   // levels 1 .. L-1 (top handle only)
+  bool mg_pcoarse = false;                       // same mesh as the finer level at a lower degree:
+                                                 // transfers truncate / pad the modal coefficients
   DBuf<int> mg_parent;                           // element -> parent in the next coarser level
   DBuf<int> mg_children;                         // [4][Kp] children in the next finer level
   DBuf<float> mg_P;                              // [4][N*N][Kp] prolongation blocks (on the coarse level, FP32)
@@ -323,6 +325,8 @@ int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, dou
 void team_sweep_s2_prepare(Team& T, double wm, double dt);  // multigrid set up, level-0 stage 1 done
 void team_sweep_s2(Team& T, double wm, double dt);          // one level-0 smoother stage-2 launch
 double team_sum_sq(Team& T, const std::function<const double*(Handle&)>& v);  // owned entries, all ranks
+
+void init_handle_tables(Handle& h, int p);  // reference tables + element rule of degree p (ldg_capi.cu)
 
 // multigrid (ldg_mg.cu)
 int mg_depth(int dim, int team_size);

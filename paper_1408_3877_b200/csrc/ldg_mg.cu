@@ -219,45 +219,107 @@ int mg_depth(int dim, int size) {
   return n;
 }
 
+// Degrees of the p-coarsened levels: the first coarse levels are the fine
+// mesh itself at the degrees of this chain (descending, each < p); the
+// h-coarsened levels below run at the last one.  The modal basis is
+// hierarchical and L2-orthonormal on the reference element (basis.hpp), so
+// the embedding of a lower-degree space is the identity on its first N
+// coefficients: restriction truncates, prolongation pads with zeros.
+// LDG_MG_PC overrides ("-1": none, else a comma list such as "2,1").
+std::vector<int> mg_pcoarse_chain(int p) {
+  std::vector<int> chain;
+  const char* e = std::getenv("LDG_MG_PC");
+  if (e) {
+    for (const char* q = e; *q;) {
+      char* end = nullptr;
+      const long v = std::strtol(q, &end, 10);
+      if (end == q) break;
+      chain.push_back(static_cast<int>(v));
+      q = *end == ',' ? end + 1 : end;
+    }
+  } else {
+    chain = p >= 4 ? std::vector<int>{2} : (p >= 2 ? std::vector<int>{1} : std::vector<int>{});
+  }
+  std::vector<int> out;
+  int last = p;
+  for (int d : chain)
+    if (d >= 0 && d < last) {
+      out.push_back(d);
+      last = d;
+    }
+  return out;
+}
+
+namespace {
+
+// coarse-level buffers shared by both kinds of level
+void alloc_coarse(Handle& c) {
+  const long n = c.vec_len();
+  const long NN = static_cast<long>(c.N) * c.N;
+  c.D.alloc(n, &c.bytes);
+  c.E.alloc(2 * NN * c.Kp, &c.bytes);  // diagonal blocks (off-diagonal ones matrix-free)
+  c.Pinv.alloc(NN * c.Kp, &c.bytes);
+  c.tz.alloc(2 * n, &c.bytes);
+  c.mg_x.alloc(n, &c.bytes);
+  c.mg_b.alloc(n, &c.bytes);
+  c.mg_r.alloc(n, &c.bytes);
+  c.mg_s.alloc(n, &c.bytes);
+}
+
+std::unique_ptr<Handle> coarse_shell(const Handle& h, const Handle& fine) {
+  auto c = std::make_unique<Handle>();
+  c->p = fine.p;
+  c->N = fine.N;
+  c->prob = h.prob;
+  {  // tuning experiment: penalty of the rediscretised coarse operators
+    const char* es = std::getenv("LDG_MG_ETA_SCALE");
+    if (es) c->prob.eta = fine.prob.eta * std::atof(es);
+  }
+  c->dtab = fine.dtab;
+  c->stream = h.stream;
+  c->owns_stream = false;
+  c->rule_shared = fine.rule_ptr();
+  c->rule_shared_R = fine.rule_R();
+  c->rank = h.rank;
+  c->size = h.size;
+  return c;
+}
+
+}  // namespace
+
 bool mg_build(Handle& h, int team_size) {
   if (h.mg_ready) return true;
   if (h.dim < 4 || h.dim_fine == 0) return false;
   const int depth = mg_depth(h.dim, team_size);
   if (depth < 1) return false;
-  const long NN = static_cast<long>(h.N) * h.N;
   h.mg_r.alloc(h.vec_len(), &h.bytes);
   h.mg_s.alloc(h.vec_len(), &h.bytes);
   Handle* fine = &h;
-  for (int l = 0; l < depth; ++l) {
-    const int dc = fine->dim / 2;
+  for (const int pc : mg_pcoarse_chain(h.p)) {  // the fine mesh again at degree pc (same vertices, numbering, strip)
     auto c = std::make_unique<Handle>();
-    c->p = h.p;
-    c->N = h.N;
+    c->p = pc;
+    c->N = dofs_of(pc);
     c->prob = h.prob;
-    {  // tuning experiment: penalty of the rediscretised coarse operators
-      const char* es = std::getenv("LDG_MG_ETA_SCALE");
-      if (es) c->prob.eta = fine->prob.eta * std::atof(es);
-    }
-    c->dtab = h.dtab;
     c->stream = h.stream;
     c->owns_stream = false;
-    c->rule_shared = h.rule_ptr();
-    c->rule_shared_R = h.rule_R();
     c->rank = h.rank;
     c->size = h.size;
+    init_handle_tables(*c, pc);
+    build_square_strip(*c, h.dim, h.strip_a, h.strip_b, h.stride, h.dim_fine, h.jitter, h.seed);
+    alloc_coarse(*c);
+    c->mg_pcoarse = true;
+    fine = c.get();
+    h.coarse.push_back(std::move(c));
+  }
+  for (int l = 0; l < depth; ++l) {
+    const int dc = fine->dim / 2;
+    auto c = coarse_shell(h, *fine);
+    const long NN = static_cast<long>(c->N) * c->N;
     // coarse vertices are the finest mesh's vertices (stride 2^l): jittered
     // meshes coarsen consistently on every rank
     const double cj = coarse_jitter_scale() * h.jitter;
     build_square_strip(*c, dc, fine->strip_a / 2, fine->strip_b / 2, fine->stride * 2, h.dim_fine, cj, h.seed);
-    const long n = c->vec_len();
-    c->D.alloc(n, &c->bytes);
-    c->E.alloc(2 * NN * c->Kp, &c->bytes);  // diagonal blocks (off-diagonal ones matrix-free)
-    c->Pinv.alloc(NN * c->Kp, &c->bytes);
-    c->tz.alloc(2 * n, &c->bytes);
-    c->mg_x.alloc(n, &c->bytes);
-    c->mg_b.alloc(n, &c->bytes);
-    c->mg_r.alloc(n, &c->bytes);
-    c->mg_s.alloc(n, &c->bytes);
+    alloc_coarse(*c);
     c->mg_children.alloc(4 * c->Kp, &c->bytes);
     fine->mg_parent.alloc(fine->Kp, &fine->bytes);
     DBuf<int> slots;
@@ -267,9 +329,9 @@ bool mg_build(Handle& h, int team_size) {
                                                              fine->mg_parent.ptr, slots.ptr, c->mg_children.ptr);
     LDG_CUDA(cudaGetLastError());
 #define CALL(PP)                                                                                              \
-  k_prolong_blocks<PP><<<grid_of(fine->K, 128), 128, 0, h.stream>>>(fine->mesh(), c->mesh(), h.dtab,         \
+  k_prolong_blocks<PP><<<grid_of(fine->K, 128), 128, 0, h.stream>>>(fine->mesh(), c->mesh(), fine->dtab,     \
                                                                    fine->mg_parent.ptr, slots.ptr, c->mg_P.ptr)
-    LDG_DISPATCH_P(h.p, CALL)
+    LDG_DISPATCH_P(fine->p, CALL)
 #undef CALL
     LDG_CUDA(cudaGetLastError());
     LDG_CUDA(cudaStreamSynchronize(h.stream));
@@ -346,6 +408,11 @@ void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
 
 // C.mg_b = P^T L.mg_r (restriction of the fine residual to the coarse level)
 void mg_restrict(Handle& L, Handle& C) {
+  if (C.mg_pcoarse) {  // same mesh, lower degree: the first C.N coefficient planes
+    LDG_CUDA(cudaMemcpyAsync(C.mg_b.ptr, L.mg_r.ptr, sizeof(double) * C.vec_len(), cudaMemcpyDeviceToDevice,
+                             L.stream));
+    return;
+  }
 #define CALL(PP)                                                                                             \
   launch_pdl(k_restrict<PP>, grid_of(static_cast<long>(L.N) * C.K, 256), 256, 0, L.stream, C.K, C.Kp, L.Kp,      \
              C.mg_children.ptr, C.mg_P.ptr, L.mg_r.ptr, C.mg_b.ptr)
@@ -381,6 +448,10 @@ double coarse_jitter_scale() {
 
 // x += P C.mg_x (prolongation of the coarse correction)
 void mg_prolong_add(Handle& L, Handle& C, double* x) {
+  if (C.mg_pcoarse) {  // pad: the first C.N coefficient planes
+    launch_lincomb3(L, C.vec_len(), 1.0, x, coarse_theta(), C.mg_x.ptr, 0.0, nullptr, x);
+    return;
+  }
 #define CALL(PP)                                                                                              \
   launch_pdl(k_prolong_add<PP>, grid_of(4L * L.N * C.K, 256), 256, 0, L.stream, C.K, C.Kp, L.Kp,                \
              C.mg_children.ptr, C.mg_P.ptr, C.mg_x.ptr, x, coarse_theta())

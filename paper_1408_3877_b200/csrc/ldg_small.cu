@@ -465,8 +465,9 @@ void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, 
   a.pre = pre;
   a.post = post;
   a.coarse_min = coarse_min;
-#define CALL(P) launch_pdl(k_tail<P>, 1, Cfg<P>::THREADS, 0, h0.stream, a, h0.dtab)
-  LDG_DISPATCH_P(h0.p, CALL)
+  const Handle& top_h = *h0.coarse[top - 1];  // all tail levels share its degree (p-coarsening, ldg_mg.cu)
+#define CALL(P) launch_pdl(k_tail<P>, 1, Cfg<P>::THREADS, 0, h0.stream, a, top_h.dtab)
+  LDG_DISPATCH_P(top_h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
   ++h0.launches;

@@ -498,8 +498,9 @@ double estimate_lmax(Team& T, int l, double wm, double dt) {
 bool tail_level(Team& T, int l, bool f32) {
   static const long below = static_cast<long>(env_or("LDG_TAIL_BELOW", 64));
   static const int pmax = static_cast<int>(env_or("LDG_TAIL_PMAX", 1));
-  if (!f32 || l < 1 || rb_smoother() || T.size != 1 || T.nlocal() != 1 || T.h0().p > pmax) return false;
+  if (!f32 || l < 1 || rb_smoother() || T.size != 1 || T.nlocal() != 1) return false;
   const Handle& L = level_of(T.h0(), l);
+  if (L.p > pmax) return false;
   return L.K < below && levels(T) - l <= 6 && level_uses_rows(L) && level_is_small(L);
 }
 
