@@ -108,6 +108,8 @@ void init_team(Team& T) {
   const size_t nred = static_cast<size_t>(ldgb::kMaxRed) * (ldgb::kMaxLocalRanks + 1);
   LDG_CUDA(cudaMallocHost(&T.red_host, nred * sizeof(double)));
   T.red_all.alloc(nred, nullptr);
+  LDG_CUDA(cudaMallocHost(&T.gs_host, sizeof(double) * ldgb::kMaxRed * (2 * ldgb::kMaxRed + 1)));
+  for (auto& e : T.gs_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 // One rank's device-side state: tables, rule, stream (the team's).
@@ -382,6 +384,9 @@ void ldg_destroy(ldg_handle* H) {
   }
   if (T.nccl && T.owns_nccl) ncclCommDestroy(static_cast<ncclComm_t>(T.nccl));
   if (T.red_host) cudaFreeHost(T.red_host);
+  if (T.gs_host) cudaFreeHost(T.gs_host);
+  for (auto& e : T.gs_ev)
+    if (e) cudaEventDestroy(e);
   cudaStream_t s = T.stream;
   delete H;  // DBuf destructors free device memory
   if (s) cudaStreamDestroy(s);

@@ -111,6 +111,7 @@ struct Handle {
   DBuf<double> Pinv;     // N*N * Kp : block-Jacobi inverse
   DBuf<double> full_r, full_y;  // 3 * N * Kp : reference residual contract
   DBuf<double> red;      // reduction scratch
+  DBuf<double> gs;       // FGMRES Gram-Schmidt coefficients on the device (h1 | h2 | hn)
   double* red_host = nullptr;  // pinned
   DBuf<double> flush;    // L2 flush buffer (measurement only)
   DBuf<double> host_stage;  // k-major staging of host states (3KN)
@@ -197,6 +198,8 @@ struct Team {
   DBuf<double> send_l, send_r, recv_l, recv_r;  // NCCL halo staging
   DBuf<double> red_all;                         // allreduce scratch
   double* red_host = nullptr;                   // pinned
+  double* gs_host = nullptr;                    // pinned: FGMRES Gram-Schmidt slots (kMaxRed x (2 kMaxRed + 1))
+  cudaEvent_t gs_ev[2] = {};                    // completion of FGMRES iterations j (ping-pong)
   std::string err;
   Handle& h0() { return *ranks[0]; }
   const Handle& h0() const { return *ranks[0]; }
@@ -311,6 +314,9 @@ void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, con
                      const double* z, double* out);
 void launch_mdots_async(Handle& h, int nv, const double* const* v, const double* w);
 void launch_maxpy(Handle& h, int nv, const double* const* v, const double* c, double alpha, double* w);
+void launch_mdots_to(Handle& h, int nv, const double* const* v, const double* w, double* out);  // results on device
+void launch_maxpy_dev(Handle& h, int nv, const double* const* v, const double* c, bool final, double* w, double* w2,
+                      double* hn_out);  // device coefficients (Gram-Schmidt without a host round trip)
 
 // per-rank assembly step (ldg_vec.cu)
 void assemble_step(Handle& h, double t);

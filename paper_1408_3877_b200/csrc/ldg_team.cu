@@ -799,6 +799,148 @@ struct IterTrace {
   }
 };
 
+// in-place sum over the processes of n device values (one rank per process)
+void allreduce_dev(Team& T, double* v, int n) {
+  if (T.nccl && T.size > T.nlocal())
+    LDG_NCCL(ncclAllReduce(v, v, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(T.nccl), T.stream));
+}
+
+// FGMRES(m) for one rank per process (the production shape): the
+// Gram-Schmidt coefficients never leave the device inside an iteration
+// (CGS2: h1 = V^T w with (w, w), w -= V h1, h2 = V^T w with (w, w),
+// w = (w - V h2) / |.| by Pythagoras, the next V-cycle input written in the
+// same pass), and the host runs one iteration behind: iteration j + 1 is
+// queued before the host waits for iteration j's coefficient slot, unless
+// the residual trend says j may already converge.  The GPU queue therefore
+// stays non-empty across the host's Givens update and launch latency.
+void fgmres_dev(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_opts& o, double tol, int m,
+                int* it_out, int* applies_out, double* rnorm_out) {
+  Handle& h0 = T.h0();
+  constexpr int kSlot = 2 * kMaxRed + 1;  // h1 (j + 2) | h2 (j + 2) | hn
+  if (h0.gs.n < static_cast<size_t>(m) * kSlot) h0.gs.alloc(static_cast<size_t>(m) * kSlot, &h0.bytes);
+  auto copy = [&](Vec dst, Vec src) {
+    LDG_CUDA(cudaMemcpyAsync(vp(h0, dst), vp(h0, src), sizeof(double) * h0.vec_len(), cudaMemcpyDeviceToDevice,
+                             T.stream));
+  };
+  auto scale_into = [&](double a, Vec src, Vec dst) { lincomb(T, a, src, 0.0, kNone, 0.0, kNone, dst); };
+  int applies = 0;
+  auto launch_it = [&](int j) {  // the GPU work of iteration j; with pc == 2 kP holds V_j on entry
+    if (pc == 2) {
+      precond(T, pc, f32, wm, dt, kP, kPh);
+      copy(gmZ(j), kPh);
+    } else {
+      precond(T, pc, f32, wm, dt, gmV(j), gmZ(j));
+    }
+    schur_apply(T, wm, dt, gmZ(j), gmV(j + 1));
+    ++applies;
+    const double* v[kMaxRed];
+    for (int d = 0; d <= j + 1; ++d) v[d] = vp(h0, gmV(d));
+    double* slot = h0.gs.ptr + static_cast<long>(j) * kSlot;
+    for (int pass = 0; pass < 2; ++pass) {
+      double* c = slot + pass * kMaxRed;
+      launch_mdots_to(h0, j + 2, v, vp(h0, gmV(j + 1)), c);
+      allreduce_dev(T, c, j + 2);
+      launch_maxpy_dev(h0, j + 1, v, c, pass == 1, vp(h0, gmV(j + 1)), pass == 1 && pc == 2 ? vp(h0, kP) : nullptr,
+                       slot + 2 * kMaxRed);
+    }
+    LDG_CUDA(cudaMemcpyAsync(T.gs_host + static_cast<long>(j) * kSlot, slot, sizeof(double) * kSlot,
+                             cudaMemcpyDeviceToHost, T.stream));
+    LDG_CUDA(cudaEventRecord(T.gs_ev[j & 1], T.stream));
+  };
+
+  int it = 0;
+  double rnorm = 0.0;
+  std::vector<double> H(static_cast<size_t>(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+  auto Hij = [&](int i, int j) -> double& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
+  while (true) {
+    schur_apply(T, wm, dt, kC, gmV(0));  // r = b - A x into V_0
+    ++applies;
+    lincomb(T, 1.0, kB, -1.0, gmV(0), 0.0, kNone, gmV(0));
+    rnorm = norm(T, gmV(0));
+    if (!(rnorm > tol) || !std::isfinite(rnorm) || it >= o.maxit) break;
+    scale_into(1.0 / rnorm, gmV(0), gmV(0));
+    if (pc == 2) copy(kP, gmV(0));
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = rnorm;
+    launch_it(0);
+    int launched = 1;  // iterations of this cycle queued on the stream
+    double r1 = rnorm, r2 = 0.0;  // last two residual estimates (trend)
+    int j = 0;
+    bool done = false;
+    for (; j < m; ++j) {
+      const bool more = j + 1 < m && it + 1 < o.maxit;
+      if (more && launched == j + 1) {  // queue j + 1 now unless j is predicted to converge
+        const double rate = r2 > 0.0 ? std::min(r1 / r2, 1.0) : 0.5;
+        if (r1 * rate > 4.0 * tol) {
+          launch_it(j + 1);
+          launched = j + 2;
+        }
+      }
+      LDG_CUDA(cudaEventSynchronize(T.gs_ev[j & 1]));
+      ++it;
+      const double* slot = T.gs_host + static_cast<long>(j) * kSlot;
+      const double *h1 = slot, *h2 = slot + kMaxRed;
+      for (int i = 0; i <= j; ++i) Hij(i, j) = h1[i] + h2[i];
+      double hn = slot[2 * kMaxRed];
+      if (hn > 0.0 && !(hn > 1e-6 * std::sqrt(std::max(h1[j + 1], 0.0)))) {
+        // cancellation guard: normalise V_{j+1} explicitly; a queued
+        // iteration j + 1 started from the unnormalised vector and is redone
+        const double s2 = norm(T, gmV(j + 1));
+        if (s2 > 0.0) {
+          hn *= s2;
+          scale_into(1.0 / s2, gmV(j + 1), gmV(j + 1));
+          if (pc == 2) copy(kP, gmV(j + 1));
+          if (launched == j + 2) launch_it(j + 1);
+        }
+      }
+      Hij(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {  // Givens rotations
+        const double a = Hij(i, j), b = Hij(i + 1, j);
+        Hij(i, j) = cs[i] * a + sn[i] * b;
+        Hij(i + 1, j) = -sn[i] * a + cs[i] * b;
+      }
+      const double a = Hij(j, j), b = Hij(j + 1, j);
+      const double r = std::hypot(a, b);
+      cs[j] = r > 0.0 ? a / r : 1.0;
+      sn[j] = r > 0.0 ? b / r : 0.0;
+      Hij(j, j) = r;
+      Hij(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rnorm = std::fabs(g[j + 1]);
+      r2 = r1;
+      r1 = rnorm;
+      if (rnorm <= tol || hn == 0.0 || !std::isfinite(rnorm)) {
+        ++j;
+        done = true;
+        break;
+      }
+      if (it >= o.maxit) {
+        ++j;
+        break;
+      }
+      if (j + 1 < m && launched == j + 1) {
+        launch_it(j + 1);
+        launched = j + 2;
+      }
+    }
+    // x += Z y, H(0:j, 0:j) y = g(0:j) (a queued iteration past j is unused)
+    for (int i = j - 1; i >= 0; --i) {
+      double v = g[i];
+      for (int k = i + 1; k < j; ++k) v -= Hij(i, k) * y[k];
+      y[i] = Hij(i, i) != 0.0 ? v / Hij(i, i) : 0.0;
+    }
+    const double* z[kMaxRed];
+    for (int d = 0; d < j; ++d) z[d] = vp(h0, gmZ(d));
+    launch_maxpy(h0, j, z, y.data(), 1.0, vp(h0, kC));
+    if (done && rnorm <= tol) break;
+    if (it >= o.maxit || !std::isfinite(rnorm)) break;
+  }
+  *it_out = it;
+  *applies_out = applies;
+  *rnorm_out = rnorm;
+}
+
 void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_opts& o, double tol, int* it_out,
             int* applies_out, double* rnorm_out) {
   Handle& h0 = T.h0();
@@ -821,6 +963,11 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
       rp->gm_m = m;
     }
   }
+  // one rank per process: device-resident Gram-Schmidt, host one iteration
+  // behind (LDG_GS_HOST=1 selects the host-side variant below, which
+  // virtual-rank teams use)
+  static const bool gs_host = env_or("LDG_GS_HOST", 0) != 0;
+  if (T.nlocal() == 1 && !gs_host) return fgmres_dev(T, pc, f32, wm, dt, o, tol, m, it_out, applies_out, rnorm_out);
   auto copy = [&](Vec dst, Vec src) {  // (ranks differ in ghost counts, hence in vector length)
     each(T, 0, [&](Handle& h) {
       LDG_CUDA(cudaMemcpyAsync(vp(h, dst), vp(h, src), sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice,

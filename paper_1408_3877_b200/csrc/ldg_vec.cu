@@ -5,6 +5,7 @@
 // k-major host vectors, and the per-rank assembly step.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -154,6 +155,40 @@ __global__ void k_dots_final(int nd, const double* __restrict__ part, double* __
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if (lane == 0) out[d] = v;
+}
+
+// Gram-Schmidt update with device-resident coefficients (no host round
+// trip between the projection and the update):
+//   FINAL 0: w -= sum_d c_d v_d
+//   FINAL 1: w = (w - sum_d c_d v_d) / hn, hn = sqrt(c_nv - sum_d c_d^2) (the
+//            norm of the updated w by Pythagoras: c_nv holds (w, w)); w2 (if
+//            set) receives a copy; block 0 stores hn at *hn_out
+template <int FINAL>
+__global__ void __launch_bounds__(256) k_maxpy_dev(long n, int nv, MDotArgs a, const double* __restrict__ c,
+                                                   double* __restrict__ w, double* __restrict__ w2,
+                                                   double* __restrict__ hn_out) {
+  __shared__ double s_c[kMaxRed];
+  __shared__ double s_inv;
+  for (int d = threadIdx.x; d < nv; d += blockDim.x) s_c[d] = -c[d];
+  if (FINAL && threadIdx.x == 0) {
+    double ss = c[nv];
+    for (int d = 0; d < nv; ++d) ss = fma(-c[d], c[d], ss);
+    const double hn = ss > 0.0 ? sqrt(ss) : 0.0;
+    s_inv = hn > 0.0 ? 1.0 / hn : 0.0;
+    if (blockIdx.x == 0) *hn_out = hn;
+  }
+  __syncthreads();
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    double acc = w[i];
+#pragma unroll 4
+    for (int d = 0; d < nv; ++d) acc = fma(s_c[d], a.v[d][i], acc);
+    if (FINAL) {
+      acc *= s_inv;
+      if (w2) w2[i] = acc;
+    }
+    w[i] = acc;
+  }
 }
 
 inline unsigned final_blocks(int nd) { return static_cast<unsigned>((nd + 7) / 8); }  // 8 warps per block
@@ -353,6 +388,36 @@ void launch_maxpy(Handle& h, int nv, const double* const* v, const double* c, do
     a.c[d] = c[d];
   }
   k_maxpy<<<kRedBlocks * 4, 256, 0, h.stream>>>(h.vec_len(), nv, a, alpha, w);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+// (v_d, w), d < nv, owned entries; the results land at out (device)
+void launch_mdots_to(Handle& h, int nv, const double* const* v, const double* w, double* out) {
+  if (nv < 1 || nv > kMaxRed) throw Error(LDG_EINVAL, "multi-dot count out of range");
+  MDotArgs a{};
+  for (int d = 0; d < nv; ++d) a.v[d] = v[d];
+  const dim3 grid(kRedBlocks, (nv + kMdotChunk - 1) / kMdotChunk);
+  k_mdot_owned<<<grid, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nv, a, w, h.red.ptr);
+  k_dots_final<<<final_blocks(nv), 256, 0, h.stream>>>(nv, h.red.ptr, out);
+  LDG_CUDA(cudaGetLastError());
+  h.launches += 2;
+}
+
+// w -= sum c_d v_d (final = false) or w = (w - sum c_d v_d) / hn with the
+// Pythagorean norm from c[nv] = (w, w) (final = true; copy into w2, hn at
+// *hn_out); c on the device
+void launch_maxpy_dev(Handle& h, int nv, const double* const* v, const double* c, bool final, double* w, double* w2,
+                      double* hn_out) {
+  if (nv < 1 || nv > kMaxRed - 1) throw Error(LDG_EINVAL, "multi-axpy count out of range");
+  MDotArgs a{};
+  for (int d = 0; d < nv; ++d) a.v[d] = v[d];
+  const long n = h.vec_len();
+  const unsigned grid = static_cast<unsigned>(std::min<long>(grid_of(n, 256), 4L * kRedBlocks));
+  if (final)
+    k_maxpy_dev<1><<<grid, 256, 0, h.stream>>>(n, nv, a, c, w, w2, hn_out);
+  else
+    k_maxpy_dev<0><<<grid, 256, 0, h.stream>>>(n, nv, a, c, w, nullptr, nullptr);
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
