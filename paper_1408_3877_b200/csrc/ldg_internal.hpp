@@ -146,7 +146,7 @@ struct Handle {
   DBuf<double> mg_zero;                          // zeros (Chebyshev eigenvalue estimate)
   double cheb_lmax = 0.0;                        // estimated largest eigenvalue of P^-1 S_c (0: not yet)
   DBuf<double> gm_V, gm_Z;                       // FGMRES basis and preconditioned basis ((m+1) and m vectors)
-  int gm_m = 0;
+  int gm_m = 0, gm_req = 0;  // basis length in use, restart length it was sized for
   bool mg_f32 = true;                            // smoother on FP32 copies (precond 2) or FP64 (3)
   bool mg_ready = false;
   struct VGraph {                                // a captured V-cycle (CUDA graph)

@@ -30,18 +30,32 @@
 #include "ldg_pack.cuh"
 #include "ldg_offdiag.cuh"
 
-// min resident CTAs per SM of the thread-per-element kernels: at p = 4 the
-// register-heavy kernels are latency-bound at 1 CTA; 4 CTAs (<= 128 registers)
-// measured 7-15% faster there and slower at p <= 3 (-DLDG_MINB_SMOOTH=n overrides)
-#ifdef LDG_MINB_SMOOTH
-#define LDG_MINB_SMOOTH_P(P) LDG_MINB_SMOOTH
-#else
-#define LDG_MINB_SMOOTH_P(P) ((P) == 4 ? 4 : 1)
+// min resident CTAs per SM of the thread-per-element kernels, per degree
+// p = 0..4 (stage 1 | stage 2).  The level-0 grids are 1024 CTAs of 128
+// (256^2 FK): 7-8 CTAs/SM (<= 73 / 64 registers, a few spilled bytes) run
+// them in one wave: V-cycle -13% at p = 2 and -14% at p = 3 (stage 2 at 7,
+// stage 1 at 8: 0.515 / 0.764 ms against 0.600 / 0.883 ms with 1 CTA); at
+// p = 4 the spills grow and 4 CTAs (<= 128 registers) stay best (7-15% over
+// 1 CTA; 8 for stage 1 measured +7% V-cycle); 8 at p <= 1 measured slower.
+// -DLDG_MINB_S1=abcde / -DLDG_MINB_S2=abcde (one digit per p = 0..4)
+// override (tuning builds).
+#ifndef LDG_MINB_S1
+#define LDG_MINB_S1 11884
+#endif
+#ifndef LDG_MINB_S2
+#define LDG_MINB_S2 11774
 #endif
 
 namespace ldgb {
 
 namespace {
+
+constexpr int minb_digit(int code, int p) { return p == 4 ? code % 10 : minb_digit(code / 10, p + 1); }
+constexpr int kMinbS1[5] = {minb_digit(LDG_MINB_S1, 0), minb_digit(LDG_MINB_S1, 1), minb_digit(LDG_MINB_S1, 2),
+                            minb_digit(LDG_MINB_S1, 3), minb_digit(LDG_MINB_S1, 4)};
+constexpr int kMinbS2[5] = {minb_digit(LDG_MINB_S2, 0), minb_digit(LDG_MINB_S2, 1), minb_digit(LDG_MINB_S2, 2),
+                            minb_digit(LDG_MINB_S2, 3), minb_digit(LDG_MINB_S2, 4)};
+static_assert(kMinbS1[0] == LDG_MINB_S1 / 10000 && kMinbS2[4] == LDG_MINB_S2 % 10, "min-blocks digits");
 
 template <int P>
 using Cfg = SmCfg<P>;
@@ -101,7 +115,7 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
 
 // tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
 template <int P, typename TT>
-__global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
+__global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
                                              TT* __restrict__ tout) {
   constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
   extern __shared__ __align__(16) float smf[];
@@ -248,7 +262,7 @@ __device__ __forceinline__ void pinv_apply(const TQ* __restrict__ Pk, long Kp, F
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
 template <int P, int MODE, typename TQ, typename TP, typename TT>
-__global__ void __launch_bounds__(128, LDG_MINB_SMOOTH_P(P)) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
+__global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
                                              const double* x,
                                              const TT* __restrict__ tz, const double* __restrict__ b, double wm,

@@ -824,7 +824,23 @@ void fgmres_dev(Team& T, int pc, bool f32, double wm, double dt, const ldg_solve
   };
   auto scale_into = [&](double a, Vec src, Vec dst) { lincomb(T, a, src, 0.0, kNone, 0.0, kNone, dst); };
   int applies = 0;
+  // LDG_TRACE_ITER=1: per-iteration device spans (work vs gaps) on stderr
+  static const bool trace = env_or("LDG_TRACE_ITER", 0) != 0;
+  std::vector<cudaEvent_t> tev;
+  cudaEvent_t t_entry = nullptr;
+  if (trace) {
+    LDG_CUDA(cudaEventCreate(&t_entry));
+    LDG_CUDA(cudaEventRecord(t_entry, T.stream));
+  }
+  auto mark = [&] {
+    if (!trace) return;
+    cudaEvent_t e;
+    LDG_CUDA(cudaEventCreate(&e));
+    LDG_CUDA(cudaEventRecord(e, T.stream));
+    tev.push_back(e);
+  };
   auto launch_it = [&](int j) {  // the GPU work of iteration j; with pc == 2 kP holds V_j on entry
+    mark();
     if (pc == 2) {
       precond(T, pc, f32, wm, dt, kP, kPh);
       copy(gmZ(j), kPh);
@@ -846,6 +862,7 @@ void fgmres_dev(Team& T, int pc, bool f32, double wm, double dt, const ldg_solve
     LDG_CUDA(cudaMemcpyAsync(T.gs_host + static_cast<long>(j) * kSlot, slot, sizeof(double) * kSlot,
                              cudaMemcpyDeviceToHost, T.stream));
     LDG_CUDA(cudaEventRecord(T.gs_ev[j & 1], T.stream));
+    mark();
   };
 
   int it = 0;
@@ -936,6 +953,24 @@ void fgmres_dev(Team& T, int pc, bool f32, double wm, double dt, const ldg_solve
     if (done && rnorm <= tol) break;
     if (it >= o.maxit || !std::isfinite(rnorm)) break;
   }
+  if (trace && tev.size() >= 2) {
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+    float work = 0.f, gap = 0.f, a = 0.f, gmax = 0.f, pre = 0.f;
+    cudaEventElapsedTime(&pre, t_entry, tev[0]);
+    cudaEventDestroy(t_entry);
+    for (size_t i = 0; i + 1 < tev.size(); i += 2) {
+      cudaEventElapsedTime(&a, tev[i], tev[i + 1]);
+      work += a;
+      if (i + 2 < tev.size()) {
+        cudaEventElapsedTime(&a, tev[i + 1], tev[i + 2]);
+        gap += a;
+        gmax = std::max(gmax, a);
+      }
+    }
+    fprintf(stderr, "[ldg trace] %zu launches: before the first %.3f ms, work %.3f ms (%.3f/it), between %.3f ms (max %.3f)\n",
+            tev.size() / 2, pre, work, work / (tev.size() / 2), gap, gmax);
+    for (auto e : tev) cudaEventDestroy(e);
+  }
   *it_out = it;
   *applies_out = applies;
   *rnorm_out = rnorm;
@@ -947,7 +982,10 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
   IterTrace tr;
   int m = o.restart > 0 ? o.restart : 30;
   m = std::min(m, kMaxRed - 2);
-  {  // basis memory: (2m + 1) vectors per rank, within free device memory
+  const int m_req = m;
+  if (h0.gm_m > 0 && h0.gm_req == m_req) {
+    m = h0.gm_m;  // sized on an earlier solve (cudaMemGetInfo stalled the host for milliseconds per step)
+  } else {  // basis memory: (2m + 1) vectors per rank, within free device memory
     size_t free_b = 0, total_b = 0;
     LDG_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double vec_b = 8.0 * h0.vec_len() * T.nlocal();
@@ -961,6 +999,7 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
       rp->gm_V.alloc(static_cast<size_t>(m + 1) * rp->vec_len(), &rp->bytes);
       rp->gm_Z.alloc(static_cast<size_t>(m) * rp->vec_len(), &rp->bytes);
       rp->gm_m = m;
+      rp->gm_req = m_req;
     }
   }
   // one rank per process: device-resident Gram-Schmidt, host one iteration
