@@ -418,6 +418,10 @@ def run_ours(args):
         for s in systems:
             s.euler_steps(dt, 1, opts)
     barrier()
+    # the timed steps' start states: the e2e pass below replays the same K
+    # steps from them (same times, same iteration counts) through host buffers
+    starts = [s.get_state() for s in systems]
+    barrier()
     clocks.mark()
     launches0 = sum(s.info()["launches"] for s in systems)
     per_p = {p: dict(ms=0.0, ms_asm=0.0, ms_solve=0.0, iters=0, applies=0, residual=0.0) for p in ps}
@@ -442,11 +446,12 @@ def run_ours(args):
     # e2e through the host-buffer C ABI call (each rank copies its owned rows)
     e2e_ms = 0.0
     h2d = 0
-    for p, s in zip(ps, systems):
-        y, t = s.get_state()
+    for p, s, (y, t) in zip(ps, systems, starts):
         pin_in = torch.from_numpy(y).pin_memory()
         pin_out = torch.empty_like(pin_in).pin_memory()
         for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
             st = s.euler_steps_host(pin_in.data_ptr(), t, dt, 1, pin_out.data_ptr(), opts)
             e2e_ms += st["ms_total"]
             t += dt

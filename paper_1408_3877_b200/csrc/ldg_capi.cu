@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -385,6 +386,9 @@ void ldg_destroy(ldg_handle* H) {
   if (T.nccl && T.owns_nccl) ncclCommDestroy(static_cast<ncclComm_t>(T.nccl));
   if (T.red_host) cudaFreeHost(T.red_host);
   if (T.gs_host) cudaFreeHost(T.gs_host);
+  for (auto& e : T.in_ev)
+    if (e) cudaEventDestroy(e);
+  if (T.in_stream) cudaStreamDestroy(T.in_stream);
   for (auto& e : T.gs_ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t s = T.stream;
@@ -725,6 +729,26 @@ int ldg_get_state(ldg_handle* H, double* y, double* t) {
 
 namespace {
 
+// LDG_ZEROCOPY=1: the device address of a pinned, mapped host buffer
+// (cudaHostAlloc / torch pin_memory), read / written by the layout kernels
+// over PCIe instead of a copy-engine transfer; nullptr otherwise.  Off by
+// default: measured at 256^2, p = 4, 1.81 ms per step against 0.97 ms for
+// the side-stream upload hidden under the assembly + setup and a 57 GB/s
+// device->host copy.
+const double* mapped_host(const double* p) {
+  static const bool on = [] {
+    const char* e = std::getenv("LDG_ZEROCOPY");
+    return e && std::atoi(e) == 1;
+  }();
+  if (!on) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? static_cast<const double*>(a.devicePointer) : nullptr;
+}
+
 void run_steps(Team& T, double dt, int nsteps, const ldg_solver_opts& o, ldg_step_stats* st) {
   Handle& h0 = T.h0();
   for (int s = 0; s < nsteps; ++s) {
@@ -777,11 +801,27 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
     // ev[5]: run_steps/team_solve re-record ev[0..4] inside the region
     LDG_CUDA(cudaEventRecord(h0.ev[5], T.stream));
     if (T.nlocal() == 1 && T.size == 1) {
-      // one rank: the stacked host state is exactly the rank's owned rows
+      // one rank: the stacked host state is exactly the rank's owned rows;
+      // uploaded on a side stream that overlaps the step's assembly and
+      // preconditioner setup (team_solve waits for it before reading Y)
       const size_t cnt = 3L * h0.K * h0.N;
       if (!h0.host_stage.ptr) h0.host_stage.alloc(cnt, &h0.bytes);
-      LDG_CUDA(cudaMemcpyAsync(h0.host_stage.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice, T.stream));
-      ldgb::launch_kmajor_to_soa(h0, h0.host_stage.ptr, 3, h0.Y.ptr);
+      if (!T.in_stream) {
+        LDG_CUDA(cudaStreamCreateWithFlags(&T.in_stream, cudaStreamNonBlocking));
+        for (auto& e : T.in_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      LDG_CUDA(cudaEventRecord(T.in_ev[0], T.stream));
+      LDG_CUDA(cudaStreamWaitEvent(T.in_stream, T.in_ev[0], 0));
+      if (const double* yd = mapped_host(y_in)) {
+        // pinned + mapped host buffer: the layout kernel reads it over PCIe
+        ldgb::launch_kmajor_to_soa(h0, yd, 3, h0.Y.ptr, T.in_stream);
+      } else {
+        LDG_CUDA(cudaMemcpyAsync(h0.host_stage.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                                 T.in_stream));
+        ldgb::launch_kmajor_to_soa(h0, h0.host_stage.ptr, 3, h0.Y.ptr, T.in_stream);
+      }
+      LDG_CUDA(cudaEventRecord(T.in_ev[1], T.in_stream));
+      T.y_pending = true;
     } else {
       scatter_from_host(T, y_in, 3, [](Handle& h) { return h.Y.ptr; });
     }
@@ -789,8 +829,12 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
     run_steps(T, dt, nsteps, o, st);
     if (T.nlocal() == 1 && T.size == 1) {
       const size_t cnt = 3L * h0.K * h0.N;
-      ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
-      LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
+      if (double* yo = const_cast<double*>(mapped_host(y_out))) {
+        ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, yo);  // written over PCIe directly
+      } else {
+        ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
+        LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
+      }
     } else {
       gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.Y.ptr); }, 3, y_out);
     }

@@ -200,6 +200,9 @@ struct Team {
   double* red_host = nullptr;                   // pinned
   double* gs_host = nullptr;                    // pinned: FGMRES Gram-Schmidt slots (kMaxRed x (2 kMaxRed + 1))
   cudaEvent_t gs_ev[2] = {};                    // completion of FGMRES iterations j (ping-pong)
+  cudaStream_t in_stream = nullptr;             // host-buffer state upload, overlapping assembly + setup
+  cudaEvent_t in_ev[2] = {};                    // [0] call start, [1] state uploaded
+  bool y_pending = false;                       // team_solve waits for in_ev[1] before reading Y
   std::string err;
   Handle& h0() { return *ranks[0]; }
   const Handle& h0() const { return *ranks[0]; }
@@ -270,7 +273,7 @@ void launch_bjac_apply(Handle& h, const double* x, double* y);
 void launch_axpby(Handle& h, long n, double a, const double* x, double b, double* y);
 void launch_dots(Handle& h, long n, int ndots, const double* const* xs, const double* const* ys, double* out_host);
 void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev);
-void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa);
+void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa, cudaStream_t stream = nullptr);
 
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);

@@ -1147,6 +1147,14 @@ void team_assemble(Team& T, double t) {
 // Y holds the previous state on entry and the solution on exit.
 int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step_stats* st) {
   Handle& h0 = T.h0();
+  // preconditioner setup first: it needs the step's operators only, so a
+  // host-buffer state upload (ldg_euler_steps_host) overlaps it
+  bool f32 = false;
+  const int pc = prepare_precond(T, o.precond, wm, dt, &f32);
+  if (T.y_pending) {
+    LDG_CUDA(cudaStreamWaitEvent(T.stream, T.in_ev[1], 0));
+    T.y_pending = false;
+  }
   each(T, 0, [&](Handle& h) {
     const long n = h.vec_len();
     LDG_CUDA(cudaMemcpyAsync(h.Yold.ptr, h.Y.ptr, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, T.stream));
@@ -1163,9 +1171,6 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   });
   const double rhs_norm = std::sqrt(sq_norm3(T, kFullR));
   const double contract = o.contract_tol > 0.0 ? o.contract_tol : 1e-10;
-
-  bool f32 = false;
-  const int pc = prepare_precond(T, o.precond, wm, dt, &f32);
 
   const double bnorm = norm(T, kB);
   // stopping test on the Schur residual: the user's rtol/atol, tightened so

@@ -334,9 +334,9 @@ void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* km) {
   ++h.launches;
 }
 
-void launch_kmajor_to_soa(Handle& h, const double* km, int nvec, double* soa) {
+void launch_kmajor_to_soa(Handle& h, const double* km, int nvec, double* soa, cudaStream_t stream) {
   const long total = static_cast<long>(nvec) * h.K * h.N;
-  k_kmajor_to_soa<<<grid_of(total, 256), 256, 0, h.stream>>>(h.K, h.N, h.Kp, nvec, km, soa);
+  k_kmajor_to_soa<<<grid_of(total, 256), 256, 0, stream ? stream : h.stream>>>(h.K, h.N, h.Kp, nvec, km, soa);
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
