@@ -42,22 +42,32 @@ double env_or(const char* name, double dflt) {
   const char* s = std::getenv(name);
   return s ? std::atof(s) : dflt;
 }
-// Sweeps (pre counts the residual-free first sweep from x = 0): V(5,5) on
-// level 0 and V(2,1) below.  Level-0 sweeps stream at ~60 % of HBM bandwidth
-// while the coarse levels are latency-bound, so smoothing moved to level 0
-// buys more per microsecond: measured at 256^2, p = 0..4, ms/step
-// 5.6/11.4/24.8/45/95 with V(2,2) everywhere vs 6.1/8.9/17.9/33.8/68.4
-// (V(4,4)+V(1,1): 6.9/10.8/19.3/37.1/78.4; swept in scripts/gpu_mgtune.sh).
+// Sweeps (pre counts the residual-free first sweep from x = 0), per degree
+// of the finest level.  Level-0 sweeps stream at ~60 % of HBM bandwidth
+// while the coarse levels are latency-bound, so smoothing sits on level 0:
+// V(5,5) there and V(2,1) below measured 6.1/8.9/17.9/33.8/68.4 ms/step at
+// 256^2, p = 0..4, against 5.6/11.4/24.8/45/95 with V(2,2) everywhere.  With
+// the p-coarsened hierarchy and Chebyshev level 0 the per-degree optimum
+// (scripts/gpu_envs_perp.sh, stable to 0.1 ms) is level 0 V(6,6) / V(4,5) /
+// V(4,6) / V(5,6) / V(5,6) and level 1 V(2,1) except V(1,1) at p = 4
+// (ms/step 5.17 / 7.47 / 11.11 / 20.11 / 38.49 against 5.59 / 7.67 / 11.88 /
+// 20.55 / 41.09 with V(5,5) + V(2,1)).  LDG_MG_* override for every degree.
 const double kOmega = env_or("LDG_MG_OMEGA", 0.7);  // damped block-Jacobi smoother
 const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));    // coarse levels
 const int kPost = static_cast<int>(env_or("LDG_MG_POST", 1));  // coarse levels
-const int kPre0 = static_cast<int>(env_or("LDG_MG_PRE0", 5));    // level 0
-const int kPost0 = static_cast<int>(env_or("LDG_MG_POST0", 5));  // level 0
 const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
-const int kPre1 = static_cast<int>(env_or("LDG_MG_PRE1", kPre));    // level 1
-const int kPost1 = static_cast<int>(env_or("LDG_MG_POST1", kPost));  // level 1
-int pre_of(int l) { return l == 0 ? kPre0 : (l == 1 ? kPre1 : kPre); }
-int post_of(int l) { return l == 0 ? kPost0 : (l == 1 ? kPost1 : kPost); }
+constexpr int kPre0P[5] = {6, 4, 4, 5, 5}, kPost0P[5] = {6, 5, 6, 6, 6};
+constexpr int kPre1P[5] = {2, 2, 2, 2, 1}, kPost1P[5] = {1, 1, 1, 1, 1};
+int sweeps_of(const char* env, const int* table, int p) {
+  const char* s = std::getenv(env);
+  return s ? std::atoi(s) : table[p < 0 ? 0 : (p > 4 ? 4 : p)];
+}
+int pre_of(int p, int l) {
+  return l == 0 ? sweeps_of("LDG_MG_PRE0", kPre0P, p) : (l == 1 ? sweeps_of("LDG_MG_PRE1", kPre1P, p) : kPre);
+}
+int post_of(int p, int l) {
+  return l == 0 ? sweeps_of("LDG_MG_POST0", kPost0P, p) : (l == 1 ? sweeps_of("LDG_MG_POST1", kPost1P, p) : kPost);
+}
 
 #define LDG_NCCL(call)                                                                          \
   do {                                                                                          \
@@ -507,22 +517,22 @@ bool tail_level(Team& T, int l, bool f32) {
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   const bool coarsest = l == levels(T) - 1;
   if (tail_level(T, l, f32) && b == kMgB && x == kMgX) {
-    small_tail_vcycle(T.h0(), l, wm, dt, kOmega, pre_of(l), post_of(l), kCoarseSweeps);
+    small_tail_vcycle(T.h0(), l, wm, dt, kOmega, pre_of(T.h0().p, l), post_of(T.h0().p, l), kCoarseSweeps);
     return;
   }
   // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
   // (every rank keeps a column), so a larger coarsest grid gets more sweeps
-  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(l) - 1) + post_of(l);
+  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(T.h0().p, l) - 1) + post_of(T.h0().p, l);
   if (fused(T, l, f32) && rb_level(T, l)) {
     each(T, l, [&](Handle& L) { f_zero(L, b, x); });
-    const int pre = coarsest ? sweeps : pre_of(l) - 1;
+    const int pre = coarsest ? sweeps : pre_of(T.h0().p, l) - 1;
     for (int s = 0; s < pre; ++s) sweep_rb(T, l, wm, dt, b, x, false);
     if (coarsest) return;
     residual_f(T, l, wm, dt, b, x, kMgR);
     for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
-    for (int s = 0; s < post_of(l); ++s) sweep_rb(T, l, wm, dt, b, x, true);
+    for (int s = 0; s < post_of(T.h0().p, l); ++s) sweep_rb(T, l, wm, dt, b, x, true);
     return;
   }
   if (fused(T, l, f32) && cheb_level(T, l) && !coarsest) {
@@ -532,7 +542,7 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     auto other = [&](Vec v) { return v == x ? kMgS : x; };
     ch.step(0, &a, &be);
     each(T, l, [&](Handle& L) { smooth_zero(L, vp(L, b), a, vp(L, cur)); });
-    for (int s = 0; s < pre_of(l) - 1; ++s) {
+    for (int s = 0; s < pre_of(T.h0().p, l) - 1; ++s) {
       ch.step(s + 1, &a, &be);
       sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, s == 0);
       cur = other(cur);
@@ -541,7 +551,7 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
-    for (int s = 0; s < post_of(l); ++s) {
+    for (int s = 0; s < post_of(T.h0().p, l); ++s) {
       ch.step(s, &a, &be);
       sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, false);
       cur = other(cur);
@@ -552,7 +562,7 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     Vec cur = (sweeps % 2) ? kMgS : x;
     auto other = [&](Vec v) { return v == x ? kMgS : x; };
     each(T, l, [&](Handle& L) { f_zero(L, b, cur); });
-    const int pre = coarsest ? sweeps : pre_of(l) - 1;
+    const int pre = coarsest ? sweeps : pre_of(T.h0().p, l) - 1;
     for (int s = 0; s < pre; ++s) {
       sweep_f(T, l, wm, dt, b, cur, other(cur));
       cur = other(cur);
@@ -562,7 +572,7 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
-    for (int s = 0; s < post_of(l); ++s) {
+    for (int s = 0; s < post_of(T.h0().p, l); ++s) {
       sweep_f(T, l, wm, dt, b, cur, other(cur));
       cur = other(cur);
     }
@@ -573,12 +583,12 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     for (int s = 0; s < sweeps; ++s) smooth(T, l, f32, wm, dt, b, x);
     return;
   }
-  for (int s = 1; s < pre_of(l); ++s) smooth(T, l, f32, wm, dt, b, x);
+  for (int s = 1; s < pre_of(T.h0().p, l); ++s) smooth(T, l, f32, wm, dt, b, x);
   residual(T, l, f32, wm, dt, b, x, kMgR);
   for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
   vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
   for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
-  for (int s = 0; s < post_of(l); ++s) smooth(T, l, f32, wm, dt, b, x);
+  for (int s = 0; s < post_of(T.h0().p, l); ++s) smooth(T, l, f32, wm, dt, b, x);
 }
 
 int64_t team_launches(Team& T) {
