@@ -53,20 +53,20 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
     default: { CALL(4); break; } \
   }
 
-// OUT: 0 FP64 SoA, 1 FP32 SoA, 2 FP32 packed (ldg_pack.cuh)
-template <int P, int OUT>
+// OUT: 0 FP64 SoA, 1 FP32 SoA, 2 FP32 packed (ldg_pack.cuh), 3 FP16 packed
+// scaled per element.  S: the arithmetic of the products and the elimination
+// -- FP32 for the FP16 smoother copy (OUT 3: the result is rounded to 11
+// bits anyway; FP32 issues twice the FMAs per cycle and holds half the
+// registers), FP64 otherwise.
+template <int P, int OUT, typename S = double>
 __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E,
                                                    const double* __restrict__ E_D, double wm, double dt, double eta,
                                                    void* __restrict__ out, float* __restrict__ out_scale) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG, Q = C::Q;
-  __shared__ __align__(16) double s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
-  __shared__ double s_piv[C::WARPS][C::EPW][2 * N + 2];
-  {
-    const double2* src = reinterpret_cast<const double2*>(T.base + T.tmH);
-    double2* dst = reinterpret_cast<double2*>(s_tab);
-    for (int t = threadIdx.x; t < 14 * NNP / 2; t += blockDim.x) dst[t] = src[t];
-  }
+  __shared__ __align__(16) S s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
+  __shared__ S s_piv[C::WARPS][C::EPW][2 * N + 2];
+  for (int t = threadIdx.x; t < 14 * NNP; t += blockDim.x) s_tab[t] = static_cast<S>(T.base[T.tmH + t]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / NG, i = lane % NG;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
   const double* tb = T.base;
 
   // a[jj] = row i of P_k
-  double a[N];
+  S a[N];
   const int ir = row ? i : 0;
   {
     const double two_a = 2.0 * g[kArea * Kp + kk];
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
 #pragma unroll
       for (int n = 0; n < 3; ++n)
         if (kind[n] == kInterior || kind[n] == kDirichlet) s += tb[T.sdiag + (ir * N + jj) * 3 + n];
-      a[jj] = wm * two_a * tb[T.mhat + ir * N + jj] + dt * eta * s;
+      a[jj] = static_cast<S>(wm * two_a * tb[T.mhat + ir * N + jj] + dt * eta * s);
     }
   }
   // a -= dt sum E (M^-1 B), as combined-E rows against the tables:
@@ -102,28 +102,34 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
     const double inv2a = 1.0 / (2.0 * g[kArea * Kp + kk]);
     const double b11 = g[kB11 * Kp + kk], b12 = g[kB12 * Kp + kk], b21 = g[kB21 * Kp + kk], b22 = g[kB22 * Kp + kk];
     // B^1_kk = -(b22 H1 - b21 H2) + sum_n f_n nu^x_n |E_n| S_d,n;  B^2_kk = -(b11 H2 - b12 H1) + ... nu^y
-    double c1[5], c2[5];  // coefficients of (tmH1, tmH2, tmSd0..2) for E^1 and E^2, with -dt and 1/(2|T|)
+    double c1d[5], c2d[5];  // coefficients of (tmH1, tmH2, tmSd0..2) for E^1 and E^2, with -dt and 1/(2|T|)
     const double sc = -dt * inv2a;
-    c1[0] = -b22 * sc;
-    c1[1] = b21 * sc;
-    c2[0] = b12 * sc;
-    c2[1] = -b11 * sc;
+    c1d[0] = -b22 * sc;
+    c1d[1] = b21 * sc;
+    c2d[0] = b12 * sc;
+    c2d[1] = -b11 * sc;
 #pragma unroll
     for (int n = 0; n < 3; ++n) {
       const int kd = m.kind[n * Kp + kk];
       const double f = kd == kInterior ? 0.5 : (kd == kNeumann ? 1.0 : 0.0);
       const double fl = f * g[(kLen0 + n) * Kp + kk] * sc;
-      c1[2 + n] = fl * g[(kNux0 + n) * Kp + kk];
-      c2[2 + n] = fl * g[(kNuy0 + n) * Kp + kk];
+      c1d[2 + n] = fl * g[(kNux0 + n) * Kp + kk];
+      c2d[2 + n] = fl * g[(kNuy0 + n) * Kp + kk];
+    }
+    S c1[5], c2[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      c1[t] = static_cast<S>(c1d[t]);
+      c2[t] = static_cast<S>(c2d[t]);
     }
 #pragma unroll 1
     for (int q = 0; q < N; ++q) {
-      const double e1 = E[(static_cast<long>(ir) * N + q) * Kp + kk];
-      const double e2 = E[(static_cast<long>(NN) + ir * N + q) * Kp + kk];
+      const S e1 = static_cast<S>(E[(static_cast<long>(ir) * N + q) * Kp + kk]);
+      const S e2 = static_cast<S>(E[(static_cast<long>(NN) + ir * N + q) * Kp + kk]);
 #pragma unroll
       for (int t = 0; t < 5; ++t) {
-        const double e = c1[t] * e1 + c2[t] * e2;
-        const double* tab = s_tab + t * NNP + q;
+        const S e = c1[t] * e1 + c2[t] * e2;
+        const S* tab = s_tab + t * NNP + q;
 #pragma unroll
         for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab[jj * NP], a[jj]);
       }
@@ -142,40 +148,40 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
       const double kappa = hl * (cx * g[(kNux0 + n) * Kp + kk] + cy * g[(kNuy0 + n) * Kp + kk]);
       const double* pth = tb + T.pth + (n * 3 + np) * Q * N;  // V^t [q][.]
       const double* pe = tb + T.pe + n * Q * N;               // U^t [q][.]
-      double aq[Q];
+      S aq[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         double dv = 0.0;
 #pragma unroll
         for (int l = 0; l < N; ++l) dv = fma(E_D[l * Kp + j], pth[q * N + l], dv);
-        aq[q] = kappa * pe[q * N + ir] * tb[T.we + q] * dv;
+        aq[q] = static_cast<S>(kappa * pe[q * N + ir] * tb[T.we + q] * dv);
       }
-      const double* tab0 = s_tab + (5 + np * 3 + n) * NNP;
+      const S* tab0 = s_tab + (5 + np * 3 + n) * NNP;
 #pragma unroll 1
       for (int q2 = 0; q2 < N; ++q2) {
-        double e = 0.0;
+        S e = 0;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) e = fma(aq[q], pth[q * N + q2], e);
+        for (int q = 0; q < Q; ++q) e = fma(aq[q], static_cast<S>(pth[q * N + q2]), e);
 #pragma unroll
         for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab0[jj * NP + q2], a[jj]);
       }
     }
   }
-  double v[N];  // row i of the augmented identity
+  S v[N];  // row i of the augmented identity
 #pragma unroll
-  for (int jj = 0; jj < N; ++jj) v[jj] = (jj == i) ? 1.0 : 0.0;
+  for (int jj = 0; jj < N; ++jj) v[jj] = (jj == i) ? S(1) : S(0);
 
   // Gauss-Jordan, partial pivoting over the rows not yet used
   bool used = !row;
   int my_col = -1;
-  double* piv = s_piv[warp][sub];
+  S* piv = s_piv[warp][sub];
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    double best = used ? -1.0 : fabs(a[c]);
+    S best = used ? S(-1) : fabs(a[c]);
     int who = i;
 #pragma unroll
     for (int o = NG / 2; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const S ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int ow = __shfl_xor_sync(0xffffffffu, who, o);
       if (ob > best || (ob == best && ow < who)) {
         best = ob;
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
       }
     }
     if (i == who && row) {
-      const double inv = 1.0 / a[c];
+      const S inv = S(1) / a[c];
 #pragma unroll
       for (int jj = 0; jj < N; ++jj) {
         a[jj] *= inv;
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
     }
     __syncwarp();
     if (row && i != who) {
-      const double f = a[c];
+      const S f = a[c];
 #pragma unroll
       for (int jj = 0; jj < N; ++jj) {
         a[jj] = fma(-f, piv[jj], a[jj]);
@@ -206,19 +212,19 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
     __syncwarp();
   }
   if constexpr (OUT == 3) {  // FP16 packed, scaled per element by max |P^-1|
-    double mx = 0.0;
+    S mx = 0;
     if (row)
 #pragma unroll
       for (int jj = 0; jj < N; ++jj) mx = fmax(mx, fabs(v[jj]));
 #pragma unroll
     for (int o = NG / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const double sc = mx > 0.0 ? mx : 1.0;
+    const S sc = mx > S(0) ? mx : S(1);
     if (row) {
       if (i == 0) out_scale[k] = static_cast<float>(sc);
-      const double inv = 1.0 / sc;
+      const S inv = S(1) / sc;
 #pragma unroll
       for (int jj = 0; jj < N; ++jj)
-        static_cast<__half*>(out)[sm_packed_p_index<P>(my_col, jj, Kp, k)] = __double2half(v[jj] * inv);
+        static_cast<__half*>(out)[sm_packed_p_index<P>(my_col, jj, Kp, k)] = __float2half(static_cast<float>(v[jj] * inv));
     }
     return;
   }
@@ -249,6 +255,9 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
   float* sc = out_kind == 3 ? h.Pscale.ptr : nullptr;
 #define LAUNCH(P, O) \
   k_bjac_warp<P, O><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, sc)
+#define LAUNCH32(P, O)                                                                                        \
+  k_bjac_warp<P, O, float><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, \
+                                                       sc)
 #define CALL(P)                                                      \
   do {                                                               \
     const unsigned grid = grid_of(h.K, Cfg<P>::EPB);                 \
@@ -256,12 +265,13 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
       case 0: LAUNCH(P, 0); break;                                   \
       case 1: LAUNCH(P, 1); break;                                   \
       case 2: LAUNCH(P, 2); break;                                   \
-      default: LAUNCH(P, 3); break;                                  \
+      default: LAUNCH32(P, 3); break;                                \
     }                                                                \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
 #undef LAUNCH
+#undef LAUNCH32
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
