@@ -230,7 +230,7 @@ class SolverOptions:
     rtol: float = 0.0
     atol: float = 0.0
     maxit: int = 20000
-    precond: int = 2  # 0 none, 1 block-Jacobi, 2 geometric multigrid V(2,2) (FK meshes; else 1)
+    precond: int = 2  # 0 none, 1 block-Jacobi, 2 geometric multigrid (p-coarsened, FK meshes; else 1)
     check_residual: bool = True
     contract_tol: float = 1e-10
     krylov: int = 0  # 0 FGMRES(restart), 1 BiCGStab

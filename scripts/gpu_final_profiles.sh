@@ -19,7 +19,7 @@ for P in 4 2; do
   echo "launch p$P rc $?" >> $O/rc.txt
 done
 timeout 1800 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:k_s2f<|k_s1f<|k_stage2<|k_stage1<|k_assemble<|k_bjac_warp<" -c 12 -f -o $O/full_p4 \
+  -k "regex:k_s2f<|k_s1f<|k_stage2<|k_stage1<|k_bjf<" -c 14 -f -o $O/full_p4 \
   python scripts/profile_step.py --p 4 --dim 256 > $O/ncu_full_p4.log 2>&1
 echo "full rc $?" >> $O/rc.txt
 cat $O/rc.txt

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--dt", type=float, default=0.05)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--assemble-only", action="store_true")
+    ap.add_argument("--blocks", action="store_true", help="BASELINE config 3 call (all 8 blocks + projection + rhs)")
     ap.add_argument("--precond", type=int, default=2)
     args = ap.parse_args()
     import torch
@@ -26,14 +27,19 @@ def main():
     s = ld.LdgSystem.square(args.dim, args.p, ld.BASELINE_SPEC)
     s.initial_state()
     opts = ld.SolverOptions(precond=args.precond)
-    if args.assemble_only:
+    if args.blocks:
+        for i in range(args.warmup):
+            print("warm-up assemble_blocks ms", s.assemble_blocks(0.05 * (i + 1)))
+    elif args.assemble_only:
         for i in range(args.warmup):
             s.assemble(0.05 * (i + 1))
     else:
         s.euler_steps(args.dt, args.warmup, opts)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
-    if args.assemble_only:
+    if args.blocks:
+        st = {"ms": s.assemble_blocks(1.0)}
+    elif args.assemble_only:
         s.assemble(1.0)
         st = {}
     else:
