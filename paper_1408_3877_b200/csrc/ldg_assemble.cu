@@ -13,7 +13,9 @@
 //                         the integrand is polynomial, so this equals the
 //                         reference's tensor contraction up to rounding.
 //  K4  B^m = -H^m + Q^m + Q_N^m and S + S_D   assembly.hpp:76-208
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ldg_internal.hpp"
 
@@ -117,9 +119,12 @@ __global__ void __launch_bounds__(128) k_project(DevMesh m, int count, const dou
 
 // ---------------------------------------------------------------- K5
 // which: 0 -> V = [-J1; -J2; eta K_D - K_N + L] (3 planes of N), 1 J1, 2 J2,
-// 3 K_D, 4 K_N, 5 L (one plane of N each).
+// 3 K_D, 4 K_N, 5 L (one plane of N each).  L = M F is written first; the
+// boundary edges (a few elements) then add their terms in place, one edge at
+// a time, so only N accumulators are live (the all-in-registers form needed
+// 255 registers at p = 4 and ran at 2.6 TB/s).
 template <int P>
-__global__ void __launch_bounds__(128) k_rhs(DevMesh m, DevTables T, ldg_coeff cd, ldg_coeff gn, double eta,
+__global__ void __launch_bounds__(128, 4) k_rhs(DevMesh m, DevTables T, ldg_coeff cd, ldg_coeff gn, double eta,
                                              double t, const double* __restrict__ D, const double* __restrict__ F,
                                              int which, double* __restrict__ out) {
   constexpr int N = Cfg<P>::N, QB = Cfg<P>::QB;
@@ -133,9 +138,23 @@ __global__ void __launch_bounds__(128) k_rhs(DevMesh m, DevTables T, ldg_coeff c
   if (k >= m.K) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
-  double j1[N], j2[N], kd[N], kn[N];
+  {
+    const bool need_l = which == 0 || which == 5;
+    double f[N];
 #pragma unroll
-  for (int i = 0; i < N; ++i) j1[i] = j2[i] = kd[i] = kn[i] = 0.0;
+    for (int j = 0; j < N; ++j) f[j] = need_l ? F[j * Kp + k] : 0.0;
+    const double two_area = 2.0 * g[kArea * Kp + k];
+    double* lo = out + (which == 0 ? 2L * N * Kp : 0L);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double l = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) l += (two_area * s_m[i * N + j]) * f[j];
+      lo[i * Kp + k] = l;
+      if (which == 0) out[i * Kp + k] = out[(N + i) * Kp + k] = 0.0;
+    }
+  }
+#pragma unroll 1
   for (int n = 0; n < 3; ++n) {
     const int kind = m.kind[n * Kp + k];
     if (kind != kDirichlet && kind != kNeumann) continue;
@@ -143,6 +162,7 @@ __global__ void __launch_bounds__(128) k_rhs(DevMesh m, DevTables T, ldg_coeff c
     double s[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) s[i] = 0.0;
+#pragma unroll 1
     for (int q = 0; q < QB; ++q) {
       double r1, r2, x1, x2;
       edge_ref_point(n, s_sb[q], &r1, &r2);
@@ -160,36 +180,26 @@ __global__ void __launch_bounds__(128) k_rhs(DevMesh m, DevTables T, ldg_coeff c
 #pragma unroll
       for (int i = 0; i < N; ++i) s[i] += cw * ph[i];
     }
+    // this edge's terms: J_D^m += nu^m |E| s, K_D += s (Dirichlet); K_N += s (Neumann)
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;  // coefficients for planes 0, 1, 2
     if (kind == kDirichlet) {
-      const double c1 = g[(kNux0 + n) * Kp + k] * len, c2 = g[(kNuy0 + n) * Kp + k] * len;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        j1[i] += c1 * s[i];
-        j2[i] += c2 * s[i];
-        kd[i] += s[i];
+      const double j1 = g[(kNux0 + n) * Kp + k] * len, j2 = g[(kNuy0 + n) * Kp + k] * len;
+      if (which == 0) {
+        c0 = -j1;
+        c1 = -j2;
+        c2 = eta;
+      } else {
+        c0 = which == 1 ? j1 : (which == 2 ? j2 : (which == 3 ? 1.0 : 0.0));
       }
     } else {
-#pragma unroll
-      for (int i = 0; i < N; ++i) kn[i] += s[i];
+      if (which == 0) c2 = -1.0;
+      else c0 = which == 4 ? 1.0 : 0.0;
     }
-  }
-  const double two_area = 2.0 * g[kArea * Kp + k];
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double l = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j) l += (two_area * s_m[i * N + j]) * F[j * Kp + k];
-    switch (which) {
-      case 0:
-        out[i * Kp + k] = -j1[i];
-        out[(N + i) * Kp + k] = -j2[i];
-        out[(2 * N + i) * Kp + k] = eta * kd[i] - kn[i] + l;
-        break;
-      case 1: out[i * Kp + k] = j1[i]; break;
-      case 2: out[i * Kp + k] = j2[i]; break;
-      case 3: out[i * Kp + k] = kd[i]; break;
-      case 4: out[i * Kp + k] = kn[i]; break;
-      default: out[i * Kp + k] = l; break;
+    for (int i = 0; i < N; ++i) {
+      if (c0 != 0.0) out[i * Kp + k] += c0 * s[i];
+      if (c1 != 0.0) out[(N + i) * Kp + k] += c1 * s[i];
+      if (c2 != 0.0) out[(2 * N + i) * Kp + k] += c2 * s[i];
     }
   }
 }
@@ -332,6 +342,225 @@ __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const 
   }
 }
 
+// K3, row form (kModeE / kModeEdiag, the production modes).  The kernel
+// above walks (i, j) with short dependent FMA chains and loads one table
+// entry per FMA; ncu at 1024^2, p = 4: 168 registers, 3 warps per scheduler,
+// 9 cycles per issued instruction, short-scoreboard (shared-load latency)
+// and fixed-latency (FMA chain) stalls on top — 3.7 TB/s.  Here a thread
+// produces one block ROW i at a time for both m:
+//   G:  acc^m[j] = sum_l D_l Ghat(i, j, l, m)     (table permuted to [i][l][j][m]:
+//       one 128-bit broadcast load feeds the m = 1, 2 FMAs of one j)
+//   E^m[j] = -(B-combination of acc)             (assembly.hpp:126-129)
+//   R:  r[j] = sum_q (w_q d_h(gamma_n(s_q)) phi_i) phi_j   per edge n,
+//       E^m[j] += c^m_n r[j]                      (rank-Qe form, see above)
+//   off-diagonal rows likewise from the neighbour's D.
+// 30 (G) or 15 (R) independent accumulators per row instead of 2-5, and the
+// per-element constants (D_k, w_q d_h) live in shared memory (one conflict-free
+// 64-bit load per use) so the registers hold the accumulators.
+template <int P>
+struct Asm2 {
+  static constexpr int N = Cfg<P>::N, Q = Cfg<P>::QE, NN = N * N;
+  static constexpr int NP = (N % 2) ? N + 1 : N;  // padded table rows (16-byte aligned)
+  // p = 4: one 384-thread CTA per SM (<= 168 registers, 12 warps; two
+  // 128-thread CTAs were register- and shared-limited to 8); below, 128
+  static constexpr int kThreads = P == 4 ? 384 : 128;
+  static constexpr int kMinBlocks = P == 4 ? 1 : 4;
+  // shared: G [i][l][j][2] | pe [n][q][NP] | pth [n][np][q][NP] | we [Q] (even) | per-thread [N + 3Q][T]
+  static constexpr int kG = 2 * N * NN, kPe = 3 * Q * NP, kPth = 9 * Q * NP, kWe = (Q + 1) / 2 * 2;
+  static constexpr int kTab = kG + kPe + kPth + kWe;
+  static constexpr int kPer = N + 3 * Q + 6;
+  static constexpr size_t smem() { return sizeof(double) * (kTab + static_cast<size_t>(kPer) * kThreads); }
+};
+
+// acc[j] += a * row[j], j < N, row 16-byte aligned in shared memory
+template <int N>
+__device__ __forceinline__ void row_axpy(double a, const double* row, double* acc) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+  for (int q = 0; q < N / 2; ++q) {
+    const double2 v = r2[q];
+    acc[2 * q] = fma(a, v.x, acc[2 * q]);
+    acc[2 * q + 1] = fma(a, v.y, acc[2 * q + 1]);
+  }
+  if (N & 1) acc[N - 1] = fma(a, row[N - 1], acc[N - 1]);
+}
+
+template <int P, int MODE>
+__device__ __forceinline__ void assemble_rows_element(const DevMesh& m, const double* __restrict__ D,
+                                                      double* __restrict__ out, const double* s_g,
+                                                      const double* s_pe, const double* s_pth,
+                                                      const double* s_we, double* per, int k) {
+  using A = Asm2<P>;
+  constexpr int N = A::N, Q = A::Q, NN = A::NN, NP = A::NP;
+  constexpr bool kDiagOnly = MODE == kModeEdiag;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  auto dk = [&](int l) -> double& { return per[l * A::kThreads]; };
+  auto wd = [&](int n, int q) -> double& { return per[(N + n * Q + q) * A::kThreads]; };
+  // c^m_n of the diagonal R terms (rolled edge loops index them)
+  auto cm = [&](int mm, int n) -> double& { return per[(N + 3 * Q + mm * 3 + n) * A::kThreads]; };
+#pragma unroll
+  for (int l = 0; l < N; ++l) dk(l) = D[l * Kp + k];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const int kind = m.kind[n * Kp + k];
+    const double len = g[(kLen0 + n) * Kp + k];
+    const double f = kind == kInterior ? 0.5 * len : (kind == kDirichlet ? len : 0.0);
+    cm(0, n) = f * g[(kNux0 + n) * Kp + k];
+    cm(1, n) = f * g[(kNuy0 + n) * Kp + k];
+#pragma unroll 1
+    for (int q = 0; q < Q; ++q) {
+      double dv = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) dv = fma(dk(l), s_pe[(n * Q + q) * NP + l], dv);
+      wd(n, q) = s_we[q] * dv;
+    }
+  }
+  const double b11 = g[kB11 * Kp + k], b12 = g[kB12 * Kp + k];
+  const double b21 = g[kB21 * Kp + k], b22 = g[kB22 * Kp + k];
+  double* o1 = out;
+  double* o2 = out + (kDiagOnly ? 1L : 4L) * NN * Kp;
+#pragma unroll 1
+  for (int i = 0; i < N; ++i) {
+    double e1[N], e2[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) e1[j] = e2[j] = 0.0;
+#pragma unroll 3
+    for (int l = 0; l < N; ++l) {
+      const double d = dk(l);
+      const double2* row = reinterpret_cast<const double2*>(s_g + (i * N + l) * 2 * N);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double2 v = row[j];
+        e1[j] = fma(d, v.x, e1[j]);
+        e2[j] = fma(d, v.y, e2[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {  // E^m = -G^m: G^1 = b22 g1 - b21 g2, G^2 = b11 g2 - b12 g1
+      const double g1 = e1[j], g2 = e2[j];
+      e1[j] = fma(b21, g2, -b22 * g1);
+      e2[j] = fma(b12, g1, -b11 * g2);
+    }
+#pragma unroll 1
+    for (int n = 0; n < 3; ++n) {
+      const double c1 = cm(0, n), c2 = cm(1, n);
+      if (c1 == 0.0 && c2 == 0.0) continue;
+      double r[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) r[j] = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const double* pr = s_pe + (n * Q + q) * NP;
+        row_axpy<N>(wd(n, q) * pr[i], pr, r);
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        e1[j] = fma(c1, r[j], e1[j]);
+        e2[j] = fma(c2, r[j], e2[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      o1[static_cast<long>(i * N + j) * Kp + k] = e1[j];
+      o2[static_cast<long>(i * N + j) * Kp + k] = e2[j];
+    }
+  }
+  if constexpr (kDiagOnly) return;
+  // off-diagonal blocks (assembly.hpp:238-247): neighbour coefficient, normal
+  // and length of the k- side.  Per edge: the neighbour's D into the (no
+  // longer needed) D_k slots, its edge samples w_q d_{k+}(theta(s_q)) into the
+  // diagonal's slots, c^m into cm (0 on boundary edges: zero blocks).  The
+  // row loop runs outside the edge loop so the compiler cannot hoist an
+  // edge's whole pth table into registers across rows.
+  int npk = 0;
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kp = m.nbr[n * Kp + k];
+    if (kp < 0) {
+      for (int q = 0; q < Q; ++q) wd(n, q) = 0.0;
+      cm(0, n) = cm(1, n) = 0.0;
+      continue;
+    }
+    const int np = m.nbrn[n * Kp + k];
+    npk |= np << (2 * n);
+    const double* pt = s_pth + (n * 3 + np) * Q * NP;
+#pragma unroll
+    for (int l = 0; l < N; ++l) dk(l) = D[l * Kp + kp];
+#pragma unroll 1
+    for (int q = 0; q < Q; ++q) {
+      double dv = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) dv = fma(dk(l), pt[q * NP + l], dv);
+      wd(n, q) = s_we[q] * dv;
+    }
+    const double half_len = 0.5 * g[(kLen0 + n) * Kp + k];
+    cm(0, n) = half_len * g[(kNux0 + n) * Kp + k];
+    cm(1, n) = half_len * g[(kNuy0 + n) * Kp + k];
+  }
+#pragma unroll 1
+  for (int i = 0; i < N; ++i) {
+#pragma unroll 1
+    for (int n = 0; n < 3; ++n) {
+      const double* pt = s_pth + (n * 3 + ((npk >> (2 * n)) & 3)) * Q * NP;
+      double r[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) r[j] = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) row_axpy<N>(wd(n, q) * s_pe[(n * Q + q) * NP + i], pt + q * NP, r);
+      const double co1 = cm(0, n), co2 = cm(1, n);
+      double* p1 = o1 + static_cast<long>(1 + n) * NN * Kp;
+      double* p2 = o2 + static_cast<long>(1 + n) * NN * Kp;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        p1[static_cast<long>(i * N + j) * Kp + k] = co1 * r[j];
+        p2[static_cast<long>(i * N + j) * Kp + k] = co2 * r[j];
+      }
+    }
+  }
+}
+
+// Persistent: the grid is sized to the resident CTAs and each CTA loops over
+// blocks of kThreads elements, so the ~65 KB of tables are staged once per
+// CTA (staged per 128 elements they cost ~15 % of the run in exposed L2
+// latency at p = 4).
+template <int P, int MODE>
+__global__ void __launch_bounds__(Asm2<P>::kThreads, Asm2<P>::kMinBlocks) k_assemble_rows(DevMesh m, DevTables T,
+                                                                        const double* __restrict__ D,
+                                                                        double* __restrict__ out) {
+  using A = Asm2<P>;
+  constexpr int N = A::N, Q = A::Q, NP = A::NP;
+  extern __shared__ __align__(16) double sm[];
+  double* s_g = sm;                 // [i][l][j][m]
+  double* s_pe = s_g + A::kG;       // [n][q][NP]
+  double* s_pth = s_pe + A::kPe;    // [n][np][q][NP]
+  double* s_we = s_pth + A::kPth;   // [q]
+  double* s_per = s_we + A::kWe;    // [v][tid]: v < N D_k, then w_q d_h on edge n at N + n Q + q
+  {
+    const double* gsrc = T.base + T.ghat;  // [i][j][l][m]
+#pragma unroll 8
+    for (int t = threadIdx.x; t < A::kG; t += blockDim.x) {
+      const int mm = t & 1, j = (t >> 1) % N, il = (t >> 1) / N, l = il % N, i = il / N;
+      s_g[t] = __ldg(gsrc + ((i * N + j) * N + l) * 2 + mm);
+    }
+    for (int t = threadIdx.x; t < 3 * Q * NP; t += blockDim.x) {
+      const int j = t % NP, nq = t / NP;
+      s_pe[t] = j < N ? T.base[T.pe + nq * N + j] : 0.0;
+    }
+    for (int t = threadIdx.x; t < 9 * Q * NP; t += blockDim.x) {
+      const int j = t % NP, nq = t / NP;
+      s_pth[t] = j < N ? T.base[T.pth + nq * N + j] : 0.0;
+    }
+    for (int t = threadIdx.x; t < Q; t += blockDim.x) s_we[t] = T.base[T.we + t];
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  double* per = s_per + tid;
+  for (int k = blockIdx.x * blockDim.x + tid; k - tid < m.K; k += gridDim.x * blockDim.x) {
+    if (k < m.K) assemble_rows_element<P, MODE>(m, D, out, s_g, s_pe, s_pth, s_we, per, k);
+  }
+}
+
 // ---------------------------------------------------------------- K4
 // Static blocks.  kStB: out = B^1 | B^2 (2 x 4 slots); kStS: S + S_D (4 slots);
 // export modes write one operator (2 comps for H/Q/QN, 1 for M/S/SD).
@@ -407,8 +636,44 @@ size_t assemble_smem() {
   return sizeof(double) * (2 * N * N * N + 3 * Q * N + 9 * Q * N + Q);
 }
 
+// Row kernel for the production modes at p = 4 (C3, 1024^2: 6.0 vs 8.6 ms,
+// 5.2 TB/s); at p = 2, 3 the (i, j) kernel measured 3-8 % faster (1.25 vs
+// 1.36 ms, 3.20 vs 3.32 ms for the whole C3-style call at 1024^2).
+// LDG_ASM_V1=1 forces the (i, j) kernel, =0 the row kernel (A/B runs).
+bool asm_v1(int p) {
+  static const int env = [] {
+    const char* e = std::getenv("LDG_ASM_V1");
+    return e ? std::atoi(e) : -1;
+  }();
+  return env < 0 ? p < 4 : env != 0;
+}
+
 template <int P, int MODE>
 void launch_assemble_p(Handle& h, double* out) {
+  if constexpr (MODE == kModeE || MODE == kModeEdiag) {
+    if (!asm_v1(P)) {
+      const size_t smem = Asm2<P>::smem();
+      auto kern = k_assemble_rows<P, MODE>;
+      static bool configured2 = false;
+      if (!configured2) {
+        LDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured2 = true;
+      }
+      static int grid_cap = 0;
+      if (!grid_cap) {
+        int dev = 0, sms = 0, per_sm = 0;
+        LDG_CUDA(cudaGetDevice(&dev));
+        LDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        LDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Asm2<P>::kThreads, smem));
+        grid_cap = std::max(1, sms * per_sm);
+      }
+      const unsigned grid = std::min<unsigned>(grid_of(h.K, Asm2<P>::kThreads), static_cast<unsigned>(grid_cap));
+      kern<<<grid, Asm2<P>::kThreads, smem, h.stream>>>(h.mesh(), h.dtab, h.D.ptr, out);
+      LDG_CUDA(cudaGetLastError());
+      ++h.launches;
+      return;
+    }
+  }
   const size_t smem = assemble_smem<P>();
   auto kern = k_assemble<P, MODE>;
   static bool configured = false;
