@@ -34,16 +34,20 @@
 // p = 0..4 (stage 1 | stage 2).  The level-0 grids are 1024 CTAs of 128
 // (256^2 FK): 7-8 CTAs/SM (<= 73 / 64 registers, a few spilled bytes) run
 // them in one wave: V-cycle -13% at p = 2 and -14% at p = 3 (stage 2 at 7,
-// stage 1 at 8: 0.515 / 0.764 ms against 0.600 / 0.883 ms with 1 CTA); at
-// p = 4 the spills grow and 4 CTAs (<= 128 registers) stay best (7-15% over
-// 1 CTA; 8 for stage 1 measured +7% V-cycle); 8 at p <= 1 measured slower.
+// stage 1 at 8: 0.515 / 0.764 ms against 0.600 / 0.883 ms with 1 CTA).  At
+// p = 4 stage 2 at 7 CTAs (72 registers, 48 bytes spilled) runs the level in
+// one wave: V-cycle 1557 -> 1435 us, step 38.4 -> 36.2 ms (5 and 6 CTAs,
+// 96 / 80 registers without spills, stay at two waves and were 1-2 % slower
+// than 4; 8 CTAs spill more: +6 %).  Stage 1 at p = 4 stays at 4 CTAs: 6, 7,
+// 8 CTAs (also with one neighbour at a time, LDG_S1_SEQ_P) measured
+// +3 / +7 / +16 % V-cycle.  8 at p <= 1 measured slower.
 // -DLDG_MINB_S1=abcde / -DLDG_MINB_S2=abcde (one digit per p = 0..4)
 // override (tuning builds).
 #ifndef LDG_MINB_S1
 #define LDG_MINB_S1 11884
 #endif
 #ifndef LDG_MINB_S2
-#define LDG_MINB_S2 11774
+#define LDG_MINB_S2 11777
 #endif
 
 namespace ldgb {
@@ -158,13 +162,35 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
     }
   }
   // the neighbours' x: every load issued before the products (one latency
-  // round instead of one per neighbour)
+  // round instead of one per neighbour) — or, when the kernel runs at a high
+  // CTA count per SM (LDG_S1_SEQ_P = p), one neighbour at a time (15 instead
+  // of 45 live registers)
   int nb[3], nbn[3];
 #pragma unroll
   for (int n = 0; n < 3; ++n) {
     nb[n] = m.nbr[n * Kp + k];
     nbn[n] = m.nbrn[n * Kp + k];
   }
+#ifdef LDG_S1_SEQ_P
+  if constexpr (P == LDG_S1_SEQ_P) {
+#pragma unroll 1
+    for (int n = 0; n < 3; ++n) {
+      if (nb[n] < 0) continue;
+      float xn1[N];
+      load_f<N>(x, Kp, nb[n], xn1);
+      ftab_mv<N, NF>(tb + (5 + n * 3 + nbn[n]) * TAB, xn1, w);
+      const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+      const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
+      const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        u1[i] = fmaf(c1, w[i], u1[i]);
+        u2[i] = fmaf(c2, w[i], u2[i]);
+      }
+    }
+  } else
+#endif
+  {
   float xn[3][N];
 #pragma unroll
   for (int n = 0; n < 3; ++n)
@@ -182,6 +208,7 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
       u1[i] = fmaf(c1, w[i], u1[i]);
       u2[i] = fmaf(c2, w[i], u2[i]);
     }
+  }
   }
   const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
 #pragma unroll
