@@ -21,11 +21,13 @@
 
 // min resident CTAs per SM of the thread-per-element kernels: at p = 4 the
 // register-heavy kernels are latency-bound at 1 CTA; 4 CTAs (<= 128 registers)
-// measured 7-15% faster there and slower at p <= 3 (-DLDG_MINB_STAGE=n overrides)
+// measured 7-15% faster there (2, 6, 7 CTAs: +24 / +48 / +38 % Schur apply).
+// At p = 3, 7 CTAs (one wave of the 256^2 level): Schur apply 145 -> 110 us,
+// full apply 153 -> 115 us; p = 2 neutral.  (-DLDG_MINB_STAGE=n overrides.)
 #ifdef LDG_MINB_STAGE
 #define LDG_MINB_STAGE_P(P) LDG_MINB_STAGE
 #else
-#define LDG_MINB_STAGE_P(P) ((P) == 4 ? 4 : 1)
+#define LDG_MINB_STAGE_P(P) ((P) == 4 ? 4 : ((P) == 3 ? 7 : 1))
 #endif
 
 namespace ldgb {

@@ -129,6 +129,46 @@ __global__ void __launch_bounds__(256) k_mdot_owned(int N, long Kp, int K, int n
   }
 }
 
+// (v_d, w) for d < nv when every entry of the vectors is owned (one rank,
+// K == Kp: no ghosts, no padding): one flat 128-bit stream per vector, 16 dots
+// per block row (w read at most twice for the FGMRES basis sizes), 512
+// threads per block.  The (j, k) form above moves 64-bit values with a
+// 1.73-iteration inner loop per plane at 256^2 and ran at ~2.4 TB/s.
+constexpr int kMdotFlatChunk = 16;
+__global__ void __launch_bounds__(512) k_mdot_flat(long n2, int nv, MDotArgs a, const double* __restrict__ w,
+                                                   double* __restrict__ part) {
+  const int d0 = blockIdx.y * kMdotFlatChunk;
+  const int nd = min(kMdotFlatChunk, nv - d0);
+  double s[kMdotFlatChunk];
+#pragma unroll
+  for (int d = 0; d < kMdotFlatChunk; ++d) s[d] = 0.0;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n2;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double2 wi = w2[i];
+#pragma unroll
+    for (int d = 0; d < kMdotFlatChunk; ++d)
+      if (d < nd) {
+        const double2 v = reinterpret_cast<const double2*>(a.v[d0 + d])[i];
+        s[d] = fma(v.x, wi.x, fma(v.y, wi.y, s[d]));
+      }
+  }
+  __shared__ double sh[kMdotFlatChunk][16];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < kMdotFlatChunk; ++d) {
+    double v = s[d];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[d][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nd) {
+    double v = 0.0;
+    for (int ww = 0; ww < 16; ++ww) v += sh[threadIdx.x][ww];
+    part[(d0 + threadIdx.x) * kRedBlocks + blockIdx.x] = v;
+  }
+}
+
 // w = alpha w + sum_d c_d v_d over the whole vector (n values)
 struct MAxpyArgs {
   const double* v[kMaxRed];
@@ -178,16 +218,24 @@ __global__ void __launch_bounds__(256) k_maxpy_dev(long n, int nv, MDotArgs a, c
     if (blockIdx.x == 0) *hn_out = hn;
   }
   __syncthreads();
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+  // 128-bit stream (n even: N Kp, Kp a multiple of 32)
+  const long n2 = n / 2;
+  double2* wv = reinterpret_cast<double2*>(w);
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n2;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
-    double acc = w[i];
+    double2 acc = wv[i];
 #pragma unroll 4
-    for (int d = 0; d < nv; ++d) acc = fma(s_c[d], a.v[d][i], acc);
-    if (FINAL) {
-      acc *= s_inv;
-      if (w2) w2[i] = acc;
+    for (int d = 0; d < nv; ++d) {
+      const double2 v = reinterpret_cast<const double2*>(a.v[d])[i];
+      acc.x = fma(s_c[d], v.x, acc.x);
+      acc.y = fma(s_c[d], v.y, acc.y);
     }
-    w[i] = acc;
+    if (FINAL) {
+      acc.x *= s_inv;
+      acc.y *= s_inv;
+      if (w2) reinterpret_cast<double2*>(w2)[i] = acc;
+    }
+    wv[i] = acc;
   }
 }
 
@@ -397,8 +445,13 @@ void launch_mdots_to(Handle& h, int nv, const double* const* v, const double* w,
   if (nv < 1 || nv > kMaxRed) throw Error(LDG_EINVAL, "multi-dot count out of range");
   MDotArgs a{};
   for (int d = 0; d < nv; ++d) a.v[d] = v[d];
-  const dim3 grid(kRedBlocks, (nv + kMdotChunk - 1) / kMdotChunk);
-  k_mdot_owned<<<grid, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nv, a, w, h.red.ptr);
+  if (h.K == h.Kp) {
+    const dim3 grid(kRedBlocks, (nv + kMdotFlatChunk - 1) / kMdotFlatChunk);
+    k_mdot_flat<<<grid, 512, 0, h.stream>>>(static_cast<long>(h.N) * h.Kp / 2, nv, a, w, h.red.ptr);
+  } else {
+    const dim3 grid(kRedBlocks, (nv + kMdotChunk - 1) / kMdotChunk);
+    k_mdot_owned<<<grid, 256, 0, h.stream>>>(h.N, h.Kp, h.K, nv, a, w, h.red.ptr);
+  }
   k_dots_final<<<final_blocks(nv), 256, 0, h.stream>>>(nv, h.red.ptr, out);
   LDG_CUDA(cudaGetLastError());
   h.launches += 2;
@@ -413,7 +466,7 @@ void launch_maxpy_dev(Handle& h, int nv, const double* const* v, const double* c
   MDotArgs a{};
   for (int d = 0; d < nv; ++d) a.v[d] = v[d];
   const long n = h.vec_len();
-  const unsigned grid = static_cast<unsigned>(std::min<long>(grid_of(n, 256), 4L * kRedBlocks));
+  const unsigned grid = static_cast<unsigned>(std::min<long>(grid_of(n / 2, 256), 4L * kRedBlocks));
   if (final)
     k_maxpy_dev<1><<<grid, 256, 0, h.stream>>>(n, nv, a, c, w, w2, hn_out);
   else
