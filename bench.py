@@ -452,6 +452,11 @@ def run_ours(args):
     for p, s, (y, t) in zip(ps, systems, starts):
         pin_in = torch.from_numpy(y).pin_memory()
         pin_out = torch.empty_like(pin_in).pin_memory()
+        # untimed warm-up call: the first host-buffer call of a handle allocates
+        # its staging buffer and creates the upload stream (host stalls the
+        # device timeline); the timed calls below restart from the same state
+        s.euler_steps_host(pin_in.data_ptr(), t, dt, 1, pin_out.data_ptr(), opts)
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()

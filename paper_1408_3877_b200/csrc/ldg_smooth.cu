@@ -75,6 +75,11 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
     default: { CALL(4); break; } \
   }
 
+#ifndef LDG_S2_PF
+#define LDG_S2_PF 0
+#endif
+__device__ __forceinline__ long Kp_of(const DevMesh& m) { return m.Kp; }
+
 __device__ __forceinline__ float comp(const float4& v, int r) {
   return r == 0 ? v.x : (r == 1 ? v.y : (r == 2 ? v.z : v.w));
 }
@@ -306,12 +311,27 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
   const float* s_pth = s_pe + 3 * Q * N;
   const float* s_we = s_pth + 9 * Q * N;
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
-  pdl_wait();
-  pdl_trigger();
   // elements [k0, kend): all of them (Jacobi, out != x) or one colour of the
   // bipartite FK element graph (red-black Gauss-Seidel, in place: an element
   // reads only the other colour's x)
   const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+#if LDG_S2_PF
+  // the static streams of this element (E, P^-1 do not change within a
+  // V-cycle) requested into L2 before waiting for the predecessor kernel, so
+  // the loads below find them there: bit 1 the P^-1 stream (read last),
+  // bit 2 E's second component.  Measured (V-cycle at 256^2, p = 2 / 3 / 4):
+  // bit 1 -1 / 0 / +3 %, bit 2 -1 / 0 / +1.5 %, both -1 / +2 / +5 %: off.
+  if (k < kend) {
+    if ((LDG_S2_PF & 1) && MODE == 1)
+      for (int q = 0; q < C::QP; ++q)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Pq + k + static_cast<long>(q) * Kp_of(m)));
+    if (LDG_S2_PF & 2)
+      for (int q = 0; q < C::QP; ++q)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Eq + static_cast<long>(C::QP + q) * Kp_of(m) + k));
+  }
+#endif
+  pdl_wait();
+  pdl_trigger();
   if (k >= kend) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
