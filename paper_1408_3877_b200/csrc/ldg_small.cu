@@ -15,7 +15,10 @@
 // Operands: E and P^-1 as FP32 SoA copies (E32, Pinv32), vectors FP64,
 // arithmetic FP64 (these levels are latency-bound; precision is free).
 // Reference operators as in ldg_apply.cu / ldg_rows.cu (assembly.hpp:76-208).
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <cstdlib>
 
 #include "ldg_internal.hpp"
 #include "ldg_offdiag.cuh"
@@ -290,7 +293,12 @@ struct TailArgs {
   int pre, post, coarse_min;
 };
 
-template <int P>
+// CL > 1: the same phases spread over a thread-block cluster of CL CTAs (one
+// per SM of a GPC), virtual blocks dealt round-robin, the phases separated by
+// cluster barriers (release/acquire at cluster scope, after a device fence
+// for the global-memory level data) instead of __syncthreads: CL SMs of
+// issue rate for the p >= 2 levels, still no launch between phases.
+template <int P, int CL>
 __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTables T) {
   using C = Cfg<P>;
   constexpr int N = C::N, NN = C::NN;
@@ -298,17 +306,28 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTabl
   pdl_wait();
   pdl_trigger();
   const int t = threadIdx.x;
+  int rank = 0;
+  if constexpr (CL > 1) rank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  const int gt = rank * blockDim.x + t, gstride = CL * blockDim.x;
+  auto bar = [&]() {
+    if constexpr (CL > 1) {
+      __threadfence();
+      cooperative_groups::this_cluster().sync();
+    } else {
+      __syncthreads();
+    }
+  };
   auto nvb = [](int K) { return (K + C::EPC - 1) / C::EPC; };
   auto zero = [&](const TailLevel& L, const double* b, double* out) {
-    for (int vb = 0; vb < nvb(L.m.K); ++vb) bj_body<P>(L.m.K, L.m.Kp, L.Pinv32, b, a.omega, out, vb, t);
-    __syncthreads();
+    for (int vb = rank; vb < nvb(L.m.K); vb += CL) bj_body<P>(L.m.K, L.m.Kp, L.Pinv32, b, a.omega, out, vb, t);
+    bar();
   };
   auto stage1 = [&](const TailLevel& L, const double* x) {
-    for (int vb = 0; vb < nvb(L.m.K); ++vb) s1_body<P>(L.m, T, x, L.tz, vb, t);
-    __syncthreads();
+    for (int vb = rank; vb < nvb(L.m.K); vb += CL) s1_body<P>(L.m, T, x, L.tz, vb, t);
+    bar();
   };
   auto stage2 = [&](const TailLevel& L, int mode, const double* x, const double* b, double* out) {
-    for (int vb = 0; vb < nvb(L.m.K); ++vb) {
+    for (int vb = rank; vb < nvb(L.m.K); vb += CL) {
       if (mode == 0)
         s2_body<P, 0>(L.m, T, L.E32, L.D, x, L.tz, b, a.wm, a.dteta, a.dt, L.Pinv32, a.omega, out, 0, L.m.K, s_r, vb,
                       t);
@@ -316,7 +335,7 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTabl
         s2_body<P, 1>(L.m, T, L.E32, L.D, x, L.tz, b, a.wm, a.dteta, a.dt, L.Pinv32, a.omega, out, 0, L.m.K, s_r, vb,
                       t);
     }
-    __syncthreads();
+    bar();
   };
   auto sweep = [&](const TailLevel& L, const double* xi, double* xo) {
     stage1(L, xi);
@@ -325,7 +344,7 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTabl
   // C.b = P^T F.r  (ldg_mg.cu k_restrict)
   auto restrict_ = [&](const TailLevel& F, const TailLevel& Cl) {
     const long Kpc = Cl.m.Kp, Kpf = F.m.Kp;
-    for (int it = t; it < N * Cl.m.K; it += blockDim.x) {
+    for (int it = gt; it < N * Cl.m.K; it += gstride) {
       const int kc = it % Cl.m.K, j = it / Cl.m.K;
       double acc = 0.0;
       for (int sl = 0; sl < 4; ++sl) {
@@ -336,12 +355,12 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTabl
       }
       Cl.b[j * Kpc + kc] = acc;
     }
-    __syncthreads();
+    bar();
   };
   // xf += P C.x  (ldg_mg.cu k_prolong_add)
   auto prolong = [&](const TailLevel& F, const TailLevel& Cl, double* xf) {
     const long Kpc = Cl.m.Kp, Kpf = F.m.Kp;
-    for (int it = t; it < 4 * N * Cl.m.K; it += blockDim.x) {
+    for (int it = gt; it < 4 * N * Cl.m.K; it += gstride) {
       const int kc = it % Cl.m.K, rest = it / Cl.m.K, sl = rest % 4, i = rest / 4;
       const int k = Cl.children[sl * Kpc + kc];
       const float* Ps = Cl.Pm + (static_cast<long>(sl) * NN + static_cast<long>(i) * N) * Kpc + kc;
@@ -350,7 +369,7 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTabl
       for (int j = 0; j < N; ++j) acc = fma(static_cast<double>(Ps[static_cast<long>(j) * Kpc]), Cl.x[j * Kpc + kc], acc);
       xf[i * Kpf + k] += acc;
     }
-    __syncthreads();
+    bar();
   };
 
   double* cur[kTailMax];
@@ -435,6 +454,41 @@ void small_zero(Handle& h, const double* b, double omega, double* out) {
 
 namespace ldgb {
 
+// CTAs of the tail kernel's cluster (LDG_TAIL_CLUSTER: 1, 4, 8 or 16).
+// Measured V-cycle at 256^2 (p = 0 / 2 / 4): one block 273 / 513 / 1437 us;
+// clusters of 8 or 16 on the same levels 292 / 525 / 1438 us (the cluster
+// barrier + fence per phase and the level data leaving the one SM's L1 cost
+// more than the extra issue rate buys); with the p >= 2 levels below 600 or
+// 2048 elements in the tail as well 295 / 542-573 / 1490-1595 us.  Off.
+int tail_cluster() {
+  static const int cl = [] {
+    const char* e = std::getenv("LDG_TAIL_CLUSTER");
+    const int v = e ? std::atoi(e) : 1;
+    return (v == 4 || v == 8 || v == 16) ? v : 1;
+  }();
+  return cl;
+}
+
+// one cluster of `cl` CTAs, programmatic stream serialisation as launch_pdl
+template <typename... KArgs, typename... Args>
+void launch_cluster(void (*kern)(KArgs...), int cl, int threads, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cl;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  LDG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // The V-cycle below level `top` (inclusive) of h's hierarchy in one block
 // (see k_tail); x of the top level receives the result, b its right-hand side.
 void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, int pre, int post, int coarse_min) {
@@ -466,7 +520,24 @@ void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, 
   a.post = post;
   a.coarse_min = coarse_min;
   const Handle& top_h = *h0.coarse[top - 1];  // all tail levels share its degree (p-coarsening, ldg_mg.cu)
-#define CALL(P) launch_pdl(k_tail<P>, 1, Cfg<P>::THREADS, 0, h0.stream, a, top_h.dtab)
+  const int cl = tail_cluster();
+#define CALL(P)                                                                                \
+  do {                                                                                         \
+    if (cl == 16) {                                                                            \
+      static bool np = false;                                                                  \
+      if (!np) {                                                                               \
+        LDG_CUDA(cudaFuncSetAttribute(k_tail<P, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
+        np = true;                                                                             \
+      }                                                                                        \
+      launch_cluster(k_tail<P, 16>, 16, Cfg<P>::THREADS, h0.stream, a, top_h.dtab);            \
+    } else if (cl == 8) {                                                                      \
+      launch_cluster(k_tail<P, 8>, 8, Cfg<P>::THREADS, h0.stream, a, top_h.dtab);              \
+    } else if (cl == 4) {                                                                      \
+      launch_cluster(k_tail<P, 4>, 4, Cfg<P>::THREADS, h0.stream, a, top_h.dtab);              \
+    } else {                                                                                   \
+      launch_pdl(k_tail<P, 1>, 1, Cfg<P>::THREADS, 0, h0.stream, a, top_h.dtab);               \
+    }                                                                                          \
+  } while (0)
   LDG_DISPATCH_P(top_h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
