@@ -295,8 +295,10 @@ void smooth_stage1(Handle& h, const double* x);                       // tz = M^
 // colour of the FK element graph (red-black Gauss-Seidel half-sweep)
 // cheb_beta != 0: Chebyshev step out <- x + omega P^-1 r + cheb_beta (x - out_old)
 // (out_old = x_{k-1}, taken as 0 when prev_zero)
+// fuse1 (p <= 1): stage 1 recomputed inside (no smooth_stage1 before it)
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, int k0 = 0, int kend = -1, double cheb_beta = 0.0, int prev_zero = 0);
+                   double* out, int k0 = 0, int kend = -1, double cheb_beta = 0.0, int prev_zero = 0,
+                   bool fuse1 = false);
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 // the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
 void small_stage1(Handle& h, const double* x);

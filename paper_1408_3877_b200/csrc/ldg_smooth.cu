@@ -223,6 +223,69 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
   }
 }
 
+// t^m_e = M_e^-1 B^m x of one element e (k_s1f's arithmetic, FP32), for the
+// fused p <= 1 sweep below: tb = the 14 m_hat^-1-premultiplied tables
+template <int P>
+__device__ __forceinline__ void s1_elem(const DevMesh& m, const float* tb, const double* __restrict__ x, int e,
+                                        float* t1, float* t2) {
+  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  float xv[N], w[N];
+  load_f<N>(x, Kp, e, xv);
+  const float b11 = static_cast<float>(g[kB11 * Kp + e]), b12 = static_cast<float>(g[kB12 * Kp + e]);
+  const float b21 = static_cast<float>(g[kB21 * Kp + e]), b22 = static_cast<float>(g[kB22 * Kp + e]);
+  ftab_mv<N, NF>(tb, xv, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    t1[i] = -b22 * w[i];
+    t2[i] = b12 * w[i];
+  }
+  ftab_mv<N, NF>(tb + TAB, xv, w);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    t1[i] = fmaf(b21, w[i], t1[i]);
+    t2[i] = fmaf(-b11, w[i], t2[i]);
+  }
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const int kind = m.kind[n * Kp + e];
+    const double len = g[(kLen0 + n) * Kp + e];
+    const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
+    if (f == 0.0) continue;
+    ftab_mv<N, NF>(tb + (2 + n) * TAB, xv, w);
+    const float c1 = static_cast<float>(f * g[(kNux0 + n) * Kp + e]);
+    const float c2 = static_cast<float>(f * g[(kNuy0 + n) * Kp + e]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      t1[i] = fmaf(c1, w[i], t1[i]);
+      t2[i] = fmaf(c2, w[i], t2[i]);
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const int nb = m.nbr[n * Kp + e];
+    if (nb < 0) continue;
+    float xn[N];
+    load_f<N>(x, Kp, nb, xn);
+    ftab_mv<N, NF>(tb + (5 + n * 3 + m.nbrn[n * Kp + e]) * TAB, xn, w);
+    const double hl = 0.5 * g[(kLen0 + n) * Kp + e];
+    const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + e]);
+    const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + e]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      t1[i] = fmaf(c1, w[i], t1[i]);
+      t2[i] = fmaf(c2, w[i], t2[i]);
+    }
+  }
+  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + e]));
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    t1[i] *= inv2a;
+    t2[i] *= inv2a;
+  }
+}
+
 // A quad of the packed stream: float4 (FP32 copy) or four FP16 values in a
 // uint2 (E scaled per element into [-1, 1], ldg_smooth.cu k_pack_e)
 __device__ __forceinline__ float4 ld_quad(const float4* p) { return __ldcs(p); }
@@ -293,7 +356,10 @@ __device__ __forceinline__ void pinv_apply(const TQ* __restrict__ Pk, long Kp, F
 // r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
-template <int P, int MODE, typename TQ, typename TP, typename TT>
+//   FUSE (p <= 1, one rank): t = M^-1 B x of the element and its neighbours
+//   recomputed here from x (s1_elem) instead of read from the stage-1 pass —
+//   the sweep is one launch instead of two (tz unused)
+template <int P, int MODE, typename TQ, typename TP, typename TT, bool FUSE = false>
 __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
                                              const double* x,
@@ -307,6 +373,7 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
   extern __shared__ __align__(16) float smf[];
   // tM | tSd 3 | tSo 9 | pe 3 | pth 9 | we (contiguous in the FP32 table buffer)
   const float* tb = stage_f(smf, T.fbase + T.fM, 13 * TAB + C::EDGE);
+  const float* tb1 = FUSE ? stage_f(smf + 13 * TAB + C::EDGE, T.fbase + T.fmH, 14 * TAB) : nullptr;
   const float* s_pe = tb + 13 * TAB;
   const float* s_pth = s_pe + 3 * Q * N;
   const float* s_we = s_pth + 9 * Q * N;
@@ -339,11 +406,18 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
 #pragma unroll
   for (int i = 0; i < N; ++i) acc[i] = 0.f;
   // diagonal blocks E^m_kk t^m_k (packed stream), scaled copy
+  if constexpr (FUSE) {
+    float t1[N], t2[N];
+    s1_elem<P>(m, tb1, x, k, t1, t2);
+    packed_apply<P, TQ>(Eq + k, Kp, [&](int j) { return t1[j]; }, acc);
+    packed_apply<P, TQ>(Eq + static_cast<long>(C::QP) * Kp + k, Kp, [&](int j) { return t2[j]; }, acc);
+  } else {
 #pragma unroll 1
-  for (int c = 0; c < 2; ++c) {
-    const TT* tc = tz + static_cast<long>(c) * N * Kp + k;
-    packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
-                        [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
+    for (int c = 0; c < 2; ++c) {
+      const TT* tc = tz + static_cast<long>(c) * N * Kp + k;
+      packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
+                          [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
+    }
   }
   if (Escale) {
     const float es = Escale[k];
@@ -359,13 +433,22 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
     const float co1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
     const float co2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
     float z[Q];
-    offdiag_z<N, Q, float>(
-        s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we,
-        [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
-        [&](int j) {
-          return fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
-        },
-        z);
+    if constexpr (FUSE) {
+      float u1[N], u2[N];
+      s1_elem<P>(m, tb1, x, kp, u1, u2);
+      offdiag_z<N, Q, float>(
+          s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we,
+          [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
+          [&](int j) { return fmaf(co1, u1[j], co2 * u2[j]); }, z);
+    } else {
+      offdiag_z<N, Q, float>(
+          s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we,
+          [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
+          [&](int j) {
+            return fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
+          },
+          z);
+    }
     offdiag_rows<N, Q, float>(s_pe + n * Q * N, z, 1.0f, acc);
   }
   const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
@@ -481,8 +564,8 @@ size_t s1_smem() {
   return sizeof(float) * 14 * Cfg<P>::N * Cfg<P>::NF;
 }
 template <int P>
-size_t s2_smem() {
-  return sizeof(float) * (13 * Cfg<P>::N * Cfg<P>::NF + Cfg<P>::EDGE);
+size_t s2_smem(bool fuse = false) {
+  return sizeof(float) * ((fuse ? 27 : 13) * Cfg<P>::N * Cfg<P>::NF + Cfg<P>::EDGE);
 }
 
 }  // namespace
@@ -558,15 +641,20 @@ void smooth_stage1(Handle& h, const double* x) {
 }
 
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, int k0, int kend, double cheb_beta, int prev_zero) {
+                   double* out, int k0, int kend, double cheb_beta, int prev_zero, bool fuse1) {
   const double dteta = dt * h.prob.eta;
   const float om = static_cast<float>(omega);
   const bool e16 = h.Eh.ptr != nullptr, p16 = h.Ph.ptr != nullptr;
   if (kend < 0) kend = h.K;
   const unsigned grid = grid_of(kend - k0, 128);
+  if (fuse1 && h.p > 2) throw Error(LDG_EINVAL, "fused stage 1 is for p <= 2");
 #define LAUNCH(P, M, TQ, EP, SC, TP, PP, PS)                                                                       \
   do {                                                                                                            \
-    if (h.tz32.ptr)                                                                                               \
+    if (fuse1)                                                                                                    \
+      launch_pdl(k_s2f<(P) <= 2 ? P : 2, M, TQ, TP, float, true>, grid, 128, s2_smem<(P) <= 2 ? P : 2>(true),     \
+                 h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, \
+                 kend, cheb_beta, prev_zero);                                                                     \
+    else if (h.tz32.ptr)                                                                                          \
       launch_pdl(k_s2f<P, M, TQ, TP, float>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,        \
                  h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend, cheb_beta, prev_zero);       \
     else                                                                                                          \

@@ -372,8 +372,30 @@ void f_zero(Handle& L, Vec b, Vec out) {
   }
 }
 
+// Optional (LDG_FUSE_S1 = highest fused degree, at most 2; default -1 = off):
+// thread-tier levels on one rank with stage 1 recomputed inside the stage-2
+// kernel for the element and its neighbours (k_s2f FUSE), one launch per
+// sweep instead of two.  Measured V-cycle at 256^2, p = 0 / 1 / 2 / 3: two
+// kernels 272 / 322 / 515 / 813 us, fused up to degree 1 338 / 469 / 598 /
+// 898 us (p = 2, 3 through their degree-1 level 1), up to degree 2 p = 2
+// 716 us: the dependent neighbour -> neighbour-geometry -> 2-hop x loads
+// cost more than the saved launch and t round trip.  Correct (tests pass
+// with it on), off.
+bool fuse_s1(Team& T, int l) {
+  static const int pmax = static_cast<int>(env_or("LDG_FUSE_S1", -1));  // highest fused degree, -1 none
+  if (pmax < 0 || T.size != 1 || T.nlocal() != 1) return false;
+  const Handle& L = level_of(T.h0(), l);
+  return tier(L) == kBig && L.p <= std::min(pmax, 2);
+}
+
 // r = b - S_c x (fused levels)
 void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
+  if (fuse_s1(T, l)) {
+    each(T, l, [&](Handle& L) {
+      smooth_stage2(L, 0, vp(L, x), vp(L, b), wm, dt, kOmega, vp(L, r), 0, -1, 0.0, 0, true);
+    });
+    return;
+  }
   halo(T, l, x, 1);
   each(T, l, [&](Handle& L) { f_stage1(L, x); });
   halo(T, l, kTz, 2);
@@ -382,6 +404,12 @@ void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
 
 // xo = xi + omega P^-1 (b - S_c xi) (fused levels)
 void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo) {
+  if (fuse_s1(T, l)) {
+    each(T, l, [&](Handle& L) {
+      smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, kOmega, vp(L, xo), 0, -1, 0.0, 0, true);
+    });
+    return;
+  }
   halo(T, l, xi, 1);
   each(T, l, [&](Handle& L) { f_stage1(L, xi); });
   halo(T, l, kTz, 2);
@@ -465,11 +493,14 @@ struct Cheb {
 
 void sweep_cheb(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo, double alpha, double beta,
                 bool prev_zero) {
-  halo(T, l, xi, 1);
-  each(T, l, [&](Handle& L) { f_stage1(L, xi); });
-  halo(T, l, kTz, 2);
+  const bool fuse = fuse_s1(T, l);
+  if (!fuse) {
+    halo(T, l, xi, 1);
+    each(T, l, [&](Handle& L) { f_stage1(L, xi); });
+    halo(T, l, kTz, 2);
+  }
   each(T, l, [&](Handle& L) {
-    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), 0, -1, beta, prev_zero ? 1 : 0);
+    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), 0, -1, beta, prev_zero ? 1 : 0, fuse);
   });
 }
 
