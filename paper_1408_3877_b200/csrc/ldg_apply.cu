@@ -29,6 +29,13 @@
 #else
 #define LDG_MINB_STAGE_P(P) ((P) == 4 ? 4 : ((P) == 3 ? 7 : 1))
 #endif
+// stage 2 alone at p = 4 (tuning builds): 5 / 6 / 7 CTAs measured Schur apply
+// 274 / 298 / 308 us against 238 us at 4
+#ifdef LDG_MINB_STAGE2_P4
+#define LDG_MINB_S2STAGE_P(P) ((P) == 4 ? LDG_MINB_STAGE2_P4 : LDG_MINB_STAGE_P(P))
+#else
+#define LDG_MINB_S2STAGE_P(P) LDG_MINB_STAGE_P(P)
+#endif
 
 namespace ldgb {
 
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1(DevMesh m, 
 // (the Krylov operator, FP64): stored diagonal blocks streamed, off-diagonal
 // blocks matrix-free from D.
 template <int P>
-__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage2(DevMesh m, DevTables T, const double* __restrict__ E,
+__global__ void __launch_bounds__(128, LDG_MINB_S2STAGE_P(P)) k_stage2(DevMesh m, DevTables T, const double* __restrict__ E,
                                                 const double* __restrict__ D, const double* __restrict__ x,
                                                 double alpha, double beta, const double* __restrict__ tz,
                                                 double gamma, const double* __restrict__ w, double delta,
