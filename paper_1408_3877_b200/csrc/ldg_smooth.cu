@@ -122,6 +122,79 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
   for (int j = 0; j < N; ++j) v[j] = static_cast<float>(x[j * Kp + col]);
 }
 
+// u1 += a * (T x), u2 += b * (T x) accumulated directly (no w temporary):
+// twice the FFMA2 of ftab_mv + combine, but 16 independent accumulator pairs
+// and 15 fewer live registers (tuning builds: LDG_S1_DIRECT = p).  Measured
+// V-cycle at 256^2: p = 2 / 3 / 4 +2.7 / +4.4 / +2.8 % (124 instead of 128
+// registers at p = 4, no spills): the extra FFMA2 issue outweighs the ILP.
+template <int N, int NF>
+__device__ __forceinline__ void ftab_acc2(const float* sT, const float* x, float a, float b, float2* u1,
+                                          float2* u2) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float4* row = reinterpret_cast<const float4*>(sT + j * NF);
+    const float2 xa = make_float2(a * x[j], a * x[j]), xb = make_float2(b * x[j], b * x[j]);
+#pragma unroll
+    for (int q = 0; q < NF / 4; ++q) {
+      const float4 t = row[q];
+      u1[2 * q] = __ffma2_rn(make_float2(t.x, t.y), xa, u1[2 * q]);
+      u2[2 * q] = __ffma2_rn(make_float2(t.x, t.y), xb, u2[2 * q]);
+      if (4 * q + 2 < N) {
+        u1[2 * q + 1] = __ffma2_rn(make_float2(t.z, t.w), xa, u1[2 * q + 1]);
+        u2[2 * q + 1] = __ffma2_rn(make_float2(t.z, t.w), xb, u2[2 * q + 1]);
+      }
+    }
+  }
+}
+
+#ifndef LDG_S1_DIRECT
+#define LDG_S1_DIRECT -1
+#endif
+template <int P, typename TT>
+__device__ __forceinline__ void s1f_direct(const DevMesh& m, const float* tb, const double* __restrict__ x, int k,
+                                           TT* __restrict__ tout) {
+  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  float2 u1[NF / 2], u2[NF / 2];
+#pragma unroll
+  for (int q = 0; q < NF / 2; ++q) u1[q] = u2[q] = make_float2(0.f, 0.f);
+  {
+    float xv[N];
+    load_f<N>(x, Kp, k, xv);
+    const float b11 = static_cast<float>(g[kB11 * Kp + k]), b12 = static_cast<float>(g[kB12 * Kp + k]);
+    const float b21 = static_cast<float>(g[kB21 * Kp + k]), b22 = static_cast<float>(g[kB22 * Kp + k]);
+    ftab_acc2<N, NF>(tb, xv, -b22, b12, u1, u2);
+    ftab_acc2<N, NF>(tb + TAB, xv, b21, -b11, u1, u2);
+#pragma unroll 1
+    for (int n = 0; n < 3; ++n) {
+      const int kind = m.kind[n * Kp + k];
+      const double len = g[(kLen0 + n) * Kp + k];
+      const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
+      if (f == 0.0) continue;
+      ftab_acc2<N, NF>(tb + (2 + n) * TAB, xv, static_cast<float>(f * g[(kNux0 + n) * Kp + k]),
+                       static_cast<float>(f * g[(kNuy0 + n) * Kp + k]), u1, u2);
+    }
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int nb = m.nbr[n * Kp + k];
+    if (nb < 0) continue;
+    float xn[N];
+    load_f<N>(x, Kp, nb, xn);
+    const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+    ftab_acc2<N, NF>(tb + (5 + n * 3 + m.nbrn[n * Kp + k]) * TAB, xn, static_cast<float>(hl * g[(kNux0 + n) * Kp + k]),
+                     static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]), u1, u2);
+  }
+  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float a1 = (i & 1) ? u1[i / 2].y : u1[i / 2].x, a2 = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
+    tout[i * Kp + k] = static_cast<TT>(inv2a * a1);
+    tout[(N + i) * Kp + k] = static_cast<TT>(inv2a * a2);
+  }
+}
+
 // tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
 template <int P, typename TT>
 __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
@@ -133,6 +206,10 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
   pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
+  if constexpr (P == LDG_S1_DIRECT) {
+    s1f_direct<P, TT>(m, tb, x, k, tout);
+    return;
+  }
   const long Kp = m.Kp;
   const double* g = m.geom;
   float xv[N], w[N], u1[N], u2[N];
