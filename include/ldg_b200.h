@@ -214,6 +214,14 @@ int ldg_l2_error(ldg_handle* h, int component, const ldg_coeff* exact, double t,
  * receives 3 or 6. */
 int ldg_to_lagrange(ldg_handle* h, int component, double* out, int* nodes);
 
+/* write_vtu (vtkout.hpp:42-108) of state component `component` (0 Z1, 1 Z2,
+ * 2 C): writes `<basename>.<t_lvl>.vtu` (ASCII VTK unstructured grid, every
+ * triangle its own 3 (p <= 1) or 6 points, the reference's file byte for
+ * byte) from the device-resident state; the path is copied to path_out
+ * (nullable, path_cap bytes).  One-process handles only. */
+int ldg_write_vtu(ldg_handle* h, int component, const char* var_name, const char* basename, int t_lvl,
+                  char* path_out, int path_cap);
+
 ldg_solver_opts ldg_default_solver_opts(void);
 
 /* nsteps implicit Euler steps of length dt (system.hpp:155-174), entirely on

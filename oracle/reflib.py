@@ -147,6 +147,25 @@ class RefMesh:
             self.h = None
 
 
+def write_vtu(h_max: float, lagrange, var_name: str, basename: str, t_lvl: int) -> str:
+    """The reference's write_vtu (vtkout.hpp:42-108) on domain_square(h_max),
+    run as oracle/_ref/ref_vtu (its iostreams cannot share this process with
+    numpy's libstdc++)."""
+    import subprocess
+    import tempfile
+
+    lag = np.ascontiguousarray(lagrange, dtype=np.float64)
+    with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as f:
+        f.write(lag.tobytes())
+        path = f.name
+    try:
+        res = subprocess.run([os.path.join(HERE, "_ref", "ref_vtu"), repr(float(h_max)), str(lag.shape[1]), path,
+                              var_name, basename, str(int(t_lvl))], capture_output=True, text=True, check=True)
+    finally:
+        os.unlink(path)
+    return res.stdout.strip()
+
+
 def ref_tensors(n: int) -> dict:
     arrs = dict(m=np.zeros(n * n), h=np.zeros(n * n * 2), g=np.zeros(n ** 3 * 2), sd=np.zeros(n * n * 3),
                 so=np.zeros(n * n * 9), rd=np.zeros(n ** 3 * 3), ro=np.zeros(n ** 3 * 9))

@@ -15,6 +15,7 @@ Reference interface -> this module
   initial_state / euler_step           LdgSystem.initial_state / euler_step
   solve_stationary                     LdgSystem.solve_stationary
   l2_error / to_lagrange (fields.hpp)  LdgSystem.l2_error / to_lagrange
+  write_vtu (vtkout.hpp)               LdgSystem.write_vtu
 Exceptions follow the reference: ValueError for std::invalid_argument,
 MeshError for ldg::MeshError, RuntimeError for solver failures.
 """
@@ -122,6 +123,7 @@ _SIGNATURES = {
     "ldg_solve_stationary": (C.c_int, [_H, C.c_double, C.POINTER(_Opts), C.POINTER(_Stats)]),
     "ldg_l2_error": (C.c_int, [_H, C.c_int, C.POINTER(_Coeff), C.c_double, C.c_int, _dp]),
     "ldg_to_lagrange": (C.c_int, [_H, C.c_int, _dp, C.POINTER(C.c_int)]),
+    "ldg_write_vtu": (C.c_int, [_H, C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p, C.c_int]),
     "ldg_apply_lhs": (C.c_int, [_H, C.c_double, _dp, _dp]),
     "ldg_time_kernels": (C.c_int, [_H, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(_Times)]),
     "ldg_sync": (C.c_int, [_H]),
@@ -471,6 +473,14 @@ class LdgSystem:
         self._check(load_library().ldg_l2_error(self._h, self._COMPONENTS[component], C.byref(c), float(t),
                                                 int(q_ord), C.byref(err)))
         return err.value
+
+    def write_vtu(self, component: str = "c", var_name: str = "u", basename: str = "out", t_lvl: int = 0) -> str:
+        """write_vtu (vtkout.hpp:42-108) of a state component from the device;
+        returns the path `<basename>.<t_lvl>.vtu`."""
+        buf = C.create_string_buffer(4096)
+        self._check(load_library().ldg_write_vtu(self._h, self._COMPONENTS[component], var_name.encode(),
+                                                 basename.encode(), int(t_lvl), buf, 4096))
+        return buf.value.decode()
 
     def to_lagrange(self, component: str = "c") -> np.ndarray:
         """to_lagrange(dof) (fields.hpp:87-97) of a state component -> K x 3 (p <= 1) or K x 6."""

@@ -542,6 +542,108 @@ int ldg_to_lagrange(ldg_handle* H, int component, double* out, int* nodes) {
   });
 }
 
+// write_vtu (vtkout.hpp:42-108) of a state component: the Lagrange samples
+// come from the device (to_lagrange above), the affine maps from the device
+// geometry (B_k, a_k1, bit-identical with mesh.hpp's lists); the file is the
+// reference's byte for byte (map_to_physical's arithmetic order,
+// mesh.hpp:64-68, and printf %.3e), assembled in memory and written once.
+int ldg_write_vtu(ldg_handle* H, int component, const char* var_name, const char* basename, int t_lvl,
+                  char* path_out, int path_cap) {
+  if (!H || !var_name || !basename) return LDG_EINVAL;
+  return guarded(H, [&] {
+    Team& T = H->team;
+    if (T.size != 1) throw Error(LDG_EINVAL, "write_vtu: one process holds the whole mesh (gather first)");
+    int M = 0;
+    const long Kglob = T.h0().Kglobal;
+    std::vector<double> lag(static_cast<size_t>(Kglob) * 6);
+    const int rc = ldg_to_lagrange(H, component, lag.data(), &M);
+    if (rc != LDG_OK) throw Error(rc, T.err);
+    std::vector<double> geo(6L * Kglob);  // b11 b12 b21 b22 a1x a1y per global element
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      const long Kp = h.Kp;
+      std::vector<double> g(static_cast<size_t>(ldgb::kGeomCount) * Kp);
+      LDG_CUDA(cudaMemcpy(g.data(), h.geom.ptr, sizeof(double) * g.size(), cudaMemcpyDeviceToHost));
+      for (int k = 0; k < h.K; ++k) {
+        double* o = geo.data() + 6L * h.gid[k];
+        o[0] = g[ldgb::kB11 * Kp + k];
+        o[1] = g[ldgb::kB12 * Kp + k];
+        o[2] = g[ldgb::kB21 * Kp + k];
+        o[3] = g[ldgb::kB22 * Kp + k];
+        o[4] = g[ldgb::kA1x * Kp + k];
+        o[5] = g[ldgb::kA1y * Kp + k];
+      }
+    }
+    static const double l1[6] = {0.0, 1.0, 0.0, 0.5, 0.0, 0.5};
+    static const double l2[6] = {0.0, 0.0, 1.0, 0.5, 0.5, 0.0};
+    static const int perm3[3] = {0, 1, 2}, perm6[6] = {0, 1, 2, 5, 3, 4};
+    const int* perm = M == 3 ? perm3 : perm6;
+    const int cell_type = M == 3 ? 5 : 22;
+    std::string out;
+    out.reserve(static_cast<size_t>(Kglob) * M * 64 + 4096);
+    char buf[96];
+    auto e3 = [&](double v) {
+      const int n = std::snprintf(buf, sizeof(buf), "%.3e", v);
+      out.append(buf, static_cast<size_t>(n));
+    };
+    out += "<?xml version=\"1.0\"?>\n<VTKFile type=\"UnstructuredGrid\" version=\"0.1\" "
+           "byte_order=\"LittleEndian\" compressor=\"vtkZLibDataCompressor\">\n  <UnstructuredGrid>\n";
+    out += "    <Piece NumberOfPoints=\"" + std::to_string(Kglob * M) + "\" NumberOfCells=\"" +
+           std::to_string(Kglob) + "\">\n      <Points>\n"
+           "        <DataArray type=\"Float32\" NumberOfComponents=\"3\" format=\"ascii\">\n";
+    for (long k = 0; k < Kglob; ++k) {
+      const double* o = geo.data() + 6 * k;
+      for (int i = 0; i < M; ++i) {
+        const double x1 = l1[perm[i]], x2 = l2[perm[i]];
+        volatile double p0 = o[0] * x1, p1 = o[1] * x2, p2 = o[2] * x1, p3 = o[3] * x2;  // no contraction
+        volatile double s0 = p0 + p1, s1 = p2 + p3;
+        out += "          ";
+        e3(s0 + o[4]);
+        out += ' ';
+        e3(s1 + o[5]);
+        out += ' ';
+        e3(0.0);
+        out += '\n';
+      }
+    }
+    out += "        </DataArray>\n      </Points>\n      <Cells>\n"
+           "        <DataArray type=\"Int32\" Name=\"connectivity\" format=\"ascii\">\n          ";
+    for (long i = 0; i < Kglob * M; ++i) {
+      out += std::to_string(i);
+      out += ' ';
+    }
+    out += "\n        </DataArray>\n        <DataArray type=\"Int32\" Name=\"offsets\" format=\"ascii\">\n          ";
+    for (long k = 1; k <= Kglob; ++k) {
+      out += std::to_string(k * M);
+      out += ' ';
+    }
+    out += "\n        </DataArray>\n        <DataArray type=\"UInt8\" Name=\"types\" format=\"ascii\">\n          ";
+    const std::string ct = std::to_string(cell_type) + " ";
+    for (long k = 0; k < Kglob; ++k) out += ct;
+    out += "\n        </DataArray>\n      </Cells>\n      <PointData Scalars=\"";
+    out += var_name;
+    out += "\">\n        <DataArray type=\"Float32\" Name=\"";
+    out += var_name;
+    out += "\" NumberOfComponents=\"1\" format=\"ascii\">\n";
+    for (long k = 0; k < Kglob; ++k) {
+      out += "          ";
+      for (int i = 0; i < M; ++i) {
+        e3(lag[static_cast<size_t>(k) * M + perm[i]]);
+        out += ' ';
+      }
+      out += '\n';
+    }
+    out += "        </DataArray>\n      </PointData>\n    </Piece>\n  </UnstructuredGrid>\n</VTKFile>\n";
+    const std::string path = std::string(basename) + "." + std::to_string(t_lvl) + ".vtu";
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw Error(LDG_EINVAL, "cannot write " + path);
+    const size_t w = std::fwrite(out.data(), 1, out.size(), f);
+    const int cl = std::fclose(f);
+    if (w != out.size() || cl != 0) throw Error(LDG_EINVAL, "write failure on " + path);
+    if (path_out && path_cap > 0) std::snprintf(path_out, static_cast<size_t>(path_cap), "%s", path.c_str());
+  });
+}
+
 int ldg_assemble(ldg_handle* H, double t) {
   if (!H) return LDG_EINVAL;
   return guarded(H, [&] {

@@ -190,6 +190,17 @@ class LdgSystem {
     return e;
   }
 
+  /// write_vtu (vtkout.hpp:42-108) of a state component (2 = C) from the
+  /// device-resident state; returns the written path.
+  std::string write_vtu(int component, const std::string& var_name, const std::string& basename,
+                        int t_lvl) const {
+    char path[4096];
+    detail::check(ldg_write_vtu(h_.get(), component, var_name.c_str(), basename.c_str(), t_lvl, path,
+                                static_cast<int>(sizeof(path))),
+                  h_.get());
+    return path;
+  }
+
   /// to_lagrange(dof) (fields.hpp:87-97) of a state component: K x 3 (p <= 1)
   /// or K x 6, k-major; *nodes receives the column count.
   std::vector<double> to_lagrange(int component = 2, int* nodes = nullptr) const {

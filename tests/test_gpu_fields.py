@@ -139,3 +139,26 @@ def test_convergence_order_on_device(p, ld, golden):
     alphas = [math.log(a / b) / math.log(2.0) for a, b in zip(errs, errs[1:])]
     target = 0.0 if p == 0 else p + 1.0
     assert abs(alphas[-1] - target) <= ORDER_TOL[p], (p, alphas)
+
+
+@pytest.mark.parametrize("p,jitter", [(1, 0.0), (2, 0.0), (3, 0.2)])
+def test_write_vtu_matches_reference_writer(p, jitter, ld, tmp_path):
+    """ldg_write_vtu (vtkout.hpp:42-108) from the device state: the file equals,
+    byte for byte, what the oracle's write_vtu restatement (itself pinned to the
+    reference writer in tests/test_oracle.py) writes for the same mesh and the
+    device's own Lagrange samples; the samples match the oracle's to_lagrange."""
+    s = ld.LdgSystem.square(6, p, ld.BASELINE_SPEC, jitter=jitter, seed=0)
+    s.initial_state()
+    s.euler_steps(0.05, 1, ld.SolverOptions(rtol=1e-14))
+    y, _ = s.get_state()
+    kn = s.block_dim
+    m = _oracle_mesh(s)
+    for comp, sl in (("c", slice(2 * kn, 3 * kn)), ("z2", slice(kn, 2 * kn))):
+        path = s.write_vtu(comp, comp, str(tmp_path / f"dev_{comp}"), 7)
+        assert path.endswith(f"dev_{comp}.7.vtu")
+        lag = s.to_lagrange(comp)
+        ref = O.write_vtu(m, lag, comp, str(tmp_path / f"ora_{comp}"), 7)
+        assert open(path).read() == open(ref).read(), (p, comp)
+        dof = y[sl].reshape(s.num_t, s.n)
+        np.testing.assert_allclose(lag, O.to_lagrange(dof), rtol=0, atol=1e-13 * np.abs(dof).max())
+    s.close()

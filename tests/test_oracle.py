@@ -7,6 +7,8 @@ against the Eigen shim (tests/golden/make_golden.py).  No GPU needed.
 """
 from __future__ import annotations
 
+import os
+
 import math
 
 import numpy as np
@@ -285,3 +287,19 @@ def test_convergence_ladder_matches_golden(golden):
     fin = ref[(ref[:, 1] == 3) & (ref[:, 0] >= 2)]
     for p, alpha in zip(fin[:, 0], fin[:, 5]):
         assert abs(alpha - (p + 1.0)) <= 0.25, (p, alpha)
+
+
+@pytest.mark.parametrize("h_max,m", [(0.25, 3), (0.5, 6), (1.0 / 3.0, 6)])
+def test_write_vtu_restatement_matches_reference(h_max, m, tmp_path):
+    """The oracle's write_vtu (vtkout.hpp:42-108) writes the reference's file
+    byte for byte (the reference writer runs as oracle/_ref/ref_vtu)."""
+    from oracle import reflib as R
+
+    if not os.path.exists(os.path.join(os.path.dirname(R.LIB_PATH), "ref_vtu")):
+        pytest.skip("oracle/_ref/ref_vtu not built (make -C oracle)")
+    mesh = O.domain_square(h_max)
+    rng = np.random.default_rng(7)
+    lag = rng.standard_normal((mesh.num_t, m)) * 10.0 ** rng.integers(-6, 6, (mesh.num_t, m))
+    a = R.write_vtu(h_max, lag, "c", str(tmp_path / "ref"), 2)
+    b = O.write_vtu(mesh, lag, "c", str(tmp_path / "ora"), 2)
+    assert open(a).read() == open(b).read()
