@@ -234,11 +234,19 @@ def test_cpp_host_mirror_simulate(ld):
     import os
     import subprocess
 
+    import tempfile
+
     sim = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "ldg_simulate")
-    for extra in ([], ["--device-resident"]):
-        r = subprocess.run([sim, "16", "1", "10", "1.0"] + extra, capture_output=True, text=True, timeout=300)
-        assert r.returncode == 0, r.stderr
-        assert "simulate: 10 steps" in r.stdout
+    for extra in (["--host"], ["--device-resident"]):
+        with tempfile.TemporaryDirectory() as d:
+            base = os.path.join(d, "c")
+            r = subprocess.run([sim, "16", "1", "10", "1.0"] + extra + [base, "5"], capture_output=True, text=True,
+                               timeout=300)
+            assert r.returncode == 0, r.stderr
+            assert "simulate: 10 steps" in r.stdout
+            # the reference's output cadence (ldg_main.cpp:195-207): step 0, then every output_every steps
+            assert sorted(os.listdir(d)) == ["c.0.vtu", "c.10.vtu", "c.5.vtu"]
+            assert open(base + ".10.vtu").read().count("\n") > 3 * 512
 
 
 def test_consecutive_handles_fp16_smoother(ld):

@@ -1,8 +1,11 @@
 // The time loop of the reference CLI's `simulate` (proj/tools/ldg_main.cpp:
 // 174-222) on the B200 path, through the C++ host mirror: build the system,
-// project c0, run num_steps implicit-Euler steps, print per-step timing.
+// project c0, run num_steps implicit-Euler steps, print per-step timing, and
+// (with a basename) write `<basename>.<step>.vtu` of c at step 0 and every
+// output_every steps (ldg_main.cpp:195-207, write_vtu of to_lagrange(c)).
 //
-//   ldg_simulate [dim=32] [p=2] [num_steps=20] [t_end=1] [--device-resident]
+//   ldg_simulate [dim=32] [p=2] [num_steps=20] [t_end=1] [--device-resident|--host]
+//                [basename] [output_every=1]
 //
 // The problem is the BASELINE.json one (c = cos7x1 cos7x2 + e^-t,
 // d = e^(x1+x2)(1 + 0.5 sin t), f derived, Dirichlet on all sides).
@@ -13,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <iostream>
+#include <string>
 
 #include "ldg_host.hpp"
 
@@ -23,6 +27,8 @@ int main(int argc, char** argv) {
   int num_steps = argc > 3 ? std::atoi(argv[3]) : 20;
   double t_end = argc > 4 ? std::atof(argv[4]) : 1.0;
   bool resident = argc > 5 && std::strcmp(argv[5], "--device-resident") == 0;
+  const std::string basename = argc > 6 ? argv[6] : "";
+  const int output_every = argc > 7 ? std::atoi(argv[7]) : 1;
   try {
     lb::ProblemSpec spec;
     spec.d = lb::coeff(LDG_FN_BASE_D);
@@ -35,6 +41,7 @@ int main(int argc, char** argv) {
     if (num_steps < 1) throw std::runtime_error("num_steps must be at least 1");
     lb::LdgSystem sys = lb::LdgSystem::square(dim, p, spec);
     lb::SystemState state = sys.initial_state();
+    if (!basename.empty()) sys.write_vtu(2, "c", basename, 0);
     const double dt = t_end / num_steps;
     const auto wall_start = std::chrono::steady_clock::now();
     for (int step = 1; step <= num_steps; ++step) {
@@ -49,6 +56,8 @@ int main(int argc, char** argv) {
       }
       const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       std::printf("step %d/%d  t = %g  (%g ms)\n", step, num_steps, state.t, ms);
+      if (!basename.empty() && output_every > 0 && step % output_every == 0)
+        std::printf("  wrote %s\n", sys.write_vtu(2, "c", basename, step).c_str());
     }
     const double total =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_start).count();
