@@ -460,7 +460,11 @@ bool cheb_on() {
   return on;
 }
 const double kChebRatio = env_or("LDG_MG_CHEB_RATIO", 20.0);
-const double kChebSafety = env_or("LDG_MG_CHEB_SAFETY", 1.15);
+// upper end of the interval = safety x the power-iteration estimate: 1.08
+// (5-step C2 bench: 1.15 p = 2 15.4 iterations / 11.2 ms, 1.05 and 1.08
+// 15.0 / 10.9 ms, other degrees unchanged; 1.0 diverges towards 21
+// iterations at p = 0).  Ratio 20 (10: p = 4 20 iterations; 30: +1 at p <= 3).
+const double kChebSafety = env_or("LDG_MG_CHEB_SAFETY", 1.08);
 const int kChebPower = static_cast<int>(env_or("LDG_MG_CHEB_POWER", 30));  // power iterations
 const int kChebLevels = static_cast<int>(env_or("LDG_MG_CHEB_LEVELS", 1));
 bool cheb_level(Team& T, int l) {

@@ -4,7 +4,7 @@ IFS=';' read -ra LIST <<< "$ENVS"
 for E in "${LIST[@]}"; do
   echo "== $E"
   env $E timeout 300 python scripts/mg_times.py 256 ${MGP:-2,4} | grep -v "^$"
-  env $E timeout 600 python bench.py --steps 2 --warmup 2 --no-cpu-baseline ${BARGS:-} > gpurun_out/bench_envs.log 2>&1
+  env $E timeout 600 python bench.py --steps ${BSTEPS:-2} --warmup 2 --no-cpu-baseline ${BARGS:-} > gpurun_out/bench_envs.log 2>&1
   python - <<'PY'
 import json
 for line in open('gpurun_out/bench_envs.log'):
