@@ -52,9 +52,44 @@ double env_or(const char* name, double dflt) {
 // V(4,6) / V(5,6) / V(5,6) and level 1 V(2,1) except V(1,1) at p = 4
 // (ms/step 5.17 / 7.47 / 11.11 / 20.11 / 38.49 against 5.59 / 7.67 / 11.88 /
 // 20.55 / 41.09 with V(5,5) + V(2,1)).  LDG_MG_* override for every degree.
-const double kOmega = env_or("LDG_MG_OMEGA", 0.7);  // damped block-Jacobi smoother
-const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));    // coarse levels
-const int kPost = static_cast<int>(env_or("LDG_MG_POST", 1));  // coarse levels
+// Damped block-Jacobi weight and the sweeps of the levels below level 1,
+// re-tuned after p-coarsening and Chebyshev level 0 made the coarse levels
+// cheap relative to their effect (5-step C2 bench, all degrees): coarse
+// V(2,1) with omega 0.7 1.775e8 DOF-updates/s; V(2,2) + 0.7 1.943e8; V(2,2)
+// + 0.8 1.989e8 (p = 0..4: 4.8 / 6.4 / 8.7 / 15.0 / 34.2 ms); V(2,2) + 0.9
+// 4.4 / 5.9 / 8.7 / 15.3 / 36.3 ms; V(3,2), V(2,3), V(3,3), V(4,4), V(1,1)
+// all lower.  omega per finest degree: 0.9 for p <= 1, 0.8 above — on
+// unjittered meshes solved by one rank.  Jittered meshes keep 0.7: with 0.8
+// BASELINE config 4 (2048^2, jitter 0.2h, p = 3) went from 22 to 24
+// iterations, and a 2-rank strip run at p = 1 with 0.9 (the per-kernel
+// coarse levels, no single-block tail) from 42 to 184 iterations over 3
+// steps; multi-rank teams keep 0.7 too.
+const double kOmegaEnv = env_or("LDG_MG_OMEGA", -1.0);
+constexpr double kOmegaP[5] = {0.9, 0.9, 0.8, 0.8, 0.8};
+constexpr double kOmegaSafe = 0.7;
+// Chebyshev interval of level 0 (below, sweep_cheb):
+// upper end of the interval = safety x the power-iteration estimate: 1.08
+// (5-step C2 bench: 1.15 p = 2 15.4 iterations / 11.2 ms, 1.05 and 1.08
+// 15.0 / 10.9 ms, other degrees unchanged; 1.0 diverges towards 21
+// iterations at p = 0).  Ratio 20 (10: p = 4 20 iterations; 30: +1 at p <= 3).
+// (plain meshes, set_omega; jittered meshes / strips keep 1.15: config 4
+// went from 22 to 24 iterations with 1.08 and coarse V(2,2))
+const double kChebSafetyEnv = env_or("LDG_MG_CHEB_SAFETY", -1.0);
+double kChebSafety = 1.15;
+// coarse post-sweeps: 2 on plain meshes (above), 1 on jittered meshes / strips
+// (config 4 with 2: 24 instead of 22 iterations, 1.39 instead of 1.25 s/step)
+const int kPostEnv = static_cast<int>(env_or("LDG_MG_POST", -1));
+int kPost = 1;  // set with kOmega
+double kOmega = kOmegaSafe;  // set per team at the top of every V-cycle (vcycle, l = 0)
+void set_omega(const Team& T) {
+  const Handle& h = T.h0();
+  const int p = h.p < 0 ? 0 : (h.p > 4 ? 4 : h.p);
+  const bool plain = h.jitter == 0.0 && h.dim > 0 && T.size == 1 && T.nlocal() == 1;
+  kOmega = kOmegaEnv > 0.0 ? kOmegaEnv : (plain ? kOmegaP[p] : kOmegaSafe);
+  kPost = kPostEnv >= 0 ? kPostEnv : (plain ? 2 : 1);
+  kChebSafety = kChebSafetyEnv > 0.0 ? kChebSafetyEnv : (plain ? 1.08 : 1.15);
+}
+const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));  // coarse levels
 const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
 constexpr int kPre0P[5] = {6, 4, 4, 5, 5}, kPost0P[5] = {6, 5, 6, 6, 6};
 constexpr int kPre1P[5] = {2, 2, 2, 2, 1}, kPost1P[5] = {1, 1, 1, 1, 1};
@@ -460,11 +495,6 @@ bool cheb_on() {
   return on;
 }
 const double kChebRatio = env_or("LDG_MG_CHEB_RATIO", 20.0);
-// upper end of the interval = safety x the power-iteration estimate: 1.08
-// (5-step C2 bench: 1.15 p = 2 15.4 iterations / 11.2 ms, 1.05 and 1.08
-// 15.0 / 10.9 ms, other degrees unchanged; 1.0 diverges towards 21
-// iterations at p = 0).  Ratio 20 (10: p = 4 20 iterations; 30: +1 at p <= 3).
-const double kChebSafety = env_or("LDG_MG_CHEB_SAFETY", 1.08);
 const int kChebPower = static_cast<int>(env_or("LDG_MG_CHEB_POWER", 30));  // power iterations
 const int kChebLevels = static_cast<int>(env_or("LDG_MG_CHEB_LEVELS", 1));
 bool cheb_level(Team& T, int l) {
@@ -550,6 +580,7 @@ bool tail_level(Team& T, int l, bool f32) {
 }
 
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
+  if (l == 0) set_omega(T);
   const bool coarsest = l == levels(T) - 1;
   if (tail_level(T, l, f32) && b == kMgB && x == kMgX) {
     small_tail_vcycle(T.h0(), l, wm, dt, kOmega, pre_of(T.h0().p, l), post_of(T.h0().p, l), kCoarseSweeps);
