@@ -92,7 +92,10 @@ void set_omega(const Team& T) {
 const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));  // coarse levels
 const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
 constexpr int kPre0P[5] = {6, 4, 4, 5, 5}, kPost0P[5] = {6, 5, 6, 6, 6};
-constexpr int kPre1P[5] = {2, 2, 2, 2, 1}, kPost1P[5] = {1, 1, 1, 1, 1};
+// level 1 V(1,1) except V(2,1) at p = 3 (with the retuned coarse levels:
+// p = 0..2 4.3 / 5.8 / 8.5 ms against 4.4 / 5.9 / 8.7 with V(2,1); V(2,2),
+// V(3,2) slower)
+constexpr int kPre1P[5] = {1, 1, 1, 2, 1}, kPost1P[5] = {1, 1, 1, 1, 1};
 int sweeps_of(const char* env, const int* table, int p) {
   const char* s = std::getenv(env);
   return s ? std::atoi(s) : table[p < 0 ? 0 : (p > 4 ? 4 : p)];
