@@ -91,7 +91,11 @@ void set_omega(const Team& T) {
 }
 const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));  // coarse levels
 const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
-constexpr int kPre0P[5] = {6, 4, 4, 5, 5}, kPost0P[5] = {6, 5, 6, 6, 6};
+// level 0 re-swept with the retuned coarse levels (5-step C2 bench): p = 1
+// V(5,6) 5.6 ms / 10 iterations (V(4,5) 5.8 / 11), p = 4 V(5,7) 33.7 / 15
+// (V(5,6) 34.2 / 16); p = 0, 2, 3 unchanged (V(4,4), V(3,5), V(4,5),
+// V(6,6) elsewhere all slower; symmetric counts lose up to 2x at p = 3).
+constexpr int kPre0P[5] = {6, 5, 4, 5, 5}, kPost0P[5] = {6, 6, 6, 6, 7};
 // level 1 V(1,1) except V(2,1) at p = 3 (with the retuned coarse levels:
 // p = 0..2 4.3 / 5.8 / 8.5 ms against 4.4 / 5.9 / 8.7 with V(2,1); V(2,2),
 // V(3,2) slower)
