@@ -517,8 +517,9 @@ def run_ours(args):
                        "parallelism": f"strips{world} (NCCL halos + allreduce)" if world > 1 else "single",
                        "l2": "flushed (256 MB write) before every timed step; p>=2 working sets exceed L2",
                        "solver": "FGMRES(30) on the exact Schur complement, p-coarsened geometric multigrid (level 0 "
-                                 "Chebyshev/block-Jacobi V(6,6)/V(4,5)/V(4,6)/V(5,6)/V(5,6) for p=0..4, "
-                                 "mixed-precision smoother), reference residual contract 1e-10",
+                                 "Chebyshev V(6,6)/V(5,6)/V(4,6)/V(5,6)/V(5,7) for p=0..4, coarse levels "
+                                 "damped block-Jacobi, mixed-precision smoother), reference residual "
+                                 "contract 1e-10",
                        "per_p": {str(p): {"ms_per_step": per_p[p]["ms"] / args.steps,
                                           "ms_assemble": per_p[p]["ms_asm"] / args.steps,
                                           "ms_solve": per_p[p]["ms_solve"] / args.steps,
