@@ -125,6 +125,7 @@ _SIGNATURES = {
     "ldg_to_lagrange": (C.c_int, [_H, C.c_int, _dp, C.POINTER(C.c_int)]),
     "ldg_write_vtu": (C.c_int, [_H, C.c_int, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p, C.c_int]),
     "ldg_apply_lhs": (C.c_int, [_H, C.c_double, _dp, _dp]),
+    "ldg_apply_schur": (C.c_int, [_H, C.c_double, _dp, _dp]),
     "ldg_time_kernels": (C.c_int, [_H, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(_Times)]),
     "ldg_sync": (C.c_int, [_H]),
 }
@@ -229,7 +230,7 @@ BASELINE_SPEC = ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn",
 
 @dataclass
 class SolverOptions:
-    rtol: float = 0.0
+    rtol: float = 1e-14  # ldg_default_solver_opts(): relative Schur residual (states within 1e-10 of the reference)
     atol: float = 0.0
     maxit: int = 20000
     precond: int = 2  # 0 none, 1 block-Jacobi, 2 geometric multigrid (p-coarsened, FK meshes; else 1)
@@ -496,6 +497,16 @@ class LdgSystem:
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.zeros_like(x)
         self._check(load_library().ldg_apply_lhs(self._h, float(dt), _d(x), _d(y)))
+        return y
+
+    def apply_schur(self, dt: float, c) -> np.ndarray:
+        """S_c c = [M + dt(eta(S + S_D) - sum_m E^m M^-1 B^m)] c (KN vector) with the
+        operators of the last assemble: the Krylov solve's operator."""
+        c = np.ascontiguousarray(c, dtype=np.float64)
+        if c.size != self.block_dim:
+            raise ValueError("vector length does not match K*N")
+        y = np.zeros_like(c)
+        self._check(load_library().ldg_apply_schur(self._h, float(dt), _d(c), _d(y)))
         return y
 
     def time_kernels(self, t: float, dt: float, reps: int = 10, flush: bool = True) -> dict:

@@ -330,7 +330,10 @@ int ldg_nccl_unique_id(char* out) {
 
 ldg_solver_opts ldg_default_solver_opts(void) {
   ldg_solver_opts o;
-  o.rtol = 0.0;
+  // relative Schur residual 1e-14: states within 1e-10 (relative L2) of the
+  // reference's direct solve at the BASELINE sizes (scripts/tol_study.py,
+  // tests/test_gpu_parity_scale.py); the contract alone left up to 6e-10 at 256^2
+  o.rtol = 1e-14;
   o.atol = 0.0;
   o.maxit = 20000;
   o.precond = 2;
@@ -974,6 +977,25 @@ int ldg_apply_lhs(ldg_handle* H, double dt, const double* x, double* y) {
     scatter_from_host(T, x, 3, [](Handle& h) { return h.Y.ptr; });
     ldgb::team_full_apply(T, 1.0, dt);
     gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.full_y.ptr); }, 3, y);
+    for (auto& rp : T.ranks)
+      LDG_CUDA(cudaMemcpyAsync(rp->Y.ptr, rp->Yold.ptr, sizeof(double) * 3 * rp->vec_len(), cudaMemcpyDeviceToDevice,
+                               T.stream));
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+  });
+}
+
+int ldg_apply_schur(ldg_handle* H, double dt, const double* c, double* y) {
+  if (!H || !c || !y) return LDG_EINVAL;
+  return guarded(H, [&] {
+    Team& T = H->team;
+    require_assembled(T);
+    ensure_solver(T);
+    for (auto& rp : T.ranks)
+      LDG_CUDA(cudaMemcpyAsync(rp->Yold.ptr, rp->Y.ptr, sizeof(double) * 3 * rp->vec_len(), cudaMemcpyDeviceToDevice,
+                               T.stream));
+    scatter_from_host(T, c, 1, [](Handle& h) { return h.Y.ptr + 2 * h.vec_len(); });
+    ldgb::team_schur_apply_c(T, 1.0, dt);
+    gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.kr_v.ptr); }, 1, y);
     for (auto& rp : T.ranks)
       LDG_CUDA(cudaMemcpyAsync(rp->Y.ptr, rp->Yold.ptr, sizeof(double) * 3 * rp->vec_len(), cudaMemcpyDeviceToDevice,
                                T.stream));

@@ -270,6 +270,23 @@ def test_oracle_euler_matches_golden(case, golden):
             assert np.linalg.norm(y - ref) / np.linalg.norm(ref) <= 1e-12
 
 
+@pytest.mark.parametrize("case", ["c1_fk16_p1", "jitter8_p2", "fk8_p0", "fk8_p3", "fk6_p4"])
+def test_oracle_schur_euler_matches_reference_lu(case, golden):
+    """The exact block-elimination solve (euler_step_schur, the 64^2 parity
+    oracle) reproduces the reference's SparseLU states (golden fixtures)."""
+    g = golden(case)
+    _, s = _oracle_system(g)
+    y, t = s.initial_state()
+    dt = float(g["dt"])
+    steps = sorted(int(k[1:]) for k in g if k.startswith("y") and k[1:].isdigit() and k != "y0")
+    last = min(steps[-1], 10)
+    for i in range(1, last + 1):
+        y, t = s.euler_step_schur(y, t, dt)
+        if i in steps:
+            ref = g[f"y{i}"]
+            assert np.linalg.norm(y - ref) / np.linalg.norm(ref) <= 1e-12
+
+
 def test_jitter_generator_matches_golden(golden):
     g = golden("jitter8_p2")
     np.testing.assert_array_equal(O.fk_jittered_coords(8, 0.2, 0), g["coords"])
