@@ -217,33 +217,94 @@ def dist_env():
     return world, rank, local
 
 
-def reference_sample(workload, steps, warmup):
-    """Reference CPU path on a bounded sample: one implicit-Euler step of every
-    p of the sweep on FK 16x16 (K = 512); DOF-updates/s over the sample."""
+REF_FUNCS = dict(d=(9, []), f=(10, []), c_d=(8, []), g_n=(11, []), c0=(8, []))
+# degrees the reference's SparseLU can factor on the C2 mesh (256^2) on one
+# host core: measured in the build container (1 Xeon core, 62 GB) one
+# implicit-Euler step took 21.7 s at p = 0 and 423 s at p = 1; at p = 2
+# (2.36M unknowns) SuperLU with COLAMD ordering -- the ordering of Eigen's
+# SparseLU -- ran out of the 62 GB host memory ("Not enough memory to perform
+# factorization"), and p = 3, 4 are larger still.
+REF_P_DEFAULT = {"c2": [0, 1]}
+CPU_SAMPLE = {"c2": ([0], 1), "c1": ([1], 100)}
+REF_STEPS = {"c1": 100}  # reference arm: implicit-Euler steps per degree (C1: the whole 100-step run)  # our line's cpu_baseline: (degrees, steps)
+REF_P_INFEASIBLE = ("p >= 2 not run: the reference's SparseLU of the 3KN system (2.36M unknowns at p = 2) "
+                    "exhausted 62 GB of host memory in the build container; p = 3, 4 are larger")
+
+
+def ref_worker(p, dim, dt, steps, jitter, bc):
+    """One process, one degree: `steps` implicit-Euler steps of the reference
+    (oracle/_ref = the unmodified headers + Eigen shim, SciPy SuperLU as its
+    SparseLU) from the initial state, timed around euler_step with
+    steady_clock as ldg_main.cpp:199-214 does.  Prints one JSON line."""
     from oracle import reflib as R
 
-    dim0, ps, dt, jitter, boundary, _ = WORKLOADS[workload]
-    dim = 16
-    funcs = dict(d=(9, []), f=(10, []), c_d=(8, []), g_n=(11, []), c0=(8, []))
     if not R.available():
         raise RuntimeError("oracle/_ref/libldgref.so missing")
-    cases = []
-    for p in ps:
+    import scipy.sparse.linalg  # noqa: F401  (the SparseLU stand-in: imported before the timed region)
+
+    boundary = {int(k): v for k, v in bc.items()}
+    warm = R.RefCase(R.RefMesh.square(0.5), n_of(p), 1.0, REF_FUNCS, boundary)  # untimed: loads SuperLU
+    warm.euler(warm.initial_state(), 0.0, dt, 1)
+    if jitter > 0.0:
+        from oracle import ldg_oracle as O
+
+        coords, v0t = O.fk_lists(dim)
+        coords = O.fk_jittered_coords(dim, jitter, 0)
+        mesh = R.RefMesh.create(coords, v0t.astype("int32"))
+    else:
         mesh = R.RefMesh.square(1.0 / dim)
-        case = R.RefCase(mesh, n_of(p), 1.0, funcs, boundary)
-        cases.append([case, case.initial_state(), 0.0, mesh])
-    dof, sec = 0, 0.0
-    for it in range(warmup + steps):
-        for c in cases:
-            y, t, s = c[0].euler(c[1], c[2], dt, 1)
-            c[1], c[2] = y, t
-            if it >= warmup:
-                sec += s
-                dof += 3 * c[3].num_t * n_of(c[0].n)
-    sample = (f"reference (unmodified headers + Eigen shim, SciPy SuperLU for SparseLU): "
-              f"FK {dim}x{dim} (K={2 * dim * dim}), p={ps}, {steps} timed implicit-Euler steps each, dt={dt:g}; "
-              f"the reference's LU cost grows superlinearly in K, so this sample overstates its 256x256 rate")
-    return dof / sec, sec, sample
+    n = n_of(p)
+    case = R.RefCase(mesh, n, 1.0, REF_FUNCS, boundary)
+    y = case.initial_state()
+    y, t, sec = case.euler(y, 0.0, dt, steps)
+    print(json.dumps({"p": p, "K": mesh.num_t, "N": n, "steps": steps, "seconds": sec,
+                      "dof": 3 * mesh.num_t * n * steps}), flush=True)
+
+
+def reference_runs(workload, ps, steps, cap_s):
+    """Runs ref_worker for every p concurrently, one process (one host core)
+    each, killed at cap_s seconds.  Returns {p: result dict | {"status": why}}."""
+    dim, _, dt, jitter, boundary, _ = WORKLOADS[workload]
+    procs = {}
+    for p in ps:
+        cmd = [sys.executable, os.path.abspath(__file__), "--ref-worker", str(p), "--steps", str(steps),
+               "--workload", workload]
+        procs[p] = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                                    env=dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1"))
+    out = {}
+    t_end = time.time() + cap_s
+    for p, pr in procs.items():
+        try:
+            so, se = pr.communicate(timeout=max(1.0, t_end - time.time()))
+            line = [x for x in so.splitlines() if x.startswith("{")]
+            out[p] = json.loads(line[-1]) if pr.returncode == 0 and line else {
+                "status": f"failed (rc {pr.returncode}): {se.strip().splitlines()[-1] if se.strip() else ''}"}
+        except subprocess.TimeoutExpired:
+            pr.kill()
+            pr.communicate()
+            out[p] = {"status": f"not finished within the {cap_s:.0f} s cap"}
+    return out, dim
+
+
+def reference_summary(res, dim, workload):
+    done = {p: r for p, r in res.items() if "seconds" in r}
+    if not done:
+        raise RuntimeError(f"no reference degree finished: {res}")
+    dof = sum(r["dof"] for r in done.values())
+    sec = sum(r["seconds"] for r in done.values())
+    per_p = {str(p): ({"seconds_per_step": r["seconds"] / r["steps"], "dof_updates_per_s": r["dof"] / r["seconds"]}
+                      if "seconds" in r else r) for p, r in sorted(res.items())}
+    try:
+        cpu = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = next((ln.split(":", 1)[1].strip() for ln in cpu.splitlines() if ln.startswith("Model name")), "?")
+    except Exception:  # pragma: no cover
+        model = "?"
+    sample = (f"reference (oracle/_ref: unmodified headers + Eigen shim, SciPy SuperLU with COLAMD as its SparseLU) "
+              f"on the {workload.upper()} mesh FK {dim}x{dim} (K={2 * dim * dim}), p={sorted(done)}, "
+              f"{next(iter(done.values()))['steps']} implicit-Euler step(s) each from the initial state, "
+              f"one single-threaded process per degree on its own core (host: {model}, nproc {os.cpu_count()}); "
+              f"value = sum of DOF updates / sum of per-degree step times (one core)")
+    return dof / sec, sec, sample, per_p, sorted(done)
 
 
 C3_METRIC, C3_UNIT = "assembled BSR bytes/s (time-dependent C-row blocks, SURVEY.md §8d)", "B/s"
@@ -282,16 +343,32 @@ def run_reference_arm(args):
                 "e2e": {"value": value, "unit": C3_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
-    value, sec, sample = reference_sample(args.workload, args.steps, args.warmup)
+    ps = ([int(x) for x in args.ref_p.split(",")] if args.ref_p else
+          REF_P_DEFAULT.get(args.workload, WORKLOADS[args.workload][1]))
+    # the reference is CPU-only and deterministic: one timed step per degree
+    # is the bounded sample (its p = 1 step alone takes ~7 min); no warm-up
+    res, dim = reference_runs(args.workload, ps, REF_STEPS.get(args.workload, 1), args.ref_cap)
+    value, sec, sample, per_p, done = reference_summary(res, dim, args.workload)
+    cfg = config_of(args.workload, dim, WORKLOADS[args.workload][1], WORKLOADS[args.workload][2], 1)
+    cfg["p_measured"] = done
+    cfg["per_p"] = per_p
+    if args.workload == "c2" and not args.ref_p:
+        cfg["p_not_run"] = REF_P_INFEASIBLE
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sec / REF_STEPS.get(args.workload, 1),  # one step of every measured p
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (analytic BASELINE.json problem)",
-            "config": {"workload": WORKLOADS[args.workload][5] + " [reference: bounded sample, see cpu_baseline]"},
+            "data": "synthetic (analytic BASELINE.json problem)", "config": cfg,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def config_of(workload, dim, ps, dt, world):
+    """The `config` both arms report for a workload (same keys, same values)."""
+    return {"workload": WORKLOADS[workload][5], "dim": dim, "K": 2 * dim * dim, "p": ps, "dt": dt,
+            "parallelism": f"strips{world} (NCCL halos + allreduce)" if world > 1 else "single"}
 
 
 def run_assembly_c3(args):
@@ -474,10 +551,12 @@ def run_ours(args):
     for p, s in zip(ps, systems):
         kern[p] = s.time_kernels(s.t, dt, reps=5, flush=True)
     kloc = dim if world == 1 else None  # per-rank byte counts below assume one GPU
-    # dominant kernel: stage 2 of the level-0 multigrid smoother (k_s2f; 3 sweep
-    # launches + 1 residual launch per V-cycle, one V-cycle per FGMRES iteration),
-    # taken at the p where it holds the largest share of the step
-    shares = {p: kern[p]["ms_sweep_s2"] * 4 * per_p[p]["iters"] / max(total_ms, 1e-9) for p in ps}
+    # dominant kernel: stage 2 of the level-0 multigrid smoother (k_s2f;
+    # s2_per_vcycle launches per V-cycle = level-0 sweeps + the residual, one
+    # V-cycle per FGMRES iteration), taken at the p where it holds the largest
+    # share of the step
+    shares = {p: kern[p]["ms_sweep_s2"] * kern[p]["s2_per_vcycle"] * per_p[p]["iters"] / max(total_ms, 1e-9)
+              for p in ps}
     pd = max(shares, key=shares.get)
     roof = None
     if kloc is not None:
@@ -501,11 +580,18 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded sample of the same workload: the lowest degree of the sweep on
+        # the same mesh (one reference step: ~22 s at 256^2, p = 0)
+        cps, csteps = CPU_SAMPLE.get(args.workload, (None, 1))
         try:
-            v, sec, sample = reference_sample(args.workload, 1, 0)
+            if cps is None:
+                raise RuntimeError("not run: the reference cannot assemble/factor this mesh on one host core "
+                                   "(SURVEY.md §8d)")
+            res, rdim = reference_runs(args.workload, cps, csteps, args.ref_cap)
+            v, sec, sample, _, _ = reference_summary(res, rdim, args.workload)
             cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample}
         except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"{e}"}
 
     if rank == 0:
         line = {
@@ -513,20 +599,20 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: analytic c, d(t), f(t) of BASELINE.json; FK mesh generated on device",
-            "config": {"workload": desc, "dim": dim, "K": 2 * dim * dim, "p": ps, "dt": dt,
-                       "parallelism": f"strips{world} (NCCL halos + allreduce)" if world > 1 else "single",
+            "config": dict(config_of(args.workload, dim, ps, dt, world), **{
                        "l2": "flushed (256 MB write) before every timed step; p>=2 working sets exceed L2",
-                       "solver": "FGMRES(30) on the exact Schur complement, p-coarsened geometric multigrid (level 0 "
-                                 "Chebyshev V(6,6)/V(5,6)/V(4,6)/V(5,6)/V(5,7) for p=0..4, coarse levels "
-                                 "damped block-Jacobi, mixed-precision smoother), reference residual "
-                                 "contract 1e-10",
+                       "solver": "default ldg_solver_opts: FGMRES(30) on the exact Schur complement to a relative "
+                                 "Schur residual of 1e-14 (states within 1e-10 relative L2 of the reference's direct "
+                                 "solve: tests/test_gpu_parity_scale.py) plus the reference residual contract 1e-10; "
+                                 "p-coarsened geometric multigrid preconditioner (level 0 Chebyshev, coarse levels "
+                                 "damped block-Jacobi, mixed-precision smoother)",
                        "per_p": {str(p): {"ms_per_step": per_p[p]["ms"] / args.steps,
                                           "ms_assemble": per_p[p]["ms_asm"] / args.steps,
                                           "ms_solve": per_p[p]["ms_solve"] / args.steps,
                                           "iterations_per_step": per_p[p]["iters"] / args.steps,
                                           "max_residual": per_p[p]["residual"],
                                           "dof_updates_per_s": 3 * 2 * dim * dim * n_of(p) * args.steps /
-                                          (per_p[p]["ms"] * 1e-3)} for p in ps}},
+                                          (per_p[p]["ms"] * 1e-3)} for p in ps}}),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
             "gpu_launches": launches,
             "roofline": roof,
@@ -553,7 +639,14 @@ def main():
     ap.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi sampler (diagnostics only)")
     ap.add_argument("--krylov", type=int, default=None, help="0 FGMRES (default), 1 BiCGStab")
     ap.add_argument("--restart", type=int, default=None, help="FGMRES restart length")
+    ap.add_argument("--ref-p", default=None, help="reference arm: comma-separated degrees (default: the feasible ones)")
+    ap.add_argument("--ref-cap", type=float, default=900.0, help="reference arm: wall-clock cap in seconds")
+    ap.add_argument("--ref-worker", type=int, default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ref_worker is not None:
+        dim, _, dt, jitter, boundary, _ = WORKLOADS[args.workload]
+        ref_worker(args.ref_worker, dim, dt, args.steps, jitter, boundary)
+        return 0
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

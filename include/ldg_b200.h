@@ -200,6 +200,39 @@ int ldg_export_operator(ldg_handle* h, int which, int64_t* nnz, int64_t* rows, i
                         int64_t cap);
 int ldg_export_vector(ldg_handle* h, int which, double* out, int64_t cap);
 
+/* The same operators in the reference's own storage: a column-major
+ * Eigen::SparseMatrix<double> with 32-bit indices after setFromTriplets +
+ * makeCompressed (SparseOperator, assembly.hpp:21-22,62-67; A as built by
+ * system.hpp:120-140).  colptr has n + 1 entries (n = K*N, or 3*K*N for
+ * LDG_OP_A), rows ascend within a column, and the stored pattern follows the
+ * reference's rules: M, H^m, G^m drop exact zeros (assembly.hpp:84,103-104,
+ * 130-131), S, S_D, Q^m, Q_N^m, R^m, R_D^m store whole blocks (explicit zeros
+ * kept).  Pass rowind/vals NULL to query *nnz.  Maps directly onto
+ * Eigen::Map<const Eigen::SparseMatrix<double>>(n, n, nnz, colptr, rowind, vals). */
+int ldg_export_operator_csc(ldg_handle* h, int which, int64_t* nnz, int32_t* colptr, int32_t* rowind, double* vals,
+                            int64_t cap);
+
+/* Block compressed sparse rows of an operator: block row b = u*K + k in the
+ * reference's element order (system.hpp:120-135), block columns ascending,
+ * each block N x N row-major with its explicit zeros; blocks in which the
+ * reference stores no entry are omitted.  rowptr has K+1 (3K+1 for A)
+ * entries; vals holds nblocks*N*N doubles.  NULL arrays query *nblocks. */
+int ldg_export_operator_bsr(ldg_handle* h, int which, int64_t* nblocks, int32_t* rowptr, int32_t* colind,
+                            double* vals, int64_t cap_blocks);
+
+/* Per-operator assembly with the caller's coefficients (one-rank handles).
+ * d_disc is the discrete coefficient D, K x N k-major (vec_dof order);
+ * the result is CSC as above.  The handle's assembled state is unchanged.
+ *   assemble_dphi_phi_coeff(mesh, rt, d_disc) -> G^m   (assembly.hpp:113-136)
+ *   assemble_edge_avg_coeff_nu(mesh, m, d_disc, sel_int, sel_dir, rt)
+ *       -> R^m (dirichlet = 0) or R_D^m (dirichlet = 1) (assembly.hpp:214-252)
+ * m is the normal component, 1 or 2 (else LDG_EINVAL, as the reference's
+ * std::invalid_argument). */
+int ldg_assemble_dphi_phi_coeff(ldg_handle* h, const double* d_disc, int m, int64_t* nnz, int32_t* colptr,
+                                int32_t* rowind, double* vals, int64_t cap);
+int ldg_assemble_edge_avg_coeff_nu(ldg_handle* h, const double* d_disc, int m, int dirichlet, int64_t* nnz,
+                                   int32_t* colptr, int32_t* rowind, double* vals, int64_t cap);
+
 /* State (SystemState, system.hpp:40-43): y is 3KN k-major per block. */
 int ldg_initial_state(ldg_handle* h);  /* system.hpp:99-107 */
 int ldg_set_state(ldg_handle* h, const double* y, double t);
@@ -266,6 +299,7 @@ typedef struct ldg_kernel_times {
   double ms_vcycle;     /* one preconditioner V-cycle (FP32 smoother), graph replay, L2 warm */
   double ms_level[8];   /* one smoothing sweep (residual + block-Jacobi) on level l, graph replay */
   double ms_sweep_s2;   /* level-0 smoother stage 2 + block-Jacobi update, one launch (L2 flushed if asked) */
+  int s2_per_vcycle;    /* launches of that kernel per V-cycle (level-0 sweeps + residual) */
 } ldg_kernel_times;
 
 /* Times each hot kernel over reps launches with CUDA events on the handle's

@@ -286,6 +286,25 @@ int ldgref_case_assemble(void* cv, double t) {
   });
 }
 
+// The per-step coefficient operators for a caller's D (K x N, k-major):
+// assemble_dphi_phi_coeff and assemble_edge_avg_coeff_nu (m = 1, 2) stored as
+// "ug1", "ug2", "ur1", "urd1", "ur2", "urd2".
+int ldgref_case_assemble_with_d(void* cv, const double* d_kmajor) {
+  auto* c = static_cast<RefCase*>(cv);
+  return guarded([&] {
+    const ldg::Mesh& m = *c->mesh;
+    const ldg::RefTensors& rt = *c->rt;
+    Eigen::VectorXd y(static_cast<Eigen::Index>(m.num_t) * rt.n);
+    std::memcpy(y.data(), d_kmajor, sizeof(double) * static_cast<size_t>(y.size()));
+    const ldg::DofMatrix d = ldg::unvec_dof(y, m.num_t, rt.n);
+    auto si = ldg::select_interior(m);
+    auto sd = ldg::select_boundary(m, c->dir_ids);
+    std::tie(c->ops["ug1"], c->ops["ug2"]) = ldg::assemble_dphi_phi_coeff(m, rt, d);
+    std::tie(c->ops["ur1"], c->ops["urd1"]) = ldg::assemble_edge_avg_coeff_nu(m, 1, d, si, sd, rt);
+    std::tie(c->ops["ur2"], c->ops["urd2"]) = ldg::assemble_edge_avg_coeff_nu(m, 2, d, si, sd, rt);
+  });
+}
+
 // Operator export, CSC order.  Returns nnz (or -1); fills when arrays non-null.
 long ldgref_case_op(void* cv, const char* name, int* rows, int* cols, double* vals) {
   auto* c = static_cast<RefCase*>(cv);

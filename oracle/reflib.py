@@ -84,6 +84,7 @@ def lib():
     L.ldgref_case_create.argtypes = [C.c_void_p, C.c_int, C.c_double, _ip, _dp, _ip, _ip, C.c_int]
     L.ldgref_case_free.argtypes = [C.c_void_p]
     L.ldgref_case_assemble.argtypes = [C.c_void_p, C.c_double]
+    L.ldgref_case_assemble_with_d.argtypes = [C.c_void_p, _dp]
     L.ldgref_case_op.restype = C.c_long
     L.ldgref_case_op.argtypes = [C.c_void_p, C.c_char_p, _ip, _ip, _dp]
     L.ldgref_case_vec.restype = C.c_long
@@ -226,6 +227,20 @@ class RefCase:
 
     def assemble(self, t: float):
         _check(lib().ldgref_case_assemble(self.h, t))
+
+    def assemble_with_d(self, d_kmajor):
+        """assemble_dphi_phi_coeff / assemble_edge_avg_coeff_nu (m = 1, 2) for a
+        caller's D (K x N, k-major): operators "ug1", "ug2", "ur1", "urd1", "ur2", "urd2"."""
+        d = np.ascontiguousarray(d_kmajor, dtype=np.float64).reshape(-1)
+        _check(lib().ldgref_case_assemble_with_d(self.h, _d(d)))
+
+    def op_csc(self, name: str):
+        """(colptr, rowind, values) of an operator exactly as the reference stores it."""
+        r, c, v = self.op(name)
+        n = self.mesh.num_t * self.n * (3 if name == "A" else 1)
+        colptr = np.zeros(n + 1, np.int64)
+        np.add.at(colptr, c.astype(np.int64) + 1, 1)
+        return np.cumsum(colptr), r, v
 
     def op(self, name: str):
         """Returns (rows, cols, vals) in CSC order."""

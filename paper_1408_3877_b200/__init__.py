@@ -82,7 +82,7 @@ class _Info(C.Structure):
 class _Times(C.Structure):
     _fields_ = [("ms_project", C.c_double), ("ms_assemble", C.c_double), ("ms_spmv", C.c_double),
                 ("ms_schur", C.c_double), ("reps", C.c_int), ("levels", C.c_int), ("ms_vcycle", C.c_double),
-                ("ms_level", C.c_double * 8), ("ms_sweep_s2", C.c_double)]
+                ("ms_level", C.c_double * 8), ("ms_sweep_s2", C.c_double), ("s2_per_vcycle", C.c_int)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -113,6 +113,10 @@ _SIGNATURES = {
     "ldg_assemble_blocks": (C.c_int, [_H, C.c_double, _dp]),
     "ldg_export_operator": (C.c_int, [_H, C.c_int, _lp, _lp, _lp, _dp, C.c_int64]),
     "ldg_export_vector": (C.c_int, [_H, C.c_int, _dp, C.c_int64]),
+    "ldg_export_operator_csc": (C.c_int, [_H, C.c_int, _lp, _ip, _ip, _dp, C.c_int64]),
+    "ldg_export_operator_bsr": (C.c_int, [_H, C.c_int, _lp, _ip, _ip, _dp, C.c_int64]),
+    "ldg_assemble_dphi_phi_coeff": (C.c_int, [_H, _dp, C.c_int, _lp, _ip, _ip, _dp, C.c_int64]),
+    "ldg_assemble_edge_avg_coeff_nu": (C.c_int, [_H, _dp, C.c_int, C.c_int, _lp, _ip, _ip, _dp, C.c_int64]),
     "ldg_initial_state": (C.c_int, [_H]),
     "ldg_set_state": (C.c_int, [_H, _dp, C.c_double]),
     "ldg_get_state": (C.c_int, [_H, _dp, _dp]),
@@ -384,6 +388,57 @@ class LdgSystem:
                                             c.ctypes.data_as(_lp), _d(v), nnz.value))
         return r, c, v
 
+    def _csc_call(self, n: int, call):
+        """Two-phase CSC export: call(nnz, colptr, rowind, vals, cap) -> scipy csc_matrix."""
+        import scipy.sparse as sp
+
+        nnz = C.c_int64()
+        self._check(call(C.byref(nnz), None, None, None, 0))
+        cp = np.zeros(n + 1, np.int32)
+        ri, v = np.zeros(nnz.value, np.int32), np.zeros(nnz.value)
+        self._check(call(C.byref(nnz), _i(cp), _i(ri), _d(v), nnz.value))
+        return sp.csc_matrix((v, ri, cp), shape=(n, n))
+
+    def operator_csc(self, name: str):
+        """An operator in the reference's storage (Eigen CSC, assembly.hpp:21-22)
+        as a scipy csc_matrix with the same colptr / rowind / values."""
+        which = OPERATORS.index(name)
+        n = (3 if name == "A" else 1) * self.block_dim
+        lib = load_library()
+        return self._csc_call(n, lambda *a: lib.ldg_export_operator_csc(self._h, which, *a))
+
+    def operator_bsr(self, name: str):
+        """(rowptr, colind, blocks[nb, N, N]) block CSR in reference element order."""
+        which = OPERATORS.index(name)
+        nbr = (3 if name == "A" else 1) * self.num_t
+        lib = load_library()
+        nb = C.c_int64()
+        self._check(lib.ldg_export_operator_bsr(self._h, which, C.byref(nb), None, None, None, 0))
+        rp, ci = np.zeros(nbr + 1, np.int32), np.zeros(nb.value, np.int32)
+        v = np.zeros(nb.value * self.n * self.n)
+        self._check(lib.ldg_export_operator_bsr(self._h, which, C.byref(nb), _i(rp), _i(ci), _d(v), nb.value))
+        return rp, ci, v.reshape(nb.value, self.n, self.n)
+
+    def assemble_dphi_phi_coeff(self, d_disc):
+        """(G^1, G^2) = assemble_dphi_phi_coeff(mesh, rt, d_disc) (assembly.hpp:113-136)
+        for a caller's K x N coefficient matrix; scipy CSC."""
+        d = np.ascontiguousarray(d_disc, dtype=np.float64).reshape(-1)
+        if d.size != self.block_dim:
+            raise ValueError("coefficient matrix shape mismatch")
+        lib = load_library()
+        return tuple(self._csc_call(self.block_dim, lambda *a, m=m: lib.ldg_assemble_dphi_phi_coeff(
+            self._h, _d(d), m, *a)) for m in (1, 2))
+
+    def assemble_edge_avg_coeff_nu(self, m: int, d_disc):
+        """(R^m, R_D^m) = assemble_edge_avg_coeff_nu(mesh, m, d_disc, sel_int, sel_dir, rt)
+        (assembly.hpp:214-252); scipy CSC."""
+        d = np.ascontiguousarray(d_disc, dtype=np.float64).reshape(-1)
+        if d.size != self.block_dim:
+            raise ValueError("coefficient matrix shape mismatch")
+        lib = load_library()
+        return tuple(self._csc_call(self.block_dim, lambda *a, w=w: lib.ldg_assemble_edge_avg_coeff_nu(
+            self._h, _d(d), int(m), w, *a)) for w in (0, 1))
+
     def vector(self, name: str) -> np.ndarray:
         which = VECTORS.index(name)
         n = (3 if name in ("V", "Y") else 1) * self.block_dim
@@ -392,13 +447,10 @@ class LdgSystem:
         return out
 
     def build_blocks(self, t: float):
-        """(A, V) of system.hpp:110-152; A as a scipy CSR matrix (3KN x 3KN)."""
-        import scipy.sparse as sp
-
+        """SystemBlocks (A, V) of system.hpp:110-152: A (3KN x 3KN) in the reference's
+        CSC storage (scipy csc_matrix), V the stacked right-hand side."""
         self.assemble(t)
-        r, c, v = self.operator("A")
-        n3 = 3 * self.block_dim
-        return sp.coo_matrix((v, (r, c)), shape=(n3, n3)).tocsr(), self.vector("V")
+        return self.operator_csc("A"), self.vector("V")
 
     def initial_state(self):
         """system.hpp:99-107 -> (y, t)."""

@@ -172,28 +172,257 @@ std::vector<double> blocks_to_host(Handle& h, const double* dev, int ncomp) {
   return out;
 }
 
-struct Coo {
-  std::vector<int64_t> r, c;
-  std::vector<double> v;
+// An operator as N x N blocks in the global numbering of system.hpp:120-135
+// (block row u*K + k, block column v*K + k'), each with the reference's
+// storage rule: `keep` blocks store every entry (the reference pushes the
+// whole block: S, S_D, Q, Q_N, R, R_D, assembly.hpp:142-252), other blocks
+// only their nonzero entries (M, H, G drop exact zeros, assembly.hpp:84,
+// 103-104,130-131).  In A (system.hpp:120-135) a block is `keep` when any
+// operator appended to it is.
+struct Blocks {
+  int N = 0;
+  int64_t nbrow = 0;                // block rows (= block columns)
+  std::vector<int64_t> br, bc;
+  std::vector<uint8_t> keep;
+  std::vector<double> v;            // N*N row-major per block
+  size_t count() const { return br.size(); }
+  bool stored(size_t b, int e) const { return keep[b] || v[b * N * N + e] != 0.0; }
 };
 
-// Appends block slot s of element k: rows (ru*K + gid(k))*N + i, cols (cu*K + gid(col))*N + j.
-void push_block(const Handle& h, const std::vector<int>& nbr_host, const double* blk, int k, int s, int ru, int cu,
-                double scale, Coo& out) {
-  const int N = h.N;
-  int col = k;
-  if (s > 0) {
-    col = nbr_host[(s - 1) * h.Kp + k];
-    if (col < 0) return;
-  }
-  const int64_t Kg = h.Kglobal;
-  const int64_t grow = ru * Kg + h.gid[k], gcol = cu * Kg + h.gid[col];
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) {
-      out.r.push_back(grow * N + i);
-      out.c.push_back(gcol * N + j);
-      out.v.push_back(scale * blk[static_cast<size_t>(s * N * N + i * N + j) * h.Kp + k]);
+// per-element edge kinds (host): bit 0 interior, 1 Dirichlet, 2 Neumann edge present
+std::vector<uint8_t> edge_kind_bits(Handle& h) {
+  std::vector<int> kd(3 * h.Kp);
+  LDG_CUDA(cudaMemcpy(kd.data(), h.kind.ptr, sizeof(int) * kd.size(), cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> bits(h.K, 0);
+  for (int n = 0; n < 3; ++n)
+    for (int k = 0; k < h.K; ++k) {
+      const int c = kd[n * h.Kp + k];
+      if (c == ldgb::kInterior) bits[k] |= 1;
+      if (c == ldgb::kDirichlet) bits[k] |= 2;
+      if (c == ldgb::kNeumann) bits[k] |= 4;
     }
+  return bits;
+}
+
+// keep rule of a diagonal block: the edge kinds whose presence makes the
+// reference push the whole block (0: none, zeros dropped)
+enum KeepDiag : uint8_t { kDropZeros = 0, kIfInt = 1, kIfDir = 2, kIfNeu = 4 };
+
+// Appends the blocks of device SoA array `blk` ([comp][4][N*N][Kp], slot 0
+// the diagonal block, slots 1..3 the neighbours across edges 0..2) of every
+// owned element: block row ru*K + gid(k), column cu*K + gid(col).
+void append_blocks(const Handle& h, const std::vector<int>& nbr_host, const std::vector<uint8_t>& bits,
+                   const std::vector<double>& blk, int comp, bool off, int ru, int cu, double scale, uint8_t keep_diag,
+                   Blocks& out) {
+  const int N = h.N;
+  const size_t NN = static_cast<size_t>(N) * N;
+  const double* base = blk.data() + static_cast<size_t>(comp) * 4 * NN * h.Kp;
+  const int64_t Kg = h.Kglobal;
+  for (int k = 0; k < h.K; ++k)
+    for (int s = 0; s < (off ? 4 : 1); ++s) {
+      int col = k;
+      if (s > 0) {
+        col = nbr_host[(s - 1) * h.Kp + k];
+        if (col < 0) continue;
+      }
+      out.br.push_back(ru * Kg + h.gid[k]);
+      out.bc.push_back(cu * Kg + h.gid[col]);
+      out.keep.push_back(s > 0 ? 1 : ((bits[k] & keep_diag) ? 1 : 0));
+      for (size_t e = 0; e < NN; ++e) out.v.push_back(scale * base[(s * NN + e) * h.Kp + k]);
+    }
+}
+
+// Every operator of build_blocks at the last ldg_assemble, as Blocks.
+Blocks collect_blocks(Team& T, int which) {
+  const bool needs_d = which == LDG_OP_G1 || which == LDG_OP_G2 || which == LDG_OP_R1 || which == LDG_OP_R2 ||
+                       which == LDG_OP_RD1 || which == LDG_OP_RD2 || which == LDG_OP_A;
+  if (needs_d) require_assembled(T);
+  Blocks out;
+  out.N = T.h0().N;
+  out.nbrow = static_cast<int64_t>(which == LDG_OP_A ? 3 : 1) * T.h0().Kglobal;
+  for (auto& rp : T.ranks) {
+    Handle& h = *rp;
+    std::vector<int> nb(3 * h.Kp);
+    LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
+    const std::vector<uint8_t> bits = edge_kind_bits(h);
+    const long NN = static_cast<long>(h.N) * h.N;
+    DBuf<double> tmp;
+    tmp.alloc(8 * NN * h.Kp, nullptr);
+    auto emit = [&](const std::vector<double>& blk, int comp, bool off, int ru, int cu, double scale, uint8_t kd) {
+      append_blocks(h, nb, bits, blk, comp, off, ru, cu, scale, kd, out);
+    };
+    if (which == LDG_OP_A) {
+      // the static blocks exactly as the matrix-free kernels rebuild them (K4)
+      ldgb::launch_static(h, ldgb::kStM, tmp.ptr);
+      const auto M = blocks_to_host(h, tmp.ptr, 1);
+      ldgb::launch_static(h, ldgb::kStB, tmp.ptr);
+      const auto B = blocks_to_host(h, tmp.ptr, 2);
+      ldgb::launch_static(h, ldgb::kStS, tmp.ptr);
+      const auto S = blocks_to_host(h, tmp.ptr, 1);
+      ldgb::launch_assemble(h, ldgb::kModeE, tmp.ptr);  // all 8 blocks (the solver keeps the diagonal ones)
+      const auto E = blocks_to_host(h, tmp.ptr, 2);
+      // append order of system.hpp:120-135; B = -H + Q + Q_N, E = -G + R + R_D, S + S_D
+      emit(M, 0, false, 0, 0, 1.0, kDropZeros);
+      emit(B, 0, true, 0, 2, 1.0, kIfInt | kIfNeu);
+      emit(M, 0, false, 1, 1, 1.0, kDropZeros);
+      emit(B, 1, true, 1, 2, 1.0, kIfInt | kIfNeu);
+      emit(E, 0, true, 2, 0, 1.0, kIfInt | kIfDir);
+      emit(E, 1, true, 2, 1, 1.0, kIfInt | kIfDir);
+      emit(S, 0, true, 2, 2, h.prob.eta, kIfInt | kIfDir);
+      continue;
+    }
+    int comp = 0;
+    bool off = false;
+    uint8_t kd = kDropZeros;
+    switch (which) {
+      case LDG_OP_MASS: ldgb::launch_static(h, ldgb::kStM, tmp.ptr); break;
+      case LDG_OP_H1: case LDG_OP_H2:
+        ldgb::launch_static(h, ldgb::kStH, tmp.ptr);
+        comp = which == LDG_OP_H2;
+        break;
+      case LDG_OP_Q1: case LDG_OP_Q2:
+        ldgb::launch_static(h, ldgb::kStQ, tmp.ptr);
+        comp = which == LDG_OP_Q2;
+        off = true;
+        kd = kIfInt;
+        break;
+      case LDG_OP_QN1: case LDG_OP_QN2:
+        ldgb::launch_static(h, ldgb::kStQN, tmp.ptr);
+        comp = which == LDG_OP_QN2;
+        kd = kIfNeu;
+        break;
+      case LDG_OP_S:
+        ldgb::launch_static(h, ldgb::kStSint, tmp.ptr);
+        off = true;
+        kd = kIfInt;
+        break;
+      case LDG_OP_SD: ldgb::launch_static(h, ldgb::kStSD, tmp.ptr); kd = kIfDir; break;
+      case LDG_OP_G1: case LDG_OP_G2:
+        ldgb::launch_assemble(h, ldgb::kModeG, tmp.ptr);
+        comp = which == LDG_OP_G2;
+        break;
+      case LDG_OP_R1: case LDG_OP_R2:
+        ldgb::launch_assemble(h, ldgb::kModeR, tmp.ptr);
+        comp = which == LDG_OP_R2;
+        off = true;
+        kd = kIfInt;
+        break;
+      default:
+        ldgb::launch_assemble(h, ldgb::kModeRD, tmp.ptr);
+        comp = which == LDG_OP_RD2;
+        kd = kIfDir;
+        break;
+    }
+    const auto blk = blocks_to_host(h, tmp.ptr, 2);
+    emit(blk, comp, off, 0, 0, 1.0, kd);
+  }
+  return out;
+}
+
+// Blocks -> compressed sparse column arrays with 32-bit indices (the
+// reference's Eigen::SparseMatrix<double>, assembly.hpp:21, after
+// setFromTriplets + makeCompressed: rows sorted within each column,
+// duplicates summed).  nnz only when rowind/vals are NULL.
+void blocks_to_csc(const Blocks& B, int64_t* nnz, int32_t* colptr, int32_t* rowind, double* vals, int64_t cap) {
+  const int N = B.N;
+  const int64_t n = B.nbrow * N;
+  if (n > INT32_MAX) throw Error(LDG_EINVAL, "operator dimension exceeds 32-bit indices");
+  // (col, row) keys of the stored entries; duplicates merged below
+  std::vector<std::pair<int64_t, int64_t>> key;
+  std::vector<double> val;
+  for (size_t b = 0; b < B.count(); ++b)
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        const int e = i * N + j;
+        if (!B.stored(b, e)) continue;
+        key.emplace_back(B.bc[b] * N + j, B.br[b] * N + i);
+        val.push_back(B.v[b * N * N + e]);
+      }
+  std::vector<size_t> ord(key.size());
+  for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return key[a] < key[b]; });
+  int64_t m = 0;
+  for (size_t q = 0; q < ord.size(); ++q)
+    if (q == 0 || key[ord[q]] != key[ord[q - 1]]) ++m;
+  if (m > INT32_MAX) throw Error(LDG_EINVAL, "nonzero count exceeds 32-bit indices");
+  *nnz = m;
+  if (!rowind || !vals || !colptr) return;
+  if (cap < m) throw Error(LDG_EINVAL, "export capacity too small");
+  std::fill(colptr, colptr + n + 1, 0);
+  int64_t w = -1;
+  for (size_t q = 0; q < ord.size(); ++q) {
+    const auto& k = key[ord[q]];
+    if (q == 0 || k != key[ord[q - 1]]) {
+      ++w;
+      rowind[w] = static_cast<int32_t>(k.second);
+      vals[w] = 0.0;
+      ++colptr[k.first + 1];
+    }
+    vals[w] += val[ord[q]];
+  }
+  for (int64_t c = 0; c < n; ++c) colptr[c + 1] += colptr[c];
+}
+
+// Blocks -> block compressed sparse rows: block rows in reference k order,
+// block columns ascending, N x N row-major blocks (explicit zeros kept);
+// blocks the reference stores no entry of are omitted.
+void blocks_to_bsr(const Blocks& B, int64_t* nblocks, int32_t* rowptr, int32_t* colind, double* vals,
+                   int64_t cap_blocks) {
+  const int N = B.N;
+  const size_t NN = static_cast<size_t>(N) * N;
+  if (B.nbrow > INT32_MAX) throw Error(LDG_EINVAL, "block dimension exceeds 32-bit indices");
+  std::vector<size_t> ord;
+  for (size_t b = 0; b < B.count(); ++b) {
+    bool any = B.keep[b] != 0;
+    for (size_t e = 0; !any && e < NN; ++e) any = B.v[b * NN + e] != 0.0;
+    if (any) ord.push_back(b);
+  }
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    return B.br[a] != B.br[b] ? B.br[a] < B.br[b] : B.bc[a] < B.bc[b];
+  });
+  int64_t m = 0;
+  for (size_t q = 0; q < ord.size(); ++q)
+    if (q == 0 || B.br[ord[q]] != B.br[ord[q - 1]] || B.bc[ord[q]] != B.bc[ord[q - 1]]) ++m;
+  *nblocks = m;
+  if (!rowptr || !colind || !vals) return;
+  if (cap_blocks < m) throw Error(LDG_EINVAL, "export capacity too small");
+  std::fill(rowptr, rowptr + B.nbrow + 1, 0);
+  int64_t w = -1;
+  for (size_t q = 0; q < ord.size(); ++q) {
+    const size_t b = ord[q];
+    if (q == 0 || B.br[b] != B.br[ord[q - 1]] || B.bc[b] != B.bc[ord[q - 1]]) {
+      ++w;
+      colind[w] = static_cast<int32_t>(B.bc[b]);
+      std::fill(vals + w * NN, vals + (w + 1) * NN, 0.0);
+      ++rowptr[B.br[b] + 1];
+    }
+    for (size_t e = 0; e < NN; ++e) vals[w * NN + e] += B.v[b * NN + e];
+  }
+  for (int64_t r = 0; r < B.nbrow; ++r) rowptr[r + 1] += rowptr[r];
+}
+
+void scatter_from_host(Team& T, const double* in, int nvec, const std::function<double*(Handle&)>& dst);
+
+// One-rank handles: runs `fn` with h.D replaced by the caller's host
+// coefficients (K x N, k-major = vec_dof order), restoring the assembled D.
+template <typename F>
+void with_host_d(Team& T, const double* d_disc, F&& fn) {
+  if (T.nlocal() != 1 || T.size != 1)
+    throw Error(LDG_EINVAL, "per-operator assembly with caller coefficients: one-rank handles only");
+  Handle& h = T.h0();
+  DBuf<double> saved;
+  saved.alloc(h.vec_len(), nullptr);
+  LDG_CUDA(cudaMemcpyAsync(saved.ptr, h.D.ptr, sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice, T.stream));
+  scatter_from_host(T, d_disc, 1, [](Handle& x) { return x.D.ptr; });
+  try {
+    fn(h);
+  } catch (...) {
+    cudaMemcpyAsync(h.D.ptr, saved.ptr, sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice, T.stream);
+    cudaStreamSynchronize(T.stream);
+    throw;
+  }
+  LDG_CUDA(cudaMemcpyAsync(h.D.ptr, saved.ptr, sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice, T.stream));
+  LDG_CUDA(cudaStreamSynchronize(T.stream));
 }
 
 // owned rows of nvec N-plane device vectors -> global k-major host array
@@ -682,87 +911,83 @@ int ldg_export_operator(ldg_handle* H, int which, int64_t* nnz, int64_t* rows, i
   return guarded(H, [&] {
     Team& T = H->team;
     if (which < 0 || which >= LDG_OP_COUNT) throw Error(LDG_EINVAL, "unknown operator");
-    const bool needs_d = which == LDG_OP_G1 || which == LDG_OP_G2 || which == LDG_OP_R1 || which == LDG_OP_R2 ||
-                         which == LDG_OP_RD1 || which == LDG_OP_RD2 || which == LDG_OP_A;
-    if (needs_d) require_assembled(T);
-    Coo coo;
-    for (auto& rp : T.ranks) {
-      Handle& h = *rp;
-      std::vector<int> nb(3 * h.Kp);
-      LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
-      const long NN = static_cast<long>(h.N) * h.N;
-      DBuf<double> tmp;
-      tmp.alloc(8 * NN * h.Kp, nullptr);
-      auto emit = [&](const std::vector<double>& blk, int comp, bool off, int ru, int cu, double scale) {
-        const double* base = blk.data() + static_cast<size_t>(comp) * 4 * NN * h.Kp;
-        for (int k = 0; k < h.K; ++k)
-          for (int s = 0; s < (off ? 4 : 1); ++s) push_block(h, nb, base, k, s, ru, cu, scale, coo);
-      };
-      if (which == LDG_OP_A) {
-        // the static blocks exactly as the matrix-free kernels rebuild them (K4)
-        ldgb::launch_static(h, ldgb::kStM, tmp.ptr);
-        const auto M = blocks_to_host(h, tmp.ptr, 1);
-        ldgb::launch_static(h, ldgb::kStB, tmp.ptr);
-        const auto B = blocks_to_host(h, tmp.ptr, 2);
-        ldgb::launch_static(h, ldgb::kStS, tmp.ptr);
-        const auto S = blocks_to_host(h, tmp.ptr, 1);
-        ldgb::launch_assemble(h, ldgb::kModeE, tmp.ptr);  // all 8 blocks (the solver keeps the diagonal ones)
-        const auto E = blocks_to_host(h, tmp.ptr, 2);
-        emit(M, 0, false, 0, 0, 1.0);
-        emit(B, 0, true, 0, 2, 1.0);
-        emit(M, 0, false, 1, 1, 1.0);
-        emit(B, 1, true, 1, 2, 1.0);
-        emit(E, 0, true, 2, 0, 1.0);
-        emit(E, 1, true, 2, 1, 1.0);
-        emit(S, 0, true, 2, 2, h.prob.eta);
-        continue;
-      }
-      int comp = 0;
-      bool off = false;
-      switch (which) {
-        case LDG_OP_MASS: ldgb::launch_static(h, ldgb::kStM, tmp.ptr); break;
-        case LDG_OP_H1: case LDG_OP_H2:
-          ldgb::launch_static(h, ldgb::kStH, tmp.ptr);
-          comp = which == LDG_OP_H2;
-          break;
-        case LDG_OP_Q1: case LDG_OP_Q2:
-          ldgb::launch_static(h, ldgb::kStQ, tmp.ptr);
-          comp = which == LDG_OP_Q2;
-          off = true;
-          break;
-        case LDG_OP_QN1: case LDG_OP_QN2:
-          ldgb::launch_static(h, ldgb::kStQN, tmp.ptr);
-          comp = which == LDG_OP_QN2;
-          break;
-        case LDG_OP_S:
-          ldgb::launch_static(h, ldgb::kStSint, tmp.ptr);
-          off = true;
-          break;
-        case LDG_OP_SD: ldgb::launch_static(h, ldgb::kStSD, tmp.ptr); break;
-        case LDG_OP_G1: case LDG_OP_G2:
-          ldgb::launch_assemble(h, ldgb::kModeG, tmp.ptr);
-          comp = which == LDG_OP_G2;
-          break;
-        case LDG_OP_R1: case LDG_OP_R2:
-          ldgb::launch_assemble(h, ldgb::kModeR, tmp.ptr);
-          comp = which == LDG_OP_R2;
-          off = true;
-          break;
-        default:
-          ldgb::launch_assemble(h, ldgb::kModeRD, tmp.ptr);
-          comp = which == LDG_OP_RD2;
-          break;
-      }
-      const auto blk = blocks_to_host(h, tmp.ptr, 2);
-      emit(blk, comp, off, 0, 0, 1.0);
-    }
-    *nnz = static_cast<int64_t>(coo.v.size());
+    const Blocks B = collect_blocks(T, which);
+    const int N = B.N;
+    const size_t NN = static_cast<size_t>(N) * N;
+    *nnz = static_cast<int64_t>(B.count() * NN);
     if (rows && cols && vals) {
       if (cap < *nnz) throw Error(LDG_EINVAL, "export capacity too small");
-      std::copy(coo.r.begin(), coo.r.end(), rows);
-      std::copy(coo.c.begin(), coo.c.end(), cols);
-      std::copy(coo.v.begin(), coo.v.end(), vals);
+      size_t w = 0;
+      for (size_t b = 0; b < B.count(); ++b)
+        for (int i = 0; i < N; ++i)
+          for (int j = 0; j < N; ++j, ++w) {
+            rows[w] = B.br[b] * N + i;
+            cols[w] = B.bc[b] * N + j;
+            vals[w] = B.v[b * NN + i * N + j];
+          }
     }
+  });
+}
+
+int ldg_export_operator_csc(ldg_handle* H, int which, int64_t* nnz, int32_t* colptr, int32_t* rowind, double* vals,
+                            int64_t cap) {
+  if (!H || !nnz) return LDG_EINVAL;
+  return guarded(H, [&] {
+    if (which < 0 || which >= LDG_OP_COUNT) throw Error(LDG_EINVAL, "unknown operator");
+    blocks_to_csc(collect_blocks(H->team, which), nnz, colptr, rowind, vals, cap);
+  });
+}
+
+int ldg_export_operator_bsr(ldg_handle* H, int which, int64_t* nblocks, int32_t* rowptr, int32_t* colind,
+                            double* vals, int64_t cap_blocks) {
+  if (!H || !nblocks) return LDG_EINVAL;
+  return guarded(H, [&] {
+    if (which < 0 || which >= LDG_OP_COUNT) throw Error(LDG_EINVAL, "unknown operator");
+    blocks_to_bsr(collect_blocks(H->team, which), nblocks, rowptr, colind, vals, cap_blocks);
+  });
+}
+
+int ldg_assemble_dphi_phi_coeff(ldg_handle* H, const double* d_disc, int m, int64_t* nnz, int32_t* colptr,
+                                int32_t* rowind, double* vals, int64_t cap) {
+  if (!H || !d_disc || !nnz) return LDG_EINVAL;
+  return guarded(H, [&] {
+    if (m != 1 && m != 2) throw Error(LDG_EINVAL, "normal component must be 1 or 2");
+    Team& T = H->team;
+    Blocks B;
+    with_host_d(T, d_disc, [&](Handle& h) {
+      B.N = h.N;
+      B.nbrow = h.Kglobal;
+      std::vector<int> nb(3 * h.Kp);
+      LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
+      DBuf<double> tmp;
+      tmp.alloc(8L * h.N * h.N * h.Kp, nullptr);
+      ldgb::launch_assemble(h, ldgb::kModeG, tmp.ptr);
+      append_blocks(h, nb, edge_kind_bits(h), blocks_to_host(h, tmp.ptr, 2), m - 1, false, 0, 0, 1.0, kDropZeros,
+                    B);
+    });
+    blocks_to_csc(B, nnz, colptr, rowind, vals, cap);
+  });
+}
+
+int ldg_assemble_edge_avg_coeff_nu(ldg_handle* H, const double* d_disc, int m, int dirichlet, int64_t* nnz,
+                                   int32_t* colptr, int32_t* rowind, double* vals, int64_t cap) {
+  if (!H || !d_disc || !nnz) return LDG_EINVAL;
+  return guarded(H, [&] {
+    if (m != 1 && m != 2) throw Error(LDG_EINVAL, "normal component must be 1 or 2");
+    Team& T = H->team;
+    Blocks B;
+    with_host_d(T, d_disc, [&](Handle& h) {
+      B.N = h.N;
+      B.nbrow = h.Kglobal;
+      std::vector<int> nb(3 * h.Kp);
+      LDG_CUDA(cudaMemcpy(nb.data(), h.nbr.ptr, sizeof(int) * nb.size(), cudaMemcpyDeviceToHost));
+      DBuf<double> tmp;
+      tmp.alloc(8L * h.N * h.N * h.Kp, nullptr);
+      ldgb::launch_assemble(h, dirichlet ? ldgb::kModeRD : ldgb::kModeR, tmp.ptr);
+      append_blocks(h, nb, edge_kind_bits(h), blocks_to_host(h, tmp.ptr, 2), m - 1, !dirichlet, 0, 0, 1.0,
+                    dirichlet ? kIfDir : kIfInt, B);
+    });
+    blocks_to_csc(B, nnz, colptr, rowind, vals, cap);
   });
 }
 
@@ -1054,6 +1279,7 @@ int ldg_time_kernels(ldg_handle* H, double t, double dt, int reps, int flush, ld
     if (out->levels > 0) {
       ldgb::team_sweep_s2_prepare(T, 1.0, dt);
       out->ms_sweep_s2 = timed([&] { ldgb::team_sweep_s2(T, 1.0, dt); });
+      out->s2_per_vcycle = ldgb::team_s2_per_vcycle(T);
     }
   });
 }

@@ -335,6 +335,7 @@ void team_schur_apply_c(Team& T, double wm, double dt);     // kr_v = S_c C (ker
 int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, double* ms_level, int max_levels);
 void team_sweep_s2_prepare(Team& T, double wm, double dt);  // multigrid set up, level-0 stage 1 done
 void team_sweep_s2(Team& T, double wm, double dt);          // one level-0 smoother stage-2 launch
+int team_s2_per_vcycle(Team& T);                            // level-0 stage-2 launches per V-cycle
 double team_sum_sq(Team& T, const std::function<const double*(Handle&)>& v);  // owned entries, all ranks
 
 void init_handle_tables(Handle& h, int p);  // reference tables + element rule of degree p (ldg_capi.cu)

@@ -1326,6 +1326,12 @@ void team_sweep_s2_prepare(Team& T, double wm, double dt) {
 void team_sweep_s2(Team& T, double wm, double dt) {
   each(T, 0, [&](Handle& L) { f_stage2(L, 1, kPh, kP, wm, dt, kMgS); });
 }
+// level 0 of vcycle(): (pre - 1) sweeps after the residual-free one, the
+// residual before restriction, post sweeps
+int team_s2_per_vcycle(Team& T) {
+  const int p = T.h0().p;
+  return pre_of(p, 0) + post_of(p, 0);
+}
 
 // Multigrid cost breakdown (kernel timing): one V-cycle of the FP32-smoother
 // preconditioner and one smoothing sweep (residual + block-Jacobi) per level,

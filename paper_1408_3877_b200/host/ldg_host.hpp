@@ -61,6 +61,31 @@ struct SystemState {
   double t = 0.0;
 };
 
+/// SparseOperator (assembly.hpp:21): the arrays of a compressed column-major
+/// Eigen::SparseMatrix<double> with int indices, maps onto
+/// Eigen::Map<const Eigen::SparseMatrix<double>>(rows, cols, nnz, outer.data(), inner.data(), values.data()).
+struct SparseOperator {
+  int rows = 0, cols = 0;
+  std::vector<int> outer;     // cols + 1 column pointers
+  std::vector<int> inner;     // row index per stored entry, ascending within a column
+  std::vector<double> values;
+  long nonZeros() const { return static_cast<long>(values.size()); }
+};
+
+/// system.hpp:57-61
+struct SystemBlocks {
+  SparseOperator a;           // 3KN x 3KN, Eq. (5) block layout
+  std::vector<double> v;      // [-J_D^1; -J_D^2; eta K_D - K_N + L]
+};
+
+/// Block CSR of an operator: N x N row-major blocks, block rows in the
+/// reference's element order.
+struct BlockOperator {
+  int n_local = 0;
+  std::vector<int> rowptr, colind;
+  std::vector<double> blocks;
+};
+
 namespace detail {
 
 inline void check(int rc, const ldg_handle* h) {
@@ -136,9 +161,66 @@ class LdgSystem {
     return out;
   }
 
-  /// The device half of build_blocks(t) (system.hpp:110-152); operators
-  /// stay in HBM (exports: ldg_export_operator).
-  void build_blocks(double t) const { detail::check(ldg_assemble(h_.get(), t), h_.get()); }
+  /// build_blocks(t) (system.hpp:110-152): assembles on the device (the
+  /// operators stay in HBM for euler_step) and returns A in the reference's
+  /// CSC storage with V.  Use assemble(t) to skip the host copy.
+  SystemBlocks build_blocks(double t) const {
+    assemble(t);
+    SystemBlocks b;
+    b.a = operator_csc(LDG_OP_A);
+    b.v.resize(3u * static_cast<size_t>(block_dim()));
+    detail::check(ldg_export_vector(h_.get(), LDG_VEC_V, b.v.data(), static_cast<int64_t>(b.v.size())), h_.get());
+    return b;
+  }
+
+  /// The device half of build_blocks(t): projection, assembly, right-hand side.
+  void assemble(double t) const { detail::check(ldg_assemble(h_.get(), t), h_.get()); }
+
+  /// One operator of the last assemble() (enum ldg_operator) as the reference stores it.
+  SparseOperator operator_csc(int which) const {
+    const int n = (which == LDG_OP_A ? 3 : 1) * block_dim();
+    return csc_call(n, [&](int64_t* nnz, int32_t* cp, int32_t* ri, double* v, int64_t cap) {
+      return ldg_export_operator_csc(h_.get(), which, nnz, cp, ri, v, cap);
+    });
+  }
+
+  /// The same operator as block CSR (N x N row-major blocks).
+  BlockOperator operator_bsr(int which) const {
+    BlockOperator b;
+    b.n_local = n_local();
+    int64_t nb = 0;
+    detail::check(ldg_export_operator_bsr(h_.get(), which, &nb, nullptr, nullptr, nullptr, 0), h_.get());
+    b.rowptr.resize(static_cast<size_t>((which == LDG_OP_A ? 3 : 1) * num_t()) + 1);
+    b.colind.resize(static_cast<size_t>(nb));
+    b.blocks.resize(static_cast<size_t>(nb) * n_local() * n_local());
+    detail::check(ldg_export_operator_bsr(h_.get(), which, &nb, b.rowptr.data(), b.colind.data(), b.blocks.data(), nb),
+                  h_.get());
+    return b;
+  }
+
+  /// assemble_dphi_phi_coeff(mesh, rt, d_disc) (assembly.hpp:113-136) -> (G^1, G^2);
+  /// d_disc is K x N, k-major.
+  std::pair<SparseOperator, SparseOperator> assemble_dphi_phi_coeff(const std::vector<double>& d_disc) const {
+    check_d(d_disc);
+    auto g = [&](int m) {
+      return csc_call(block_dim(), [&](int64_t* nnz, int32_t* cp, int32_t* ri, double* v, int64_t cap) {
+        return ldg_assemble_dphi_phi_coeff(h_.get(), d_disc.data(), m, nnz, cp, ri, v, cap);
+      });
+    };
+    return {g(1), g(2)};
+  }
+
+  /// assemble_edge_avg_coeff_nu(mesh, m, d_disc, sel_int, sel_dir, rt)
+  /// (assembly.hpp:214-252) -> (R^m, R_D^m).
+  std::pair<SparseOperator, SparseOperator> assemble_edge_avg_coeff_nu(int m, const std::vector<double>& d_disc) const {
+    check_d(d_disc);
+    auto r = [&](int dir) {
+      return csc_call(block_dim(), [&](int64_t* nnz, int32_t* cp, int32_t* ri, double* v, int64_t cap) {
+        return ldg_assemble_edge_avg_coeff_nu(h_.get(), d_disc.data(), m, dir, nnz, cp, ri, v, cap);
+      });
+    };
+    return {r(0), r(1)};
+  }
 
   /// system.hpp:99-107
   SystemState initial_state() const {
@@ -213,6 +295,21 @@ class LdgSystem {
  private:
   LdgSystem(ldg_handle* h, ProblemSpec spec) : h_(h), spec_(std::move(spec)) { load_info(); }
   void load_info() { detail::check(ldg_get_info(h_.get(), &info_), h_.get()); }
+  void check_d(const std::vector<double>& d) const {
+    if (d.size() != static_cast<size_t>(block_dim())) throw std::invalid_argument("coefficient matrix shape mismatch");
+  }
+  template <typename F>
+  SparseOperator csc_call(int n, F&& call) const {
+    SparseOperator op;
+    op.rows = op.cols = n;
+    int64_t nnz = 0;
+    detail::check(call(&nnz, nullptr, nullptr, nullptr, 0), h_.get());
+    op.outer.resize(static_cast<size_t>(n) + 1);
+    op.inner.resize(static_cast<size_t>(nnz));
+    op.values.resize(static_cast<size_t>(nnz));
+    detail::check(call(&nnz, op.outer.data(), op.inner.data(), op.values.data(), nnz), h_.get());
+    return op;
+  }
 
   std::unique_ptr<ldg_handle, detail::HandleDeleter> h_;
   ProblemSpec spec_;
