@@ -106,6 +106,17 @@ typedef struct ldg_handle ldg_handle;
 int ldg_reference_tensors(int n_local, double* m, double* h, double* g, double* sd, double* so, double* rd,
                           double* ro);
 
+/* The RefTensors argument of the reference's LdgSystem(mesh, spec, rt)
+ * (system.hpp:67): replaces the handle's own reference tensors (same layout
+ * as ldg_reference_tensors; rd / ro may be NULL -- R^m is assembled in the
+ * exact rank-Q edge form).  With the tensors of the caller's
+ * build_ref_tensors, every static block and G^m come out of the same
+ * tables the reference multiplies, so the stored patterns of
+ * ldg_export_operator_csc coincide with the reference's to the last
+ * explicit zero.  Invalidates the assembled operators. */
+int ldg_set_reference_tensors(ldg_handle* h, const double* m, const double* hh, const double* g, const double* sd,
+                              const double* so, const double* rd, const double* ro);
+
 /* Selects the CUDA device used by handles created afterwards on this thread
  * (one process per GPU: the rank's local device). */
 int ldg_set_device(int device);

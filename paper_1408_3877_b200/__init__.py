@@ -96,6 +96,7 @@ _lib = None
 _SIGNATURES = {
     "ldg_reference_tensors": (C.c_int, [C.c_int] + [_dp] * 7),
     "ldg_set_device": (C.c_int, [C.c_int]),
+    "ldg_set_reference_tensors": (C.c_int, [_H] + [_dp] * 7),
     "ldg_create": (C.c_int, [_dp, C.c_int, _ip, C.c_int, _ip, C.c_int, C.POINTER(_Problem), C.POINTER(_H)]),
     "ldg_create_square": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(_Problem),
                                     C.POINTER(_H)]),
@@ -387,6 +388,15 @@ class LdgSystem:
         self._check(lib.ldg_export_operator(self._h, which, C.byref(nnz), r.ctypes.data_as(_lp),
                                             c.ctypes.data_as(_lp), _d(v), nnz.value))
         return r, c, v
+
+    def set_reference_tensors(self, rt: dict):
+        """The caller's RefTensors (the rt of LdgSystem(mesh, spec, rt), system.hpp:67):
+        dict with m, h, g, sd, so (and optionally rd, ro) in the reference layout."""
+        arrs = {k: np.ascontiguousarray(rt[k], dtype=np.float64) for k in ("m", "h", "g", "sd", "so")}
+        opt = {k: (np.ascontiguousarray(rt[k], dtype=np.float64) if k in rt else None) for k in ("rd", "ro")}
+        self._check(load_library().ldg_set_reference_tensors(
+            self._h, *[_d(arrs[k]) for k in ("m", "h", "g", "sd", "so")],
+            *[(_d(opt[k]) if opt[k] is not None else None) for k in ("rd", "ro")]))
 
     def _csc_call(self, n: int, call):
         """Two-phase CSC export: call(nnz, colptr, rowind, vals, cap) -> scipy csc_matrix."""

@@ -268,14 +268,27 @@ __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const 
       double e1 = 0.0, e2 = 0.0;
       if (MODE == kModeE || MODE == kModeG) {
         const double* gij = s_g + (i * N + j) * N * 2;
-        double g1 = 0.0, g2 = 0.0;
+        double g1 = 0.0, g2 = 0.0, G1, G2;
+        if (MODE == kModeG) {
+          // G^m alone (exports, ldg_assemble_dphi_phi_coeff): the reference's
+          // operation order and rounding (assembly.hpp:122-129, no fused
+          // multiply-add), so its exact zeros -- dropped from G's pattern -- match
 #pragma unroll
-        for (int l = 0; l < N; ++l) {
-          g1 += dk[l] * gij[2 * l];
-          g2 += dk[l] * gij[2 * l + 1];
+          for (int l = 0; l < N; ++l) {
+            g1 = __dadd_rn(g1, __dmul_rn(dk[l], gij[2 * l]));
+            g2 = __dadd_rn(g2, __dmul_rn(dk[l], gij[2 * l + 1]));
+          }
+          G1 = __dsub_rn(__dmul_rn(b22, g1), __dmul_rn(b21, g2));
+          G2 = __dsub_rn(__dmul_rn(b11, g2), __dmul_rn(b12, g1));
+        } else {
+#pragma unroll
+          for (int l = 0; l < N; ++l) {
+            g1 += dk[l] * gij[2 * l];
+            g2 += dk[l] * gij[2 * l + 1];
+          }
+          G1 = b22 * g1 - b21 * g2;
+          G2 = b11 * g2 - b12 * g1;
         }
-        const double G1 = b22 * g1 - b21 * g2;
-        const double G2 = b11 * g2 - b12 * g1;
         if (MODE == kModeE) {
           e1 = -G1;
           e2 = -G2;
@@ -594,7 +607,10 @@ __global__ void __launch_bounds__(128) k_static(DevMesh m, DevTables T, int mode
     // diagonal
     for (int ij = 0; ij < NN; ++ij) {
       const double h1 = s_h[2 * ij], h2 = s_h[2 * ij + 1];
-      const double H = (c == 0) ? (b22 * h1 - b21 * h2) : (b11 * h2 - b12 * h1);
+      // the reference's rounding (assembly.hpp:100-101, no fused multiply-add):
+      // its exact zeros -- dropped from H's pattern -- come out as exact zeros here
+      const double H = (c == 0) ? __dsub_rn(__dmul_rn(b22, h1), __dmul_rn(b21, h2))
+                                : __dsub_rn(__dmul_rn(b11, h2), __dmul_rn(b12, h1));
       double v = 0.0;
       switch (mode) {
         case kStM: v = 2.0 * g[kArea * Kp + k] * s_m[ij]; break;

@@ -543,6 +543,38 @@ int ldg_reference_tensors(int n_local, double* m, double* h, double* g, double* 
   });
 }
 
+int ldg_set_reference_tensors(ldg_handle* H, const double* m, const double* hh, const double* g, const double* sd,
+                              const double* so, const double* rd, const double* ro) {
+  if (!H || !m || !hh || !g || !sd || !so) return LDG_EINVAL;
+  return guarded(H, [&] {
+    Team& T = H->team;
+    const int N = T.h0().N;
+    const size_t n2 = static_cast<size_t>(N) * N, n3 = n2 * N;
+    ldgb::RefTensors rt;
+    rt.n = N;
+    rt.m.assign(m, m + n2);
+    rt.h.assign(hh, hh + 2 * n2);
+    rt.g.assign(g, g + 2 * n3);
+    rt.sd.assign(sd, sd + 3 * n2);
+    rt.so.assign(so, so + 9 * n2);
+    if (rd) rt.rd.assign(rd, rd + 3 * n3);  // R^m uses the exact rank-Q edge form
+    if (ro) rt.ro.assign(ro, ro + 9 * n3);
+    LDG_CUDA(cudaStreamSynchronize(T.stream));
+    for (auto& rp : T.ranks) {
+      Handle& h = *rp;
+      ldgb::HostTables tb = ldgb::build_tables(h.p, &rt);
+      if (tb.data.size() != h.tables.data.size()) throw Error(LDG_EINVAL, "reference tensor layout mismatch");
+      h.tables = std::move(tb);
+      // in place: the same-degree multigrid levels share this buffer (dtab copies)
+      LDG_CUDA(cudaMemcpy(h.tab.ptr, h.tables.data.data(), sizeof(double) * h.tables.data.size(),
+                          cudaMemcpyHostToDevice));
+      const ldgb::FTables F = ldgb::build_f32_tables(h.tables);
+      LDG_CUDA(cudaMemcpy(h.ftab.ptr, F.data.data(), sizeof(float) * F.data.size(), cudaMemcpyHostToDevice));
+      h.assembled = false;
+    }
+  });
+}
+
 int ldg_set_device(int device) {
   return guarded(nullptr, [&] { LDG_CUDA(cudaSetDevice(device)); });
 }

@@ -306,7 +306,7 @@ std::vector<double> invert(std::vector<double> a, int n) {
 
 }  // namespace
 
-HostTables build_tables(int p) {
+HostTables build_tables(int p, const RefTensors* caller_rt) {
   if (p < 0 || p > kMaxP) throw std::invalid_argument("polynomial order must be zero to four");
   HostTables ht;
   TableLayout& L = ht.lay;
@@ -319,7 +319,8 @@ HostTables build_tables(int p) {
   L.R = static_cast<int>(proj.w.size());
   L.Qe = static_cast<int>(exact.w.size());
   L.Qb = static_cast<int>(bnd.w.size());
-  const RefTensors rt = reference_tensors(N);
+  const RefTensors rt = caller_rt ? *caller_rt : reference_tensors(N);
+  if (rt.n != N) throw std::invalid_argument("reference tensor size mismatch");
 
   long off = 0;
   auto take = [&off](long n) {

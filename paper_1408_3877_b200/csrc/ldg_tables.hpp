@@ -72,7 +72,9 @@ struct HostTables {
   std::vector<double> data;
 };
 
-HostTables build_tables(int p);
+// caller_rt: the caller's RefTensors (the rt argument of the reference's
+// LdgSystem(mesh, spec, rt), system.hpp:67) instead of the library's own
+HostTables build_tables(int p, const RefTensors* caller_rt = nullptr);
 
 // FP32 copies of the transposed static tables for the mixed-precision
 // multigrid smoother (ldg_smooth.cu), rows padded to NF = N rounded up to 4

@@ -78,6 +78,12 @@ struct SystemBlocks {
   std::vector<double> v;      // [-J_D^1; -J_D^2; eta K_D - K_N + L]
 };
 
+/// RefTensors (reftensors.hpp:25-50): the same flat index layout.
+struct RefTensors {
+  int n = 0;
+  std::vector<double> m, h, g, sd, so, rd, ro;
+};
+
 /// Block CSR of an operator: N x N row-major blocks, block rows in the
 /// reference's element order.
 struct BlockOperator {
@@ -171,6 +177,16 @@ class LdgSystem {
     b.v.resize(3u * static_cast<size_t>(block_dim()));
     detail::check(ldg_export_vector(h_.get(), LDG_VEC_V, b.v.data(), static_cast<int64_t>(b.v.size())), h_.get());
     return b;
+  }
+
+  /// The rt of the reference's LdgSystem(mesh, spec, rt) (system.hpp:67): the
+  /// device operators are then built from the caller's tensors.
+  void set_reference_tensors(const RefTensors& rt) const {
+    if (rt.n != n_local()) throw std::invalid_argument("reference tensor size mismatch");
+    detail::check(ldg_set_reference_tensors(h_.get(), rt.m.data(), rt.h.data(), rt.g.data(), rt.sd.data(),
+                                            rt.so.data(), rt.rd.empty() ? nullptr : rt.rd.data(),
+                                            rt.ro.empty() ? nullptr : rt.ro.data()),
+                  h_.get());
   }
 
   /// The device half of build_blocks(t): projection, assembly, right-hand side.

@@ -72,6 +72,8 @@ def _pair(name, ld):
     case.assemble(T_OPS)
     spec = ld.ProblemSpec(**BASE, eta=1.0, boundary=MIXED)
     s = ld.LdgSystem.square(dim, p, spec, jitter=jitter, seed=0)
+    # the reference's own RefTensors, as its LdgSystem(mesh, spec, rt) receives them
+    s.set_reference_tensors(R.ref_tensors(O.local_dof_count(p)))
     s.assemble(T_OPS)
     return s, case, mesh
 
@@ -92,6 +94,21 @@ def test_csc_export_is_the_reference_storage(name, ld):
     for op in OPS:
         cp, ri, v = case.op_csc(op)
         _same_csc(s.operator_csc(op), cp, ri, v, f"{name}/{op}")
+
+
+@pytest.mark.parametrize("name", ["fk16_p2", "jitter12_p3"])
+def test_csc_export_with_library_tensors(name, ld):
+    """Without the caller's tensors (the library's own build_ref_tensors, equal to
+    the reference's to ~1e-14 but not bit for bit): A's pattern is still the
+    reference's (its M blocks drop the same exact zeros; every other block of A
+    is stored whole), values within 1e-12."""
+    dim, p, jitter = CASES[name]
+    s0, case, _ = _pair(name, ld)
+    spec = ld.ProblemSpec(**BASE, eta=1.0, boundary=MIXED)
+    s = ld.LdgSystem.square(dim, p, spec, jitter=jitter, seed=0)
+    s.assemble(T_OPS)
+    for op in ("A", "mass", "s", "sd", "q1", "qn2", "r1", "rd2"):
+        _same_csc(s.operator_csc(op), *case.op_csc(op), f"{name}/{op} (library tensors)")
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
@@ -151,9 +168,12 @@ def test_cpp_mirror_build_blocks_returns_reference_csc(ld, tmp_path):
     D = np.random.default_rng(9).uniform(0.5, 1.5, mesh.num_t * O.local_dof_count(p))
     dfile = tmp_path / "d.bin"
     D.tofile(dfile)
+    rt = R.ref_tensors(O.local_dof_count(p))
+    rtfile = tmp_path / "rt.bin"
+    np.concatenate([rt[k] for k in ("m", "h", "g", "sd", "so")]).tofile(rtfile)
     pre = str(tmp_path / "out")
-    res = subprocess.run([exe, str(dim), str(p), repr(T_OPS), pre, str(dfile)], capture_output=True, text=True,
-                         timeout=300)
+    res = subprocess.run([exe, str(dim), str(p), repr(T_OPS), pre, str(dfile), str(rtfile)], capture_output=True,
+                         text=True, timeout=300)
     assert res.returncode == 0, res.stderr
 
     def load(name):

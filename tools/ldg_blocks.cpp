@@ -4,7 +4,11 @@
 // the per-operator results assemble_dphi_phi_coeff / assemble_edge_avg_coeff_nu
 // (assembly.hpp:113-136, 214-252) for that D, as raw little-endian arrays.
 //
-//   ldg_blocks dim p t out_prefix [d_file (K*N doubles, k-major)]
+//   ldg_blocks dim p t out_prefix [d_file (K*N doubles, k-major) [rt_file]]
+//
+// rt_file: the caller's reference tensors m | h | g | sd | so (raw doubles,
+// reftensors.hpp layout), passed to set_reference_tensors as the reference's
+// LdgSystem(mesh, spec, rt) receives its rt.
 //
 // Files: <prefix>.A.{outer,inner}.i32 / .A.values.f64, <prefix>.V.f64 and,
 // with d_file, <prefix>.{G1,G2,R1,RD1,R2,RD2}.{outer,inner}.i32 / .values.f64.
@@ -54,6 +58,23 @@ int main(int argc, char** argv) {
     spec.g_n = lb::coeff(LDG_FN_BASE_GN);
     spec.boundary = {{1, lb::Bc::kDirichlet}, {2, lb::Bc::kDirichlet}, {3, lb::Bc::kNeumann}, {4, lb::Bc::kNeumann}};
     lb::LdgSystem sys = lb::LdgSystem::square(dim, p, spec);
+    if (argc > 6) {  // the caller's RefTensors: m | h | g | sd | so, raw doubles
+      lb::RefTensors rt;
+      const size_t n = static_cast<size_t>(sys.n_local());
+      rt.n = static_cast<int>(n);
+      rt.m.resize(n * n);
+      rt.h.resize(2 * n * n);
+      rt.g.resize(2 * n * n * n);
+      rt.sd.resize(3 * n * n);
+      rt.so.resize(9 * n * n);
+      FILE* f = std::fopen(argv[6], "rb");
+      bool ok = f != nullptr;
+      for (auto* v : {&rt.m, &rt.h, &rt.g, &rt.sd, &rt.so})
+        ok = ok && std::fread(v->data(), sizeof(double), v->size(), f) == v->size();
+      if (f) std::fclose(f);
+      if (!ok) throw std::invalid_argument("cannot read the reference tensor file");
+      sys.set_reference_tensors(rt);
+    }
     const lb::SystemBlocks b = sys.build_blocks(t);
     dump_op(prefix, "A", b.a);
     dump(prefix + ".V.f64", b.v);
