@@ -49,6 +49,11 @@ WORKLOADS = {
 }
 
 
+# weak scaling: the rank count at which the workload's own mesh is reached
+# (C4 is quoted on 8 GPUs; C5's weak series is dim = 4096 sqrt(P/8))
+WEAK_ANCHOR = {"c4": 8, "c5": 8}
+
+
 def n_of(p):
     return (p + 1) * (p + 2) // 2
 
@@ -456,8 +461,10 @@ def run_ours(args):
     dim1, ps, dt, jitter, boundary, desc = WORKLOADS[args.workload]
     if args.p is not None:
         ps = [int(x) for x in args.p.split(",")]
-    # N > 1: strips of one FK(dim) mesh, dim chosen for ~dim1^2 elements per GPU (weak scaling)
-    dim = strips.weak_dim(dim1, world)
+    # strips of one FK(dim) mesh: weak scaling keeps the elements per GPU of the
+    # workload's anchor (C4/C5: their 8-GPU size), strong
+    # scaling keeps the mesh
+    dim = strips.scaled_dim(dim1, world, args.scaling, WEAK_ANCHOR.get(args.workload, 1))
     spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
                           boundary=boundary)
     opts = ld.SolverOptions()
@@ -597,7 +604,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: analytic c, d(t), f(t) of BASELINE.json; FK mesh generated on device",
             "config": dict(config_of(args.workload, dim, ps, dt, world), **{
                        "l2": "flushed (256 MB write) before every timed step; p>=2 working sets exceed L2",
@@ -635,6 +642,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--p", default=None, help="comma-separated degrees (overrides the workload's sweep)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = fixed elements per GPU (the workload's anchor size), strong = fixed mesh")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi sampler (diagnostics only)")
     ap.add_argument("--krylov", type=int, default=None, help="0 FGMRES (default), 1 BiCGStab")

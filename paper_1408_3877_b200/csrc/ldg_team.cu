@@ -243,10 +243,16 @@ template <typename F>
 void reduce_dots(Team& T, int nd, F launch, double* out, int level = 0) {
   if (nd > kMaxRed || T.nlocal() > kMaxLocalRanks) throw Error(LDG_EINVAL, "reduction too large");
   for (auto& rp : T.ranks) launch(level_of(*rp, level));
-  if (T.nlocal() == 1 && T.size == 1) {
-    LDG_CUDA(cudaMemcpyAsync(T.red_host, dots_result(level_of(T.h0(), level)), sizeof(double) * nd,
-                             cudaMemcpyDeviceToHost, T.stream));
+  if (T.nlocal() == 1) {
+    // one rank per process (or one GPU): the partials stay on the device, one
+    // in-place ncclAllReduce across the processes, one read of the sums
+    double* part = dots_result(level_of(T.h0(), level));
+    if (T.nccl && T.size > 1)
+      LDG_NCCL(ncclAllReduce(part, part, nd, ncclDouble, ncclSum, static_cast<ncclComm_t>(T.nccl), T.stream));
+    LDG_CUDA(cudaMemcpyAsync(T.red_host, part, sizeof(double) * nd, cudaMemcpyDeviceToHost, T.stream));
   } else {
+    // virtual ranks of one process: summed on the host in rank order
+    // (deterministic), then across processes
     // rank r's partial sums in slot r + 1 of the scratch (slot 0: the result)
     for (int r = 0; r < T.nlocal(); ++r)
       LDG_CUDA(cudaMemcpyAsync(T.red_all.ptr + kMaxRed * (r + 1), dots_result(level_of(*T.ranks[r], level)),

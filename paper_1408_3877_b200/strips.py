@@ -74,3 +74,21 @@ def weak_dim(base_dim: int, size: int) -> int:
         return base_dim
     unit = 32 * size
     return int(math.ceil(base_dim * math.sqrt(size) / unit)) * unit
+
+
+def scaled_dim(base_dim: int, size: int, scaling: str = "weak", anchor: int = 1) -> int:
+    """Global FK dim of a scaling run on `size` ranks.
+
+    strong: the mesh is fixed (base_dim; every rank owns base_dim / size
+    columns).  weak: about base_dim^2 / anchor elements per rank, i.e.
+    dim = base_dim * sqrt(size / anchor) (config 5 is anchored
+    at 8 GPUs, dim = 4096 sqrt(P/8) -> 1448, 2048, 2896, 4096), rounded up so
+    every rank owns a multiple of 32 columns (multigrid depth)."""
+    if scaling == "strong":
+        if base_dim % size:
+            raise ValueError(f"FK {base_dim} does not split into {size} equal strips")
+        return base_dim
+    if scaling != "weak":
+        raise ValueError(f"unknown scaling {scaling!r}")
+    unit = 32 * size
+    return int(math.ceil(base_dim * math.sqrt(size / anchor) / unit - 1e-9)) * unit
