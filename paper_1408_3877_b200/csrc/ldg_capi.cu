@@ -1067,6 +1067,7 @@ int ldg_initial_state(ldg_handle* H) {
       LDG_CUDA(cudaMemsetAsync(h.Y.ptr, 0, sizeof(double) * 3 * h.vec_len(), T.stream));
       ldgb::launch_project(h, h.prob.c0, 0.0, h.rule_ptr(), h.rule_R(), h.Y.ptr + 2 * h.vec_len(), h.K);
       h.t = 0.0;
+      h.hist_ok = false;
     }
     LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
@@ -1077,7 +1078,10 @@ int ldg_set_state(ldg_handle* H, const double* y, double t) {
   return guarded(H, [&] {
     Team& T = H->team;
     scatter_from_host(T, y, 3, [](Handle& h) { return h.Y.ptr; });
-    for (auto& rp : T.ranks) rp->t = t;
+    for (auto& rp : T.ranks) {
+      rp->t = t;
+      rp->hist_ok = false;
+    }
   });
 }
 
@@ -1168,6 +1172,13 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
       // preconditioner setup (team_solve waits for it before reading Y)
       const size_t cnt = 3L * h0.K * h0.N;
       if (!h0.host_stage.ptr) h0.host_stage.alloc(cnt, &h0.bytes);
+      if (!h0.host_in.ptr) {
+        h0.host_in.alloc(cnt, &h0.bytes);
+        h0.in_same.alloc(1, &h0.bytes);
+      }
+      // a caller's time loop hands back the last output: then the solver's
+      // extrapolated start stays valid (checked on the device, bit for bit)
+      const bool cont = h0.hist_ok && h0.stage_is_output && t == h0.t && !mapped_host(y_in);
       if (!T.in_stream) {
         LDG_CUDA(cudaStreamCreateWithFlags(&T.in_stream, cudaStreamNonBlocking));
         for (auto& e : T.in_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1178,14 +1189,17 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
         // pinned + mapped host buffer: the layout kernel reads it over PCIe
         ldgb::launch_kmajor_to_soa(h0, yd, 3, h0.Y.ptr, T.in_stream);
       } else {
-        LDG_CUDA(cudaMemcpyAsync(h0.host_stage.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice,
-                                 T.in_stream));
-        ldgb::launch_kmajor_to_soa(h0, h0.host_stage.ptr, 3, h0.Y.ptr, T.in_stream);
+        LDG_CUDA(cudaMemcpyAsync(h0.host_in.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice, T.in_stream));
+        if (cont) ldgb::launch_same(h0, cnt, h0.host_in.ptr, h0.host_stage.ptr, h0.in_same.ptr, T.in_stream);
+        ldgb::launch_kmajor_to_soa(h0, h0.host_in.ptr, 3, h0.Y.ptr, T.in_stream);
       }
       LDG_CUDA(cudaEventRecord(T.in_ev[1], T.in_stream));
       T.y_pending = true;
+      h0.hist_ok = cont;
+      h0.hist_same = cont ? h0.in_same.ptr : nullptr;
     } else {
       scatter_from_host(T, y_in, 3, [](Handle& h) { return h.Y.ptr; });
+      for (auto& rp : T.ranks) rp->hist_ok = false;
     }
     for (auto& rp : T.ranks) rp->t = t;
     run_steps(T, dt, nsteps, o, st);
@@ -1196,6 +1210,7 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
       } else {
         ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
         LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
+        h0.stage_is_output = true;
       }
     } else {
       gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.Y.ptr); }, 3, y_out);
@@ -1217,7 +1232,10 @@ int ldg_solve_stationary(ldg_handle* H, double t, const ldg_solver_opts* opts, l
     if (st) *st = ldg_step_stats{};
     ldgb::team_assemble(T, t);
     ldgb::team_solve(T, 0.0, 1.0, o, st);
-    for (auto& rp : T.ranks) rp->t = t;
+    for (auto& rp : T.ranks) {
+      rp->t = t;
+      rp->hist_ok = false;
+    }
     LDG_CUDA(cudaStreamSynchronize(T.stream));
   });
 }

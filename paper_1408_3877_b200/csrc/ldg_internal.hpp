@@ -100,6 +100,17 @@ struct Handle {
   DBuf<double> Sst;      // 4 * N*N * Kp
   DBuf<double> Vv;       // 3 * N * Kp
   DBuf<double> Y, Yold;  // 3 * N * Kp
+  // initial guess of the next implicit-Euler solve: C^{n-1} of the last step
+  // (Chist, time hist_t, step hist_dt) extrapolates C^n linearly in time;
+  // valid only while Y is the output of that step (any external state write
+  // clears hist_ok)
+  DBuf<double> Chist;
+  double hist_t = 0.0, hist_dt = 0.0;
+  bool hist_ok = false;
+  const int* hist_same = nullptr;  // host-buffer call: device flag "uploaded state == last output"
+  DBuf<int> in_same;
+  DBuf<double> host_in;            // k-major upload of a host state (host_stage keeps the last output)
+  bool stage_is_output = false;
   double t = 0.0;
   double t_assembled = -1.0;
   bool assembled = false;
@@ -271,6 +282,8 @@ void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double*
 void launch_bjac_setup(Handle& h, double wm, double dt);
 void launch_bjac_apply(Handle& h, const double* x, double* y);
 void launch_axpby(Handle& h, long n, double a, const double* x, double b, double* y);
+void launch_extrap(Handle& h, long n, double r, const double* c, const double* cprev, const int* same, double* out);
+void launch_same(Handle& h, long n, const double* a, const double* b, int* same, cudaStream_t stream);
 void launch_dots(Handle& h, long n, int ndots, const double* const* xs, const double* const* ys, double* out_host);
 void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev);
 void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa, cudaStream_t stream = nullptr);

@@ -366,6 +366,12 @@ void smooth(Team& T, int level, bool f32, double wm, double dt, Vec b, Vec x) {
 
 int levels(Team& T) { return 1 + static_cast<int>(T.h0().coarse.size()); }
 
+// linear-in-time initial guess of the Euler solves (team_solve); LDG_EXTRAP=0 off
+bool extrapolate_guess() {
+  static const bool on = env_or("LDG_EXTRAP", 1) != 0;
+  return on;
+}
+
 // The mixed-precision (f32) smoother runs every level through three
 // operations: stage 1, stage 2 with the block-Jacobi update (x ping-ponging
 // between two buffers) and the residual-free first sweep.  Kernel shape by
@@ -1244,9 +1250,18 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
     LDG_CUDA(cudaStreamWaitEvent(T.stream, T.in_ev[1], 0));
     T.y_pending = false;
   }
+  // Krylov start: C^n, or for a continued time integration the linear
+  // extrapolation C^n + (dt / dt_prev)(C^n - C^{n-1}) (an O(dt^2) guess;
+  // the stopping rule is relative to the right-hand side, so a smaller
+  // initial residual saves iterations at the same final accuracy)
+  const bool extrap = wm != 0.0 && extrapolate_guess() && T.h0().hist_ok &&
+                      std::fabs(T.h0().t - (T.h0().hist_t + T.h0().hist_dt)) <= 1e-12 * std::max(1.0, std::fabs(T.h0().t));
   each(T, 0, [&](Handle& h) {
     const long n = h.vec_len();
     LDG_CUDA(cudaMemcpyAsync(h.Yold.ptr, h.Y.ptr, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, T.stream));
+    if (extrap) launch_extrap(h, n, dt / h.hist_dt, vp(h, kCold), h.Chist.ptr, h.hist_same, vp(h, kC));
+    h.hist_ok = false;
+    h.hist_same = nullptr;
     // Schur right-hand side b = wm M C^n + dt (V_C - sum E^m M^-1 V_Z^m): t = M^-1 V_Z (local)
     launch_stage1(h, h.Vv.ptr, 1.0, nullptr, 0.0, h.tz.ptr);
   });
@@ -1295,6 +1310,16 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
     launch_lincomb3(h, n3, 1.0, h.full_y.ptr, -1.0, h.full_r.ptr, 0.0, nullptr, h.full_y.ptr);
   });
   const double res = std::sqrt(sq_norm3(T, kFullY)) / std::max(rhs_norm, 1.0);
+  if (wm != 0.0 && extrapolate_guess()) {  // C^n becomes the next step's C^{n-1}
+    each(T, 0, [&](Handle& h) {
+      if (!h.Chist.ptr) h.Chist.alloc(h.vec_len(), &h.bytes);
+      LDG_CUDA(cudaMemcpyAsync(h.Chist.ptr, vp(h, kCold), sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice,
+                               T.stream));
+      h.hist_t = h.t;
+      h.hist_dt = dt;
+      h.hist_ok = res <= contract;
+    });
+  }
   if (st) {
     st->iterations += it;
     st->applies += applies;

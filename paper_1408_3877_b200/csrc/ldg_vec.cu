@@ -353,6 +353,38 @@ void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, con
   ++h.launches;
 }
 
+// out = (1 + r) c - r c_prev, or c where *same == 0 (extrapolated Krylov
+// start; `same` flags a host-buffer state that continues the last output)
+__global__ void k_extrap(long n, double r, const double* __restrict__ c, const double* __restrict__ cprev,
+                         const int* __restrict__ same, double* __restrict__ out) {
+  const bool on = same == nullptr || *same != 0;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    out[i] = on ? fma(r, c[i] - cprev[i], c[i]) : c[i];
+}
+
+// *same = 0 unless a[i] == b[i] for every i (bitwise state continuity)
+__global__ void k_same(long n, const double* __restrict__ a, const double* __restrict__ b, int* same) {
+  bool eq = true;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    eq &= __double_as_longlong(a[i]) == __double_as_longlong(b[i]);
+  if (__syncthreads_and(eq) == 0 && threadIdx.x == 0) *same = 0;
+}
+
+void launch_extrap(Handle& h, long n, double r, const double* c, const double* cprev, const int* same, double* out) {
+  k_extrap<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, r, c, cprev, same, out);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_same(Handle& h, long n, const double* a, const double* b, int* same, cudaStream_t stream) {
+  LDG_CUDA(cudaMemsetAsync(same, 0xff, sizeof(int), stream));
+  k_same<<<kRedBlocks * 4, 256, 0, stream>>>(n, a, b, same);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
 void launch_axpby(Handle& h, long n, double a, const double* x, double b, double* y) {
   k_axpby<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, a, x, b, y);
   LDG_CUDA(cudaGetLastError());

@@ -234,3 +234,40 @@ def test_c2_default_solver_reaches_tight_solution(p, ld):
         y, _ = s.get_state()
         rel = np.linalg.norm(y - tight[i]) / np.linalg.norm(tight[i])
         assert rel <= STATE_TOL, f"p={p} step {i + 1}: {rel:.3e} ({st['iterations']} iterations)"
+
+
+def test_extrapolated_start_host_loop_matches_device_loop(ld):
+    """The Krylov start of a continued time integration is the linear
+    extrapolation 2 C^n - C^{n-1} (team_solve).  A caller's host-buffer time
+    loop (ldg_euler_steps_host, output handed back as the next input) keeps it:
+    the continuation is detected on the device bit for bit, so the host loop
+    reproduces the device loop exactly (same states, same iteration counts);
+    a state that does not continue the last output falls back to C^n."""
+    dim, p, dt = 64, 2, 1.0 / 20
+    dev = ld.LdgSystem.square(dim, p, ld.BASELINE_SPEC)
+    y0, _ = dev.initial_state()
+    dev_states, dev_its = [], []
+    for _ in range(5):
+        st = dev.euler_steps(dt, 1)
+        dev_its.append(st["iterations"])
+        dev_states.append(dev.get_state()[0])
+    host = ld.LdgSystem.square(dim, p, ld.BASELINE_SPEC)
+    host.initial_state()
+    yin = np.ascontiguousarray(y0.copy())
+    yout = np.empty_like(yin)
+    t = 0.0
+    for i in range(5):
+        st = host.euler_steps_host(yin.ctypes.data, t, dt, 1, yout.ctypes.data)
+        t += dt
+        assert st["iterations"] == dev_its[i], (i, st["iterations"], dev_its[i])
+        assert np.array_equal(yout, dev_states[i]), f"step {i + 1}: max |diff| {np.abs(yout - dev_states[i]).max()}"
+        yin[:] = yout
+    assert sum(dev_its[1:]) < 4 * dev_its[0], dev_its  # the extrapolated starts need fewer iterations
+    # a state that does not continue the last output: the plain start, same answer as set_state + step
+    ypert = yin * (1.0 + 1e-3)
+    st = host.euler_steps_host(ypert.ctypes.data, t, dt, 1, yout.ctypes.data)
+    ref = ld.LdgSystem.square(dim, p, ld.BASELINE_SPEC)
+    ref.set_state(ypert, t)
+    ref.euler_steps(dt, 1)
+    yr, _ = ref.get_state()
+    assert np.linalg.norm(yout - yr) / np.linalg.norm(yr) <= 1e-12
