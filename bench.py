@@ -472,16 +472,27 @@ def run_ours(args):
         opts.krylov = args.krylov
     if args.restart is not None:
         opts.restart = args.restart
-    systems = []
-    for p in ps:
+    def make(p):
         if world > 1:
             ids = [ld.nccl_unique_id() if rank == 0 else None]
             torch.distributed.broadcast_object_list(ids, src=0)
             s = ld.LdgSystem.square_dist(dim, p, spec, rank, world, ids[0], jitter=jitter, seed=0)
         else:
             s = ld.LdgSystem.square(dim, p, spec, jitter=jitter, seed=0)
+        return s
+
+    systems = [make(p) for p in ps]
+    for s in systems:
         s.initial_state()
-        systems.append(s)
+    # e2e twins: the same time integration driven through host buffers (the
+    # C ABI call a caller's time loop makes), so their timed steps are the
+    # device-timed steps (same states, same solver history, same iterations)
+    twins = [make(p) for p in ps]
+    twin_io = []
+    for s in twins:
+        y0, t0 = s.initial_state()
+        pin_in = torch.from_numpy(y0).pin_memory()
+        twin_io.append([pin_in, torch.empty_like(pin_in).pin_memory(), t0])
     dof_step = sum(3 * s.num_t * s.n for s in systems)  # whole-job DOF per step (global K)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > 126 MB L2
 
@@ -500,14 +511,18 @@ def run_ours(args):
     clocks = ClockSampler(local)
     if not args.no_clocks:
         clocks.start()
-    # warm-up (W full steps)
+    def twin_step(i):
+        pin_in, pin_out, t = twin_io[i]
+        st = twins[i].euler_steps_host(pin_in.data_ptr(), t, dt, 1, pin_out.data_ptr(), opts)
+        pin_in.copy_(pin_out)
+        twin_io[i][2] = t + dt
+        return st
+
+    # warm-up (W full steps), the twins alike
     for _ in range(args.warmup):
-        for s in systems:
+        for i, s in enumerate(systems):
             s.euler_steps(dt, 1, opts)
-    barrier()
-    # the timed steps' start states: the e2e pass below replays the same K
-    # steps from them (same times, same iteration counts) through host buffers
-    starts = [s.get_state() for s in systems]
+            twin_step(i)
     barrier()
     clocks.mark()
     launches0 = sum(s.info()["launches"] for s in systems)
@@ -530,25 +545,19 @@ def run_ours(args):
     total_ms = max_over_ranks(sum(r["ms"] for r in per_p.values()))
     value = dof_step * args.steps / (total_ms * 1e-3)
 
-    # e2e through the host-buffer C ABI call (each rank copies its owned rows)
+    # e2e through the host-buffer C ABI call (each rank copies its owned rows):
+    # the twins run the same K steps as the device-timed systems above
     e2e_ms = 0.0
     h2d = 0
-    for p, s, (y, t) in zip(ps, systems, starts):
-        pin_in = torch.from_numpy(y).pin_memory()
-        pin_out = torch.empty_like(pin_in).pin_memory()
-        # untimed warm-up call: the first host-buffer call of a handle allocates
-        # its staging buffer and creates the upload stream (host stalls the
-        # device timeline); the timed calls below restart from the same state
-        s.euler_steps_host(pin_in.data_ptr(), t, dt, 1, pin_out.data_ptr(), opts)
+    e2e_iters = 0
+    for _ in range(args.steps):
+        flush.zero_()
         torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            st = s.euler_steps_host(pin_in.data_ptr(), t, dt, 1, pin_out.data_ptr(), opts)
+        for i in range(len(ps)):
+            st = twin_step(i)
             e2e_ms += st["ms_total"]
-            t += dt
-            pin_in.copy_(pin_out)
-        h2d += y.nbytes
+            e2e_iters += st["iterations"]
+    h2d = sum(io[0].numel() * io[0].element_size() for io in twin_io)
     e2e_ms = max_over_ranks(e2e_ms)
     e2e_value = dof_step * args.steps / (e2e_ms * 1e-3)
 
@@ -620,14 +629,17 @@ def run_ours(args):
                                           "max_residual": per_p[p]["residual"],
                                           "dof_updates_per_s": 3 * 2 * dim * dim * n_of(p) * args.steps /
                                           (per_p[p]["ms"] * 1e-3)} for p in ps}}),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d,
+                    "iterations": e2e_iters, "device_iterations": sum(r["iters"] for r in per_p.values()),
+                    "note": "ldg_euler_steps_host on a twin system integrating the same steps from t = 0 "
+                            "(pinned host state in, host state out, copies inside the timed region)"},
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    for s in systems:
+    for s in systems + twins:
         s.close()
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -19,6 +19,7 @@ namespace ldgb {
 
 constexpr int kMaxRed = 80;        // dot products per reduction (FGMRES basis + 1)
 constexpr int kMaxLocalRanks = 16; // ranks of one process (virtual ranks share a GPU)
+constexpr int kExtrapMax = 4;      // history of the extrapolated Euler start (team_solve)
 
 // Exceptions carry the ABI status they map to.
 struct Error : std::runtime_error {
@@ -100,14 +101,18 @@ struct Handle {
   DBuf<double> Sst;      // 4 * N*N * Kp
   DBuf<double> Vv;       // 3 * N * Kp
   DBuf<double> Y, Yold;  // 3 * N * Kp
-  // initial guess of the next implicit-Euler solve: C^{n-1} of the last step
-  // (Chist, time hist_t, step hist_dt) extrapolates C^n linearly in time;
-  // valid only while Y is the output of that step (any external state write
-  // clears hist_ok)
-  DBuf<double> Chist;
-  double hist_t = 0.0, hist_dt = 0.0;
+  // initial guess of the next implicit-Euler solve: C^{n-1}, C^{n-2} of the
+  // last steps (Chist[i] at time hist_time[i]) extrapolate C^n in time
+  // (team_solve).  hist_dev (device int) counts the valid history
+  // vectors as the device sees them; hist_ok (host) says Y is the output of
+  // the last solve at time hist_t0 + hist_dt, cleared by any external state
+  // write.  hist_same (host-buffer calls): device flag "uploaded state == last
+  // output", 0 drops the history on the device.
+  DBuf<double> Chist[kExtrapMax];  // C^{n-1}, C^{n-2}, ... (kExtrapMax)
+  DBuf<int> hist_dev;     // [0] valid history vectors, [1] order used by the last start
+  double hist_time[kExtrapMax] = {}, hist_dt = 0.0;
   bool hist_ok = false;
-  const int* hist_same = nullptr;  // host-buffer call: device flag "uploaded state == last output"
+  const int* hist_same = nullptr;
   DBuf<int> in_same;
   DBuf<double> host_in;            // k-major upload of a host state (host_stage keeps the last output)
   bool stage_is_output = false;
@@ -282,7 +287,11 @@ void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double*
 void launch_bjac_setup(Handle& h, double wm, double dt);
 void launch_bjac_apply(Handle& h, const double* x, double* y);
 void launch_axpby(Handle& h, long n, double a, const double* x, double b, double* y);
-void launch_extrap(Handle& h, long n, double r, const double* c, const double* cprev, const int* same, double* out);
+// out = Krylov start from C^n (c) and the history (ldg_vec.cu k_extrap)
+// w[o - 1][j]: Lagrange weights of order o for c (j = 0) and c_j (j >= 1)
+void launch_extrap(Handle& h, long n, int order, const double (*w)[kExtrapMax + 1], const double* c,
+                   const double* const* hist_vec, int* hist, const int* same, double* out);
+void launch_hist_shift(Handle& h, long n, const double* c, double* const* hist_vec, int* hist);
 void launch_same(Handle& h, long n, const double* a, const double* b, int* same, cudaStream_t stream);
 void launch_dots(Handle& h, long n, int ndots, const double* const* xs, const double* const* ys, double* out_host);
 void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev);

@@ -366,10 +366,14 @@ void smooth(Team& T, int level, bool f32, double wm, double dt, Vec b, Vec x) {
 
 int levels(Team& T) { return 1 + static_cast<int>(T.h0().coarse.size()); }
 
-// linear-in-time initial guess of the Euler solves (team_solve); LDG_EXTRAP=0 off
-bool extrapolate_guess() {
-  static const bool on = env_or("LDG_EXTRAP", 1) != 0;
-  return on;
+// order of the in-time extrapolated start of the Euler solves (team_solve):
+// 0 = C^n, 1 = linear, ... 4 (LDG_EXTRAP for tuning runs).  Measured on the
+// 5-step C2 bench (ms per sweep step / FGMRES iterations at p = 4): C^n 81.4 /
+// 18.0, linear 71.7 / 15.8, quadratic 61.3 / 13.0, cubic 55.9 / 11.2, quartic
+// 52.0 / 10.2, quintic 51.7 / 10.0 (p = 0, 1 already worse than quartic).
+int extrap_order() {
+  static const int o = static_cast<int>(env_or("LDG_EXTRAP", 4));
+  return o < 0 ? 0 : (o > kExtrapMax ? kExtrapMax : o);
 }
 
 // The mixed-precision (f32) smoother runs every level through three
@@ -1250,16 +1254,42 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
     LDG_CUDA(cudaStreamWaitEvent(T.stream, T.in_ev[1], 0));
     T.y_pending = false;
   }
-  // Krylov start: C^n, or for a continued time integration the linear
-  // extrapolation C^n + (dt / dt_prev)(C^n - C^{n-1}) (an O(dt^2) guess;
-  // the stopping rule is relative to the right-hand side, so a smaller
-  // initial residual saves iterations at the same final accuracy)
-  const bool extrap = wm != 0.0 && extrapolate_guess() && T.h0().hist_ok &&
-                      std::fabs(T.h0().t - (T.h0().hist_t + T.h0().hist_dt)) <= 1e-12 * std::max(1.0, std::fabs(T.h0().t));
+  // Krylov start: C^n, or for a continued time integration the Lagrange
+  // extrapolation in time of C^n and the last steps' C (order
+  // extrap_order(), limited on the device to the valid history).  The
+  // stopping rule is relative to the right-hand side, so a smaller initial
+  // residual saves iterations at the same final accuracy.
+  const Handle& H0 = T.h0();
+  const int order = wm != 0.0 && H0.hist_ok &&
+                            std::fabs(H0.t - (H0.hist_time[0] + H0.hist_dt)) <= 1e-12 * std::max(1.0, std::fabs(H0.t))
+                        ? extrap_order()
+                        : 0;
+  double w[kExtrapMax][kExtrapMax + 1] = {};
+  {
+    // nodes t_n, t_{n-1}, ... (distinct when the device says the history is valid)
+    const double tx = H0.t + dt;
+    double tn[kExtrapMax + 1] = {H0.t};
+    for (int j = 0; j < kExtrapMax; ++j) tn[j + 1] = H0.hist_time[j];
+    for (int o = 1; o <= kExtrapMax; ++o)
+      for (int j = 0; j <= o; ++j) {
+        double l = 1.0;
+        for (int m = 0; m <= o; ++m)
+          if (m != j) l *= (tn[m] != tn[j]) ? (tx - tn[m]) / (tn[j] - tn[m]) : 0.0;
+        w[o - 1][j] = l;
+      }
+  }
   each(T, 0, [&](Handle& h) {
     const long n = h.vec_len();
     LDG_CUDA(cudaMemcpyAsync(h.Yold.ptr, h.Y.ptr, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, T.stream));
-    if (extrap) launch_extrap(h, n, dt / h.hist_dt, vp(h, kCold), h.Chist.ptr, h.hist_same, vp(h, kC));
+    if (wm != 0.0 && extrap_order() > 0) {
+      if (!h.hist_dev.ptr) {
+        for (auto& b : h.Chist) b.alloc(n, &h.bytes);
+        h.hist_dev.alloc(2, &h.bytes);  // zeroed: no history
+      }
+      const double* hv[kExtrapMax];
+      for (int j = 0; j < kExtrapMax; ++j) hv[j] = h.Chist[j].ptr;
+      launch_extrap(h, n, order, w, vp(h, kCold), hv, h.hist_dev.ptr, h.hist_same, vp(h, kC));
+    }
     h.hist_ok = false;
     h.hist_same = nullptr;
     // Schur right-hand side b = wm M C^n + dt (V_C - sum E^m M^-1 V_Z^m): t = M^-1 V_Z (local)
@@ -1310,12 +1340,13 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
     launch_lincomb3(h, n3, 1.0, h.full_y.ptr, -1.0, h.full_r.ptr, 0.0, nullptr, h.full_y.ptr);
   });
   const double res = std::sqrt(sq_norm3(T, kFullY)) / std::max(rhs_norm, 1.0);
-  if (wm != 0.0 && extrapolate_guess()) {  // C^n becomes the next step's C^{n-1}
+  if (wm != 0.0 && extrap_order() > 0) {  // C^n becomes the next step's C^{n-1}
     each(T, 0, [&](Handle& h) {
-      if (!h.Chist.ptr) h.Chist.alloc(h.vec_len(), &h.bytes);
-      LDG_CUDA(cudaMemcpyAsync(h.Chist.ptr, vp(h, kCold), sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice,
-                               T.stream));
-      h.hist_t = h.t;
+      double* hv[kExtrapMax];
+      for (int j = 0; j < kExtrapMax; ++j) hv[j] = h.Chist[j].ptr;
+      launch_hist_shift(h, h.vec_len(), vp(h, kCold), hv, h.hist_dev.ptr);
+      for (int j = kExtrapMax - 1; j > 0; --j) h.hist_time[j] = h.hist_time[j - 1];
+      h.hist_time[0] = h.t;
       h.hist_dt = dt;
       h.hist_ok = res <= contract;
     });

@@ -353,14 +353,43 @@ void launch_lincomb3(Handle& h, long n, double a, const double* x, double b, con
   ++h.launches;
 }
 
-// out = (1 + r) c - r c_prev, or c where *same == 0 (extrapolated Krylov
-// start; `same` flags a host-buffer state that continues the last output)
-__global__ void k_extrap(long n, double r, const double* __restrict__ c, const double* __restrict__ cprev,
+// Krylov start of an implicit-Euler solve: Lagrange extrapolation in time of
+// C^n (c) and the history C^{n-1..n-3} at the order min(order, hist[0]),
+// dropped to the plain start c where *same == 0 (a host-buffer state that does
+// not continue the last output); the order used goes to hist[1].
+struct ExtrapArgs {
+  double w[kExtrapMax][kExtrapMax + 1];
+  const double* v[kExtrapMax];
+};
+__global__ void k_extrap(long n, int order, ExtrapArgs a, const double* __restrict__ c, int* hist,
                          const int* __restrict__ same, double* __restrict__ out) {
-  const bool on = same == nullptr || *same != 0;
+  int o = min(order, hist[0]);
+  if (same && *same == 0) o = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) hist[1] = o;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long>(gridDim.x) * blockDim.x)
-    out[i] = on ? fma(r, c[i] - cprev[i], c[i]) : c[i];
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    double r = c[i];
+    if (o > 0) {
+      const double* w = a.w[o - 1];
+      r *= w[0];
+      for (int j = 1; j <= o; ++j) r = fma(w[j], a.v[j - 1][i], r);
+    }
+    out[i] = r;
+  }
+}
+
+// after a solve from C^n: the history moves down one slot and C^n enters
+// slot 0; valid count hist[0] = 1 after a plain start, else one more
+struct HistArgs {
+  double* v[kExtrapMax];
+};
+__global__ void k_hist_shift(long n, const double* __restrict__ c, HistArgs a, int* hist) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    for (int j = kExtrapMax - 1; j > 0; --j) a.v[j][i] = a.v[j - 1][i];
+    a.v[0][i] = c[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) hist[0] = hist[1] == 0 ? 1 : min(hist[0] + 1, kExtrapMax);
 }
 
 // *same = 0 unless a[i] == b[i] for every i (bitwise state continuity)
@@ -372,8 +401,21 @@ __global__ void k_same(long n, const double* __restrict__ a, const double* __res
   if (__syncthreads_and(eq) == 0 && threadIdx.x == 0) *same = 0;
 }
 
-void launch_extrap(Handle& h, long n, double r, const double* c, const double* cprev, const int* same, double* out) {
-  k_extrap<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, r, c, cprev, same, out);
+void launch_extrap(Handle& h, long n, int order, const double (*w)[kExtrapMax + 1], const double* c,
+                   const double* const* hist_vec, int* hist, const int* same, double* out) {
+  ExtrapArgs a{};
+  for (int o = 0; o < kExtrapMax; ++o)
+    for (int j = 0; j <= kExtrapMax; ++j) a.w[o][j] = w[o][j];
+  for (int j = 0; j < kExtrapMax; ++j) a.v[j] = hist_vec[j];
+  k_extrap<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, order, a, c, hist, same, out);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
+void launch_hist_shift(Handle& h, long n, const double* c, double* const* hist_vec, int* hist) {
+  HistArgs a{};
+  for (int j = 0; j < kExtrapMax; ++j) a.v[j] = hist_vec[j];
+  k_hist_shift<<<kRedBlocks * 4, 256, 0, h.stream>>>(n, c, a, hist);
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
