@@ -526,7 +526,8 @@ def run_ours(args):
     barrier()
     clocks.mark()
     launches0 = sum(s.info()["launches"] for s in systems)
-    per_p = {p: dict(ms=0.0, ms_asm=0.0, ms_solve=0.0, iters=0, applies=0, residual=0.0) for p in ps}
+    per_p = {p: dict(ms=0.0, ms_asm=0.0, ms_solve=0.0, ms_setup=0.0, ms_krylov=0.0, iters=0, applies=0, residual=0.0)
+             for p in ps}
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -535,6 +536,8 @@ def run_ours(args):
             r = per_p[p]
             r["ms_asm"] += st["ms_assemble"]
             r["ms_solve"] += st["ms_solve"]
+            r["ms_setup"] += st["ms_setup"]
+            r["ms_krylov"] += st["ms_krylov"]
             r["ms"] += st["ms_assemble"] + st["ms_solve"]
             r["iters"] += st["iterations"]
             r["applies"] += st["applies"]
@@ -625,6 +628,8 @@ def run_ours(args):
                        "per_p": {str(p): {"ms_per_step": per_p[p]["ms"] / args.steps,
                                           "ms_assemble": per_p[p]["ms_asm"] / args.steps,
                                           "ms_solve": per_p[p]["ms_solve"] / args.steps,
+                                          "ms_solve_setup": per_p[p]["ms_setup"] / args.steps,
+                                          "ms_krylov": per_p[p]["ms_krylov"] / args.steps,
                                           "iterations_per_step": per_p[p]["iters"] / args.steps,
                                           "max_residual": per_p[p]["residual"],
                                           "dof_updates_per_s": 3 * 2 * dim * dim * n_of(p) * args.steps /

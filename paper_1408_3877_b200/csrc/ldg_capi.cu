@@ -653,6 +653,13 @@ void ldg_destroy(ldg_handle* H) {
   for (auto& e : T.in_ev)
     if (e) cudaEventDestroy(e);
   if (T.in_stream) cudaStreamDestroy(T.in_stream);
+  for (auto& e : T.setup_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& st : T.setup_stream)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
   for (auto& e : T.gs_ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t s = T.stream;

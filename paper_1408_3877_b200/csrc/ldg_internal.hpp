@@ -217,6 +217,9 @@ struct Team {
   double* gs_host = nullptr;                    // pinned: FGMRES Gram-Schmidt slots (kMaxRed x (2 kMaxRed + 1))
   cudaEvent_t gs_ev[2] = {};                    // completion of FGMRES iterations j (ping-pong)
   cudaStream_t in_stream = nullptr;             // host-buffer state upload, overlapping assembly + setup
+  cudaStream_t setup_stream[2] = {};            // multigrid setup of level 0 / of the coarse levels, overlapping
+  cudaEvent_t setup_ev[3] = {};                 // the right-hand side (team_solve): fork, two joins
+  bool setup_pending = false;
   cudaEvent_t in_ev[2] = {};                    // [0] call start, [1] state uploaded
   bool y_pending = false;                       // team_solve waits for in_ev[1] before reading Y
   std::string err;
@@ -366,6 +369,8 @@ void init_handle_tables(Handle& h, int p);  // reference tables + element rule o
 int mg_depth(int dim, int team_size);
 bool mg_build(Handle& h, int team_size);                    // false: no hierarchy for this mesh
 void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32);  // per step: coarse E, block-Jacobi
+void mg_setup_top(Handle& h, double wm, double dt, bool f32);               // level 0's part of mg_setup_step
+void mg_setup_coarse(Handle& h, double t, double wm, double dt, bool f32);  // the coarse levels' part
 void mg_restrict(Handle& fine, Handle& coarse);             // coarse.mg_b = P^T fine.mg_r
 void mg_prolong_add(Handle& fine, Handle& coarse, double* x);  // x += P coarse.mg_x
 int mg_levels(const Handle& h);

@@ -392,8 +392,18 @@ void debug_level(Handle& L, int l) {
 }
 
 void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32) {
+  mg_setup_top(h, wm, dt, f32);
+  mg_setup_coarse(h, t, wm, dt, f32);
+}
+
+void mg_setup_top(Handle& h, double wm, double dt, bool f32) {
   if (f32) mg_setup_f32_level(h, wm, dt);
   if (debug_nan()) debug_level(h, 0);
+}
+
+// every coarse level is rediscretised from d(t) on its own mesh: independent
+// of level 0 and of each other
+void mg_setup_coarse(Handle& h, double t, double wm, double dt, bool f32) {
   for (auto& cp : h.coarse) {
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);

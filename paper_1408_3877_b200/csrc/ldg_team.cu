@@ -95,7 +95,12 @@ const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
 // V(5,6) 5.6 ms / 10 iterations (V(4,5) 5.8 / 11), p = 4 V(5,7) 33.7 / 15
 // (V(5,6) 34.2 / 16); p = 0, 2, 3 unchanged (V(4,4), V(3,5), V(4,5),
 // V(6,6) elsewhere all slower; symmetric counts lose up to 2x at p = 3).
-constexpr int kPre0P[5] = {6, 5, 4, 5, 5}, kPost0P[5] = {6, 6, 6, 6, 7};
+// With the extrapolated Krylov start (fewer, so relatively more valuable,
+// V-cycles) re-swept on the 5-step C2 bench (ms per step p = 0..4): V(6,6) /
+// V(5,6) / V(4,6) / V(5,6) / V(5,7) 4.68 / 4.83 / 6.85 / 11.31 / 23.78;
+// V(6,7) everywhere 4.79 / 4.73 / 7.00 / 11.24 / 23.51; V(5,6) everywhere
+// 4.98 / 4.82 / 6.62 / 11.32 / 23.56; V(4,5), V(3,5), V(4,6) all slower.
+constexpr int kPre0P[5] = {6, 6, 5, 6, 6}, kPost0P[5] = {6, 7, 6, 7, 7};
 // level 1 V(1,1) except V(2,1) at p = 3 (with the retuned coarse levels:
 // p = 0..2 4.3 / 5.8 / 8.5 ms against 4.4 / 5.9 / 8.7 with V(2,1); V(2,2),
 // V(3,2) slower)
@@ -365,6 +370,12 @@ void smooth(Team& T, int level, bool f32, double wm, double dt, Vec b, Vec x) {
 }
 
 int levels(Team& T) { return 1 + static_cast<int>(T.h0().coarse.size()); }
+
+// multigrid setup on side streams overlapping the right-hand side (LDG_SETUP_OVERLAP=0 off)
+bool setup_overlap() {
+  static const bool on = env_or("LDG_SETUP_OVERLAP", 1) != 0;
+  return on;
+}
 
 // order of the in-time extrapolated start of the Euler solves (team_solve):
 // 0 = C^n, 1 = linear, ... 4 (LDG_EXTRAP for tuning runs).  Measured on the
@@ -755,10 +766,53 @@ int prepare_precond(Team& T, int pc, double wm, double dt, bool* f32) {
   *f32 = pc == 2;
   if (pc == 1 || pc == 3) each(T, 0, [&](Handle& h) { launch_bjac_setup(h, wm, dt); });
   if (pc >= 2) {
-    for (auto& rp : T.ranks) mg_setup_step(*rp, rp->t_assembled, wm, dt, *f32);
+    if (T.nlocal() == 1 && setup_overlap()) {
+      // one rank: level 0's block-Jacobi inverses and the coarse levels'
+      // rediscretisation run on two side streams, concurrently with each
+      // other and with the Schur right-hand side on the main stream; the
+      // Krylov loop waits for both (join_precond)
+      Handle& h = T.h0();
+      if (!T.setup_stream[0]) {
+        for (auto& st : T.setup_stream) LDG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& e : T.setup_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      LDG_CUDA(cudaEventRecord(T.setup_ev[0], T.stream));
+      for (auto& st : T.setup_stream) LDG_CUDA(cudaStreamWaitEvent(st, T.setup_ev[0], 0));
+      auto on_stream = [&](cudaStream_t st, auto&& fn) {  // the levels' launches go to st
+        std::vector<cudaStream_t> saved;
+        saved.push_back(h.stream);
+        for (auto& c : h.coarse) saved.push_back(c->stream);
+        h.stream = st;
+        for (auto& c : h.coarse) c->stream = st;
+        try {
+          fn();
+        } catch (...) {
+          h.stream = saved[0];
+          for (size_t i = 0; i < h.coarse.size(); ++i) h.coarse[i]->stream = saved[i + 1];
+          throw;
+        }
+        h.stream = saved[0];
+        for (size_t i = 0; i < h.coarse.size(); ++i) h.coarse[i]->stream = saved[i + 1];
+      };
+      on_stream(T.setup_stream[0], [&] { mg_setup_top(h, wm, dt, *f32); });
+      on_stream(T.setup_stream[1], [&] { mg_setup_coarse(h, h.t_assembled, wm, dt, *f32); });
+      LDG_CUDA(cudaEventRecord(T.setup_ev[1], T.setup_stream[0]));
+      LDG_CUDA(cudaEventRecord(T.setup_ev[2], T.setup_stream[1]));
+      T.setup_pending = true;
+    } else {
+      for (auto& rp : T.ranks) mg_setup_step(*rp, rp->t_assembled, wm, dt, *f32);
+    }
     pc = 2;
   }
   return pc;
+}
+
+// the main stream waits for the preconditioner set up on the side streams
+void join_precond(Team& T) {
+  if (!T.setup_pending) return;
+  LDG_CUDA(cudaStreamWaitEvent(T.stream, T.setup_ev[1], 0));
+  LDG_CUDA(cudaStreamWaitEvent(T.stream, T.setup_ev[2], 0));
+  T.setup_pending = false;
 }
 
 void lincomb(Team& T, double a, Vec x, double b, Vec y, double c, Vec z, Vec out) {
@@ -1319,6 +1373,7 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   int applies = 0;
   int it = 0;
   double rnorm = 0.0;
+  join_precond(T);
   LDG_CUDA(cudaEventRecord(h0.ev[3], T.stream));  // end of the per-solve setup
   if (o.krylov == 0) {
     fgmres(T, pc, f32, wm, dt, o, tol, &it, &applies, &rnorm);
@@ -1383,6 +1438,7 @@ void team_schur_apply_c(Team& T, double wm, double dt) { schur_apply(T, wm, dt, 
 void team_sweep_s2_prepare(Team& T, double wm, double dt) {
   bool f32 = false;
   prepare_precond(T, 2, wm, dt, &f32);
+  join_precond(T);
   each(T, 0, [&](Handle& L) { f_stage1(L, kPh); });
 }
 void team_sweep_s2(Team& T, double wm, double dt) {
@@ -1402,6 +1458,7 @@ int team_s2_per_vcycle(Team& T) {
 int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, double* ms_level, int max_levels) {
   bool f32 = false;
   if (prepare_precond(T, 2, wm, dt, &f32) != 2) return 0;
+  join_precond(T);
   Handle& h = T.h0();
   const int nl = levels(T);
   auto graph_time = [&](auto&& body) {
