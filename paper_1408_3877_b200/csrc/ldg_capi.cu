@@ -644,6 +644,7 @@ void ldg_destroy(ldg_handle* H) {
   if (T.stream) cudaStreamSynchronize(T.stream);
   for (auto& rp : T.ranks) {
     ldgb::mg_release(*rp);
+    for (auto& c : rp->coarse) ldgb::dense_release(*c);
     for (auto& e : rp->ev)
       if (e) cudaEventDestroy(e);
   }

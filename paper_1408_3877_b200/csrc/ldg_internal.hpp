@@ -161,6 +161,17 @@ struct Handle {
   DBuf<double> mg_s;                             // V-cycle ping-pong partner of x (fused smoother)
   DBuf<double> mg_zero;                          // zeros (Chebyshev eigenvalue estimate)
   double cheb_lmax = 0.0;                        // estimated largest eigenvalue of P^-1 S_c (0: not yet)
+  // dense coarsest level (ldg_dense.cu): -S_c as a column-major n x n matrix,
+  // its LU and inverse; dense_level on the top handle (0: none)
+  int dense_level = 0;
+  int dn_n = 0;
+  DBuf<double> dn_A, dn_inv, dn_X, dn_T, dn_zero, dn_work, dn_T2, dn_X2, dn_res;
+  DBuf<int> dn_ipiv, dn_info;
+  void* dn_solver = nullptr;                     // cusolverDnHandle_t
+  void* dn_blas = nullptr;                       // cublasHandle_t (Newton-Schulz refinement)
+  double* dn_res_host = nullptr;                 // pinned: last Newton-Schulz residual
+  bool dn_valid = false;                         // dn_inv inverts a recent operator (same wm, dt)
+  double dn_dt = 0.0, dn_wm = 0.0;
   DBuf<double> gm_V, gm_Z;                       // FGMRES basis and preconditioned basis ((m+1) and m vectors)
   int gm_m = 0, gm_req = 0;  // basis length in use, restart length it was sized for
   bool mg_f32 = true;                            // smoother on FP32 copies (precond 2) or FP64 (3)
@@ -367,6 +378,13 @@ void init_handle_tables(Handle& h, int p);  // reference tables + element rule o
 
 // multigrid (ldg_mg.cu)
 int mg_depth(int dim, int team_size);
+// dense coarsest level (ldg_dense.cu)
+long dense_max();
+bool dense_candidate(const Handle& L);
+void dense_alloc(Handle& L);
+void dense_release(Handle& L);
+void dense_setup(Handle& L, double wm, double dt, bool f32);
+void dense_solve(Handle& L, const double* b, double* x);
 bool mg_build(Handle& h, int team_size);                    // false: no hierarchy for this mesh
 void mg_setup_step(Handle& h, double t, double wm, double dt, bool f32);  // per step: coarse E, block-Jacobi
 void mg_setup_top(Handle& h, double wm, double dt, bool f32);               // level 0's part of mg_setup_step

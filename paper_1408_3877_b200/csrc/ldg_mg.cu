@@ -338,6 +338,14 @@ bool mg_build(Handle& h, int team_size) {
     fine = c.get();
     h.coarse.push_back(std::move(c));
   }
+  // dense coarsest level: the first h-level small enough (single rank)
+  for (size_t i = 0; i < h.coarse.size(); ++i) {
+    Handle& c = *h.coarse[i];
+    if (!dense_candidate(c)) continue;
+    dense_alloc(c);
+    h.dense_level = static_cast<int>(i) + 1;
+    break;
+  }
   h.mg_ready = true;
   return true;
 }
@@ -405,6 +413,8 @@ void mg_setup_top(Handle& h, double wm, double dt, bool f32) {
 // of level 0 and of each other
 void mg_setup_coarse(Handle& h, double t, double wm, double dt, bool f32) {
   for (auto& cp : h.coarse) {
+    const int lvl = static_cast<int>(&cp - &h.coarse[0]) + 1;
+    if (h.dense_level > 0 && lvl > h.dense_level) break;  // below the dense level: never visited
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);
     launch_assemble(c, kModeEdiag, c.E.ptr);
@@ -412,7 +422,8 @@ void mg_setup_coarse(Handle& h, double t, double wm, double dt, bool f32) {
       mg_setup_f32_level(c, wm, dt);
     else
       launch_bjac_setup(c, wm, dt);
-    if (debug_nan()) debug_level(c, static_cast<int>(&cp - &h.coarse[0]) + 1);
+    if (lvl == h.dense_level) dense_setup(c, wm, dt, f32);
+    if (debug_nan()) debug_level(c, lvl);
   }
 }
 

@@ -266,6 +266,29 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_bj_small(int K, long Kp,
   bj_body<P>(K, Kp, Pinv, b, omega, out, blockIdx.x, threadIdx.x);
 }
 
+// ------------------------------------------------- dense coarse operator
+// Column c of the level operator applied to the unit vector e_c (SoA index
+// c = i * Kp + k), for the dense coarsest-level solve (ldg_dense.cu): the
+// stage bodies above with blockIdx.y = column, stage 2 in residual mode with
+// b = 0, so column c of `out` is -S_c e_c.
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s1_batch(DevMesh m, DevTables T, const double* X,
+                                                              double* Tz, long stride) {
+  const long c = blockIdx.y;
+  s1_body<P>(m, T, X + c * stride, Tz + 2 * c * stride, blockIdx.x, threadIdx.x);
+}
+
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_batch(DevMesh m, DevTables T, const float* __restrict__ E,
+                                                              const double* __restrict__ D, const double* X,
+                                                              const double* Tz, const double* zero, double wm,
+                                                              double dteta, double dt, double* out, long stride) {
+  __shared__ double s_r[Cfg<P>::N][Cfg<P>::EPC];
+  const long c = blockIdx.y;
+  s2_body<P, 0>(m, T, E, D, X + c * stride, Tz + 2 * c * stride, zero, wm, dteta, dt, nullptr, 0.0, out + c * stride,
+                0, m.K, s_r, blockIdx.x, threadIdx.x);
+}
+
 // ---------------------------------------------------------------- tail
 // The coarsest levels (a few dozen elements) of a V-cycle in ONE thread block:
 // every phase (sweep stages, residual, restriction, prolongation) is a loop
@@ -438,6 +461,25 @@ void small_stage2(Handle& h, int mode, const double* x, const double* b, double 
 #undef CALL
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
+}
+
+// out[:, c] = -S_c e_c for c < ncols (X = identity, stride = N * Kp; Tz: 2
+// stride values per column; zero: stride zeros)
+void small_dense_columns(Handle& h, const double* X, double* Tz, const double* zero, double wm, double dt, double* out,
+                         int ncols) {
+  const long stride = h.vec_len();
+  const double dteta = dt * h.prob.eta;
+#define CALL(P)                                                                                              \
+  do {                                                                                                       \
+    const dim3 grid(grid_of(h.K, Cfg<P>::EPC), ncols);                                                       \
+    k_s1_batch<P><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, X, Tz, stride);                  \
+    k_s2_batch<P><<<grid, Cfg<P>::THREADS, 0, h.stream>>>(h.mesh(), h.dtab, h.E32.ptr, h.D.ptr, X, Tz, zero, \
+                                                          wm, dteta, dt, out, stride);                       \
+  } while (0)
+  LDG_DISPATCH_P(h.p, CALL)
+#undef CALL
+  LDG_CUDA(cudaGetLastError());
+  h.launches += 2;
 }
 
 void small_zero(Handle& h, const double* b, double omega, double* out) {

@@ -615,6 +615,11 @@ bool tail_level(Team& T, int l, bool f32) {
 
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   if (l == 0) set_omega(T);
+  if (l > 0 && l == T.h0().dense_level) {  // dense coarsest level (ldg_dense.cu): x = S_c^-1 b
+    Handle& L = level_of(T.h0(), l);
+    dense_solve(L, vp(L, b), vp(L, x));
+    return;
+  }
   const bool coarsest = l == levels(T) - 1;
   if (tail_level(T, l, f32) && b == kMgB && x == kMgX) {
     small_tail_vcycle(T.h0(), l, wm, dt, kOmega, pre_of(T.h0().p, l), post_of(T.h0().p, l), kCoarseSweeps);
@@ -1483,6 +1488,11 @@ int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, dou
   *ms_vcycle = graph_time([&] { vcycle(T, 0, f32, wm, dt, kP, kPh); });
   for (int l = 0; l < nl && l < max_levels; ++l) {
     const Vec b = l == 0 ? kP : kMgB, x = l == 0 ? kPh : kMgX;
+    if (l > 0 && l == h.dense_level) {  // the dense coarsest level: one solve; the levels below are never visited
+      Handle& L = level_of(h, l);
+      ms_level[l] = graph_time([&] { dense_solve(L, vp(L, b), vp(L, x)); });
+      return l + 1;
+    }
     if (fused(T, l, f32))
       ms_level[l] = graph_time([&] { sweep_f(T, l, wm, dt, b, x, kMgS); });
     else
