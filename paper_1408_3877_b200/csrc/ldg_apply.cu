@@ -532,9 +532,7 @@ void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double*
 
 void launch_bjac_setup(Handle& h, double wm, double dt) { launch_bjac(h, wm, dt, 0); }
 
-// FP32 inverses from the FP64 E of the level (multigrid smoother copies):
-// packed for the fused smoother kernels, plain SoA for the row kernels
-void launch_bjac_setup_quad(Handle& h, double wm, double dt) { launch_bjac(h, wm, dt, 2); }
+// FP32 inverses from the FP64 E of the level (row-kernel smoother copies)
 
 void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt) { launch_bjac(h, wm, dt, 1); }
 

@@ -53,7 +53,7 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
     default: { CALL(4); break; } \
   }
 
-// OUT: 0 FP64 SoA, 1 FP32 SoA, 2 FP32 packed (ldg_pack.cuh), 3 FP16 packed
+// OUT: 0 FP64 SoA, 1 FP32 SoA, 3 FP16 packed (ldg_pack.cuh)
 // scaled per element.  S: the arithmetic of the products and the elimination
 // -- FP32 for the FP16 smoother copy (OUT 3: the result is rounded to 11
 // bits anyway; FP32 issues twice the FMAs per cycle and holds half the
@@ -245,12 +245,11 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
 
 }  // namespace
 
-// Pinv (FP64 SoA), Pinv32 (FP32 SoA), Pq (FP32 packed) or Ph + Pscale (FP16
-// packed, scaled per element) from the level's FP64 E
+// Pinv (FP64 SoA), Pinv32 (FP32 SoA) or Ph + Pscale (FP16 packed, scaled per
+// element) from the level's FP64 E
 void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
   void* out = out_kind == 0   ? static_cast<void*>(h.Pinv.ptr)
               : out_kind == 1 ? static_cast<void*>(h.Pinv32.ptr)
-              : out_kind == 2 ? static_cast<void*>(h.Pq.ptr)
                               : static_cast<void*>(h.Ph.ptr);
   float* sc = out_kind == 3 ? h.Pscale.ptr : nullptr;
 #define LAUNCH(P, O) \
@@ -264,7 +263,6 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
     switch (out_kind) {                                              \
       case 0: LAUNCH(P, 0); break;                                   \
       case 1: LAUNCH(P, 1); break;                                   \
-      case 2: LAUNCH(P, 2); break;                                   \
       default: LAUNCH32(P, 3); break;                                \
     }                                                                \
   } while (0)

@@ -1103,32 +1103,16 @@ int ldg_get_state(ldg_handle* H, double* y, double* t) {
 
 namespace {
 
-// LDG_ZEROCOPY=1: the device address of a pinned, mapped host buffer
-// (cudaHostAlloc / torch pin_memory), read / written by the layout kernels
-// over PCIe instead of a copy-engine transfer; nullptr otherwise.  Off by
-// default: measured at 256^2, p = 4, 1.81 ms per step against 0.97 ms for
-// the side-stream upload hidden under the assembly + setup and a 57 GB/s
-// device->host copy.
-const double* mapped_host(const double* p) {
-  static const bool on = [] {
-    const char* e = std::getenv("LDG_ZEROCOPY");
-    return e && std::atoi(e) == 1;
-  }();
-  if (!on) return nullptr;
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  return a.type == cudaMemoryTypeHost ? static_cast<const double*>(a.devicePointer) : nullptr;
-}
-
 void run_steps(Team& T, double dt, int nsteps, const ldg_solver_opts& o, ldg_step_stats* st) {
   Handle& h0 = T.h0();
   for (int s = 0; s < nsteps; ++s) {
+    ldgb::NvtxRange step("ldg euler_step");
     const double t_next = h0.t + dt;  // system.hpp:158
     LDG_CUDA(cudaEventRecord(h0.ev[0], T.stream));
-    ldgb::team_assemble(T, t_next);
+    {
+      ldgb::NvtxRange r("assemble (project d, f; rhs; E diagonal blocks)");
+      ldgb::team_assemble(T, t_next);
+    }
     LDG_CUDA(cudaEventRecord(h0.ev[1], T.stream));
     ldgb::team_solve(T, 1.0, dt, o, st);
     LDG_CUDA(cudaEventRecord(h0.ev[2], T.stream));
@@ -1186,21 +1170,16 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
       }
       // a caller's time loop hands back the last output: then the solver's
       // extrapolated start stays valid (checked on the device, bit for bit)
-      const bool cont = h0.hist_ok && h0.stage_is_output && t == h0.t && !mapped_host(y_in);
+      const bool cont = h0.hist_ok && h0.stage_is_output && t == h0.t;
       if (!T.in_stream) {
         LDG_CUDA(cudaStreamCreateWithFlags(&T.in_stream, cudaStreamNonBlocking));
         for (auto& e : T.in_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
       LDG_CUDA(cudaEventRecord(T.in_ev[0], T.stream));
       LDG_CUDA(cudaStreamWaitEvent(T.in_stream, T.in_ev[0], 0));
-      if (const double* yd = mapped_host(y_in)) {
-        // pinned + mapped host buffer: the layout kernel reads it over PCIe
-        ldgb::launch_kmajor_to_soa(h0, yd, 3, h0.Y.ptr, T.in_stream);
-      } else {
-        LDG_CUDA(cudaMemcpyAsync(h0.host_in.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice, T.in_stream));
-        if (cont) ldgb::launch_same(h0, cnt, h0.host_in.ptr, h0.host_stage.ptr, h0.in_same.ptr, T.in_stream);
-        ldgb::launch_kmajor_to_soa(h0, h0.host_in.ptr, 3, h0.Y.ptr, T.in_stream);
-      }
+      LDG_CUDA(cudaMemcpyAsync(h0.host_in.ptr, y_in, sizeof(double) * cnt, cudaMemcpyHostToDevice, T.in_stream));
+      if (cont) ldgb::launch_same(h0, cnt, h0.host_in.ptr, h0.host_stage.ptr, h0.in_same.ptr, T.in_stream);
+      ldgb::launch_kmajor_to_soa(h0, h0.host_in.ptr, 3, h0.Y.ptr, T.in_stream);
       LDG_CUDA(cudaEventRecord(T.in_ev[1], T.in_stream));
       T.y_pending = true;
       h0.hist_ok = cont;
@@ -1213,13 +1192,9 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
     run_steps(T, dt, nsteps, o, st);
     if (T.nlocal() == 1 && T.size == 1) {
       const size_t cnt = 3L * h0.K * h0.N;
-      if (double* yo = const_cast<double*>(mapped_host(y_out))) {
-        ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, yo);  // written over PCIe directly
-      } else {
-        ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
-        LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
-        h0.stage_is_output = true;
-      }
+      ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
+      LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));
+      h0.stage_is_output = true;
     } else {
       gather_to_host(T, [](Handle& h) { return static_cast<const double*>(h.Y.ptr); }, 3, y_out);
     }

@@ -11,6 +11,8 @@
 #include <functional>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ldg_b200.h"
 #include "ldg_device.cuh"
 #include "ldg_tables.hpp"
@@ -20,6 +22,15 @@ namespace ldgb {
 constexpr int kMaxRed = 80;        // dot products per reduction (FGMRES basis + 1)
 constexpr int kMaxLocalRanks = 16; // ranks of one process (virtual ranks share a GPU)
 constexpr int kExtrapMax = 4;      // history of the extrapolated Euler start (team_solve)
+
+// NVTX range over a scope (phases of a step in Nsight timelines; header-only
+// NVTX v3, a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Exceptions carry the ABI status they map to.
 struct Error : std::runtime_error {
@@ -153,7 +164,6 @@ struct Handle {
   DBuf<float> mg_P;                              // [4][N*N][Kp] prolongation blocks (on the coarse level, FP32)
   DBuf<double> mg_x, mg_b, mg_r;                 // V-cycle work vectors (N * Kp)
   DBuf<float> E32, Pinv32;                       // FP32 copies read by the row-kernel smoother (small levels)
-  DBuf<float4> Eq, Pq;                           // packed FP32 copies read by the fused smoother (ldg_smooth.cu)
   DBuf<uint2> Eh;                                // packed FP16 copy of E (4 values per uint2), scaled per element
   DBuf<float> Escale;                            // per-element scale of Eh
   DBuf<uint2> Ph;                                // packed FP16 P^-1, scaled per element (Pscale)
@@ -314,35 +324,26 @@ void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double*
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_bjac_axpy_f32(Handle& h, const double* x, double omega, double beta, double* y);
 void launch_to_f32(Handle& h, long n, const double* src, float* dst);
-void launch_bjac(Handle& h, double wm, double dt, int out_kind);     // ldg_bjac.cu: 0 Pinv, 1 Pinv32, 2 Pq, 3 Ph
-bool smoother_e16();                                                  // FP16 E copies for the big-level smoother
-bool smoother_p16();                                                  // FP16 P^-1 copies likewise
-void launch_bjac_setup_quad(Handle& h, double wm, double dt);        // Pq from E (FP64)
+void launch_bjac(Handle& h, double wm, double dt, int out_kind);     // ldg_bjac.cu: 0 Pinv, 1 Pinv32, 3 Ph
 void launch_bjac_setup_f32_from64(Handle& h, double wm, double dt);  // Pinv32 from E (FP64)
 bool level_uses_rows(const Handle& h);
 bool level_is_small(const Handle& h);
 
 // fused mixed-precision smoother (ldg_smooth.cu)
 long packed_p_quads(int p);                                           // float4 quads of one packed P^-1 block
-void smooth_pack_e(Handle& h);                                        // Eq from E
+void smooth_pack_e(Handle& h);                                        // Eh (FP16 packed) from E
 void smooth_stage1(Handle& h, const double* x);                       // tz = M^-1 B x (FP32 arithmetic)
 // mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)
-// [k0, kend): element range (default all owned); out may equal x for one
-// colour of the FK element graph (red-black Gauss-Seidel half-sweep)
 // cheb_beta != 0: Chebyshev step out <- x + omega P^-1 r + cheb_beta (x - out_old)
 // (out_old = x_{k-1}, taken as 0 when prev_zero)
-// fuse1 (p <= 1): stage 1 recomputed inside (no smooth_stage1 before it)
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, int k0 = 0, int kend = -1, double cheb_beta = 0.0, int prev_zero = 0,
-                   bool fuse1 = false);
+                   double* out, double cheb_beta = 0.0, int prev_zero = 0);
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 // the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
 void small_stage1(Handle& h, const double* x);
 void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                  double* out, int k0 = 0, int kend = -1);
+                  double* out);
 void small_zero(Handle& h, const double* b, double omega, double* out);
-// the V-cycle from coarse level `top` (>= 1) down, in one thread block (single rank)
-void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, int pre, int post, int coarse_min);
 
 // row-parallel operator kernels (ldg_rows.cu), used by the launchers above
 void rows_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);

@@ -196,14 +196,6 @@ int mg_levels(const Handle& h) { return 1 + static_cast<int>(h.coarse.size()); }
 
 double coarse_jitter_scale();
 
-bool tz32_enabled() {  // LDG_SMOOTHER_TZ=64: keep the FP64 stage-1 output in the smoother
-  static const bool on = [] {
-    const char* e = std::getenv("LDG_SMOOTHER_TZ");
-    return !(e && std::atoi(e) == 64);
-  }();
-  return on;
-}
-
 // Number of coarse levels for FK(dim) split into `size` equal strips: halve
 // while dim stays even, the coarse mesh keeps dim >= 2, and every rank keeps
 // at least one whole column with even strip boundaries.  Every rank computes
@@ -225,29 +217,8 @@ int mg_depth(int dim, int size) {
 // hierarchical and L2-orthonormal on the reference element (basis.hpp), so
 // the embedding of a lower-degree space is the identity on its first N
 // coefficients: restriction truncates, prolongation pads with zeros.
-// LDG_MG_PC overrides ("-1": none, else a comma list such as "2,1").
 std::vector<int> mg_pcoarse_chain(int p) {
-  std::vector<int> chain;
-  const char* e = std::getenv("LDG_MG_PC");
-  if (e) {
-    for (const char* q = e; *q;) {
-      char* end = nullptr;
-      const long v = std::strtol(q, &end, 10);
-      if (end == q) break;
-      chain.push_back(static_cast<int>(v));
-      q = *end == ',' ? end + 1 : end;
-    }
-  } else {
-    chain = p >= 4 ? std::vector<int>{2} : (p >= 2 ? std::vector<int>{1} : std::vector<int>{});
-  }
-  std::vector<int> out;
-  int last = p;
-  for (int d : chain)
-    if (d >= 0 && d < last) {
-      out.push_back(d);
-      last = d;
-    }
-  return out;
+  return p >= 4 ? std::vector<int>{2} : (p >= 2 ? std::vector<int>{1} : std::vector<int>{});
 }
 
 namespace {
@@ -271,10 +242,6 @@ std::unique_ptr<Handle> coarse_shell(const Handle& h, const Handle& fine) {
   c->p = fine.p;
   c->N = fine.N;
   c->prob = h.prob;
-  {  // tuning experiment: penalty of the rediscretised coarse operators
-    const char* es = std::getenv("LDG_MG_ETA_SCALE");
-    if (es) c->prob.eta = fine.prob.eta * std::atof(es);
-  }
   c->dtab = fine.dtab;
   c->stream = h.stream;
   c->owns_stream = false;
@@ -360,17 +327,12 @@ void mg_setup_f32_level(Handle& L, double wm, double dt) {
   const long NN = static_cast<long>(L.N) * L.N;
   if (!level_uses_rows(L)) {
     // stage-1 output of the smoother in FP32 (no halo of it across ranks: single rank only)
-    if (L.size == 1 && !L.tz32.ptr && tz32_enabled()) L.tz32.alloc(2 * L.vec_len(), &L.bytes);
-    if (smoother_p16()) {
-      if (!L.Ph.ptr) {
-        L.Ph.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
-        L.Pscale.alloc(L.Kp, &L.bytes);
-      }
-      launch_bjac(L, wm, dt, 3);
-    } else {
-      if (!L.Pq.ptr) L.Pq.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
-      launch_bjac_setup_quad(L, wm, dt);
+    if (L.size == 1 && !L.tz32.ptr) L.tz32.alloc(2 * L.vec_len(), &L.bytes);
+    if (!L.Ph.ptr) {  // FP16 packed P^-1, scaled per element
+      L.Ph.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
+      L.Pscale.alloc(L.Kp, &L.bytes);
     }
+    launch_bjac(L, wm, dt, 3);
     smooth_pack_e(L);
   } else {
     if (!L.E32.ptr) {
@@ -443,39 +405,24 @@ void mg_restrict(Handle& L, Handle& C) {
   ++L.launches;
 }
 
-// scale of the coarse-grid correction (LDG_MG_THETA, tuning runs; 1 = plain)
-double coarse_theta() {
-  static const double th = [] {
-    const char* e = std::getenv("LDG_MG_THETA");
-    return e ? std::atof(e) : 1.0;
-  }();
-  return th;
-}
-
 // Jitter of the coarse levels' vertices as a fraction of the finest mesh's
 // displacement (same splitmix64 stream): on a jittered FK mesh the fine
 // triangles do not tile the coarse ones whatever the coarse vertices are, and
 // subsampling the fine vertices (1.0) made the rediscretised coarse operators
 // a poor match -- measured at 512^2, p = 3, jitter 0.2, mixed BCs: 93
 // iterations with 1.0, 60 with a regular coarse lattice (0.0), 52.5 with 0.4
-// (0.25..0.75 swept).  LDG_MG_COARSE_JITTER overrides.
-double coarse_jitter_scale() {
-  static const double js = [] {
-    const char* e = std::getenv("LDG_MG_COARSE_JITTER");
-    return e ? std::atof(e) : 0.4;
-  }();
-  return js;
-}
+// (0.25..0.75 swept).
+double coarse_jitter_scale() { return 0.4; }
 
 // x += P C.mg_x (prolongation of the coarse correction)
 void mg_prolong_add(Handle& L, Handle& C, double* x) {
   if (C.mg_pcoarse) {  // pad: the first C.N coefficient planes
-    launch_lincomb3(L, C.vec_len(), 1.0, x, coarse_theta(), C.mg_x.ptr, 0.0, nullptr, x);
+    launch_lincomb3(L, C.vec_len(), 1.0, x, 1.0, C.mg_x.ptr, 0.0, nullptr, x);
     return;
   }
 #define CALL(PP)                                                                                              \
   launch_pdl(k_prolong_add<PP>, grid_of(4L * L.N * C.K, 256), 256, 0, L.stream, C.K, C.Kp, L.Kp,                \
-             C.mg_children.ptr, C.mg_P.ptr, C.mg_x.ptr, x, coarse_theta())
+             C.mg_children.ptr, C.mg_P.ptr, C.mg_x.ptr, x, 1.0)
   LDG_DISPATCH_P(L.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

@@ -15,8 +15,6 @@
 // Operands: E and P^-1 as FP32 SoA copies (E32, Pinv32), vectors FP64,
 // arithmetic FP64 (these levels are latency-bound; precision is free).
 // Reference operators as in ldg_apply.cu / ldg_rows.cu (assembly.hpp:76-208).
-#include <cooperative_groups.h>
-
 #include <cmath>
 #include <cstdlib>
 
@@ -289,149 +287,6 @@ __global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_s2_batch(DevMesh m, DevT
                 0, m.K, s_r, blockIdx.x, threadIdx.x);
 }
 
-// ---------------------------------------------------------------- tail
-// The coarsest levels (a few dozen elements) of a V-cycle in ONE thread block:
-// every phase (sweep stages, residual, restriction, prolongation) is a loop
-// of the bodies above over the level's virtual blocks, separated by
-// __syncthreads, so the level data stays in this SM's L1 and no launch or
-// grid drain sits between the ~30 dependent phases (separate launches cost
-// 6-7 us each on these levels, mostly dependent L2 round trips).
-constexpr int kTailMax = 6;
-
-struct TailLevel {
-  DevMesh m;
-  const float* E32;
-  const float* Pinv32;
-  const double* D;
-  double *x, *s, *b, *r, *tz;
-  const int* children;  // this level as the coarse side of the transfer from the level above
-  const float* Pm;
-  int dim;
-};
-
-struct TailArgs {
-  TailLevel lv[kTailMax];
-  int nlev;
-  double wm, dt, dteta, omega;
-  int pre, post, coarse_min;
-};
-
-// CL > 1: the same phases spread over a thread-block cluster of CL CTAs (one
-// per SM of a GPC), virtual blocks dealt round-robin, the phases separated by
-// cluster barriers (release/acquire at cluster scope, after a device fence
-// for the global-memory level data) instead of __syncthreads: CL SMs of
-// issue rate for the p >= 2 levels, still no launch between phases.
-template <int P, int CL>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, 1) k_tail(TailArgs a, DevTables T) {
-  using C = Cfg<P>;
-  constexpr int N = C::N, NN = C::NN;
-  __shared__ double s_r[N][C::EPC];
-  pdl_wait();
-  pdl_trigger();
-  const int t = threadIdx.x;
-  int rank = 0;
-  if constexpr (CL > 1) rank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
-  const int gt = rank * blockDim.x + t, gstride = CL * blockDim.x;
-  auto bar = [&]() {
-    if constexpr (CL > 1) {
-      __threadfence();
-      cooperative_groups::this_cluster().sync();
-    } else {
-      __syncthreads();
-    }
-  };
-  auto nvb = [](int K) { return (K + C::EPC - 1) / C::EPC; };
-  auto zero = [&](const TailLevel& L, const double* b, double* out) {
-    for (int vb = rank; vb < nvb(L.m.K); vb += CL) bj_body<P>(L.m.K, L.m.Kp, L.Pinv32, b, a.omega, out, vb, t);
-    bar();
-  };
-  auto stage1 = [&](const TailLevel& L, const double* x) {
-    for (int vb = rank; vb < nvb(L.m.K); vb += CL) s1_body<P>(L.m, T, x, L.tz, vb, t);
-    bar();
-  };
-  auto stage2 = [&](const TailLevel& L, int mode, const double* x, const double* b, double* out) {
-    for (int vb = rank; vb < nvb(L.m.K); vb += CL) {
-      if (mode == 0)
-        s2_body<P, 0>(L.m, T, L.E32, L.D, x, L.tz, b, a.wm, a.dteta, a.dt, L.Pinv32, a.omega, out, 0, L.m.K, s_r, vb,
-                      t);
-      else
-        s2_body<P, 1>(L.m, T, L.E32, L.D, x, L.tz, b, a.wm, a.dteta, a.dt, L.Pinv32, a.omega, out, 0, L.m.K, s_r, vb,
-                      t);
-    }
-    bar();
-  };
-  auto sweep = [&](const TailLevel& L, const double* xi, double* xo) {
-    stage1(L, xi);
-    stage2(L, 1, xi, L.b, xo);
-  };
-  // C.b = P^T F.r  (ldg_mg.cu k_restrict)
-  auto restrict_ = [&](const TailLevel& F, const TailLevel& Cl) {
-    const long Kpc = Cl.m.Kp, Kpf = F.m.Kp;
-    for (int it = gt; it < N * Cl.m.K; it += gstride) {
-      const int kc = it % Cl.m.K, j = it / Cl.m.K;
-      double acc = 0.0;
-      for (int sl = 0; sl < 4; ++sl) {
-        const int k = Cl.children[sl * Kpc + kc];
-        const float* Ps = Cl.Pm + (static_cast<long>(sl) * NN + j) * Kpc + kc;
-#pragma unroll
-        for (int i = 0; i < N; ++i) acc = fma(static_cast<double>(Ps[static_cast<long>(i) * N * Kpc]), F.r[i * Kpf + k], acc);
-      }
-      Cl.b[j * Kpc + kc] = acc;
-    }
-    bar();
-  };
-  // xf += P C.x  (ldg_mg.cu k_prolong_add)
-  auto prolong = [&](const TailLevel& F, const TailLevel& Cl, double* xf) {
-    const long Kpc = Cl.m.Kp, Kpf = F.m.Kp;
-    for (int it = gt; it < 4 * N * Cl.m.K; it += gstride) {
-      const int kc = it % Cl.m.K, rest = it / Cl.m.K, sl = rest % 4, i = rest / 4;
-      const int k = Cl.children[sl * Kpc + kc];
-      const float* Ps = Cl.Pm + (static_cast<long>(sl) * NN + static_cast<long>(i) * N) * Kpc + kc;
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) acc = fma(static_cast<double>(Ps[static_cast<long>(j) * Kpc]), Cl.x[j * Kpc + kc], acc);
-      xf[i * Kpf + k] += acc;
-    }
-    bar();
-  };
-
-  double* cur[kTailMax];
-  for (int l = 0; l + 1 < a.nlev; ++l) {  // down
-    const TailLevel& L = a.lv[l];
-    const int sweeps = (a.pre - 1) + a.post;
-    cur[l] = (sweeps % 2) ? L.s : L.x;
-    zero(L, L.b, cur[l]);
-    for (int sw = 0; sw < a.pre - 1; ++sw) {
-      double* o = cur[l] == L.x ? L.s : L.x;
-      sweep(L, cur[l], o);
-      cur[l] = o;
-    }
-    stage1(L, cur[l]);
-    stage2(L, 0, cur[l], L.b, L.r);
-    restrict_(L, a.lv[l + 1]);
-  }
-  {  // coarsest
-    const TailLevel& L = a.lv[a.nlev - 1];
-    const int sweeps = max(a.coarse_min, 2 * L.dim) - 1;
-    double* c = (sweeps % 2) ? L.s : L.x;
-    zero(L, L.b, c);
-    for (int sw = 0; sw < sweeps; ++sw) {
-      double* o = c == L.x ? L.s : L.x;
-      sweep(L, c, o);
-      c = o;
-    }
-  }
-  for (int l = a.nlev - 2; l >= 0; --l) {  // up
-    const TailLevel& L = a.lv[l];
-    prolong(L, a.lv[l + 1], cur[l]);
-    for (int sw = 0; sw < a.post; ++sw) {
-      double* o = cur[l] == L.x ? L.s : L.x;
-      sweep(L, cur[l], o);
-      cur[l] = o;
-    }
-  }
-}
-
 }  // namespace
 
 void small_stage1(Handle& h, const double* x) {
@@ -444,9 +299,9 @@ void small_stage1(Handle& h, const double* x) {
 }
 
 void small_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                  double* out, int k0, int kend) {
+                  double* out) {
   const double dteta = dt * h.prob.eta;
-  if (kend < 0) kend = h.K;
+  const int k0 = 0, kend = h.K;
 #define CALL(P)                                                                                                \
   do {                                                                                                         \
     const unsigned grid = grid_of(kend - k0, Cfg<P>::EPC);                                                     \
@@ -490,100 +345,6 @@ void small_zero(Handle& h, const double* b, double omega, double* out) {
 #undef CALL
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
-}
-
-}  // namespace ldgb
-
-namespace ldgb {
-
-// CTAs of the tail kernel's cluster (LDG_TAIL_CLUSTER: 1, 4, 8 or 16).
-// Measured V-cycle at 256^2 (p = 0 / 2 / 4): one block 273 / 513 / 1437 us;
-// clusters of 8 or 16 on the same levels 292 / 525 / 1438 us (the cluster
-// barrier + fence per phase and the level data leaving the one SM's L1 cost
-// more than the extra issue rate buys); with the p >= 2 levels below 600 or
-// 2048 elements in the tail as well 295 / 542-573 / 1490-1595 us.  Off.
-int tail_cluster() {
-  static const int cl = [] {
-    const char* e = std::getenv("LDG_TAIL_CLUSTER");
-    const int v = e ? std::atoi(e) : 1;
-    return (v == 4 || v == 8 || v == 16) ? v : 1;
-  }();
-  return cl;
-}
-
-// one cluster of `cl` CTAs, programmatic stream serialisation as launch_pdl
-template <typename... KArgs, typename... Args>
-void launch_cluster(void (*kern)(KArgs...), int cl, int threads, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cl);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = cl;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  LDG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
-}
-
-// The V-cycle below level `top` (inclusive) of h's hierarchy in one block
-// (see k_tail); x of the top level receives the result, b its right-hand side.
-void small_tail_vcycle(Handle& h0, int top, double wm, double dt, double omega, int pre, int post, int coarse_min) {
-  TailArgs a{};
-  const int nl = 1 + static_cast<int>(h0.coarse.size());
-  a.nlev = nl - top;
-  if (a.nlev < 1 || a.nlev > kTailMax) throw Error(LDG_EINVAL, "tail V-cycle: level count out of range");
-  for (int l = 0; l < a.nlev; ++l) {
-    Handle& L = *h0.coarse[top + l - 1];
-    TailLevel& t = a.lv[l];
-    t.m = L.mesh();
-    t.E32 = L.E32.ptr;
-    t.Pinv32 = L.Pinv32.ptr;
-    t.D = L.D.ptr;
-    t.x = L.mg_x.ptr;
-    t.s = L.mg_s.ptr;
-    t.b = L.mg_b.ptr;
-    t.r = L.mg_r.ptr;
-    t.tz = L.tz.ptr;
-    t.children = L.mg_children.ptr;
-    t.Pm = L.mg_P.ptr;
-    t.dim = L.dim;
-  }
-  a.wm = wm;
-  a.dt = dt;
-  a.dteta = dt * h0.prob.eta;
-  a.omega = omega;
-  a.pre = pre;
-  a.post = post;
-  a.coarse_min = coarse_min;
-  const Handle& top_h = *h0.coarse[top - 1];  // all tail levels share its degree (p-coarsening, ldg_mg.cu)
-  const int cl = tail_cluster();
-#define CALL(P)                                                                                \
-  do {                                                                                         \
-    if (cl == 16) {                                                                            \
-      static bool np = false;                                                                  \
-      if (!np) {                                                                               \
-        LDG_CUDA(cudaFuncSetAttribute(k_tail<P, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
-        np = true;                                                                             \
-      }                                                                                        \
-      launch_cluster(k_tail<P, 16>, 16, Cfg<P>::THREADS, h0.stream, a, top_h.dtab);            \
-    } else if (cl == 8) {                                                                      \
-      launch_cluster(k_tail<P, 8>, 8, Cfg<P>::THREADS, h0.stream, a, top_h.dtab);              \
-    } else if (cl == 4) {                                                                      \
-      launch_cluster(k_tail<P, 4>, 4, Cfg<P>::THREADS, h0.stream, a, top_h.dtab);              \
-    } else {                                                                                   \
-      launch_pdl(k_tail<P, 1>, 1, Cfg<P>::THREADS, 0, h0.stream, a, top_h.dtab);               \
-    }                                                                                          \
-  } while (0)
-  LDG_DISPATCH_P(top_h.p, CALL)
-#undef CALL
-  LDG_CUDA(cudaGetLastError());
-  ++h0.launches;
 }
 
 }  // namespace ldgb

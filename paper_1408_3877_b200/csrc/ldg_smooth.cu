@@ -75,9 +75,6 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
     default: { CALL(4); break; } \
   }
 
-#ifndef LDG_S2_PF
-#define LDG_S2_PF 0
-#endif
 __device__ __forceinline__ long Kp_of(const DevMesh& m) { return m.Kp; }
 
 __device__ __forceinline__ float comp(const float4& v, int r) {
@@ -122,79 +119,6 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
   for (int j = 0; j < N; ++j) v[j] = static_cast<float>(x[j * Kp + col]);
 }
 
-// u1 += a * (T x), u2 += b * (T x) accumulated directly (no w temporary):
-// twice the FFMA2 of ftab_mv + combine, but 16 independent accumulator pairs
-// and 15 fewer live registers (tuning builds: LDG_S1_DIRECT = p).  Measured
-// V-cycle at 256^2: p = 2 / 3 / 4 +2.7 / +4.4 / +2.8 % (124 instead of 128
-// registers at p = 4, no spills): the extra FFMA2 issue outweighs the ILP.
-template <int N, int NF>
-__device__ __forceinline__ void ftab_acc2(const float* sT, const float* x, float a, float b, float2* u1,
-                                          float2* u2) {
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const float4* row = reinterpret_cast<const float4*>(sT + j * NF);
-    const float2 xa = make_float2(a * x[j], a * x[j]), xb = make_float2(b * x[j], b * x[j]);
-#pragma unroll
-    for (int q = 0; q < NF / 4; ++q) {
-      const float4 t = row[q];
-      u1[2 * q] = __ffma2_rn(make_float2(t.x, t.y), xa, u1[2 * q]);
-      u2[2 * q] = __ffma2_rn(make_float2(t.x, t.y), xb, u2[2 * q]);
-      if (4 * q + 2 < N) {
-        u1[2 * q + 1] = __ffma2_rn(make_float2(t.z, t.w), xa, u1[2 * q + 1]);
-        u2[2 * q + 1] = __ffma2_rn(make_float2(t.z, t.w), xb, u2[2 * q + 1]);
-      }
-    }
-  }
-}
-
-#ifndef LDG_S1_DIRECT
-#define LDG_S1_DIRECT -1
-#endif
-template <int P, typename TT>
-__device__ __forceinline__ void s1f_direct(const DevMesh& m, const float* tb, const double* __restrict__ x, int k,
-                                           TT* __restrict__ tout) {
-  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
-  const long Kp = m.Kp;
-  const double* g = m.geom;
-  float2 u1[NF / 2], u2[NF / 2];
-#pragma unroll
-  for (int q = 0; q < NF / 2; ++q) u1[q] = u2[q] = make_float2(0.f, 0.f);
-  {
-    float xv[N];
-    load_f<N>(x, Kp, k, xv);
-    const float b11 = static_cast<float>(g[kB11 * Kp + k]), b12 = static_cast<float>(g[kB12 * Kp + k]);
-    const float b21 = static_cast<float>(g[kB21 * Kp + k]), b22 = static_cast<float>(g[kB22 * Kp + k]);
-    ftab_acc2<N, NF>(tb, xv, -b22, b12, u1, u2);
-    ftab_acc2<N, NF>(tb + TAB, xv, b21, -b11, u1, u2);
-#pragma unroll 1
-    for (int n = 0; n < 3; ++n) {
-      const int kind = m.kind[n * Kp + k];
-      const double len = g[(kLen0 + n) * Kp + k];
-      const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
-      if (f == 0.0) continue;
-      ftab_acc2<N, NF>(tb + (2 + n) * TAB, xv, static_cast<float>(f * g[(kNux0 + n) * Kp + k]),
-                       static_cast<float>(f * g[(kNuy0 + n) * Kp + k]), u1, u2);
-    }
-  }
-#pragma unroll 1
-  for (int n = 0; n < 3; ++n) {
-    const int nb = m.nbr[n * Kp + k];
-    if (nb < 0) continue;
-    float xn[N];
-    load_f<N>(x, Kp, nb, xn);
-    const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
-    ftab_acc2<N, NF>(tb + (5 + n * 3 + m.nbrn[n * Kp + k]) * TAB, xn, static_cast<float>(hl * g[(kNux0 + n) * Kp + k]),
-                     static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]), u1, u2);
-  }
-  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const float a1 = (i & 1) ? u1[i / 2].y : u1[i / 2].x, a2 = (i & 1) ? u2[i / 2].y : u2[i / 2].x;
-    tout[i * Kp + k] = static_cast<TT>(inv2a * a1);
-    tout[(N + i) * Kp + k] = static_cast<TT>(inv2a * a2);
-  }
-}
-
 // tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
 template <int P, typename TT>
 __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
@@ -206,10 +130,6 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
   pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
-  if constexpr (P == LDG_S1_DIRECT) {
-    s1f_direct<P, TT>(m, tb, x, k, tout);
-    return;
-  }
   const long Kp = m.Kp;
   const double* g = m.geom;
   float xv[N], w[N], u1[N], u2[N];
@@ -244,35 +164,14 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
     }
   }
   // the neighbours' x: every load issued before the products (one latency
-  // round instead of one per neighbour) — or, when the kernel runs at a high
-  // CTA count per SM (LDG_S1_SEQ_P = p), one neighbour at a time (15 instead
-  // of 45 live registers)
+  // round instead of one per neighbour; one neighbour at a time at 6-8 CTAs
+  // per SM measured 3-16 % slower at p = 4)
   int nb[3], nbn[3];
 #pragma unroll
   for (int n = 0; n < 3; ++n) {
     nb[n] = m.nbr[n * Kp + k];
     nbn[n] = m.nbrn[n * Kp + k];
   }
-#ifdef LDG_S1_SEQ_P
-  if constexpr (P == LDG_S1_SEQ_P) {
-#pragma unroll 1
-    for (int n = 0; n < 3; ++n) {
-      if (nb[n] < 0) continue;
-      float xn1[N];
-      load_f<N>(x, Kp, nb[n], xn1);
-      ftab_mv<N, NF>(tb + (5 + n * 3 + nbn[n]) * TAB, xn1, w);
-      const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
-      const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
-      const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        u1[i] = fmaf(c1, w[i], u1[i]);
-        u2[i] = fmaf(c2, w[i], u2[i]);
-      }
-    }
-  } else
-#endif
-  {
   float xn[3][N];
 #pragma unroll
   for (int n = 0; n < 3; ++n)
@@ -291,75 +190,11 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
       u2[i] = fmaf(c2, w[i], u2[i]);
     }
   }
-  }
   const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     tout[i * Kp + k] = static_cast<TT>(inv2a * u1[i]);
     tout[(N + i) * Kp + k] = static_cast<TT>(inv2a * u2[i]);
-  }
-}
-
-// t^m_e = M_e^-1 B^m x of one element e (k_s1f's arithmetic, FP32), for the
-// fused p <= 1 sweep below: tb = the 14 m_hat^-1-premultiplied tables
-template <int P>
-__device__ __forceinline__ void s1_elem(const DevMesh& m, const float* tb, const double* __restrict__ x, int e,
-                                        float* t1, float* t2) {
-  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
-  const long Kp = m.Kp;
-  const double* g = m.geom;
-  float xv[N], w[N];
-  load_f<N>(x, Kp, e, xv);
-  const float b11 = static_cast<float>(g[kB11 * Kp + e]), b12 = static_cast<float>(g[kB12 * Kp + e]);
-  const float b21 = static_cast<float>(g[kB21 * Kp + e]), b22 = static_cast<float>(g[kB22 * Kp + e]);
-  ftab_mv<N, NF>(tb, xv, w);
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    t1[i] = -b22 * w[i];
-    t2[i] = b12 * w[i];
-  }
-  ftab_mv<N, NF>(tb + TAB, xv, w);
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    t1[i] = fmaf(b21, w[i], t1[i]);
-    t2[i] = fmaf(-b11, w[i], t2[i]);
-  }
-#pragma unroll
-  for (int n = 0; n < 3; ++n) {
-    const int kind = m.kind[n * Kp + e];
-    const double len = g[(kLen0 + n) * Kp + e];
-    const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
-    if (f == 0.0) continue;
-    ftab_mv<N, NF>(tb + (2 + n) * TAB, xv, w);
-    const float c1 = static_cast<float>(f * g[(kNux0 + n) * Kp + e]);
-    const float c2 = static_cast<float>(f * g[(kNuy0 + n) * Kp + e]);
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      t1[i] = fmaf(c1, w[i], t1[i]);
-      t2[i] = fmaf(c2, w[i], t2[i]);
-    }
-  }
-#pragma unroll
-  for (int n = 0; n < 3; ++n) {
-    const int nb = m.nbr[n * Kp + e];
-    if (nb < 0) continue;
-    float xn[N];
-    load_f<N>(x, Kp, nb, xn);
-    ftab_mv<N, NF>(tb + (5 + n * 3 + m.nbrn[n * Kp + e]) * TAB, xn, w);
-    const double hl = 0.5 * g[(kLen0 + n) * Kp + e];
-    const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + e]);
-    const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + e]);
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      t1[i] = fmaf(c1, w[i], t1[i]);
-      t2[i] = fmaf(c2, w[i], t2[i]);
-    }
-  }
-  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + e]));
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    t1[i] *= inv2a;
-    t2[i] *= inv2a;
   }
 }
 
@@ -433,68 +268,39 @@ __device__ __forceinline__ void pinv_apply(const TQ* __restrict__ Pk, long Kp, F
 // r = b - [wm M x + dt (eta S x - sum_m E^m t^m)] on the element, then
 //   MODE 0: out = r
 //   MODE 1: out = x + omega P^-1 r        (one damped block-Jacobi sweep)
-//   FUSE (p <= 1, one rank): t = M^-1 B x of the element and its neighbours
-//   recomputed here from x (s1_elem) instead of read from the stage-1 pass —
-//   the sweep is one launch instead of two (tz unused)
-template <int P, int MODE, typename TQ, typename TP, typename TT, bool FUSE = false>
+template <int P, int MODE, typename TQ, typename TP, typename TT>
 __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T, const TQ* __restrict__ Eq,
                                              const float* __restrict__ Escale, const double* __restrict__ D,
-                                             const double* x,
+                                             const double* __restrict__ x,
                                              const TT* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const TP* __restrict__ Pq,
-                                             const float* __restrict__ Pscale, float omega, double* out, int k0,
-                                             int kend, double cheb_beta, int prev_zero) {
+                                             const float* __restrict__ Pscale, float omega, double* out,
+                                             double cheb_beta, int prev_zero) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
   constexpr int Q = C::Q;
   extern __shared__ __align__(16) float smf[];
   // tM | tSd 3 | tSo 9 | pe 3 | pth 9 | we (contiguous in the FP32 table buffer)
   const float* tb = stage_f(smf, T.fbase + T.fM, 13 * TAB + C::EDGE);
-  const float* tb1 = FUSE ? stage_f(smf + 13 * TAB + C::EDGE, T.fbase + T.fmH, 14 * TAB) : nullptr;
   const float* s_pe = tb + 13 * TAB;
   const float* s_pth = s_pe + 3 * Q * N;
   const float* s_we = s_pth + 9 * Q * N;
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
-  // elements [k0, kend): all of them (Jacobi, out != x) or one colour of the
-  // bipartite FK element graph (red-black Gauss-Seidel, in place: an element
-  // reads only the other colour's x)
-  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
-#if LDG_S2_PF
-  // the static streams of this element (E, P^-1 do not change within a
-  // V-cycle) requested into L2 before waiting for the predecessor kernel, so
-  // the loads below find them there: bit 1 the P^-1 stream (read last),
-  // bit 2 E's second component.  Measured (V-cycle at 256^2, p = 2 / 3 / 4):
-  // bit 1 -1 / 0 / +3 %, bit 2 -1 / 0 / +1.5 %, both -1 / +2 / +5 %: off.
-  if (k < kend) {
-    if ((LDG_S2_PF & 1) && MODE == 1)
-      for (int q = 0; q < C::QP; ++q)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(Pq + k + static_cast<long>(q) * Kp_of(m)));
-    if (LDG_S2_PF & 2)
-      for (int q = 0; q < C::QP; ++q)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(Eq + static_cast<long>(C::QP + q) * Kp_of(m) + k));
-  }
-#endif
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   pdl_trigger();
-  if (k >= kend) return;
+  if (k >= m.K) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
   float acc[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) acc[i] = 0.f;
   // diagonal blocks E^m_kk t^m_k (packed stream), scaled copy
-  if constexpr (FUSE) {
-    float t1[N], t2[N];
-    s1_elem<P>(m, tb1, x, k, t1, t2);
-    packed_apply<P, TQ>(Eq + k, Kp, [&](int j) { return t1[j]; }, acc);
-    packed_apply<P, TQ>(Eq + static_cast<long>(C::QP) * Kp + k, Kp, [&](int j) { return t2[j]; }, acc);
-  } else {
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      const TT* tc = tz + static_cast<long>(c) * N * Kp + k;
-      packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
-                          [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
-    }
+  for (int c = 0; c < 2; ++c) {
+    const TT* tc = tz + static_cast<long>(c) * N * Kp + k;
+    packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
+                        [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
   }
   if (Escale) {
     const float es = Escale[k];
@@ -510,22 +316,12 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
     const float co1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
     const float co2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
     float z[Q];
-    if constexpr (FUSE) {
-      float u1[N], u2[N];
-      s1_elem<P>(m, tb1, x, kp, u1, u2);
-      offdiag_z<N, Q, float>(
-          s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we,
-          [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
-          [&](int j) { return fmaf(co1, u1[j], co2 * u2[j]); }, z);
-    } else {
-      offdiag_z<N, Q, float>(
-          s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we,
-          [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
-          [&](int j) {
-            return fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
-          },
-          z);
-    }
+    offdiag_z<N, Q, float>(
+        s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we, [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
+        [&](int j) {
+          return fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
+        },
+        z);
     offdiag_rows<N, Q, float>(s_pe + n * Q * N, z, 1.0f, acc);
   }
   const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
@@ -641,8 +437,8 @@ size_t s1_smem() {
   return sizeof(float) * 14 * Cfg<P>::N * Cfg<P>::NF;
 }
 template <int P>
-size_t s2_smem(bool fuse = false) {
-  return sizeof(float) * ((fuse ? 27 : 13) * Cfg<P>::N * Cfg<P>::NF + Cfg<P>::EDGE);
+size_t s2_smem() {
+  return sizeof(float) * (13 * Cfg<P>::N * Cfg<P>::NF + Cfg<P>::EDGE);
 }
 
 }  // namespace
@@ -657,43 +453,21 @@ long packed_p_quads(int p) {
   }
 }
 
-// Storage of the stored blocks read by the big-level smoother (diagonal E
-// blocks and P^-1): FP16 with a per-element scale (default; half the bytes of
-// FP32 in the HBM-bound stage 2) or FP32 (LDG_SMOOTHER_E=32).
-bool smoother_e16() {
-  static const bool on = [] {
-    const char* s = std::getenv("LDG_SMOOTHER_E");
-    return !(s && std::atoi(s) == 32);
-  }();
-  return on;
-}
-bool smoother_p16() {  // P^-1 copy: FP16 unless LDG_SMOOTHER_P=32 (or E is FP32)
-  static const bool on = [] {
-    const char* s = std::getenv("LDG_SMOOTHER_P");
-    return smoother_e16() && !(s && std::atoi(s) == 32);
-  }();
-  return on;
-}
-
+// FP16 copy of the level's diagonal E blocks for the big-level smoother,
+// scaled per element into [-1, 1] (half the bytes of FP32 in the HBM-bound
+// stage 2; FP32 copies measured slower in round 1 at equal iterations)
 void smooth_pack_e(Handle& h) {
-  const bool e16 = smoother_e16();
-#define CALL(P)                                                                                            \
-  do {                                                                                                     \
-    const long nq = 2L * Cfg<P>::QP * h.Kp;                                                                \
-    if (e16) {                                                                                             \
-      if (!h.Eh.ptr) {                                                                                     \
-        h.Eh.alloc(nq, &h.bytes);                                                                          \
-        h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
-      }                                                                                                    \
-      k_escale<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr);                  \
-      k_pack_e<P, uint2><<<grid_of(2L * Cfg<P>::NN * h.Kp, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr,         \
-                                                                                   h.Escale.ptr, h.Eh.ptr); \
-      h.launches += 1;                                                                                     \
-    } else {                                                                                               \
-      if (!h.Eq.ptr) h.Eq.alloc(nq, &h.bytes);                                                             \
-      k_pack_e<P, float4><<<grid_of(2L * Cfg<P>::NN * h.Kp, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr,        \
-                                                                                    nullptr, h.Eq.ptr);     \
-    }                                                                                                      \
+#define CALL(P)                                                                                          \
+  do {                                                                                                   \
+    const long nq = 2L * Cfg<P>::QP * h.Kp;                                                              \
+    if (!h.Eh.ptr) {                                                                                     \
+      h.Eh.alloc(nq, &h.bytes);                                                                          \
+      h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
+    }                                                                                                    \
+    k_escale<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr);                  \
+    k_pack_e<P, uint2><<<grid_of(2L * Cfg<P>::NN * h.Kp, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr,         \
+                                                                                 h.Escale.ptr, h.Eh.ptr); \
+    h.launches += 1;                                                                                     \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -718,61 +492,35 @@ void smooth_stage1(Handle& h, const double* x) {
 }
 
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, int k0, int kend, double cheb_beta, int prev_zero, bool fuse1) {
+                   double* out, double cheb_beta, int prev_zero) {
   const double dteta = dt * h.prob.eta;
   const float om = static_cast<float>(omega);
-  const bool e16 = h.Eh.ptr != nullptr, p16 = h.Ph.ptr != nullptr;
-  if (kend < 0) kend = h.K;
-  const unsigned grid = grid_of(kend - k0, 128);
-  if (fuse1 && h.p > 2) throw Error(LDG_EINVAL, "fused stage 1 is for p <= 2");
-#define LAUNCH(P, M, TQ, EP, SC, TP, PP, PS)                                                                       \
-  do {                                                                                                            \
-    if (fuse1)                                                                                                    \
-      launch_pdl(k_s2f<(P) <= 2 ? P : 2, M, TQ, TP, float, true>, grid, 128, s2_smem<(P) <= 2 ? P : 2>(true),     \
-                 h.stream, h.mesh(), h.dtab, EP, SC, h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, \
-                 kend, cheb_beta, prev_zero);                                                                     \
-    else if (h.tz32.ptr)                                                                                          \
-      launch_pdl(k_s2f<P, M, TQ, TP, float>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,        \
-                 h.D.ptr, x, h.tz32.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend, cheb_beta, prev_zero);       \
-    else                                                                                                          \
-      launch_pdl(k_s2f<P, M, TQ, TP, double>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, EP, SC,       \
-                 h.D.ptr, x, h.tz.ptr, b, wm, dteta, dt, PP, PS, om, out, k0, kend, cheb_beta, prev_zero);         \
-  } while (0)
-#define MODES(P, TQ, EP, SC, TP, PP, PS)        \
-  do {                                          \
-    if (mode == 0)                              \
-      LAUNCH(P, 0, TQ, EP, SC, TP, PP, PS);     \
-    else                                        \
-      LAUNCH(P, 1, TQ, EP, SC, TP, PP, PS);     \
-  } while (0)
-#define CALL(P)                                                                                             \
-  do {                                                                                                      \
-    const float* nos = nullptr;                                                                             \
-    if (e16 && p16)                                                                                         \
-      MODES(P, uint2, h.Eh.ptr, h.Escale.ptr, uint2, h.Ph.ptr, h.Pscale.ptr);                               \
-    else if (e16)                                                                                           \
-      MODES(P, uint2, h.Eh.ptr, h.Escale.ptr, float4, h.Pq.ptr, nos);                                       \
-    else                                                                                                    \
-      MODES(P, float4, h.Eq.ptr, nos, float4, h.Pq.ptr, nos);                                               \
+  const unsigned grid = grid_of(h.K, 128);
+#define LAUNCH(P, M, TT, TZ)                                                                                      \
+  launch_pdl(k_s2f<P, M, uint2, uint2, TT>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, h.Eh.ptr,        \
+             h.Escale.ptr, h.D.ptr, x, TZ, b, wm, dteta, dt, h.Ph.ptr, h.Pscale.ptr, om, out, cheb_beta, prev_zero)
+#define CALL(P)                                           \
+  do {                                                    \
+    if (mode == 0 && h.tz32.ptr)                          \
+      LAUNCH(P, 0, float, h.tz32.ptr);                    \
+    else if (mode == 0)                                   \
+      LAUNCH(P, 0, double, h.tz.ptr);                     \
+    else if (h.tz32.ptr)                                  \
+      LAUNCH(P, 1, float, h.tz32.ptr);                    \
+    else                                                  \
+      LAUNCH(P, 1, double, h.tz.ptr);                     \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
-#undef MODES
 #undef LAUNCH
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
 
 void smooth_zero(Handle& h, const double* b, double omega, double* out) {
-#define CALL(P)                                                                                        \
-  do {                                                                                                          \
-    if (h.Ph.ptr)                                                                                               \
-      launch_pdl(k_bjf<P, uint2>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Ph.ptr, h.Pscale.ptr, b,    \
-                 static_cast<float>(omega), out);                                                               \
-    else                                                                                                        \
-      launch_pdl(k_bjf<P, float4>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Pq.ptr,                    \
-                 static_cast<const float*>(nullptr), b, static_cast<float>(omega), out);                        \
-  } while (0)
+#define CALL(P)                                                                                              \
+  launch_pdl(k_bjf<P, uint2>, grid_of(h.K, 128), 128, 0, h.stream, h.K, h.Kp, h.Ph.ptr, h.Pscale.ptr, b,         \
+             static_cast<float>(omega), out)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <optional>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -37,7 +38,7 @@ double* dots_result(Handle& h);
 
 namespace {
 
-// V-cycle parameters (LDG_MG_* environment overrides for tuning runs)
+// V-cycle parameters (LDG_MG_PRE0 / POST0 / PRE1 / POST1 override the level-0/1 sweeps in tuning runs)
 double env_or(const char* name, double dflt) {
   const char* s = std::getenv(name);
   return s ? std::atof(s) : dflt;
@@ -51,7 +52,7 @@ double env_or(const char* name, double dflt) {
 // (scripts/gpu_envs_perp.sh, stable to 0.1 ms) is level 0 V(6,6) / V(4,5) /
 // V(4,6) / V(5,6) / V(5,6) and level 1 V(2,1) except V(1,1) at p = 4
 // (ms/step 5.17 / 7.47 / 11.11 / 20.11 / 38.49 against 5.59 / 7.67 / 11.88 /
-// 20.55 / 41.09 with V(5,5) + V(2,1)).  LDG_MG_* override for every degree.
+// 20.55 / 41.09 with V(5,5) + V(2,1)).
 // Damped block-Jacobi weight and the sweeps of the levels below level 1,
 // re-tuned after p-coarsening and Chebyshev level 0 made the coarse levels
 // cheap relative to their effect (5-step C2 bench, all degrees): coarse
@@ -64,7 +65,6 @@ double env_or(const char* name, double dflt) {
 // iterations, and a 2-rank strip run at p = 1 with 0.9 (the per-kernel
 // coarse levels, no single-block tail) from 42 to 184 iterations over 3
 // steps; multi-rank teams keep 0.7 too.
-const double kOmegaEnv = env_or("LDG_MG_OMEGA", -1.0);
 constexpr double kOmegaP[5] = {0.9, 0.9, 0.8, 0.8, 0.8};
 constexpr double kOmegaSafe = 0.7;
 // Chebyshev interval of level 0 (below, sweep_cheb):
@@ -74,23 +74,21 @@ constexpr double kOmegaSafe = 0.7;
 // iterations at p = 0).  Ratio 20 (10: p = 4 20 iterations; 30: +1 at p <= 3).
 // (plain meshes, set_omega; jittered meshes / strips keep 1.15: config 4
 // went from 22 to 24 iterations with 1.08 and coarse V(2,2))
-const double kChebSafetyEnv = env_or("LDG_MG_CHEB_SAFETY", -1.0);
 double kChebSafety = 1.15;
 // coarse post-sweeps: 2 on plain meshes (above), 1 on jittered meshes / strips
 // (config 4 with 2: 24 instead of 22 iterations, 1.39 instead of 1.25 s/step)
-const int kPostEnv = static_cast<int>(env_or("LDG_MG_POST", -1));
 int kPost = 1;  // set with kOmega
 double kOmega = kOmegaSafe;  // set per team at the top of every V-cycle (vcycle, l = 0)
 void set_omega(const Team& T) {
   const Handle& h = T.h0();
   const int p = h.p < 0 ? 0 : (h.p > 4 ? 4 : h.p);
   const bool plain = h.jitter == 0.0 && h.dim > 0 && T.size == 1 && T.nlocal() == 1;
-  kOmega = kOmegaEnv > 0.0 ? kOmegaEnv : (plain ? kOmegaP[p] : kOmegaSafe);
-  kPost = kPostEnv >= 0 ? kPostEnv : (plain ? 2 : 1);
-  kChebSafety = kChebSafetyEnv > 0.0 ? kChebSafetyEnv : (plain ? 1.08 : 1.15);
+  kOmega = plain ? kOmegaP[p] : kOmegaSafe;
+  kPost = plain ? 2 : 1;
+  kChebSafety = plain ? 1.08 : 1.15;
 }
-const int kPre = static_cast<int>(env_or("LDG_MG_PRE", 2));  // coarse levels
-const int kCoarseSweeps = static_cast<int>(env_or("LDG_MG_COARSE", 2));
+constexpr int kPre = 2;           // coarse levels
+constexpr int kCoarseSweeps = 2;  // at least, on the coarsest level
 // level 0 re-swept with the retuned coarse levels (5-step C2 bench): p = 1
 // V(5,6) 5.6 ms / 10 iterations (V(4,5) 5.8 / 11), p = 4 V(5,7) 33.7 / 15
 // (V(5,6) 34.2 / 16); p = 0, 2, 3 unchanged (V(4,4), V(3,5), V(4,5),
@@ -441,30 +439,8 @@ void f_zero(Handle& L, Vec b, Vec out) {
   }
 }
 
-// Optional (LDG_FUSE_S1 = highest fused degree, at most 2; default -1 = off):
-// thread-tier levels on one rank with stage 1 recomputed inside the stage-2
-// kernel for the element and its neighbours (k_s2f FUSE), one launch per
-// sweep instead of two.  Measured V-cycle at 256^2, p = 0 / 1 / 2 / 3: two
-// kernels 272 / 322 / 515 / 813 us, fused up to degree 1 338 / 469 / 598 /
-// 898 us (p = 2, 3 through their degree-1 level 1), up to degree 2 p = 2
-// 716 us: the dependent neighbour -> neighbour-geometry -> 2-hop x loads
-// cost more than the saved launch and t round trip.  Correct (tests pass
-// with it on), off.
-bool fuse_s1(Team& T, int l) {
-  static const int pmax = static_cast<int>(env_or("LDG_FUSE_S1", -1));  // highest fused degree, -1 none
-  if (pmax < 0 || T.size != 1 || T.nlocal() != 1) return false;
-  const Handle& L = level_of(T.h0(), l);
-  return tier(L) == kBig && L.p <= std::min(pmax, 2);
-}
-
 // r = b - S_c x (fused levels)
 void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
-  if (fuse_s1(T, l)) {
-    each(T, l, [&](Handle& L) {
-      smooth_stage2(L, 0, vp(L, x), vp(L, b), wm, dt, kOmega, vp(L, r), 0, -1, 0.0, 0, true);
-    });
-    return;
-  }
   halo(T, l, x, 1);
   each(T, l, [&](Handle& L) { f_stage1(L, x); });
   halo(T, l, kTz, 2);
@@ -473,67 +449,24 @@ void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
 
 // xo = xi + omega P^-1 (b - S_c xi) (fused levels)
 void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo) {
-  if (fuse_s1(T, l)) {
-    each(T, l, [&](Handle& L) {
-      smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, kOmega, vp(L, xo), 0, -1, 0.0, 0, true);
-    });
-    return;
-  }
   halo(T, l, xi, 1);
   each(T, l, [&](Handle& L) { f_stage1(L, xi); });
   halo(T, l, kTz, 2);
   each(T, l, [&](Handle& L) { f_stage2(L, 1, xi, b, wm, dt, xo); });
 }
 
-// Red-black block Gauss-Seidel (LDG_MG_SMOOTHER=rb): the element graph of an
-// FK mesh is bipartite (a lower triangle's neighbours are uppers), so each
-// colour is updated in place from the other colour's current values; stage 1
-// is recomputed in between (t depends on x).  Owned lowers are the elements
-// [0, K/2), owned uppers [K/2, K) on every level and strip.
-bool rb_smoother() {
-  static const bool on = [] {
-    const char* s = std::getenv("LDG_MG_SMOOTHER");
-    return s && std::string(s) == "rb";
-  }();
-  return on;
-}
-const double kOmegaGS = env_or("LDG_MG_OMEGA_GS", 1.0);
 // second Gram-Schmidt pass when the first removed more than (1 - eta) of |w|^2
-const double kReorthEta = env_or("LDG_REORTH_ETA", 0.5);
+constexpr double kReorthEta = 0.5;
 
-void sweep_rb(Team& T, int l, double wm, double dt, Vec b, Vec x, bool reverse) {
-  for (int h = 0; h < 2; ++h) {
-    const int c = reverse ? 1 - h : h;
-    halo(T, l, x, 1);
-    each(T, l, [&](Handle& L) { f_stage1(L, x); });
-    halo(T, l, kTz, 2);
-    each(T, l, [&](Handle& L) {
-      const int half = L.K / 2, k0 = c ? half : 0, k1 = c ? L.K : half;
-      if (tier(L) == kBig)
-        smooth_stage2(L, 1, vp(L, x), vp(L, b), wm, dt, kOmegaGS, vp(L, x), k0, k1);
-      else
-        small_stage2(L, 1, vp(L, x), vp(L, b), wm, dt, kOmegaGS, vp(L, x), k0, k1);
-    });
-  }
-}
-
-bool rb_level(Team& T, int l) { return rb_smoother() && tier(level_of(T.h0(), l)) != kMid; }
-
-// Chebyshev smoothing (LDG_MG_CHEB=1) on the first LDG_MG_CHEB_LEVELS levels
-// that run the fused thread kernels: the damped Jacobi sweeps replaced by
-// Chebyshev steps for P^-1 S_c on [lmax / ratio, lmax], lmax from a power
-// iteration when the V-cycle graph is captured.  Same kernels (the step's
-// extra term reads x_{k-1} from the ping-pong partner).
-bool cheb_on() {
-  static const bool on = env_or("LDG_MG_CHEB", 1) != 0;
-  return on;
-}
-const double kChebRatio = env_or("LDG_MG_CHEB_RATIO", 20.0);
-const int kChebPower = static_cast<int>(env_or("LDG_MG_CHEB_POWER", 30));  // power iterations
-const int kChebLevels = static_cast<int>(env_or("LDG_MG_CHEB_LEVELS", 1));
-bool cheb_level(Team& T, int l) {
-  return cheb_on() && l < kChebLevels && l + 1 < levels(T) && tier(level_of(T.h0(), l)) == kBig;
-}
+// Chebyshev smoothing on level 0 when it runs the fused thread kernels: the
+// damped Jacobi sweeps replaced by Chebyshev steps for P^-1 S_c on
+// [lmax / 20, lmax], lmax from a power iteration when the V-cycle graph is
+// captured.  Same kernels (the step's extra term reads x_{k-1} from the
+// ping-pong partner).  Measured against Jacobi level-0 sweeps in round 1
+// (ratio 10: p = 4 20 iterations; 30: +1 at p <= 3).
+constexpr double kChebRatio = 20.0;
+constexpr int kChebPower = 30;  // power iterations
+bool cheb_level(Team& T, int l) { return l == 0 && l + 1 < levels(T) && tier(level_of(T.h0(), l)) == kBig; }
 
 struct Cheb {
   double theta, delta, sigma, rho;
@@ -561,14 +494,11 @@ struct Cheb {
 
 void sweep_cheb(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo, double alpha, double beta,
                 bool prev_zero) {
-  const bool fuse = fuse_s1(T, l);
-  if (!fuse) {
-    halo(T, l, xi, 1);
-    each(T, l, [&](Handle& L) { f_stage1(L, xi); });
-    halo(T, l, kTz, 2);
-  }
+  halo(T, l, xi, 1);
+  each(T, l, [&](Handle& L) { f_stage1(L, xi); });
+  halo(T, l, kTz, 2);
   each(T, l, [&](Handle& L) {
-    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), 0, -1, beta, prev_zero ? 1 : 0, fuse);
+    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), beta, prev_zero ? 1 : 0);
   });
 }
 
@@ -599,20 +529,6 @@ double estimate_lmax(Team& T, int l, double wm, double dt) {
 // One V-cycle on level l: x = V(b).  Fused levels alternate x with the
 // level's scratch vector; the first (residual-free) sweep writes whichever
 // buffer makes the last sweep land in x.
-// Levels below LDG_TAIL_BELOW elements (default 64, i.e. the 8- and
-// 32-element levels, and only for p <= 1) run as one block
-// (small_tail_vcycle) on a single rank with the Jacobi smoother.  Measured
-// V-cycle at 256^2: p = 0 222 vs 239 us; p = 2 527 vs 504 us and p = 4 1593
-// vs 1312 us (one SM lacks the issue rate for the larger blocks).
-bool tail_level(Team& T, int l, bool f32) {
-  static const long below = static_cast<long>(env_or("LDG_TAIL_BELOW", 64));
-  static const int pmax = static_cast<int>(env_or("LDG_TAIL_PMAX", 1));
-  if (!f32 || l < 1 || rb_smoother() || T.size != 1 || T.nlocal() != 1) return false;
-  const Handle& L = level_of(T.h0(), l);
-  if (L.p > pmax) return false;
-  return L.K < below && levels(T) - l <= 6 && level_uses_rows(L) && level_is_small(L);
-}
-
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   if (l == 0) set_omega(T);
   if (l > 0 && l == T.h0().dense_level) {  // dense coarsest level (ldg_dense.cu): x = S_c^-1 b
@@ -621,25 +537,9 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     return;
   }
   const bool coarsest = l == levels(T) - 1;
-  if (tail_level(T, l, f32) && b == kMgB && x == kMgX) {
-    small_tail_vcycle(T.h0(), l, wm, dt, kOmega, pre_of(T.h0().p, l), post_of(T.h0().p, l), kCoarseSweeps);
-    return;
-  }
   // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
   // (every rank keeps a column), so a larger coarsest grid gets more sweeps
   const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(T.h0().p, l) - 1) + post_of(T.h0().p, l);
-  if (fused(T, l, f32) && rb_level(T, l)) {
-    each(T, l, [&](Handle& L) { f_zero(L, b, x); });
-    const int pre = coarsest ? sweeps : pre_of(T.h0().p, l) - 1;
-    for (int s = 0; s < pre; ++s) sweep_rb(T, l, wm, dt, b, x, false);
-    if (coarsest) return;
-    residual_f(T, l, wm, dt, b, x, kMgR);
-    for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
-    vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
-    for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), x));
-    for (int s = 0; s < post_of(T.h0().p, l); ++s) sweep_rb(T, l, wm, dt, b, x, true);
-    return;
-  }
   if (fused(T, l, f32) && cheb_level(T, l) && !coarsest) {
     Cheb ch(level_of(T.h0(), l).cheb_lmax);
     double a, be;
@@ -722,7 +622,6 @@ void precond_mg(Team& T, bool f32, double wm, double dt, Vec b, Vec x) {
     if (!cheb_level(T, l)) continue;
     const double lmax = estimate_lmax(T, l, wm, dt);  // (kernels run eagerly, before capture)
     for (auto& rp : T.ranks) level_of(*rp, l).cheb_lmax = lmax;
-    if (env_or("LDG_DEBUG_CHEB", 0) != 0) fprintf(stderr, "[ldg cheb] level %d lmax %.6g\n", l, lmax);
   }
   const int64_t before = team_launches(T);
   cudaGraph_t graph = nullptr;
@@ -1163,8 +1062,7 @@ void fgmres(Team& T, int pc, bool f32, double wm, double dt, const ldg_solver_op
   // one rank per process: device-resident Gram-Schmidt, host one iteration
   // behind (LDG_GS_HOST=1 selects the host-side variant below, which
   // virtual-rank teams use)
-  static const bool gs_host = env_or("LDG_GS_HOST", 0) != 0;
-  if (T.nlocal() == 1 && !gs_host) return fgmres_dev(T, pc, f32, wm, dt, o, tol, m, it_out, applies_out, rnorm_out);
+  if (T.nlocal() == 1) return fgmres_dev(T, pc, f32, wm, dt, o, tol, m, it_out, applies_out, rnorm_out);
   auto copy = [&](Vec dst, Vec src) {  // (ranks differ in ghost counts, hence in vector length)
     each(T, 0, [&](Handle& h) {
       LDG_CUDA(cudaMemcpyAsync(vp(h, dst), vp(h, src), sizeof(double) * h.vec_len(), cudaMemcpyDeviceToDevice,
@@ -1308,6 +1206,8 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   // preconditioner setup first: it needs the step's operators only, so a
   // host-buffer state upload (ldg_euler_steps_host) overlaps it
   bool f32 = false;
+  std::optional<NvtxRange> phase;  // NVTX: one range per phase of the solve
+  phase.emplace("solve setup (preconditioner, Schur rhs)");
   const int pc = prepare_precond(T, o.precond, wm, dt, &f32);
   if (T.y_pending) {
     LDG_CUDA(cudaStreamWaitEvent(T.stream, T.in_ev[1], 0));
@@ -1380,6 +1280,8 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   double rnorm = 0.0;
   join_precond(T);
   LDG_CUDA(cudaEventRecord(h0.ev[3], T.stream));  // end of the per-solve setup
+  phase.reset();
+  phase.emplace(o.krylov == 0 ? "FGMRES (V-cycle + Schur operator per iteration)" : "BiCGStab");
   if (o.krylov == 0) {
     fgmres(T, pc, f32, wm, dt, o, tol, &it, &applies, &rnorm);
   } else {
@@ -1387,6 +1289,8 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   }
 
   LDG_CUDA(cudaEventRecord(h0.ev[4], T.stream));  // end of the Krylov loop
+  phase.reset();
+  phase.emplace("flux recovery + residual contract");
   // flux recovery Z^m = M^-1 (V_Z^m - B^m C), written into Y[0 .. 2n)
 
   halo(T, 0, kC, 1);

@@ -1,11 +1,12 @@
-# ncu launch lists (gpu__time_duration, --clock-control none) of one
-# implicit-Euler step at 256^2 for each p in $PS.
+# bench line + ncu launch lists of one p=4 and one p=2 step (steady state: 5 warm-up steps)
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/ll
+O=gpurun_out/${1:-r02_prof}
 mkdir -p $O
-for P in ${PS:-4 3 2}; do
-  timeout 600 python scripts/profile_step.py --p $P --dim 256 > $O/plain_p$P.log 2>&1 && \
+timeout 600 python bench.py --no-cpu-baseline > $O/bench_c2.jsonl 2> $O/bench_c2.err; echo "c2 rc $?" >> $O/rc.txt
+for P in 4 2; do
+  timeout 600 python scripts/profile_step.py --p $P --dim 256 --warmup 5 > $O/plain_p$P.log 2>&1 && \
   timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $O/launches_p$P.csv python scripts/profile_step.py --p $P --dim 256 > $O/ncu_p$P.log 2>&1
-  echo "p$P rc $?"
+    --log-file $O/launches_p$P.csv python scripts/profile_step.py --p $P --dim 256 --warmup 5 > $O/ncu_launch_p$P.log 2>&1
+  echo "launch p$P rc $?" >> $O/rc.txt
 done
+cat $O/rc.txt

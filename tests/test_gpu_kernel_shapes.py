@@ -7,8 +7,10 @@ parity meshes (<= 32^2) would only ever see the row kernels.  Each case runs
 in a subprocess with the switch forced one way, and checks the multigrid
 solve against block-Jacobi (same state to the solve tolerance) and the FP32
 smoother against the FP64 one (same iteration count within a small margin).
-With the thread kernels on level 0 the default V-cycle smooths level 0 with
-Chebyshev polynomials (LDG_MG_CHEB); the last case covers the Jacobi sweeps."""
+With the thread kernels on level 0 the V-cycle smooths level 0 with Chebyshev
+polynomials.  The coarsest level is a dense solve on one rank (ldg_dense.cu);
+LDG_DENSE_MAX=0 covers the smoothed coarsest level the strip teams use, and
+the last case the serial preconditioner setup and the plain Krylov start."""
 from __future__ import annotations
 
 import json
@@ -66,13 +68,10 @@ def _run(rows_below: int, extra: dict | None = None) -> dict:
     return json.loads(line[4:])
 
 
-@pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (2048, {"LDG_MG_SMOOTHER": "rb"}),
-                                               (2048, {"LDG_TAIL_PMAX": "4", "LDG_TAIL_BELOW": "200"}),
-                                               (0, {"LDG_SMOOTHER_P": "32"}), (0, {"LDG_SMOOTHER_E": "32"}),
-                                               (0, {"LDG_MG_CHEB": "0"})],
-                         ids=["thread_kernels_fused_smoother", "row_kernels", "red_black_gauss_seidel",
-                              "single_block_coarse_tail", "fp32_block_inverse_copy", "fp32_smoother_copies",
-                              "jacobi_level0_no_chebyshev"])
+@pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (0, {"LDG_DENSE_MAX": "0"}),
+                                               (2048, {"LDG_SETUP_OVERLAP": "0", "LDG_EXTRAP": "0"})],
+                         ids=["thread_kernels_fused_smoother", "row_kernels", "thread_kernels_smoothed_coarsest",
+                              "default_shapes_serial_setup_plain_start"])
 def test_kernel_shape(rows_below, extra):
     out = _run(rows_below, extra)
     for key, r in out.items():
