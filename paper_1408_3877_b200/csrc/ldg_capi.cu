@@ -645,6 +645,7 @@ void ldg_destroy(ldg_handle* H) {
   for (auto& rp : T.ranks) {
     ldgb::mg_release(*rp);
     for (auto& c : rp->coarse) ldgb::dense_release(*c);
+    if (rp->replica) ldgb::dense_release(*rp->replica);
     for (auto& e : rp->ev)
       if (e) cudaEventDestroy(e);
   }

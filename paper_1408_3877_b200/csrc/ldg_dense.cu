@@ -79,7 +79,52 @@ __global__ void __launch_bounds__(256) k_dense_gemv(int n, const double* __restr
   }
 }
 
+// global FK id of local element k of strip q (W columns from q W; local
+// order: owned lowers then owned uppers, mesh.hpp:237-242 / ldg_mesh.cu)
+__device__ __forceinline__ int strip_gid(int q, int W, int dim, int k) {
+  const int a = q * W;
+  if (k < W * dim) return (a + k / dim) * dim + k % dim;
+  const int kk = k - W * dim;
+  return dim * dim + (a + kk / dim) * dim + kk % dim;
+}
+
+// the packed owned rows of all ranks ([q][i][k], k < 2 W dim) -> global SoA
+__global__ void k_rep_scatter(int size, int W, int dim, int N, long KpR, const double* __restrict__ recv,
+                              double* __restrict__ out) {
+  const long Kown = 2L * W * dim, n = static_cast<long>(size) * N * Kown;
+  for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(t / (N * Kown));
+    const long rem = t % (N * Kown);
+    const int i = static_cast<int>(rem / Kown), k = static_cast<int>(rem % Kown);
+    out[i * KpR + strip_gid(q, W, dim, k)] = recv[t];
+  }
+}
+
+// global SoA -> the owned rows of strip q (plane stride Kp)
+__global__ void k_rep_gather(int q, int W, int dim, int N, long KpR, long Kp, const double* __restrict__ xr,
+                             double* __restrict__ x) {
+  const long Kown = 2L * W * dim, n = static_cast<long>(N) * Kown;
+  for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(t / Kown), k = static_cast<int>(t % Kown);
+    x[i * Kp + k] = xr[i * KpR + strip_gid(q, W, dim, k)];
+  }
+}
+
 }  // namespace
+
+void launch_rep_scatter(Handle& R, int size, int W, const double* recv) {
+  k_rep_scatter<<<64, 256, 0, R.stream>>>(size, W, R.dim, R.N, R.Kp, recv, R.mg_b.ptr);
+  LDG_CUDA(cudaGetLastError());
+  ++R.launches;
+}
+
+void launch_rep_gather(Handle& R, Handle& L, int q, double* x) {
+  k_rep_gather<<<64, 256, 0, R.stream>>>(q, L.strip_w(), R.dim, R.N, R.Kp, L.Kp, R.mg_x.ptr, x);
+  LDG_CUDA(cudaGetLastError());
+  ++R.launches;
+}
 
 // largest dense coarsest level (unknowns); LDG_DENSE_MAX for tuning runs, 0 off
 long dense_max() {
@@ -100,6 +145,19 @@ bool dense_candidate(const Handle& L) {
   const long n = static_cast<long>(L.N) * L.K;
   return L.dim > 0 && !L.mg_pcoarse && L.size == 1 && L.p <= 1 && L.K == L.Kp && L.K % 32 == 0 &&
          n <= dense_max();
+}
+
+// Strip teams: the coarsest level of a truncated strip hierarchy (every
+// rank keeps a column) was smoothed with 2 dim sweeps, each with a halo
+// exchange, and left the distributed solves ~2x the single-rank iterations.
+// Its global mesh is tiny (2 dim^2 elements), so every rank holds it whole
+// (a one-rank Handle regenerated from the same vertex stream) with a dense
+// inverse; the V-cycle gathers the coarsest right-hand side from all ranks
+// (ncclAllGather of the owned rows), solves redundantly, and keeps its rows.
+// Degree <= 2 (the alternative here is the smoothed truncated level).
+bool replica_candidate(const Handle& C) {
+  const long K = 2L * C.dim * C.dim, n = static_cast<long>(C.N) * K;
+  return C.size > 1 && C.dim > 0 && C.p <= 2 && K % 32 == 0 && n <= dense_max();
 }
 
 void dense_alloc(Handle& L) {

@@ -174,6 +174,10 @@ struct Handle {
   // dense coarsest level (ldg_dense.cu): -S_c as a column-major n x n matrix,
   // its LU and inverse; dense_level on the top handle (0: none)
   int dense_level = 0;
+  // strip teams: the whole coarsest strip level replicated on every rank as a
+  // one-rank mesh with a dense inverse (top handle; ldg_team.cu replica_solve)
+  std::unique_ptr<Handle> replica;
+  int replica_level = 0;                         // the strip level it replaces (0: none)
   int dn_n = 0;
   DBuf<double> dn_A, dn_inv, dn_X, dn_T, dn_zero, dn_work, dn_T2, dn_X2, dn_res;
   DBuf<int> dn_ipiv, dn_info;
@@ -233,6 +237,7 @@ struct Team {
   bool owns_nccl = false;
   cudaStream_t stream = nullptr;
   DBuf<double> send_l, send_r, recv_l, recv_r;  // NCCL halo staging
+  DBuf<double> rep_send, rep_recv;              // coarsest-level gather (replicated dense solve)
   DBuf<double> red_all;                         // allreduce scratch
   double* red_host = nullptr;                   // pinned
   double* gs_host = nullptr;                    // pinned: FGMRES Gram-Schmidt slots (kMaxRed x (2 kMaxRed + 1))
@@ -382,6 +387,9 @@ int mg_depth(int dim, int team_size);
 // dense coarsest level (ldg_dense.cu)
 long dense_max();
 bool dense_candidate(const Handle& L);
+bool replica_candidate(const Handle& coarsest);  // strip level whose global mesh can be solved densely
+void launch_rep_scatter(Handle& R, int size, int W, const double* recv);  // packed owned rows -> R.mg_b
+void launch_rep_gather(Handle& R, Handle& L, int q, double* x);           // R.mg_x -> owned rows of strip q
 void dense_alloc(Handle& L);
 void dense_release(Handle& L);
 void dense_setup(Handle& L, double wm, double dt, bool f32);

@@ -305,6 +305,30 @@ bool mg_build(Handle& h, int team_size) {
     fine = c.get();
     h.coarse.push_back(std::move(c));
   }
+  // strip team: the coarsest strip level replicated whole on this rank
+  // (the first h-level small enough; the levels below it are never visited)
+  int rl = 0;
+  for (size_t i = 0; team_size > 1 && i < h.coarse.size() && !rl; ++i)
+    if (!h.coarse[i]->mg_pcoarse && replica_candidate(*h.coarse[i])) rl = static_cast<int>(i) + 1;
+  if (rl > 0) {
+    const Handle& C = *h.coarse[rl - 1];
+    h.replica_level = rl;
+    auto r = std::make_unique<Handle>();
+    r->p = C.p;
+    r->N = C.N;
+    r->prob = C.prob;
+    r->dtab = C.dtab;
+    r->stream = h.stream;
+    r->owns_stream = false;
+    r->rule_shared = C.rule_ptr();
+    r->rule_shared_R = C.rule_R();
+    r->rank = 0;
+    r->size = 1;
+    build_square_strip(*r, C.dim, 0, C.dim, C.stride, C.dim_fine, C.jitter, C.seed);
+    alloc_coarse(*r);
+    dense_alloc(*r);
+    h.replica = std::move(r);
+  }
   // dense coarsest level: the first h-level small enough (single rank)
   for (size_t i = 0; i < h.coarse.size(); ++i) {
     Handle& c = *h.coarse[i];
@@ -377,6 +401,7 @@ void mg_setup_coarse(Handle& h, double t, double wm, double dt, bool f32) {
   for (auto& cp : h.coarse) {
     const int lvl = static_cast<int>(&cp - &h.coarse[0]) + 1;
     if (h.dense_level > 0 && lvl > h.dense_level) break;  // below the dense level: never visited
+    if (h.replica_level > 0 && lvl > h.replica_level) break;
     Handle& c = *cp;
     launch_project(c, h.prob.d, t, c.rule_ptr(), c.rule_R(), c.D.ptr, c.Kg);
     launch_assemble(c, kModeEdiag, c.E.ptr);
@@ -386,6 +411,12 @@ void mg_setup_coarse(Handle& h, double t, double wm, double dt, bool f32) {
       launch_bjac_setup(c, wm, dt);
     if (lvl == h.dense_level) dense_setup(c, wm, dt, f32);
     if (debug_nan()) debug_level(c, lvl);
+  }
+  if (h.replica) {  // the replicated coarsest strip level: same operator, whole mesh
+    Handle& r = *h.replica;
+    launch_project(r, h.prob.d, t, r.rule_ptr(), r.rule_R(), r.D.ptr, r.Kg);
+    launch_assemble(r, kModeEdiag, r.E.ptr);
+    dense_setup(r, wm, dt, false);
   }
 }
 

@@ -529,8 +529,42 @@ double estimate_lmax(Team& T, int l, double wm, double dt) {
 // One V-cycle on level l: x = V(b).  Fused levels alternate x with the
 // level's scratch vector; the first (residual-free) sweep writes whichever
 // buffer makes the last sweep land in x.
+// Strip teams: the coarsest strip level solved on every rank's replica of its
+// whole mesh (ldg_dense.cu replica_candidate): the owned rows of b from all
+// ranks (one ncclAllGather, or device copies between virtual ranks), a
+// redundant dense solve, the owned rows of x back.
+void replica_solve(Team& T, int l, Vec b, Vec x) {
+  Handle& L0 = level_of(T.h0(), l);
+  const long cnt = static_cast<long>(L0.N) * L0.K;  // owned rows, equal on every rank
+  for (int r = 0; r < T.nlocal(); ++r) {
+    Handle& L = level_of(*T.ranks[r], l);
+    LDG_CUDA(cudaMemcpy2DAsync(T.rep_send.ptr + r * cnt, sizeof(double) * L.K, vp(L, b), sizeof(double) * L.Kp,
+                               sizeof(double) * L.K, L.N, cudaMemcpyDeviceToDevice, T.stream));
+  }
+  if (T.nlocal() == T.size) {  // every rank local: the gather is a copy
+    LDG_CUDA(cudaMemcpyAsync(T.rep_recv.ptr, T.rep_send.ptr, sizeof(double) * cnt * T.size, cudaMemcpyDeviceToDevice,
+                             T.stream));
+  } else {
+    if (T.nlocal() != 1 || !T.nccl) throw Error(LDG_ENCCL, "replicated coarse solve: one rank per process expected");
+    LDG_NCCL(ncclAllGather(T.rep_send.ptr, T.rep_recv.ptr, cnt, ncclDouble, static_cast<ncclComm_t>(T.nccl),
+                           T.stream));
+  }
+  for (int r = 0; r < T.nlocal(); ++r) {
+    Handle& top = *T.ranks[r];
+    Handle& R = *top.replica;
+    Handle& L = level_of(top, l);
+    launch_rep_scatter(R, T.size, L.strip_w(), T.rep_recv.ptr);
+    dense_solve(R, R.mg_b.ptr, R.mg_x.ptr);
+    launch_rep_gather(R, L, T.first + r, vp(L, x));
+  }
+}
+
 void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   if (l == 0) set_omega(T);
+  if (l > 0 && l == T.h0().replica_level) {
+    replica_solve(T, l, b, x);
+    return;
+  }
   if (l > 0 && l == T.h0().dense_level) {  // dense coarsest level (ldg_dense.cu): x = S_c^-1 b
     Handle& L = level_of(T.h0(), l);
     dense_solve(L, vp(L, b), vp(L, x));
@@ -666,6 +700,12 @@ int prepare_precond(Team& T, int pc, double wm, double dt, bool* f32) {
     bool ok = true;
     for (auto& rp : T.ranks) ok = mg_build(*rp, T.size) && ok;
     if (!ok) pc = 1;  // no FK hierarchy (general mesh): block-Jacobi
+    if (ok && T.h0().replica && !T.rep_recv.ptr) {  // gather staging (before any V-cycle capture)
+      const Handle& C = *T.h0().coarse[T.h0().replica_level - 1];
+      const long cnt = static_cast<long>(C.N) * C.K;
+      T.rep_send.alloc(cnt * T.nlocal(), nullptr);
+      T.rep_recv.alloc(cnt * T.size, nullptr);
+    }
   }
   *f32 = pc == 2;
   if (pc == 1 || pc == 3) each(T, 0, [&](Handle& h) { launch_bjac_setup(h, wm, dt); });
@@ -683,20 +723,24 @@ int prepare_precond(Team& T, int pc, double wm, double dt, bool* f32) {
       LDG_CUDA(cudaEventRecord(T.setup_ev[0], T.stream));
       for (auto& st : T.setup_stream) LDG_CUDA(cudaStreamWaitEvent(st, T.setup_ev[0], 0));
       auto on_stream = [&](cudaStream_t st, auto&& fn) {  // the levels' launches go to st
+        std::vector<Handle*> hs{&h};
+        for (auto& c : h.coarse) hs.push_back(c.get());
+        if (h.replica) hs.push_back(h.replica.get());
         std::vector<cudaStream_t> saved;
-        saved.push_back(h.stream);
-        for (auto& c : h.coarse) saved.push_back(c->stream);
-        h.stream = st;
-        for (auto& c : h.coarse) c->stream = st;
+        for (Handle* x : hs) {
+          saved.push_back(x->stream);
+          x->stream = st;
+        }
+        auto restore = [&] {
+          for (size_t i = 0; i < hs.size(); ++i) hs[i]->stream = saved[i];
+        };
         try {
           fn();
         } catch (...) {
-          h.stream = saved[0];
-          for (size_t i = 0; i < h.coarse.size(); ++i) h.coarse[i]->stream = saved[i + 1];
+          restore();
           throw;
         }
-        h.stream = saved[0];
-        for (size_t i = 0; i < h.coarse.size(); ++i) h.coarse[i]->stream = saved[i + 1];
+        restore();
       };
       on_stream(T.setup_stream[0], [&] { mg_setup_top(h, wm, dt, *f32); });
       on_stream(T.setup_stream[1], [&] { mg_setup_coarse(h, h.t_assembled, wm, dt, *f32); });
@@ -1395,6 +1439,10 @@ int team_time_mg(Team& T, double wm, double dt, int reps, double* ms_vcycle, dou
     if (l > 0 && l == h.dense_level) {  // the dense coarsest level: one solve; the levels below are never visited
       Handle& L = level_of(h, l);
       ms_level[l] = graph_time([&] { dense_solve(L, vp(L, b), vp(L, x)); });
+      return l + 1;
+    }
+    if (l > 0 && l == h.replica_level) {
+      ms_level[l] = graph_time([&] { replica_solve(T, l, b, x); });
       return l + 1;
     }
     if (fused(T, l, f32))

@@ -57,15 +57,17 @@ def test_strip_euler_steps_match_single(nranks, p, pc, krylov, ld):
     grp.initial_state()
     st1 = one.euler_steps(0.1, 3, opts)
     st2 = grp.euler_steps(0.1, 3, opts)
+    print(f"iterations one rank {st1['iterations']}, {nranks} strips {st2['iterations']}")
     assert st2["residual"] <= 1e-10
     y1, t1 = one.get_state()
     y2, t2 = grp.get_state()
     assert t1 == t2
     assert np.linalg.norm(y2 - y1) / np.linalg.norm(y1) <= 1e-10
-    # the distributed multigrid stays within a small factor of the single-rank
-    # iteration count (strips stop coarsening while every rank keeps a column
-    # and smooth that level; one rank solves its coarsest level densely)
-    assert st2["iterations"] <= 2.5 * st1["iterations"] + 6, (st1["iterations"], st2["iterations"])
+    # the distributed multigrid stays close to the single-rank iteration count
+    # (strips stop coarsening while every rank keeps a column; that level is
+    # solved on a per-rank replica of its whole mesh, as one rank solves its
+    # coarsest level densely)
+    assert st2["iterations"] <= 1.5 * st1["iterations"] + 6, (st1["iterations"], st2["iterations"])
 
 
 def test_strip_host_buffer_step(ld):
