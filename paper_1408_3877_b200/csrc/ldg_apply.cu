@@ -309,12 +309,13 @@ __device__ __forceinline__ void apply_S(const STab<P>& tb, const DevMesh& m, con
 // stage 1: tout^m = M_k^-1 (sigma vz^m + tau sum_s B^m[s] x_col(s))
 template <int P>
 __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1(DevMesh m, DevTables T, const double* __restrict__ vz, double sigma,
-                                                const double* __restrict__ x, double tau, double* __restrict__ tout) {
+                                                const double* __restrict__ x, double tau, double* __restrict__ tout,
+                                                int k0, int k1) {
   constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
   const STab<P> tb = stage_tables<P>(sm, T);
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m.K) return;
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
   double u1[N], u2[N];
@@ -349,12 +350,12 @@ __global__ void __launch_bounds__(128, LDG_MINB_S2STAGE_P(P)) k_stage2(DevMesh m
                                                 const double* __restrict__ D, const double* __restrict__ x,
                                                 double alpha, double beta, const double* __restrict__ tz,
                                                 double gamma, const double* __restrict__ w, double delta,
-                                                double* __restrict__ y) {
+                                                double* __restrict__ y, int k0, int k1) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
   const STab<P> tb = stage_tables<P, true>(sm, T);
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m.K) return;
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
   const long Kp = m.Kp;
   double acc[N];
 #pragma unroll
@@ -486,13 +487,19 @@ bool use_rows(const Handle& h) {
 
 }  // namespace
 
-void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout) {
-  if (use_rows(h)) return rows_stage1(h, vz, sigma, x, tau, tout);
-  const unsigned grid = grid_of(h.K, 128);
-#define CALL(P)                                                                                       \
-  do {                                                                                                \
-    set_smem(k_stage1<P>, tab_smem<P>());                                                             \
-    k_stage1<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, vz, sigma, x, tau, tout);   \
+void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout, int k0,
+                   int k1) {
+  if (k1 < 0) k1 = h.K;
+  if (k1 <= k0) return;
+  if (use_rows(h)) {
+    if (k0 != 0 || k1 != h.K) throw Error(LDG_EINVAL, "element range on the row kernels");
+    return rows_stage1(h, vz, sigma, x, tau, tout);
+  }
+  const unsigned grid = grid_of(k1 - k0, 128);
+#define CALL(P)                                                                                               \
+  do {                                                                                                        \
+    set_smem(k_stage1<P>, tab_smem<P>());                                                                     \
+    k_stage1<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, vz, sigma, x, tau, tout, k0, k1);   \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -501,14 +508,19 @@ void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, d
 }
 
 void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
-                   const double* w, double delta, double* y) {
-  if (use_rows(h)) return rows_stage2<double>(h, h.E.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
-  const unsigned grid = grid_of(h.K, 128);
+                   const double* w, double delta, double* y, int k0, int k1) {
+  if (k1 < 0) k1 = h.K;
+  if (k1 <= k0) return;
+  if (use_rows(h)) {
+    if (k0 != 0 || k1 != h.K) throw Error(LDG_EINVAL, "element range on the row kernels");
+    return rows_stage2<double>(h, h.E.ptr, x, alpha_m, beta_s, tz, gamma_e, w, delta, y);
+  }
+  const unsigned grid = grid_of(k1 - k0, 128);
 #define CALL(P)                                                                                               \
   do {                                                                                                        \
     set_smem(k_stage2<P>, tab_edge_smem<P>());                                                                \
     k_stage2<P><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, x, alpha_m,  \
-                                                             beta_s, tz, gamma_e, w, delta, y);               \
+                                                             beta_s, tz, gamma_e, w, delta, y, k0, k1);       \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

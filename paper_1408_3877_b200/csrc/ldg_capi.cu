@@ -657,6 +657,12 @@ void ldg_destroy(ldg_handle* H) {
   if (T.in_stream) cudaStreamDestroy(T.in_stream);
   for (auto& e : T.setup_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : T.comm_ev)
+    if (e) cudaEventDestroy(e);
+  if (T.comm_stream) {
+    cudaStreamSynchronize(T.comm_stream);
+    cudaStreamDestroy(T.comm_stream);
+  }
   for (auto& st : T.setup_stream)
     if (st) {
       cudaStreamSynchronize(st);

@@ -237,6 +237,8 @@ struct Team {
   bool owns_nccl = false;
   cudaStream_t stream = nullptr;
   DBuf<double> send_l, send_r, recv_l, recv_r;  // NCCL halo staging
+  cudaStream_t comm_stream = nullptr;           // NCCL halo exchange, overlapping the interior elements
+  cudaEvent_t comm_ev[2] = {};                  // packed (main -> comm), landed (comm -> main)
   DBuf<double> rep_send, rep_recv;              // coarsest-level gather (replicated dense solve)
   DBuf<double> red_all;                         // allreduce scratch
   double* red_host = nullptr;                   // pinned
@@ -309,9 +311,11 @@ void upload_lagrange_phi(Handle& h, DBuf<double>& buf);
 void launch_lagrange(Handle& h, const double* phi, const double* u, double* out);  // out: K x nodes k-major
 
 // solver (ldg_solve.cu)
-void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout);
+// [k0, k1): owned element range (default all; thread-per-element levels only)
+void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, double tau, double* tout, int k0 = 0,
+                   int k1 = -1);
 void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, const double* tz, double gamma_e,
-                   const double* w, double delta, double* y);
+                   const double* w, double delta, double* y, int k0 = 0, int k1 = -1);
 void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double* out);
 void launch_bjac_setup(Handle& h, double wm, double dt);
 void launch_bjac_apply(Handle& h, const double* x, double* y);
@@ -337,12 +341,12 @@ bool level_is_small(const Handle& h);
 // fused mixed-precision smoother (ldg_smooth.cu)
 long packed_p_quads(int p);                                           // float4 quads of one packed P^-1 block
 void smooth_pack_e(Handle& h);                                        // Eh (FP16 packed) from E
-void smooth_stage1(Handle& h, const double* x);                       // tz = M^-1 B x (FP32 arithmetic)
+void smooth_stage1(Handle& h, const double* x, int k0 = 0, int k1 = -1);  // tz = M^-1 B x (FP32 arithmetic)
 // mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)
 // cheb_beta != 0: Chebyshev step out <- x + omega P^-1 r + cheb_beta (x - out_old)
 // (out_old = x_{k-1}, taken as 0 when prev_zero)
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, double cheb_beta = 0.0, int prev_zero = 0);
+                   double* out, double cheb_beta = 0.0, int prev_zero = 0, int k0 = 0, int k1 = -1);
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 // the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
 void small_stage1(Handle& h, const double* x);

@@ -122,14 +122,14 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
 // tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
 template <int P, typename TT>
 __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
-                                             TT* __restrict__ tout) {
+                                             TT* __restrict__ tout, int k0, int k1) {
   constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
   extern __shared__ __align__(16) float smf[];
   const float* tb = stage_f(smf, T.fbase + T.fmH, 14 * TAB);  // tmH 2 | tmSd 3 | tmSo 9
   pdl_wait();
   pdl_trigger();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m.K) return;
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
   float xv[N], w[N], u1[N], u2[N];
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
                                              const TT* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const TP* __restrict__ Pq,
                                              const float* __restrict__ Pscale, float omega, double* out,
-                                             double cheb_beta, int prev_zero) {
+                                             double cheb_beta, int prev_zero, int k0, int k1) {
   using C = Cfg<P>;
   constexpr int N = C::N, NF = C::NF, TAB = N * NF;
   constexpr int Q = C::Q;
@@ -286,10 +286,10 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
   const float* s_pth = s_pe + 3 * Q * N;
   const float* s_we = s_pth + 9 * Q * N;
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   pdl_trigger();
-  if (k >= m.K) return;
+  if (k >= k1) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
   float acc[N];
@@ -475,15 +475,16 @@ void smooth_pack_e(Handle& h) {
   ++h.launches;
 }
 
-void smooth_stage1(Handle& h, const double* x) {
-#define CALL(P)                                                                            \
-  do {                                                                                                          \
-    if (h.tz32.ptr)                                                                                             \
-      launch_pdl(k_s1f<P, float>, grid_of(h.K, 128), 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x,          \
-                 h.tz32.ptr);                                                                                   \
-    else                                                                                                        \
-      launch_pdl(k_s1f<P, double>, grid_of(h.K, 128), 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x,         \
-                 h.tz.ptr);                                                                                     \
+void smooth_stage1(Handle& h, const double* x, int k0, int k1) {
+  if (k1 < 0) k1 = h.K;
+  if (k1 <= k0) return;
+  const unsigned grid = grid_of(k1 - k0, 128);
+#define CALL(P)                                                                                               \
+  do {                                                                                                        \
+    if (h.tz32.ptr)                                                                                           \
+      launch_pdl(k_s1f<P, float>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz32.ptr, k0, k1); \
+    else                                                                                                      \
+      launch_pdl(k_s1f<P, double>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr, k0, k1); \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -492,13 +493,16 @@ void smooth_stage1(Handle& h, const double* x) {
 }
 
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
-                   double* out, double cheb_beta, int prev_zero) {
+                   double* out, double cheb_beta, int prev_zero, int k0, int k1) {
   const double dteta = dt * h.prob.eta;
   const float om = static_cast<float>(omega);
-  const unsigned grid = grid_of(h.K, 128);
+  if (k1 < 0) k1 = h.K;
+  if (k1 <= k0) return;
+  const unsigned grid = grid_of(k1 - k0, 128);
 #define LAUNCH(P, M, TT, TZ)                                                                                      \
   launch_pdl(k_s2f<P, M, uint2, uint2, TT>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, h.Eh.ptr,        \
-             h.Escale.ptr, h.D.ptr, x, TZ, b, wm, dteta, dt, h.Ph.ptr, h.Pscale.ptr, om, out, cheb_beta, prev_zero)
+             h.Escale.ptr, h.D.ptr, x, TZ, b, wm, dteta, dt, h.Ph.ptr, h.Pscale.ptr, om, out, cheb_beta, prev_zero, \
+             k0, k1)
 #define CALL(P)                                           \
   do {                                                    \
     if (mode == 0 && h.tz32.ptr)                          \

@@ -179,10 +179,15 @@ bool cudaStreamIsCapturing_(cudaStream_t s) {
   return st != cudaStreamCaptureStatusNone;
 }
 
-// Refreshes the ghost columns of vector v (ncomp blocks of N planes) on
-// level `level` of every local rank.
-void halo(Team& T, int level, Vec v, int ncomp) {
-  if (T.size == 1) return;
+// Ghost-column refresh of vector v (ncomp blocks of N planes) on level
+// `level` of every local rank, split for overlap with computation:
+// halo_begin copies the ghosts of local neighbours (virtual ranks: device
+// copies, complete in stream order) and posts the exchange with remote ones
+// (owned boundary columns packed on the main stream, ncclSend/Recv on the
+// team's comm stream); halo_end joins the comm stream and unpacks.  Returns
+// whether a remote exchange is in flight.
+bool halo_begin(Team& T, int level, Vec v, int ncomp) {
+  if (T.size == 1) return false;
   bool remote = false;
   for (int r = 0; r < T.nlocal(); ++r) {
     Handle& L = level_of(*T.ranks[r], level);
@@ -205,38 +210,86 @@ void halo(Team& T, int level, Vec v, int ncomp) {
       }
     }
   }
-  if (!remote) return;
-  // remote neighbours: pack the owned boundary columns, exchange, unpack
+  if (!remote) return false;
   auto* comm = static_cast<ncclComm_t>(T.nccl);
   if (!comm) throw Error(LDG_ENCCL, "ranks without a communicator");
-  for (int r = 0; r < T.nlocal(); ++r) {
-    Handle& L = level_of(*T.ranks[r], level);
-    const int g = T.first + r;
-    const long rows = static_cast<long>(ncomp) * L.N;
-    const long cnt = rows * L.dim;
-    const bool left = L.ghost_left && !T.local(g - 1), right = L.ghost_right && !T.local(g + 1);
-    if (static_cast<long>(T.send_l.n) < cnt) {
-      // sized once for the largest exchange (3 components on level 0): the
-      // V-cycle graphs bake these pointers, so they must never move
-      if (cudaStreamIsCapturing_(T.stream)) throw Error(LDG_ENCCL, "halo staging allocated during graph capture");
-      const long cap = std::max(cnt, 3L * T.h0().N * T.h0().dim);
-      for (DBuf<double>* b : {&T.send_l, &T.send_r, &T.recv_l, &T.recv_r}) b->alloc(cap, nullptr);
-    }
-    if (left) copy_cols(T.send_l.ptr, L.dim, vp(L, v) + L.own_left_off(), L.Kp, L.dim, rows, T.stream);
-    if (right) copy_cols(T.send_r.ptr, L.dim, vp(L, v) + L.own_right_off(), L.Kp, L.dim, rows, T.stream);
-    LDG_NCCL(ncclGroupStart());
-    if (left) {
-      LDG_NCCL(ncclSend(T.send_l.ptr, cnt, ncclDouble, g - 1, comm, T.stream));
-      LDG_NCCL(ncclRecv(T.recv_l.ptr, cnt, ncclDouble, g - 1, comm, T.stream));
-    }
-    if (right) {
-      LDG_NCCL(ncclSend(T.send_r.ptr, cnt, ncclDouble, g + 1, comm, T.stream));
-      LDG_NCCL(ncclRecv(T.recv_r.ptr, cnt, ncclDouble, g + 1, comm, T.stream));
-    }
-    LDG_NCCL(ncclGroupEnd());
-    if (left) copy_cols(vp(L, v) + L.ghost_left_off(), L.Kp, T.recv_l.ptr, L.dim, L.dim, rows, T.stream);
-    if (right) copy_cols(vp(L, v) + L.ghost_right_off(), L.Kp, T.recv_r.ptr, L.dim, L.dim, rows, T.stream);
+  if (T.nlocal() != 1) throw Error(LDG_ENCCL, "remote halo: one rank per process expected");
+  if (!T.comm_stream) {
+    if (cudaStreamIsCapturing_(T.stream)) throw Error(LDG_ENCCL, "comm stream created during graph capture");
+    LDG_CUDA(cudaStreamCreateWithFlags(&T.comm_stream, cudaStreamNonBlocking));
+    for (auto& e : T.comm_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  Handle& L = level_of(T.h0(), level);
+  const int g = T.first;
+  const long rows = static_cast<long>(ncomp) * L.N;
+  const long cnt = rows * L.dim;
+  const bool left = L.ghost_left != 0, right = L.ghost_right != 0;
+  if (static_cast<long>(T.send_l.n) < cnt) {
+    // sized once for the largest exchange (3 components on level 0): the
+    // V-cycle graphs bake these pointers, so they must never move
+    if (cudaStreamIsCapturing_(T.stream)) throw Error(LDG_ENCCL, "halo staging allocated during graph capture");
+    const long cap = std::max(cnt, 3L * T.h0().N * T.h0().dim);
+    for (DBuf<double>* b : {&T.send_l, &T.send_r, &T.recv_l, &T.recv_r}) b->alloc(cap, nullptr);
+  }
+  if (left) copy_cols(T.send_l.ptr, L.dim, vp(L, v) + L.own_left_off(), L.Kp, L.dim, rows, T.stream);
+  if (right) copy_cols(T.send_r.ptr, L.dim, vp(L, v) + L.own_right_off(), L.Kp, L.dim, rows, T.stream);
+  LDG_CUDA(cudaEventRecord(T.comm_ev[0], T.stream));
+  LDG_CUDA(cudaStreamWaitEvent(T.comm_stream, T.comm_ev[0], 0));
+  LDG_NCCL(ncclGroupStart());
+  if (left) {
+    LDG_NCCL(ncclSend(T.send_l.ptr, cnt, ncclDouble, g - 1, comm, T.comm_stream));
+    LDG_NCCL(ncclRecv(T.recv_l.ptr, cnt, ncclDouble, g - 1, comm, T.comm_stream));
+  }
+  if (right) {
+    LDG_NCCL(ncclSend(T.send_r.ptr, cnt, ncclDouble, g + 1, comm, T.comm_stream));
+    LDG_NCCL(ncclRecv(T.recv_r.ptr, cnt, ncclDouble, g + 1, comm, T.comm_stream));
+  }
+  LDG_NCCL(ncclGroupEnd());
+  LDG_CUDA(cudaEventRecord(T.comm_ev[1], T.comm_stream));
+  return true;
+}
+
+void halo_end(Team& T, int level, Vec v, int ncomp) {
+  LDG_CUDA(cudaStreamWaitEvent(T.stream, T.comm_ev[1], 0));
+  Handle& L = level_of(T.h0(), level);
+  const long rows = static_cast<long>(ncomp) * L.N;
+  if (L.ghost_left) copy_cols(vp(L, v) + L.ghost_left_off(), L.Kp, T.recv_l.ptr, L.dim, L.dim, rows, T.stream);
+  if (L.ghost_right) copy_cols(vp(L, v) + L.ghost_right_off(), L.Kp, T.recv_r.ptr, L.dim, L.dim, rows, T.stream);
+}
+
+void halo(Team& T, int level, Vec v, int ncomp) {
+  if (halo_begin(T, level, v, ncomp)) halo_end(T, level, v, ncomp);
+}
+
+// Owned elements of a strip whose stencil reaches no ghost: the lowers of
+// column a touch the ghost uppers of column a - 1, the uppers of column b - 1
+// the ghost lowers of column b; everything in between is interior.
+int interior_lo(const Handle& L) { return L.ghost_left ? L.dim : 0; }
+int interior_hi(const Handle& L) { return L.ghost_right ? L.K - L.dim : L.K; }
+
+// A stage on `level` whose input v needs fresh ghost columns.  On strips with
+// thread-per-element kernels (ranged == true) the interior elements run while
+// the halo is in flight and the boundary columns after it lands (virtual
+// ranks take the same split, so one GPU exercises the element ranges);
+// otherwise the whole level after the halo.  launch(L, k0, k1), k1 = -1: all.
+template <typename F>
+void staged(Team& T, int level, Vec v, int ncomp, bool ranged, F launch) {
+  if (T.size == 1) {
+    each(T, level, [&](Handle& L) { launch(L, 0, -1); });
+    return;
+  }
+  const bool pending = halo_begin(T, level, v, ncomp);
+  if (!ranged) {
+    if (pending) halo_end(T, level, v, ncomp);
+    each(T, level, [&](Handle& L) { launch(L, 0, -1); });
+    return;
+  }
+  each(T, level, [&](Handle& L) { launch(L, interior_lo(L), interior_hi(L)); });
+  if (pending) halo_end(T, level, v, ncomp);
+  each(T, level, [&](Handle& L) {
+    launch(L, 0, interior_lo(L));
+    launch(L, interior_hi(L), L.K);
+  });
 }
 
 // Launches per-rank partial dots (launch(h) issues launch_dots_async), then
@@ -339,11 +392,13 @@ void each(Team& T, int level, F f) {
 // y = a1 (wM x) + b1 dt eta S x - g1 dt sum E^m t^m(x) + d1 w   (tz = M^-1 B x computed here)
 void schur_like(Team& T, int level, bool f32, Vec x, double alpha, double beta, double gamma, Vec w, double delta,
                 Vec y) {
-  halo(T, level, x, 1);
-  each(T, level, [&](Handle& L) { launch_stage1(L, nullptr, 0.0, vp(L, x), 1.0, L.tz.ptr); });
-  halo(T, level, kTz, 2);
   (void)f32;  // the FP32 smoother has its own kernels (f_stage1 / f_stage2)
-  each(T, level, [&](Handle& L) { launch_stage2(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y)); });
+  const bool ranged = !level_uses_rows(level_of(T.h0(), level));
+  staged(T, level, x, 1, ranged,
+         [&](Handle& L, int k0, int k1) { launch_stage1(L, nullptr, 0.0, vp(L, x), 1.0, L.tz.ptr, k0, k1); });
+  staged(T, level, kTz, 2, ranged, [&](Handle& L, int k0, int k1) {
+    launch_stage2(L, vp(L, x), alpha, beta, L.tz.ptr, gamma, vp(L, w), delta, vp(L, y), k0, k1);
+  });
 }
 
 void schur_apply(Team& T, double wm, double dt, Vec x, Vec y) {
@@ -405,17 +460,17 @@ Tier tier(const Handle& L) {
   return level_is_small(L) ? kSmall : kMid;
 }
 
-void f_stage1(Handle& L, Vec x) {
+void f_stage1(Handle& L, Vec x, int k0 = 0, int k1 = -1) {
   switch (tier(L)) {
-    case kBig: smooth_stage1(L, vp(L, x)); break;
+    case kBig: smooth_stage1(L, vp(L, x), k0, k1); break;
     case kMid: rows_stage1(L, nullptr, 0.0, vp(L, x), 1.0, L.tz.ptr); break;
     default: small_stage1(L, vp(L, x)); break;
   }
 }
 
-void f_stage2(Handle& L, int mode, Vec x, Vec b, double wm, double dt, Vec out) {
+void f_stage2(Handle& L, int mode, Vec x, Vec b, double wm, double dt, Vec out, int k0 = 0, int k1 = -1) {
   switch (tier(L)) {
-    case kBig: smooth_stage2(L, mode, vp(L, x), vp(L, b), wm, dt, kOmega, vp(L, out)); break;
+    case kBig: smooth_stage2(L, mode, vp(L, x), vp(L, b), wm, dt, kOmega, vp(L, out), 0.0, 0, k0, k1); break;
     case kSmall: small_stage2(L, mode, vp(L, x), vp(L, b), wm, dt, kOmega, vp(L, out)); break;
     default: {
       const double eta = L.prob.eta;
@@ -439,20 +494,20 @@ void f_zero(Handle& L, Vec b, Vec out) {
   }
 }
 
+bool ranged_level(Team& T, int l) { return tier(level_of(T.h0(), l)) == kBig; }
+
 // r = b - S_c x (fused levels)
 void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
-  halo(T, l, x, 1);
-  each(T, l, [&](Handle& L) { f_stage1(L, x); });
-  halo(T, l, kTz, 2);
-  each(T, l, [&](Handle& L) { f_stage2(L, 0, x, b, wm, dt, r); });
+  const bool rg = ranged_level(T, l);
+  staged(T, l, x, 1, rg, [&](Handle& L, int k0, int k1) { f_stage1(L, x, k0, k1); });
+  staged(T, l, kTz, 2, rg, [&](Handle& L, int k0, int k1) { f_stage2(L, 0, x, b, wm, dt, r, k0, k1); });
 }
 
 // xo = xi + omega P^-1 (b - S_c xi) (fused levels)
 void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo) {
-  halo(T, l, xi, 1);
-  each(T, l, [&](Handle& L) { f_stage1(L, xi); });
-  halo(T, l, kTz, 2);
-  each(T, l, [&](Handle& L) { f_stage2(L, 1, xi, b, wm, dt, xo); });
+  const bool rg = ranged_level(T, l);
+  staged(T, l, xi, 1, rg, [&](Handle& L, int k0, int k1) { f_stage1(L, xi, k0, k1); });
+  staged(T, l, kTz, 2, rg, [&](Handle& L, int k0, int k1) { f_stage2(L, 1, xi, b, wm, dt, xo, k0, k1); });
 }
 
 // second Gram-Schmidt pass when the first removed more than (1 - eta) of |w|^2
@@ -494,11 +549,9 @@ struct Cheb {
 
 void sweep_cheb(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo, double alpha, double beta,
                 bool prev_zero) {
-  halo(T, l, xi, 1);
-  each(T, l, [&](Handle& L) { f_stage1(L, xi); });
-  halo(T, l, kTz, 2);
-  each(T, l, [&](Handle& L) {
-    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), beta, prev_zero ? 1 : 0);
+  staged(T, l, xi, 1, true, [&](Handle& L, int k0, int k1) { f_stage1(L, xi, k0, k1); });
+  staged(T, l, kTz, 2, true, [&](Handle& L, int k0, int k1) {
+    smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), beta, prev_zero ? 1 : 0, k0, k1);
   });
 }
 
