@@ -58,25 +58,56 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
 // -- FP32 for the FP16 smoother copy (OUT 3: the result is rounded to 11
 // bits anyway; FP32 issues twice the FMAs per cycle and holds half the
 // registers), FP64 otherwise.
+// The block's diagonal E blocks are staged in shared memory first (one
+// coalesced 128-byte segment per plane and 16 elements, every load of the
+// block in flight at once): read straight from HBM by row-lanes of different
+// elements, the 2 N^2 loads per lane touched a sector each (k_bjac_warp<4>
+// was L1-bound at 1.44 ms for 518 MB).  The edge tables sit in shared memory
+// too, and the neighbour's d_h at the edge points (Q dot products of length
+// N) is computed once per element instead of once per row-lane.
+template <int P, typename S>
+struct BjacSmem {
+  using C = Cfg<P>;
+  static constexpr int EPAD = 2 * C::NN + 1;  // odd row: conflict-free row-lane reads
+  static constexpr int EDGE = 12 * C::Q * C::N + C::Q;
+  static constexpr size_t bytes() { return sizeof(S) * (static_cast<size_t>(C::EPB) * EPAD + EDGE); }
+};
+
 template <int P, int OUT, typename S = double>
 __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E,
                                                    const double* __restrict__ E_D, double wm, double dt, double eta,
                                                    void* __restrict__ out, float* __restrict__ out_scale) {
   using C = Cfg<P>;
+  using SM = BjacSmem<P, S>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG, Q = C::Q;
   __shared__ __align__(16) S s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
   __shared__ S s_piv[C::WARPS][C::EPW][2 * N + 2];
+  extern __shared__ __align__(16) unsigned char bjac_smem[];
+  S* s_E = reinterpret_cast<S*>(bjac_smem);     // [EPB][EPAD]: E^1_kk | E^2_kk rows of the block's elements
+  S* s_pe = s_E + C::EPB * SM::EPAD;            // U^t [n][q][N]
+  S* s_pth = s_pe + 3 * Q * N;                  // V^t [n][np][q][N]
+  S* s_we = s_pth + 9 * Q * N;                  // [Q]
+  const long Kp = m.Kp;
+  const int kb = blockIdx.x * C::EPB;
   for (int t = threadIdx.x; t < 14 * NNP; t += blockDim.x) s_tab[t] = static_cast<S>(T.base[T.tmH + t]);
+  for (int t = threadIdx.x; t < 3 * Q * N; t += blockDim.x) s_pe[t] = static_cast<S>(T.base[T.pe + t]);
+  for (int t = threadIdx.x; t < 9 * Q * N; t += blockDim.x) s_pth[t] = static_cast<S>(T.base[T.pth + t]);
+  for (int t = threadIdx.x; t < Q; t += blockDim.x) s_we[t] = static_cast<S>(T.base[T.we + t]);
+  for (int t = threadIdx.x; t < 2 * NN * C::EPB; t += blockDim.x) {
+    const int v = t / C::EPB, e = t % C::EPB, ke = kb + e;
+    s_E[e * SM::EPAD + v] = ke < m.K ? static_cast<S>(E[static_cast<long>(v) * Kp + ke]) : S(0);
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / NG, i = lane % NG;
-  const int k = (blockIdx.x * C::WARPS + warp) * C::EPW + sub;
+  const int el = warp * C::EPW + sub;
+  const int k = kb + el;
   const bool live = k < m.K;
   const bool row = live && i < N;
   const int kk = live ? k : 0;
-  const long Kp = m.Kp;
   const double* g = m.geom;
   const double* tb = T.base;
+  const unsigned gmask = (NG == 32 ? 0xffffffffu : ((1u << NG) - 1u) << (NG * sub));  // this element's lanes
 
   // a[jj] = row i of P_k
   S a[N];
@@ -122,10 +153,11 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
       c1[t] = static_cast<S>(c1d[t]);
       c2[t] = static_cast<S>(c2d[t]);
     }
+    const S* erow = s_E + el * SM::EPAD + ir * N;
 #pragma unroll 1
     for (int q = 0; q < N; ++q) {
-      const S e1 = static_cast<S>(E[(static_cast<long>(ir) * N + q) * Kp + kk]);
-      const S e2 = static_cast<S>(E[(static_cast<long>(NN) + ir * N + q) * Kp + kk]);
+      const S e1 = erow[q];
+      const S e2 = erow[NN + q];
 #pragma unroll
       for (int t = 0; t < 5; ++t) {
         const S e = c1[t] * e1 + c2[t] * e2;
@@ -140,28 +172,32 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
 #pragma unroll 1
     for (int s = 1; s < 4; ++s) {
       const int j = m.nbr[(s - 1) * Kp + kk];
-      if (j < 0) continue;
+      if (j < 0) continue;  // uniform over the element's lanes
       const int n = s - 1, np = m.nbrn[n * Kp + kk];
       const double h = -dt * 0.5 * g[(kLen0 + np) * Kp + j] / (2.0 * g[kArea * Kp + j]);
       const double cx = h * g[(kNux0 + np) * Kp + j], cy = h * g[(kNuy0 + np) * Kp + j];
       const double hl = 0.5 * g[(kLen0 + n) * Kp + kk];
       const double kappa = hl * (cx * g[(kNux0 + n) * Kp + kk] + cy * g[(kNuy0 + n) * Kp + kk]);
-      const double* pth = tb + T.pth + (n * 3 + np) * Q * N;  // V^t [q][.]
-      const double* pe = tb + T.pe + n * Q * N;               // U^t [q][.]
+      const S* pth = s_pth + (n * 3 + np) * Q * N;  // V^t [q][.]
+      const S* pe = s_pe + n * Q * N;               // U^t [q][.]
+      // lane q < Q of the element: the neighbour's d_h at edge point q
+      S dq = 0;
+      if (i < Q) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) dq = fma(static_cast<S>(E_D[l * Kp + j]), pth[i * N + l], dq);
+      }
       S aq[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        double dv = 0.0;
-#pragma unroll
-        for (int l = 0; l < N; ++l) dv = fma(E_D[l * Kp + j], pth[q * N + l], dv);
-        aq[q] = static_cast<S>(kappa * pe[q * N + ir] * tb[T.we + q] * dv);
+        const S dv = __shfl_sync(gmask, dq, q, NG);
+        aq[q] = static_cast<S>(kappa) * pe[q * N + ir] * s_we[q] * dv;
       }
       const S* tab0 = s_tab + (5 + np * 3 + n) * NNP;
 #pragma unroll 1
       for (int q2 = 0; q2 < N; ++q2) {
         S e = 0;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) e = fma(aq[q], static_cast<S>(pth[q * N + q2]), e);
+        for (int q = 0; q < Q; ++q) e = fma(aq[q], pth[q * N + q2], e);
 #pragma unroll
         for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab0[jj * NP + q2], a[jj]);
       }
@@ -252,11 +288,22 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
               : out_kind == 1 ? static_cast<void*>(h.Pinv32.ptr)
                               : static_cast<void*>(h.Ph.ptr);
   float* sc = out_kind == 3 ? h.Pscale.ptr : nullptr;
-#define LAUNCH(P, O) \
-  k_bjac_warp<P, O><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, sc)
+#define LAUNCH(P, O)                                                                                          \
+  do {                                                                                                        \
+    const size_t smem = BjacSmem<P, double>::bytes(); /* + static: always opt in beyond 48 KB */             \
+    LDG_CUDA(cudaFuncSetAttribute(k_bjac_warp<P, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                                    static_cast<int>(smem)));                                                 \
+    k_bjac_warp<P, O><<<grid, 256, smem, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, \
+                                                      sc);                                                    \
+  } while (0)
 #define LAUNCH32(P, O)                                                                                        \
-  k_bjac_warp<P, O, float><<<grid, 256, 0, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, \
-                                                       sc)
+  do {                                                                                                        \
+    const size_t smem = BjacSmem<P, float>::bytes();                                                          \
+    LDG_CUDA(cudaFuncSetAttribute(k_bjac_warp<P, O, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                    static_cast<int>(smem)));                                                 \
+    k_bjac_warp<P, O, float><<<grid, 256, smem, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt,       \
+                                                             h.prob.eta, out, sc);                            \
+  } while (0)
 #define CALL(P)                                                      \
   do {                                                               \
     const unsigned grid = grid_of(h.K, Cfg<P>::EPB);                 \

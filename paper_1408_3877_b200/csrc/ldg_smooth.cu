@@ -399,37 +399,54 @@ __global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const TP* __restric
   for (int i = 0; i < N; ++i) out[i * Kp + k] = static_cast<double>(om * d[i]);
 }
 
-// Eq[c][q][k] from E[(c*4 + s)*NN + i*N + j][k] (FP64, row-major blocks);
-// one thread per output quad, zero in the padding columns
-// per-element scale of the FP16 copy: max |E| over the element's 2 diagonal blocks
+// FP16 packed copy of the diagonal blocks E[(c*NN + i*N + j)][k] (FP64),
+// one thread per element: pass 1 the element's scale max |E| over its two
+// blocks, pass 2 the quads of ldg_pack.cuh (slot v -> (i, j), zero padding)
+// as 8-byte stores, each pass a coalesced sweep over the 2 N^2 planes.
+// (Was two kernels, a per-element max and one thread per FP16 value with
+// 2-byte scattered stores: 68 + 264 us at p = 4, 256^2.)
 template <int P>
-__global__ void k_escale(long Kp, const double* __restrict__ E, float* __restrict__ scale) {
-  constexpr int NN = Cfg<P>::NN;
+__global__ void __launch_bounds__(128) k_pack_eh(long Kp, const double* __restrict__ E, float* __restrict__ scale,
+                                                 uint2* __restrict__ Eq) {
+  using C = Cfg<P>;
+  constexpr int N = C::N, NN = C::NN;
   const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
   if (k >= Kp) return;
   double mx = 0.0;
+#pragma unroll 8
   for (int v = 0; v < 2 * NN; ++v) mx = fmax(mx, fabs(E[v * Kp + k]));
-  scale[k] = mx > 0.0 ? static_cast<float>(mx) : 1.0f;
-}
-
-__device__ __forceinline__ void put_val(float4* q, int r, float v, float) { reinterpret_cast<float*>(q)[r] = v; }
-__device__ __forceinline__ void put_val(uint2* q, int r, float v, float inv) {
-  reinterpret_cast<__half*>(q)[r] = __float2half_rn(v * inv);
-}
-
-// packed copy of the diagonal blocks E[(c*NN + i*N + j)][k] (FP64), one thread
-// per value; the padding slots keep the zeros of the allocation
-template <int P, typename TQ>
-__global__ void k_pack_e(long Kp, const double* __restrict__ E, const float* __restrict__ scale, TQ* __restrict__ Eq) {
-  using C = Cfg<P>;
-  constexpr int N = C::N, NN = C::NN;
-  const long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-  if (t >= 2L * NN * Kp) return;
-  const long k = t % Kp;
-  const int rest = static_cast<int>(t / Kp), c = rest / NN, ij = rest % NN, i = ij / N, j = ij % N;
-  const int v = sm_packed_slot<P>(i, j);
-  put_val(Eq + (static_cast<long>(c) * C::QP + (v >> 2)) * Kp + k, v & 3, static_cast<float>(E[t]),
-          scale ? 1.0f / scale[k] : 1.0f);
+  const float sc = mx > 0.0 ? static_cast<float>(mx) : 1.0f;
+  scale[k] = sc;
+  const float inv = 1.0f / sc;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+#pragma unroll 4
+    for (int q = 0; q < C::QP; ++q) {
+      __half hv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int v = 4 * q + r;
+        int i, j;
+        bool ok;
+        if constexpr (C::kFlat) {
+          j = v / N;
+          i = v % N;
+          ok = v < NN;
+        } else {
+          const int g = v / (C::QC * 4), w = v % (C::QC * 4);
+          j = g * C::CC + w / N;
+          i = w % N;
+          ok = j < N;
+        }
+        const float val = ok ? static_cast<float>(E[(static_cast<long>(c) * NN + i * N + j) * Kp + k]) : 0.0f;
+        hv[r] = __float2half_rn(val * inv);
+      }
+      uint2 u;
+      u.x = static_cast<unsigned>(__half_as_ushort(hv[0])) | (static_cast<unsigned>(__half_as_ushort(hv[1])) << 16);
+      u.y = static_cast<unsigned>(__half_as_ushort(hv[2])) | (static_cast<unsigned>(__half_as_ushort(hv[3])) << 16);
+      Eq[(static_cast<long>(c) * C::QP + q) * Kp + k] = u;
+    }
+  }
 }
 
 template <int P>
@@ -464,10 +481,7 @@ void smooth_pack_e(Handle& h) {
       h.Eh.alloc(nq, &h.bytes);                                                                          \
       h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
     }                                                                                                    \
-    k_escale<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr);                  \
-    k_pack_e<P, uint2><<<grid_of(2L * Cfg<P>::NN * h.Kp, 256), 256, 0, h.stream>>>(h.Kp, h.E.ptr,         \
-                                                                                 h.Escale.ptr, h.Eh.ptr); \
-    h.launches += 1;                                                                                     \
+    k_pack_eh<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr, h.Eh.ptr);       \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
