@@ -342,6 +342,41 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1(DevMesh m, 
   tab_mv_store<N, NP>(tb.Minv(), u2, inv2a, tout + N * Kp, Kp, k);
 }
 
+// stage 1 of the Krylov operator, tout^m = tau M_k^-1 B^m x (no vz term):
+// the same products against the m_hat^-1-premultiplied tables (tmH | tmSd |
+// tmSo, the STab offsets of tH | tSd | tSo), so the result is a scale by
+// 1/(2|T_k|) instead of a trailing M^-1 product (225 scalar table loads and
+// FMAs per component at p = 4)
+template <int P>
+__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1m(DevMesh m, DevTables T,
+                                                                      const double* __restrict__ x, double tau,
+                                                                      double* __restrict__ tout, int k0, int k1) {
+  constexpr int N = Cfg<P>::N, NNP = N * Cfg<P>::NP;
+  extern __shared__ __align__(16) double sm[];
+  {
+    const double2* src = reinterpret_cast<const double2*>(T.base + T.tmH);
+    double2* dst = reinterpret_cast<double2*>(sm);
+    for (int i = threadIdx.x; i < 14 * NNP / 2; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
+  const STab<P> tb{sm};
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  double u1[N], u2[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) u1[i] = u2[i] = 0.0;
+  const EdgeData e = load_edges(m, k);
+  apply_B<P>(tb, m, e, k, g[kB11 * Kp + k], g[kB12 * Kp + k], g[kB21 * Kp + k], g[kB22 * Kp + k], x, u1, u2);
+  const double sc = tau / (2.0 * g[kArea * Kp + k]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    tout[i * Kp + k] = sc * u1[i];
+    tout[(N + i) * Kp + k] = sc * u2[i];
+  }
+}
+
 // stage 2: y = alpha M_k x_k + beta (S + S_D) x - gamma sum_m sum_s E^m[s] tz^m_col + delta w
 // (the Krylov operator, FP64): stored diagonal blocks streamed, off-diagonal
 // blocks matrix-free from D.
@@ -496,10 +531,17 @@ void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, d
     return rows_stage1(h, vz, sigma, x, tau, tout);
   }
   const unsigned grid = grid_of(k1 - k0, 128);
+  // the Krylov operator's stage 1 (x only): premultiplied tables, no trailing M^-1 product
 #define CALL(P)                                                                                               \
   do {                                                                                                        \
-    set_smem(k_stage1<P>, tab_smem<P>());                                                                     \
-    k_stage1<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, vz, sigma, x, tau, tout, k0, k1);   \
+    if (!vz && x) {                                                                                           \
+      const size_t sm14 = sizeof(double) * 14 * Cfg<P>::N * Cfg<P>::NP;                                       \
+      set_smem(k_stage1m<P>, sm14);                                                                           \
+      k_stage1m<P><<<grid, 128, sm14, h.stream>>>(h.mesh(), h.dtab, x, tau, tout, k0, k1);                    \
+    } else {                                                                                                  \
+      set_smem(k_stage1<P>, tab_smem<P>());                                                                   \
+      k_stage1<P><<<grid, 128, tab_smem<P>(), h.stream>>>(h.mesh(), h.dtab, vz, sigma, x, tau, tout, k0, k1); \
+    }                                                                                                         \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

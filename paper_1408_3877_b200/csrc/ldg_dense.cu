@@ -58,23 +58,45 @@ __global__ void k_identity(long n, double* __restrict__ a) {
     a[i] = (i % (n + 1) == 0) ? 1.0 : 0.0;
 }
 
-// y = alpha A x, A column-major n x n (n a multiple of 32): 32 rows per block,
-// the columns split over 8 warps, partial sums reduced in shared memory
+// y = alpha A x, A column-major n x n (n a multiple of 32): 32 rows x
+// n / kGemvSplit columns per block (the columns of a block split over its 8
+// warps, partial sums reduced in shared memory); the last block of a row
+// group to finish (arrival counter, reset by it for the next replay) adds the
+// kGemvSplit partials in a fixed order, so the result is deterministic.  The
+// inverse (1.2-2 MB) comes from HBM once per V-cycle: 12 blocks over all
+// columns streamed it at a few hundred GB/s, 12 x 8 blocks fill the GPU.
+constexpr int kGemvSplit = 8;
 __global__ void __launch_bounds__(256) k_dense_gemv(int n, const double* __restrict__ a, const double* x,
-                                                    double alpha, double* y) {
+                                                    double alpha, double* y, double* part_g, int* arrivals) {
   __shared__ double part[8][33];
+  __shared__ bool last;
   pdl_wait();
   pdl_trigger();
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   const int row = blockIdx.x * 32 + lx;
+  const int c0 = blockIdx.y * (n / kGemvSplit), c1 = blockIdx.y + 1 == kGemvSplit ? n : c0 + n / kGemvSplit;
   double s = 0.0;
-  for (int c = ly; c < n; c += 8) s = fma(a[static_cast<long>(c) * n + row], x[c], s);
+  for (int c = c0 + ly; c < c1; c += 8) s = fma(a[static_cast<long>(c) * n + row], x[c], s);
   part[ly][lx] = s;
   __syncthreads();
   if (ly == 0) {
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += part[w][lx];
+    part_g[static_cast<long>(blockIdx.y) * n + row] = t;
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int done = atomicAdd(arrivals + blockIdx.x, 1);
+    last = done == kGemvSplit - 1;
+    if (last) arrivals[blockIdx.x] = 0;
+  }
+  __syncthreads();
+  if (last && ly == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (int b = 0; b < kGemvSplit; ++b) t += __ldcg(part_g + static_cast<long>(b) * n + row);
     y[row] = alpha * t;
   }
 }
@@ -177,6 +199,8 @@ void dense_alloc(Handle& L) {
   LDG_CUSOLVER(cusolverDnDgetrf_bufferSize(s, L.dn_n, L.dn_n, L.dn_A.ptr, L.dn_n, &lwork));
   L.dn_work.alloc(static_cast<size_t>(lwork > 0 ? lwork : 1), &L.bytes);
   L.dn_T2.alloc(n * n, &L.bytes);
+  L.dn_part.alloc(kGemvSplit * n, &L.bytes);
+  L.dn_cnt.alloc(n / 32, &L.bytes);  // zeroed: arrival counters of k_dense_gemv
   L.dn_X2.alloc(n * n, &L.bytes);
   L.dn_res.alloc(1, &L.bytes);
   cublasHandle_t b = nullptr;
@@ -250,8 +274,8 @@ void dense_setup(Handle& L, double wm, double dt, bool f32) {
 
 // x = S_c^-1 b = -(B^-1) b on the dense level
 void dense_solve(Handle& L, const double* b, double* x) {
-  launch_pdl(k_dense_gemv, dim3(L.dn_n / 32), dim3(256), 0, L.stream, L.dn_n,
-             static_cast<const double*>(L.dn_inv.ptr), b, -1.0, x);
+  launch_pdl(k_dense_gemv, dim3(L.dn_n / 32, kGemvSplit), dim3(256), 0, L.stream, L.dn_n,
+             static_cast<const double*>(L.dn_inv.ptr), b, -1.0, x, L.dn_part.ptr, L.dn_cnt.ptr);
   LDG_CUDA(cudaGetLastError());
   ++L.launches;
 }

@@ -180,7 +180,8 @@ struct Handle {
   int replica_level = 0;                         // the strip level it replaces (0: none)
   int dn_n = 0;
   DBuf<double> dn_A, dn_inv, dn_X, dn_T, dn_zero, dn_work, dn_T2, dn_X2, dn_res;
-  DBuf<int> dn_ipiv, dn_info;
+  DBuf<int> dn_ipiv, dn_info, dn_cnt;
+  DBuf<double> dn_part;                          // GEMV partial sums (deterministic split reduction)
   void* dn_solver = nullptr;                     // cusolverDnHandle_t
   void* dn_blas = nullptr;                       // cublasHandle_t (Newton-Schulz refinement)
   double* dn_res_host = nullptr;                 // pinned: last Newton-Schulz residual

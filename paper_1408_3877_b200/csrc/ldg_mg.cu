@@ -218,7 +218,12 @@ int mg_depth(int dim, int size) {
 // the embedding of a lower-degree space is the identity on its first N
 // coefficients: restriction truncates, prolongation pads with zeros.
 std::vector<int> mg_pcoarse_chain(int p) {
-  return p >= 4 ? std::vector<int>{2} : (p >= 2 ? std::vector<int>{1} : std::vector<int>{});
+  static const bool two_steps = [] {  // LDG_MG_PC4=21: p = 4 -> 2 -> 1 (A/B runs)
+    const char* e = std::getenv("LDG_MG_PC4");
+    return e && std::atoi(e) == 21;
+  }();
+  if (p >= 4) return two_steps ? std::vector<int>{2, 1} : std::vector<int>{2};
+  return p >= 2 ? std::vector<int>{1} : std::vector<int>{};
 }
 
 namespace {

@@ -132,3 +132,23 @@ def test_strip_plan_covers_mesh():
         assert np.all(seen == 1)
     assert strips.mg_depth(256, 1) == 7 and strips.mg_depth(32, 4) == 3 and strips.mg_depth(384, 2) == 6
     assert strips.weak_dim(256, 1) == 256 and strips.weak_dim(256, 2) == 384 and strips.weak_dim(256, 8) == 768
+
+
+def test_scaling_dims():
+    """bench.py's multi-GPU sizes (SURVEY.md §8d): strong = the workload's
+    mesh on every rank count; weak = its elements per GPU, C5 anchored at
+    8 GPUs (dim = 4096 sqrt(P/8) -> 1448, 2048, 2896, 4096, rounded up to
+    32-column strips so every rank keeps the multigrid depth)."""
+    from paper_1408_3877_b200 import strips
+
+    assert [strips.scaled_dim(4096, p, "strong") for p in (1, 2, 4, 8)] == [4096] * 4
+    weak = [strips.scaled_dim(4096, p, "weak", anchor=8) for p in (1, 2, 4, 8)]
+    assert weak == [1472, 2048, 2944, 4096]
+    for p, d in zip((1, 2, 4, 8), weak):
+        assert d % (32 * p) == 0 and abs(d * d / p - 4096 ** 2 / 8) / (4096 ** 2 / 8) < 0.1
+        assert strips.mg_depth(d, p) >= 5
+    assert [strips.scaled_dim(256, p) for p in (1, 2, 4, 8)] == [strips.weak_dim(256, p) for p in (1, 2, 4, 8)]
+    import pytest
+
+    with pytest.raises(ValueError):
+        strips.scaled_dim(100, 3, "strong")
