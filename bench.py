@@ -659,8 +659,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--p", default=None, help="comma-separated degrees (overrides the workload's sweep)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = fixed elements per GPU (the workload's anchor size), strong = fixed mesh")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: weak = fixed elements per GPU (the workload's anchor size), strong = fixed mesh "
+                         "(default: strong for C4/C5, whose meshes are quoted for the whole job, weak otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi sampler (diagnostics only)")
     ap.add_argument("--krylov", type=int, default=None, help="0 FGMRES (default), 1 BiCGStab")
@@ -669,6 +670,8 @@ def main():
     ap.add_argument("--ref-cap", type=float, default=900.0, help="reference arm: wall-clock cap in seconds")
     ap.add_argument("--ref-worker", type=int, default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "strong" if args.workload in WEAK_ANCHOR else "weak"
     if args.ref_worker is not None:
         dim, _, dt, jitter, boundary, _ = WORKLOADS[args.workload]
         ref_worker(args.ref_worker, dim, dt, args.steps, jitter, boundary)

@@ -65,6 +65,30 @@ inline unsigned grid_of(long n, int block) { return static_cast<unsigned>((n + b
 // was L1-bound at 1.44 ms for 518 MB).  The edge tables sit in shared memory
 // too, and the neighbour's d_h at the edge points (Q dot products of length
 // N) is computed once per element instead of once per row-lane.
+// a[jj] += e * row[jj], jj < N, row 16-byte aligned in shared memory
+template <typename S, int N, int NJ>
+__device__ __forceinline__ void row_fma(const S* row, S e, S* a) {
+  if constexpr (sizeof(S) == 4) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll
+    for (int q = 0; q < NJ / 4; ++q) {
+      const float4 v = r4[q];
+      if (4 * q < N) a[4 * q] = fmaf(e, v.x, a[4 * q]);
+      if (4 * q + 1 < N) a[4 * q + 1] = fmaf(e, v.y, a[4 * q + 1]);
+      if (4 * q + 2 < N) a[4 * q + 2] = fmaf(e, v.z, a[4 * q + 2]);
+      if (4 * q + 3 < N) a[4 * q + 3] = fmaf(e, v.w, a[4 * q + 3]);
+    }
+  } else {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+    for (int q = 0; q < NJ / 2; ++q) {
+      const double2 v = r2[q];
+      if (2 * q < N) a[2 * q] = fma(e, v.x, a[2 * q]);
+      if (2 * q + 1 < N) a[2 * q + 1] = fma(e, v.y, a[2 * q + 1]);
+    }
+  }
+}
+
 template <int P, typename S>
 struct BjacSmem {
   using C = Cfg<P>;
@@ -80,7 +104,11 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
   using C = Cfg<P>;
   using SM = BjacSmem<P, S>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG, Q = C::Q;
-  __shared__ __align__(16) S s_tab[14 * NNP];  // tmH 2 | tmSd 3 | tmSo 9 (contiguous in the table buffer)
+  // tmH 2 | tmSd 3 | tmSo 9 transposed to [t][q][jj] rows of NJ (vector loads
+  // over jj: one 128-bit broadcast load per 4 (FP32) / 2 (FP64) FMAs instead
+  // of a scalar load per FMA -- the kernel was issue-bound on them)
+  constexpr int VW = 16 / sizeof(S), NJ = (N + VW - 1) / VW * VW, TJ = N * NJ;
+  __shared__ __align__(16) S s_tab[14 * TJ];
   __shared__ S s_piv[C::WARPS][C::EPW][2 * N + 2];
   extern __shared__ __align__(16) unsigned char bjac_smem[];
   S* s_E = reinterpret_cast<S*>(bjac_smem);     // [EPB][EPAD]: E^1_kk | E^2_kk rows of the block's elements
@@ -89,7 +117,10 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
   S* s_we = s_pth + 9 * Q * N;                  // [Q]
   const long Kp = m.Kp;
   const int kb = blockIdx.x * C::EPB;
-  for (int t = threadIdx.x; t < 14 * NNP; t += blockDim.x) s_tab[t] = static_cast<S>(T.base[T.tmH + t]);
+  for (int x = threadIdx.x; x < 14 * TJ; x += blockDim.x) {
+    const int t = x / TJ, q = (x % TJ) / NJ, jj = x % NJ;  // Tab_t[q][jj] = stored transpose [jj][q]
+    s_tab[x] = jj < N ? static_cast<S>(T.base[T.tmH + t * NNP + jj * NP + q]) : S(0);
+  }
   for (int t = threadIdx.x; t < 3 * Q * N; t += blockDim.x) s_pe[t] = static_cast<S>(T.base[T.pe + t]);
   for (int t = threadIdx.x; t < 9 * Q * N; t += blockDim.x) s_pth[t] = static_cast<S>(T.base[T.pth + t]);
   for (int t = threadIdx.x; t < Q; t += blockDim.x) s_we[t] = static_cast<S>(T.base[T.we + t]);
@@ -161,9 +192,7 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
 #pragma unroll
       for (int t = 0; t < 5; ++t) {
         const S e = c1[t] * e1 + c2[t] * e2;
-        const S* tab = s_tab + t * NNP + q;
-#pragma unroll
-        for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab[jj * NP], a[jj]);
+        row_fma<S, N, NJ>(s_tab + t * TJ + q * NJ, e, a);
       }
     }
     // off-diagonal slots: E^m_{k,j} against M_j^-1 B^m_{j,k} = (nu^m_j |E_j| / (4 |T_j|)) s_off(np, n).
@@ -192,14 +221,13 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
         const S dv = __shfl_sync(gmask, dq, q, NG);
         aq[q] = static_cast<S>(kappa) * pe[q * N + ir] * s_we[q] * dv;
       }
-      const S* tab0 = s_tab + (5 + np * 3 + n) * NNP;
+      const S* tab0 = s_tab + (5 + np * 3 + n) * TJ;
 #pragma unroll 1
       for (int q2 = 0; q2 < N; ++q2) {
         S e = 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q) e = fma(aq[q], pth[q * N + q2], e);
-#pragma unroll
-        for (int jj = 0; jj < N; ++jj) a[jj] = fma(e, tab0[jj * NP + q2], a[jj]);
+        row_fma<S, N, NJ>(tab0 + q2 * NJ, e, a);
       }
     }
   }

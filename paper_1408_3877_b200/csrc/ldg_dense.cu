@@ -52,6 +52,17 @@ __global__ void k_ns_residual(long n, const double* __restrict__ t, double* out)
     atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
+// B[u][u] = 1 for the unknowns of padding elements (u = i Kp + k, k >= K):
+// their columns and rows are otherwise zero
+__global__ void k_pad_identity(int N, int K, long Kp, double* __restrict__ a) {
+  const long n = N * Kp;
+  for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < N * (Kp - K);
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long u = (t / (Kp - K)) * Kp + K + t % (Kp - K);
+    a[u * n + u] = 1.0;
+  }
+}
+
 __global__ void k_identity(long n, double* __restrict__ a) {
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n * n;
        i += static_cast<long>(gridDim.x) * blockDim.x)
@@ -164,9 +175,8 @@ long dense_max() {
 // 7.6 / 8.0 / 7.6; ms per step 4.67 / 4.73 / 6.62 / 11.25 -> 3.94 / 4.13 /
 // 6.11 / 10.13).
 bool dense_candidate(const Handle& L) {
-  const long n = static_cast<long>(L.N) * L.K;
-  return L.dim > 0 && !L.mg_pcoarse && L.size == 1 && L.p <= 1 && L.K == L.Kp && L.K % 32 == 0 &&
-         n <= dense_max();
+  const long n = static_cast<long>(L.N) * L.Kp;  // padding elements carry identity rows
+  return !L.mg_pcoarse && L.size == 1 && L.p <= 1 && n <= dense_max();
 }
 
 // Strip teams: the coarsest level of a truncated strip hierarchy (every
@@ -183,7 +193,7 @@ bool replica_candidate(const Handle& C) {
 }
 
 void dense_alloc(Handle& L) {
-  const long n = static_cast<long>(L.N) * L.K;
+  const long n = static_cast<long>(L.N) * L.Kp;
   L.dn_n = static_cast<int>(n);
   L.dn_A.alloc(n * n, &L.bytes);
   L.dn_inv.alloc(n * n, &L.bytes);
@@ -233,6 +243,11 @@ void dense_setup(Handle& L, double wm, double dt, bool f32) {
     launch_to_f32(L, nn, L.E.ptr, L.E32.ptr);
   }
   small_dense_columns(L, L.dn_X.ptr, L.dn_T.ptr, L.dn_zero.ptr, wm, dt, L.dn_A.ptr, n);
+  if (L.Kp > L.K) {
+    k_pad_identity<<<32, 256, 0, L.stream>>>(L.N, L.K, L.Kp, L.dn_A.ptr);
+    LDG_CUDA(cudaGetLastError());
+    ++L.launches;
+  }
   const size_t bytes = sizeof(double) * n * n;
   // the previous step's Newton-Schulz residual (its pinned copy completed
   // with that step) decides between refinement and a fresh factorisation

@@ -103,6 +103,10 @@ struct Handle {
   DBuf<double> geom;     // kGeomCount * Kp
   DBuf<int> nbr, nbrn, kind, bid;  // 3 * Kp
   std::vector<int> gid;  // local -> global element id
+  // host lists of a general mesh (ldg_create): the red-refinement hierarchy
+  // of the multigrid is detected from them (ldg_mg.cu mg_build_general)
+  std::vector<double> host_xy;
+  std::vector<int> host_v0t, host_ids;
 
   // per-step operators / vectors
   DBuf<double> D, F;     // N * Kp

@@ -423,6 +423,12 @@ void build_general_mesh(Handle& h, const double* coords, int nv, const int* v0t,
   }
   h.gid.resize(nt);
   for (int k = 0; k < nt; ++k) h.gid[k] = k;
+  h.host_xy.assign(coords, coords + 2L * nv);
+  h.host_v0t.assign(v0t, v0t + 3L * nt);
+  if (id_e0t)
+    h.host_ids.assign(id_e0t, id_e0t + 3L * nt);
+  else
+    h.host_ids.clear();
   topology_and_geometry(h, bbox, ids.ptr);
   ids.release(nullptr);
 }

@@ -15,6 +15,7 @@
 // coarsest level (dim 2) gets two smoothing sweeps.  Prototyped in numpy
 // against the oracle first: 12-27 BiCGStab iterations for p = 1..4
 // independent of h, against 170-2100 with block-Jacobi alone.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -259,8 +260,139 @@ std::unique_ptr<Handle> coarse_shell(const Handle& h, const Handle& fine) {
 
 }  // namespace
 
+// The coarse mesh of a red refinement (refine_uniform, mesh.hpp:258-293):
+// parent c's children are 4c..4c+3 = (a1, m3, m2), (m3, a2, m1), (m2, m1,
+// a3), (m3, m1, m2) with m_n the midpoint of the edge opposite a_n, the
+// parent's vertices numbered before every midpoint, and a parent edge's
+// boundary ID on its child edges.  False when the mesh is not one.
+bool coarsen_red(const std::vector<double>& xy, const std::vector<int>& t, const std::vector<int>& ids, int K,
+                 std::vector<double>* cxy, std::vector<int>* ct, std::vector<int>* cids) {
+  if (K < 4 || K % 4 != 0) return false;
+  const int Kc = K / 4;
+  ct->assign(3L * Kc, 0);
+  int amax = -1, mmin = 1 << 30;
+  double scale = 0.0;
+  for (double v : xy) scale = std::max(scale, std::fabs(v));
+  const double tol = 1e-12 * std::max(scale, 1.0);
+  auto mid_ok = [&](int m, int a, int b) {
+    return std::fabs(xy[2 * m] - 0.5 * (xy[2 * a] + xy[2 * b])) <= tol &&
+           std::fabs(xy[2 * m + 1] - 0.5 * (xy[2 * a + 1] + xy[2 * b + 1])) <= tol;
+  };
+  for (int c = 0; c < Kc; ++c) {
+    const int* t0 = &t[3L * (4 * c)];
+    const int* t1 = t0 + 3;
+    const int* t2 = t0 + 6;
+    const int* t3 = t0 + 9;
+    const int a1 = t0[0], m3 = t0[1], m2 = t0[2], a2 = t1[1], m1 = t1[2], a3 = t2[2];
+    if (t1[0] != m3 || t2[0] != m2 || t2[1] != m1 || t3[0] != m3 || t3[1] != m1 || t3[2] != m2) return false;
+    if (!mid_ok(m1, a2, a3) || !mid_ok(m2, a3, a1) || !mid_ok(m3, a1, a2)) return false;
+    (*ct)[3 * c] = a1;
+    (*ct)[3 * c + 1] = a2;
+    (*ct)[3 * c + 2] = a3;
+    amax = std::max({amax, a1, a2, a3});
+    mmin = std::min({mmin, m1, m2, m3});
+  }
+  if (mmin <= amax) return false;  // parent vertices first, then the midpoints
+  cxy->assign(xy.begin(), xy.begin() + 2L * (amax + 1));
+  cids->clear();
+  if (!ids.empty()) {
+    cids->assign(3L * Kc, 0);
+    for (int c = 0; c < Kc; ++c) {
+      (*cids)[3 * c] = ids[3L * (4 * c + 1)];         // edge a2-a3: child (m3, a2, m1), edge 0
+      (*cids)[3 * c + 1] = ids[3L * (4 * c + 2) + 1];  // edge a3-a1: child (m2, m1, a3), edge 1
+      (*cids)[3 * c + 2] = ids[3L * (4 * c) + 2];      // edge a1-a2: child (a1, m3, m2), edge 2
+    }
+  }
+  return true;
+}
+
+// General meshes (ldg_create, one rank): the p-coarsened levels on the same
+// mesh, then h-levels while the mesh is a red refinement of a coarser one
+// (the reference's convergence ladder is domain_square refined by
+// refine_uniform), then the dense coarsest level when small enough.  Without
+// a red-refinement hierarchy there is no multigrid (block-Jacobi).
+bool mg_build_general(Handle& h) {
+  std::vector<double> xy = h.host_xy, cxy;
+  std::vector<int> t = h.host_v0t, ids = h.host_ids, ct, cids;
+  std::vector<std::vector<double>> lxy;
+  std::vector<std::vector<int>> lt, lids;
+  int K = h.K;
+  while (lt.size() < 12 && coarsen_red(xy, t, ids, K, &cxy, &ct, &cids)) {
+    lxy.push_back(cxy);
+    lt.push_back(ct);
+    lids.push_back(cids);
+    xy.swap(cxy);
+    t.swap(ct);
+    ids.swap(cids);
+    K /= 4;
+  }
+  if (lt.empty()) return false;
+  h.mg_r.alloc(h.vec_len(), &h.bytes);
+  h.mg_s.alloc(h.vec_len(), &h.bytes);
+  Handle* fine = &h;
+  for (const int pc : mg_pcoarse_chain(h.p)) {  // the same mesh at degree pc
+    auto c = std::make_unique<Handle>();
+    c->p = pc;
+    c->N = dofs_of(pc);
+    c->prob = h.prob;
+    c->stream = h.stream;
+    c->owns_stream = false;
+    c->rank = h.rank;
+    c->size = h.size;
+    init_handle_tables(*c, pc);
+    build_general_mesh(*c, h.host_xy.data(), static_cast<int>(h.host_xy.size() / 2), h.host_v0t.data(), h.K,
+                       h.host_ids.empty() ? nullptr : h.host_ids.data());
+    alloc_coarse(*c);
+    c->mg_pcoarse = true;
+    fine = c.get();
+    h.coarse.push_back(std::move(c));
+  }
+  for (size_t l = 0; l < lt.size(); ++l) {
+    auto c = coarse_shell(h, *fine);
+    const int Kc = static_cast<int>(lt[l].size() / 3);
+    build_general_mesh(*c, lxy[l].data(), static_cast<int>(lxy[l].size() / 2), lt[l].data(), Kc,
+                       lids[l].empty() ? nullptr : lids[l].data());
+    alloc_coarse(*c);
+    const long NN = static_cast<long>(c->N) * c->N;
+    // parent f / 4, slot f % 4 (refine_uniform's child order)
+    std::vector<int> parent(fine->Kp, 0), slot(fine->Kp, 0), children(4L * c->Kp, 0);
+    for (int f = 0; f < fine->K; ++f) {
+      parent[f] = f / 4;
+      slot[f] = f % 4;
+      children[static_cast<long>(f % 4) * c->Kp + f / 4] = f;
+    }
+    c->mg_children.alloc(4 * c->Kp, &c->bytes);
+    fine->mg_parent.alloc(fine->Kp, &fine->bytes);
+    DBuf<int> slots;
+    slots.alloc(fine->Kp, nullptr);
+    LDG_CUDA(cudaMemcpy(c->mg_children.ptr, children.data(), sizeof(int) * children.size(), cudaMemcpyHostToDevice));
+    LDG_CUDA(cudaMemcpy(fine->mg_parent.ptr, parent.data(), sizeof(int) * parent.size(), cudaMemcpyHostToDevice));
+    LDG_CUDA(cudaMemcpy(slots.ptr, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice));
+    c->mg_P.alloc(4 * NN * c->Kp, &c->bytes);
+#define CALL(PP)                                                                                              \
+  k_prolong_blocks<PP><<<grid_of(fine->K, 128), 128, 0, h.stream>>>(fine->mesh(), c->mesh(), fine->dtab,     \
+                                                                   fine->mg_parent.ptr, slots.ptr, c->mg_P.ptr)
+    LDG_DISPATCH_P(fine->p, CALL)
+#undef CALL
+    LDG_CUDA(cudaGetLastError());
+    LDG_CUDA(cudaStreamSynchronize(h.stream));
+    fine = c.get();
+    h.coarse.push_back(std::move(c));
+  }
+  for (size_t i = 0; i < h.coarse.size(); ++i) {
+    Handle& c = *h.coarse[i];
+    if (!dense_candidate(c)) continue;
+    dense_alloc(c);
+    h.dense_level = static_cast<int>(i) + 1;
+    break;
+  }
+  h.mg_ready = true;
+  return true;
+}
+
 bool mg_build(Handle& h, int team_size) {
   if (h.mg_ready) return true;
+  if (h.dim == 0 && team_size == 1 && !h.host_v0t.empty()) return mg_build_general(h);
   if (h.dim < 4 || h.dim_fine == 0) return false;
   const int depth = mg_depth(h.dim, team_size);
   if (depth < 1) return false;

@@ -626,7 +626,9 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
   const bool coarsest = l == levels(T) - 1;
   // the coarsest level is 2x2 on one rank; strips stop coarsening earlier
   // (every rank keeps a column), so a larger coarsest grid gets more sweeps
-  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * level_of(T.h0(), l).dim) - 1 : (pre_of(T.h0().p, l) - 1) + post_of(T.h0().p, l);
+  const Handle& Ll = level_of(T.h0(), l);
+  const int ldim = Ll.dim > 0 ? Ll.dim : static_cast<int>(std::sqrt(0.5 * Ll.K));  // general meshes: ~sqrt(K/2)
+  const int sweeps = coarsest ? std::max(kCoarseSweeps, 2 * ldim) - 1 : (pre_of(T.h0().p, l) - 1) + post_of(T.h0().p, l);
   if (fused(T, l, f32) && cheb_level(T, l) && !coarsest) {
     Cheb ch(level_of(T.h0(), l).cheb_lmax);
     double a, be;

@@ -1,8 +1,8 @@
 #!/bin/bash
-# Copy the round-end evidence from gpurun_out/final (scripts/gpu_final_profiles.sh)
-# into profiles/ under the round prefix ($1, default r01).
-R=${1:-r01}
-F=gpurun_out/final
+# Copy the round-end evidence from gpurun_out/<dir> (scripts/gpu_final_profiles.sh <dir>)
+# into profiles/ under the round prefix: bash scripts/collect_profiles.sh r02 gpurun_out/r02_ev1
+R=${1:-r02}
+F=${2:-gpurun_out/final}
 P=profiles
 set -e
 for w in c2 ref_c2 c1 c3 c4 c5; do
@@ -18,9 +18,15 @@ for p in 4 2; do
     cp $F/plain_p$p.log $P/${R}_launches_final_p${p}_step.log
   fi
 done
-if [ -f $F/full_p4.ncu-rep ]; then
-  python scripts/ncu_traffic.py $F/full_p4.ncu-rep $P/${R}_ncu_traffic.json 4 256 > $P/${R}_ncu_full_p4_traffic.txt
-  python scripts/ncu_table.py $F/full_p4.ncu-rep > $P/${R}_ncu_full_p4_table.txt
-  ncu -i $F/full_p4.ncu-rep --page details --print-summary per-kernel > $P/${R}_ncu_full_p4_details.txt 2>/dev/null || true
+N=$F
+[ -f $F/ncu/full_p4.ncu-rep ] && N=$F/ncu
+if [ -f $N/full_p4.ncu-rep ]; then
+  python scripts/ncu_traffic.py $N/full_p4.ncu-rep $P/${R}_ncu_traffic.json 4 256 > $P/${R}_ncu_full_p4_traffic.txt
+  python scripts/ncu_table.py $N/full_p4.ncu-rep > $P/${R}_ncu_full_p4_table.txt
+  ncu -i $N/full_p4.ncu-rep --page details --print-summary per-kernel > $P/${R}_ncu_full_p4_details.txt 2>/dev/null || true
+fi
+if [ -f $N/full_p2.ncu-rep ]; then
+  python scripts/ncu_table.py $N/full_p2.ncu-rep > $P/${R}_ncu_full_p2_table.txt
+  ncu -i $N/full_p2.ncu-rep --page details --print-summary per-kernel > $P/${R}_ncu_full_p2_details.txt 2>/dev/null || true
 fi
 ls -la $P | tail -30

@@ -271,3 +271,35 @@ def test_extrapolated_start_host_loop_matches_device_loop(ld):
     ref.euler_steps(dt, 1)
     yr, _ = ref.get_state()
     assert np.linalg.norm(yout - yr) / np.linalg.norm(yr) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_general_mesh_red_refinement_multigrid(p, ld):
+    """A mesh handed over as lists (ldg_create) that is the reference's
+    convergence ladder -- domain_square(1/3) refined four times by
+    refine_uniform (mesh.hpp:258-293), K = 4608 -- gets the multigrid
+    preconditioner: its red-refinement hierarchy is detected from the lists
+    (children 4c..4c+3, parent vertices first).  Same states as block-Jacobi
+    and as the oracle's exact solve, far fewer iterations."""
+    m = O.domain_square(1.0 / 3.0)
+    for _ in range(4):
+        m = O.refine_uniform(m)
+    spec = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
+                          boundary={1: "D", 2: "D", 3: "D", 4: "D"})
+    res = {}
+    for pc in (1, 2):
+        s = ld.LdgSystem.from_mesh(m.coord_v, m.v0t.astype(np.int32), p, spec, id_e0t=m.id_e0t.astype(np.int32))
+        s.initial_state()
+        st = s.euler_steps(0.05, 2, ld.SolverOptions(rtol=1e-13, precond=pc, maxit=20000))
+        assert st["residual"] <= 1e-10
+        res[pc] = (s.get_state()[0], st["iterations"])
+        s.close()
+    (y1, it1), (y2, it2) = res[1], res[2]
+    assert np.linalg.norm(y2 - y1) / np.linalg.norm(y1) <= 1e-9
+    assert it2 * 5 < it1, (it1, it2)
+    osys = O.LdgSystem(m, O.ProblemSpec(**BASE, eta=1.0, boundary=ALL_D), O.build_ref_tensors((p + 1) * (p + 2) // 2))
+    y, t = osys.initial_state()
+    for _ in range(2):
+        y, t = osys.euler_step_schur(y, t, 0.05)
+    assert np.linalg.norm(y2 - y) / np.linalg.norm(y) <= STATE_TOL
+    print(f"p={p}: block-Jacobi {it1} iterations, red-refinement multigrid {it2}")
