@@ -219,11 +219,24 @@ int mg_depth(int dim, int size) {
 // the embedding of a lower-degree space is the identity on its first N
 // coefficients: restriction truncates, prolongation pads with zeros.
 std::vector<int> mg_pcoarse_chain(int p) {
-  static const bool two_steps = [] {  // LDG_MG_PC4=21: p = 4 -> 2 -> 1 (A/B runs)
-    const char* e = std::getenv("LDG_MG_PC4");
-    return e && std::atoi(e) == 21;
-  }();
-  if (p >= 4) return two_steps ? std::vector<int>{2, 1} : std::vector<int>{2};
+  // A/B runs: LDG_MG_PC<p>="2,1" overrides the chain of degree p
+  char name[16];
+  snprintf(name, sizeof(name), "LDG_MG_PC%d", p);
+  if (const char* e = std::getenv(name)) {
+    std::vector<int> chain;
+    int last = p;
+    for (const char* q = e; *q;) {
+      char* end = nullptr;
+      const long v = std::strtol(q, &end, 10);
+      if (end == q) break;
+      if (v >= 0 && v < last) chain.push_back(static_cast<int>(last = static_cast<int>(v)));
+      q = *end == ',' ? end + 1 : end;
+    }
+    return chain;
+  }
+  // p = 4: 4 -> 2 -> 1 (with the dense degree-1 coarsest level: 23.0 ->
+  // 19.8 ms per step, 9.6 -> 8.4 iterations on C2 against 4 -> 2)
+  if (p >= 4) return {2, 1};
   return p >= 2 ? std::vector<int>{1} : std::vector<int>{};
 }
 
