@@ -124,9 +124,22 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
   for (int t = threadIdx.x; t < 3 * Q * N; t += blockDim.x) s_pe[t] = static_cast<S>(T.base[T.pe + t]);
   for (int t = threadIdx.x; t < 9 * Q * N; t += blockDim.x) s_pth[t] = static_cast<S>(T.base[T.pth + t]);
   for (int t = threadIdx.x; t < Q; t += blockDim.x) s_we[t] = static_cast<S>(T.base[T.we + t]);
-  for (int t = threadIdx.x; t < 2 * NN * C::EPB; t += blockDim.x) {
-    const int v = t / C::EPB, e = t % C::EPB, ke = kb + e;
-    s_E[e * SM::EPAD + v] = ke < m.K ? static_cast<S>(E[static_cast<long>(v) * Kp + ke]) : S(0);
+  {
+    // 8 loads in flight per thread (a rolled loop issued them one latency at a time)
+    constexpr int TOT = 2 * NN * C::EPB, B = 8;
+    for (int t0 = threadIdx.x; t0 < TOT; t0 += B * 256) {
+      double vals[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int t = t0 + b * 256, v = t / C::EPB, e = t % C::EPB, ke = kb + e;
+        vals[b] = (t < TOT && ke < m.K) ? __ldg(E + static_cast<long>(v) * Kp + ke) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int t = t0 + b * 256, v = t / C::EPB, e = t % C::EPB;
+        if (t < TOT) s_E[e * SM::EPAD + v] = static_cast<S>(vals[b]);
+      }
+    }
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

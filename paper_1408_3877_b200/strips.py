@@ -90,5 +90,7 @@ def scaled_dim(base_dim: int, size: int, scaling: str = "weak", anchor: int = 1)
         return base_dim
     if scaling != "weak":
         raise ValueError(f"unknown scaling {scaling!r}")
+    if size == anchor:
+        return base_dim
     unit = 32 * size
     return int(math.ceil(base_dim * math.sqrt(size / anchor) / unit - 1e-9)) * unit
