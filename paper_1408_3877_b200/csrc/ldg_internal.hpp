@@ -21,7 +21,7 @@ namespace ldgb {
 
 constexpr int kMaxRed = 80;        // dot products per reduction (FGMRES basis + 1)
 constexpr int kMaxLocalRanks = 16; // ranks of one process (virtual ranks share a GPU)
-constexpr int kExtrapMax = 4;      // history of the extrapolated Euler start (team_solve)
+constexpr int kExtrapMax = 7;      // history of the extrapolated Euler start (team_solve)
 
 // NVTX range over a scope (phases of a step in Nsight timelines; header-only
 // NVTX v3, a no-op unless a tool is attached)

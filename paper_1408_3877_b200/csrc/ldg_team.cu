@@ -437,10 +437,23 @@ bool setup_overlap() {
 // 0 = C^n, 1 = linear, ... 4 (LDG_EXTRAP for tuning runs).  Measured on the
 // 5-step C2 bench (ms per sweep step / FGMRES iterations at p = 4): C^n 81.4 /
 // 18.0, linear 71.7 / 15.8, quadratic 61.3 / 13.0, cubic 55.9 / 11.2, quartic
-// 52.0 / 10.2, quintic 51.7 / 10.0 (p = 0, 1 already worse than quartic).
-int extrap_order() {
-  static const int o = static_cast<int>(env_or("LDG_EXTRAP", 4));
-  return o < 0 ? 0 : (o > kExtrapMax ? kExtrapMax : o);
+// 52.0 / 10.2, quintic 51.7 / 10.0.
+// Per degree, from the 20-step C2 bench (the 5-step one has too little
+// history to tell; ms per step p = 0..4, order 4 / 5 / 6 / 7 / 8):
+//   p = 0  2.84 / 2.72 / 2.64 / 2.51 / 2.61
+//   p = 1  3.37 / 3.04 / 2.81 / 2.66 / 2.77
+//   p = 2  5.32 / 4.31 / 3.92 / 3.68 / 3.84
+//   p = 3  9.11 / 7.31 / 6.66 / 6.72 / 7.04
+//   p = 4 18.87 / 15.11 / 12.92 / 13.13 / 13.73
+// (sweep step 39.5 ms at order 4 -> 28.4 ms with the table).  The start only
+// changes the iteration count: every solve stops on the same relative
+// residual, and a poor extrapolation (non-smooth data) costs iterations, not
+// accuracy.
+constexpr int kExtrapP[5] = {7, 7, 7, 6, 6};
+int extrap_order(int p) {
+  static const int o = static_cast<int>(env_or("LDG_EXTRAP", -1));
+  const int v = o >= 0 ? o : kExtrapP[p < 0 ? 0 : (p > 4 ? 4 : p)];
+  return v > kExtrapMax ? kExtrapMax : v;
 }
 
 // The mixed-precision (f32) smoother runs every level through three
@@ -1323,7 +1336,7 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   const Handle& H0 = T.h0();
   const int order = wm != 0.0 && H0.hist_ok &&
                             std::fabs(H0.t - (H0.hist_time[0] + H0.hist_dt)) <= 1e-12 * std::max(1.0, std::fabs(H0.t))
-                        ? extrap_order()
+                        ? extrap_order(H0.p)
                         : 0;
   double w[kExtrapMax][kExtrapMax + 1] = {};
   {
@@ -1342,7 +1355,7 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   each(T, 0, [&](Handle& h) {
     const long n = h.vec_len();
     LDG_CUDA(cudaMemcpyAsync(h.Yold.ptr, h.Y.ptr, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, T.stream));
-    if (wm != 0.0 && extrap_order() > 0) {
+    if (wm != 0.0 && extrap_order(h.p) > 0) {
       if (!h.hist_dev.ptr) {
         for (auto& b : h.Chist) b.alloc(n, &h.bytes);
         h.hist_dev.alloc(2, &h.bytes);  // zeroed: no history
@@ -1406,7 +1419,7 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
     launch_lincomb3(h, n3, 1.0, h.full_y.ptr, -1.0, h.full_r.ptr, 0.0, nullptr, h.full_y.ptr);
   });
   const double res = std::sqrt(sq_norm3(T, kFullY)) / std::max(rhs_norm, 1.0);
-  if (wm != 0.0 && extrap_order() > 0) {  // C^n becomes the next step's C^{n-1}
+  if (wm != 0.0 && extrap_order(h0.p) > 0) {  // C^n becomes the next step's C^{n-1}
     each(T, 0, [&](Handle& h) {
       double* hv[kExtrapMax];
       for (int j = 0; j < kExtrapMax; ++j) hv[j] = h.Chist[j].ptr;
