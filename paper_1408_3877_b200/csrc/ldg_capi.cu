@@ -52,6 +52,12 @@ void init_handle_tables(Handle& h, int p) {
     h.dtab.fpe = F.fpe;
     h.dtab.fpth = F.fpth;
     h.dtab.fwe = F.fwe;
+    h.dtab.QF = F.QF;
+    h.dtab.fR = F.fR;
+    h.dtab.fpeT = F.fpeT;
+    h.dtab.fpthT = F.fpthT;
+    h.dtab.fweR = F.fweR;
+    h.dtab.fRend = F.fRend;
   }
   upload_rule(h, std::max(2 * p, 1), h.rule_elem, &h.rule_elem_R);
 }

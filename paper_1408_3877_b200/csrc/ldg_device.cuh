@@ -46,6 +46,9 @@ struct DevTables {
   const float* fbase;
   int NF;
   long fmH, fmSd, fmSo, fM, fSd, fSo, fpe, fpth, fwe;
+  // rank-Qe edge block (FTables): peR | peT | pthT | weR, rows padded to NF / QF
+  int QF;
+  long fR, fpeT, fpthT, fweR, fRend;
 };
 
 struct DevMesh {

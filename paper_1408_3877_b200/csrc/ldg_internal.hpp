@@ -139,6 +139,9 @@ struct Handle {
   DBuf<double> kr_r, kr_rh, kr_p, kr_v, kr_s, kr_t, kr_ph, kr_sh, kr_b;
   DBuf<double> tz;       // 2 * N * Kp : M^-1 B^m x
   DBuf<float> tz32;      // the same for the FP32 smoother on single-rank thread-per-element levels
+  // edge traces of the FP32 smoother (single rank, ldg_smooth.cu): values at the Qe points of
+  // each local edge, [n][q][Kp]: tr32 = x | -(c1 t^1 + c2 t^2) of the current sweep, dtr32 = d_h (per step)
+  DBuf<float> tr32, dtr32;
   DBuf<double> Pinv;     // N*N * Kp : block-Jacobi inverse
   DBuf<double> full_r, full_y;  // 3 * N * Kp : reference residual contract
   DBuf<double> red;      // reduction scratch
@@ -352,6 +355,7 @@ void smooth_stage1(Handle& h, const double* x, int k0 = 0, int k1 = -1);  // tz 
 // (out_old = x_{k-1}, taken as 0 when prev_zero)
 void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double wm, double dt, double omega,
                    double* out, double cheb_beta = 0.0, int prev_zero = 0, int k0 = 0, int k1 = -1);
+int smooth_trace_min_p();  // degrees >= this exchange edge traces between the smoother's stages
 void smooth_zero(Handle& h, const double* b, double omega, double* out);  // out = omega P^-1 b
 // the same three operations for small levels (ldg_small.cu; E32 / Pinv32 SoA copies)
 void small_stage1(Handle& h, const double* x);

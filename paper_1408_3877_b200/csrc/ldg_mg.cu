@@ -501,7 +501,14 @@ void mg_setup_f32_level(Handle& L, double wm, double dt) {
   const long NN = static_cast<long>(L.N) * L.N;
   if (!level_uses_rows(L)) {
     // stage-1 output of the smoother in FP32 (no halo of it across ranks: single rank only)
-    if (L.size == 1 && !L.tz32.ptr) L.tz32.alloc(2 * L.vec_len(), &L.bytes);
+    if (L.size == 1 && !L.tz32.ptr) {
+      L.tz32.alloc(2 * L.vec_len(), &L.bytes);
+      if (L.p >= smooth_trace_min_p()) {
+        const long q = (3 * L.p + 2) / 2;  // edge rule of the rank-Qe form
+        L.tr32.alloc(6 * q * L.Kp, &L.bytes);
+        L.dtr32.alloc(3 * q * L.Kp, &L.bytes);
+      }
+    }
     if (!L.Ph.ptr) {  // FP16 packed P^-1, scaled per element
       L.Ph.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
       L.Pscale.alloc(L.Kp, &L.bytes);

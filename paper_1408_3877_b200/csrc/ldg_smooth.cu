@@ -25,6 +25,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <type_traits>
 
 #include "ldg_internal.hpp"
 #include "ldg_pack.cuh"
@@ -44,7 +46,7 @@
 // -DLDG_MINB_S1=abcde / -DLDG_MINB_S2=abcde (one digit per p = 0..4)
 // override (tuning builds).
 #ifndef LDG_MINB_S1
-#define LDG_MINB_S1 11884
+#define LDG_MINB_S1 11874
 #endif
 #ifndef LDG_MINB_S2
 #define LDG_MINB_S2 11777
@@ -119,82 +121,235 @@ __device__ __forceinline__ void load_f(const double* __restrict__ x, long Kp, in
   for (int j = 0; j < N; ++j) v[j] = static_cast<float>(x[j * Kp + col]);
 }
 
-// tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out
+// ---- rank-Qe edge terms --------------------------------------------------
+// Every edge matrix of the smoother is a quadrature sum over the Qe points
+// of the edge rule (FTables: s_diag_n = peR_n^t diag(we) peR_n, s_offdiag =
+// peR_n^t diag(we) pthT_{n,np}^t, and the off-diagonal E blocks with the
+// sampled d, ldg_offdiag.cuh), so one edge costs its projections onto the
+// points (N Qe each), a pointwise combination, and ONE product back
+// (Qe N) instead of an N x N table product per term: per edge at p = 4,
+// stage 2 runs 525 FMAs where the table form ran 765, stage 1 315 for 510,
+// and the staged tables shrink from 13-14 N x NF blocks to 7 KB.
+// Edge traces between stage 1 and stage 2 from this degree on (measured at
+// 256^2, level-0 sweep: p = 4 88.3 -> 76.2 us; p = 3 42.8 either way; p <= 2
+// and the small levels lose 2 us per sweep to the longer stage 1)
+#ifndef LDG_TRACE_MINP
+#define LDG_TRACE_MINP 3
+#endif
+constexpr int kTraceMinP = LDG_TRACE_MINP;
+
+template <int P>
+struct RankCfg {
+  static constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, Q = Cfg<P>::Q, QF = (Q + 3) / 4 * 4;
+  static constexpr int kPeT = 3 * Q * NF, kPthT = kPeT + 3 * N * QF, kWe = kPthT + 9 * N * QF;
+  static constexpr int kFloats = kWe + QF;  // [peR | peT | pthT | weR]
+};
+
+// z (QF values as pairs) += T[j][.] v: row j of a [N][QF] projection table
+template <int QF>
+__device__ __forceinline__ void rank_acc(const float* rowj, float v, float2* z) {
+  const float2 vv = make_float2(v, v);
+  const float4* r4 = reinterpret_cast<const float4*>(rowj);
+#pragma unroll
+  for (int c = 0; c < QF / 4; ++c) {
+    const float4 t = r4[c];
+    z[2 * c] = __ffma2_rn(make_float2(t.x, t.y), vv, z[2 * c]);
+    z[2 * c + 1] = __ffma2_rn(make_float2(t.z, t.w), vv, z[2 * c + 1]);
+  }
+}
+
+// out (NF values as pairs) += sum_q R[q][.] z[q]: the rows of peR_n
+template <int Q, int NF>
+__device__ __forceinline__ void rank_out(const float* R, const float2* z, float2* out) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const float zq = (q & 1) ? z[q / 2].y : z[q / 2].x;
+    const float2 vv = make_float2(zq, zq);
+    const float4* r4 = reinterpret_cast<const float4*>(R + q * NF);
+#pragma unroll
+    for (int c = 0; c < NF / 4; ++c) {
+      const float4 t = r4[c];
+      out[2 * c] = __ffma2_rn(make_float2(t.x, t.y), vv, out[2 * c]);
+      out[2 * c + 1] = __ffma2_rn(make_float2(t.z, t.w), vv, out[2 * c + 1]);
+    }
+  }
+}
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+
+// copies two launch-invariant table blocks into shared memory (one barrier)
+__device__ __forceinline__ void stage_f2(float* sm, const float* a, int na, const float* b, int nb) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float4* d4 = reinterpret_cast<float4*>(sm);
+  for (int i = threadIdx.x; i < na / 4; i += blockDim.x) d4[i] = a4[i];
+  for (int i = threadIdx.x; i < nb / 4; i += blockDim.x) d4[na / 4 + i] = b4[i];
+  __syncthreads();
+}
+
+// tout^m = M_k^-1 B^m x (both m), FP32 arithmetic, FP64 in/out.  The element
+// part -H^m from the two m_hat^-1-premultiplied tables, the edge parts
+// Q^m + Q_N^m in rank-Qe form (m_hat = I to rounding in FP32).
+//
+// With `tr` (single-rank levels) the element also leaves its edge traces for
+// stage 2, [n][q][Kp] at the Qe points of its own edges: x (already
+// projected here) and -(c1 t^1 + c2 t^2), c = nu |E| / 2 — what the
+// neighbour across edge n needs of this element, with the neighbour's sign
+// of the normal.  Stage 2 then reads Qe values per edge and quantity instead
+// of gathering the neighbour's N-vectors and projecting them again.
 template <int P, typename TT>
 __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
-                                             TT* __restrict__ tout, int k0, int k1) {
-  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF;
+                                             TT* __restrict__ tout, float* __restrict__ tr, int k0, int k1) {
+  using RC = RankCfg<P>;
+  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF, Q = RC::Q, QF = RC::QF;
   extern __shared__ __align__(16) float smf[];
-  const float* tb = stage_f(smf, T.fbase + T.fmH, 14 * TAB);  // tmH 2 | tmSd 3 | tmSo 9
-  pdl_wait();
-  pdl_trigger();
-  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= k1) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
-  float xv[N], w[N], u1[N], u2[N];
-  load_f<N>(x, Kp, k, xv);
-  const float b11 = static_cast<float>(g[kB11 * Kp + k]), b12 = static_cast<float>(g[kB12 * Kp + k]);
-  const float b21 = static_cast<float>(g[kB21 * Kp + k]), b22 = static_cast<float>(g[kB22 * Kp + k]);
-  ftab_mv<N, NF>(tb, xv, w);
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    u1[i] = -b22 * w[i];
-    u2[i] = b12 * w[i];
-  }
-  ftab_mv<N, NF>(tb + TAB, xv, w);
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    u1[i] = fmaf(b21, w[i], u1[i]);
-    u2[i] = fmaf(-b11, w[i], u2[i]);
-  }
-#pragma unroll 1
-  for (int n = 0; n < 3; ++n) {
-    const int kind = m.kind[n * Kp + k];
-    const double len = g[(kLen0 + n) * Kp + k];
-    const double f = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
-    if (f == 0.0) continue;
-    ftab_mv<N, NF>(tb + (2 + n) * TAB, xv, w);
-    const float c1 = static_cast<float>(f * g[(kNux0 + n) * Kp + k]);
-    const float c2 = static_cast<float>(f * g[(kNuy0 + n) * Kp + k]);
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      u1[i] = fmaf(c1, w[i], u1[i]);
-      u2[i] = fmaf(c2, w[i], u2[i]);
-    }
-  }
-  // the neighbours' x: every load issued before the products (one latency
-  // round instead of one per neighbour; one neighbour at a time at 6-8 CTAs
-  // per SM measured 3-16 % slower at p = 4)
-  int nb[3], nbn[3];
+  const int kt = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = kt < k1 ? kt : k1 - 1;
+  // the element's mesh data is launch-invariant: in flight across the table
+  // staging and the dependency wait
+  int kind[3], nb[3], nbn[3];
+  float c1[3], c2[3];
 #pragma unroll
   for (int n = 0; n < 3; ++n) {
+    kind[n] = m.kind[n * Kp + k];
     nb[n] = m.nbr[n * Kp + k];
     nbn[n] = m.nbrn[n * Kp + k];
-  }
-  float xn[3][N];
-#pragma unroll
-  for (int n = 0; n < 3; ++n)
-#pragma unroll
-    for (int j = 0; j < N; ++j) xn[n][j] = nb[n] >= 0 ? static_cast<float>(x[j * Kp + nb[n]]) : 0.f;
-#pragma unroll
-  for (int n = 0; n < 3; ++n) {
-    if (nb[n] < 0) continue;
-    ftab_mv<N, NF>(tb + (5 + n * 3 + nbn[n]) * TAB, xn[n], w);
     const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
-    const float c1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
-    const float c2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
+    c1[n] = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
+    c2[n] = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
+  }
+  const float b11 = static_cast<float>(g[kB11 * Kp + k]), b12 = static_cast<float>(g[kB12 * Kp + k]);
+  const float b21 = static_cast<float>(g[kB21 * Kp + k]), b22 = static_cast<float>(g[kB22 * Kp + k]);
+  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
+  stage_f2(smf, T.fbase + T.fmH, 2 * TAB, T.fbase + T.fR, RC::kFloats);
+  const float* tb = smf;
+  const float* s_R = smf + 2 * TAB;
+  pdl_wait();
+  pdl_trigger();
+  if (kt >= k1) return;
+  float2 u1[NF / 2], u2[NF / 2];
+  {
+    float2 w1[NF / 2], w2[NF / 2];
+    float2 zo[3][QF / 2];  // own projections onto the three edges' points
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      u1[i] = fmaf(c1, w[i], u1[i]);
-      u2[i] = fmaf(c2, w[i], u2[i]);
+    for (int c = 0; c < NF / 2; ++c) w1[c] = w2[c] = f2(0.f);
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+#pragma unroll
+      for (int c = 0; c < QF / 2; ++c) zo[n][c] = f2(0.f);
+    // one pass over the element's x: both H products and (with traces) the three projections
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const float xj = static_cast<float>(x[j * Kp + k]);
+      rank_acc<NF>(tb + j * NF, xj, w1);
+      rank_acc<NF>(tb + TAB + j * NF, xj, w2);
+      if (tr) {
+#pragma unroll
+        for (int n = 0; n < 3; ++n) rank_acc<QF>(s_R + RC::kPeT + (n * N + j) * QF, xj, zo[n]);
+      }
+    }
+    if (tr) {
+#pragma unroll
+      for (int n = 0; n < 3; ++n)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) tr[(n * Q + q) * Kp + k] = (q & 1) ? zo[n][q / 2].y : zo[n][q / 2].x;
+    }
+#pragma unroll
+    for (int c = 0; c < NF / 2; ++c) {
+      u1[c] = __ffma2_rn(f2(b21), w2[c], mul2(f2(-b22), w1[c]));
+      u2[c] = __ffma2_rn(f2(-b11), w2[c], mul2(f2(b12), w1[c]));
     }
   }
-  const float inv2a = static_cast<float>(1.0 / (2.0 * g[kArea * Kp + k]));
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    // own side: nu |E| / 2 on interior edges, nu |E| on Neumann edges, none on Dirichlet edges
+    const float fo = kind[n] == kInterior ? 1.f : (kind[n] == kNeumann ? 2.f : 0.f);
+    if (fo == 0.f && nb[n] < 0) continue;
+    float2 z[QF / 2];
+#pragma unroll
+    for (int c = 0; c < QF / 2; ++c) z[c] = f2(0.f);
+    if (fo != 0.f) {
+      if (tr) {  // the element's own x trace, just written
+        float zq[QF];
+#pragma unroll
+        for (int q = 0; q < QF; ++q) zq[q] = q < Q ? fo * tr[(n * Q + q) * Kp + k] : 0.f;
+#pragma unroll
+        for (int c = 0; c < QF / 2; ++c) z[c] = make_float2(zq[2 * c], zq[2 * c + 1]);
+      } else {
+        const float* pT = s_R + RC::kPeT + n * N * QF;
+#pragma unroll
+        for (int j = 0; j < N; ++j) rank_acc<QF>(pT + j * QF, fo * static_cast<float>(x[j * Kp + k]), z);
+      }
+    }
+    if (nb[n] >= 0) {
+      const float* tT = s_R + RC::kPthT + (n * 3 + nbn[n]) * N * QF;
+      const int kp = nb[n];
+#pragma unroll
+      for (int j = 0; j < N; ++j) rank_acc<QF>(tT + j * QF, static_cast<float>(x[j * Kp + kp]), z);
+    }
+    const float4* we4 = reinterpret_cast<const float4*>(s_R + RC::kWe);
+#pragma unroll
+    for (int c = 0; c < QF / 4; ++c) {
+      const float4 w = we4[c];
+      z[2 * c] = mul2(z[2 * c], make_float2(w.x, w.y));
+      z[2 * c + 1] = mul2(z[2 * c + 1], make_float2(w.z, w.w));
+    }
+    float2 sv[NF / 2];
+#pragma unroll
+    for (int c = 0; c < NF / 2; ++c) sv[c] = f2(0.f);
+    rank_out<Q, NF>(s_R + n * Q * NF, z, sv);
+#pragma unroll
+    for (int c = 0; c < NF / 2; ++c) {
+      u1[c] = __ffma2_rn(f2(c1[n]), sv[c], u1[c]);
+      u2[c] = __ffma2_rn(f2(c2[n]), sv[c], u2[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NF / 2; ++c) {
+    u1[c] = mul2(u1[c], f2(inv2a));
+    u2[c] = mul2(u2[c], f2(inv2a));
+  }
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    tout[i * Kp + k] = static_cast<TT>(inv2a * u1[i]);
-    tout[(N + i) * Kp + k] = static_cast<TT>(inv2a * u2[i]);
+    tout[i * Kp + k] = static_cast<TT>((i & 1) ? u1[i / 2].y : u1[i / 2].x);
+    tout[(N + i) * Kp + k] = static_cast<TT>((i & 1) ? u2[i / 2].y : u2[i / 2].x);
+  }
+  if (tr) {
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      float2 zu[QF / 2];
+#pragma unroll
+      for (int c = 0; c < QF / 2; ++c) zu[c] = f2(0.f);
+      const float* pT = s_R + RC::kPeT + n * N * QF;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const float t1 = (j & 1) ? u1[j / 2].y : u1[j / 2].x, t2 = (j & 1) ? u2[j / 2].y : u2[j / 2].x;
+        rank_acc<QF>(pT + j * QF, -fmaf(c1[n], t1, c2[n] * t2), zu);
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) tr[((3 + n) * Q + q) * Kp + k] = (q & 1) ? zu[q / 2].y : zu[q / 2].x;
+    }
+  }
+}
+
+// d_h at the edge points of every element (per step and level): dtr[n][q][k] = sum_j peR_n[q][j] D[j][k]
+template <int P>
+__global__ void __launch_bounds__(128) k_dtrace(long Kp, int Kg, const float* __restrict__ peR,
+                                                const double* __restrict__ D, float* __restrict__ dtr) {
+  constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, Q = RankCfg<P>::Q;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= Kg) return;
+  float dv[N];
+  load_f<N>(D, Kp, k, dv);
+#pragma unroll 1
+  for (int nq = 0; nq < 3 * Q; ++nq) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fmaf(__ldg(peR + nq * NF + j), dv[j], s);
+    dtr[nq * Kp + k] = s;
   }
 }
 
@@ -275,16 +430,13 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
                                              const TT* __restrict__ tz, const double* __restrict__ b, double wm,
                                              double dteta, double dt, const TP* __restrict__ Pq,
                                              const float* __restrict__ Pscale, float omega, double* out,
-                                             double cheb_beta, int prev_zero, int k0, int k1) {
+                                             double cheb_beta, int prev_zero, int k0, int k1,
+                                             const float* __restrict__ tr, const float* __restrict__ dtr) {
   using C = Cfg<P>;
-  constexpr int N = C::N, NF = C::NF, TAB = N * NF;
-  constexpr int Q = C::Q;
+  using RC = RankCfg<P>;
+  constexpr int N = C::N, NF = C::NF, Q = RC::Q, QF = RC::QF;
   extern __shared__ __align__(16) float smf[];
-  // tM | tSd 3 | tSo 9 | pe 3 | pth 9 | we (contiguous in the FP32 table buffer)
-  const float* tb = stage_f(smf, T.fbase + T.fM, 13 * TAB + C::EDGE);
-  const float* s_pe = tb + 13 * TAB;
-  const float* s_pth = s_pe + 3 * Q * N;
-  const float* s_we = s_pth + 9 * Q * N;
+  const float* s_R = stage_f(smf, T.fbase + T.fR, RC::kFloats);  // peR | peT | pthT | weR
   __shared__ float s_r[MODE == 1 && !C::kFlat ? N : 1][128];  // the residual, for the grouped P^-1 stream
   const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
@@ -292,9 +444,10 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
   if (k >= k1) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
-  float acc[N];
+  float acc[NF];
 #pragma unroll
-  for (int i = 0; i < N; ++i) acc[i] = 0.f;
+  for (int i = 0; i < NF; ++i) acc[i] = 0.f;
+  const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
   // diagonal blocks E^m_kk t^m_k (packed stream), scaled copy
 #pragma unroll 1
   for (int c = 0; c < 2; ++c) {
@@ -302,56 +455,112 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
     packed_apply<P, TQ>(Eq + static_cast<long>(c) * C::QP * Kp + k, Kp,
                         [&](int j) { return static_cast<float>(tc[j * Kp]); }, acc);
   }
-  if (Escale) {
-    const float es = Escale[k];
-#pragma unroll
-    for (int i = 0; i < N; ++i) acc[i] *= es;
-  }
-  // off-diagonal blocks, matrix-free from D (ldg_offdiag.cuh)
-#pragma unroll 1
-  for (int n = 0; n < 3; ++n) {
-    const int kp = m.nbr[n * Kp + k];
-    if (kp < 0) continue;
-    const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
-    const float co1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
-    const float co2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
-    float z[Q];
-    offdiag_z<N, Q, float>(
-        s_pth + (n * 3 + m.nbrn[n * Kp + k]) * Q * N, s_we, [&](int j) { return static_cast<float>(D[j * Kp + kp]); },
-        [&](int j) {
-          return fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
-        },
-        z);
-    offdiag_rows<N, Q, float>(s_pe + n * Q * N, z, 1.0f, acc);
-  }
-  const float fdt = static_cast<float>(dt), fdteta = static_cast<float>(dteta);
-#pragma unroll
-  for (int i = 0; i < N; ++i) acc[i] *= fdt;
   {
-    float xv[N], w[N];
-    load_f<N>(x, Kp, k, xv);
-    ftab_mv<N, NF>(tb, xv, w);
-    const float sm = static_cast<float>(-wm * 2.0 * g[kArea * Kp + k]);
+    const float es = (Escale ? Escale[k] : 1.0f) * fdt;
+    const float sm = static_cast<float>(-wm * 2.0 * g[kArea * Kp + k]);  // mass term, m_hat = I in FP32
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc[i] = fmaf(sm, w[i], acc[i]);
+    for (int i = 0; i < N; ++i) acc[i] = fmaf(sm, static_cast<float>(x[i * Kp + k]), es * acc[i]);
+  }
+  // Everything that crosses edge n, in rank-Qe form with one product back:
+  //   + dt   E^m_{k,kp} t^m_kp  (matrix-free from D, ldg_offdiag.cuh)   interior
+  //   - dt eta s_diag_n x_k                                            interior, Dirichlet
+  //   + dt eta s_offdiag_{n,np} x_kp                                   interior
+  if constexpr (std::is_same<TT, float>::value && P >= kTraceMinP) {
+    // single-rank levels: the traces stage 1 left at the edge points (the
+    // neighbour's point q' = Qe - 1 - q: its edge runs the other way)
 #pragma unroll 1
     for (int n = 0; n < 3; ++n) {
       const int kind = m.kind[n * Kp + k];
-      if (kind != kInterior && kind != kDirichlet) continue;
-      ftab_mv<N, NF>(tb + (1 + n) * TAB, xv, w);
+      const int kp = m.nbr[n * Kp + k];
+      const bool pen = kind == kInterior || kind == kDirichlet;
+      if (!pen && kp < 0) continue;
+      float z[Q];
 #pragma unroll
-      for (int i = 0; i < N; ++i) acc[i] = fmaf(-fdteta, w[i], acc[i]);
+      for (int q = 0; q < Q; ++q) z[q] = pen ? -fdteta * tr[(n * Q + q) * Kp + k] : 0.f;
+      if (kp >= 0) {
+        const long at = static_cast<long>(m.nbrn[n * Kp + k]) * Q * Kp + kp;
+        const float* xt = tr + at;
+        const float* ut = xt + 3 * Q * Kp;
+        const float* dt_ = dtr + at;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const long o = static_cast<long>(Q - 1 - q) * Kp;
+          z[q] = fmaf(fdteta, xt[o], fmaf(fdt * dt_[o], ut[o], z[q]));
+        }
+      }
+      const float* we = s_R + RC::kWe;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) z[q] *= we[q];
+      float2* out2 = reinterpret_cast<float2*>(acc);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const float2 vv = f2(z[q]);
+        const float4* r4 = reinterpret_cast<const float4*>(s_R + (n * Q + q) * NF);
+#pragma unroll
+        for (int c = 0; c < NF / 4; ++c) {
+          const float4 t = r4[c];
+          out2[2 * c] = __ffma2_rn(make_float2(t.x, t.y), vv, out2[2 * c]);
+          out2[2 * c + 1] = __ffma2_rn(make_float2(t.z, t.w), vv, out2[2 * c + 1]);
+        }
+      }
     }
-  }
+  } else {
 #pragma unroll 1
   for (int n = 0; n < 3; ++n) {
+    const int kind = m.kind[n * Kp + k];
     const int kp = m.nbr[n * Kp + k];
-    if (kp < 0) continue;
-    float xn[N], w[N];
-    load_f<N>(x, Kp, kp, xn);
-    ftab_mv<N, NF>(tb + (4 + n * 3 + m.nbrn[n * Kp + k]) * TAB, xn, w);
+    const bool pen = kind == kInterior || kind == kDirichlet;
+    if (!pen && kp < 0) continue;
+    float2 z[QF / 2];
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc[i] = fmaf(fdteta, w[i], acc[i]);
+    for (int c = 0; c < QF / 2; ++c) z[c] = f2(0.f);
+    if (pen) {
+      const float* pT = s_R + RC::kPeT + n * N * QF;
+#pragma unroll
+      for (int j = 0; j < N; ++j) rank_acc<QF>(pT + j * QF, static_cast<float>(x[j * Kp + k]), z);
+#pragma unroll
+      for (int c = 0; c < QF / 2; ++c) z[c] = mul2(z[c], f2(-fdteta));
+    }
+    if (kp >= 0) {
+      const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+      const float co1 = static_cast<float>(hl * g[(kNux0 + n) * Kp + k]);
+      const float co2 = static_cast<float>(hl * g[(kNuy0 + n) * Kp + k]);
+      const float* tT = s_R + RC::kPthT + (n * 3 + m.nbrn[n * Kp + k]) * N * QF;
+      float2 dv[QF / 2], uv[QF / 2], xn[QF / 2];
+#pragma unroll
+      for (int c = 0; c < QF / 2; ++c) dv[c] = uv[c] = xn[c] = f2(0.f);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const float dj = static_cast<float>(D[j * Kp + kp]);
+        const float uj =
+            fmaf(co1, static_cast<float>(tz[j * Kp + kp]), co2 * static_cast<float>(tz[(N + j) * Kp + kp]));
+        const float xj = static_cast<float>(x[j * Kp + kp]);
+        const float4* r4 = reinterpret_cast<const float4*>(tT + j * QF);
+#pragma unroll
+        for (int c = 0; c < QF / 4; ++c) {
+          const float4 t = r4[c];
+          const float2 ta = make_float2(t.x, t.y), tb2 = make_float2(t.z, t.w);
+          dv[2 * c] = __ffma2_rn(ta, f2(dj), dv[2 * c]);
+          dv[2 * c + 1] = __ffma2_rn(tb2, f2(dj), dv[2 * c + 1]);
+          uv[2 * c] = __ffma2_rn(ta, f2(uj), uv[2 * c]);
+          uv[2 * c + 1] = __ffma2_rn(tb2, f2(uj), uv[2 * c + 1]);
+          xn[2 * c] = __ffma2_rn(ta, f2(xj), xn[2 * c]);
+          xn[2 * c + 1] = __ffma2_rn(tb2, f2(xj), xn[2 * c + 1]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < QF / 2; ++c)
+        z[c] = __ffma2_rn(f2(fdteta), xn[c], __ffma2_rn(mul2(f2(fdt), dv[c]), uv[c], z[c]));
+    }
+    const float4* we4 = reinterpret_cast<const float4*>(s_R + RC::kWe);
+#pragma unroll
+    for (int c = 0; c < QF / 4; ++c) {
+      const float4 w = we4[c];
+      z[2 * c] = mul2(z[2 * c], make_float2(w.x, w.y));
+      z[2 * c + 1] = mul2(z[2 * c + 1], make_float2(w.z, w.w));
+    }
+    rank_out<Q, NF>(s_R + n * Q * NF, z, reinterpret_cast<float2*>(acc));
+  }
   }
   if constexpr (MODE == 0) {
 #pragma unroll
@@ -451,14 +660,16 @@ __global__ void __launch_bounds__(128) k_pack_eh(long Kp, const double* __restri
 
 template <int P>
 size_t s1_smem() {
-  return sizeof(float) * 14 * Cfg<P>::N * Cfg<P>::NF;
+  return sizeof(float) * (2 * Cfg<P>::N * Cfg<P>::NF + RankCfg<P>::kFloats);
 }
 template <int P>
 size_t s2_smem() {
-  return sizeof(float) * (13 * Cfg<P>::N * Cfg<P>::NF + Cfg<P>::EDGE);
+  return sizeof(float) * RankCfg<P>::kFloats;
 }
 
 }  // namespace
+
+int smooth_trace_min_p() { return kTraceMinP; }
 
 long packed_p_quads(int p) {
   switch (p) {
@@ -482,6 +693,11 @@ void smooth_pack_e(Handle& h) {
       h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
     }                                                                                                    \
     k_pack_eh<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr, h.Eh.ptr);       \
+    if (h.dtr32.ptr && P >= kTraceMinP) {                                                                \
+      k_dtrace<P><<<grid_of(h.Kg, 128), 128, 0, h.stream>>>(h.Kp, h.Kg, h.dtab.fbase + h.dtab.fR, h.D.ptr, \
+                                                            h.dtr32.ptr);                                \
+      ++h.launches;                                                                                      \
+    }                                                                                                    \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -496,9 +712,11 @@ void smooth_stage1(Handle& h, const double* x, int k0, int k1) {
 #define CALL(P)                                                                                               \
   do {                                                                                                        \
     if (h.tz32.ptr)                                                                                           \
-      launch_pdl(k_s1f<P, float>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz32.ptr, k0, k1); \
+      launch_pdl(k_s1f<P, float>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz32.ptr,         \
+                 P >= kTraceMinP ? h.tr32.ptr : nullptr, k0, k1);                                                                                         \
     else                                                                                                      \
-      launch_pdl(k_s1f<P, double>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr, k0, k1); \
+      launch_pdl(k_s1f<P, double>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr,          \
+                 static_cast<float*>(nullptr), k0, k1);                                                       \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -516,7 +734,7 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
 #define LAUNCH(P, M, TT, TZ)                                                                                      \
   launch_pdl(k_s2f<P, M, uint2, uint2, TT>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, h.Eh.ptr,        \
              h.Escale.ptr, h.D.ptr, x, TZ, b, wm, dteta, dt, h.Ph.ptr, h.Pscale.ptr, om, out, cheb_beta, prev_zero, \
-             k0, k1)
+             k0, k1, (h.tz32.ptr && TZ == static_cast<const void*>(h.tz32.ptr)) ? h.tr32.ptr : nullptr, h.dtr32.ptr)
 #define CALL(P)                                           \
   do {                                                    \
     if (mode == 0 && h.tz32.ptr)                          \

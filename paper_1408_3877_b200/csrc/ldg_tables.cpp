@@ -441,8 +441,26 @@ FTables build_f32_tables(const HostTables& ht) {
   f.fpe = f.fSo + 9 * tab;
   f.fpth = f.fpe + 3 * qn;
   f.fwe = f.fpth + 9 * qn;
-  f.total = (f.fwe + L.Qe + 3) / 4 * 4;
+  f.QF = (L.Qe + 3) / 4 * 4;
+  f.fR = (f.fwe + L.Qe + 3) / 4 * 4;
+  f.fpeT = f.fR + 3L * L.Qe * f.NF;
+  f.fpthT = f.fpeT + 3L * N * f.QF;
+  f.fweR = f.fpthT + 9L * N * f.QF;
+  f.fRend = f.fweR + f.QF;
+  f.total = f.fRend;
   f.data.assign(f.total, 0.0f);
+  for (int n = 0; n < 3; ++n)
+    for (int q = 0; q < L.Qe; ++q)
+      for (int i = 0; i < N; ++i) {
+        const float v = static_cast<float>(ht.data[L.pe + (n * L.Qe + q) * N + i]);
+        f.data[f.fR + (n * L.Qe + q) * f.NF + i] = v;
+        f.data[f.fpeT + (n * N + i) * f.QF + q] = v;
+      }
+  for (int e = 0; e < 9; ++e)
+    for (int q = 0; q < L.Qe; ++q)
+      for (int j = 0; j < N; ++j)
+        f.data[f.fpthT + (e * N + j) * f.QF + q] = static_cast<float>(ht.data[L.pth + (e * L.Qe + q) * N + j]);
+  for (int q = 0; q < L.Qe; ++q) f.data[f.fweR + q] = static_cast<float>(ht.data[L.we + q]);
   for (long t = 0; t < 3 * qn; ++t) f.data[f.fpe + t] = static_cast<float>(ht.data[L.pe + t]);
   for (long t = 0; t < 9 * qn; ++t) f.data[f.fpth + t] = static_cast<float>(ht.data[L.pth + t]);
   for (int q = 0; q < L.Qe; ++q) f.data[f.fwe + q] = static_cast<float>(ht.data[L.we + q]);

@@ -82,9 +82,17 @@ HostTables build_tables(int p, const RefTensors* caller_rt = nullptr);
 //   [tmH 2 | tmSd 3 | tmSo 9]  stage 1 (m_hat^-1 applied)
 //   [tM 1 | tSd 3 | tSo 9]     stage 2
 //   [pe 3*Qe*N | pth 9*Qe*N | we Qe (padded to 4)]  matrix-free off-diagonal E
+// and the rank-Qe edge block every edge term of the smoother is applied from
+// (s_diag_n = pe_n^t diag(we) pe_n, s_offdiag_{n,np} = pe_n^t diag(we) pth_{n,np}:
+// the Qe-point rule is exact for degree 3p >= 2p), QF = Qe rounded up to 4:
+//   [peR 3][Qe][NF]    phi_i at the points of edge n, one row per point (the output product)
+//   [peT 3][N][QF]     the same transposed, one row per basis function (own projection)
+//   [pthT 9][N][QF]    phi_j at the theta-mapped points of the pair (n, np) (neighbour projection)
+//   [weR QF]           rule weights
 struct FTables {
-  int NF = 0;
+  int NF = 0, QF = 0;
   long fmH = 0, fmSd = 0, fmSo = 0, fM = 0, fSd = 0, fSo = 0, fpe = 0, fpth = 0, fwe = 0, total = 0;
+  long fR = 0, fpeT = 0, fpthT = 0, fweR = 0, fRend = 0;
   std::vector<float> data;
 };
 FTables build_f32_tables(const HostTables& ht);
