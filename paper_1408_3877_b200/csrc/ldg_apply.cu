@@ -377,10 +377,221 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1m(DevMesh m,
   }
 }
 
+// ---- rank-Qe edge form (TableLayout rkR..rkW, when DevTables::rank_ok) ------
+// Every edge operator is a Qe-point quadrature sum (s_diag_n = pe_n^t W pe_n,
+// s_offdiag_{n,np} = pe_n^t W pth_{n,np}, the off-diagonal E blocks with the
+// sampled d, ldg_offdiag.cuh), so an edge costs the projections of the
+// vectors onto its points, a pointwise combination and ONE product back
+// instead of an N x N table product per term; the derivative tables are
+// degree-lower-triangular and their zero chunks are skipped.  Same integrals
+// as the tables (exact rule), different rounding (<= 1e-15 relative).
+template <int P>
+struct RkCfg {
+  static constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP, Q = Cfg<P>::Q, QP = (Q + 1) / 2 * 2;
+  static constexpr int kR = 0, kRm = 3 * Q * NP, kT = 6 * Q * NP, kV = kT + 3 * N * QP, kW = kV + 9 * N * QP;
+  static constexpr int kCount = kW + QP;
+};
+
+// copies two launch-invariant table blocks (even counts, 16-byte aligned) into shared memory
+__device__ __forceinline__ void stage_d2(double* sm, const double* a, int na, const double* b, int nb) {
+  const double2* a2 = reinterpret_cast<const double2*>(a);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  double2* d2 = reinterpret_cast<double2*>(sm);
+  for (int i = threadIdx.x; i < na / 2; i += blockDim.x) d2[i] = a2[i];
+  for (int i = threadIdx.x; i < nb / 2; i += blockDim.x) d2[na / 2 + i] = b2[i];
+  __syncthreads();
+}
+
+// z[0..QP) += row[.] v
+template <int QP>
+__device__ __forceinline__ void rk_acc(const double* row, double v, double* z) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+  for (int c = 0; c < QP / 2; ++c) {
+    const double2 t = r2[c];
+    z[2 * c] = fma(t.x, v, z[2 * c]);
+    z[2 * c + 1] = fma(t.y, v, z[2 * c + 1]);
+  }
+}
+
+// out[0..N) += sum_q R[q][.] z[q]
+template <int N, int NP, int Q>
+__device__ __forceinline__ void rk_out(const double* R, const double* z, double* out) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double2* r2 = reinterpret_cast<const double2*>(R + q * NP);
+#pragma unroll
+    for (int c = 0; c < N / 2; ++c) {
+      const double2 t = r2[c];
+      out[2 * c] = fma(t.x, z[q], out[2 * c]);
+      out[2 * c + 1] = fma(t.y, z[q], out[2 * c + 1]);
+    }
+    if (N & 1) out[N - 1] = fma(R[q * NP + N - 1], z[q], out[N - 1]);
+  }
+}
+
+__host__ __device__ constexpr int hier_first_row(int j) {
+  int d = 0;
+  while ((d + 1) * (d + 2) / 2 <= j) ++d;  // degree of phi_j
+  return (d + 1) * (d + 2) / 2;            // first basis function of degree d + 1
+}
+
+// stage 1 of the Krylov operator in rank form: tout^m = tau M_k^-1 B^m x
+template <int P>
+__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m, DevTables T,
+                                                                      const double* __restrict__ x, double tau,
+                                                                      double* __restrict__ tout, int k0, int k1) {
+  using RC = RkCfg<P>;
+  constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP, NNP = N * NP, Q = RC::Q, QP = RC::QP;
+  extern __shared__ __align__(16) double sm[];
+  stage_d2(sm, T.base + T.tmH, 2 * NNP, T.base + T.rkR, RC::kCount);
+  const double* rk = sm + 2 * NNP;
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  double u1[N], u2[N];
+  {
+    double w1[N], w2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w1[i] = w2[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double xj = x[j * Kp + k];
+      const int first = hier_first_row(j);
+      const double2* r1 = reinterpret_cast<const double2*>(sm + j * NP);
+      const double2* r2 = reinterpret_cast<const double2*>(sm + NNP + j * NP);
+#pragma unroll
+      for (int c = 0; c < N / 2; ++c) {
+        if (2 * c + 1 < first) continue;
+        const double2 a = r1[c], b = r2[c];
+        w1[2 * c] = fma(a.x, xj, w1[2 * c]);
+        w1[2 * c + 1] = fma(a.y, xj, w1[2 * c + 1]);
+        w2[2 * c] = fma(b.x, xj, w2[2 * c]);
+        w2[2 * c + 1] = fma(b.y, xj, w2[2 * c + 1]);
+      }
+      if ((N & 1) && N - 1 >= first) {
+        w1[N - 1] = fma(sm[j * NP + N - 1], xj, w1[N - 1]);
+        w2[N - 1] = fma(sm[NNP + j * NP + N - 1], xj, w2[N - 1]);
+      }
+    }
+    const double b11 = g[kB11 * Kp + k], b12 = g[kB12 * Kp + k], b21 = g[kB21 * Kp + k], b22 = g[kB22 * Kp + k];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fma(b21, w2[i], -b22 * w1[i]);
+      u2[i] = fma(-b11, w2[i], b12 * w1[i]);
+    }
+  }
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kind = m.kind[n * Kp + k];
+    const int kp = m.nbr[n * Kp + k];
+    const double len = g[(kLen0 + n) * Kp + k];
+    const double co = kind == kInterior ? 0.5 * len : (kind == kNeumann ? len : 0.0);
+    if (co == 0.0 && kp < 0) continue;
+    double z[QP];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) z[q] = 0.0;
+    if (co != 0.0) {
+      const double* tT = rk + RC::kT + n * N * QP;
+#pragma unroll
+      for (int j = 0; j < N; ++j) rk_acc<QP>(tT + j * QP, co * x[j * Kp + k], z);
+    }
+    if (kp >= 0) {
+      const double hl = 0.5 * len;
+      const double* tV = rk + RC::kV + (n * 3 + m.nbrn[n * Kp + k]) * N * QP;
+#pragma unroll
+      for (int j = 0; j < N; ++j) rk_acc<QP>(tV + j * QP, hl * x[j * Kp + kp], z);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) z[q] *= rk[RC::kW + q];
+    double sv[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) sv[i] = 0.0;
+    rk_out<N, NP, Q>(rk + RC::kRm + n * Q * NP, z, sv);
+    const double nux = g[(kNux0 + n) * Kp + k], nuy = g[(kNuy0 + n) * Kp + k];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      u1[i] = fma(nux, sv[i], u1[i]);
+      u2[i] = fma(nuy, sv[i], u2[i]);
+    }
+  }
+  const double sc = tau / (2.0 * g[kArea * Kp + k]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    tout[i * Kp + k] = sc * u1[i];
+    tout[(N + i) * Kp + k] = sc * u2[i];
+  }
+}
+
+// Everything crossing the edges of element k in the C row, rank form:
+//   acc += ce sum_{kp} E_{k,kp} t_kp  +  beta ((S + S_D) x)_k
+// t = (t^1, t^2) at stride N Kp (null: no E term), x null / beta 0: no S term
+template <int P>
+__device__ __forceinline__ void edges_rank(const double* rk, const DevMesh& m, int k, const double* __restrict__ D,
+                                           const double* __restrict__ t, double ce, const double* __restrict__ x,
+                                           double beta, double* acc) {
+  using RC = RkCfg<P>;
+  constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP, Q = RC::Q, QP = RC::QP;
+  const long Kp = m.Kp;
+  const double* g = m.geom;
+  const bool sx = x != nullptr && beta != 0.0;
+#pragma unroll 1
+  for (int n = 0; n < 3; ++n) {
+    const int kind = m.kind[n * Kp + k];
+    const int kp = m.nbr[n * Kp + k];
+    const bool pen = sx && (kind == kInterior || kind == kDirichlet);
+    if (!pen && kp < 0) continue;
+    double z[QP];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) z[q] = 0.0;
+    if (pen) {
+      const double* tT = rk + RC::kT + n * N * QP;
+#pragma unroll
+      for (int j = 0; j < N; ++j) rk_acc<QP>(tT + j * QP, beta * x[j * Kp + k], z);
+    }
+    if (kp >= 0) {
+      const double* tV = rk + RC::kV + (n * 3 + m.nbrn[n * Kp + k]) * N * QP;
+      if (t) {
+        const double hl = 0.5 * g[(kLen0 + n) * Kp + k];
+        const double co1 = hl * g[(kNux0 + n) * Kp + k], co2 = hl * g[(kNuy0 + n) * Kp + k];
+        double dv[QP], uv[QP];
+#pragma unroll
+        for (int q = 0; q < QP; ++q) dv[q] = uv[q] = 0.0;
+#pragma unroll(N <= 6 ? N : 3)
+        for (int j = 0; j < N; ++j) {
+          const double dj = D[j * Kp + kp];
+          const double uj = fma(co1, t[j * Kp + kp], co2 * t[(N + j) * Kp + kp]);
+          const double xj = sx ? -beta * x[j * Kp + kp] : 0.0;
+          const double2* r2 = reinterpret_cast<const double2*>(tV + j * QP);
+#pragma unroll
+          for (int c = 0; c < QP / 2; ++c) {
+            const double2 tt = r2[c];
+            dv[2 * c] = fma(tt.x, dj, dv[2 * c]);
+            dv[2 * c + 1] = fma(tt.y, dj, dv[2 * c + 1]);
+            uv[2 * c] = fma(tt.x, uj, uv[2 * c]);
+            uv[2 * c + 1] = fma(tt.y, uj, uv[2 * c + 1]);
+            z[2 * c] = fma(tt.x, xj, z[2 * c]);
+            z[2 * c + 1] = fma(tt.y, xj, z[2 * c + 1]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < QP; ++q) z[q] = fma(ce * dv[q], uv[q], z[q]);
+      } else if (sx) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) rk_acc<QP>(tV + j * QP, -beta * x[j * Kp + kp], z);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) z[q] *= rk[RC::kW + q];
+    rk_out<N, NP, Q>(rk + RC::kR + n * Q * NP, z, acc);
+  }
+}
+
 // stage 2: y = alpha M_k x_k + beta (S + S_D) x - gamma sum_m sum_s E^m[s] tz^m_col + delta w
 // (the Krylov operator, FP64): stored diagonal blocks streamed, off-diagonal
 // blocks matrix-free from D.
-template <int P>
+template <int P, bool RK>
 __global__ void __launch_bounds__(128, LDG_MINB_S2STAGE_P(P)) k_stage2(DevMesh m, DevTables T, const double* __restrict__ E,
                                                 const double* __restrict__ D, const double* __restrict__ x,
                                                 double alpha, double beta, const double* __restrict__ tz,
@@ -388,6 +599,37 @@ __global__ void __launch_bounds__(128, LDG_MINB_S2STAGE_P(P)) k_stage2(DevMesh m
                                                 double* __restrict__ y, int k0, int k1) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
+  if constexpr (RK) {  // tM | rank-Qe edge block
+    stage_d2(sm, T.base + T.tM, N * NP, T.base + T.rkR, RkCfg<P>::kCount);
+    const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
+    const long Kp = m.Kp;
+    double acc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = 0.0;
+    if (tz) {
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c)
+        block_mv_gather<N>(E + static_cast<long>(c) * NN * Kp, Kp, k, tz + static_cast<long>(c) * N * Kp, k, acc);
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] *= -gamma;
+    }
+    edges_rank<P>(sm + N * NP, m, k, D, tz, -gamma, x, beta, acc);
+    if (x && alpha != 0.0) {
+      double v[N];
+      tab_mv_g<N, NP>(sm, x, Kp, k, v);
+      const double sa = alpha * 2.0 * m.geom[kArea * Kp + k];
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(sa, v[i], acc[i]);
+    }
+    if (w) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = fma(delta, w[i * Kp + k], acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[i * Kp + k] = acc[i];
+    return;
+  }
   const STab<P> tb = stage_tables<P, true>(sm, T);
   const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= k1) return;
@@ -512,6 +754,15 @@ __global__ void k_to_f32(long n, const double* __restrict__ src, float* __restri
 // 2048-element levels sweep in 27 / 26 us on thread-per-element kernels vs
 // 57 / 54 us otherwise at p = 4, hence the default of 2048).
 // LDG_ROWS_BELOW overrides the switch.
+// LDG_RANK_FORM=0: the table kernels even when the tensors allow the rank form (A/B, tests)
+bool rank_form() {
+  static const bool on = [] {
+    const char* s = std::getenv("LDG_RANK_FORM");
+    return s ? std::atoi(s) != 0 : true;
+  }();
+  return on;
+}
+
 bool use_rows(const Handle& h) {
   static const long below = [] {
     const char* s = std::getenv("LDG_ROWS_BELOW");
@@ -534,7 +785,11 @@ void launch_stage1(Handle& h, const double* vz, double sigma, const double* x, d
   // the Krylov operator's stage 1 (x only): premultiplied tables, no trailing M^-1 product
 #define CALL(P)                                                                                               \
   do {                                                                                                        \
-    if (!vz && x) {                                                                                           \
+    if (!vz && x && h.dtab.rank_ok && rank_form()) {                                                          \
+      const size_t smr = sizeof(double) * (2 * Cfg<P>::N * Cfg<P>::NP + RkCfg<P>::kCount);                    \
+      set_smem(k_stage1r<P>, smr);                                                                            \
+      k_stage1r<P><<<grid, 128, smr, h.stream>>>(h.mesh(), h.dtab, x, tau, tout, k0, k1);                     \
+    } else if (!vz && x) {                                                                                    \
       const size_t sm14 = sizeof(double) * 14 * Cfg<P>::N * Cfg<P>::NP;                                       \
       set_smem(k_stage1m<P>, sm14);                                                                           \
       k_stage1m<P><<<grid, 128, sm14, h.stream>>>(h.mesh(), h.dtab, x, tau, tout, k0, k1);                    \
@@ -560,9 +815,17 @@ void launch_stage2(Handle& h, const double* x, double alpha_m, double beta_s, co
   const unsigned grid = grid_of(k1 - k0, 128);
 #define CALL(P)                                                                                               \
   do {                                                                                                        \
-    set_smem(k_stage2<P>, tab_edge_smem<P>());                                                                \
-    k_stage2<P><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, x, alpha_m,  \
-                                                             beta_s, tz, gamma_e, w, delta, y, k0, k1);       \
+    if (h.dtab.rank_ok && rank_form()) {                                                                      \
+      const size_t smr = sizeof(double) * (Cfg<P>::N * Cfg<P>::NP + RkCfg<P>::kCount);                        \
+      set_smem(k_stage2<P, true>, smr);                                                                       \
+      k_stage2<P, true><<<grid, 128, smr, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, x, alpha_m, beta_s, \
+                                                      tz, gamma_e, w, delta, y, k0, k1);                      \
+    } else {                                                                                                  \
+      set_smem(k_stage2<P, false>, tab_edge_smem<P>());                                                       \
+      k_stage2<P, false><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, x,  \
+                                                                      alpha_m, beta_s, tz, gamma_e, w, delta, \
+                                                                      y, k0, k1);                             \
+    }                                                                                                         \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

@@ -370,13 +370,17 @@ __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const 
 // 30 (G) or 15 (R) independent accumulators per row instead of 2-5, and the
 // per-element constants (D_k, w_q d_h) live in shared memory (one conflict-free
 // 64-bit load per use) so the registers hold the accumulators.
+// -DLDG_ASM_THREADS_P4=n: CTA size of the row kernel at p = 4 (tuning builds)
+#ifndef LDG_ASM_THREADS_P4
+#define LDG_ASM_THREADS_P4 448
+#endif
 template <int P>
 struct Asm2 {
   static constexpr int N = Cfg<P>::N, Q = Cfg<P>::QE, NN = N * N;
   static constexpr int NP = (N % 2) ? N + 1 : N;  // padded table rows (16-byte aligned)
   // p = 4: one 384-thread CTA per SM (<= 168 registers, 12 warps; two
   // 128-thread CTAs were register- and shared-limited to 8); below, 128
-  static constexpr int kThreads = P == 4 ? 384 : 128;
+  static constexpr int kThreads = P == 4 ? LDG_ASM_THREADS_P4 : 128;
   static constexpr int kMinBlocks = P == 4 ? 1 : 4;
   // shared: G [i][l][j][2] | pe [n][q][NP] | pth [n][np][q][NP] | we [Q] (even) | per-thread [N + 3Q][T]
   static constexpr int kG = 2 * N * NN, kPe = 3 * Q * NP, kPth = 9 * Q * NP, kWe = (Q + 1) / 2 * 2;

@@ -36,7 +36,8 @@ void init_handle_tables(Handle& h, int p) {
   h.dtab = DevTables{h.tab.ptr, L.p,    L.N,    L.R,   L.Qe,  L.Qb,   L.proj_phi, L.proj_w, L.proj_x,
                      L.mhat,    L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe,   L.pth,      L.we,     L.pb,
                      L.sb,      L.wb,   L.total, L.mono, L.NP,  L.tH,   L.tSd,      L.tSo,    L.tM,
-                     L.tMinv,   L.tmH,  L.tmSd, L.tmSo};
+                     L.tMinv,   L.tmH,  L.tmSd, L.tmSo,  L.QP,  L.rank_ok ? 1 : 0, L.rkR, L.rkRm, L.rkT,
+                     L.rkV,     L.rkW,  L.rkEnd};
   {
     const FTables F = build_f32_tables(h.tables);
     h.ftab.alloc(F.data.size(), &h.bytes);

@@ -42,6 +42,9 @@ struct DevTables {
   int NP;
   long tH, tSd, tSo, tM, tMinv;
   long tmH, tmSd, tmSo;
+  // rank-Qe edge block (TableLayout rkR..rkW), usable when rank_ok
+  int QP, rank_ok;
+  long rkR, rkRm, rkT, rkV, rkW, rkEnd;
   // FP32 smoother tables (FTables in ldg_tables.hpp), offsets in floats
   const float* fbase;
   int NF;

@@ -158,6 +158,30 @@ __device__ __forceinline__ void rank_acc(const float* rowj, float v, float2* z) 
   }
 }
 
+// The same for column j of a derivative table h_hat(., ., m): the modal basis
+// is hierarchical by degree (N = 1, 3, 6, 10, 15 functions up to degree
+// 0..4) and d phi_i has a lower degree than phi_i, so H[i][j] = int d_m phi_i
+// phi_j vanishes unless deg phi_i > deg phi_j: the 4-row chunks below the
+// first row of degree deg(j) + 1 are skipped (29 of 60 chunks remain at p = 4).
+__host__ __device__ constexpr int hier_first_row(int j) {
+  int d = 0;
+  while ((d + 1) * (d + 2) / 2 <= j) ++d;  // degree of phi_j
+  return (d + 1) * (d + 2) / 2;            // first basis function of degree d + 1
+}
+template <int NF>
+__device__ __forceinline__ void hier_acc(const float* rowj, float v, float2* z, int j) {
+  const float2 vv = make_float2(v, v);
+  const float4* r4 = reinterpret_cast<const float4*>(rowj);
+  const int first = hier_first_row(j);
+#pragma unroll
+  for (int c = 0; c < NF / 4; ++c) {
+    if (4 * c + 3 < first) continue;
+    const float4 t = r4[c];
+    z[2 * c] = __ffma2_rn(make_float2(t.x, t.y), vv, z[2 * c]);
+    z[2 * c + 1] = __ffma2_rn(make_float2(t.z, t.w), vv, z[2 * c + 1]);
+  }
+}
+
 // out (NF values as pairs) += sum_q R[q][.] z[q]: the rows of peR_n
 template <int Q, int NF>
 __device__ __forceinline__ void rank_out(const float* R, const float2* z, float2* out) {
@@ -244,8 +268,8 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       const float xj = static_cast<float>(x[j * Kp + k]);
-      rank_acc<NF>(tb + j * NF, xj, w1);
-      rank_acc<NF>(tb + TAB + j * NF, xj, w2);
+      hier_acc<NF>(tb + j * NF, xj, w1, j);
+      hier_acc<NF>(tb + TAB + j * NF, xj, w2, j);
       if (tr) {
 #pragma unroll
         for (int n = 0; n < 3; ++n) rank_acc<QF>(s_R + RC::kPeT + (n * N + j) * QF, xj, zo[n]);

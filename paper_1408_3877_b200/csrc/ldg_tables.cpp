@@ -353,6 +353,13 @@ HostTables build_tables(int p, const RefTensors* caller_rt) {
   L.tmH = take(2L * N * L.NP);
   L.tmSd = take(3L * N * L.NP);
   L.tmSo = take(9L * N * L.NP);
+  L.QP = (L.Qe + 1) & ~1;
+  L.rkR = take(3L * L.Qe * L.NP);
+  L.rkRm = take(3L * L.Qe * L.NP);
+  L.rkT = take(3L * N * L.QP);
+  L.rkV = take(9L * N * L.QP);
+  L.rkW = take(L.QP);
+  L.rkEnd = off;
   L.total = off;
   ht.data.assign(off, 0.0);
   double* d = ht.data.data();
@@ -422,6 +429,51 @@ HostTables build_tables(int p, const RefTensors* caller_rt) {
     for (int np = 0; np < 3; ++np)
       minv_times(L.tmSo + (nm * 3 + np) * N * NP,
                  [&](int a, int j) { return rt.so[((a * N + j) * 3 + nm) * 3 + np]; });
+  // rank-Qe edge block
+  for (int n = 0; n < 3; ++n)
+    for (int q = 0; q < L.Qe; ++q)
+      for (int i = 0; i < N; ++i) {
+        const double v = d[L.pe + (n * L.Qe + q) * N + i];
+        d[L.rkR + (n * L.Qe + q) * NP + i] = v;
+        d[L.rkT + (n * N + i) * L.QP + q] = v;
+        double s = 0.0;
+        for (int a = 0; a < N; ++a) s += minv[i * N + a] * d[L.pe + (n * L.Qe + q) * N + a];
+        d[L.rkRm + (n * L.Qe + q) * NP + i] = s;
+      }
+  for (int e = 0; e < 9; ++e)
+    for (int q = 0; q < L.Qe; ++q)
+      for (int j = 0; j < N; ++j) d[L.rkV + (e * N + j) * L.QP + q] = d[L.pth + (e * L.Qe + q) * N + j];
+  for (int q = 0; q < L.Qe; ++q) d[L.rkW + q] = exact.w[q];
+  // do the caller's tensors have the structure the rank form assumes?
+  {
+    double dev = 0.0, ref = 0.0;
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        for (int n = 0; n < 3; ++n) {
+          double sd = 0.0;
+          for (int q = 0; q < L.Qe; ++q)
+            sd += exact.w[q] * d[L.pe + (n * L.Qe + q) * N + i] * d[L.pe + (n * L.Qe + q) * N + j];
+          dev = std::max(dev, std::fabs(sd - rt.sd[(i * N + j) * 3 + n]));
+          ref = std::max(ref, std::fabs(sd));
+          for (int np = 0; np < 3; ++np) {
+            double so = 0.0;
+            for (int q = 0; q < L.Qe; ++q)
+              so += exact.w[q] * d[L.pe + (n * L.Qe + q) * N + i] * d[L.pth + ((n * 3 + np) * L.Qe + q) * N + j];
+            dev = std::max(dev, std::fabs(so - rt.so[((i * N + j) * 3 + n) * 3 + np]));
+          }
+        }
+        // h_hat[i][j][m] = 0 unless deg(phi_i) > deg(phi_j)
+        int dj = 0;
+        while ((dj + 1) * (dj + 2) / 2 <= j) ++dj;
+        if (i < (dj + 1) * (dj + 2) / 2)
+          for (int m = 0; m < 2; ++m) {
+            double s = 0.0;  // entry of m_hat^-1 h_hat, as staged
+            for (int a = 0; a < N; ++a) s += minv[i * N + a] * rt.h[(a * N + j) * 2 + m];
+            dev = std::max(dev, std::fabs(s));
+          }
+      }
+    L.rank_ok = dev <= 1e-13 * std::max(ref, 1.0);
+  }
   return ht;
 }
 

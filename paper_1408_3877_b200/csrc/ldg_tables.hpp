@@ -64,6 +64,20 @@ struct TableLayout {
   long tMinv;                        // [N][NP]     m_hat^-1 ^t
   long tmH, tmSd, tmSo;              // the same with m_hat^-1 applied: (m_hat^-1 T)^t,
                                      // for stage 1 (t = M^-1 B x in one pass)
+  // rank-Qe edge block of the FP64 operator kernels (ldg_apply.cu), contiguous,
+  // QP = Qe rounded up to even:
+  //   rkR  [3][Qe][NP]   phi_i at the points of edge n (rows of pe, padded)
+  //   rkRm [3][Qe][NP]   the same with m_hat^-1 applied (stage 1 output)
+  //   rkT  [3][N][QP]    pe transposed (own projection)
+  //   rkV  [9][N][QP]    pth transposed (neighbour projection)
+  //   rkW  [QP]          weights
+  int QP = 0;
+  long rkR = 0, rkRm = 0, rkT = 0, rkV = 0, rkW = 0, rkEnd = 0;
+  // the caller's s_diag / s_offdiag equal pe^t diag(we) pe / pth to 1e-13 and
+  // h_hat is degree-lower-triangular (true for the library's own tensors):
+  // the operator kernels may use the rank-Qe edge form and skip the zero
+  // chunks of the derivative tables
+  bool rank_ok = false;
   long total = 0;
 };
 
