@@ -27,7 +27,13 @@
 #ifdef LDG_MINB_STAGE
 #define LDG_MINB_STAGE_P(P) LDG_MINB_STAGE
 #else
-#define LDG_MINB_STAGE_P(P) ((P) == 4 ? 4 : ((P) == 3 ? 7 : 1))
+#ifndef LDG_MINB_STAGE_P3
+#define LDG_MINB_STAGE_P3 7
+#endif
+#ifndef LDG_MINB_STAGE_P4
+#define LDG_MINB_STAGE_P4 4
+#endif
+#define LDG_MINB_STAGE_P(P) ((P) == 4 ? LDG_MINB_STAGE_P4 : ((P) == 3 ? LDG_MINB_STAGE_P3 : 1))
 #endif
 // stage 2 alone at p = 4 (tuning builds): 5 / 6 / 7 CTAs measured Schur apply
 // 274 / 298 / 308 us against 238 us at 4
@@ -436,21 +442,16 @@ __host__ __device__ constexpr int hier_first_row(int j) {
   return (d + 1) * (d + 2) / 2;            // first basis function of degree d + 1
 }
 
-// stage 1 of the Krylov operator in rank form: tout^m = tau M_k^-1 B^m x
+// u^m = B^m x in rank form (B^m = -H^m + Q^m + Q_N^m): the H part from the two
+// derivative tables at sH (tH, or tmH with m_hat^-1 applied), the edge parts
+// through rows rR of the output table (rkR, or rkRm with m_hat^-1 applied)
 template <int P>
-__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m, DevTables T,
-                                                                      const double* __restrict__ x, double tau,
-                                                                      double* __restrict__ tout, int k0, int k1) {
+__device__ __forceinline__ void apply_B_rank(const double* sH, const double* rk, int rR, const DevMesh& m, int k,
+                                             const double* __restrict__ x, double* u1, double* u2) {
   using RC = RkCfg<P>;
   constexpr int N = Cfg<P>::N, NP = Cfg<P>::NP, NNP = N * NP, Q = RC::Q, QP = RC::QP;
-  extern __shared__ __align__(16) double sm[];
-  stage_d2(sm, T.base + T.tmH, 2 * NNP, T.base + T.rkR, RC::kCount);
-  const double* rk = sm + 2 * NNP;
-  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= k1) return;
   const long Kp = m.Kp;
   const double* g = m.geom;
-  double u1[N], u2[N];
   {
     double w1[N], w2[N];
 #pragma unroll
@@ -459,8 +460,8 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m,
     for (int j = 0; j < N; ++j) {
       const double xj = x[j * Kp + k];
       const int first = hier_first_row(j);
-      const double2* r1 = reinterpret_cast<const double2*>(sm + j * NP);
-      const double2* r2 = reinterpret_cast<const double2*>(sm + NNP + j * NP);
+      const double2* r1 = reinterpret_cast<const double2*>(sH + j * NP);
+      const double2* r2 = reinterpret_cast<const double2*>(sH + NNP + j * NP);
 #pragma unroll
       for (int c = 0; c < N / 2; ++c) {
         if (2 * c + 1 < first) continue;
@@ -471,8 +472,8 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m,
         w2[2 * c + 1] = fma(b.y, xj, w2[2 * c + 1]);
       }
       if ((N & 1) && N - 1 >= first) {
-        w1[N - 1] = fma(sm[j * NP + N - 1], xj, w1[N - 1]);
-        w2[N - 1] = fma(sm[NNP + j * NP + N - 1], xj, w2[N - 1]);
+        w1[N - 1] = fma(sH[j * NP + N - 1], xj, w1[N - 1]);
+        w2[N - 1] = fma(sH[NNP + j * NP + N - 1], xj, w2[N - 1]);
       }
     }
     const double b11 = g[kB11 * Kp + k], b12 = g[kB12 * Kp + k], b21 = g[kB21 * Kp + k], b22 = g[kB22 * Kp + k];
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m,
     double sv[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) sv[i] = 0.0;
-    rk_out<N, NP, Q>(rk + RC::kRm + n * Q * NP, z, sv);
+    rk_out<N, NP, Q>(rk + rR + n * Q * NP, z, sv);
     const double nux = g[(kNux0 + n) * Kp + k], nuy = g[(kNuy0 + n) * Kp + k];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -516,7 +517,23 @@ __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m,
       u2[i] = fma(nuy, sv[i], u2[i]);
     }
   }
-  const double sc = tau / (2.0 * g[kArea * Kp + k]);
+}
+
+// stage 1 of the Krylov operator in rank form: tout^m = tau M_k^-1 B^m x
+template <int P>
+__global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_stage1r(DevMesh m, DevTables T,
+                                                                      const double* __restrict__ x, double tau,
+                                                                      double* __restrict__ tout, int k0, int k1) {
+  using RC = RkCfg<P>;
+  constexpr int N = Cfg<P>::N, NNP = N * Cfg<P>::NP;
+  extern __shared__ __align__(16) double sm[];
+  stage_d2(sm, T.base + T.tmH, 2 * NNP, T.base + T.rkR, RC::kCount);
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  const long Kp = m.Kp;
+  double u1[N], u2[N];
+  apply_B_rank<P>(sm, sm + 2 * NNP, RC::kRm, m, k, x, u1, u2);
+  const double sc = tau / (2.0 * m.geom[kArea * Kp + k]);
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     tout[i * Kp + k] = sc * u1[i];
@@ -667,12 +684,53 @@ __global__ void __launch_bounds__(128, LDG_MINB_S2STAGE_P(P)) k_stage2(DevMesh m
 // full (W + dt A) Y, Y = [Z1; Z2; C] (system.hpp:161-167):
 //   out_Zm = dt (M z^m_k + B^m c)
 //   out_C  = wm M c_k + dt (sum_m E^m z^m + eta (S + S_D) c)
-template <int P>
+template <int P, bool RK>
 __global__ void __launch_bounds__(128, LDG_MINB_STAGE_P(P)) k_full(DevMesh m, DevTables T, const double* __restrict__ E,
                                               const double* __restrict__ D, const double* __restrict__ Yin,
                                               double wm, double dt, double eta, double* __restrict__ out) {
   constexpr int N = Cfg<P>::N, NN = N * N, NP = Cfg<P>::NP;
   extern __shared__ __align__(16) double sm[];
+  if constexpr (RK) {  // tH 2 | tM | rank-Qe edge block
+    {
+      const double2* a2 = reinterpret_cast<const double2*>(T.base + T.tH);
+      const double2* b2 = reinterpret_cast<const double2*>(T.base + T.tM);
+      const double2* c2 = reinterpret_cast<const double2*>(T.base + T.rkR);
+      double2* d2 = reinterpret_cast<double2*>(sm);
+      for (int i = threadIdx.x; i < N * NP; i += blockDim.x) d2[i] = a2[i];
+      for (int i = threadIdx.x; i < N * NP / 2; i += blockDim.x) d2[N * NP + i] = b2[i];
+      for (int i = threadIdx.x; i < RkCfg<P>::kCount / 2; i += blockDim.x) d2[3 * N * NP / 2 + i] = c2[i];
+      __syncthreads();
+    }
+    const double* sM = sm + 2 * N * NP;
+    const double* rk = sm + 3 * N * NP;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m.K) return;
+    const long Kp = m.Kp;
+    const double two_a = 2.0 * m.geom[kArea * Kp + k];
+    const double* C = Yin + 2L * N * Kp;
+    double w[N];
+    {
+      double u1[N], u2[N];
+      apply_B_rank<P>(sm, rk, RkCfg<P>::kR, m, k, C, u1, u2);
+      tab_mv_g<N, NP>(sM, Yin, Kp, k, w);
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[i * Kp + k] = dt * fma(two_a, w[i], u1[i]);
+      tab_mv_g<N, NP>(sM, Yin + static_cast<long>(N) * Kp, Kp, k, w);
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[(N + i) * Kp + k] = dt * fma(two_a, w[i], u2[i]);
+    }
+    double acc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c)
+      block_mv_gather<N>(E + static_cast<long>(c) * NN * Kp, Kp, k, Yin + static_cast<long>(c) * N * Kp, k, acc);
+    edges_rank<P>(rk, m, k, D, Yin, 1.0, C, eta, acc);
+    tab_mv_g<N, NP>(sM, C, Kp, k, w);
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[(2 * N + i) * Kp + k] = fma(wm * two_a, w[i], dt * acc[i]);
+    return;
+  }
   const STab<P> tb = stage_tables<P, true>(sm, T);
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m.K) return;
@@ -837,9 +895,16 @@ void launch_full_apply(Handle& h, const double* Y, double wm, double dt, double*
   const unsigned grid = grid_of(h.K, 128);
 #define CALL(P)                                                                                                 \
   do {                                                                                                          \
-    set_smem(k_full<P>, tab_edge_smem<P>());                                                                    \
-    k_full<P><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, Y, wm, dt,       \
-                                                           h.prob.eta, out);                                    \
+    if (h.dtab.rank_ok && rank_form()) {                                                                        \
+      const size_t smr = sizeof(double) * (3 * Cfg<P>::N * Cfg<P>::NP + RkCfg<P>::kCount);                      \
+      set_smem(k_full<P, true>, smr);                                                                           \
+      k_full<P, true><<<grid, 128, smr, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, Y, wm, dt, h.prob.eta,  \
+                                                    out);                                                       \
+    } else {                                                                                                    \
+      set_smem(k_full<P, false>, tab_edge_smem<P>());                                                           \
+      k_full<P, false><<<grid, 128, tab_edge_smem<P>(), h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, Y, wm,  \
+                                                                    dt, h.prob.eta, out);                       \
+    }                                                                                                           \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL

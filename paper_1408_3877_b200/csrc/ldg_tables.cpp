@@ -469,7 +469,7 @@ HostTables build_tables(int p, const RefTensors* caller_rt) {
           for (int m = 0; m < 2; ++m) {
             double s = 0.0;  // entry of m_hat^-1 h_hat, as staged
             for (int a = 0; a < N; ++a) s += minv[i * N + a] * rt.h[(a * N + j) * 2 + m];
-            dev = std::max(dev, std::fabs(s));
+            dev = std::max(dev, std::max(std::fabs(s), std::fabs(rt.h[(i * N + j) * 2 + m])));
           }
       }
     L.rank_ok = dev <= 1e-13 * std::max(ref, 1.0);
