@@ -90,9 +90,15 @@ def bytes_sweep_s2(dim, p):
     """Compulsory bytes of the level-0 smoother stage 2 with the fused block-Jacobi
     update (k_s2f, FP16 packed E diagonal blocks and P^-1, each with a per-element
     scale): E 2 blocks x quads x 8 B, P quads x 8 B, 2 scales, vectors x, t (2),
-    D, b, out (FP64), geometry (10 doubles) and topology (9 ints)."""
+    D, b, out (FP64), geometry (10 doubles) and topology (9 ints); from p = 3 on the
+    edge-trace form (see below)."""
     K, N = 2 * dim * dim, n_of(p)
     q = packed_quads(p)
+    if p >= 3:
+        # edge-trace form (ldg_smooth.cu, kTraceMinP): no D and no edge geometry; instead the
+        # traces x, -(c1 t1 + c2 t2), d_h at the Qe points of the 3 edges (FP32), the area
+        qe = (3 * p + 2) // 2
+        return K * (3 * q * 8 + 2 * 4 + 8 * 5 * N + 4 * 9 * qe + 8 * 1 + 4 * 9)
     return K * (2 * q * 8 + q * 8 + 2 * 4 + 8 * 6 * N + 8 * 10 + 4 * 9)
 
 

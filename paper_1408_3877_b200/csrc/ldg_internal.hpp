@@ -142,6 +142,7 @@ struct Handle {
   // edge traces of the FP32 smoother (single rank, ldg_smooth.cu): values at the Qe points of
   // each local edge, [n][q][Kp]: tr32 = x | -(c1 t^1 + c2 t^2) of the current sweep, dtr32 = d_h (per step)
   DBuf<float> tr32, dtr32;
+  int xtr_cur = 0;  // which x-trace buffer of tr32 belongs to the vector stage 1 sees next
   DBuf<double> Pinv;     // N*N * Kp : block-Jacobi inverse
   DBuf<double> full_r, full_y;  // 3 * N * Kp : reference residual contract
   DBuf<double> red;      // reduction scratch
@@ -349,7 +350,8 @@ bool level_is_small(const Handle& h);
 // fused mixed-precision smoother (ldg_smooth.cu)
 long packed_p_quads(int p);                                           // float4 quads of one packed P^-1 block
 void smooth_pack_e(Handle& h);                                        // Eh (FP16 packed) from E
-void smooth_stage1(Handle& h, const double* x, int k0 = 0, int k1 = -1);  // tz = M^-1 B x (FP32 arithmetic)
+// chained: x is the output of the preceding smooth_stage2 (mode 1) launch on this level
+void smooth_stage1(Handle& h, const double* x, int k0 = 0, int k1 = -1, bool chained = false);  // tz = M^-1 B x (FP32 arithmetic)
 // mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)
 // cheb_beta != 0: Chebyshev step out <- x + omega P^-1 r + cheb_beta (x - out_old)
 // (out_old = x_{k-1}, taken as 0 when prev_zero)

@@ -505,7 +505,7 @@ void mg_setup_f32_level(Handle& L, double wm, double dt) {
       L.tz32.alloc(2 * L.vec_len(), &L.bytes);
       if (L.p >= smooth_trace_min_p()) {
         const long q = (3 * L.p + 2) / 2;  // edge rule of the rank-Qe form
-        L.tr32.alloc(6 * q * L.Kp, &L.bytes);
+        L.tr32.alloc(9 * q * L.Kp, &L.bytes);  // x traces A | u traces | x traces B
         L.dtr32.alloc(3 * q * L.Kp, &L.bytes);
       }
     }

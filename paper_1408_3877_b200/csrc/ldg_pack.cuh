@@ -2,6 +2,11 @@
 // shared with the block-Jacobi setup that writes P^-1 in it (ldg_apply.cu).
 #pragma once
 
+// -DLDG_UNR_P4=n: column groups of a packed block in flight per step at p = 4 (tuning builds)
+#ifndef LDG_UNR_P4
+#define LDG_UNR_P4 1
+#endif
+
 namespace ldgb {
 
 // Packing of the stored N x N blocks into float4 quads.
@@ -27,7 +32,7 @@ struct SmCfg {
   static constexpr int QP = kFlat ? (NN + 3) / 4 : QS;    // quads of one packed block (E^m_kk or P^-1)
   static constexpr int Q = (3 * P + 2) / 2;               // edge rule of the matrix-free off-diagonal E
   static constexpr int EDGE = (12 * Q * N + Q + 3) / 4 * 4;  // FP32 edge tables (pe, pth, we), padded
-  static constexpr int UNR = kFlat ? 1 : (16 / QC > 0 ? 16 / QC : 1);  // groups unrolled per step
+  static constexpr int UNR = kFlat ? 1 : (P == 4 ? LDG_UNR_P4 : (16 / QC > 0 ? 16 / QC : 1));  // groups unrolled per step
 };
 
 // (quad, component) of value (i, j) of a packed block: flat = column-major

@@ -59,6 +59,12 @@ namespace {
 constexpr int minb_digit(int code, int p) { return p == 4 ? code % 10 : minb_digit(code / 10, p + 1); }
 constexpr int kMinbS1[5] = {minb_digit(LDG_MINB_S1, 0), minb_digit(LDG_MINB_S1, 1), minb_digit(LDG_MINB_S1, 2),
                             minb_digit(LDG_MINB_S1, 3), minb_digit(LDG_MINB_S1, 4)};
+// stage 1 on chained sweeps (no projections of x: fewer registers)
+#ifndef LDG_MINB_S1C
+#define LDG_MINB_S1C 11874
+#endif
+constexpr int kMinbS1c[5] = {minb_digit(LDG_MINB_S1C, 0), minb_digit(LDG_MINB_S1C, 1), minb_digit(LDG_MINB_S1C, 2),
+                             minb_digit(LDG_MINB_S1C, 3), minb_digit(LDG_MINB_S1C, 4)};
 constexpr int kMinbS2[5] = {minb_digit(LDG_MINB_S2, 0), minb_digit(LDG_MINB_S2, 1), minb_digit(LDG_MINB_S2, 2),
                             minb_digit(LDG_MINB_S2, 3), minb_digit(LDG_MINB_S2, 4)};
 static_assert(kMinbS1[0] == LDG_MINB_S1 / 10000 && kMinbS2[4] == LDG_MINB_S2 % 10, "min-blocks digits");
@@ -222,9 +228,14 @@ __device__ __forceinline__ void stage_f2(float* sm, const float* a, int na, cons
 // neighbour across edge n needs of this element, with the neighbour's sign
 // of the normal.  Stage 2 then reads Qe values per edge and quantity instead
 // of gathering the neighbour's N-vectors and projecting them again.
-template <int P, typename TT>
-__global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T, const double* __restrict__ x,
-                                             TT* __restrict__ tout, float* __restrict__ tr, int k0, int k1) {
+// CH ("chained"): x is the output of the preceding stage-2 launch, which
+// left its x traces already (k_s2f epilogue): no projection of x at all here,
+// the neighbours' contribution is Qe trace values per edge.
+// tr = x traces [3][Q][Kp] (read if CH, written otherwise) | u traces [3][Q][Kp] at tr + utr_off.
+template <int P, typename TT, bool CH>
+__global__ void __launch_bounds__(128, CH ? kMinbS1c[P] : kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
+                                             const double* __restrict__ x, TT* __restrict__ tout,
+                                             float* __restrict__ tr, long utr_off, int k0, int k1) {
   using RC = RankCfg<P>;
   constexpr int N = Cfg<P>::N, NF = Cfg<P>::NF, TAB = N * NF, Q = RC::Q, QF = RC::QF;
   extern __shared__ __align__(16) float smf[];
@@ -270,12 +281,12 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
       const float xj = static_cast<float>(x[j * Kp + k]);
       hier_acc<NF>(tb + j * NF, xj, w1, j);
       hier_acc<NF>(tb + TAB + j * NF, xj, w2, j);
-      if (tr) {
+      if (!CH && tr) {
 #pragma unroll
         for (int n = 0; n < 3; ++n) rank_acc<QF>(s_R + RC::kPeT + (n * N + j) * QF, xj, zo[n]);
       }
     }
-    if (tr) {
+    if (!CH && tr) {
 #pragma unroll
       for (int n = 0; n < 3; ++n)
 #pragma unroll
@@ -309,10 +320,22 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
       }
     }
     if (nb[n] >= 0) {
-      const float* tT = s_R + RC::kPthT + (n * 3 + nbn[n]) * N * QF;
       const int kp = nb[n];
+      if constexpr (CH) {  // the neighbour's x trace at the matching points (its edge runs the other way)
+        const float* xt = tr + static_cast<long>(nbn[n]) * Q * Kp + kp;
+        float zq[QF];
 #pragma unroll
-      for (int j = 0; j < N; ++j) rank_acc<QF>(tT + j * QF, static_cast<float>(x[j * Kp + kp]), z);
+        for (int q = 0; q < QF; ++q) zq[q] = q < Q ? xt[(Q - 1 - q) * Kp] : 0.f;
+#pragma unroll
+        for (int c = 0; c < QF / 2; ++c) {
+          z[c].x += zq[2 * c];
+          z[c].y += zq[2 * c + 1];
+        }
+      } else {
+        const float* tT = s_R + RC::kPthT + (n * 3 + nbn[n]) * N * QF;
+#pragma unroll
+        for (int j = 0; j < N; ++j) rank_acc<QF>(tT + j * QF, static_cast<float>(x[j * Kp + kp]), z);
+      }
     }
     const float4* we4 = reinterpret_cast<const float4*>(s_R + RC::kWe);
 #pragma unroll
@@ -354,7 +377,7 @@ __global__ void __launch_bounds__(128, kMinbS1[P]) k_s1f(DevMesh m, DevTables T,
         rank_acc<QF>(pT + j * QF, -fmaf(c1[n], t1, c2[n] * t2), zu);
       }
 #pragma unroll
-      for (int q = 0; q < Q; ++q) tr[((3 + n) * Q + q) * Kp + k] = (q & 1) ? zu[q / 2].y : zu[q / 2].x;
+      for (int q = 0; q < Q; ++q) tr[utr_off + (n * Q + q) * Kp + k] = (q & 1) ? zu[q / 2].y : zu[q / 2].x;
     }
   }
 }
@@ -455,7 +478,8 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
                                              double dteta, double dt, const TP* __restrict__ Pq,
                                              const float* __restrict__ Pscale, float omega, double* out,
                                              double cheb_beta, int prev_zero, int k0, int k1,
-                                             const float* __restrict__ tr, const float* __restrict__ dtr) {
+                                             const float* __restrict__ tr, const float* __restrict__ utr,
+                                             const float* __restrict__ dtr, float* __restrict__ xtr_out) {
   using C = Cfg<P>;
   using RC = RankCfg<P>;
   constexpr int N = C::N, NF = C::NF, Q = RC::Q, QF = RC::QF;
@@ -504,7 +528,7 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
       if (kp >= 0) {
         const long at = static_cast<long>(m.nbrn[n * Kp + k]) * Q * Kp + kp;
         const float* xt = tr + at;
-        const float* ut = xt + 3 * Q * Kp;
+        const float* ut = utr + at;
         const float* dt_ = dtr + at;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -603,13 +627,35 @@ __global__ void __launch_bounds__(128, kMinbS2[P]) k_s2f(DevMesh m, DevTables T,
     const float om = Pscale ? omega * Pscale[k] : omega;
     if (cheb_beta == 0.0) {
 #pragma unroll
-      for (int i = 0; i < N; ++i)
-        out[i * Kp + k] = fma(static_cast<double>(om), static_cast<double>(d[i]), x[i * Kp + k]);
+      for (int i = 0; i < N; ++i) {
+        const double xn = fma(static_cast<double>(om), static_cast<double>(d[i]), x[i * Kp + k]);
+        out[i * Kp + k] = xn;
+        d[i] = static_cast<float>(xn);
+      }
     } else {  // Chebyshev step: out (holding x_{k-1}, or 0) <- x + a P^-1 r + beta (x - x_{k-1})
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         const double xi = x[i * Kp + k], xp = prev_zero ? 0.0 : out[i * Kp + k];
-        out[i * Kp + k] = fma(static_cast<double>(om), static_cast<double>(d[i]), fma(cheb_beta, xi - xp, xi));
+        const double xn = fma(static_cast<double>(om), static_cast<double>(d[i]), fma(cheb_beta, xi - xp, xi));
+        out[i * Kp + k] = xn;
+        d[i] = static_cast<float>(xn);
+      }
+    }
+    if constexpr (std::is_same<TT, float>::value && P >= kTraceMinP) {
+      // the new x at the edge points, for the next sweep's stage 1 and stage 2 (the other
+      // trace buffer: neighbours still read this sweep's)
+      if (xtr_out) {
+#pragma unroll 1
+        for (int n = 0; n < 3; ++n) {
+          float2 z[QF / 2];
+#pragma unroll
+          for (int c = 0; c < QF / 2; ++c) z[c] = f2(0.f);
+          const float* pT = s_R + RC::kPeT + n * N * QF;
+#pragma unroll
+          for (int j = 0; j < N; ++j) rank_acc<QF>(pT + j * QF, d[j], z);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) xtr_out[(n * Q + q) * Kp + k] = (q & 1) ? z[q / 2].y : z[q / 2].x;
+        }
       }
     }
   }
@@ -729,18 +775,29 @@ void smooth_pack_e(Handle& h) {
   ++h.launches;
 }
 
-void smooth_stage1(Handle& h, const double* x, int k0, int k1) {
+// Trace buffers of a single-rank level (tr32): x traces A | u traces | x traces B,
+// 3 Q planes each.  h.xtr_cur selects the x-trace buffer that belongs to the
+// vector stage 1 is given; a MODE 1 stage 2 writes the other one and flips.
+void smooth_stage1(Handle& h, const double* x, int k0, int k1, bool chained) {
   if (k1 < 0) k1 = h.K;
   if (k1 <= k0) return;
   const unsigned grid = grid_of(k1 - k0, 128);
 #define CALL(P)                                                                                               \
   do {                                                                                                        \
-    if (h.tz32.ptr)                                                                                           \
-      launch_pdl(k_s1f<P, float>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz32.ptr,         \
-                 P >= kTraceMinP ? h.tr32.ptr : nullptr, k0, k1);                                                                                         \
-    else                                                                                                      \
-      launch_pdl(k_s1f<P, double>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr,          \
-                 static_cast<float*>(nullptr), k0, k1);                                                       \
+    if (h.tz32.ptr) {                                                                                         \
+      const long planes = 3L * RankCfg<P>::Q * h.Kp;                                                          \
+      float* xt = (P >= kTraceMinP && h.tr32.ptr) ? h.tr32.ptr + (h.xtr_cur ? 2 * planes : 0) : nullptr;      \
+      const long uoff = h.xtr_cur ? -planes : planes;                                                         \
+      if (chained && xt)                                                                                      \
+        launch_pdl(k_s1f<P, float, true>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz32.ptr, \
+                   xt, uoff, k0, k1);                                                                         \
+      else                                                                                                    \
+        launch_pdl(k_s1f<P, float, false>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x,            \
+                   h.tz32.ptr, xt, uoff, k0, k1);                                                             \
+    } else {                                                                                                  \
+      launch_pdl(k_s1f<P, double, false>, grid, 128, s1_smem<P>(), h.stream, h.mesh(), h.dtab, x, h.tz.ptr,   \
+                 static_cast<float*>(nullptr), 0L, k0, k1);                                                   \
+    }                                                                                                         \
   } while (0)
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
@@ -755,10 +812,18 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
   if (k1 < 0) k1 = h.K;
   if (k1 <= k0) return;
   const unsigned grid = grid_of(k1 - k0, 128);
+  bool traced = false;
 #define LAUNCH(P, M, TT, TZ)                                                                                      \
-  launch_pdl(k_s2f<P, M, uint2, uint2, TT>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, h.Eh.ptr,        \
-             h.Escale.ptr, h.D.ptr, x, TZ, b, wm, dteta, dt, h.Ph.ptr, h.Pscale.ptr, om, out, cheb_beta, prev_zero, \
-             k0, k1, (h.tz32.ptr && TZ == static_cast<const void*>(h.tz32.ptr)) ? h.tr32.ptr : nullptr, h.dtr32.ptr)
+  do {                                                                                                            \
+    const long planes = 3L * RankCfg<P>::Q * h.Kp;                                                                \
+    const bool trp = P >= kTraceMinP && h.tr32.ptr && static_cast<const void*>(TZ) == h.tz32.ptr;                 \
+    const float* xt = trp ? h.tr32.ptr + (h.xtr_cur ? 2 * planes : 0) : nullptr;                                  \
+    float* xo = (trp && M == 1) ? h.tr32.ptr + (h.xtr_cur ? 0 : 2 * planes) : nullptr;                            \
+    launch_pdl(k_s2f<P, M, uint2, uint2, TT>, grid, 128, s2_smem<P>(), h.stream, h.mesh(), h.dtab, h.Eh.ptr,      \
+               h.Escale.ptr, h.D.ptr, x, TZ, b, wm, dteta, dt, h.Ph.ptr, h.Pscale.ptr, om, out, cheb_beta,        \
+               prev_zero, k0, k1, xt, trp ? h.tr32.ptr + planes : nullptr, h.dtr32.ptr, xo);                      \
+    traced = xo != nullptr;                                                                                       \
+  } while (0)
 #define CALL(P)                                           \
   do {                                                    \
     if (mode == 0 && h.tz32.ptr)                          \
@@ -775,6 +840,7 @@ void smooth_stage2(Handle& h, int mode, const double* x, const double* b, double
 #undef LAUNCH
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
+  if (traced) h.xtr_cur ^= 1;  // the x traces of `out` are in the other buffer
 }
 
 void smooth_zero(Handle& h, const double* b, double omega, double* out) {

@@ -476,9 +476,9 @@ Tier tier(const Handle& L) {
   return level_is_small(L) ? kSmall : kMid;
 }
 
-void f_stage1(Handle& L, Vec x, int k0 = 0, int k1 = -1) {
+void f_stage1(Handle& L, Vec x, int k0 = 0, int k1 = -1, bool chained = false) {
   switch (tier(L)) {
-    case kBig: smooth_stage1(L, vp(L, x), k0, k1); break;
+    case kBig: smooth_stage1(L, vp(L, x), k0, k1, chained); break;
     case kMid: rows_stage1(L, nullptr, 0.0, vp(L, x), 1.0, L.tz.ptr); break;
     default: small_stage1(L, vp(L, x)); break;
   }
@@ -513,16 +513,18 @@ void f_zero(Handle& L, Vec b, Vec out) {
 bool ranged_level(Team& T, int l) { return tier(level_of(T.h0(), l)) == kBig; }
 
 // r = b - S_c x (fused levels)
-void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r) {
+// chained: x is the output of the sweep launched just before on this level
+// (its stage 2 left the x traces, ldg_smooth.cu)
+void residual_f(Team& T, int l, double wm, double dt, Vec b, Vec x, Vec r, bool chained = false) {
   const bool rg = ranged_level(T, l);
-  staged(T, l, x, 1, rg, [&](Handle& L, int k0, int k1) { f_stage1(L, x, k0, k1); });
+  staged(T, l, x, 1, rg, [&](Handle& L, int k0, int k1) { f_stage1(L, x, k0, k1, chained); });
   staged(T, l, kTz, 2, rg, [&](Handle& L, int k0, int k1) { f_stage2(L, 0, x, b, wm, dt, r, k0, k1); });
 }
 
 // xo = xi + omega P^-1 (b - S_c xi) (fused levels)
-void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo) {
+void sweep_f(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo, bool chained = false) {
   const bool rg = ranged_level(T, l);
-  staged(T, l, xi, 1, rg, [&](Handle& L, int k0, int k1) { f_stage1(L, xi, k0, k1); });
+  staged(T, l, xi, 1, rg, [&](Handle& L, int k0, int k1) { f_stage1(L, xi, k0, k1, chained); });
   staged(T, l, kTz, 2, rg, [&](Handle& L, int k0, int k1) { f_stage2(L, 1, xi, b, wm, dt, xo, k0, k1); });
 }
 
@@ -564,8 +566,8 @@ struct Cheb {
 };
 
 void sweep_cheb(Team& T, int l, double wm, double dt, Vec b, Vec xi, Vec xo, double alpha, double beta,
-                bool prev_zero) {
-  staged(T, l, xi, 1, true, [&](Handle& L, int k0, int k1) { f_stage1(L, xi, k0, k1); });
+                bool prev_zero, bool chained) {
+  staged(T, l, xi, 1, true, [&](Handle& L, int k0, int k1) { f_stage1(L, xi, k0, k1, chained); });
   staged(T, l, kTz, 2, true, [&](Handle& L, int k0, int k1) {
     smooth_stage2(L, 1, vp(L, xi), vp(L, b), wm, dt, alpha, vp(L, xo), beta, prev_zero ? 1 : 0, k0, k1);
   });
@@ -654,16 +656,16 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     each(T, l, [&](Handle& L) { smooth_zero(L, vp(L, b), a, vp(L, cur)); });
     for (int s = 0; s < pre_of(T.h0().p, l) - 1; ++s) {
       ch.step(s + 1, &a, &be);
-      sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, s == 0);
+      sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, s == 0, s > 0);
       cur = other(cur);
     }
-    residual_f(T, l, wm, dt, b, cur, kMgR);
+    residual_f(T, l, wm, dt, b, cur, kMgR, pre_of(T.h0().p, l) > 1);
     for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
     for (int s = 0; s < post_of(T.h0().p, l); ++s) {
       ch.step(s, &a, &be);
-      sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, false);
+      sweep_cheb(T, l, wm, dt, b, cur, other(cur), a, be, false, s > 0);
       cur = other(cur);
     }
     return;
@@ -674,16 +676,16 @@ void vcycle(Team& T, int l, bool f32, double wm, double dt, Vec b, Vec x) {
     each(T, l, [&](Handle& L) { f_zero(L, b, cur); });
     const int pre = coarsest ? sweeps : pre_of(T.h0().p, l) - 1;
     for (int s = 0; s < pre; ++s) {
-      sweep_f(T, l, wm, dt, b, cur, other(cur));
+      sweep_f(T, l, wm, dt, b, cur, other(cur), s > 0);
       cur = other(cur);
     }
     if (coarsest) return;
-    residual_f(T, l, wm, dt, b, cur, kMgR);
+    residual_f(T, l, wm, dt, b, cur, kMgR, pre > 0);
     for (auto& rp : T.ranks) mg_restrict(level_of(*rp, l), level_of(*rp, l + 1));
     vcycle(T, l + 1, f32, wm, dt, kMgB, kMgX);
     for (auto& rp : T.ranks) mg_prolong_add(level_of(*rp, l), level_of(*rp, l + 1), vp(level_of(*rp, l), cur));
     for (int s = 0; s < post_of(T.h0().p, l); ++s) {
-      sweep_f(T, l, wm, dt, b, cur, other(cur));
+      sweep_f(T, l, wm, dt, b, cur, other(cur), s > 0);
       cur = other(cur);
     }
     return;

@@ -10,7 +10,7 @@ for w in c2 ref_c2 c1 c3 c4 c5; do
 done
 cp $F/pytest_gpu.log $P/${R}_pytest_gpu_final.log
 cp $F/gpu.txt $P/${R}_gpu.txt
-for p in 4 2; do
+for p in 4 3 2; do
   if [ -f $F/launches_p$p.csv ]; then
     python scripts/ncu_summary.py $F/launches_p$p.csv > $P/${R}_launches_final_p${p}_summary.txt
     python scripts/ncu_by_grid.py $F/launches_p$p.csv > $P/${R}_launches_final_p${p}_by_grid.txt

@@ -69,9 +69,10 @@ def _run(rows_below: int, extra: dict | None = None) -> dict:
 
 
 @pytest.mark.parametrize("rows_below,extra", [(0, None), (1 << 30, None), (0, {"LDG_DENSE_MAX": "0"}),
-                                               (2048, {"LDG_SETUP_OVERLAP": "0", "LDG_EXTRAP": "0"})],
+                                               (2048, {"LDG_SETUP_OVERLAP": "0", "LDG_EXTRAP": "0"}),
+                                               (0, {"LDG_RANK_FORM": "0"})],
                          ids=["thread_kernels_fused_smoother", "row_kernels", "thread_kernels_smoothed_coarsest",
-                              "default_shapes_serial_setup_plain_start"])
+                              "default_shapes_serial_setup_plain_start", "thread_kernels_table_operator"])
 def test_kernel_shape(rows_below, extra):
     out = _run(rows_below, extra)
     for key, r in out.items():
@@ -88,3 +89,47 @@ def test_kernel_shape(rows_below, extra):
         # FP32-arithmetic fused smoother costs up to ~15% more iterations on the
         # jittered mixed-BC meshes, whose multigrid needs 80-200 iterations at 32^2
         assert it2 <= 1.25 * it3 + 3, (key, r)
+
+
+APPLY_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1408_3877_b200 as ld
+mixed = ld.ProblemSpec(d="base_d", f="base_f", c_d="base_c", g_n="base_gn", c0="base_c", eta=1.0,
+                       boundary={1: "D", 2: "N", 3: "N", 4: "D"})
+out = {}
+for p in range(5):
+    s = ld.LdgSystem.square(48, p, mixed, jitter=0.2, seed=3)
+    y0, _ = s.initial_state()
+    s.assemble(0.3)
+    rng = np.random.default_rng(p)
+    x = rng.standard_normal(y0.shape)
+    c = rng.standard_normal(y0.size // 3)
+    out[str(p)] = {"lhs": s.apply_lhs(0.05, x).tolist(), "schur": s.apply_schur(0.05, c).tolist()}
+    s.close()
+print("JSON" + json.dumps(out))
+"""
+
+
+def test_rank_form_operator_equals_table_operator():
+    """The Krylov operator and the residual-contract operator in rank-Qe edge form
+    (k_stage1r, k_stage2<RK>, k_full<RK>: the default for the library's own tensors)
+    against the N x N table kernels (LDG_RANK_FORM=0) on a jittered mixed-BC mesh
+    large enough for the thread-per-element kernels: same integrals, rounding only."""
+    import numpy as np
+
+    res = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, LDG_RANK_FORM=flag, LDG_ROWS_BELOW="0")
+        r = subprocess.run([sys.executable, "-c", APPLY_SCRIPT, ROOT], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        line = [l for l in r.stdout.splitlines() if l.startswith("JSON")][-1]
+        res[flag] = json.loads(line[4:])
+    for p in range(5):
+        for key in ("lhs", "schur"):
+            a, b = np.array(res["1"][str(p)][key]), np.array(res["0"][str(p)][key])
+            err = np.abs(a - b).max() / np.abs(b).max()
+            print("RESULT rank-vs-table", p, key, err)
+            assert err <= 1e-13, (p, key, err)
