@@ -89,6 +89,27 @@ __device__ __forceinline__ void row_fma(const S* row, S e, S* a) {
   }
 }
 
+// the same for the first `lim` entries only (compile-time after unrolling)
+template <typename S, int NJ>
+__device__ __forceinline__ void row_fma_lim(const S* row, S e, S* a, int lim) {
+  constexpr int VW = 16 / sizeof(S);
+#pragma unroll
+  for (int q = 0; q < NJ / VW; ++q) {
+    if (q * VW >= lim) continue;
+    if constexpr (sizeof(S) == 4) {
+      const float4 v = reinterpret_cast<const float4*>(row)[q];
+      if (4 * q < lim) a[4 * q] = fmaf(e, v.x, a[4 * q]);
+      if (4 * q + 1 < lim) a[4 * q + 1] = fmaf(e, v.y, a[4 * q + 1]);
+      if (4 * q + 2 < lim) a[4 * q + 2] = fmaf(e, v.z, a[4 * q + 2]);
+      if (4 * q + 3 < lim) a[4 * q + 3] = fmaf(e, v.w, a[4 * q + 3]);
+    } else {
+      const double2 v = reinterpret_cast<const double2*>(row)[q];
+      if (2 * q < lim) a[2 * q] = fma(e, v.x, a[2 * q]);
+      if (2 * q + 1 < lim) a[2 * q + 1] = fma(e, v.y, a[2 * q + 1]);
+    }
+  }
+}
+
 template <int P, typename S>
 struct BjacSmem {
   using C = Cfg<P>;
@@ -110,6 +131,7 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
   constexpr int VW = 16 / sizeof(S), NJ = (N + VW - 1) / VW * VW, TJ = N * NJ;
   __shared__ __align__(16) S s_tab[14 * TJ];
   __shared__ S s_piv[C::WARPS][C::EPW][2 * N + 2];
+  __shared__ __align__(16) S s_g2[9 * Q * NJ];  // bjG2 [n*3+np][q][jj], rows of NJ
   extern __shared__ __align__(16) unsigned char bjac_smem[];
   S* s_E = reinterpret_cast<S*>(bjac_smem);     // [EPB][EPAD]: E^1_kk | E^2_kk rows of the block's elements
   S* s_pe = s_E + C::EPB * SM::EPAD;            // U^t [n][q][N]
@@ -120,6 +142,10 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
   for (int x = threadIdx.x; x < 14 * TJ; x += blockDim.x) {
     const int t = x / TJ, q = (x % TJ) / NJ, jj = x % NJ;  // Tab_t[q][jj] = stored transpose [jj][q]
     s_tab[x] = jj < N ? static_cast<S>(T.base[T.tmH + t * NNP + jj * NP + q]) : S(0);
+  }
+  for (int x = threadIdx.x; x < 9 * Q * NJ; x += blockDim.x) {
+    const int eq = x / NJ, jj = x % NJ;
+    s_g2[x] = jj < N ? static_cast<S>(T.base[T.bjG2 + eq * N + jj]) : S(0);
   }
   for (int t = threadIdx.x; t < 3 * Q * N; t += blockDim.x) s_pe[t] = static_cast<S>(T.base[T.pe + t]);
   for (int t = threadIdx.x; t < 9 * Q * N; t += blockDim.x) s_pth[t] = static_cast<S>(T.base[T.pth + t]);
@@ -198,12 +224,30 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
       c2[t] = static_cast<S>(c2d[t]);
     }
     const S* erow = s_E + el * SM::EPAD + ir * N;
+    if (T.rank_ok) {
+      // h_hat(q, jj, m) = 0 unless deg phi_q > deg phi_jj (hierarchical basis): only the
+      // columns below the first function of degree deg(q) are touched (28 of 60 chunks at p = 4)
+#pragma unroll
+      for (int q = 1; q < N; ++q) {
+        const S e1 = erow[q];
+        const S e2 = erow[NN + q];
+        int dq = 0;
+        while ((dq + 1) * (dq + 2) / 2 <= q) ++dq;
+        const int lim = dq * (dq + 1) / 2;  // jj < lim
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const S e = c1[t] * e1 + c2[t] * e2;
+          row_fma_lim<S, NJ>(s_tab + t * TJ + q * NJ, e, a, lim);
+        }
+      }
+    }
 #pragma unroll 1
     for (int q = 0; q < N; ++q) {
       const S e1 = erow[q];
       const S e2 = erow[NN + q];
 #pragma unroll
       for (int t = 0; t < 5; ++t) {
+        if (t < 2 && T.rank_ok) continue;
         const S e = c1[t] * e1 + c2[t] * e2;
         row_fma<S, N, NJ>(s_tab + t * TJ + q * NJ, e, a);
       }
@@ -234,14 +278,11 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
         const S dv = __shfl_sync(gmask, dq, q, NG);
         aq[q] = static_cast<S>(kappa) * pe[q * N + ir] * s_we[q] * dv;
       }
-      const S* tab0 = s_tab + (5 + np * 3 + n) * TJ;
-#pragma unroll 1
-      for (int q2 = 0; q2 < N; ++q2) {
-        S e = 0;
+      // row i of E_{k,j} (M_j^-1 B_{j,k}) = sum_q aq[q] (V^t M^-1 B)[q][.]: the rank-Qe row
+      // space carried through the neighbour's block on the host (bjG2), Q row updates instead of N
+      const S* g2 = s_g2 + (n * 3 + np) * Q * NJ;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) e = fma(aq[q], pth[q * N + q2], e);
-        row_fma<S, N, NJ>(tab0 + q2 * NJ, e, a);
-      }
+      for (int q = 0; q < Q; ++q) row_fma<S, N, NJ>(g2 + q * NJ, aq[q], a);
     }
   }
   S v[N];  // row i of the augmented identity

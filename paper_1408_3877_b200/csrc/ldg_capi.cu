@@ -37,7 +37,7 @@ void init_handle_tables(Handle& h, int p) {
                      L.mhat,    L.minv, L.ghat, L.hhat, L.sdiag, L.soff, L.pe,   L.pth,      L.we,     L.pb,
                      L.sb,      L.wb,   L.total, L.mono, L.NP,  L.tH,   L.tSd,      L.tSo,    L.tM,
                      L.tMinv,   L.tmH,  L.tmSd, L.tmSo,  L.QP,  L.rank_ok ? 1 : 0, L.rkR, L.rkRm, L.rkT,
-                     L.rkV,     L.rkW,  L.rkEnd};
+                     L.rkV,     L.rkW,  L.rkEnd, L.bjG2};
   {
     const FTables F = build_f32_tables(h.tables);
     h.ftab.alloc(F.data.size(), &h.bytes);

@@ -45,6 +45,7 @@ struct DevTables {
   // rank-Qe edge block (TableLayout rkR..rkW), usable when rank_ok
   int QP, rank_ok;
   long rkR, rkRm, rkT, rkV, rkW, rkEnd;
+  long bjG2;  // block-Jacobi setup table (TableLayout::bjG2)
   // FP32 smoother tables (FTables in ldg_tables.hpp), offsets in floats
   const float* fbase;
   int NF;

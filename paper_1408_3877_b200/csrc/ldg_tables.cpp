@@ -360,6 +360,7 @@ HostTables build_tables(int p, const RefTensors* caller_rt) {
   L.rkV = take(9L * N * L.QP);
   L.rkW = take(L.QP);
   L.rkEnd = off;
+  L.bjG2 = take(9L * L.Qe * N);
   L.total = off;
   ht.data.assign(off, 0.0);
   double* d = ht.data.data();
@@ -444,6 +445,15 @@ HostTables build_tables(int p, const RefTensors* caller_rt) {
     for (int q = 0; q < L.Qe; ++q)
       for (int j = 0; j < N; ++j) d[L.rkV + (e * N + j) * L.QP + q] = d[L.pth + (e * L.Qe + q) * N + j];
   for (int q = 0; q < L.Qe; ++q) d[L.rkW + q] = exact.w[q];
+  for (int n = 0; n < 3; ++n)
+    for (int np = 0; np < 3; ++np)
+      for (int q = 0; q < L.Qe; ++q)
+        for (int j = 0; j < N; ++j) {
+          double s = 0.0;
+          for (int i = 0; i < N; ++i)  // (m_hat^-1 s_off(np, n))[i][j] = stored transpose at tmSo[(np, n)][j*NP + i]
+            s += d[L.pth + ((n * 3 + np) * L.Qe + q) * N + i] * d[L.tmSo + (np * 3 + n) * N * NP + j * NP + i];
+          d[L.bjG2 + ((n * 3 + np) * L.Qe + q) * N + j] = s;
+        }
   // do the caller's tensors have the structure the rank form assumes?
   {
     double dev = 0.0, ref = 0.0;

@@ -78,6 +78,9 @@ struct TableLayout {
   // the operator kernels may use the rank-Qe edge form and skip the zero
   // chunks of the derivative tables
   bool rank_ok = false;
+  // block-Jacobi setup (ldg_bjac.cu): bjG2[n*3+np][q][j] = sum_i pth_{n,np}[q][i] (m_hat^-1 s_off(np, n))[i][j],
+  // the row space of an off-diagonal E block (rank Qe) carried through the neighbour's M^-1 B block
+  long bjG2 = 0;
   long total = 0;
 };
 

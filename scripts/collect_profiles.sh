@@ -19,14 +19,12 @@ for p in 4 3 2; do
   fi
 done
 N=$F
-[ -f $F/ncu/full_p4.ncu-rep ] && N=$F/ncu
-if [ -f $N/full_p4.ncu-rep ]; then
-  python scripts/ncu_traffic.py $N/full_p4.ncu-rep $P/${R}_ncu_traffic.json 4 256 > $P/${R}_ncu_full_p4_traffic.txt
-  python scripts/ncu_table.py $N/full_p4.ncu-rep > $P/${R}_ncu_full_p4_table.txt
-  ncu -i $N/full_p4.ncu-rep --page details --print-summary per-kernel > $P/${R}_ncu_full_p4_details.txt 2>/dev/null || true
-fi
-if [ -f $N/full_p2.ncu-rep ]; then
-  python scripts/ncu_table.py $N/full_p2.ncu-rep > $P/${R}_ncu_full_p2_table.txt
-  ncu -i $N/full_p2.ncu-rep --page details --print-summary per-kernel > $P/${R}_ncu_full_p2_details.txt 2>/dev/null || true
-fi
+[ -d $F/ncu ] && N=$F/ncu
+# summaries written on the GPU box by scripts/gpu_ncu_full.sh
+for p in 4 2; do
+  [ -f $N/full_p${p}_table.txt ] && cp $N/full_p${p}_table.txt $P/${R}_ncu_full_p${p}_table.txt
+  [ -f $N/full_p${p}_details.txt ] && cp $N/full_p${p}_details.txt $P/${R}_ncu_full_p${p}_details.txt
+done
+[ -f $N/full_p4_traffic.txt ] && cp $N/full_p4_traffic.txt $P/${R}_ncu_full_p4_traffic.txt
+[ -f $N/ncu_traffic.json ] && cp $N/ncu_traffic.json $P/${R}_ncu_traffic.json
 ls -la $P | tail -30
