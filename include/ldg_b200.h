@@ -117,6 +117,15 @@ int ldg_reference_tensors(int n_local, double* m, double* h, double* g, double* 
 int ldg_set_reference_tensors(ldg_handle* h, const double* m, const double* hh, const double* g, const double* sd,
                               const double* so, const double* rd, const double* ro);
 
+/* Host-only: do these reference tensors (NULL, NULL, ...: the library's own)
+ * have the structure the rank-Q_e operator kernels assume -- s_diag /
+ * s_offdiag (reftensors.hpp:106-128) equal to the Q_e-point edge quadrature
+ * of the basis traces to 1e-13, h_hat (reftensors.hpp:76-84) zero unless
+ * deg phi_i > deg phi_j?  When not, the handle applies the operator from the
+ * N x N tables instead (same results, more work).  *supported = 1 / 0. */
+int ldg_rank_form_supported(int n_local, const double* m, const double* hh, const double* g, const double* sd,
+                            const double* so, int* supported);
+
 /* Selects the CUDA device used by handles created afterwards on this thread
  * (one process per GPU: the rank's local device). */
 int ldg_set_device(int device);

@@ -95,6 +95,7 @@ _lib = None
 # library exports exactly what include/ldg_b200.h declares.
 _SIGNATURES = {
     "ldg_reference_tensors": (C.c_int, [C.c_int] + [_dp] * 7),
+    "ldg_rank_form_supported": (C.c_int, [C.c_int] + [_dp] * 5 + [C.POINTER(C.c_int)]),
     "ldg_set_device": (C.c_int, [C.c_int]),
     "ldg_set_reference_tensors": (C.c_int, [_H] + [_dp] * 7),
     "ldg_create": (C.c_int, [_dp, C.c_int, _ip, C.c_int, _ip, C.c_int, C.POINTER(_Problem), C.POINTER(_H)]),
@@ -152,6 +153,21 @@ def load_library():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def rank_form_supported(n_local: int, tensors: dict | None = None) -> bool:
+    """Host-only: may the operator kernels use the rank-Q_e edge form with these reference
+    tensors (None: the library's own)?  See ldg_rank_form_supported in include/ldg_b200.h."""
+    lib = load_library()
+    ok = C.c_int(-1)
+    if tensors is None:
+        args = [None] * 5
+    else:
+        keep = [np.ascontiguousarray(tensors[k], dtype=np.float64).ravel() for k in ("m", "h", "g", "sd", "so")]
+        args = [a.ctypes.data_as(_dp) for a in keep]
+    rc = lib.ldg_rank_form_supported(int(n_local), *args, C.byref(ok))
+    _raise(rc, lib.ldg_last_error(None).decode())
+    return bool(ok.value)
 
 
 def reference_tensors(n_local: int) -> dict:

@@ -370,17 +370,17 @@ __global__ void __launch_bounds__(128) k_assemble(DevMesh m, DevTables T, const 
 // 30 (G) or 15 (R) independent accumulators per row instead of 2-5, and the
 // per-element constants (D_k, w_q d_h) live in shared memory (one conflict-free
 // 64-bit load per use) so the registers hold the accumulators.
-// -DLDG_ASM_THREADS_P4=n: CTA size of the row kernel at p = 4 (tuning builds)
-#ifndef LDG_ASM_THREADS_P4
-#define LDG_ASM_THREADS_P4 448
-#endif
-template <int P>
+// CTA size of the row kernel at p = 4: 384 threads (<= 168 registers, no spills) and, for
+// meshes that fit two rounds of 148 x 448 elements (the 256^2 level: 2.3 rounds of 384),
+// 448 threads at 128 registers (0.290 -> 0.261 ms at 256^2; at 1024^2, all blocks, the
+// 448-thread build was 7 % slower, so large meshes keep 384).
+template <int P, bool WIDE = false>
 struct Asm2 {
   static constexpr int N = Cfg<P>::N, Q = Cfg<P>::QE, NN = N * N;
   static constexpr int NP = (N % 2) ? N + 1 : N;  // padded table rows (16-byte aligned)
   // p = 4: one 384-thread CTA per SM (<= 168 registers, 12 warps; two
   // 128-thread CTAs were register- and shared-limited to 8); below, 128
-  static constexpr int kThreads = P == 4 ? LDG_ASM_THREADS_P4 : 128;
+  static constexpr int kThreads = P == 4 ? (WIDE ? 448 : 384) : 128;
   static constexpr int kMinBlocks = P == 4 ? 1 : 4;
   // shared: G [i][l][j][2] | pe [n][q][NP] | pth [n][np][q][NP] | we [Q] (even) | per-thread [N + 3Q][T]
   static constexpr int kG = 2 * N * NN, kPe = 3 * Q * NP, kPth = 9 * Q * NP, kWe = (Q + 1) / 2 * 2;
@@ -402,12 +402,12 @@ __device__ __forceinline__ void row_axpy(double a, const double* row, double* ac
   if (N & 1) acc[N - 1] = fma(a, row[N - 1], acc[N - 1]);
 }
 
-template <int P, int MODE>
+template <int P, int MODE, bool WIDE>
 __device__ __forceinline__ void assemble_rows_element(const DevMesh& m, const double* __restrict__ D,
                                                       double* __restrict__ out, const double* s_g,
                                                       const double* s_pe, const double* s_pth,
                                                       const double* s_we, double* per, int k) {
-  using A = Asm2<P>;
+  using A = Asm2<P, WIDE>;
   constexpr int N = A::N, Q = A::Q, NN = A::NN, NP = A::NP;
   constexpr bool kDiagOnly = MODE == kModeEdiag;
   const long Kp = m.Kp;
@@ -541,11 +541,11 @@ __device__ __forceinline__ void assemble_rows_element(const DevMesh& m, const do
 // blocks of kThreads elements, so the ~65 KB of tables are staged once per
 // CTA (staged per 128 elements they cost ~15 % of the run in exposed L2
 // latency at p = 4).
-template <int P, int MODE>
-__global__ void __launch_bounds__(Asm2<P>::kThreads, Asm2<P>::kMinBlocks) k_assemble_rows(DevMesh m, DevTables T,
+template <int P, int MODE, bool WIDE>
+__global__ void __launch_bounds__(Asm2<P, WIDE>::kThreads, Asm2<P, WIDE>::kMinBlocks) k_assemble_rows(DevMesh m, DevTables T,
                                                                         const double* __restrict__ D,
                                                                         double* __restrict__ out) {
-  using A = Asm2<P>;
+  using A = Asm2<P, WIDE>;
   constexpr int N = A::N, Q = A::Q, NP = A::NP;
   extern __shared__ __align__(16) double sm[];
   double* s_g = sm;                 // [i][l][j][m]
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(Asm2<P>::kThreads, Asm2<P>::kMinBlocks) k_asse
   const int tid = threadIdx.x;
   double* per = s_per + tid;
   for (int k = blockIdx.x * blockDim.x + tid; k - tid < m.K; k += gridDim.x * blockDim.x) {
-    if (k < m.K) assemble_rows_element<P, MODE>(m, D, out, s_g, s_pe, s_pth, s_we, per, k);
+    if (k < m.K) assemble_rows_element<P, MODE, WIDE>(m, D, out, s_g, s_pe, s_pth, s_we, per, k);
   }
 }
 
@@ -668,29 +668,39 @@ bool asm_v1(int p) {
   return env < 0 ? p < 4 : env != 0;
 }
 
+template <int P, int MODE, bool WIDE>
+void launch_assemble_rows(Handle& h, double* out, int sms) {
+  using A = Asm2<P, WIDE>;
+  const size_t smem = A::smem();
+  auto kern = k_assemble_rows<P, MODE, WIDE>;
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    int per_sm = 0;
+    LDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    LDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, A::kThreads, smem));
+    grid_cap = std::max(1, sms * per_sm);
+  }
+  const unsigned grid = std::min<unsigned>(grid_of(h.K, A::kThreads), static_cast<unsigned>(grid_cap));
+  kern<<<grid, A::kThreads, smem, h.stream>>>(h.mesh(), h.dtab, h.D.ptr, out);
+  LDG_CUDA(cudaGetLastError());
+  ++h.launches;
+}
+
 template <int P, int MODE>
 void launch_assemble_p(Handle& h, double* out) {
   if constexpr (MODE == kModeE || MODE == kModeEdiag) {
     if (!asm_v1(P)) {
-      const size_t smem = Asm2<P>::smem();
-      auto kern = k_assemble_rows<P, MODE>;
-      static bool configured2 = false;
-      if (!configured2) {
-        LDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured2 = true;
-      }
-      static int grid_cap = 0;
-      if (!grid_cap) {
-        int dev = 0, sms = 0, per_sm = 0;
+      // the wide CTA when the mesh fits two rounds of it on the SMs (Asm2)
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
         LDG_CUDA(cudaGetDevice(&dev));
         LDG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        LDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Asm2<P>::kThreads, smem));
-        grid_cap = std::max(1, sms * per_sm);
       }
-      const unsigned grid = std::min<unsigned>(grid_of(h.K, Asm2<P>::kThreads), static_cast<unsigned>(grid_cap));
-      kern<<<grid, Asm2<P>::kThreads, smem, h.stream>>>(h.mesh(), h.dtab, h.D.ptr, out);
-      LDG_CUDA(cudaGetLastError());
-      ++h.launches;
+      if (P == 4 && h.K <= 2L * sms * Asm2<P, true>::kThreads && h.K > 2L * sms * Asm2<P, false>::kThreads)
+        launch_assemble_rows<P, MODE, true>(h, out, sms);
+      else
+        launch_assemble_rows<P, MODE, false>(h, out, sms);
       return;
     }
   }

@@ -550,6 +550,31 @@ int ldg_reference_tensors(int n_local, double* m, double* h, double* g, double* 
   });
 }
 
+int ldg_rank_form_supported(int n_local, const double* m, const double* hh, const double* g, const double* sd,
+                            const double* so, int* supported) {
+  if (!supported) return LDG_EINVAL;
+  return guarded(nullptr, [&] {
+    int p = -1;
+    for (int q = 0; q <= 4; ++q)
+      if ((q + 1) * (q + 2) / 2 == n_local) p = q;
+    if (p < 0) throw Error(LDG_EINVAL, "unsupported number of local basis functions");
+    if (!m && !hh && !g && !sd && !so) {
+      *supported = ldgb::build_tables(p).lay.rank_ok ? 1 : 0;
+      return;
+    }
+    if (!m || !hh || !g || !sd || !so) throw Error(LDG_EINVAL, "all of m, h, g, sd, so or none");
+    const size_t n2 = static_cast<size_t>(n_local) * n_local, n3 = n2 * n_local;
+    ldgb::RefTensors rt;
+    rt.n = n_local;
+    rt.m.assign(m, m + n2);
+    rt.h.assign(hh, hh + 2 * n2);
+    rt.g.assign(g, g + 2 * n3);
+    rt.sd.assign(sd, sd + 3 * n2);
+    rt.so.assign(so, so + 9 * n2);
+    *supported = ldgb::build_tables(p, &rt).lay.rank_ok ? 1 : 0;
+  });
+}
+
 int ldg_set_reference_tensors(ldg_handle* H, const double* m, const double* hh, const double* g, const double* sd,
                               const double* so, const double* rd, const double* ro) {
   if (!H || !m || !hh || !g || !sd || !so) return LDG_EINVAL;
@@ -577,6 +602,14 @@ int ldg_set_reference_tensors(ldg_handle* H, const double* m, const double* hh, 
                           cudaMemcpyHostToDevice));
       const ldgb::FTables F = ldgb::build_f32_tables(h.tables);
       LDG_CUDA(cudaMemcpy(h.ftab.ptr, F.data.data(), sizeof(float) * F.data.size(), cudaMemcpyHostToDevice));
+      // may the operator kernels use the rank-Qe edge form with these tensors?  (kernel
+      // choice is baked into the captured V-cycles: drop them)
+      const int ok = h.tables.lay.rank_ok ? 1 : 0;
+      h.dtab.rank_ok = ok;
+      for (auto& c : h.coarse)
+        if (c && c->p == h.p) c->dtab.rank_ok = ok;
+      if (h.replica && h.replica->p == h.p) h.replica->dtab.rank_ok = ok;
+      ldgb::mg_release(h);
       h.assembled = false;
     }
   });

@@ -96,3 +96,22 @@ def test_cpp_host_mirror_fails_loudly_without_gpu():
     r = subprocess.run([SIM, "4", "1", "2"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 1
     assert "no CPU fallback" in r.stderr
+
+
+@pytest.mark.parametrize("n", [1, 3, 6, 10, 15])
+def test_rank_form_guard(n):
+    """The rank-Q_e operator kernels are used only for tensors with the structure they
+    assume (ldg_rank_form_supported, host-only): the library's own tensors have it, the
+    reference's (golden) tensors have it, tensors with a perturbed s_offdiag or a filled
+    upper part of h_hat do not."""
+    import paper_1408_3877_b200 as ld
+
+    assert ld.rank_form_supported(n)
+    t = ld.reference_tensors(n)
+    assert ld.rank_form_supported(n, t)
+    bad = {k: v.copy() for k, v in t.items()}
+    bad["so"][0] += 1e-9
+    assert not ld.rank_form_supported(n, bad)
+    bad = {k: v.copy() for k, v in t.items()}
+    bad["h"].reshape(n, n, 2)[0, n - 1, 0] += 1e-9  # deg(phi_0) = 0 <= deg(phi_{n-1})
+    assert not ld.rank_form_supported(n, bad)

@@ -320,3 +320,36 @@ def test_write_vtu_restatement_matches_reference(h_max, m, tmp_path):
     a = R.write_vtu(h_max, lag, "c", str(tmp_path / "ref"), 2)
     b = O.write_vtu(mesh, lag, "c", str(tmp_path / "ora"), 2)
     assert open(a).read() == open(b).read()
+
+
+@pytest.mark.parametrize("p", range(5))
+def test_edge_tensors_are_rank_qe_quadrature_sums(p):
+    """The identities behind the rank-Q_e operator and smoother kernels,
+    on the restated reference tensors (pinned to the reference's above): with the
+    Q_e = (3p + 2) // 2 point Gauss rule on the edge, U_n[q, i] = phi_i(gamma_n(s_q)) and
+    V_{n,np}[q, j] = phi_j(theta_{n,np}(gamma_n(s_q))),
+        s_diag[:, :, n] = U_n^T W U_n,   s_offdiag[:, :, n, np] = U_n^T W V_{n,np},
+    the neighbour's trace points are this element's in reverse order, and h_hat[i, j, m]
+    vanishes unless deg phi_i > deg phi_j (hierarchical modal basis)."""
+    n = O.local_dof_count(p)
+    rt = O.build_ref_tensors(n)
+    q = (3 * p + 2) // 2
+    s, w = O.gauss_legendre_unit(q)
+    assert np.allclose(s[::-1], 1.0 - s, atol=1e-15)
+    tol = 1e-13 * max(1.0, np.abs(rt.s_diag).max())
+    for nm in range(1, 4):
+        g = O.gamma_map(nm, s)
+        U = O.phi_table(n, g[:, 0], g[:, 1])
+        assert np.abs(np.einsum("r,ri,rj->ij", w, U, U) - rt.s_diag[:, :, nm - 1]).max() <= tol
+        for np_ in range(1, 4):
+            th = O.theta_map(nm, np_, g)
+            V = O.phi_table(n, th[:, 0], th[:, 1])
+            assert np.abs(np.einsum("r,ri,rj->ij", w, U, V) - rt.s_offdiag[:, :, nm - 1, np_ - 1]).max() <= tol
+            # the same physical points seen from the neighbour's edge np, reversed
+            gn = O.gamma_map(np_, s[::-1])
+            assert np.abs(O.phi_table(n, gn[:, 0], gn[:, 1]) - V).max() <= tol
+    deg = [d for d in range(p + 1) for _ in range(d + 1)]
+    for i in range(n):
+        for j in range(n):
+            if deg[i] <= deg[j]:
+                assert np.abs(rt.h_hat[i, j, :]).max() <= tol, (i, j)
