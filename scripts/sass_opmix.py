@@ -8,7 +8,8 @@ import sys
 
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1408_3877_b200/libldg_b200.so"
 HOT = ["k_s2f<4, 1, uint2, uint2, float>", "k_s2f<3, 1, uint2, uint2, float>", "k_s2f<2, 1, uint2, uint2, float>",
-       "k_s1f<4, float>", "k_s1f<3, float>", "k_stage1<4", "k_stage2<4", "k_full<4",
+       "k_s1f<4, float, false>", "k_s1f<4, float, true>", "k_s1f<3, float, true>", "k_stage1r<4", "k_stage1m<4",
+       "k_stage2<4, true>", "k_stage2<4, false>", "k_full<4, true>",
        "k_assemble_rows<4, 4", "k_assemble_rows<4, 0", "k_bjac_warp<4, 3", "k_dense_gemv", "k_mdot_flat"]
 OPS = ["DFMA", "DMUL", "DADD", "FFMA2", "FFMA", "FMUL2", "HFMA2", "HADD2", "F2F", "LDG.E.128", "LDG.E.64",
        "LDG.E.CONSTANT.128", "LDG.E", "LDS.128", "LDS.64", "LDS", "STG.E.128", "STG.E.64", "STG.E", "SHFL",
