@@ -790,7 +790,13 @@ int prepare_precond(Team& T, int pc, double wm, double dt, bool* f32) {
       // Krylov loop waits for both (join_precond)
       Handle& h = T.h0();
       if (!T.setup_stream[0]) {
-        for (auto& st : T.setup_stream) LDG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        // the coarse levels' chain of small latency-bound kernels gets the higher priority:
+        // its CTAs take the SM slots the 8192-CTA block-Jacobi kernel of level 0 frees
+        int least = 0, greatest = 0;
+        LDG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        const int coarse_prio = env_or("LDG_SETUP_PRIO", 1) != 0 ? greatest : least;
+        LDG_CUDA(cudaStreamCreateWithPriority(&T.setup_stream[0], cudaStreamNonBlocking, least));
+        LDG_CUDA(cudaStreamCreateWithPriority(&T.setup_stream[1], cudaStreamNonBlocking, coarse_prio));
         for (auto& e : T.setup_ev) LDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
       LDG_CUDA(cudaEventRecord(T.setup_ev[0], T.stream));
