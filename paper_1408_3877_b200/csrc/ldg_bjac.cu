@@ -121,7 +121,8 @@ struct BjacSmem {
 template <int P, int OUT, typename S = double>
 __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const double* __restrict__ E,
                                                    const double* __restrict__ E_D, double wm, double dt, double eta,
-                                                   void* __restrict__ out, float* __restrict__ out_scale) {
+                                                   void* __restrict__ out, float* __restrict__ out_scale,
+                                                   uint2* __restrict__ Eq, float* __restrict__ Escale) {
   using C = Cfg<P>;
   using SM = BjacSmem<P, S>;
   constexpr int N = C::N, NN = C::NN, NP = C::NP, NNP = C::NNP, NG = C::NG, Q = C::Q;
@@ -168,6 +169,59 @@ __global__ void __launch_bounds__(256) k_bjac_warp(DevMesh m, DevTables T, const
     }
   }
   __syncthreads();
+  if constexpr (OUT == 3) {
+    // The smoother's FP16 copy of the diagonal E blocks (ldg_pack.cuh quads, scaled per
+    // element into [-1, 1]) leaves from the staged block: the same values the separate
+    // packing kernel produced from a second and third pass over E (k_pack_eh: 183 us at
+    // p = 4, 256^2), written as coalesced 8-byte stores, 16+ consecutive elements per plane.
+    if (Eq) {
+      using PC = SmCfg<P>;
+      __shared__ float s_sc[C::EPB];
+      constexpr int LPE = 256 / C::EPB;  // lanes per element (1 .. 16), consecutive threads
+      {
+        const int e = threadIdx.x / LPE, l = threadIdx.x % LPE;
+        float mx = 0.f;
+        for (int v = l; v < 2 * NN; v += LPE) mx = fmaxf(mx, fabsf(static_cast<float>(s_E[e * SM::EPAD + v])));
+#pragma unroll
+        for (int o = LPE / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (l == 0) {
+          const float sc = mx > 0.f ? mx : 1.0f;
+          s_sc[e] = sc;
+          if (kb + e < m.K) Escale[kb + e] = sc;
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < 2 * PC::QP * C::EPB; t += 256) {
+        const int plane = t / C::EPB, e = t % C::EPB, ke = kb + e;
+        if (ke >= m.K) continue;
+        const int c = plane / PC::QP, q = plane % PC::QP;
+        const float inv = 1.0f / s_sc[e];
+        __half hv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int v = 4 * q + r;
+          int ii, jj;
+          bool ok;
+          if constexpr (PC::kFlat) {
+            jj = v / N;
+            ii = v % N;
+            ok = v < NN;
+          } else {
+            const int gq = v / (PC::QC * 4), w = v % (PC::QC * 4);
+            jj = gq * PC::CC + w / N;
+            ii = w % N;
+            ok = jj < N;
+          }
+          const float val = ok ? static_cast<float>(s_E[e * SM::EPAD + c * NN + ii * N + jj]) : 0.0f;
+          hv[r] = __float2half_rn(val * inv);
+        }
+        uint2 u;
+        u.x = static_cast<unsigned>(__half_as_ushort(hv[0])) | (static_cast<unsigned>(__half_as_ushort(hv[1])) << 16);
+        u.y = static_cast<unsigned>(__half_as_ushort(hv[2])) | (static_cast<unsigned>(__half_as_ushort(hv[3])) << 16);
+        Eq[(static_cast<long>(c) * PC::QP + q) * Kp + ke] = u;
+      }
+    }
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / NG, i = lane % NG;
   const int el = warp * C::EPW + sub;
@@ -370,13 +424,14 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
               : out_kind == 1 ? static_cast<void*>(h.Pinv32.ptr)
                               : static_cast<void*>(h.Ph.ptr);
   float* sc = out_kind == 3 ? h.Pscale.ptr : nullptr;
+  if (out_kind == 3) smooth_pack_alloc(h);  // the kind-3 kernel also writes the FP16 copy of E
 #define LAUNCH(P, O)                                                                                          \
   do {                                                                                                        \
     const size_t smem = BjacSmem<P, double>::bytes(); /* + static: always opt in beyond 48 KB */             \
     LDG_CUDA(cudaFuncSetAttribute(k_bjac_warp<P, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
                                     static_cast<int>(smem)));                                                 \
     k_bjac_warp<P, O><<<grid, 256, smem, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt, h.prob.eta, out, \
-                                                      sc);                                                    \
+                                                      sc, nullptr, nullptr);                                  \
   } while (0)
 #define LAUNCH32(P, O)                                                                                        \
   do {                                                                                                        \
@@ -384,7 +439,7 @@ void launch_bjac(Handle& h, double wm, double dt, int out_kind) {
     LDG_CUDA(cudaFuncSetAttribute(k_bjac_warp<P, O, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                     static_cast<int>(smem)));                                                 \
     k_bjac_warp<P, O, float><<<grid, 256, smem, h.stream>>>(h.mesh(), h.dtab, h.E.ptr, h.D.ptr, wm, dt,       \
-                                                             h.prob.eta, out, sc);                            \
+                                                             h.prob.eta, out, sc, h.Eh.ptr, h.Escale.ptr);    \
   } while (0)
 #define CALL(P)                                                      \
   do {                                                               \

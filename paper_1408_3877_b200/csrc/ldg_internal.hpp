@@ -349,7 +349,8 @@ bool level_is_small(const Handle& h);
 
 // fused mixed-precision smoother (ldg_smooth.cu)
 long packed_p_quads(int p);                                           // float4 quads of one packed P^-1 block
-void smooth_pack_e(Handle& h);                                        // Eh (FP16 packed) from E
+void smooth_pack_alloc(Handle& h);  // Eh / Escale of the level (filled by launch_bjac, kind 3)
+void smooth_dtraces(Handle& h);     // d_h at the edge points for the trace-form smoother
 // chained: x is the output of the preceding smooth_stage2 (mode 1) launch on this level
 void smooth_stage1(Handle& h, const double* x, int k0 = 0, int k1 = -1, bool chained = false);  // tz = M^-1 B x (FP32 arithmetic)
 // mode 0: out = b - S_c x;  mode 1: out = x + omega P^-1 (b - S_c x)

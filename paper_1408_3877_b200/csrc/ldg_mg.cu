@@ -513,8 +513,8 @@ void mg_setup_f32_level(Handle& L, double wm, double dt) {
       L.Ph.alloc(packed_p_quads(L.p) * L.Kp, &L.bytes);
       L.Pscale.alloc(L.Kp, &L.bytes);
     }
-    launch_bjac(L, wm, dt, 3);
-    smooth_pack_e(L);
+    launch_bjac(L, wm, dt, 3);  // also writes the FP16 copy of E (Eh, Escale) from its staged blocks
+    smooth_dtraces(L);
   } else {
     if (!L.E32.ptr) {
       L.E32.alloc(2 * NN * L.Kp, &L.bytes);

@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(128) k_dtrace(long Kp, int Kg, const float* __
 }
 
 // A quad of the packed stream: float4 (FP32 copy) or four FP16 values in a
-// uint2 (E scaled per element into [-1, 1], ldg_smooth.cu k_pack_e)
+// uint2 (E scaled per element into [-1, 1], written by k_bjac_warp, ldg_bjac.cu)
 __device__ __forceinline__ float4 ld_quad(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ float4 ld_quad(const uint2* p) {
   const uint2 u = __ldcs(p);
@@ -678,56 +678,6 @@ __global__ void __launch_bounds__(128) k_bjf(int K, long Kp, const TP* __restric
   for (int i = 0; i < N; ++i) out[i * Kp + k] = static_cast<double>(om * d[i]);
 }
 
-// FP16 packed copy of the diagonal blocks E[(c*NN + i*N + j)][k] (FP64),
-// one thread per element: pass 1 the element's scale max |E| over its two
-// blocks, pass 2 the quads of ldg_pack.cuh (slot v -> (i, j), zero padding)
-// as 8-byte stores, each pass a coalesced sweep over the 2 N^2 planes.
-// (Was two kernels, a per-element max and one thread per FP16 value with
-// 2-byte scattered stores: 68 + 264 us at p = 4, 256^2.)
-template <int P>
-__global__ void __launch_bounds__(128) k_pack_eh(long Kp, const double* __restrict__ E, float* __restrict__ scale,
-                                                 uint2* __restrict__ Eq) {
-  using C = Cfg<P>;
-  constexpr int N = C::N, NN = C::NN;
-  const long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-  if (k >= Kp) return;
-  double mx = 0.0;
-#pragma unroll 8
-  for (int v = 0; v < 2 * NN; ++v) mx = fmax(mx, fabs(E[v * Kp + k]));
-  const float sc = mx > 0.0 ? static_cast<float>(mx) : 1.0f;
-  scale[k] = sc;
-  const float inv = 1.0f / sc;
-#pragma unroll 1
-  for (int c = 0; c < 2; ++c) {
-#pragma unroll 4
-    for (int q = 0; q < C::QP; ++q) {
-      __half hv[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int v = 4 * q + r;
-        int i, j;
-        bool ok;
-        if constexpr (C::kFlat) {
-          j = v / N;
-          i = v % N;
-          ok = v < NN;
-        } else {
-          const int g = v / (C::QC * 4), w = v % (C::QC * 4);
-          j = g * C::CC + w / N;
-          i = w % N;
-          ok = j < N;
-        }
-        const float val = ok ? static_cast<float>(E[(static_cast<long>(c) * NN + i * N + j) * Kp + k]) : 0.0f;
-        hv[r] = __float2half_rn(val * inv);
-      }
-      uint2 u;
-      u.x = static_cast<unsigned>(__half_as_ushort(hv[0])) | (static_cast<unsigned>(__half_as_ushort(hv[1])) << 16);
-      u.y = static_cast<unsigned>(__half_as_ushort(hv[2])) | (static_cast<unsigned>(__half_as_ushort(hv[3])) << 16);
-      Eq[(static_cast<long>(c) * C::QP + q) * Kp + k] = u;
-    }
-  }
-}
-
 template <int P>
 size_t s1_smem() {
   return sizeof(float) * (2 * Cfg<P>::N * Cfg<P>::NF + RankCfg<P>::kFloats);
@@ -751,18 +701,21 @@ long packed_p_quads(int p) {
   }
 }
 
-// FP16 copy of the level's diagonal E blocks for the big-level smoother,
-// scaled per element into [-1, 1] (half the bytes of FP32 in the HBM-bound
-// stage 2; FP32 copies measured slower in round 1 at equal iterations)
-void smooth_pack_e(Handle& h) {
+// Buffers of the FP16 copy of the level's diagonal E blocks for the big-level
+// smoother, scaled per element into [-1, 1] (half the bytes of FP32 in the
+// HBM-bound stage 2; FP32 copies measured slower in round 1 at equal iterations)
+void smooth_pack_alloc(Handle& h) {
+  if (h.Eh.ptr) return;
+  h.Eh.alloc(2L * packed_p_quads(h.p) * h.Kp, &h.bytes);
+  h.Escale.alloc(h.Kp, &h.bytes);
+}
+
+// d_h at the edge points for the trace-form smoother (per step; the FP16 copy of E
+// itself, Eh / Escale, is written by the block-Jacobi setup from its staged blocks,
+// ldg_bjac.cu)
+void smooth_dtraces(Handle& h) {
 #define CALL(P)                                                                                          \
   do {                                                                                                   \
-    const long nq = 2L * Cfg<P>::QP * h.Kp;                                                              \
-    if (!h.Eh.ptr) {                                                                                     \
-      h.Eh.alloc(nq, &h.bytes);                                                                          \
-      h.Escale.alloc(h.Kp, &h.bytes);                                                                    \
-    }                                                                                                    \
-    k_pack_eh<P><<<grid_of(h.Kp, 128), 128, 0, h.stream>>>(h.Kp, h.E.ptr, h.Escale.ptr, h.Eh.ptr);       \
     if (h.dtr32.ptr && P >= kTraceMinP) {                                                                \
       k_dtrace<P><<<grid_of(h.Kg, 128), 128, 0, h.stream>>>(h.Kp, h.Kg, h.dtab.fbase + h.dtab.fR, h.D.ptr, \
                                                             h.dtr32.ptr);                                \
@@ -772,7 +725,6 @@ void smooth_pack_e(Handle& h) {
   LDG_DISPATCH_P(h.p, CALL)
 #undef CALL
   LDG_CUDA(cudaGetLastError());
-  ++h.launches;
 }
 
 // Trace buffers of a single-rank level (tr32): x traces A | u traces | x traces B,

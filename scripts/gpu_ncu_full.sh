@@ -7,7 +7,7 @@ O=gpurun_out/${1:-ncu_full}
 mkdir -p $O
 timeout 600 python scripts/profile_step.py --p 4 --dim 256 --warmup 5 > $O/plain_p4.log 2>&1 || { echo "plain p4 failed" >> $O/rc.txt; exit 1; }
 timeout 1800 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:k_s2f<\(int\)4, \(int\)1|k_s1f<\(int\)4|k_stage2<\(int\)4|k_stage1<\(int\)4|k_stage1r<\(int\)4|k_dtrace<\(int\)4|k_bjac_warp<\(int\)4|k_assemble_rows<\(int\)4|k_full<\(int\)4|k_pack_eh<\(int\)4" -c 20 -f -o $O/full_p4 \
+  -k "regex:k_s2f<\(int\)4, \(int\)1|k_s1f<\(int\)4|k_stage2<\(int\)4|k_stage1<\(int\)4|k_stage1r<\(int\)4|k_dtrace<\(int\)4|k_bjac_warp<\(int\)4|k_assemble_rows<\(int\)4|k_full<\(int\)4" -c 20 -f -o $O/full_p4 \
   python scripts/profile_step.py --p 4 --dim 256 --warmup 5 > $O/ncu_full_p4.log 2>&1
 echo "full p4 rc $?" >> $O/rc.txt
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
