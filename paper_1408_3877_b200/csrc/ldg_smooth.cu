@@ -7,16 +7,17 @@
 // copies; vectors stay FP64 and the outer Krylov operator is untouched, so
 // only the preconditioner's contraction depends on the rounding.
 //
-//  * Stored blocks are packed per element and streamed as float4: Eq[c][q][k]
-//    holds values 4q..4q+3 of component c's four blocks in (slot, column, row)
-//    order, so a warp moves 512 contiguous bytes per load instruction and the
-//    quarter as many load instructions as the FP32 scalar layout issues.
-//    P^-1 is packed the same way (column-major, NN rounded up to 4).
+//  * The stored blocks (E^m_kk, P_k^-1) are FP16, scaled per element, packed
+//    four values to a 64-bit quad in the (column group, column, row) order of
+//    ldg_pack.cuh and streamed one quad plane at a time: a warp moves 256
+//    contiguous bytes per load instruction.
 //  * Stage 2 and the block-Jacobi update are one kernel: the residual of the
 //    element never leaves registers (ping-pong x_in -> x_out, since stage 2
 //    reads the neighbours' x).
-//  * The reference tables live in shared memory as FP32 rows of NF = N
-//    rounded to 4 (one 128-bit broadcast load per 4 entries).
+//  * Every edge term is applied in rank-Qe form from small shared-memory
+//    tables (RankCfg below); from p = 3 on stage 1 hands its projections to
+//    stage 2 as edge traces, and chained sweeps reuse the traces stage 2
+//    leaves of its output.
 //
 // Reference operators restated (as in ldg_apply.cu): B^m = -H^m + Q^m + Q_N^m
 // (assembly.hpp:92-109, 174-208), S + S_D (assembly.hpp:142-168), M = 2|T| mhat.
@@ -34,17 +35,15 @@
 
 // min resident CTAs per SM of the thread-per-element kernels, per degree
 // p = 0..4 (stage 1 | stage 2).  The level-0 grids are 1024 CTAs of 128
-// (256^2 FK): 7-8 CTAs/SM (<= 73 / 64 registers, a few spilled bytes) run
-// them in one wave: V-cycle -13% at p = 2 and -14% at p = 3 (stage 2 at 7,
-// stage 1 at 8: 0.515 / 0.764 ms against 0.600 / 0.883 ms with 1 CTA).  At
-// p = 4 stage 2 at 7 CTAs (72 registers, 48 bytes spilled) runs the level in
-// one wave: V-cycle 1557 -> 1435 us, step 38.4 -> 36.2 ms (5 and 6 CTAs,
-// 96 / 80 registers without spills, stay at two waves and were 1-2 % slower
-// than 4; 8 CTAs spill more: +6 %).  Stage 1 at p = 4 stays at 4 CTAs: 6, 7,
-// 8 CTAs (also with one neighbour at a time, LDG_S1_SEQ_P) measured
-// +3 / +7 / +16 % V-cycle.  8 at p <= 1 measured slower.
-// -DLDG_MINB_S1=abcde / -DLDG_MINB_S2=abcde (one digit per p = 0..4)
-// override (tuning builds).
+// (256^2 FK): 7-8 CTAs/SM (<= 72 / 64 registers) run them in ONE wave, and
+// anything that takes stage 2 above one wave loses (round 2, p = 4, with the
+// trace-form kernel: two column groups in flight at 5 / 6 CTAs 86 / 100 us
+// per sweep against 76 at 7; 8 CTAs 84).  Stage 1 at p = 4 stays at 4 CTAs
+// (128 registers; 5 / 6 / 7 CTAs: sweep 81.7 / 85.2 / 77.4 us against 76.8,
+// chained or not), at p = 3 7 CTAs beat 8 (41.8 vs 45.1 us per sweep).  8 at
+// p <= 1 measured slower.
+// -DLDG_MINB_S1=abcde / -DLDG_MINB_S1C=abcde (chained sweeps) /
+// -DLDG_MINB_S2=abcde (one digit per p = 0..4) override (tuning builds).
 #ifndef LDG_MINB_S1
 #define LDG_MINB_S1 11874
 #endif
