@@ -1150,9 +1150,12 @@ int ldg_get_state(ldg_handle* H, double* y, double* t) {
 
 namespace {
 
-void run_steps(Team& T, double dt, int nsteps, const ldg_solver_opts& o, ldg_step_stats* st) {
+void run_steps(Team& T, double dt, int nsteps, const ldg_solver_opts& o, ldg_step_stats* st,
+               double* host_out = nullptr) {
   Handle& h0 = T.h0();
+  T.early_out_sent = false;
   for (int s = 0; s < nsteps; ++s) {
+    T.early_out = s + 1 == nsteps ? host_out : nullptr;  // the last step's state goes out early (team_solve)
     ldgb::NvtxRange step("ldg euler_step");
     const double t_next = h0.t + dt;  // system.hpp:158
     LDG_CUDA(cudaEventRecord(h0.ev[0], T.stream));
@@ -1236,8 +1239,20 @@ int ldg_euler_steps_host(ldg_handle* H, const double* y_in, double t, double dt,
       for (auto& rp : T.ranks) rp->hist_ok = false;
     }
     for (auto& rp : T.ranks) rp->t = t;
-    run_steps(T, dt, nsteps, o, st);
-    if (T.nlocal() == 1 && T.size == 1) {
+    const bool one = T.nlocal() == 1 && T.size == 1;
+    try {
+      run_steps(T, dt, nsteps, o, st, one && nsteps > 0 ? y_out : nullptr);
+    } catch (...) {
+      T.early_out = nullptr;
+      if (T.early_out_sent) cudaStreamSynchronize(T.in_stream);  // the copy targets the caller's buffer
+      T.early_out_sent = false;
+      throw;
+    }
+    if (one && T.early_out_sent) {
+      LDG_CUDA(cudaStreamWaitEvent(T.stream, T.in_ev[3], 0));  // sent under the last step's contract check
+      T.early_out_sent = false;
+      h0.stage_is_output = true;
+    } else if (one) {
       const size_t cnt = 3L * h0.K * h0.N;
       ldgb::launch_soa_to_kmajor(h0, h0.Y.ptr, 3, h0.host_stage.ptr);
       LDG_CUDA(cudaMemcpyAsync(y_out, h0.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, T.stream));

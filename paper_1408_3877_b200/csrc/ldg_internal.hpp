@@ -257,8 +257,12 @@ struct Team {
   cudaStream_t setup_stream[2] = {};            // multigrid setup of level 0 / of the coarse levels, overlapping
   cudaEvent_t setup_ev[3] = {};                 // the right-hand side (team_solve): fork, two joins
   bool setup_pending = false;
-  cudaEvent_t in_ev[2] = {};                    // [0] call start, [1] state uploaded
+  cudaEvent_t in_ev[4] = {};                    // [0] call start, [1] state uploaded, [2] Y final, [3] state downloaded
   bool y_pending = false;                       // team_solve waits for in_ev[1] before reading Y
+  // host-buffer time loop, one rank: the last step's state leaves for the caller's buffer on
+  // in_stream as soon as the flux recovery has written it, under the residual-contract check
+  double* early_out = nullptr;
+  bool early_out_sent = false;
   std::string err;
   Handle& h0() { return *ranks[0]; }
   const Handle& h0() const { return *ranks[0]; }
@@ -336,7 +340,7 @@ void launch_extrap(Handle& h, long n, int order, const double (*w)[kExtrapMax + 
 void launch_hist_shift(Handle& h, long n, const double* c, double* const* hist_vec, int* hist);
 void launch_same(Handle& h, long n, const double* a, const double* b, int* same, cudaStream_t stream);
 void launch_dots(Handle& h, long n, int ndots, const double* const* xs, const double* const* ys, double* out_host);
-void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev);
+void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* kmajor_dev, cudaStream_t stream = nullptr);
 void launch_kmajor_to_soa(Handle& h, const double* kmajor_dev, int nvec, double* soa, cudaStream_t stream = nullptr);
 
 void launch_bjac_axpy(Handle& h, const double* x, double omega, double beta, double* y);

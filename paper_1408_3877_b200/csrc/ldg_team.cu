@@ -1419,6 +1419,19 @@ int team_solve(Team& T, double wm, double dt, const ldg_solver_opts& o, ldg_step
   halo(T, 0, kC, 1);
   each(T, 0, [&](Handle& h) { launch_stage1(h, h.Vv.ptr, 1.0, vp(h, kC), -1.0, h.Y.ptr); });
 
+  if (T.early_out && T.in_stream && T.size == 1 && T.nlocal() == 1) {
+    // the new state is final: its copy to the caller's host buffer overlaps the contract check
+    Handle& h = T.h0();
+    const size_t cnt = 3L * h.K * h.N;
+    LDG_CUDA(cudaEventRecord(T.in_ev[2], T.stream));
+    LDG_CUDA(cudaStreamWaitEvent(T.in_stream, T.in_ev[2], 0));
+    launch_soa_to_kmajor(h, h.Y.ptr, 3, h.host_stage.ptr, T.in_stream);
+    LDG_CUDA(cudaMemcpyAsync(T.early_out, h.host_stage.ptr, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
+                             T.in_stream));
+    LDG_CUDA(cudaEventRecord(T.in_ev[3], T.in_stream));
+    T.early_out_sent = true;
+    T.early_out = nullptr;
+  }
   // reference residual contract on the full system (system.hpp:198-203)
   halo(T, 0, kY, 3);
   each(T, 0, [&](Handle& h) {

@@ -444,9 +444,9 @@ void launch_dots(Handle& h, long n, int nd, const double* const* xs, const doubl
   for (int d = 0; d < nd; ++d) out_host[d] = h.red_host[d];
 }
 
-void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* km) {
+void launch_soa_to_kmajor(Handle& h, const double* soa, int nvec, double* km, cudaStream_t stream) {
   const long total = static_cast<long>(nvec) * h.K * h.N;
-  k_soa_to_kmajor<<<grid_of(total, 256), 256, 0, h.stream>>>(h.K, h.N, h.Kp, nvec, soa, km);
+  k_soa_to_kmajor<<<grid_of(total, 256), 256, 0, stream ? stream : h.stream>>>(h.K, h.N, h.Kp, nvec, soa, km);
   LDG_CUDA(cudaGetLastError());
   ++h.launches;
 }
