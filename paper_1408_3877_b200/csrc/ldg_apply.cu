@@ -23,7 +23,10 @@
 // register-heavy kernels are latency-bound at 1 CTA; 4 CTAs (<= 128 registers)
 // measured 7-15% faster there (2, 6, 7 CTAs: +24 / +48 / +38 % Schur apply).
 // At p = 3, 7 CTAs (one wave of the 256^2 level): Schur apply 145 -> 110 us,
-// full apply 153 -> 115 us; p = 2 neutral.  (-DLDG_MINB_STAGE=n overrides.)
+// full apply 153 -> 115 us.  With the rank-form kernels p = 1, 2 want one wave
+// too (7 CTAs: 150 / 91 registers otherwise, 2.3 / 1.4 waves; Schur apply
+// 55.4 -> 51.1 us and full apply 62 -> 52 us at p = 2).  (-DLDG_MINB_STAGE=n
+// overrides all, -DLDG_MINB_STAGE_P<p>=n one degree.)
 #ifdef LDG_MINB_STAGE
 #define LDG_MINB_STAGE_P(P) LDG_MINB_STAGE
 #else
@@ -33,7 +36,14 @@
 #ifndef LDG_MINB_STAGE_P4
 #define LDG_MINB_STAGE_P4 4
 #endif
-#define LDG_MINB_STAGE_P(P) ((P) == 4 ? LDG_MINB_STAGE_P4 : ((P) == 3 ? LDG_MINB_STAGE_P3 : 1))
+#ifndef LDG_MINB_STAGE_P2
+#define LDG_MINB_STAGE_P2 7
+#endif
+#ifndef LDG_MINB_STAGE_P1
+#define LDG_MINB_STAGE_P1 7
+#endif
+#define LDG_MINB_STAGE_P(P) \
+  ((P) == 4 ? LDG_MINB_STAGE_P4 : ((P) == 3 ? LDG_MINB_STAGE_P3 : ((P) == 2 ? LDG_MINB_STAGE_P2 : ((P) == 1 ? LDG_MINB_STAGE_P1 : 1))))
 #endif
 // stage 2 alone at p = 4 (tuning builds): 5 / 6 / 7 CTAs measured Schur apply
 // 274 / 298 / 308 us against 238 us at 4

@@ -41,14 +41,17 @@
 // per sweep against 76 at 7; 8 CTAs 84).  Stage 1 at p = 4 stays at 4 CTAs
 // (128 registers; 5 / 6 / 7 CTAs: sweep 81.7 / 85.2 / 77.4 us against 76.8,
 // chained or not), at p = 3 7 CTAs beat 8 (41.8 vs 45.1 us per sweep).  8 at
-// p <= 1 measured slower.
+// p <= 1 measured slower; 7 at p = 1 is needed all the same: left alone the
+// compiler takes 80 registers, 6 CTAs/SM hold 888 of the level's 1024 CTAs
+// and the rest runs as a second wave (p = 1 sweep 14.3 -> 9.6 us, 10-step
+// C2 bench 30.7 -> 29.9 ms: every degree >= 2 smooths a p = 1 level of 256^2).
 // -DLDG_MINB_S1=abcde / -DLDG_MINB_S1C=abcde (chained sweeps) /
 // -DLDG_MINB_S2=abcde (one digit per p = 0..4) override (tuning builds).
 #ifndef LDG_MINB_S1
-#define LDG_MINB_S1 11874
+#define LDG_MINB_S1 17874
 #endif
 #ifndef LDG_MINB_S2
-#define LDG_MINB_S2 11777
+#define LDG_MINB_S2 17777
 #endif
 
 namespace ldgb {
@@ -60,7 +63,7 @@ constexpr int kMinbS1[5] = {minb_digit(LDG_MINB_S1, 0), minb_digit(LDG_MINB_S1, 
                             minb_digit(LDG_MINB_S1, 3), minb_digit(LDG_MINB_S1, 4)};
 // stage 1 on chained sweeps (no projections of x: fewer registers)
 #ifndef LDG_MINB_S1C
-#define LDG_MINB_S1C 11874
+#define LDG_MINB_S1C 17874
 #endif
 constexpr int kMinbS1c[5] = {minb_digit(LDG_MINB_S1C, 0), minb_digit(LDG_MINB_S1C, 1), minb_digit(LDG_MINB_S1C, 2),
                              minb_digit(LDG_MINB_S1C, 3), minb_digit(LDG_MINB_S1C, 4)};
